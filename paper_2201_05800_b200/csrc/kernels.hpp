@@ -1,0 +1,117 @@
+// Device-side data structures and kernel launchers of the slab operator.
+//
+// Every slab-type apply of the reference is one fused kernel of the form
+//
+//   R_r = sum_j T(r,j) X_j + sum_j S(r,j) G_j + c_r W          (r < n_out)
+//
+// where X_j (j < n_in) are the input temporal blocks, G_j = F(X_j) is the
+// DG-SEM spatial operator applied per block (spatial.hpp:107-266) -- or its
+// Jacobian action J_F(U_j) X_j -- and W is an optional spatial vector.
+// The reference callers map onto (T, S, c) as follows (built in stg.cpp):
+//   st_residual   (stdg.hpp:56-76):  T = e e^T - D^T M, S = -(dt/2) M, c = -e_1, W = u_n
+//   st_jacobian v (stdg.hpp:79-110): same T, S, c = 0
+//   rk residual A-form   (lodg.hpp:111-114): T = I, S = -dt A, c = -1, W = u
+//   rk residual A^-1-form (lodg.hpp:116-118): T = A^-1/dt, S = -I, c = -rowsum(A^-1)/dt
+//   rk u_next (lodg.hpp:142-145): n_out = 1, T = 0, S = dt b^T, c = 1, W = u
+//   SemiDiscreteSystem::rhs:          n_in = n_out = 1, T = 0, S = 1, c = 0
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace stg {
+
+constexpr int kMaxN = 6;  // max LGL nodes per axis (degree <= 5)
+constexpr int kMaxT = 6;  // max temporal nodes / stages
+
+// Spatial operator coefficients for constant-velocity advection, weak form
+// divided by the diagonal mass (spatial.hpp:117-156, 158-208, 265):
+//   F[.. i_a ..] += V[a][i][k] u[.. k ..]                 (volume + own traces)
+//   F[.. i_a = 0 ..] += cL[a] * u_{c - e_a}[.. i_a = N ..] (upwind neighbour)
+//   F[.. i_a = N ..] += cR[a] * u_{c + e_a}[.. i_a = 0 ..] (downwind neighbour)
+// with V[a][i][k] = (2/h_a) b_a w_k D(k,i)/w_i plus the LLF own-trace terms
+// -(2/h_a)/w_N * alpha_a at (N,N) and +(2/h_a)/w_0 * beta_a at (0,0),
+// alpha = (b+|b|)/2, beta = (b-|b|)/2 (llf_flux, spatial.hpp:20-25).
+struct SpatialCoef {
+  double V[3][kMaxN][kMaxN];
+  double cL[3];
+  double cR[3];
+  // Burgers (d = 1, EXTENSION): raw D(i,k), 2/h and 1/w_0, 1/w_N
+  double Dm[kMaxN][kMaxN];
+  double sc;
+  double inv_w0;
+  double inv_wN;
+};
+
+struct MixCoef {
+  double T[kMaxT][kMaxT];
+  double S[kMaxT][kMaxT];
+  double c[kMaxT];
+};
+
+struct Geometry {
+  int dim;
+  int n1;      // LGL nodes per axis
+  int npc;     // nodes per cell
+  int nx, ny, nz;
+  int n_cells;
+  long long n_sdof;
+};
+
+enum class Model : int { advection = 0, burgers = 1 };
+
+struct SlabArgs {
+  SpatialCoef sp;
+  MixCoef mx;
+  Geometry g;
+  int n_in;     // input temporal blocks
+  int n_out;    // output blocks
+  int has_w;    // W term present
+  int jvp;      // 0: G = F(X); 1: G = J_F(U) X (Burgers; advection ignores U)
+  int full_s;   // S not diagonal
+  int model;
+  const double* X;  // n_in blocks
+  const double* U;  // linearisation point (jvp && burgers), n_in blocks
+  const double* W;  // spatial vector or null
+  double* R;        // n_out blocks
+};
+
+// ---- launchers (kernels_slab.cu) -------------------------------------------
+// Returns the number of kernels launched (>= 1) or -1 if no kernel fits.
+int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
+// Fast TMA path: d = 3, n = 4, n_in = n_out = 4, advection, nx % 8 == 0.
+bool slab_fast_supported(const SlabArgs& a);
+int launch_slab_fast(const SlabArgs& a, cudaStream_t s);
+
+// ---- vector kernels (kernels_vec.cu) ----------------------------------------
+// All reductions are deterministic: fixed grid for a given n, fixed-order
+// block and final reductions (no atomics).
+int reduce_grid(long long n);
+void vec_fill(double* x, double v, long long n, cudaStream_t s);
+void vec_copy(double* y, const double* x, long long n, cudaStream_t s);
+void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s);
+// y = a*x + b*y
+void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s);
+// U_j = u for j < nb (1 (x) u, stdg.hpp:131)
+void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t s);
+// out[j] = <V_j, w>, j < k (V_j = V + j*ldv); partial buffer >= grid*k doubles
+void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
+                  double* partial, double* out, cudaStream_t s);
+// w -= sum_{j<k} h[j] V_j (h on device), then out2[j] = <V_j, w> (if dots) and
+// out2[k] = <w,w>; partial buffer >= grid*(k+1)
+void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
+                    long long n, int want_dots, double* partial, double* out2, cudaStream_t s);
+// y = x / sqrt(*nrm2)  (nrm2 on device)
+void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
+                       cudaStream_t s);
+// x += sum_{j<k} y[j] V_j (y on device)
+void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
+                 cudaStream_t s);
+// *out = max |x_i|
+void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s);
+// *out = <x,y>
+void vec_dot(const double* x, const double* y, long long n, double* partial, double* out,
+             cudaStream_t s);
+
+}  // namespace stg

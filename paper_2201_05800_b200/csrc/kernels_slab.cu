@@ -1,0 +1,601 @@
+// Fused space-time DG-SEM slab-operator kernels (sm_100a, fp64).
+//
+// One launch computes, for every element and every output temporal block,
+//   R_r = sum_j T(r,j) X_j + sum_j S(r,j) G_j + c_r W
+// with G_j the DG-SEM spatial operator of block j (see kernels.hpp for how the
+// reference callers st_residual / st_jacobian / rk_step map onto T, S, c).
+// The spatial operator restates SpatialOperator::rhs (spatial.hpp:107-266)
+// for constant-velocity advection: the weak-form volume term by sum
+// factorisation (spatial.hpp:117-156), LLF faces (spatial.hpp:20-25,
+// 158-208) gathered from neighbour traces (no atomics; every element
+// recomputes its own face fluxes, which is bitwise deterministic), and the
+// mass division (spatial.hpp:265) folded into the coefficients.
+//
+// Kernels:
+//   slab1d_kernel<N1>        d = 1: one thread per element, all temporal nodes
+//                            in registers; advection and Burgers (EXTENSION).
+//   slab_generic_kernel<D,N1> d = 2, 3: one thread per spatial node with the
+//                            element staged in shared memory.
+//   slab3d_n4_tma<...>       d = 3, N = 3, n_tau = 4 (the c4/c5 target): one
+//                            TMA tensor load (128B-swizzled) of an 8-element
+//                            x-pencil, two register-tiled phases (x/y, then
+//                            z/t) exchanging partial results through shared
+//                            memory.
+#include <cuda.h>
+
+#include "kernels.hpp"
+
+namespace stg {
+namespace {
+
+constexpr int kThreads1d = 128;
+
+__device__ __forceinline__ int wrap_m(int c, int n) { return c == 0 ? n - 1 : c - 1; }
+__device__ __forceinline__ int wrap_p(int c, int n) { return c == n - 1 ? 0 : c + 1; }
+
+// ---------------------------------------------------------------------------
+// Spatial operators on one line of N1 nodes (1-D element)
+// ---------------------------------------------------------------------------
+template <int N1>
+__device__ __forceinline__ void advection_line(const SpatialCoef& sp, const double* x, double xl,
+                                               double xr, double* G) {
+#pragma unroll
+  for (int i = 0; i < N1; ++i) {
+    double g = 0.0;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) g = fma(sp.V[0][i][k], x[k], g);
+    G[i] = g;
+  }
+  G[0] = fma(sp.cL[0], xl, G[0]);
+  G[N1 - 1] = fma(sp.cR[0], xr, G[N1 - 1]);
+}
+
+// Burgers (EXTENSION, not in the reference): flux differencing with the
+// entropy-conservative two-point flux f#(a,b) = (a^2+ab+b^2)/6, LLF
+// interface flux with lambda = max(|uL|,|uR|), SAT lifting.
+__device__ __forceinline__ double bf(double u) { return 0.5 * u * u; }
+__device__ __forceinline__ double bec(double a, double b) { return (a * a + a * b + b * b) / 6.0; }
+__device__ __forceinline__ double bllf(double uL, double uR) {
+  const double lam = fmax(fabs(uL), fabs(uR));
+  return 0.5 * (bf(uL) + bf(uR)) + 0.5 * lam * (uL - uR);
+}
+__device__ __forceinline__ double dbllf(double uL, double uR, double vL, double vR) {
+  const double aL = fabs(uL), aR = fabs(uR);
+  double lam, dlam;
+  if (aL >= aR) {
+    lam = aL;
+    dlam = (uL >= 0.0 ? 1.0 : -1.0) * vL;
+  } else {
+    lam = aR;
+    dlam = (uR >= 0.0 ? 1.0 : -1.0) * vR;
+  }
+  return 0.5 * (uL * vL + uR * vR) + 0.5 * dlam * (uL - uR) + 0.5 * lam * (vL - vR);
+}
+
+template <int N1>
+__device__ __forceinline__ void burgers_line(const SpatialCoef& sp, const double* u, double ul,
+                                             double ur, double* G) {
+#pragma unroll
+  for (int i = 0; i < N1; ++i) {
+    double vol = 0.0;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) vol += 2.0 * sp.Dm[i][k] * bec(u[i], u[k]);
+    G[i] = -sp.sc * vol;
+  }
+  G[N1 - 1] -= sp.sc * (bllf(u[N1 - 1], ur) - bf(u[N1 - 1])) * sp.inv_wN;
+  G[0] += sp.sc * (bllf(ul, u[0]) - bf(u[0])) * sp.inv_w0;
+}
+
+template <int N1>
+__device__ __forceinline__ void burgers_jvp_line(const SpatialCoef& sp, const double* u, double ul,
+                                                 double ur, const double* v, double vl, double vr,
+                                                 double* G) {
+#pragma unroll
+  for (int i = 0; i < N1; ++i) {
+    double vol = 0.0;
+#pragma unroll
+    for (int k = 0; k < N1; ++k)
+      vol += 2.0 * sp.Dm[i][k] *
+             ((2.0 * u[i] + u[k]) * v[i] + (u[i] + 2.0 * u[k]) * v[k]) / 6.0;
+    G[i] = -sp.sc * vol;
+  }
+  G[N1 - 1] -= sp.sc * (dbllf(u[N1 - 1], ur, v[N1 - 1], vr) - u[N1 - 1] * v[N1 - 1]) * sp.inv_wN;
+  G[0] += sp.sc * (dbllf(ul, u[0], vl, v[0]) - u[0] * v[0]) * sp.inv_w0;
+}
+
+// ---------------------------------------------------------------------------
+// d = 1: one thread per element
+// ---------------------------------------------------------------------------
+template <int N1>
+__global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = a.g.nx;
+  if (c >= K) return;
+  const long long ns = a.g.n_sdof;
+  const int cl = wrap_m(c, K), cr = wrap_p(c, K);
+  const long long oc = (long long)c * N1, ol = (long long)cl * N1 + (N1 - 1),
+                  orr = (long long)cr * N1;
+  double x[kMaxT][N1];
+  double G[kMaxT][N1];
+#pragma unroll
+  for (int j = 0; j < kMaxT; ++j) {
+    if (j < a.n_in) {
+      const double* Xj = a.X + j * ns;
+#pragma unroll
+      for (int i = 0; i < N1; ++i) x[j][i] = Xj[oc + i];
+      const double xl = Xj[ol], xr = Xj[orr];
+      if (a.model == int(Model::advection)) {
+        advection_line<N1>(a.sp, x[j], xl, xr, G[j]);
+      } else if (!a.jvp) {
+        burgers_line<N1>(a.sp, x[j], xl, xr, G[j]);
+      } else {
+        const double* Uj = a.U + j * ns;
+        double u[N1];
+#pragma unroll
+        for (int i = 0; i < N1; ++i) u[i] = Uj[oc + i];
+        burgers_jvp_line<N1>(a.sp, u, Uj[ol], Uj[orr], x[j], xl, xr, G[j]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N1; ++i) x[j][i] = G[j][i] = 0.0;
+    }
+  }
+  double w[N1];
+#pragma unroll
+  for (int i = 0; i < N1; ++i) w[i] = a.has_w ? a.W[oc + i] : 0.0;
+#pragma unroll
+  for (int r = 0; r < kMaxT; ++r) {
+    if (r >= a.n_out) break;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double acc = a.mx.c[r] * w[i];
+#pragma unroll
+      for (int j = 0; j < kMaxT; ++j) {
+        if (j < a.n_in) {
+          acc = fma(a.mx.T[r][j], x[j][i], acc);
+          acc = fma(a.mx.S[r][j], G[j][i], acc);
+        }
+      }
+      a.R[r * ns + oc + i] = acc;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// d = 2, 3 generic: one thread per spatial node, element in shared memory
+// ---------------------------------------------------------------------------
+template <int D, int N1>
+struct GenericShape {
+  static constexpr int NPC = D == 2 ? N1 * N1 : N1 * N1 * N1;
+  static constexpr int E = NPC >= 128 ? 1 : (NPC >= 64 ? 2 : (NPC >= 32 ? 4 : 8));
+  static constexpr int THREADS = E * NPC;
+};
+
+template <int D, int N1>
+__global__ void __launch_bounds__(GenericShape<D, N1>::THREADS)
+    slab_generic_kernel(const SlabArgs a) {
+  using Sh = GenericShape<D, N1>;
+  constexpr int NPC = Sh::NPC;
+  constexpr int E = Sh::E;
+  constexpr int S1 = N1, S2 = N1 * N1;  // node strides for y, z
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x;
+  const int e = tid / NPC, node = tid - e * NPC;
+  const int cell = blockIdx.x * E + e;
+  const bool active = cell < a.g.n_cells;
+  const long long ns = a.g.n_sdof;
+  const int nin = a.n_in;
+  double* Xs = sm + (size_t)e * kMaxT * NPC;
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < kMaxT; ++j)
+      if (j < nin) Xs[j * NPC + node] = a.X[j * ns + (long long)cell * NPC + node];
+  }
+  __syncthreads();
+  if (!active) return;
+
+  const int ix = node % N1;
+  const int iy = (node / N1) % N1;
+  const int iz = D == 3 ? node / S2 : 0;
+  const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
+  const int cx = cell % nx;
+  const int cy = (cell / nx) % ny;
+  const int cz = D == 3 ? cell / (nx * ny) : 0;
+  // neighbour cells and the traces this node needs (face gather)
+  const bool fxL = ix == 0 && a.sp.cL[0] != 0.0, fxR = ix == N1 - 1 && a.sp.cR[0] != 0.0;
+  const bool fyL = iy == 0 && a.sp.cL[1] != 0.0, fyR = iy == N1 - 1 && a.sp.cR[1] != 0.0;
+  const bool fzL = D == 3 && iz == 0 && a.sp.cL[2] != 0.0;
+  const bool fzR = D == 3 && iz == N1 - 1 && a.sp.cR[2] != 0.0;
+  const long long oxL = ((long long)(cell - cx + wrap_m(cx, nx))) * NPC + node + (N1 - 1);
+  const long long oxR = ((long long)(cell - cx + wrap_p(cx, nx))) * NPC + node - (N1 - 1);
+  const long long oyL = ((long long)(cell + (wrap_m(cy, ny) - cy) * nx)) * NPC + node + (N1 - 1) * S1;
+  const long long oyR = ((long long)(cell + (wrap_p(cy, ny) - cy) * nx)) * NPC + node - (N1 - 1) * S1;
+  const long long ozL = ((long long)(cell + (wrap_m(cz, nz) - cz) * nx * ny)) * NPC + node + (N1 - 1) * S2;
+  const long long ozR = ((long long)(cell + (wrap_p(cz, nz) - cz) * nx * ny)) * NPC + node - (N1 - 1) * S2;
+
+  double x[kMaxT], G[kMaxT];
+#pragma unroll
+  for (int j = 0; j < kMaxT; ++j) {
+    x[j] = 0.0;
+    G[j] = 0.0;
+    if (j < nin) {
+      const double* Xe = Xs + j * NPC;
+      x[j] = Xe[node];
+      double g = 0.0;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) g = fma(a.sp.V[0][ix][k], Xe[node - ix + k], g);
+#pragma unroll
+      for (int k = 0; k < N1; ++k) g = fma(a.sp.V[1][iy][k], Xe[node + (k - iy) * S1], g);
+      if (D == 3) {
+#pragma unroll
+        for (int k = 0; k < N1; ++k) g = fma(a.sp.V[2][iz][k], Xe[node + (k - iz) * S2], g);
+      }
+      const double* Xj = a.X + j * ns;
+      if (fxL) g = fma(a.sp.cL[0], Xj[oxL], g);
+      if (fxR) g = fma(a.sp.cR[0], Xj[oxR], g);
+      if (fyL) g = fma(a.sp.cL[1], Xj[oyL], g);
+      if (fyR) g = fma(a.sp.cR[1], Xj[oyR], g);
+      if (fzL) g = fma(a.sp.cL[2], Xj[ozL], g);
+      if (fzR) g = fma(a.sp.cR[2], Xj[ozR], g);
+      G[j] = g;
+    }
+  }
+  const long long o = (long long)cell * NPC + node;
+  const double w = a.has_w ? a.W[o] : 0.0;
+#pragma unroll
+  for (int r = 0; r < kMaxT; ++r) {
+    if (r >= a.n_out) break;
+    double acc = a.mx.c[r] * w;
+#pragma unroll
+    for (int j = 0; j < kMaxT; ++j) {
+      if (j < nin) {
+        acc = fma(a.mx.T[r][j], x[j], acc);
+        acc = fma(a.mx.S[r][j], G[j], acc);
+      }
+    }
+    a.R[r * ns + o] = acc;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// d = 3, N = 3, n_tau = 4: TMA-staged, register-tiled two-phase kernel
+// ---------------------------------------------------------------------------
+namespace fast {
+constexpr int E = 8;                    // elements per CTA (an x-pencil segment)
+constexpr int THREADS = 16 * E;         // 16 threads per element per phase
+constexpr int ROWS = 4 * E * 4;         // rows (t, e, z), 16 doubles = 128 B each
+constexpr int TILE_DOUBLES = ROWS * 16;
+constexpr unsigned TILE_BYTES = TILE_DOUBLES * 8u;  // 16 KiB
+constexpr int SMEM_BYTES = 2 * TILE_BYTES + 1024 + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// 128B swizzle (CU_TENSOR_MAP_SWIZZLE_128B): the 16-byte chunk c of row r
+// lives at chunk c ^ (r & 7).  q = double index (0..15) within the row.
+__device__ __forceinline__ int swz(int row, int q) {
+  return row * 16 + ((((q >> 1) ^ (row & 7)) << 1) | (q & 1));
+}
+__device__ __forceinline__ int row_of(int t, int e, int z) { return (t * E + e) * 4 + z; }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ double2 ldg2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+}  // namespace fast
+
+template <bool FULL_S>
+__global__ void __launch_bounds__(fast::THREADS, 4)
+    slab3d_n4_tma(const __grid_constant__ CUtensorMap tmX, const SlabArgs a) {
+  using namespace fast;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  double* Xs = reinterpret_cast<double*>(base);
+  double* FA = Xs + TILE_DOUBLES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(FA + TILE_DOUBLES);
+  const uint32_t bar_a = smem_u32(bar);
+
+  const int tid = threadIdx.x;
+  const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
+  const long long ns = a.g.n_sdof;
+  const int e0 = blockIdx.x * E;  // first cell of the pencil segment
+  const int cx0 = e0 % nx;
+  const int cy = (e0 / nx) % ny;
+  const int cz = e0 / (nx * ny);
+
+  if (tid == 0) {
+    mbar_init(bar_a, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_expect_tx(bar_a, TILE_BYTES);
+    tma_load_4d(smem_u32(Xs), &tmX, bar_a, 0, 0, e0, 0);
+  }
+
+  const bool nLx = a.sp.cL[0] != 0.0, nRx = a.sp.cR[0] != 0.0;
+  const bool nLy = a.sp.cL[1] != 0.0, nRy = a.sp.cR[1] != 0.0;
+  const bool nLz = a.sp.cL[2] != 0.0, nRz = a.sp.cR[2] != 0.0;
+
+  // ---- phase-A identity (e, z, t) and its early global loads -------------
+  const int zA = tid & 3, eA = (tid >> 2) & (E - 1), tA = tid >> 5;
+  const int cellA = e0 + eA;
+  const double* XtA = a.X + tA * ns;
+  double yl[4] = {0, 0, 0, 0}, yr[4] = {0, 0, 0, 0};
+  double hl[4] = {0, 0, 0, 0}, hr[4] = {0, 0, 0, 0};
+  {
+    const int cym = cy == 0 ? ny - 1 : cy - 1, cyp = cy == ny - 1 ? 0 : cy + 1;
+    if (nLy) {
+      const double* p = XtA + (long long)(cellA + (cym - cy) * nx) * 64 + zA * 16 + 12;
+      const double2 v0 = fast::ldg2(p), v1 = fast::ldg2(p + 2);
+      yl[0] = v0.x; yl[1] = v0.y; yl[2] = v1.x; yl[3] = v1.y;
+    }
+    if (nRy) {
+      const double* p = XtA + (long long)(cellA + (cyp - cy) * nx) * 64 + zA * 16;
+      const double2 v0 = fast::ldg2(p), v1 = fast::ldg2(p + 2);
+      yr[0] = v0.x; yr[1] = v0.y; yr[2] = v1.x; yr[3] = v1.y;
+    }
+    if (eA == 0 && nLx) {
+      const int c = e0 - cx0 + (cx0 == 0 ? nx - 1 : cx0 - 1);
+      const double* p = XtA + (long long)c * 64 + zA * 16 + 3;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) hl[y] = __ldg(p + 4 * y);
+    }
+    if (eA == E - 1 && nRx) {
+      const int cxe = cx0 + E - 1;
+      const int c = e0 - cx0 + (cxe == nx - 1 ? 0 : cxe + 1);
+      const double* p = XtA + (long long)c * 64 + zA * 16;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) hr[y] = __ldg(p + 4 * y);
+    }
+  }
+  // ---- phase-B identity (e, x, y) and its early global loads -------------
+  const int xB = tid & 3, yB = (tid >> 2) & 3, eB = tid >> 4;
+  const int cellB = e0 + eB;
+  const int qB = yB * 4 + xB;
+  double zl[4] = {0, 0, 0, 0}, zr[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
+  {
+    const int czm = cz == 0 ? nz - 1 : cz - 1, czp = cz == nz - 1 ? 0 : cz + 1;
+    if (nLz) {
+      const double* p = a.X + (long long)(cellB + (czm - cz) * nx * ny) * 64 + 48 + qB;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) zl[t] = __ldg(p + t * ns);
+    }
+    if (nRz) {
+      const double* p = a.X + (long long)(cellB + (czp - cz) * nx * ny) * 64 + qB;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) zr[t] = __ldg(p + t * ns);
+    }
+    if (a.has_w) {
+      const double* p = a.W + (long long)cellB * 64 + qB;
+#pragma unroll
+      for (int z = 0; z < 4; ++z) w[z] = __ldg(p + 16 * z);
+    }
+  }
+
+  while (!fast::mbar_try_wait(bar_a, 0)) {
+  }
+
+  // ---- phase A: x and y derivatives of the (y,x) plane at (t, e, z) -------
+  {
+    const int row = row_of(tA, eA, zA);
+    const int sw = row & 7;
+    double u[16];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double2 v = *reinterpret_cast<const double2*>(Xs + row * 16 + ((c ^ sw) << 1));
+      u[2 * c] = v.x;
+      u[2 * c + 1] = v.y;
+    }
+    if (nLx && eA > 0) {
+      const int rl = row_of(tA, eA - 1, zA);
+#pragma unroll
+      for (int y = 0; y < 4; ++y) hl[y] = Xs[swz(rl, 4 * y + 3)];
+    }
+    if (nRx && eA < E - 1) {
+      const int rr = row_of(tA, eA + 1, zA);
+#pragma unroll
+      for (int y = 0; y < 4; ++y) hr[y] = Xs[swz(rr, 4 * y)];
+    }
+    double f[16];
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        double g = 0.0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g = fma(a.sp.V[0][x][k], u[4 * y + k], g);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g = fma(a.sp.V[1][y][k], u[4 * k + x], g);
+        if (x == 0) g = fma(a.sp.cL[0], hl[y], g);
+        if (x == 3) g = fma(a.sp.cR[0], hr[y], g);
+        if (y == 0) g = fma(a.sp.cL[1], yl[x], g);
+        if (y == 3) g = fma(a.sp.cR[1], yr[x], g);
+        f[4 * y + x] = g;
+      }
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<double2*>(FA + row * 16 + ((c ^ sw) << 1)) =
+          make_double2(f[2 * c], f[2 * c + 1]);
+  }
+  __syncthreads();
+
+  // ---- phase B: z derivative, temporal mixing, store ----------------------
+  {
+    double u[4][4], f[4][4];  // [t][z]
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        const int o = swz(row_of(t, eB, z), qB);
+        u[t][z] = Xs[o];
+        f[t][z] = FA[o];
+      }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        double g = f[t][z];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) g = fma(a.sp.V[2][z][k], u[t][k], g);
+        if (z == 0) g = fma(a.sp.cL[2], zl[t], g);
+        if (z == 3) g = fma(a.sp.cR[2], zr[t], g);
+        f[t][z] = g;
+      }
+    double* Rb = a.R + (long long)cellB * 64 + qB;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int z = 0; z < 4; ++z) {
+        double acc = a.mx.c[r] * w[z];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc = fma(a.mx.T[r][j], u[j][z], acc);
+        if (FULL_S) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc = fma(a.mx.S[r][j], f[j][z], acc);
+        } else {
+          acc = fma(a.mx.S[r][r], f[r][z], acc);
+        }
+        Rb[r * ns + 16 * z] = acc;
+      }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host-side launch helpers
+// ---------------------------------------------------------------------------
+template <int N1>
+int launch1d(const SlabArgs& a, cudaStream_t s) {
+  const int blocks = (a.g.nx + kThreads1d - 1) / kThreads1d;
+  slab1d_kernel<N1><<<blocks, kThreads1d, 0, s>>>(a);
+  return 1;
+}
+
+template <int D, int N1>
+int launch_generic_t(const SlabArgs& a, cudaStream_t s) {
+  using Sh = GenericShape<D, N1>;
+  const int blocks = (a.g.n_cells + Sh::E - 1) / Sh::E;
+  const size_t smem = size_t(Sh::E) * kMaxT * Sh::NPC * sizeof(double);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(slab_generic_kernel<D, N1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+  }
+  slab_generic_kernel<D, N1><<<blocks, Sh::THREADS, smem, s>>>(a);
+  return 1;
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn get_encode() {
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
+  const int d = a.g.dim, n1 = a.g.n1;
+  if (d == 1) {
+    switch (n1) {
+      case 2: return launch1d<2>(a, s);
+      case 3: return launch1d<3>(a, s);
+      case 4: return launch1d<4>(a, s);
+      case 5: return launch1d<5>(a, s);
+      case 6: return launch1d<6>(a, s);
+      default: return -1;
+    }
+  }
+  if (a.model != int(Model::advection)) return -1;
+  if (d == 2) {
+    switch (n1) {
+      case 2: return launch_generic_t<2, 2>(a, s);
+      case 3: return launch_generic_t<2, 3>(a, s);
+      case 4: return launch_generic_t<2, 4>(a, s);
+      case 5: return launch_generic_t<2, 5>(a, s);
+      case 6: return launch_generic_t<2, 6>(a, s);
+      default: return -1;
+    }
+  }
+  if (d == 3) {
+    switch (n1) {
+      case 2: return launch_generic_t<3, 2>(a, s);
+      case 3: return launch_generic_t<3, 3>(a, s);
+      case 4: return launch_generic_t<3, 4>(a, s);
+      case 5: return launch_generic_t<3, 5>(a, s);
+      default: return -1;
+    }
+  }
+  return -1;
+}
+
+bool slab_fast_supported(const SlabArgs& a) {
+  return a.g.dim == 3 && a.g.n1 == 4 && a.n_in == 4 && a.n_out == 4 &&
+         a.model == int(Model::advection) && a.g.nx % fast::E == 0 &&
+         (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 && get_encode() != nullptr;
+}
+
+int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
+  EncodeFn enc = get_encode();
+  if (!enc) return -1;
+  CUtensorMap map;
+  const cuuint64_t gdim[4] = {16, 4, cuuint64_t(a.g.n_cells), 4};
+  const cuuint64_t gstride[3] = {128, 512, cuuint64_t(a.g.n_sdof) * 8};
+  const cuuint32_t box[4] = {16, 4, fast::E, 4};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.X), gdim,
+                         gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return -1;
+  const int blocks = a.g.n_cells / fast::E;
+  if (a.full_s) {
+    slab3d_n4_tma<true><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+  } else {
+    slab3d_n4_tma<false><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+  }
+  return 1;
+}
+
+}  // namespace stg

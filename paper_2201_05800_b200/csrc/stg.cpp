@@ -1,0 +1,872 @@
+// Host side of the C ABI (include/stg_cuda.h): handle, constants, operator
+// dispatch, device-resident GMRES(m), Newton and the STDG / LoDG steps.
+// Control flow follows the reference drivers (stdg.hpp:120-143,
+// lodg.hpp:89-149, newton.hpp:102-130); all vector work is on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/stg_cuda.h"
+#include "constants.hpp"
+#include "kernels.hpp"
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NonconvergenceError : std::runtime_error {
+  std::vector<double> history;
+  NonconvergenceError(const std::string& w, std::vector<double> h)
+      : std::runtime_error(w), history(std::move(h)) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+thread_local std::string g_create_error;
+
+std::string fmt_short(double v) {
+  char buf[32];
+  std::snprintf(buf, sizeof buf, "%.6g", v);
+  return buf;
+}
+
+struct DevBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    ck(cudaMalloc(&p, count * sizeof(double)), "cudaMalloc");
+    n = count;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct stg_handle {
+  stg_desc desc{};
+  stg::Geometry g{};
+  int n1 = 0, nt = 0;
+  long long n_sdof = 0, n_dof = 0;
+  stg::SpatialCoef sp{};
+  stg::LglRule rule, trule;
+  std::vector<double> D, Dt;  // row-major D(j,i) at [j*n+i]
+  stg::Tableau tab;
+  std::vector<double> Ainv;
+  cudaStream_t stream = nullptr;
+  int kernel_pref = STG_KERNEL_AUTO;
+  std::string err;
+  long long launches = 0;
+
+  // workspace
+  DevBuf small;    // device scalars / Hessenberg columns
+  DevBuf partial;  // reduction partials
+  DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
+  double* pinned = nullptr;  // pinned host mirror of `small`
+  static constexpr int kSmall = 1024;
+
+  ~stg_handle() {
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+namespace {
+
+using Op = std::function<void(const double* x, double* y)>;
+
+void check_launch(stg_handle* h) {
+  ck(cudaGetLastError(), "kernel launch");
+}
+
+// ---- operator dispatch ----------------------------------------------------
+void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
+           const double* U, const double* W, double* R, bool jvp, bool full_s) {
+  stg::SlabArgs a{};
+  a.sp = h->sp;
+  a.mx = mx;
+  a.g = h->g;
+  a.n_in = n_in;
+  a.n_out = n_out;
+  a.has_w = W != nullptr;
+  a.jvp = jvp ? 1 : 0;
+  a.full_s = full_s ? 1 : 0;
+  a.model = h->desc.model;
+  a.X = X;
+  a.U = U;
+  a.W = W;
+  a.R = R;
+  int launched = -1;
+  if (h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(a)) {
+    launched = stg::launch_slab_fast(a, h->stream);
+  } else if (h->kernel_pref == STG_KERNEL_FAST) {
+    throw std::invalid_argument("fast kernel requested but not applicable to this problem");
+  }
+  if (launched < 0) launched = stg::launch_slab_generic(a, h->stream);
+  if (launched < 0) throw std::invalid_argument("no kernel for this (dim, degree, model)");
+  h->launches += launched;
+  check_launch(h);
+}
+
+stg::MixCoef zero_mix() {
+  stg::MixCoef m;
+  std::memset(&m, 0, sizeof m);
+  return m;
+}
+
+// st_residual (stdg.hpp:56-76): T = e e^T - D^T M, S = -(dt/2) M, c = -e_1.
+stg::MixCoef st_mix(const stg_handle* h, double dt, bool with_un) {
+  stg::MixCoef m = zero_mix();
+  const int n = h->nt;
+  for (int i = 0; i < n; ++i) {
+    for (int j = 0; j < n; ++j) {
+      double v = -(h->Dt[size_t(j) * n + i] * h->trule.w[j]);
+      if (i == n - 1 && j == n - 1) v += 1.0;
+      m.T[i][j] = v;
+    }
+    m.S[i][i] = -(0.5 * dt * h->trule.w[i]);
+  }
+  if (with_un) m.c[0] = -1.0;
+  return m;
+}
+
+// rk_step residual (lodg.hpp:104-122)
+stg::MixCoef stage_mix(const stg_handle* h, int form, double dt, bool with_u) {
+  stg::MixCoef m = zero_mix();
+  const int s = h->nt;
+  if (form == STG_FORM_A) {
+    for (int i = 0; i < s; ++i) {
+      m.T[i][i] = 1.0;
+      for (int j = 0; j < s; ++j) m.S[i][j] = -(dt * h->tab.A[size_t(i) * s + j]);
+      if (with_u) m.c[i] = -1.0;
+    }
+  } else {
+    for (int i = 0; i < s; ++i) {
+      double rs = 0.0;
+      for (int j = 0; j < s; ++j) {
+        m.T[i][j] = h->Ainv[size_t(i) * s + j] / dt;
+        rs += m.T[i][j];
+      }
+      m.S[i][i] = -1.0;
+      if (with_u) m.c[i] = -rs;
+    }
+  }
+  return m;
+}
+
+void validate_desc(const stg_desc* d) {
+  if (!d) throw std::invalid_argument("stg_create: null descriptor");
+  if (d->dim < 1 || d->dim > 3) throw std::invalid_argument("uniform_mesh: d in {1,2,3}");
+  if (d->degree < 1 || d->degree + 1 > stg::kMaxN)
+    throw std::invalid_argument("dg_space: degree must be in [1, 5]");
+  if (d->n_tau < 2 || d->n_tau > stg::kMaxT)
+    throw std::invalid_argument("sbp_operators: n_tau must be in [2, 6]");
+  if (d->model != STG_MODEL_ADVECTION && d->model != STG_MODEL_BURGERS)
+    throw std::invalid_argument("unknown model");
+  if (d->model == STG_MODEL_BURGERS && d->dim != 1)
+    throw std::invalid_argument("burgers model: d = 1 only");
+  if (d->dim == 3 && d->degree + 1 > 5)
+    throw std::invalid_argument("d = 3 supports degree <= 4");
+  long long cells = 1;
+  for (int a = 0; a < d->dim; ++a) {
+    if (d->cells[a] < 1) throw std::invalid_argument("uniform_mesh: need cells >= 1");
+    if (!(d->upper[a] > d->lower[a]))
+      throw std::invalid_argument("uniform_mesh: need upper > lower");
+    cells *= d->cells[a];
+  }
+  if (cells > (1LL << 30)) throw std::invalid_argument("too many cells");
+}
+
+void build_constants(stg_handle* h) {
+  const stg_desc& d = h->desc;
+  h->n1 = d.degree + 1;
+  h->nt = d.n_tau;
+  h->rule = stg::lgl(h->n1);
+  h->D = stg::diff_matrix(h->rule);
+  h->trule = stg::lgl(h->nt);
+  h->Dt = stg::diff_matrix(h->trule);
+  h->tab = stg::lobatto(h->nt);
+  h->Ainv = stg::inverse(h->tab.A, h->nt);
+
+  stg::Geometry& g = h->g;
+  g.dim = d.dim;
+  g.n1 = h->n1;
+  g.npc = 1;
+  for (int a = 0; a < d.dim; ++a) g.npc *= h->n1;
+  g.nx = d.cells[0];
+  g.ny = d.dim >= 2 ? d.cells[1] : 1;
+  g.nz = d.dim >= 3 ? d.cells[2] : 1;
+  g.n_cells = g.nx * g.ny * g.nz;
+  g.n_sdof = (long long)g.n_cells * g.npc;
+  h->n_sdof = g.n_sdof;
+  h->n_dof = g.n_sdof * h->nt;
+
+  stg::SpatialCoef& sp = h->sp;
+  std::memset(&sp, 0, sizeof sp);
+  const int n = h->n1;
+  const auto& w = h->rule.w;
+  for (int a = 0; a < d.dim; ++a) {
+    const double hsp = (d.upper[a] - d.lower[a]) / double(d.cells[a]);
+    const double s = 2.0 / hsp;
+    if (d.model == STG_MODEL_ADVECTION) {
+      const double b = d.velocity[a];
+      const double alpha = 0.5 * (b + std::abs(b)), beta = 0.5 * (b - std::abs(b));
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k)
+          sp.V[a][i][k] = s * b * (w[k] * h->D[size_t(k) * n + i]) / w[i];
+      sp.V[a][n - 1][n - 1] += -(s / w[n - 1]) * alpha;
+      sp.V[a][0][0] += (s / w[0]) * beta;
+      sp.cL[a] = (s / w[0]) * alpha;
+      sp.cR[a] = -(s / w[n - 1]) * beta;
+    }
+    if (a == 0) {
+      sp.sc = s;
+      sp.inv_w0 = 1.0 / w[0];
+      sp.inv_wN = 1.0 / w[n - 1];
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) sp.Dm[i][k] = h->D[size_t(i) * n + k];
+    }
+  }
+}
+
+void ensure_workspace(stg_handle* h) {
+  if (!h->pinned) {
+    ck(cudaMallocHost(&h->pinned, sizeof(double) * stg_handle::kSmall), "cudaMallocHost");
+    h->small.ensure(stg_handle::kSmall);
+    h->partial.ensure(size_t(148 * 8) * 80);
+  }
+}
+
+// ---- device reductions returning to the host --------------------------------
+double dev_maxabs(stg_handle* h, const double* x, long long n) {
+  stg::vec_maxabs(x, n, h->partial.p, h->small.p, h->stream);
+  h->launches += 2;
+  ck(cudaMemcpyAsync(h->pinned, h->small.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream),
+     "memcpy");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  return h->pinned[0];
+}
+
+double dev_dot(stg_handle* h, const double* x, const double* y, long long n) {
+  stg::vec_dot(x, y, n, h->partial.p, h->small.p, h->stream);
+  h->launches += 2;
+  ck(cudaMemcpyAsync(h->pinned, h->small.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream),
+     "memcpy");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  return h->pinned[0];
+}
+
+struct GmresStats {
+  int iterations = 0;
+  double rel_residual = 0.0;
+  bool converged = false;
+};
+
+// Restarted GMRES(m), right-unpreconditioned, classical Gram-Schmidt with one
+// full re-orthogonalisation (CGS2) in three fused passes, Givens rotations on
+// the host.  Stops when ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at
+// newton.hpp:68-77).  x holds the initial guess.
+GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
+                 double tol, int max_it) {
+  ensure_workspace(h);
+  if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
+  if (m > 60) throw std::invalid_argument("gmres: restart <= 60");
+  GmresStats st;
+  const long long ld = round_up(n, 32);
+  h->basis.ensure(size_t(ld) * (m + 1));
+  h->wv.ensure(size_t(n));
+  double* V = h->basis.p;
+  double* w = h->wv.p;
+  double* dsm = h->small.p;  // [0..m+1] h1, [64..] h2/norm, [128..] h3/norm, [256..] y
+  double* hp = h->pinned;
+  cudaStream_t s = h->stream;
+
+  const double bnorm = std::sqrt(dev_dot(h, b, b, n));
+  if (bnorm == 0.0) {
+    stg::vec_fill(x, 0.0, n, s);
+    h->launches++;
+    st.converged = true;
+    return st;
+  }
+  std::vector<double> H(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m);
+  auto Hat = [&](int i, int j) -> double& { return H[size_t(i) * m + j]; };
+  int total = 0;
+  while (true) {
+    A(x, w);                                   // w = A x
+    stg::vec_axpby(w, 1.0, b, -1.0, n, s);     // w = b - A x
+    h->launches++;
+    stg::vec_multidot(w, 0, 1, w, n, h->partial.p, dsm + 200, s);
+    h->launches += 2;
+    ck(cudaMemcpyAsync(hp + 200, dsm + 200, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
+    stg::vec_scale_invsqrt(V, w, dsm + 200, n, s);  // V_0 = r / ||r||
+    h->launches++;
+    ck(cudaStreamSynchronize(s), "sync");
+    const double beta = std::sqrt(hp[200]);
+    st.rel_residual = beta / bnorm;
+    if (st.rel_residual <= tol) {
+      st.converged = true;
+      break;
+    }
+    if (total >= max_it) break;
+    std::fill(g.begin(), g.end(), 0.0);
+    g[0] = beta;
+    int k = 0;
+    for (; k < m && total < max_it; ++k) {
+      ++total;
+      A(V + size_t(k) * ld, w);
+      const int kk = k + 1;  // vectors V_0..V_k
+      stg::vec_multidot(V, ld, kk, w, n, h->partial.p, dsm, s);                    // h1
+      stg::vec_update_dot(w, V, ld, kk, dsm, n, 1, h->partial.p, dsm + 64, s);     // w -= V h1; h2
+      stg::vec_update_dot(w, V, ld, kk, dsm + 64, n, 0, h->partial.p, dsm + 128, s);  // w -= V h2
+      stg::vec_scale_invsqrt(V + size_t(k + 1) * ld, w, dsm + 128 + kk, n, s);
+      h->launches += 7;
+      ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
+      ck(cudaStreamSynchronize(s), "sync");
+      for (int j = 0; j <= k; ++j) Hat(j, k) = hp[j] + hp[64 + j];
+      const double hn = std::sqrt(hp[128 + kk]);
+      Hat(k + 1, k) = hn;
+      for (int j = 0; j < k; ++j) {
+        const double t0 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);
+        Hat(j + 1, k) = -sn[j] * Hat(j, k) + cs[j] * Hat(j + 1, k);
+        Hat(j, k) = t0;
+      }
+      const double den = std::hypot(Hat(k, k), Hat(k + 1, k));
+      cs[k] = den == 0.0 ? 1.0 : Hat(k, k) / den;
+      sn[k] = den == 0.0 ? 0.0 : Hat(k + 1, k) / den;
+      Hat(k, k) = den;
+      Hat(k + 1, k) = 0.0;
+      g[k + 1] = -sn[k] * g[k];
+      g[k] = cs[k] * g[k];
+      if (std::abs(g[k + 1]) / bnorm <= tol || hn == 0.0 || !std::isfinite(hn)) {
+        ++k;
+        break;
+      }
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double acc = g[i];
+      for (int j = i + 1; j < k; ++j) acc -= Hat(i, j) * y[j];
+      y[i] = acc / Hat(i, i);
+    }
+    std::memcpy(hp + 256, y.data(), sizeof(double) * k);
+    ck(cudaMemcpyAsync(dsm + 256, hp + 256, sizeof(double) * k, cudaMemcpyHostToDevice, s),
+       "memcpy");
+    stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
+    h->launches++;
+    ck(cudaStreamSynchronize(s), "sync");  // hp+256 reused next cycle
+  }
+  st.iterations = total;
+  check_launch(h);
+  return st;
+}
+
+struct NewtonOut {
+  int iterations = 0;
+  int linear_iterations = 0;
+  double final_residual = 0.0;
+  std::vector<double> history;
+};
+
+// newton_solve (newton.hpp:102-130) on device vectors; u holds u0 on entry.
+NewtonOut newton(stg_handle* h, const Op& residual,
+                 const std::function<Op(const double*)>& jacobian, double* u, long long n,
+                 const stg_newton_config& cfg) {
+  ensure_workspace(h);
+  h->res.ensure(size_t(n));
+  h->delta.ensure(size_t(n));
+  double* r = h->res.p;
+  double* du = h->delta.p;
+  NewtonOut out;
+  residual(u, r);
+  double norm = dev_maxabs(h, r, n);
+  const double norm0 = norm;
+  out.history.push_back(norm);
+  auto converged = [&](double v) { return v <= cfg.abs_tol || v <= cfg.rel_tol * norm0; };
+  while (!converged(norm)) {
+    if (out.iterations >= cfg.max_iter)
+      throw NonconvergenceError("newton_solve: no convergence in " +
+                                    std::to_string(cfg.max_iter) + " iterations, residual " +
+                                    fmt_short(norm),
+                                out.history);
+    const Op J = jacobian(u);
+    stg::vec_axpby(r, 0.0, r, -1.0, n, h->stream);  // r = -r
+    stg::vec_fill(du, 0.0, n, h->stream);
+    h->launches += 2;
+    const GmresStats gs = gmres(h, J, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
+                                cfg.gmres_max_it);
+    out.linear_iterations += gs.iterations;
+    if (!gs.converged)
+      throw std::runtime_error("linear_solve: GMRES did not converge, error " +
+                               fmt_short(gs.rel_residual));
+    stg::vec_axpy(u, 1.0, du, n, h->stream);
+    h->launches++;
+    ++out.iterations;
+    residual(u, r);
+    norm = dev_maxabs(h, r, n);
+    out.history.push_back(norm);
+  }
+  out.final_residual = norm;
+  return out;
+}
+
+void fill_info(stg_solve_info* info, const NewtonOut& o) {
+  if (!info) return;
+  info->newton_iterations = o.iterations;
+  info->linear_iterations = o.linear_iterations;
+  info->final_residual = o.final_residual;
+  info->n_history = int(std::min<size_t>(o.history.size(), STG_MAX_HISTORY));
+  for (int i = 0; i < info->n_history; ++i) info->residual_history[i] = o.history[size_t(i)];
+}
+
+// ---- operators as closures ---------------------------------------------------
+void st_residual(stg_handle* h, double dt, const double* un, const double* U, double* R) {
+  apply(h, st_mix(h, dt, un != nullptr), h->nt, h->nt, U, nullptr, un, R, false, false);
+}
+
+void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
+            double fd_eps) {
+  if (h->desc.model == STG_MODEL_ADVECTION) {
+    // linear: J v = R(v) with the u_n coupling removed (stdg.hpp:79-110)
+    apply(h, st_mix(h, dt, false), h->nt, h->nt, v, nullptr, nullptr, Jv, false, false);
+  } else if (fd_eps <= 0.0) {
+    apply(h, st_mix(h, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, false);
+  } else {
+    // [R(U + eps v) - R(U)] / eps (u_n terms cancel and are omitted)
+    h->tmp1.ensure(size_t(h->n_dof));
+    h->tmp2.ensure(size_t(h->n_dof));
+    stg::vec_copy(h->tmp1.p, U, h->n_dof, h->stream);
+    stg::vec_axpy(h->tmp1.p, fd_eps, v, h->n_dof, h->stream);
+    h->launches += 2;
+    apply(h, st_mix(h, dt, false), h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false, false);
+    apply(h, st_mix(h, dt, false), h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false, false);
+    stg::vec_axpby(Jv, -1.0 / fd_eps, h->tmp2.p, 1.0 / fd_eps, h->n_dof, h->stream);
+    h->launches++;
+  }
+}
+
+void stage_residual(stg_handle* h, int form, double dt, const double* u, const double* U,
+                    double* R) {
+  apply(h, stage_mix(h, form, dt, true), h->nt, h->nt, U, nullptr, u, R, false,
+        form == STG_FORM_A);
+}
+
+void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double* v, double* Jv,
+               double fd_eps) {
+  const bool full = form == STG_FORM_A;
+  if (h->desc.model == STG_MODEL_ADVECTION) {
+    apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, v, nullptr, nullptr, Jv, false, full);
+  } else if (fd_eps <= 0.0) {
+    apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, full);
+  } else {
+    h->tmp1.ensure(size_t(h->n_dof));
+    h->tmp2.ensure(size_t(h->n_dof));
+    stg::vec_copy(h->tmp1.p, U, h->n_dof, h->stream);
+    stg::vec_axpy(h->tmp1.p, fd_eps, v, h->n_dof, h->stream);
+    h->launches += 2;
+    apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false,
+          full);
+    apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false,
+          full);
+    stg::vec_axpby(Jv, -1.0 / fd_eps, h->tmp2.p, 1.0 / fd_eps, h->n_dof, h->stream);
+    h->launches++;
+  }
+}
+
+stg_newton_config effective_cfg(const stg_newton_config* cfg) {
+  stg_newton_config c;
+  stg_newton_config_default(&c);
+  if (cfg) c = *cfg;
+  if (c.linear != STG_LINEAR_AUTO && c.linear != STG_LINEAR_GMRES)
+    throw std::invalid_argument("linear method: only GMRES runs on the device");
+  if (c.max_iter < 0) throw std::invalid_argument("max_iter >= 0");
+  return c;
+}
+
+void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
+                  const stg_newton_config* cfgp, double* U, double* u_next,
+                  stg_solve_info* info) {
+  (void)t_n;  // the advection / Burgers fluxes are time independent
+  if (!(dt > 0)) throw std::invalid_argument("stdg_step: dt > 0 required");
+  const stg_newton_config cfg = effective_cfg(cfgp);
+  const long long n = h->n_dof;
+  stg::vec_broadcast(U, u_n, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u_n (stdg.hpp:131)
+  h->launches++;
+  const double eps = cfg.fd_eps;
+  NewtonOut o;
+  try {
+    o = newton(
+        h, [&](const double* X, double* R) { st_residual(h, dt, u_n, X, R); },
+        [&](const double* X) -> Op {
+          return [h, dt, X, eps](const double* v, double* Jv) { st_jvp(h, dt, X, v, Jv, eps); };
+        },
+        U, n, cfg);
+  } catch (const NonconvergenceError& e) {
+    throw NonconvergenceError("stdg_step element at t=" + fmt_short(t_n) + ", dt=" + fmt_short(dt) +
+                                  ": " + e.what(),
+                              e.history);
+  }
+  if (u_next) {
+    stg::vec_copy(u_next, U + (h->nt - 1) * h->n_sdof, h->n_sdof, h->stream);
+    h->launches++;
+  }
+  fill_info(info, o);
+}
+
+void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
+                const stg_newton_config* cfgp, double* U, double* u_next, stg_solve_info* info) {
+  if (!(dt > 0)) throw std::invalid_argument("rk_step: dt > 0 required");
+  if (form != STG_FORM_A && form != STG_FORM_A_INV) throw std::invalid_argument("bad form");
+  const stg_newton_config cfg = effective_cfg(cfgp);
+  const long long n = h->n_dof;
+  stg::vec_broadcast(U, u, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u (lodg.hpp:131)
+  h->launches++;
+  const double eps = cfg.fd_eps;
+  NewtonOut o;
+  try {
+    o = newton(
+        h, [&](const double* X, double* R) { stage_residual(h, form, dt, u, X, R); },
+        [&](const double* X) -> Op {
+          return [h, form, dt, X, eps](const double* v, double* Jv) {
+            stage_jvp(h, form, dt, X, v, Jv, eps);
+          };
+        },
+        U, n, cfg);
+  } catch (const NonconvergenceError& e) {
+    throw NonconvergenceError("rk_step at t=" + fmt_short(t) + ", dt=" + fmt_short(dt) + ": " +
+                                  e.what(),
+                              e.history);
+  }
+  if (u_next) {
+    // u_next = u + dt sum_j b_j F(U_j)  (lodg.hpp:142-145)
+    stg::MixCoef m = zero_mix();
+    for (int j = 0; j < h->nt; ++j) m.S[0][j] = dt * h->tab.b[size_t(j)];
+    m.c[0] = 1.0;
+    apply(h, m, h->nt, 1, U, nullptr, u, u_next, false, true);
+  }
+  fill_info(info, o);
+}
+
+template <class F>
+int guarded(stg_handle* h, F&& f) {
+  std::string* err = h ? &h->err : &g_create_error;
+  try {
+    f();
+    return STG_OK;
+  } catch (const NonconvergenceError& e) {
+    *err = e.what();
+    return STG_ERR_NONCONVERGENCE;
+  } catch (const CudaError& e) {
+    *err = e.what();
+    return STG_ERR_CUDA;
+  } catch (const std::invalid_argument& e) {
+    *err = e.what();
+    return STG_ERR_INVALID;
+  } catch (const std::exception& e) {
+    *err = e.what();
+    return STG_ERR_RUNTIME;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
+}
+
+}  // namespace
+
+extern "C" {
+
+void stg_newton_config_default(stg_newton_config* c) {
+  if (!c) return;
+  c->abs_tol = 1e-12;
+  c->rel_tol = 1e-12;
+  c->max_iter = 50;
+  c->linear = STG_LINEAR_AUTO;
+  c->gmres_restart = 30;
+  c->gmres_tol = 1e-12;
+  c->gmres_max_it = 1000;
+  c->fd_eps = 0.0;
+}
+
+const char* stg_last_error(const stg_handle* h) {
+  return h ? h->err.c_str() : g_create_error.c_str();
+}
+
+int stg_create(const stg_desc* desc, stg_handle** out) {
+  return guarded(nullptr, [&] {
+    need(out, "stg_create");
+    *out = nullptr;
+    validate_desc(desc);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+      cudaGetLastError();
+      throw CudaError("stg_create: no CUDA device (there is no CPU fallback)");
+    }
+    auto h = std::make_unique<stg_handle>();
+    h->desc = *desc;
+    build_constants(h.get());
+    ensure_workspace(h.get());
+    *out = h.release();
+  });
+}
+
+void stg_destroy(stg_handle* h) { delete h; }
+
+int stg_set_stream(stg_handle* h, void* s) {
+  return guarded(h, [&] {
+    need(h, "stg_set_stream");
+    h->stream = static_cast<cudaStream_t>(s);
+  });
+}
+
+int stg_set_kernel(stg_handle* h, int k) {
+  return guarded(h, [&] {
+    need(h, "stg_set_kernel");
+    if (k < STG_KERNEL_AUTO || k > STG_KERNEL_FAST) throw std::invalid_argument("bad kernel id");
+    h->kernel_pref = k;
+  });
+}
+
+int stg_sizes(const stg_handle* h, long long* n_sdof, long long* n_dof) {
+  if (!h) return STG_ERR_INVALID;
+  if (n_sdof) *n_sdof = h->n_sdof;
+  if (n_dof) *n_dof = h->n_dof;
+  return STG_OK;
+}
+
+int stg_constants(const stg_handle* h, double* nodes, double* weights, double* d_tau) {
+  if (!h) return STG_ERR_INVALID;
+  if (nodes) std::memcpy(nodes, h->rule.x.data(), sizeof(double) * h->n1);
+  if (weights) std::memcpy(weights, h->rule.w.data(), sizeof(double) * h->n1);
+  if (d_tau) std::memcpy(d_tau, h->Dt.data(), sizeof(double) * h->nt * h->nt);
+  return STG_OK;
+}
+
+long long stg_kernel_launches(const stg_handle* h) { return h ? h->launches : 0; }
+
+int stg_lgl_rule(int n, double* nodes, double* weights) {
+  return guarded(nullptr, [&] {
+    const stg::LglRule r = stg::lgl(n);
+    if (nodes) std::memcpy(nodes, r.x.data(), sizeof(double) * n);
+    if (weights) std::memcpy(weights, r.w.data(), sizeof(double) * n);
+  });
+}
+
+int stg_diff_matrix(int n, double* D) {
+  return guarded(nullptr, [&] {
+    need(D, "D");
+    const std::vector<double> M = stg::diff_matrix(stg::lgl(n));
+    std::memcpy(D, M.data(), sizeof(double) * M.size());
+  });
+}
+
+int stg_lobatto_tableau(int s, double* A, double* b, double* c) {
+  return guarded(nullptr, [&] {
+    const stg::Tableau t = stg::lobatto(s);
+    if (A) std::memcpy(A, t.A.data(), sizeof(double) * s * s);
+    if (b) std::memcpy(b, t.b.data(), sizeof(double) * s);
+    if (c) std::memcpy(c, t.c.data(), sizeof(double) * s);
+  });
+}
+
+int stg_spatial_rhs(stg_handle* h, double t, const double* u, double* F) {
+  return guarded(h, [&] {
+    need(h, "stg_spatial_rhs");
+    need(u, "u");
+    need(F, "F");
+    (void)t;
+    stg::MixCoef m = zero_mix();
+    m.S[0][0] = 1.0;
+    apply(h, m, 1, 1, u, nullptr, nullptr, F, false, false);
+  });
+}
+
+int stg_spatial_jvp(stg_handle* h, double t, const double* u, const double* v, double* Jv) {
+  return guarded(h, [&] {
+    need(h, "stg_spatial_jvp");
+    need(v, "v");
+    need(Jv, "Jv");
+    (void)t;
+    stg::MixCoef m = zero_mix();
+    m.S[0][0] = 1.0;
+    const bool nl = h->desc.model != STG_MODEL_ADVECTION;
+    if (nl) need(u, "u");
+    apply(h, m, 1, 1, v, nl ? u : nullptr, nullptr, Jv, nl, false);
+  });
+}
+
+int stg_st_residual(stg_handle* h, double t_n, double dt, const double* u_n, const double* U,
+                    double* R) {
+  return guarded(h, [&] {
+    need(h, "stg_st_residual");
+    need(u_n, "u_n");
+    need(U, "U");
+    need(R, "R");
+    (void)t_n;
+    st_residual(h, dt, u_n, U, R);
+  });
+}
+
+int stg_st_jvp(stg_handle* h, double t_n, double dt, const double* U, const double* v,
+               double* Jv, double fd_eps) {
+  return guarded(h, [&] {
+    need(h, "stg_st_jvp");
+    need(v, "v");
+    need(Jv, "Jv");
+    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    (void)t_n;
+    st_jvp(h, dt, U, v, Jv, fd_eps);
+  });
+}
+
+int stg_stage_residual(stg_handle* h, int form, double t, double dt, const double* u,
+                       const double* U, double* R) {
+  return guarded(h, [&] {
+    need(h, "stg_stage_residual");
+    need(u, "u");
+    need(U, "U");
+    need(R, "R");
+    (void)t;
+    if (form != STG_FORM_A && form != STG_FORM_A_INV) throw std::invalid_argument("bad form");
+    stage_residual(h, form, dt, u, U, R);
+  });
+}
+
+int stg_stage_jvp(stg_handle* h, int form, double t, double dt, const double* U,
+                  const double* v, double* Jv, double fd_eps) {
+  return guarded(h, [&] {
+    need(h, "stg_stage_jvp");
+    need(v, "v");
+    need(Jv, "Jv");
+    (void)t;
+    if (form != STG_FORM_A && form != STG_FORM_A_INV) throw std::invalid_argument("bad form");
+    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    stage_jvp(h, form, dt, U, v, Jv, fd_eps);
+  });
+}
+
+int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const double* b,
+                 double* x, int restart, double tol, int max_it, int* iterations,
+                 double* rel_residual) {
+  return guarded(h, [&] {
+    need(h, "stg_gmres_st");
+    need(b, "b");
+    need(x, "x");
+    (void)t_n;
+    const GmresStats st = gmres(
+        h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
+        restart, tol, max_it);
+    if (iterations) *iterations = st.iterations;
+    if (rel_residual) *rel_residual = st.rel_residual;
+    if (!st.converged)
+      throw std::runtime_error("linear_solve: GMRES did not converge, error " +
+                               fmt_short(st.rel_residual));
+  });
+}
+
+int stg_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
+                  const stg_newton_config* cfg, double* U, double* u_next,
+                  stg_solve_info* info) {
+  return guarded(h, [&] {
+    need(h, "stg_stdg_step");
+    need(u_n, "u_n");
+    need(U, "U");
+    do_stdg_step(h, t_n, dt, u_n, cfg, U, u_next, info);
+  });
+}
+
+int stg_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
+                const stg_newton_config* cfg, double* U, double* u_next, stg_solve_info* info) {
+  return guarded(h, [&] {
+    need(h, "stg_rk_step");
+    need(u, "u");
+    need(U, "U");
+    do_rk_step(h, form, t, dt, u, cfg, U, u_next, info);
+  });
+}
+
+// ---- host-buffer variants -------------------------------------------------------
+int stg_st_residual_host(stg_handle* h, double t_n, double dt, const double* u_n,
+                         const double* U, double* R) {
+  return guarded(h, [&] {
+    need(h, "stg_st_residual_host");
+    need(u_n, "u_n");
+    need(U, "U");
+    need(R, "R");
+    (void)t_n;
+    h->host_U.ensure(size_t(h->n_dof));
+    h->host_R.ensure(size_t(h->n_dof));
+    h->host_u.ensure(size_t(h->n_sdof));
+    cudaStream_t s = h->stream;
+    ck(cudaMemcpyAsync(h->host_U.p, U, sizeof(double) * h->n_dof, cudaMemcpyHostToDevice, s), "H2D");
+    ck(cudaMemcpyAsync(h->host_u.p, u_n, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
+       "H2D");
+    st_residual(h, dt, h->host_u.p, h->host_U.p, h->host_R.p);
+    ck(cudaMemcpyAsync(R, h->host_R.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int stg_stdg_step_host(stg_handle* h, double t_n, double dt, const double* u_n,
+                       const stg_newton_config* cfg, double* U, double* u_next,
+                       stg_solve_info* info) {
+  return guarded(h, [&] {
+    need(h, "stg_stdg_step_host");
+    need(u_n, "u_n");
+    need(U, "U");
+    h->host_U.ensure(size_t(h->n_dof));
+    h->host_u.ensure(size_t(h->n_sdof));
+    h->host_u2.ensure(size_t(h->n_sdof));
+    cudaStream_t s = h->stream;
+    ck(cudaMemcpyAsync(h->host_u.p, u_n, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
+       "H2D");
+    do_stdg_step(h, t_n, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
+    ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
+    if (u_next)
+      ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,
+                         s),
+         "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+int stg_rk_step_host(stg_handle* h, int form, double t, double dt, const double* u,
+                     const stg_newton_config* cfg, double* U, double* u_next,
+                     stg_solve_info* info) {
+  return guarded(h, [&] {
+    need(h, "stg_rk_step_host");
+    need(u, "u");
+    need(U, "U");
+    h->host_U.ensure(size_t(h->n_dof));
+    h->host_u.ensure(size_t(h->n_sdof));
+    h->host_u2.ensure(size_t(h->n_sdof));
+    cudaStream_t s = h->stream;
+    ck(cudaMemcpyAsync(h->host_u.p, u, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
+       "H2D");
+    do_rk_step(h, form, t, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
+    ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
+    if (u_next)
+      ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,
+                         s),
+         "D2H");
+    ck(cudaStreamSynchronize(s), "sync");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,293 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): ||x_gpu - x_cpu||_inf / ||x_cpu||_inf <= 1e-12
+for R(U) and J.v; <= 1e-10 for converged slab solutions at the same solver
+tolerances.  Oracle-sized cases run every kernel family; the full c4 / c2
+sizes are compared directly (the oracle finishes them in seconds) and through
+size-independent properties (free stream, linearity, determinism).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2201_05800_b200 import configs as C
+from paper_2201_05800_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2201_05800_b200.api import (  # noqa: E402
+    NewtonConfig, NonconvergenceError, SlabOperator,
+)
+
+TOL_OP = 1e-12
+TOL_SOLVE = 1e-10
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    b = np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda")
+
+
+def pair(cfg, kernel=L.STG_KERNEL_AUTO):
+    op = SlabOperator(**cfg.kwargs(), kernel=kernel)
+    pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
+                   list(cfg.velocity), model=cfg.model, n_tau=cfg.n_tau)
+    return op, pr
+
+
+def make(dim, degree, n_tau, cells, velocity, model=L.STG_MODEL_ADVECTION, dt=0.01, u0=None):
+    lower = (0.0,) * dim
+    upper = (1.0,) * dim if model == L.STG_MODEL_ADVECTION else (2 * np.pi,)
+    return C.Config(f"t{dim}{degree}{n_tau}", dim, degree, n_tau, tuple(cells), lower, upper,
+                    tuple(velocity), dt, u0 or ("burgers" if model else "sin2pi_x"), 7,
+                    model=model)
+
+
+CASES = [
+    C.CONFIGS["c1"],                                            # exact c1
+    C.CONFIGS["c2"].scaled((8, 8)),                             # c2 physics, small mesh
+    C.CONFIGS["c4"].scaled((8, 8, 8)),                          # c4 physics, small mesh
+    C.CONFIGS["c3"].scaled((64,)),                              # Burgers
+    make(3, 3, 4, (16, 4, 4), (-0.7, 0.4, -1.1)),               # fast kernel, upwind on both sides
+    make(3, 3, 4, (6, 5, 3), (0.3, -1.2, 0.8)),                 # generic (nx % 8 != 0)
+    make(3, 2, 3, (4, 3, 5), (1.0, 0.5, -0.25)),
+    make(2, 2, 3, (5, 7), (-1.0, 0.3)),
+    make(2, 3, 2, (4, 4), (0.0, 1.0)),
+    make(1, 2, 3, (9,), (-1.5,)),
+    make(1, 5, 6, (7,), (0.8,)),
+    make(3, 4, 5, (3, 2, 2), (1.0, -1.0, 0.5)),
+]
+IDS = [c.name if c.name[0] == "c" else f"d{c.dim}p{c.degree}nt{c.n_tau}{c.cells}" for c in CASES]
+
+
+def kernels_for(cfg):
+    ks = [L.STG_KERNEL_GENERIC]
+    if cfg.dim == 3 and cfg.degree == 3 and cfg.n_tau == 4 and cfg.cells[0] % 8 == 0:
+        ks.append(L.STG_KERNEL_FAST)
+    return ks
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+def test_st_residual_parity(cfg):
+    U = C.random_slab(cfg)
+    un = C.initial_state(cfg)
+    for k in kernels_for(cfg):
+        op, pr = pair(cfg, k)
+        ref = pr.st_residual(0.0, cfg.dt, un, U)
+        got = op.st_residual(0.0, cfg.dt, dev(un), dev(U))
+        assert rel(got, ref) <= TOL_OP, (k, rel(got, ref))
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+def test_st_jvp_parity(cfg):
+    U = C.random_slab(cfg)
+    if cfg.model == L.STG_MODEL_BURGERS:
+        U = 1.0 + 0.3 * U
+    v = np.random.default_rng(11).uniform(-1, 1, cfg.n_dof)
+    for k in kernels_for(cfg):
+        op, pr = pair(cfg, k)
+        ref = pr.st_jvp(0.0, cfg.dt, U, v)
+        got = op.st_jvp(0.0, cfg.dt, dev(U), dev(v))
+        assert rel(got, ref) <= TOL_OP, (k, rel(got, ref))
+
+
+@pytest.mark.parametrize("cfg", CASES, ids=IDS)
+@pytest.mark.parametrize("form", [L.STG_FORM_A, L.STG_FORM_A_INV])
+def test_stage_residual_and_jvp_parity(cfg, form):
+    if cfg.n_tau > 4:
+        pytest.skip("lobatto_tableau closed forms stored for s <= 4 (operators.hpp:76-112)")
+    U = C.random_slab(cfg)
+    if cfg.model == L.STG_MODEL_BURGERS:
+        U = 1.0 + 0.3 * U
+    u = C.initial_state(cfg)
+    v = np.random.default_rng(5).uniform(-1, 1, cfg.n_dof)
+    for k in kernels_for(cfg):
+        op, pr = pair(cfg, k)
+        ref = pr.stage_residual(cfg.n_tau, form, 0.0, cfg.dt, u, U)
+        got = op.stage_residual(form, 0.0, cfg.dt, dev(u), dev(U))
+        assert rel(got, ref) <= TOL_OP, ("residual", k, rel(got, ref))
+        ref = pr.stage_jvp(cfg.n_tau, form, 0.0, cfg.dt, U, v)
+        got = op.stage_jvp(form, 0.0, cfg.dt, dev(U), dev(v))
+        assert rel(got, ref) <= TOL_OP, ("jvp", k, rel(got, ref))
+
+
+@pytest.mark.parametrize("cfg", CASES[:4], ids=IDS[:4])
+def test_spatial_rhs_parity(cfg):
+    op, pr = pair(cfg)
+    u = C.initial_state(cfg) + np.random.default_rng(3).uniform(-0.1, 0.1, cfg.n_sdof)
+    assert rel(op.spatial_rhs(dev(u)), pr.rhs(u)) <= TOL_OP
+    v = np.random.default_rng(4).uniform(-1, 1, cfg.n_sdof)
+    assert rel(op.spatial_jvp(dev(u), dev(v)), pr.spatial_jvp(u, v)) <= TOL_OP
+
+
+def test_spatial_single_cell_kat():  # test_spatial.cpp:56-65 on the device
+    op = SlabOperator(1, 1, 2, (1,), (0.0,), (1.0,), (1.0,))
+    A = np.array([[-1.0, 1.0], [1.0, -1.0]])
+    for u in (np.array([1.0, 0.0]), np.array([0.3, -0.7])):
+        assert np.abs(op.spatial_rhs(dev(u)).cpu().numpy() - A @ u).max() < 1e-14
+
+
+# ---- full-size configs ---------------------------------------------------------
+@pytest.mark.parametrize("name", ["c4", "c2"])
+def test_full_size_residual_parity(name):
+    cfg = C.CONFIGS[name]
+    O.set_threads(O.max_threads())
+    op, pr = pair(cfg)
+    U = C.random_slab(cfg)
+    un = C.initial_state(cfg)
+    ref = pr.st_residual(0.0, cfg.dt, un, U)
+    got = op.st_residual(0.0, cfg.dt, dev(un), dev(U))
+    assert rel(got, ref) <= TOL_OP
+    v = np.random.default_rng(cfg.seed + 100).uniform(-1, 1, cfg.n_dof)
+    ref = pr.st_jvp(0.0, cfg.dt, U, v)
+    got = op.st_jvp(0.0, cfg.dt, dev(U), dev(v))
+    assert rel(got, ref) <= TOL_OP
+
+
+@pytest.mark.parametrize("name", ["c4", "c2"])
+def test_full_size_properties(name):
+    cfg = C.CONFIGS[name]
+    op = SlabOperator(**cfg.kwargs())
+    # free stream: U = 1 (x) c with u_n = c gives R = 0 (SBP telescoping + D1 = 0)
+    c = dev(np.full(cfg.n_sdof, 0.37))
+    U = c.repeat(cfg.n_tau)
+    assert op.st_residual(0.0, cfg.dt, c, U).abs().max().item() <= 1e-12
+    # linearity: R(U1 + U2; un1 + un2) = R(U1; un1) + R(U2; un2)
+    U1, U2 = dev(C.random_slab(cfg, 1)), dev(C.random_slab(cfg, 2))
+    u1, u2 = dev(C.initial_state(cfg)), dev(np.cos(C.initial_state(cfg)))
+    lhs = op.st_residual(0.0, cfg.dt, u1 + u2, U1 + U2)
+    rhs = op.st_residual(0.0, cfg.dt, u1, U1) + op.st_residual(0.0, cfg.dt, u2, U2)
+    assert rel(lhs, rhs.cpu().numpy()) <= 1e-13
+    # J v = R(v) - R(0) for the linear model
+    z = torch.zeros_like(U1)
+    jv = op.st_jvp(0.0, cfg.dt, None, U2)
+    diff = op.st_residual(0.0, cfg.dt, u1, U2) - op.st_residual(0.0, cfg.dt, u1, z)
+    assert rel(jv, diff.cpu().numpy()) <= 1e-13
+    # determinism: bitwise identical reruns
+    a = op.st_residual(0.0, cfg.dt, u1, U1)
+    b = op.st_residual(0.0, cfg.dt, u1, U1)
+    assert torch.equal(a, b)
+
+
+def test_fast_and_generic_kernels_agree_full_c4():
+    cfg = C.CONFIGS["c4"]
+    fast = SlabOperator(**cfg.kwargs(), kernel=L.STG_KERNEL_FAST)
+    gen = SlabOperator(**cfg.kwargs(), kernel=L.STG_KERNEL_GENERIC)
+    U, un = dev(C.random_slab(cfg)), dev(C.initial_state(cfg))
+    a = fast.st_residual(0.0, cfg.dt, un, U)
+    b = gen.st_residual(0.0, cfg.dt, un, U)
+    assert rel(a, b.cpu().numpy()) <= 1e-13
+
+
+def test_host_buffer_variant_matches_device():
+    cfg = C.CONFIGS["c4"].scaled((8, 8, 8))
+    op = SlabOperator(**cfg.kwargs())
+    U, un = C.random_slab(cfg), C.initial_state(cfg)
+    a = op.st_residual_host(0.0, cfg.dt, un, U)
+    b = op.st_residual(0.0, cfg.dt, dev(un), dev(U)).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+# ---- solvers ---------------------------------------------------------------------
+def test_c1_slab_solve_vs_oracle():
+    cfg = C.CONFIGS["c1"]
+    op, pr = pair(cfg)
+    un = C.initial_state(cfg)
+    Uo, uo, _, _ = pr.stdg_step(0.0, cfg.dt, un, linear=O.DENSE_LU)
+    cfgn = NewtonConfig(abs_tol=1e-14, rel_tol=1e-13, gmres_tol=1e-13)
+    U, un1, info = op.stdg_step(0.0, cfg.dt, dev(un), cfgn)
+    assert rel(U, Uo) <= TOL_SOLVE
+    assert rel(un1, uo) <= TOL_SOLVE
+    assert info.newton_iterations >= 1 and info.linear_iterations > 0
+    assert np.allclose(U[-cfg.n_sdof:].cpu().numpy(), un1.cpu().numpy(), rtol=0, atol=0)
+
+
+def test_gmres_matches_oracle_gmres_small_3d():
+    cfg = C.CONFIGS["c4"].scaled((8, 8, 8))
+    op, pr = pair(cfg)
+    un = C.initial_state(cfg)
+    cfgn = dict(abs_tol=0.0, rel_tol=1e-12, gmres_tol=1e-13)
+    Uo, uo, _, lino = pr.stdg_step(0.0, cfg.dt, un, linear=O.GMRES, **cfgn)
+    U, un1, info = op.stdg_step(0.0, cfg.dt, dev(un), NewtonConfig(**cfgn))
+    assert rel(U, Uo) <= TOL_SOLVE
+
+
+@pytest.mark.parametrize("form", [L.STG_FORM_A, L.STG_FORM_A_INV])
+def test_rk_step_vs_oracle_and_equivalence(form):
+    # test_stdg.cpp:111-135 on the device: STDG slab == LoDG stages
+    cfg = make(1, 2, 3, (8,), (1.0,), dt=0.05)
+    op, pr = pair(cfg)
+    u0 = np.sin(2 * np.pi * C.node_coords(cfg)[:, 0]) + 0.3
+    tight = NewtonConfig(abs_tol=1e-14, rel_tol=1e-13, gmres_tol=1e-14)
+    Ua, ua, _ = op.stdg_step(0.0, cfg.dt, dev(u0), tight)
+    Ub, ub, info = op.rk_step(form, 0.0, cfg.dt, dev(u0), tight)
+    assert rel(ua, ub.cpu().numpy()) <= 1e-10
+    assert rel(Ua, Ub.cpu().numpy()) <= 1e-9
+    Uo, uo, _, _ = pr.rk_step(3, form, 0.0, cfg.dt, u0, linear=O.DENSE_LU)
+    assert rel(ub, uo) <= TOL_SOLVE
+
+
+def test_lodg_stages_match_stdg_slab_small_c5():
+    # c5 physics on a small mesh: stage solution == slab solution to 1e-10
+    cfg = C.CONFIGS["c5"].scaled((8, 8, 8))
+    op = SlabOperator(**cfg.kwargs())
+    un = dev(C.initial_state(cfg))
+    tight = NewtonConfig(abs_tol=0.0, rel_tol=1e-13, gmres_tol=1e-14)
+    Ua, ua, _ = op.stdg_step(0.0, cfg.dt, un, tight)
+    Ub, ub, _ = op.rk_step(L.STG_FORM_A_INV, 0.0, cfg.dt, un, tight)
+    assert rel(Ub, Ua.cpu().numpy()) <= TOL_SOLVE
+    assert rel(ub, ua.cpu().numpy()) <= TOL_SOLVE
+
+
+def test_burgers_newton_vs_oracle():
+    cfg = C.CONFIGS["c3"].scaled((64,))
+    op, pr = pair(cfg)
+    un = C.initial_state(cfg)
+    Uo, uo, ito, _ = pr.stdg_step(0.0, 1e-3, un, linear=O.DENSE_LU, abs_tol=1e-13, rel_tol=1e-13)
+    U, un1, info = op.stdg_step(0.0, 1e-3, dev(un),
+                                NewtonConfig(abs_tol=1e-13, rel_tol=1e-13, gmres_tol=1e-14))
+    assert info.newton_iterations >= 2  # nonlinear
+    assert rel(U, Uo) <= TOL_SOLVE
+
+
+def test_burgers_fd_jvp_close_to_exact():
+    cfg = C.CONFIGS["c3"].scaled((64,))
+    op = SlabOperator(**cfg.kwargs())
+    U = dev(1.0 + 0.3 * C.random_slab(cfg))
+    v = dev(np.random.default_rng(1).uniform(-1, 1, cfg.n_dof))
+    ex = op.st_jvp(0.0, 1e-3, U, v)
+    fd = op.st_jvp(0.0, 1e-3, U, v, fd_eps=1e-7)
+    assert rel(fd, ex.cpu().numpy()) <= 1e-6
+
+
+def test_nonconvergence_and_bad_input_errors():
+    cfg = C.CONFIGS["c1"]
+    op = SlabOperator(**cfg.kwargs())
+    un = dev(C.initial_state(cfg))
+    with pytest.raises(NonconvergenceError, match="stdg_step element at t=0"):
+        op.stdg_step(0.0, cfg.dt, un, NewtonConfig(max_iter=0))
+    with pytest.raises(ValueError):
+        op.stdg_step(0.0, -1.0, un)
+    with pytest.raises(ValueError):
+        op.st_residual(0.0, cfg.dt, un, dev(np.zeros(cfg.n_dof - 1)))
+    with pytest.raises(ValueError):
+        SlabOperator(3, 3, 4, (8, 8, 8), (0, 0, 0), (1, 1, 1), (1, 1, 1),
+                     kernel=L.STG_KERNEL_FAST).stage_residual  # ok to construct
+        SlabOperator(3, 3, 3, (6, 6, 6), (0, 0, 0), (1, 1, 1), (1, 1, 1),
+                     kernel=L.STG_KERNEL_FAST).st_residual(
+            0.0, 0.01, dev(np.zeros(6 ** 3 * 64)), dev(np.zeros(3 * 6 ** 3 * 64)))
+
+
+def test_launch_counter_counts_native_kernels():
+    cfg = C.CONFIGS["c4"].scaled((8, 8, 8))
+    op = SlabOperator(**cfg.kwargs())
+    n0 = op.kernel_launches()
+    op.st_residual(0.0, cfg.dt, dev(C.initial_state(cfg)), dev(C.random_slab(cfg)))
+    assert op.kernel_launches() == n0 + 1
