@@ -23,6 +23,8 @@
 //                            memory.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "kernels.hpp"
 
 namespace stg {
@@ -317,8 +319,9 @@ __global__ void __launch_bounds__(fast::THREADS, 4)
     slab3d_n4_tma(const __grid_constant__ CUtensorMap tmX, const SlabArgs a) {
   using namespace fast;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // align to 1024 B (128B-swizzle atoms) by integer offset so the pointer
+  // keeps its shared-memory provenance (LDS/STS, not generic LD/ST)
+  unsigned char* base = smem_raw + ((1024u - (fast::smem_u32(smem_raw) & 1023u)) & 1023u);
   double* Xs = reinterpret_cast<double*>(base);
   double* FA = Xs + TILE_DOUBLES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(FA + TILE_DOUBLES);
@@ -491,6 +494,270 @@ __global__ void __launch_bounds__(fast::THREADS, 4)
 }
 
 // ---------------------------------------------------------------------------
+// d = 3, N = 3, n_tau = 4, persistent + double-buffered: every operand of a
+// segment (8-element x-pencil tile, y/z face traces of the upwind/downwind
+// neighbour rows, x halos, u_n) arrives by TMA into a 2-stage ring, so the
+// loads of segment i+1 are in flight while segment i is computed.  No
+// synchronous global loads remain; R is stored with coalesced STG.
+// ---------------------------------------------------------------------------
+namespace pst {
+using fast::E;
+constexpr int THREADS = 16 * E;
+constexpr int MAIN = 16384;          // [t][e][z] x 128 B rows, 128B-swizzled
+constexpr int FACE = 4096;           // y face: [t][e][z][x]; z face: [t][e][y][x]
+constexpr int WBUF = 4096;           // u_n: [e][64]
+constexpr int HALO = 1024;           // [t][z][y][2]
+constexpr int OFF_YL = MAIN, OFF_YR = OFF_YL + FACE, OFF_ZL = OFF_YR + FACE,
+              OFF_ZR = OFF_ZL + FACE, OFF_W = OFF_ZR + FACE, OFF_HL = OFF_W + WBUF,
+              OFF_HR = OFF_HL + HALO;
+constexpr int STAGE = ((OFF_HR + HALO + 1023) / 1024) * 1024;  // 39936
+constexpr int FA_OFF = 2 * STAGE;
+constexpr int BAR_OFF = FA_OFF + MAIN;
+constexpr int SMEM_BYTES = BAR_OFF + 64 + 1024;
+
+struct Maps {
+  CUtensorMap main;   // 4-D {16, 4, cells, 4}, box {16, 4, E, 4}, swizzle 128B
+  CUtensorMap yface;  // 5-D {4, 4, 4, cells, 4}, box {4, 1, 4, E, 4}
+  CUtensorMap zface;  // 5-D, box {4, 4, 1, E, 4}
+  CUtensorMap halo;   // 5-D, box {2, 4, 4, 1, 4}
+  CUtensorMap w;      // 2-D {64, cells}, box {64, E}
+};
+
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+struct Need {
+  bool lx, rx, ly, ry, lz, rz, w;
+};
+
+// Issue every TMA of segment `seg` into the stage at `sbase` (one thread).
+__device__ __forceinline__ void issue(const Maps& m, const SlabArgs& a, const Need& nd, int seg,
+                                      unsigned char* sbase, uint32_t bar) {
+  const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
+  const int e0 = seg * E;
+  const int cx0 = e0 % nx, cy = (e0 / nx) % ny, cz = e0 / (nx * ny);
+  uint32_t bytes = MAIN;
+  bytes += nd.ly ? FACE : 0;
+  bytes += nd.ry ? FACE : 0;
+  bytes += nd.lz ? FACE : 0;
+  bytes += nd.rz ? FACE : 0;
+  bytes += nd.w ? WBUF : 0;
+  bytes += nd.lx ? HALO : 0;
+  bytes += nd.rx ? HALO : 0;
+  fast::mbar_expect_tx(bar, bytes);
+  const uint32_t s = fast::smem_u32(sbase);
+  fast::tma_load_4d(s, &m.main, bar, 0, 0, e0, 0);
+  if (nd.ly) tma_load_5d(s + OFF_YL, &m.yface, bar, 0, 3, 0, e0 + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx, 0);
+  if (nd.ry) tma_load_5d(s + OFF_YR, &m.yface, bar, 0, 0, 0, e0 + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx, 0);
+  if (nd.lz) tma_load_5d(s + OFF_ZL, &m.zface, bar, 0, 0, 3, e0 + ((cz == 0 ? nz - 1 : cz - 1) - cz) * nx * ny, 0);
+  if (nd.rz) tma_load_5d(s + OFF_ZR, &m.zface, bar, 0, 0, 0, e0 + ((cz == nz - 1 ? 0 : cz + 1) - cz) * nx * ny, 0);
+  if (nd.w) tma_load_2d(s + OFF_W, &m.w, bar, 0, e0);
+  if (nd.lx) tma_load_5d(s + OFF_HL, &m.halo, bar, 2, 0, 0, e0 - cx0 + (cx0 == 0 ? nx - 1 : cx0 - 1), 0);
+  if (nd.rx) {
+    const int cxe = cx0 + E - 1;
+    tma_load_5d(s + OFF_HR, &m.halo, bar, 0, 0, 0, e0 - cx0 + (cxe == nx - 1 ? 0 : cxe + 1), 0);
+  }
+}
+}  // namespace pst
+
+template <bool FULL_S>
+__global__ void __launch_bounds__(pst::THREADS, 2)
+    slab3d_n4_persist(const __grid_constant__ pst::Maps maps, const SlabArgs a) {
+  using namespace pst;
+  using fast::row_of;
+  using fast::swz;
+  extern __shared__ unsigned char smem_raw[];
+  // align to 1024 B (128B-swizzle atoms) by integer offset so the pointer
+  // keeps its shared-memory provenance (LDS/STS, not generic LD/ST)
+  unsigned char* base = smem_raw + ((1024u - (fast::smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* FA = reinterpret_cast<double*>(base + FA_OFF);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + BAR_OFF);
+  const uint32_t bar0 = fast::smem_u32(bars), bar1 = fast::smem_u32(bars + 1);
+
+  const int tid = threadIdx.x;
+  const long long ns = a.g.n_sdof;
+  const int nseg = a.g.n_cells / E;
+  const Need nd{a.sp.cL[0] != 0.0, a.sp.cR[0] != 0.0, a.sp.cL[1] != 0.0, a.sp.cR[1] != 0.0,
+                a.sp.cL[2] != 0.0, a.sp.cR[2] != 0.0, a.has_w != 0};
+
+  if (tid == 0) {
+    fast::mbar_init(bar0, 1);
+    fast::mbar_init(bar1, 1);
+    fast::fence_mbar_init();
+  }
+  __syncthreads();
+  int seg = blockIdx.x;
+  if (tid == 0 && seg < nseg) issue(maps, a, nd, seg, base, bar0);
+
+  // thread identities of the two phases
+  const int zA = tid & 3, eA = (tid >> 2) & (E - 1), tA = tid >> 5;
+  const int xB = tid & 3, yB = (tid >> 2) & 3, eB = tid >> 4;
+  const int qB = yB * 4 + xB;
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int st = it & 1;
+    unsigned char* sb = base + st * STAGE;
+    const double* Xs = reinterpret_cast<const double*>(sb);
+    if (tid == 0) {
+      const int nxt = seg + gridDim.x;
+      if (nxt < nseg) {
+        fence_proxy_async();
+        issue(maps, a, nd, nxt, base + (st ^ 1) * STAGE, st ? bar0 : bar1);
+      }
+    }
+    while (!fast::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+
+    // ---- phase A: x and y derivatives of the (y,x) plane at (t, e, z) -----
+    {
+      const int row = row_of(tA, eA, zA);
+      const int sw = row & 7;
+      double u[16];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const double2 v = *reinterpret_cast<const double2*>(Xs + row * 16 + ((c ^ sw) << 1));
+        u[2 * c] = v.x;
+        u[2 * c + 1] = v.y;
+      }
+      double hl[4] = {0, 0, 0, 0}, hr[4] = {0, 0, 0, 0};
+      double yl[4] = {0, 0, 0, 0}, yr[4] = {0, 0, 0, 0};
+      if (nd.lx) {
+        if (eA > 0) {
+          const int rl = row_of(tA, eA - 1, zA);
+#pragma unroll
+          for (int y = 0; y < 4; ++y) hl[y] = Xs[swz(rl, 4 * y + 3)];
+        } else {
+          const double* H = reinterpret_cast<const double*>(sb + OFF_HL) + (tA * 4 + zA) * 8;
+#pragma unroll
+          for (int y = 0; y < 4; ++y) hl[y] = H[2 * y + 1];
+        }
+      }
+      if (nd.rx) {
+        if (eA < E - 1) {
+          const int rr = row_of(tA, eA + 1, zA);
+#pragma unroll
+          for (int y = 0; y < 4; ++y) hr[y] = Xs[swz(rr, 4 * y)];
+        } else {
+          const double* H = reinterpret_cast<const double*>(sb + OFF_HR) + (tA * 4 + zA) * 8;
+#pragma unroll
+          for (int y = 0; y < 4; ++y) hr[y] = H[2 * y];
+        }
+      }
+      const int fo = ((tA * E + eA) * 4 + zA) * 4;
+      if (nd.ly) {
+        const double* Y = reinterpret_cast<const double*>(sb + OFF_YL) + fo;
+        const double2 v0 = *reinterpret_cast<const double2*>(Y);
+        const double2 v1 = *reinterpret_cast<const double2*>(Y + 2);
+        yl[0] = v0.x; yl[1] = v0.y; yl[2] = v1.x; yl[3] = v1.y;
+      }
+      if (nd.ry) {
+        const double* Y = reinterpret_cast<const double*>(sb + OFF_YR) + fo;
+        const double2 v0 = *reinterpret_cast<const double2*>(Y);
+        const double2 v1 = *reinterpret_cast<const double2*>(Y + 2);
+        yr[0] = v0.x; yr[1] = v0.y; yr[2] = v1.x; yr[3] = v1.y;
+      }
+      double f[16];
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          double g = 0.0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) g = fma(a.sp.V[0][x][k], u[4 * y + k], g);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) g = fma(a.sp.V[1][y][k], u[4 * k + x], g);
+          if (x == 0) g = fma(a.sp.cL[0], hl[y], g);
+          if (x == 3) g = fma(a.sp.cR[0], hr[y], g);
+          if (y == 0) g = fma(a.sp.cL[1], yl[x], g);
+          if (y == 3) g = fma(a.sp.cR[1], yr[x], g);
+          f[4 * y + x] = g;
+        }
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        *reinterpret_cast<double2*>(FA + row * 16 + ((c ^ sw) << 1)) =
+            make_double2(f[2 * c], f[2 * c + 1]);
+    }
+    __syncthreads();
+
+    // ---- phase B: z derivative, temporal mixing, store ---------------------
+    {
+      const int e0 = seg * E;
+      const int cellB = e0 + eB;
+      double u[4][4], f[4][4];  // [t][z]
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          const int o = swz(row_of(t, eB, z), qB);
+          u[t][z] = Xs[o];
+          f[t][z] = FA[o];
+        }
+      double zl[4] = {0, 0, 0, 0}, zr[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
+      if (nd.lz) {
+        const double* Z = reinterpret_cast<const double*>(sb + OFF_ZL) + eB * 16 + qB;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) zl[t] = Z[t * E * 16];
+      }
+      if (nd.rz) {
+        const double* Z = reinterpret_cast<const double*>(sb + OFF_ZR) + eB * 16 + qB;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) zr[t] = Z[t * E * 16];
+      }
+      if (nd.w) {
+        const double* W = reinterpret_cast<const double*>(sb + OFF_W) + eB * 64 + qB;
+#pragma unroll
+        for (int z = 0; z < 4; ++z) w[z] = W[16 * z];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          double g = f[t][z];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) g = fma(a.sp.V[2][z][k], u[t][k], g);
+          if (z == 0) g = fma(a.sp.cL[2], zl[t], g);
+          if (z == 3) g = fma(a.sp.cR[2], zr[t], g);
+          f[t][z] = g;
+        }
+      double* Rb = a.R + (long long)cellB * 64 + qB;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          double acc = a.mx.c[r] * w[z];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc = fma(a.mx.T[r][j], u[j][z], acc);
+          if (FULL_S) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc = fma(a.mx.S[r][j], f[j][z], acc);
+          } else {
+            acc = fma(a.mx.S[r][r], f[r][z], acc);
+          }
+          Rb[r * ns + 16 * z] = acc;
+        }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // host-side launch helpers
 // ---------------------------------------------------------------------------
 template <int N1>
@@ -576,24 +843,101 @@ bool slab_fast_supported(const SlabArgs& a) {
          (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 && get_encode() != nullptr;
 }
 
+namespace {
+bool encode(EncodeFn enc, CUtensorMap* map, const double* base, int rank, const cuuint64_t* gdim,
+            const cuuint64_t* gstride, const cuuint32_t* box, CUtensorMapSwizzle swz) {
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), gdim, gstride,
+             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int fast_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("STG_FAST_VARIANT");
+    v = e ? std::atoi(e) : 2;
+  }
+  return v;
+}
+}  // namespace
+
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   EncodeFn enc = get_encode();
   if (!enc) return -1;
-  CUtensorMap map;
-  const cuuint64_t gdim[4] = {16, 4, cuuint64_t(a.g.n_cells), 4};
-  const cuuint64_t gstride[3] = {128, 512, cuuint64_t(a.g.n_sdof) * 8};
-  const cuuint32_t box[4] = {16, 4, fast::E, 4};
-  const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.X), gdim,
-                         gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) return -1;
-  const int blocks = a.g.n_cells / fast::E;
-  if (a.full_s) {
-    slab3d_n4_tma<true><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+  const cuuint64_t cells = cuuint64_t(a.g.n_cells);
+  const cuuint64_t tstride = cuuint64_t(a.g.n_sdof) * 8;
+  if (fast_variant() == 1) {
+    CUtensorMap map;
+    const cuuint64_t gdim[4] = {16, 4, cells, 4};
+    const cuuint64_t gstride[3] = {128, 512, tstride};
+    const cuuint32_t box[4] = {16, 4, fast::E, 4};
+    if (!encode(enc, &map, a.X, 4, gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
+    const int blocks = a.g.n_cells / fast::E;
+    if (a.full_s) {
+      slab3d_n4_tma<true><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+    } else {
+      slab3d_n4_tma<false><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+    }
+    return 1;
+  }
+  pst::Maps m;
+  {
+    const cuuint64_t gdim[4] = {16, 4, cells, 4};
+    const cuuint64_t gstride[3] = {128, 512, tstride};
+    const cuuint32_t box[4] = {16, 4, pst::E, 4};
+    if (!encode(enc, &m.main, a.X, 4, gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
+  }
+  {
+    const cuuint64_t gdim[5] = {4, 4, 4, cells, 4};
+    const cuuint64_t gstride[4] = {32, 128, 512, tstride};
+    const cuuint32_t by[5] = {4, 1, 4, pst::E, 4};
+    const cuuint32_t bz[5] = {4, 4, 1, pst::E, 4};
+    const cuuint32_t bh[5] = {2, 4, 4, 1, 4};
+    if (!encode(enc, &m.yface, a.X, 5, gdim, gstride, by, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
+    if (!encode(enc, &m.zface, a.X, 5, gdim, gstride, bz, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
+    if (!encode(enc, &m.halo, a.X, 5, gdim, gstride, bh, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
+  }
+  if (a.has_w) {
+    if (reinterpret_cast<uintptr_t>(a.W) & 15) return -1;
+    const cuuint64_t gdim[2] = {64, cells};
+    const cuuint64_t gstride[1] = {512};
+    const cuuint32_t box[2] = {64, pst::E};
+    if (!encode(enc, &m.w, a.W, 2, gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
   } else {
-    slab3d_n4_tma<false><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+    m.w = m.main;  // unused
+  }
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(slab3d_n4_persist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         pst::SMEM_BYTES);
+    cudaFuncSetAttribute(slab3d_n4_persist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         pst::SMEM_BYTES);
+    attr = true;
+  }
+  const int nseg = a.g.n_cells / pst::E;
+  static int per_sm = [] {
+    const char* e = std::getenv("STG_FAST_CTAS_PER_SM");
+    const int v = e ? std::atoi(e) : 2;
+    return v < 1 ? 1 : (v > 2 ? 2 : v);
+  }();
+  int grid = per_sm * num_sms();
+  if (grid > nseg) grid = nseg;
+  if (a.full_s) {
+    slab3d_n4_persist<true><<<grid, pst::THREADS, pst::SMEM_BYTES, s>>>(m, a);
+  } else {
+    slab3d_n4_persist<false><<<grid, pst::THREADS, pst::SMEM_BYTES, s>>>(m, a);
   }
   return 1;
 }

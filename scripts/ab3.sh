@@ -1,0 +1,6 @@
+#!/bin/bash
+mkdir -p gpurun_out
+for v in 1 2; do
+  STG_FAST_VARIANT=$v timeout 300 python bench.py --steps 8000 --no-cpu --no-extra > gpurun_out/bench_v$v.json 2>/dev/null
+done
+timeout 900 python -m pytest tests -x -q -m gpu -k "parity and (c4 or fast or d3)" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
