@@ -47,6 +47,21 @@ def dist_env():
     return ws, rank, local
 
 
+def reduce_max(value: float, dist, device) -> float:
+    """Max over ranks (the job's time is its slowest replica's)."""
+    import torch
+    if dist is None:
+        return float(value)
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def whole_job_value(world_size: int, n_dof: int, steps: int, ms: float) -> float:
+    """DOF-applications/s over all replicas (weak scaling: fixed work per GPU)."""
+    return world_size * n_dof * steps / (ms / 1e3)
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -214,13 +229,9 @@ def run_ours(args):
         if dist:
             dist.barrier()
     launches = op.kernel_launches() - launches0
-    ms = ev0.elapsed_time(ev1)
-    if dist:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = reduce_max(ev0.elapsed_time(ev1), dist, dev)
     ms_step = ms / args.steps
-    value = ws * cfg.n_dof * args.steps / (ms / 1e3)
+    value = whole_job_value(ws, cfg.n_dof, args.steps, ms)
 
     hbm, hbm_src = peaks()
     alg = C.residual_bytes(cfg)
@@ -229,7 +240,7 @@ def run_ours(args):
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("slab3d_n4_tma")
+            traffic = json.loads(tf.read_text()).get("slab3d_n4_persist")
         except Exception:
             traffic = None
 
@@ -245,15 +256,14 @@ def run_ours(args):
         op.st_residual_host(0.0, cfg.dt, npun, npU, out=npR)
     if dist:
         dist.barrier()
-    t0 = time.perf_counter()
+    torch.cuda.synchronize()
+    ev0.record(stream)  # the host entry point's copies run on this stream
     for _ in range(e2e_steps):
         op.st_residual_host(0.0, cfg.dt, npun, npU, out=npR)
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_val = ws * cfg.n_dof * e2e_steps / e2e_s
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = reduce_max(ev0.elapsed_time(ev1), dist, dev)
+    e2e_val = whole_job_value(ws, cfg.n_dof, e2e_steps, e2e_ms)
 
     extra = {}
     if not args.no_extra and rank == 0:
@@ -327,16 +337,107 @@ def extras(op, cfg, C, NewtonConfig, torch, dev, args):
         ms = timed(lambda: op.stage_residual(form, 0.0, cfg.dt, un, U, out=R), stream, torch, 50)
         out[name] = {"dof_per_s": cfg.n_dof / (ms / 1e3), "ms": ms,
                      "hbm_frac": C.residual_bytes(cfg) / (ms / 1e3) / 1e9 / hbm}
-    # one slab solve (GMRES(30), rel tol 1e-10), u_n resident, from guess 1 (x) u_n
-    cfgn = NewtonConfig(abs_tol=0.0, rel_tol=1e-10, gmres_tol=1e-10, gmres_restart=30)
+    out.update(solves(op, cfg, C, NewtonConfig, torch, dev, args))
+    return out
+
+
+def _wall(torch, fn):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    Us, un1, info = op.stdg_step(0.0, cfg.dt, un, cfgn)
+    r = fn()
     torch.cuda.synchronize()
-    out["slab_solve"] = {"seconds": time.perf_counter() - t0, "gmres_tol": 1e-10,
-                         "newton_iterations": info.newton_iterations,
-                         "gmres_iterations": info.linear_iterations,
-                         "final_residual_inf": info.final_residual}
+    return time.perf_counter() - t0, r
+
+
+def solves(op, cfg, C, NewtonConfig, torch, dev, args):
+    """Slab solves of every BASELINE config (device-resident u_n, from guess
+    1 (x) u_n, wall time with a CUDA sync on both sides), the c5 stage system
+    against the c4 slab, and the CPU oracle's c4 / c1 solve times beside them."""
+    from paper_2201_05800_b200.api import SlabOperator
+    from paper_2201_05800_b200 import _lib as L
+    out = {}
+    un = torch.as_tensor(C.initial_state(cfg), device=dev)
+    # c4: one Newton step, GMRES(30) to rel tol 1e-10 (||r||_2 <= 1e-10 ||b||_2)
+    nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10, gmres_restart=30)
+    op.stdg_step(0.0, cfg.dt, un, nc)  # warm (workspace allocation)
+    t, (U4, u4, info) = _wall(torch, lambda: op.stdg_step(0.0, cfg.dt, un, nc))
+    out["c4_slab_solve"] = {"seconds": t, "gmres_tol": 1e-10, "newton": info.newton_iterations,
+                            "gmres_iterations": info.linear_iterations,
+                            "final_residual_inf": info.final_residual}
+    # c5: Lobatto IIIC s=4 stage system (A^-1 form) on the c4 mesh, vs the c4 slab
+    c5 = C.CONFIGS["c5"]
+    op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, un, nc)  # warm (lazy module load of its kernels)
+    t, (U5, u5, info5) = _wall(torch, lambda: op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, un, nc))
+    gap = float((U5 - U4).abs().max() / U4.abs().max())
+    out["c5_stage_solve"] = {"seconds": t, "newton": info5.newton_iterations,
+                             "gmres_iterations": info5.linear_iterations,
+                             "max_rel_gap_to_c4_slab": gap}
+    # c2: 2-D N=4, R(U) rate and slab solve
+    c2 = C.CONFIGS["c2"]
+    op2 = SlabOperator(**c2.kwargs())
+    U2 = torch.as_tensor(C.random_slab(c2), device=dev)
+    u2 = torch.as_tensor(C.initial_state(c2), device=dev)
+    R2 = torch.empty_like(U2)
+    ms = timed(lambda: op2.st_residual(0.0, c2.dt, u2, U2, out=R2), torch.cuda.current_stream(),
+               torch, 30)
+    hbm, _ = peaks()
+    op2.stdg_step(0.0, c2.dt, u2, nc)
+    t, (_, _, info2) = _wall(torch, lambda: op2.stdg_step(0.0, c2.dt, u2, nc))
+    out["c2"] = {"residual_dof_per_s": c2.n_dof / (ms / 1e3),
+                 "residual_hbm_frac": C.residual_bytes(c2) / (ms / 1e3) / 1e9 / hbm,
+                 "slab_solve_s": t, "gmres_iterations": info2.linear_iterations}
+    del op2, U2, u2, R2
+    # c1: 1000 R(U) applies (launch-latency bound) and the GMRES slab solve at 1e-12
+    c1 = C.CONFIGS["c1"]
+    op1 = SlabOperator(**c1.kwargs())
+    u1 = torch.as_tensor(C.initial_state(c1), device=dev)
+    U1 = torch.as_tensor(C.random_slab(c1), device=dev)
+    R1 = torch.empty_like(U1)
+    us = 1e3 * timed(lambda: op1.st_residual(0.0, c1.dt, u1, U1, out=R1),
+                     torch.cuda.current_stream(), torch, 1000)
+    nc1 = NewtonConfig(abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12)
+    op1.stdg_step(0.0, c1.dt, u1, nc1)
+    t1, (_, _, info1) = _wall(torch, lambda: op1.stdg_step(0.0, c1.dt, u1, nc1))
+    out["c1"] = {"us_per_residual_python_loop": us, "slab_solve_s": t1,
+                 "gmres_iterations": info1.linear_iterations}
+    # c3: Burgers, inexact Newton-GMRES with FD J.v (eps 1e-7), 10 slabs
+    c3 = C.CONFIGS["c3"]
+    op3 = SlabOperator(**c3.kwargs())
+    u = torch.as_tensor(C.initial_state(c3), device=dev)
+    nc3 = NewtonConfig(abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-6, fd_eps=1e-7)
+    op3.stdg_step(0.0, c3.dt, u, nc3)  # warm
+    its = []
+
+    def ten():
+        uu = u
+        for k in range(10):
+            _, uu, inf = op3.stdg_step(k * c3.dt, c3.dt, uu, nc3)
+            its.append([inf.newton_iterations, inf.linear_iterations])
+        return uu
+    t3, _ = _wall(torch, ten)
+    out["c3_10_slabs"] = {"seconds": t3, "per_slab_s": t3 / 10, "newton_gmres": its}
+    # CPU reference (oracle) solves beside them
+    if not args.no_cpu:
+        try:
+            import oracle as O
+            thr = O.max_threads()
+            O.set_threads(thr)
+            pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
+                           list(cfg.velocity), n_tau=cfg.n_tau)
+            t0 = time.perf_counter()
+            _, _, nit, lin = pr.stdg_step(0.0, cfg.dt, C.initial_state(cfg), linear=O.GMRES,
+                                          abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10)
+            out["cpu_c4_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": thr,
+                                        "gmres_iterations": lin, "kind": "port (MGS GMRES)"}
+            O.set_threads(1)
+            p1 = O.Problem(1, 3, [64], [0.0], [1.0], [1.0], n_tau=4)
+            t0 = time.perf_counter()
+            _, _, _, lin1 = p1.stdg_step(0.0, c1.dt, C.initial_state(c1), linear=O.GMRES,
+                                         abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12)
+            out["cpu_c1_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": 1,
+                                        "gmres_iterations": lin1}
+        except Exception as e:
+            out["cpu_solves"] = f"unavailable: {e}"
     return out
 
 

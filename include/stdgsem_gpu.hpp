@@ -1,0 +1,379 @@
+// stdgsem_gpu.hpp -- C++ host mirror of the reference stdgsem slab interface,
+// backed by the CUDA library through the C ABI (stg_cuda.h).
+//
+// Header-only; link against libstg_cuda.so.  Same free-function names,
+// argument meaning and exception types as the reference headers:
+//   st_residual   stdg.hpp:56-76        st_jacobian  stdg.hpp:79-110 (matrix-free)
+//   stdg_step     stdg.hpp:120-143      stdg_integrate stdg.hpp:152-173
+//   rk_step       lodg.hpp:89-149       integrate    lodg.hpp:158-181
+//   NewtonConfig  newton.hpp:30-38      NonconvergenceError newton.hpp:40-48
+// Vectors are std::vector<double> on the host (the reference's Eigen::VectorXd
+// role); each call moves them to the device once, runs there, and copies the
+// result back.  For device-resident loops use the DeviceVec overloads.
+// Status codes map back to std::invalid_argument / std::runtime_error /
+// NonconvergenceError; CUDA failures throw CudaError (there is no CPU path).
+#pragma once
+
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "stg_cuda.h"
+
+namespace stdgsem {
+namespace gpu {
+
+using Vec = std::vector<double>;
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+struct NonconvergenceError : std::runtime_error {
+  Vec last_iterate;
+  std::vector<double> residual_history;
+  NonconvergenceError(const std::string& what, std::vector<double> history)
+      : std::runtime_error(what), residual_history(std::move(history)) {}
+};
+
+inline void check(int code, const stg_handle* h) {
+  if (code == STG_OK) return;
+  const std::string msg = stg_last_error(h);
+  switch (code) {
+    case STG_ERR_INVALID: throw std::invalid_argument(msg);
+    case STG_ERR_NONCONVERGENCE: throw NonconvergenceError(msg, {});
+    case STG_ERR_CUDA: throw CudaError(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+
+// RAII device vector.
+class DeviceVec {
+ public:
+  DeviceVec() = default;
+  explicit DeviceVec(size_t n) : n_(n) { check(stg_device_alloc((long long)n, &p_), nullptr); }
+  explicit DeviceVec(const Vec& v) : DeviceVec(v.size()) { upload(v); }
+  DeviceVec(DeviceVec&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+  DeviceVec& operator=(DeviceVec&& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    return *this;
+  }
+  DeviceVec(const DeviceVec&) = delete;
+  DeviceVec& operator=(const DeviceVec&) = delete;
+  ~DeviceVec() {
+    if (p_) stg_device_free(p_);
+  }
+  void upload(const Vec& v) {
+    if (v.size() != n_) throw std::invalid_argument("DeviceVec::upload: size mismatch");
+    check(stg_memcpy(p_, v.data(), (long long)n_, 0), nullptr);
+  }
+  Vec download() const {
+    Vec v(n_);
+    check(stg_memcpy(v.data(), p_, (long long)n_, 1), nullptr);
+    return v;
+  }
+  double* data() { return p_; }
+  const double* data() const { return p_; }
+  size_t size() const { return n_; }
+
+ private:
+  double* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+// ---- discretisation data (mesh.hpp, models.hpp) ------------------------------
+struct Mesh {  // mesh.hpp:14-35; d = 3 is an extension of the reference
+  int d = 1;
+  std::vector<double> lower, upper;
+  std::vector<int> cells;
+};
+
+inline Mesh uniform_mesh(int d, const std::vector<double>& lower,
+                         const std::vector<double>& upper, const std::vector<int>& cells) {
+  if (d < 1 || d > 3) throw std::invalid_argument("uniform_mesh: d in {1,2,3}");
+  if (int(lower.size()) != d || int(upper.size()) != d || int(cells.size()) != d)
+    throw std::invalid_argument("uniform_mesh: inconsistent sizes");
+  return Mesh{d, lower, upper, cells};
+}
+
+struct DgSpace {  // mesh.hpp:59-91 (r = 1)
+  Mesh mesh;
+  int p = 1;
+  int dof() const {
+    int npc = 1, nc = 1;
+    for (int a = 0; a < mesh.d; ++a) {
+      npc *= p + 1;
+      nc *= mesh.cells[size_t(a)];
+    }
+    return npc * nc;
+  }
+};
+inline DgSpace dg_space(const Mesh& m, int p) { return DgSpace{m, p}; }
+
+struct FluxModel {  // models.hpp:23-36, constant-velocity advection or Burgers
+  int kind = STG_MODEL_ADVECTION;
+  std::vector<double> b;
+};
+inline FluxModel advection_model(const std::vector<double>& b) {
+  return FluxModel{STG_MODEL_ADVECTION, b};
+}
+inline FluxModel burgers_model() { return FluxModel{STG_MODEL_BURGERS, {0.0}}; }
+
+enum class LinearMethod { auto_select = STG_LINEAR_AUTO, gmres = STG_LINEAR_GMRES };
+enum class JacobianForm { a_form = STG_FORM_A, a_inv_form = STG_FORM_A_INV };
+
+struct NewtonConfig {  // newton.hpp:30-38
+  double abs_tol = 1e-12;
+  double rel_tol = 1e-12;
+  int max_iter = 50;
+  LinearMethod linear = LinearMethod::auto_select;
+  int gmres_restart = 30;
+  double gmres_tol = 1e-12;
+  int gmres_max_it = 1000;
+  double fd_eps = 0.0;
+  stg_newton_config c() const {
+    return stg_newton_config{abs_tol, rel_tol, max_iter, int(linear), gmres_restart, gmres_tol,
+                             gmres_max_it, fd_eps};
+  }
+};
+
+// The slab operator for one (space, model, n_tau): owns a C-ABI handle.
+class SlabOperator {
+ public:
+  SlabOperator(const DgSpace& space, const FluxModel& model, int n_tau) {
+    stg_desc d{};
+    d.dim = space.mesh.d;
+    d.degree = space.p;
+    d.n_tau = n_tau;
+    d.model = model.kind;
+    for (int a = 0; a < 3; ++a) {
+      d.cells[a] = a < d.dim ? space.mesh.cells[size_t(a)] : 1;
+      d.lower[a] = a < d.dim ? space.mesh.lower[size_t(a)] : 0.0;
+      d.upper[a] = a < d.dim ? space.mesh.upper[size_t(a)] : 1.0;
+      d.velocity[a] = a < int(model.b.size()) ? model.b[size_t(a)] : 0.0;
+    }
+    stg_handle* h = nullptr;
+    check(stg_create(&d, &h), nullptr);
+    h_.reset(h);
+    long long ns = 0, nd = 0;
+    stg_sizes(h, &ns, &nd);
+    n_sdof_ = size_t(ns);
+    n_dof_ = size_t(nd);
+  }
+  stg_handle* handle() const { return h_.get(); }
+  size_t n_sdof() const { return n_sdof_; }
+  size_t n_dof() const { return n_dof_; }
+
+ private:
+  struct Del {
+    void operator()(stg_handle* h) const { stg_destroy(h); }
+  };
+  std::unique_ptr<stg_handle, Del> h_;
+  size_t n_sdof_ = 0, n_dof_ = 0;
+};
+
+// SemiDiscreteSystem (system.hpp:16-23): the seam.  Lazily creates one slab
+// operator per number of temporal nodes.
+class SemiDiscreteSystem {
+ public:
+  SemiDiscreteSystem(DgSpace space, FluxModel model)
+      : space_(std::move(space)), model_(std::move(model)) {}
+  int dof() const { return space_.dof(); }
+  SlabOperator& op(int n_tau) const {
+    for (auto& e : ops_)
+      if (e.first == n_tau) return *e.second;
+    ops_.emplace_back(n_tau, std::make_shared<SlabOperator>(space_, model_, n_tau));
+    return *ops_.back().second;
+  }
+  // rhs(t, u) = F(u) (spatial.hpp:107-266)
+  Vec rhs(double t, const Vec& u) const {
+    SlabOperator& o = op(2);
+    DeviceVec du(u), F(o.n_sdof());
+    check(stg_spatial_rhs(o.handle(), t, du.data(), F.data()), o.handle());
+    return F.download();
+  }
+
+ private:
+  DgSpace space_;
+  FluxModel model_;
+  mutable std::vector<std::pair<int, std::shared_ptr<SlabOperator>>> ops_;
+};
+
+inline SemiDiscreteSystem assemble_semidiscrete(const DgSpace& space, const FluxModel& model) {
+  if (model.kind == STG_MODEL_ADVECTION && int(model.b.size()) != space.mesh.d)
+    throw std::invalid_argument("assemble_semidiscrete: dimension mismatch");
+  return SemiDiscreteSystem(space, model);
+}
+
+struct SbpOperators {  // operators.hpp:16-22 (the library builds D, M itself)
+  int n = 0;
+};
+inline SbpOperators sbp_operators(int n) {
+  if (n < 2) throw std::invalid_argument("sbp_operators: need n >= 2");
+  return SbpOperators{n};
+}
+struct ButcherTableau {  // operators.hpp:24-30
+  int s = 0;
+};
+inline ButcherTableau lobatto_tableau(int s) {
+  if (s < 2 || s > 4)
+    throw std::invalid_argument("lobatto_tableau: closed forms stored for s in {2,3,4}");
+  return ButcherTableau{s};
+}
+
+struct TimeElementSystem {  // stdg.hpp:21-29
+  SemiDiscreteSystem system;
+  SbpOperators ops;
+  double t_n = 0.0;
+  double dt = 0.0;
+  Vec u_n;
+  int n_tau() const { return ops.n; }
+};
+
+// st_residual (stdg.hpp:56-76)
+inline Vec st_residual(const TimeElementSystem& sys, const Vec& U) {
+  SlabOperator& o = sys.system.op(sys.ops.n);
+  if (U.size() != o.n_dof())
+    throw std::invalid_argument("st_residual: expected " + std::to_string(o.n_dof()) +
+                                " unknowns");
+  Vec R(o.n_dof());
+  check(stg_st_residual_host(o.handle(), sys.t_n, sys.dt, sys.u_n.data(), U.data(), R.data()),
+        o.handle());
+  return R;
+}
+
+// st_jacobian (stdg.hpp:79-110) as a matrix-free action J(U) v.
+inline Vec st_jacobian_apply(const TimeElementSystem& sys, const Vec& U, const Vec& v,
+                             double fd_eps = 0.0) {
+  SlabOperator& o = sys.system.op(sys.ops.n);
+  if (U.size() != o.n_dof() || v.size() != o.n_dof())
+    throw std::invalid_argument("st_jacobian: expected " + std::to_string(o.n_dof()) +
+                                " unknowns");
+  DeviceVec dU(U), dv(v), Jv(o.n_dof());
+  check(stg_st_jvp(o.handle(), sys.t_n, sys.dt, dU.data(), dv.data(), Jv.data(), fd_eps),
+        o.handle());
+  return Jv.download();
+}
+
+struct StdgStepResult {  // stdg.hpp:112-116
+  Vec U;
+  Vec u_next;
+  int newton_iterations = 0;
+  int linear_iterations = 0;
+};
+
+// stdg_step (stdg.hpp:120-143)
+inline StdgStepResult stdg_step(const SemiDiscreteSystem& system, const SbpOperators& ops,
+                                double t_n, const Vec& u_n, double dt,
+                                const NewtonConfig& cfg = {}) {
+  SlabOperator& o = system.op(ops.n);
+  if (u_n.size() != o.n_sdof()) throw std::invalid_argument("stdg_step: u_n size mismatch");
+  StdgStepResult r;
+  r.U.resize(o.n_dof());
+  r.u_next.resize(o.n_sdof());
+  stg_solve_info info{};
+  const stg_newton_config c = cfg.c();
+  const int code = stg_stdg_step_host(o.handle(), t_n, dt, u_n.data(), &c, r.U.data(),
+                                      r.u_next.data(), &info);
+  if (code == STG_ERR_NONCONVERGENCE)
+    throw NonconvergenceError(stg_last_error(o.handle()),
+                              std::vector<double>(info.residual_history,
+                                                  info.residual_history + info.n_history));
+  check(code, o.handle());
+  r.newton_iterations = info.newton_iterations;
+  r.linear_iterations = info.linear_iterations;
+  return r;
+}
+
+struct StdgTrajectory {  // stdg.hpp:145-150
+  Vec times;
+  std::vector<Vec> states;
+  std::vector<Vec> element_solutions;
+  int total_newton_iterations = 0;
+};
+
+// stdg_integrate (stdg.hpp:152-173)
+inline StdgTrajectory stdg_integrate(const SemiDiscreteSystem& system, const SbpOperators& ops,
+                                     double t0, const Vec& u0, double t_end, int n_steps,
+                                     const NewtonConfig& cfg = {}) {
+  if (n_steps < 1) throw std::invalid_argument("stdg_integrate: n_steps >= 1 required");
+  StdgTrajectory traj;
+  traj.times.resize(size_t(n_steps) + 1);
+  for (int k = 0; k <= n_steps; ++k) traj.times[size_t(k)] = t0 + (t_end - t0) * k / n_steps;
+  traj.states.push_back(u0);
+  const double dt = (t_end - t0) / n_steps;
+  for (int k = 0; k < n_steps; ++k) {
+    StdgStepResult st = stdg_step(system, ops, traj.times[size_t(k)], traj.states.back(), dt, cfg);
+    traj.states.push_back(std::move(st.u_next));
+    traj.element_solutions.push_back(std::move(st.U));
+    traj.total_newton_iterations += st.newton_iterations;
+  }
+  return traj;
+}
+
+struct RkStepResult {  // lodg.hpp:33-38
+  Vec u_next;
+  std::vector<Vec> stages;
+  int newton_iterations = 0;
+  double t_next = 0.0;
+};
+
+// rk_step (lodg.hpp:89-149)
+inline RkStepResult rk_step(const SemiDiscreteSystem& system, const ButcherTableau& tab, double t,
+                            const Vec& u, double dt, const NewtonConfig& cfg = {},
+                            JacobianForm jac_form = JacobianForm::a_form) {
+  SlabOperator& o = system.op(tab.s);
+  if (u.size() != o.n_sdof()) throw std::invalid_argument("rk_step: u size mismatch");
+  Vec U(o.n_dof());
+  RkStepResult r;
+  r.u_next.resize(o.n_sdof());
+  stg_solve_info info{};
+  const stg_newton_config c = cfg.c();
+  const int code = stg_rk_step_host(o.handle(), int(jac_form), t, dt, u.data(), &c, U.data(),
+                                    r.u_next.data(), &info);
+  if (code == STG_ERR_NONCONVERGENCE)
+    throw NonconvergenceError(stg_last_error(o.handle()),
+                              std::vector<double>(info.residual_history,
+                                                  info.residual_history + info.n_history));
+  check(code, o.handle());
+  const size_t ns = o.n_sdof();
+  for (int j = 0; j < tab.s; ++j)
+    r.stages.emplace_back(U.begin() + long(j * ns), U.begin() + long((j + 1) * ns));
+  r.newton_iterations = info.newton_iterations;
+  r.t_next = t + dt;
+  return r;
+}
+
+struct RkTrajectory {  // lodg.hpp:151-156
+  Vec times;
+  std::vector<Vec> states;
+  std::vector<std::vector<Vec>> stage_solutions;
+  int total_newton_iterations = 0;
+};
+
+// integrate (lodg.hpp:158-181)
+inline RkTrajectory integrate(const SemiDiscreteSystem& system, const ButcherTableau& tab,
+                              double t0, const Vec& u0, double t_end, int n_steps,
+                              const NewtonConfig& cfg = {},
+                              JacobianForm jac_form = JacobianForm::a_form) {
+  if (n_steps < 1) throw std::invalid_argument("integrate: n_steps >= 1 required");
+  RkTrajectory traj;
+  traj.times.resize(size_t(n_steps) + 1);
+  for (int k = 0; k <= n_steps; ++k) traj.times[size_t(k)] = t0 + (t_end - t0) * k / n_steps;
+  traj.states.push_back(u0);
+  const double dt = (t_end - t0) / n_steps;
+  for (int k = 0; k < n_steps; ++k) {
+    RkStepResult st =
+        rk_step(system, tab, traj.times[size_t(k)], traj.states.back(), dt, cfg, jac_form);
+    traj.states.push_back(std::move(st.u_next));
+    traj.stage_solutions.push_back(std::move(st.stages));
+    traj.total_newton_iterations += st.newton_iterations;
+  }
+  return traj;
+}
+
+}  // namespace gpu
+}  // namespace stdgsem

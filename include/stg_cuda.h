@@ -145,7 +145,8 @@ int stg_st_residual(stg_handle* h, double t_n, double dt, const double* u_n,
                     const double* U, double* R);
 
 /* st_jacobian (stdg.hpp:79-110) applied matrix-free: Jv = dR/dU(U) v.
- * fd_eps > 0 (nonlinear models): forward difference [R(U+eps v)-R(U)]/eps. */
+ * fd_eps > 0 (nonlinear models): forward difference [R(U+h v)-R(U)]/h with
+ * h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (Walker-Pernice parameter). */
 int stg_st_jvp(stg_handle* h, double t_n, double dt, const double* U, const double* v,
                double* Jv, double fd_eps);
 
@@ -188,6 +189,13 @@ int stg_stdg_step_host(stg_handle* h, double t_n, double dt, const double* u_n,
 int stg_rk_step_host(stg_handle* h, int form, double t, double dt, const double* u,
                      const stg_newton_config* cfg, double* U, double* u_next,
                      stg_solve_info* info);
+
+/* ---- device memory helpers (so FFI callers need no CUDA runtime of their own) */
+int stg_device_alloc(long long n_doubles, double** out);
+int stg_device_free(double* p);
+/* dir: 0 = host -> device, 1 = device -> host, 2 = device -> device */
+int stg_memcpy(double* dst, const double* src, long long n_doubles, int dir);
+int stg_device_synchronize(void);
 
 /* ---- host-only constants (no device needed) -------------------------------- */
 /* lgl_rule (quadrature.hpp:66-105): n nodes and weights. */

@@ -715,12 +715,19 @@ inline System advection_system(const Advection& op) {
   sys.linear = true;
   auto opp = std::make_shared<Advection>(op);
   sys.rhs = [opp](double, const double* u, double* F) { advection_rhs(*opp, u, F); };
-  sys.jac = [opp](double, const double*, const double* v, double* Jv) {
+  // The zero-state probe rhs(0) is computed once and cached, as the
+  // reference caches the Jacobian of linear models (spatial.hpp:375-383).
+  auto base = std::make_shared<Vec>();
+  sys.jac = [opp, base](double, const double*, const double* v, double* Jv) {
     const int64_t n = opp->s.dof();
-    Vec zero(size_t(n), 0.0), base(static_cast<size_t>(n));
-    advection_rhs(*opp, zero.data(), base.data());
+    if (base->empty()) {
+      Vec zero(static_cast<size_t>(n), 0.0);
+      base->resize(static_cast<size_t>(n));
+      advection_rhs(*opp, zero.data(), base->data());
+    }
     advection_rhs(*opp, v, Jv);
-    for (int64_t i = 0; i < n; ++i) Jv[i] -= base[size_t(i)];
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) Jv[i] -= (*base)[size_t(i)];
   };
   return sys;
 }
@@ -915,6 +922,7 @@ struct GmresStats {
 
 inline double dot(const double* a, const double* b, int64_t n) {
   double s = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : s)
   for (int64_t i = 0; i < n; ++i) s += a[i] * b[i];
   return s;
 }
@@ -957,12 +965,19 @@ inline GmresStats gmres(const LinOp& A, const double* b, double* x, int64_t n,
       for (int j = 0; j <= k; ++j) {
         const double hjk = dot(w.data(), V[j].data(), n);
         H(j, k) = hjk;
-        for (int64_t i = 0; i < n; ++i) w[size_t(i)] -= hjk * V[j][size_t(i)];
+        double* wp = w.data();
+        const double* vp = V[j].data();
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) wp[i] -= hjk * vp[i];
       }
       const double hn = std::sqrt(dot(w.data(), w.data(), n));
       H(k + 1, k) = hn;
-      if (hn != 0.0)
-        for (int64_t i = 0; i < n; ++i) V[k + 1][size_t(i)] = w[size_t(i)] / hn;
+      if (hn != 0.0) {
+        double* vp = V[k + 1].data();
+        const double* wp = w.data();
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < n; ++i) vp[i] = wp[i] / hn;
+      }
       for (int j = 0; j < k; ++j) {
         const double t0 = cs[j] * H(j, k) + sn[j] * H(j + 1, k);
         H(j + 1, k) = -sn[j] * H(j, k) + cs[j] * H(j + 1, k);
@@ -987,8 +1002,12 @@ inline GmresStats gmres(const LinOp& A, const double* b, double* x, int64_t n,
       for (int j = i + 1; j < k; ++j) s -= H(i, j) * y[size_t(j)];
       y[size_t(i)] = s / H(i, i);
     }
-    for (int j = 0; j < k; ++j)
-      for (int64_t i = 0; i < n; ++i) x[i] += y[size_t(j)] * V[j][size_t(i)];
+    for (int j = 0; j < k; ++j) {
+      const double yj = y[size_t(j)];
+      const double* vp = V[j].data();
+#pragma omp parallel for schedule(static)
+      for (int64_t i = 0; i < n; ++i) x[i] += yj * vp[i];
+    }
   }
   st.iterations = total;
   return st;

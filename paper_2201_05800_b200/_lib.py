@@ -26,6 +26,7 @@ EXPORTS = (
     "stg_stage_residual", "stg_stage_jvp", "stg_gmres_st", "stg_stdg_step", "stg_rk_step",
     "stg_st_residual_host", "stg_stdg_step_host", "stg_rk_step_host", "stg_kernel_launches",
     "stg_lgl_rule", "stg_diff_matrix", "stg_lobatto_tableau",
+    "stg_device_alloc", "stg_device_free", "stg_memcpy", "stg_device_synchronize",
 )
 
 
@@ -100,5 +101,8 @@ def load() -> ctypes.CDLL:
     L.stg_lgl_rule.argtypes = [_i, _vp, _vp]
     L.stg_diff_matrix.argtypes = [_i, _vp]
     L.stg_lobatto_tableau.argtypes = [_i, _vp, _vp, _vp]
+    L.stg_device_alloc.argtypes = [ctypes.c_longlong, ctypes.POINTER(_vp)]
+    L.stg_device_free.argtypes = [_vp]
+    L.stg_memcpy.argtypes = [_vp, _vp, ctypes.c_longlong, _i]
     _LIB = L
     return L

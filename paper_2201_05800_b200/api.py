@@ -235,7 +235,8 @@ class SlabOperator:
         code = fn(self._h, *head, _ptr(u, self.n_sdof, what), ctypes.byref(c),
                   _ptr(U, self.n_dof, "U"), _ptr(u_next, self.n_sdof, "u_next"), ctypes.byref(info))
         if code == L.STG_ERR_NONCONVERGENCE:
-            raise NonconvergenceError(self._lib.stg_last_error(self._h).decode())
+            raise NonconvergenceError(self._lib.stg_last_error(self._h).decode(),
+                                      _info(info).residual_history)
         _raise(self._h, code, self._lib)
         return U, u_next, _info(info)
 
@@ -271,7 +272,8 @@ class SlabOperator:
                                             ctypes.byref(c), U.ctypes.data, un1.ctypes.data,
                                             ctypes.byref(info))
         if code == L.STG_ERR_NONCONVERGENCE:
-            raise NonconvergenceError(self._lib.stg_last_error(self._h).decode())
+            raise NonconvergenceError(self._lib.stg_last_error(self._h).decode(),
+                                      _info(info).residual_history)
         _raise(self._h, code, self._lib)
         return U, un1, _info(info)
 

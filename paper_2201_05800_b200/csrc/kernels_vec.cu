@@ -81,15 +81,19 @@ __global__ void k_scale_invsqrt(double* y, const double* x, const double* nrm2, 
 }
 
 // ---- multi-vector kernels: block = 8 warps x 32 lanes.  Warp g owns basis
-// vectors j = g, g+8, g+16, ... (MPW of them); lane l owns element i = base+l.
+// vectors j = g, g+8, g+16, ... (MPW of them); per iteration the block covers
+// kU = 8 slots of 32 consecutive elements (lane l of slot u owns element
+// base + 32u + l), so every thread keeps MPW*kU independent loads in flight.
 // Every V_j entry is loaded once per pass and kept in a register for the
-// second half of a fused pass; cross-warp sums go through shared memory in a
-// fixed order.
+// second half of a fused pass; the cross-warp sum of slot u is done by warp u
+// (balanced), in a fixed order.
 constexpr int kWarps = 8;
 constexpr int kMultiBlock = 32 * kWarps;
+constexpr int kU = 8;
+constexpr int kTile = 32 * kU;
 
 int multi_grid(long long n) {
-  long long g = (n + 31) / 32;
+  long long g = (n + kTile - 1) / kTile;
   if (g < 1) g = 1;
   if (g > 148 * 4) g = 148 * 4;
   return int(g);
@@ -105,12 +109,25 @@ __global__ void __launch_bounds__(kMultiBlock) k_multidot(const double* __restri
   double acc[MPW];
 #pragma unroll
   for (int m = 0; m < MPW; ++m) acc[m] = 0.0;
-  for (long long i = (long long)blockIdx.x * 32 + lane; i < n; i += (long long)gridDim.x * 32) {
-    const double wi = w[i];
+  for (long long base = (long long)blockIdx.x * kTile; base < n;
+       base += (long long)gridDim.x * kTile) {
+    double wv[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const long long i = base + 32 * u + lane;
+      wv[u] = i < n ? w[i] : 0.0;
+    }
 #pragma unroll
     for (int m = 0; m < MPW; ++m) {
       const int j = g + kWarps * m;
-      if (j < k) acc[m] = fma(V[j * ldv + i], wi, acc[m]);
+      if (j < k) {
+        const double* Vj = V + j * ldv;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const long long i = base + 32 * u + lane;
+          if (i < n) acc[m] = fma(Vj[i], wv[u], acc[m]);
+        }
+      }
     }
   }
 #pragma unroll
@@ -121,9 +138,8 @@ __global__ void __launch_bounds__(kMultiBlock) k_multidot(const double* __restri
   }
 }
 
-// w -= sum_j h_j V_j; optionally dots <V_j, w_new>; always <w_new, w_new>.
-// part[b*(k+1) + j], j < k dots (0 if !dots), j = k norm^2.
-// If combine_only, w is x and the update is x += sum_j h_j V_j (no dots/norm).
+// w += sign * sum_j h_j V_j; optionally dots <V_j, w_new>; always <w_new, w_new>.
+// part[b*(k+1) + j], j < k dots (0 if !dots), j = k norm^2 (part may be null).
 template <int MPW>
 __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
                                                         const double* __restrict__ V,
@@ -131,8 +147,8 @@ __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
                                                         const double* __restrict__ h,
                                                         long long n, int dots, double sign,
                                                         double* part) {
-  __shared__ double red[kWarps][32];
-  __shared__ double wnew[32];
+  __shared__ double red[kWarps][kU][32];
+  __shared__ double wnew[kU][32];
   __shared__ double hs[kWarps * MPW];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   for (int j = threadIdx.x; j < kWarps * MPW; j += blockDim.x) hs[j] = j < k ? h[j] : 0.0;
@@ -141,48 +157,67 @@ __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
 #pragma unroll
   for (int m = 0; m < MPW; ++m) acc[m] = 0.0;
   double nrm = 0.0;
-  for (long long base = (long long)blockIdx.x * 32; base < n; base += (long long)gridDim.x * 32) {
-    const long long i = base + lane;
-    const bool in = i < n;
-    double v[MPW];
-    double p = 0.0;
+  for (long long base = (long long)blockIdx.x * kTile; base < n;
+       base += (long long)gridDim.x * kTile) {
+    double v[MPW][kU];
+    double p[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) p[u] = 0.0;
 #pragma unroll
     for (int m = 0; m < MPW; ++m) {
       const int j = g + kWarps * m;
-      v[m] = (in && j < k) ? V[j * ldv + i] : 0.0;
-      p = fma(hs[j], v[m], p);
+      const double hj = hs[j];
+      const double* Vj = V + j * ldv;
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const long long i = base + 32 * u + lane;
+        v[m][u] = (j < k && i < n) ? Vj[i] : 0.0;
+        p[u] = fma(hj, v[m][u], p[u]);
+      }
     }
-    red[g][lane] = p;
+#pragma unroll
+    for (int u = 0; u < kU; ++u) red[g][u][lane] = p[u];
     __syncthreads();
-    if (g == 0) {
+    {
+      // warp g finishes slot u = g
+      const long long i = base + 32 * g + lane;
       double s = 0.0;
 #pragma unroll
-      for (int q = 0; q < kWarps; ++q) s += red[q][lane];
+      for (int q = 0; q < kWarps; ++q) s += red[q][g][lane];
       double wi = 0.0;
-      if (in) {
+      if (i < n) {
         wi = fma(sign, s, w[i]);
         w[i] = wi;
       }
-      wnew[lane] = wi;
+      wnew[g][lane] = wi;
       nrm = fma(wi, wi, nrm);
     }
     __syncthreads();
     if (dots) {
-      const double wi = wnew[lane];
 #pragma unroll
-      for (int m = 0; m < MPW; ++m) acc[m] = fma(v[m], wi, acc[m]);
+      for (int u = 0; u < kU; ++u) {
+        const double wi = wnew[u][lane];
+#pragma unroll
+        for (int m = 0; m < MPW; ++m) acc[m] = fma(v[m][u], wi, acc[m]);
+      }
     }
   }
   if (part == nullptr) return;
+  __shared__ double nr[kWarps];
 #pragma unroll
   for (int m = 0; m < MPW; ++m) {
     const int j = g + kWarps * m;
     const double s = warp_sum(acc[m]);
     if (lane == 0 && j < k) part[(size_t)blockIdx.x * (k + 1) + j] = dots ? s : 0.0;
   }
-  if (g == 0) {
-    const double s = warp_sum(nrm);
-    if (lane == 0) part[(size_t)blockIdx.x * (k + 1) + k] = s;
+  const double sn = warp_sum(nrm);
+  if (lane == 0) nr[g] = sn;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) t += nr[q];
+    part[(size_t)blockIdx.x * (k + 1) + k] = t;
   }
 }
 

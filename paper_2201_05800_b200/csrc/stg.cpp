@@ -440,6 +440,33 @@ void st_residual(stg_handle* h, double dt, const double* un, const double* U, do
   apply(h, st_mix(h, dt, un != nullptr), h->nt, h->nt, U, nullptr, un, R, false, false);
 }
 
+// Forward-difference Jacobian action [R(U + h v) - R(U)] / h of the slab /
+// stage residual without its constant (u_n / u) coupling, which cancels.
+// h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (the Walker-Pernice differencing
+// parameter, as in PETSc's MFFD "wp"), so the perturbation is relative to the
+// state regardless of the scaling of the Krylov vector v.
+void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, const double* v,
+            double* Jv, double fd_eps) {
+  const long long n = h->n_dof;
+  const double vn = std::sqrt(dev_dot(h, v, v, n));
+  if (vn == 0.0) {
+    stg::vec_fill(Jv, 0.0, n, h->stream);
+    h->launches++;
+    return;
+  }
+  const double un = std::sqrt(dev_dot(h, U, U, n));
+  const double eps = fd_eps * std::sqrt(1.0 + un) / vn;
+  h->tmp1.ensure(size_t(n));
+  h->tmp2.ensure(size_t(n));
+  stg::vec_copy(h->tmp1.p, U, n, h->stream);
+  stg::vec_axpy(h->tmp1.p, eps, v, n, h->stream);
+  h->launches += 2;
+  apply(h, mix, h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false, full);
+  apply(h, mix, h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false, full);
+  stg::vec_axpby(Jv, -1.0 / eps, h->tmp2.p, 1.0 / eps, n, h->stream);
+  h->launches++;
+}
+
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
             double fd_eps) {
   if (h->desc.model == STG_MODEL_ADVECTION) {
@@ -448,16 +475,7 @@ void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* 
   } else if (fd_eps <= 0.0) {
     apply(h, st_mix(h, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, false);
   } else {
-    // [R(U + eps v) - R(U)] / eps (u_n terms cancel and are omitted)
-    h->tmp1.ensure(size_t(h->n_dof));
-    h->tmp2.ensure(size_t(h->n_dof));
-    stg::vec_copy(h->tmp1.p, U, h->n_dof, h->stream);
-    stg::vec_axpy(h->tmp1.p, fd_eps, v, h->n_dof, h->stream);
-    h->launches += 2;
-    apply(h, st_mix(h, dt, false), h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false, false);
-    apply(h, st_mix(h, dt, false), h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false, false);
-    stg::vec_axpby(Jv, -1.0 / fd_eps, h->tmp2.p, 1.0 / fd_eps, h->n_dof, h->stream);
-    h->launches++;
+    fd_jvp(h, st_mix(h, dt, false), false, U, v, Jv, fd_eps);
   }
 }
 
@@ -475,17 +493,7 @@ void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double
   } else if (fd_eps <= 0.0) {
     apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, full);
   } else {
-    h->tmp1.ensure(size_t(h->n_dof));
-    h->tmp2.ensure(size_t(h->n_dof));
-    stg::vec_copy(h->tmp1.p, U, h->n_dof, h->stream);
-    stg::vec_axpy(h->tmp1.p, fd_eps, v, h->n_dof, h->stream);
-    h->launches += 2;
-    apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false,
-          full);
-    apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false,
-          full);
-    stg::vec_axpby(Jv, -1.0 / fd_eps, h->tmp2.p, 1.0 / fd_eps, h->n_dof, h->stream);
-    h->launches++;
+    fd_jvp(h, stage_mix(h, form, dt, false), full, U, v, Jv, fd_eps);
   }
 }
 
@@ -518,6 +526,9 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
         },
         U, n, cfg);
   } catch (const NonconvergenceError& e) {
+    NewtonOut partial;
+    partial.history = e.history;  // residual history travels back (newton.hpp:40-48)
+    fill_info(info, partial);
     throw NonconvergenceError("stdg_step element at t=" + fmt_short(t_n) + ", dt=" + fmt_short(dt) +
                                   ": " + e.what(),
                               e.history);
@@ -549,6 +560,9 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
         },
         U, n, cfg);
   } catch (const NonconvergenceError& e) {
+    NewtonOut partial;
+    partial.history = e.history;
+    fill_info(info, partial);
     throw NonconvergenceError("rk_step at t=" + fmt_short(t) + ", dt=" + fmt_short(dt) + ": " +
                                   e.what(),
                               e.history);
@@ -659,6 +673,38 @@ int stg_constants(const stg_handle* h, double* nodes, double* weights, double* d
 }
 
 long long stg_kernel_launches(const stg_handle* h) { return h ? h->launches : 0; }
+
+int stg_device_alloc(long long n, double** out) {
+  return guarded(nullptr, [&] {
+    need(out, "stg_device_alloc");
+    if (n < 0) throw std::invalid_argument("stg_device_alloc: n >= 0");
+    *out = nullptr;
+    if (n > 0) ck(cudaMalloc(out, size_t(n) * sizeof(double)), "cudaMalloc");
+  });
+}
+
+int stg_device_free(double* p) {
+  return guarded(nullptr, [&] {
+    if (p) ck(cudaFree(p), "cudaFree");
+  });
+}
+
+int stg_memcpy(double* dst, const double* src, long long n, int dir) {
+  return guarded(nullptr, [&] {
+    if (n < 0 || dir < 0 || dir > 2) throw std::invalid_argument("stg_memcpy: bad arguments");
+    if (n == 0) return;
+    need(dst, "dst");
+    need(src, "src");
+    const cudaMemcpyKind k = dir == 0   ? cudaMemcpyHostToDevice
+                             : dir == 1 ? cudaMemcpyDeviceToHost
+                                        : cudaMemcpyDeviceToDevice;
+    ck(cudaMemcpy(dst, src, size_t(n) * sizeof(double), k), "cudaMemcpy");
+  });
+}
+
+int stg_device_synchronize(void) {
+  return guarded(nullptr, [&] { ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize"); });
+}
 
 int stg_lgl_rule(int n, double* nodes, double* weights) {
   return guarded(nullptr, [&] {

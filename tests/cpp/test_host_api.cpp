@@ -1,0 +1,222 @@
+// C++ tests of the reference-mirroring host API (include/stdgsem_gpu.hpp),
+// written like the reference's own doctest cases (test_stdg.cpp,
+// test_lodg.cpp) but with a tiny local CHECK harness (doctest is absent).
+// Built and run by tests/test_cpp_host_api.py on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+
+#include "stdgsem_gpu.hpp"
+
+using namespace stdgsem::gpu;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                      \
+  do {                                                                   \
+    if (cond) {                                                          \
+      ++g_pass;                                                          \
+    } else {                                                             \
+      ++g_fail;                                                          \
+      std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+    }                                                                    \
+  } while (0)
+
+static double maxabs(const Vec& a) {
+  double m = 0;
+  for (double x : a) m = std::max(m, std::abs(x));
+  return m;
+}
+static double maxdiff(const Vec& a, const Vec& b) {
+  double m = 0;
+  for (size_t i = 0; i < a.size(); ++i) m = std::max(m, std::abs(a[i] - b[i]));
+  return m;
+}
+static double norm2(const Vec& a) {
+  double s = 0;
+  for (double x : a) s += x * x;
+  return std::sqrt(s);
+}
+
+static SemiDiscreteSystem advection_1d(int cells, int p) {  // test_stdg.cpp:23-28
+  return assemble_semidiscrete(dg_space(uniform_mesh(1, {0.0}, {1.0}, {cells}), p),
+                               advection_model({1.0}));
+}
+
+// LGL nodes of the space (for interpolate_scalar, mesh.hpp:145-165)
+static Vec interp_1d(int cells, int p, double (*f)(double)) {
+  std::vector<double> x(size_t(p) + 1), w(size_t(p) + 1);
+  stg_lgl_rule(p + 1, x.data(), w.data());
+  Vec u;
+  const double h = 1.0 / cells;
+  for (int c = 0; c < cells; ++c)
+    for (int i = 0; i <= p; ++i) u.push_back(f((c + 0.5 * (1.0 + x[size_t(i)])) * h));
+  return u;
+}
+
+static void test_stdg_equals_rk() {  // test_stdg.cpp:111-135
+  auto adv = advection_1d(8, 2);
+  const Vec u0 = interp_1d(8, 2, [](double x) { return std::sin(2 * M_PI * x) + 0.3; });
+  NewtonConfig tight;
+  tight.abs_tol = 1e-14;
+  tight.rel_tol = 1e-13;
+  tight.gmres_tol = 1e-14;
+  for (int n_tau : {2, 3}) {
+    auto a = stdg_step(adv, sbp_operators(n_tau), 0.0, u0, 0.05, tight);
+    auto b = rk_step(adv, lobatto_tableau(n_tau), 0.0, u0, 0.05, tight, JacobianForm::a_inv_form);
+    Vec d(a.u_next.size());
+    for (size_t i = 0; i < d.size(); ++i) d[i] = a.u_next[i] - b.u_next[i];
+    CHECK(norm2(d) / norm2(b.u_next) <= 1e-10);
+    const size_t ns = u0.size();
+    for (int j = 0; j < n_tau; ++j) {
+      Vec aj(a.U.begin() + long(j * ns), a.U.begin() + long((j + 1) * ns));
+      CHECK(maxdiff(aj, b.stages[size_t(j)]) <= 1e-9);
+    }
+  }
+}
+
+static void test_st_residual_constant_and_dt() {  // test_stdg.cpp:53-73
+  auto adv = advection_1d(4, 1);
+  const int dof = adv.dof();
+  TimeElementSystem e0{adv, sbp_operators(3), 0.0, 0.25, Vec(size_t(dof), 2.5)};
+  CHECK(maxabs(st_residual(e0, Vec(size_t(3 * dof), 2.5))) <= 1e-12);
+  Vec U(size_t(3 * dof));
+  for (int i = 0; i < 3 * dof; ++i) U[size_t(i)] = -0.7 + 2.0 * i / (3 * dof - 1);
+  TimeElementSystem e1{adv, sbp_operators(3), 0.0, 0.1, Vec(size_t(dof), 0.0)};
+  TimeElementSystem e2{adv, sbp_operators(3), 0.0, 0.2, Vec(size_t(dof), 0.0)};
+  const double w3[3] = {1.0 / 3, 4.0 / 3, 1.0 / 3};
+  Vec R1 = st_residual(e1, U), R2 = st_residual(e2, U);
+  double worst = 0.0;
+  for (int i = 0; i < 3; ++i) {
+    Vec Ui(U.begin() + i * dof, U.begin() + (i + 1) * dof);
+    const Vec F = adv.rhs(0.0, Ui);
+    for (int k = 0; k < dof; ++k)
+      worst = std::max(worst, std::abs(R2[size_t(i * dof + k)] - R1[size_t(i * dof + k)] +
+                                       0.05 * w3[i] * F[size_t(k)]));
+  }
+  CHECK(worst <= 1e-14);
+}
+
+static void test_st_jacobian_fd() {  // test_stdg.cpp:88-109
+  auto adv = advection_1d(4, 1);
+  const int dof = adv.dof();
+  Vec un(static_cast<size_t>(dof));
+  for (int i = 0; i < dof; ++i) un[size_t(i)] = 0.1 + 0.8 * i / (dof - 1);
+  TimeElementSystem elem{adv, sbp_operators(3), 0.2, 0.13, un};
+  Vec U(size_t(3 * dof));
+  for (int i = 0; i < 3 * dof; ++i) U[size_t(i)] = std::sin(0.7 * i + 0.3);
+  std::mt19937 gen(17);
+  std::uniform_real_distribution<double> dist(-1.0, 1.0);
+  const double h = 1e-6;
+  for (int trial = 0; trial < 3; ++trial) {
+    Vec v(U.size()), Up(U), Um(U);
+    for (size_t i = 0; i < v.size(); ++i) {
+      v[i] = dist(gen);
+      Up[i] += h * v[i];
+      Um[i] -= h * v[i];
+    }
+    const Vec rp = st_residual(elem, Up), rm = st_residual(elem, Um);
+    const Vec jv = st_jacobian_apply(elem, U, v);
+    double worst = 0.0;
+    for (size_t i = 0; i < v.size(); ++i)
+      worst = std::max(worst, std::abs((rp[i] - rm[i]) / (2 * h) - jv[i]));
+    CHECK(worst <= 1e-6 * (1.0 + maxabs(jv)));
+  }
+}
+
+static void test_integrate_basics() {  // test_stdg.cpp:169-192, test_lodg.cpp:159-175
+  auto adv = advection_1d(8, 1);
+  const Vec u0 = interp_1d(8, 1, [](double x) { return std::cos(2 * M_PI * x); });
+  bool threw = false;
+  try {
+    stdg_integrate(adv, sbp_operators(2), 0.0, u0, 1.0, 0);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw);
+  auto tr = stdg_integrate(adv, sbp_operators(2), 0.0, u0, 1.0, 4);
+  CHECK(tr.times.size() == 5);
+  for (int k = 0; k <= 4; ++k) CHECK(tr.times[size_t(k)] == 0.25 * k);
+  CHECK(tr.states.size() == 5);
+  CHECK(tr.element_solutions.size() == 4);
+  auto rk = integrate(adv, lobatto_tableau(2), 0.0, u0, 1.0, 4);
+  CHECK(rk.stage_solutions.size() == 4 && rk.stage_solutions[0].size() == 2);
+}
+
+static void test_rk_stiffly_accurate_and_forms() {  // test_lodg.cpp:64-95
+  auto adv = advection_1d(16, 2);
+  const Vec u0 = interp_1d(16, 2, [](double x) { return std::sin(2 * M_PI * x); });
+  for (auto form : {JacobianForm::a_form, JacobianForm::a_inv_form}) {
+    auto st = rk_step(adv, lobatto_tableau(3), 0.0, u0, 0.01, {}, form);
+    CHECK(maxdiff(st.u_next, st.stages.back()) <= 1e-12);
+  }
+  auto adv8 = advection_1d(8, 2);
+  const Vec v0 = interp_1d(8, 2, [](double x) { return std::exp(std::sin(2 * M_PI * x)); });
+  for (int s : {2, 3}) {
+    auto a = rk_step(adv8, lobatto_tableau(s), 0.0, v0, 0.05, {}, JacobianForm::a_form);
+    auto b = rk_step(adv8, lobatto_tableau(s), 0.0, v0, 0.05, {}, JacobianForm::a_inv_form);
+    Vec d(a.u_next.size());
+    for (size_t i = 0; i < d.size(); ++i) d[i] = a.u_next[i] - b.u_next[i];
+    CHECK(norm2(d) / norm2(b.u_next) <= 1e-11);
+  }
+}
+
+static void test_linear_one_newton_iteration() {  // test_lodg.cpp:123-132
+  auto adv = advection_1d(8, 1);
+  const Vec u0 = interp_1d(8, 1, [](double x) { return std::cos(2 * M_PI * x); });
+  NewtonConfig cfg;
+  cfg.gmres_tol = 1e-14;
+  for (auto form : {JacobianForm::a_form, JacobianForm::a_inv_form})
+    CHECK(rk_step(adv, lobatto_tableau(2), 0.0, u0, 0.1, cfg, form).newton_iterations == 1);
+}
+
+static void test_nonconvergence_context() {  // test_lodg.cpp:179-194
+  auto adv = advection_1d(8, 1);
+  const Vec u0 = interp_1d(8, 1, [](double x) { return std::cos(2 * M_PI * x); });
+  NewtonConfig cfg;
+  cfg.max_iter = 0;
+  bool threw = false;
+  try {
+    rk_step(adv, lobatto_tableau(2), 0.5, u0, 0.1, cfg);
+  } catch (const NonconvergenceError& e) {
+    threw = true;
+    CHECK(std::string(e.what()).find("rk_step at t=0.5") != std::string::npos);
+    CHECK(e.residual_history.size() == 1);
+  }
+  CHECK(threw);
+  bool inv = false;
+  try {
+    uniform_mesh(4, {0, 0, 0, 0}, {1, 1, 1, 1}, {2, 2, 2, 2});
+  } catch (const std::invalid_argument&) {
+    inv = true;
+  }
+  CHECK(inv);
+  bool bad_dt = false;
+  try {
+    stdg_step(adv, sbp_operators(2), 0.0, u0, -0.1);
+  } catch (const std::invalid_argument&) {
+    bad_dt = true;
+  }
+  CHECK(bad_dt);
+}
+
+static void test_3d_free_stream() {  // EXTENSION: d = 3 (acceptance.cpp:334-343 analogue)
+  auto sys = assemble_semidiscrete(
+      dg_space(uniform_mesh(3, {0, 0, 0}, {1, 1, 1}, {8, 4, 4}), 3), advection_model({1, 1, 1}));
+  const int dof = sys.dof();
+  TimeElementSystem e{sys, sbp_operators(4), 0.0, 0.002, Vec(size_t(dof), 0.37)};
+  CHECK(maxabs(st_residual(e, Vec(size_t(4 * dof), 0.37))) <= 1e-12);
+}
+
+int main() {
+  test_stdg_equals_rk();
+  test_st_residual_constant_and_dt();
+  test_st_jacobian_fd();
+  test_integrate_basics();
+  test_rk_stiffly_accurate_and_forms();
+  test_linear_one_newton_iteration();
+  test_nonconvergence_context();
+  test_3d_free_stream();
+  std::printf("passed %d failed %d\n", g_pass, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}

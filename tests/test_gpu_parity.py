@@ -271,8 +271,9 @@ def test_nonconvergence_and_bad_input_errors():
     cfg = C.CONFIGS["c1"]
     op = SlabOperator(**cfg.kwargs())
     un = dev(C.initial_state(cfg))
-    with pytest.raises(NonconvergenceError, match="stdg_step element at t=0"):
+    with pytest.raises(NonconvergenceError, match="stdg_step element at t=0") as ei:
         op.stdg_step(0.0, cfg.dt, un, NewtonConfig(max_iter=0))
+    assert len(ei.value.residual_history) == 1  # newton.hpp:40-48 carries the history
     with pytest.raises(ValueError):
         op.stdg_step(0.0, -1.0, un)
     with pytest.raises(ValueError):
