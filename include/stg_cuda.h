@@ -60,6 +60,17 @@ extern "C" {
 #define STG_LINEAR_AUTO 0
 #define STG_LINEAR_GMRES 3
 
+/* Right preconditioner of the device GMRES.  The reference's Eigen::GMRES
+ * defaults to a diagonal preconditioner (newton.hpp:69); point Jacobi stalls
+ * on these Jacobians, so the block versions are provided:
+ *   TBLOCK  temporal-block Jacobi (n_tau x n_tau per spatial node, advection)
+ *   EBLOCK  element-block Jacobi (exact element-local block, d = 1)
+ *   AUTO    EBLOCK for d = 1, TBLOCK otherwise. */
+#define STG_PRECOND_NONE 0
+#define STG_PRECOND_TBLOCK 1
+#define STG_PRECOND_EBLOCK 2
+#define STG_PRECOND_AUTO 3
+
 /* Kernel selection (for tests / benchmarking; AUTO picks the fastest valid). */
 #define STG_KERNEL_AUTO 0
 #define STG_KERNEL_GENERIC 1
@@ -92,6 +103,7 @@ typedef struct stg_newton_config {
   double gmres_tol;   /* default 1e-12, ||r||_2 <= tol ||b||_2 */
   int gmres_max_it;   /* default 1000 */
   double fd_eps;      /* FD Jacobian-vector step (Burgers); <= 0: exact */
+  int precond;        /* STG_PRECOND_*; default AUTO */
 } stg_newton_config;
 
 #define STG_MAX_HISTORY 64
@@ -163,9 +175,9 @@ int stg_stage_jvp(stg_handle* h, int form, double t, double dt, const double* U,
 /* ---- solvers (device pointers) ------------------------------------------ */
 
 /* linear_solve GMRES branch (newton.hpp:68-77) on the slab Jacobian at U:
- * solves J(U) x = b, x holds the initial guess on entry. */
+ * solves J(U) x = b, x holds the initial guess on entry; precond = STG_PRECOND_*. */
 int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const double* b,
-                 double* x, int restart, double tol, int max_it, int* iterations,
+                 double* x, int restart, double tol, int max_it, int precond, int* iterations,
                  double* rel_residual);
 
 /* stdg_step (stdg.hpp:120-143): Newton from 1 (x) u_n; U (n_dof) receives the

@@ -16,6 +16,7 @@ STG_MODEL_ADVECTION, STG_MODEL_BURGERS = 0, 1
 STG_FORM_A, STG_FORM_A_INV = 0, 1
 STG_LINEAR_AUTO, STG_LINEAR_GMRES = 0, 3
 STG_KERNEL_AUTO, STG_KERNEL_GENERIC, STG_KERNEL_FAST = 0, 1, 2
+STG_PRECOND_NONE, STG_PRECOND_TBLOCK, STG_PRECOND_EBLOCK, STG_PRECOND_AUTO = 0, 1, 2, 3
 STG_MAX_HISTORY = 64
 
 # every symbol include/stg_cuda.h declares
@@ -42,7 +43,7 @@ class StgNewtonConfig(ctypes.Structure):
     _fields_ = [
         ("abs_tol", ctypes.c_double), ("rel_tol", ctypes.c_double), ("max_iter", ctypes.c_int),
         ("linear", ctypes.c_int), ("gmres_restart", ctypes.c_int), ("gmres_tol", ctypes.c_double),
-        ("gmres_max_it", ctypes.c_int), ("fd_eps", ctypes.c_double),
+        ("gmres_max_it", ctypes.c_int), ("fd_eps", ctypes.c_double), ("precond", ctypes.c_int),
     ]
 
 
@@ -89,7 +90,7 @@ def load() -> ctypes.CDLL:
     L.stg_st_jvp.argtypes = [_vp, _d, _d, _vp, _vp, _vp, _d]
     L.stg_stage_residual.argtypes = [_vp, _i, _d, _d, _vp, _vp, _vp]
     L.stg_stage_jvp.argtypes = [_vp, _i, _d, _d, _vp, _vp, _vp, _d]
-    L.stg_gmres_st.argtypes = [_vp, _d, _d, _vp, _vp, _vp, _i, _d, _i, ctypes.POINTER(_i),
+    L.stg_gmres_st.argtypes = [_vp, _d, _d, _vp, _vp, _vp, _i, _d, _i, _i, ctypes.POINTER(_i),
                                ctypes.POINTER(_d)]
     cfgp = ctypes.POINTER(StgNewtonConfig)
     infop = ctypes.POINTER(StgSolveInfo)

@@ -61,10 +61,12 @@ class NewtonConfig:  # newton.hpp:30-38 (+ fd_eps for nonlinear J v)
     gmres_tol: float = 1e-12
     gmres_max_it: int = 1000
     fd_eps: float = 0.0
+    precond: int = L.STG_PRECOND_AUTO  # block-Jacobi right preconditioner (stg_cuda.h)
 
     def to_c(self) -> L.StgNewtonConfig:
         return L.StgNewtonConfig(self.abs_tol, self.rel_tol, self.max_iter, self.linear,
-                                 self.gmres_restart, self.gmres_tol, self.gmres_max_it, self.fd_eps)
+                                 self.gmres_restart, self.gmres_tol, self.gmres_max_it, self.fd_eps,
+                                 self.precond)
 
 
 @dataclass
@@ -214,14 +216,14 @@ class SlabOperator:
         return out
 
     def gmres_st(self, t_n: float, dt: float, U, b, x=None, restart: int = 30, tol: float = 1e-12,
-                 max_it: int = 1000):
+                 max_it: int = 1000, precond: int = L.STG_PRECOND_AUTO):
         """linear_solve GMRES branch (newton.hpp:68-77) on the slab Jacobian."""
         x = torch.zeros(self.n_dof, dtype=torch.float64, device="cuda") if x is None else x
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0.0)
         Up = _ptr(U, self.n_dof, "U") if U is not None else None
         self._call(self._lib.stg_gmres_st, float(t_n), float(dt), Up, _ptr(b, self.n_dof, "b"),
-                   _ptr(x, self.n_dof, "x"), int(restart), float(tol), int(max_it),
+                   _ptr(x, self.n_dof, "x"), int(restart), float(tol), int(max_it), int(precond),
                    ctypes.byref(it), ctypes.byref(rr))
         return x, it.value, rr.value
 

@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 LIB = PKG / "libstg_cuda.so"
 OBJDIR = PKG / "build_obj"
 
-SOURCES = ["kernels_slab.cu", "kernels_vec.cu", "stg.cpp"]
+SOURCES = ["kernels_slab.cu", "kernels_vec.cu", "kernels_precond.cu", "stg.cpp"]
 HEADERS = ["kernels.hpp", "constants.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

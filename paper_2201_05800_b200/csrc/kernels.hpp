@@ -84,9 +84,23 @@ int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
 bool slab_fast_supported(const SlabArgs& a);
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s);
 
+// ---- block-Jacobi preconditioners (kernels_precond.cu) ----------------------
+// out[t][cell][k] = sum_j minv[k][t][j] in[j][cell][k]   (npc class tables)
+void precond_tblock(double* out, const double* in, const double* minv, int nt, int npc,
+                    long long ns, cudaStream_t s);
+// out_e = B_e in_e, B_e = B + e * bstride (bstride 0: one shared block), d = 1
+void precond_eblock(double* out, const double* in, const double* B, long long bstride, int nt,
+                    int n1, int ncells, long long ns, cudaStream_t s);
+// per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U
+bool build_burgers_eblock(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s);
+
 // ---- vector kernels (kernels_vec.cu) ----------------------------------------
 // All reductions are deterministic: fixed grid for a given n, fixed-order
-// block and final reductions (no atomics).
+// block and final reductions (the only atomic is the completion counter that
+// elects the finishing block; the sum order never depends on it).
+// `partial` buffers hold kPartialDoubles doubles followed by one zeroed
+// 32-bit completion counter.
+constexpr long long kPartialDoubles = 148LL * 8 * 80;
 int reduce_grid(long long n);
 void vec_fill(double* x, double v, long long n, cudaStream_t s);
 void vec_copy(double* y, const double* x, long long n, cudaStream_t s);
@@ -98,10 +112,13 @@ void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t
 // out[j] = <V_j, w>, j < k (V_j = V + j*ldv); partial buffer >= grid*k doubles
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
                   double* partial, double* out, cudaStream_t s);
-// w -= sum_{j<k} h[j] V_j (h on device), then out2[j] = <V_j, w> (if dots) and
-// out2[k] = <w,w>; partial buffer >= grid*(k+1)
+// w = (w - sum_{j<k} h[j] V_j) * s (h on device), then out2[j] = <V_j, w> (if
+// dots) and out2[k] = <w,w>; partial buffer >= grid*(k+1).  s = 1 unless
+// scale_src = [h_0..h_{k-1}, <w,w>] is given: then s = 1/sqrt(<w,w> - sum h^2)
+// (Pythagorean norm of the projected vector), written to scale_out[0].
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
-                    long long n, int want_dots, double* partial, double* out2, cudaStream_t s);
+                    long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
+                    const double* scale_src = nullptr, double* scale_out = nullptr);
 // y = x / sqrt(*nrm2)  (nrm2 on device)
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
                        cudaStream_t s);

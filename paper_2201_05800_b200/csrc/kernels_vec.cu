@@ -26,23 +26,29 @@ __device__ __forceinline__ double warp_max(double v) {
   return v;
 }
 
-// out[j] = sum_b part[b*cnt + j] in fixed order (one block, one warp per j).
-__global__ void finish_sum(const double* part, int nblocks, int cnt, double* out) {
+// Last-block completion: every block publishes its partials, bumps the
+// counter, and the block that arrives last finishes the reduction -- in the
+// fixed block order, so the result does not depend on arrival order -- and
+// resets the counter for the next launch.  Saves one launch per reduction.
+__device__ __forceinline__ bool is_last_block(unsigned* counter) {
+  __shared__ unsigned last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(counter, 1u) == gridDim.x - 1 ? 1u : 0u;
+  __syncthreads();
+  return last != 0u;
+}
+
+__device__ __forceinline__ void block_finish_sum(const double* part, int nblocks, int cnt,
+                                                 double* out, unsigned* counter) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int j = warp; j < cnt; j += nw) {
     double s = 0.0;
-    for (int b = lane; b < nblocks; b += 32) s += part[(size_t)b * cnt + j];
+    for (int b = lane; b < nblocks; b += 32) s += __ldcg(part + (size_t)b * cnt + j);
     s = warp_sum(s);
     if (lane == 0) out[j] = s;
   }
-}
-
-__global__ void finish_max(const double* part, int nblocks, double* out) {
-  const int lane = threadIdx.x & 31;
-  double m = 0.0;
-  for (int b = lane; b < nblocks; b += 32) m = fmax(m, part[b]);
-  m = warp_max(m);
-  if (lane == 0) out[0] = m;
+  if (threadIdx.x == 0) *counter = 0u;
 }
 
 __global__ void k_fill(double* x, double v, long long n) {
@@ -104,7 +110,8 @@ template <int MPW>
 __global__ void __launch_bounds__(kMultiBlock) k_multidot(const double* __restrict__ V,
                                                           long long ldv, int k,
                                                           const double* __restrict__ w,
-                                                          long long n, double* part) {
+                                                          long long n, double* part,
+                                                          double* out, unsigned* counter) {
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   double acc[MPW];
 #pragma unroll
@@ -136,6 +143,7 @@ __global__ void __launch_bounds__(kMultiBlock) k_multidot(const double* __restri
     const double s = warp_sum(acc[m]);
     if (lane == 0 && j < k) part[(size_t)blockIdx.x * k + j] = s;
   }
+  if (is_last_block(counter)) block_finish_sum(part, gridDim.x, k, out, counter);
 }
 
 // w += sign * sum_j h_j V_j; optionally dots <V_j, w_new>; always <w_new, w_new>.
@@ -146,13 +154,32 @@ __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
                                                         long long ldv, int k,
                                                         const double* __restrict__ h,
                                                         long long n, int dots, double sign,
-                                                        double* part) {
+                                                        double* part,
+                                                        const double* __restrict__ scale_src,
+                                                        double* scale_out, double* out,
+                                                        unsigned* counter) {
   __shared__ double red[kWarps][kU][32];
   __shared__ double wnew[kU][32];
   __shared__ double hs[kWarps * MPW];
+  __shared__ double sc;
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   for (int j = threadIdx.x; j < kWarps * MPW; j += blockDim.x) hs[j] = j < k ? h[j] : 0.0;
+  if (threadIdx.x == 0) {
+    // scale_src = [h_0..h_{k-1}, <w,w>]: normalise by the Pythagorean norm
+    // sqrt(<w,w> - sum h_j^2) of the projected vector (fallback: ||w||)
+    double s = 1.0;
+    if (scale_src) {
+      const double ww = scale_src[k];
+      double hh = 0.0;
+      for (int j = 0; j < k; ++j) hh = fma(scale_src[j], scale_src[j], hh);
+      const double est = ww - hh;
+      s = est > 1e-28 * ww ? 1.0 / sqrt(est) : (ww > 0.0 ? 1.0 / sqrt(ww) : 1.0);
+      if (scale_out && blockIdx.x == 0) scale_out[0] = s;
+    }
+    sc = s;
+  }
   __syncthreads();
+  const double s = sc;
   double acc[MPW];
 #pragma unroll
   for (int m = 0; m < MPW; ++m) acc[m] = 0.0;
@@ -181,12 +208,12 @@ __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
     {
       // warp g finishes slot u = g
       const long long i = base + 32 * g + lane;
-      double s = 0.0;
+      double sum = 0.0;
 #pragma unroll
-      for (int q = 0; q < kWarps; ++q) s += red[q][g][lane];
+      for (int q = 0; q < kWarps; ++q) sum += red[q][g][lane];
       double wi = 0.0;
       if (i < n) {
-        wi = fma(sign, s, w[i]);
+        wi = fma(sign, sum, w[i]) * s;
         w[i] = wi;
       }
       wnew[g][lane] = wi;
@@ -219,10 +246,12 @@ __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
     for (int q = 0; q < kWarps; ++q) t += nr[q];
     part[(size_t)blockIdx.x * (k + 1) + k] = t;
   }
+  if (is_last_block(counter)) block_finish_sum(part, gridDim.x, k + 1, out, counter);
 }
 
 __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x, long long n,
-                                                   double* part) {
+                                                   double* part, double* out,
+                                                   unsigned* counter) {
   __shared__ double red[kBlock / 32];
   double m = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -235,6 +264,15 @@ __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x,
     double r = 0.0;
     for (int w = 0; w < kBlock / 32; ++w) r = fmax(r, red[w]);
     part[blockIdx.x] = r;
+  }
+  if (is_last_block(counter) && threadIdx.x < 32) {
+    double r = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) r = fmax(r, __ldcg(part + b));
+    r = warp_max(r);
+    if (threadIdx.x == 0) {
+      out[0] = r;
+      *counter = 0u;
+    }
   }
 }
 
@@ -284,32 +322,41 @@ void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long
     CALL;                                \
   }
 
+// The completion counter lives right after the partial-sum area (see
+// kPartialDoubles in kernels.hpp); it is zero between launches.
+unsigned* counter_of(double* partial) {
+  return reinterpret_cast<unsigned*>(partial + kPartialDoubles);
+}
+
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
                   double* partial, double* out, cudaStream_t s) {
   const int g = multi_grid(n);
-  STG_DISPATCH_MPW(k, (k_multidot<MPW><<<g, kMultiBlock, 0, s>>>(V, ldv, k, w, n, partial)));
-  finish_sum<<<1, 1024, 0, s>>>(partial, g, k, out);
+  unsigned* c = counter_of(partial);
+  STG_DISPATCH_MPW(k, (k_multidot<MPW><<<g, kMultiBlock, 0, s>>>(V, ldv, k, w, n, partial, out,
+                                                                 c)));
 }
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
-                    long long n, int want_dots, double* partial, double* out2, cudaStream_t s) {
+                    long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
+                    const double* scale_src, double* scale_out) {
   const int g = multi_grid(n);
+  unsigned* c = counter_of(partial);
   STG_DISPATCH_MPW(k, (k_update<MPW><<<g, kMultiBlock, 0, s>>>(w, V, ldv, k, h, n, want_dots,
-                                                               -1.0, partial)));
-  finish_sum<<<1, 1024, 0, s>>>(partial, g, k + 1, out2);
+                                                               -1.0, partial, scale_src,
+                                                               scale_out, out2, c)));
 }
 
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
                  cudaStream_t s) {
   const int g = multi_grid(n);
   STG_DISPATCH_MPW(k, (k_update<MPW><<<g, kMultiBlock, 0, s>>>(x, V, ldv, k, y, n, 0, 1.0,
+                                                               nullptr, nullptr, nullptr, nullptr,
                                                                nullptr)));
 }
 
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s) {
   const int g = grid_for(n);
-  k_maxabs<<<g, kBlock, 0, s>>>(x, n, partial);
-  finish_max<<<1, 32, 0, s>>>(partial, g, out);
+  k_maxabs<<<g, kBlock, 0, s>>>(x, n, partial, out, counter_of(partial));
 }
 
 void vec_dot(const double* x, const double* y, long long n, double* partial, double* out,

@@ -76,11 +76,13 @@ struct stg_handle {
   int kernel_pref = STG_KERNEL_AUTO;
   std::string err;
   long long launches = 0;
+  long long reorth = 0;  // Arnoldi steps that needed a second Gram-Schmidt pass
 
   // workspace
   DevBuf small;    // device scalars / Hessenberg columns
   DevBuf partial;  // reduction partials
   DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
+  DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
 
@@ -193,6 +195,10 @@ void validate_desc(const stg_desc* d) {
     cells *= d->cells[a];
   }
   if (cells > (1LL << 30)) throw std::invalid_argument("too many cells");
+  long long npc = 1;
+  for (int a = 0; a < d->dim; ++a) npc *= d->degree + 1;
+  if (cells * npc >= (1LL << 31))
+    throw std::invalid_argument("mesh too large: n_sdof must stay below 2^31");
 }
 
 void build_constants(stg_handle* h) {
@@ -251,14 +257,17 @@ void ensure_workspace(stg_handle* h) {
   if (!h->pinned) {
     ck(cudaMallocHost(&h->pinned, sizeof(double) * stg_handle::kSmall), "cudaMallocHost");
     h->small.ensure(stg_handle::kSmall);
-    h->partial.ensure(size_t(148 * 8) * 80);
+    // reduction partials + the zeroed completion counter (kernels.hpp)
+    h->partial.ensure(size_t(stg::kPartialDoubles) + 1);
+    ck(cudaMemset(h->partial.p, 0, sizeof(double) * (size_t(stg::kPartialDoubles) + 1)),
+       "cudaMemset");
   }
 }
 
 // ---- device reductions returning to the host --------------------------------
 double dev_maxabs(stg_handle* h, const double* x, long long n) {
   stg::vec_maxabs(x, n, h->partial.p, h->small.p, h->stream);
-  h->launches += 2;
+  h->launches += 1;  // fused last-block reduction
   ck(cudaMemcpyAsync(h->pinned, h->small.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream),
      "memcpy");
   ck(cudaStreamSynchronize(h->stream), "sync");
@@ -267,7 +276,7 @@ double dev_maxabs(stg_handle* h, const double* x, long long n) {
 
 double dev_dot(stg_handle* h, const double* x, const double* y, long long n) {
   stg::vec_dot(x, y, n, h->partial.p, h->small.p, h->stream);
-  h->launches += 2;
+  h->launches += 1;
   ck(cudaMemcpyAsync(h->pinned, h->small.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream),
      "memcpy");
   ck(cudaStreamSynchronize(h->stream), "sync");
@@ -280,12 +289,14 @@ struct GmresStats {
   bool converged = false;
 };
 
-// Restarted GMRES(m), right-unpreconditioned, classical Gram-Schmidt with one
-// full re-orthogonalisation (CGS2) in three fused passes, Givens rotations on
-// the host.  Stops when ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at
-// newton.hpp:68-77).  x holds the initial guess.
+// Restarted GMRES(m), right-preconditioned (A P^-1 y = b, x = P^-1 y; P null:
+// unpreconditioned), classical Gram-Schmidt with one full
+// re-orthogonalisation (CGS2) in three fused passes, Givens rotations on the
+// host.  Right preconditioning keeps the stopping test on the true residual,
+// ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at newton.hpp:68-77).
+// x holds the initial guess.
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
-                 double tol, int max_it) {
+                 double tol, int max_it, const Op* P = nullptr) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > 60) throw std::invalid_argument("gmres: restart <= 60");
@@ -293,6 +304,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   const long long ld = round_up(n, 32);
   h->basis.ensure(size_t(ld) * (m + 1));
   h->wv.ensure(size_t(n));
+  if (P) {
+    h->zv.ensure(size_t(n));
+    h->zc.ensure(size_t(n));
+  }
   double* V = h->basis.p;
   double* w = h->wv.p;
   double* dsm = h->small.p;  // [0..m+1] h1, [64..] h2/norm, [128..] h3/norm, [256..] y
@@ -314,7 +329,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     stg::vec_axpby(w, 1.0, b, -1.0, n, s);     // w = b - A x
     h->launches++;
     stg::vec_multidot(w, 0, 1, w, n, h->partial.p, dsm + 200, s);
-    h->launches += 2;
+    h->launches += 1;
     ck(cudaMemcpyAsync(hp + 200, dsm + 200, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
     stg::vec_scale_invsqrt(V, w, dsm + 200, n, s);  // V_0 = r / ||r||
     h->launches++;
@@ -331,17 +346,44 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     int k = 0;
     for (; k < m && total < max_it; ++k) {
       ++total;
-      A(V + size_t(k) * ld, w);
+      // Arnoldi step: the operator writes A P^-1 v_k straight into the next
+      // basis slot; one pass computes h = V^T w and <w,w>; one fused pass
+      // projects and normalises with the Pythagorean norm.  A second
+      // (classical) Gram-Schmidt pass runs only if that norm shows heavy
+      // cancellation (||w - V h||^2 < 1e-4 ||w||^2, DGKS-style), which keeps
+      // the orthogonality loss per step near 1e-14 at two passes per step.
+      double* vn = V + size_t(k + 1) * ld;
+      if (P) {
+        (*P)(V + size_t(k) * ld, h->zv.p);  // z = P^-1 v_k
+        A(h->zv.p, vn);
+      } else {
+        A(V + size_t(k) * ld, vn);
+      }
       const int kk = k + 1;  // vectors V_0..V_k
-      stg::vec_multidot(V, ld, kk, w, n, h->partial.p, dsm, s);                    // h1
-      stg::vec_update_dot(w, V, ld, kk, dsm, n, 1, h->partial.p, dsm + 64, s);     // w -= V h1; h2
-      stg::vec_update_dot(w, V, ld, kk, dsm + 64, n, 0, h->partial.p, dsm + 128, s);  // w -= V h2
-      stg::vec_scale_invsqrt(V + size_t(k + 1) * ld, w, dsm + 128 + kk, n, s);
-      h->launches += 7;
+      stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s);  // [h_0..h_k, <w,w>]
+      stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190);
+      h->launches += 2;
       ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
       ck(cudaStreamSynchronize(s), "sync");
-      for (int j = 0; j <= k; ++j) Hat(j, k) = hp[j] + hp[64 + j];
-      const double hn = std::sqrt(hp[128 + kk]);
+      const double ww = hp[kk];
+      double hh = 0.0;
+      for (int j = 0; j <= k; ++j) hh += hp[j] * hp[j];
+      const double sigma = 1.0 / hp[190];  // norm used to scale the stored vector
+      for (int j = 0; j <= k; ++j) Hat(j, k) = hp[j];
+      double hn = sigma;
+      if (!(ww - hh > 1e-4 * ww) || std::abs(hp[64 + kk] - 1.0) > 1e-10) {
+        // re-orthogonalise the stored (scaled) vector: g2 = V^T vn, vn -= V g2
+        stg::vec_multidot(V, ld, kk, vn, n, h->partial.p, dsm + 128, s);
+        stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s);
+        stg::vec_scale_invsqrt(vn, vn, dsm + 64 + kk, n, s);
+        h->launches += 3;
+        ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
+        ck(cudaStreamSynchronize(s), "sync");
+        for (int j = 0; j <= k; ++j) Hat(j, k) += sigma * hp[128 + j];
+        hn = sigma * std::sqrt(hp[64 + kk]);
+        h->reorth++;
+      }
+      if (!(ww > 0.0)) hn = 0.0;  // exact breakdown: A P^-1 v_k = 0
       Hat(k + 1, k) = hn;
       for (int j = 0; j < k; ++j) {
         const double t0 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);
@@ -368,8 +410,16 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     std::memcpy(hp + 256, y.data(), sizeof(double) * k);
     ck(cudaMemcpyAsync(dsm + 256, hp + 256, sizeof(double) * k, cudaMemcpyHostToDevice, s),
        "memcpy");
-    stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
-    h->launches++;
+    if (P) {
+      stg::vec_fill(h->zc.p, 0.0, n, s);
+      stg::vec_combine(h->zc.p, V, ld, k, dsm + 256, n, s);  // t = V y
+      (*P)(h->zc.p, h->zv.p);                                // P^-1 t
+      stg::vec_axpy(x, 1.0, h->zv.p, n, s);                  // x += P^-1 V y
+      h->launches += 3;
+    } else {
+      stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
+      h->launches++;
+    }
     ck(cudaStreamSynchronize(s), "sync");  // hp+256 reused next cycle
   }
   st.iterations = total;
@@ -384,9 +434,16 @@ struct NewtonOut {
   std::vector<double> history;
 };
 
+// The linear system of one Newton iteration: the Jacobian action and an
+// optional right preconditioner (empty function: none).
+struct LinSys {
+  Op A;
+  Op P;
+};
+
 // newton_solve (newton.hpp:102-130) on device vectors; u holds u0 on entry.
 NewtonOut newton(stg_handle* h, const Op& residual,
-                 const std::function<Op(const double*)>& jacobian, double* u, long long n,
+                 const std::function<LinSys(const double*)>& jacobian, double* u, long long n,
                  const stg_newton_config& cfg) {
   ensure_workspace(h);
   h->res.ensure(size_t(n));
@@ -405,12 +462,12 @@ NewtonOut newton(stg_handle* h, const Op& residual,
                                     std::to_string(cfg.max_iter) + " iterations, residual " +
                                     fmt_short(norm),
                                 out.history);
-    const Op J = jacobian(u);
+    const LinSys J = jacobian(u);
     stg::vec_axpby(r, 0.0, r, -1.0, n, h->stream);  // r = -r
     stg::vec_fill(du, 0.0, n, h->stream);
     h->launches += 2;
-    const GmresStats gs = gmres(h, J, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
-                                cfg.gmres_max_it);
+    const GmresStats gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
+                                cfg.gmres_max_it, J.P ? &J.P : nullptr);
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
@@ -497,6 +554,87 @@ void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double
   }
 }
 
+int resolve_precond(const stg_handle* h, int kind) {
+  if (kind == STG_PRECOND_AUTO)
+    return h->desc.dim == 1 ? STG_PRECOND_EBLOCK
+                            : (h->desc.model == STG_MODEL_ADVECTION ? STG_PRECOND_TBLOCK
+                                                                    : STG_PRECOND_NONE);
+  if (kind == STG_PRECOND_EBLOCK && h->desc.dim != 1)
+    throw std::invalid_argument("element-block Jacobi: d = 1 only");
+  if (kind == STG_PRECOND_TBLOCK && h->desc.model != STG_MODEL_ADVECTION)
+    throw std::invalid_argument("temporal-block Jacobi: advection only");
+  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_AUTO)
+    throw std::invalid_argument("unknown preconditioner");
+  return kind;
+}
+
+// Right preconditioner for the Jacobian with temporal mixing (T, S) at the
+// linearisation point U (used by the Burgers element blocks only).
+Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U) {
+  kind = resolve_precond(h, kind);
+  if (kind == STG_PRECOND_NONE) return Op();
+  const int nt = h->nt, n1 = h->n1, npc = h->g.npc, d = h->desc.dim;
+  const long long ns = h->n_sdof;
+  if (kind == STG_PRECOND_TBLOCK) {
+    // block of node class k: T + v_k S with v_k = sum_a V_a(i_a, i_a)
+    std::vector<double> tab(size_t(npc) * nt * nt), B(size_t(nt) * nt);
+    for (int k = 0; k < npc; ++k) {
+      const int idx[3] = {k % n1, (k / n1) % n1, k / (n1 * n1)};
+      double v = 0.0;
+      for (int a = 0; a < d; ++a) v += h->sp.V[a][idx[a]][idx[a]];
+      for (int r = 0; r < nt; ++r)
+        for (int j = 0; j < nt; ++j) B[size_t(r) * nt + j] = mx.T[r][j] + v * mx.S[r][j];
+      const std::vector<double> Bi = stg::inverse(B, nt);
+      std::copy(Bi.begin(), Bi.end(), tab.begin() + long(size_t(k) * nt * nt));
+    }
+    h->ptab.ensure(tab.size());
+    ck(cudaMemcpyAsync(h->ptab.p, tab.data(), sizeof(double) * tab.size(),
+                       cudaMemcpyHostToDevice, h->stream), "H2D");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    const double* dt = h->ptab.p;
+    return [h, dt, nt, npc, ns](const double* in, double* out) {
+      stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream);
+      h->launches++;
+    };
+  }
+  // element-block Jacobi, d = 1: block (r,i),(j,q) of the element-local Jacobian
+  const int nb = nt * n1;
+  const int ncells = h->g.n_cells;
+  long long bstride = 0;
+  if (h->desc.model == STG_MODEL_ADVECTION) {
+    std::vector<double> B(size_t(nb) * nb);
+    for (int r = 0; r < nt; ++r)
+      for (int i = 0; i < n1; ++i)
+        for (int j = 0; j < nt; ++j)
+          for (int q = 0; q < n1; ++q)
+            B[size_t(r * n1 + i) * nb + size_t(j * n1 + q)] =
+                (i == q ? mx.T[r][j] : 0.0) + mx.S[r][j] * h->sp.V[0][i][q];
+    const std::vector<double> Bi = stg::inverse(B, nb);
+    h->ptab.ensure(Bi.size());
+    ck(cudaMemcpyAsync(h->ptab.p, Bi.data(), sizeof(double) * Bi.size(), cudaMemcpyHostToDevice,
+                       h->stream), "H2D");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+  } else {
+    stg::SlabArgs a{};
+    a.sp = h->sp;
+    a.mx = mx;
+    a.g = h->g;
+    a.n_in = nt;
+    a.n_out = nt;
+    h->ptab.ensure(size_t(ncells) * nb * nb);
+    if (!stg::build_burgers_eblock(h->ptab.p, U, a, h->stream))
+      throw std::invalid_argument("element-block Jacobi: degree <= 3 for Burgers");
+    h->launches++;
+    check_launch(h);
+    bstride = (long long)nb * nb;
+  }
+  const double* tab = h->ptab.p;
+  return [h, tab, bstride, nt, n1, ncells, ns](const double* in, double* out) {
+    stg::precond_eblock(out, in, tab, bstride, nt, n1, ncells, ns, h->stream);
+    h->launches++;
+  };
+}
+
 stg_newton_config effective_cfg(const stg_newton_config* cfg) {
   stg_newton_config c;
   stg_newton_config_default(&c);
@@ -521,8 +659,11 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
   try {
     o = newton(
         h, [&](const double* X, double* R) { st_residual(h, dt, u_n, X, R); },
-        [&](const double* X) -> Op {
-          return [h, dt, X, eps](const double* v, double* Jv) { st_jvp(h, dt, X, v, Jv, eps); };
+        [&](const double* X) -> LinSys {
+          LinSys L;
+          L.A = [h, dt, X, eps](const double* v, double* Jv) { st_jvp(h, dt, X, v, Jv, eps); };
+          L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
+          return L;
         },
         U, n, cfg);
   } catch (const NonconvergenceError& e) {
@@ -553,10 +694,13 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
   try {
     o = newton(
         h, [&](const double* X, double* R) { stage_residual(h, form, dt, u, X, R); },
-        [&](const double* X) -> Op {
-          return [h, form, dt, X, eps](const double* v, double* Jv) {
+        [&](const double* X) -> LinSys {
+          LinSys L;
+          L.A = [h, form, dt, X, eps](const double* v, double* Jv) {
             stage_jvp(h, form, dt, X, v, Jv, eps);
           };
+          L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
+          return L;
         },
         U, n, cfg);
   } catch (const NonconvergenceError& e) {
@@ -616,6 +760,7 @@ void stg_newton_config_default(stg_newton_config* c) {
   c->gmres_tol = 1e-12;
   c->gmres_max_it = 1000;
   c->fd_eps = 0.0;
+  c->precond = STG_PRECOND_AUTO;
 }
 
 const char* stg_last_error(const stg_handle* h) {
@@ -808,16 +953,18 @@ int stg_stage_jvp(stg_handle* h, int form, double t, double dt, const double* U,
 }
 
 int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const double* b,
-                 double* x, int restart, double tol, int max_it, int* iterations,
+                 double* x, int restart, double tol, int max_it, int precond, int* iterations,
                  double* rel_residual) {
   return guarded(h, [&] {
     need(h, "stg_gmres_st");
     need(b, "b");
     need(x, "x");
     (void)t_n;
+    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
     const GmresStats st = gmres(
         h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
-        restart, tol, max_it);
+        restart, tol, max_it, P ? &P : nullptr);
     if (iterations) *iterations = st.iterations;
     if (rel_residual) *rel_residual = st.rel_residual;
     if (!st.converged)

@@ -257,6 +257,40 @@ def test_burgers_newton_vs_oracle():
     assert rel(U, Uo) <= TOL_SOLVE
 
 
+@pytest.mark.parametrize("name,cells,pcs", [
+    ("c4", (8, 8, 8), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK]),
+    ("c2", (16, 16), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK]),
+    ("c1", (64,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
+    ("c3", (256,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
+])
+def test_preconditioners_same_solution_fewer_iterations(name, cells, pcs):
+    cfg = C.CONFIGS[name].scaled(cells)
+    op = SlabOperator(**cfg.kwargs())
+    un = dev(C.initial_state(cfg))
+    dt = cfg.dt if name != "c3" else 1e-3
+    sols, its = [], []
+    for pc in pcs:
+        nc = NewtonConfig(abs_tol=1e-13, rel_tol=1e-12, gmres_tol=1e-13, precond=pc,
+                          gmres_max_it=5000)
+        U, u1, info = op.stdg_step(0.0, dt, un, nc)
+        sols.append(U.cpu().numpy())
+        its.append(info.linear_iterations)
+    assert rel(sols[1], sols[0]) <= TOL_SOLVE
+    assert its[1] < its[0], its
+
+
+def test_preconditioned_stage_solve_matches_slab():
+    cfg = C.CONFIGS["c5"].scaled((8, 8, 8))
+    op = SlabOperator(**cfg.kwargs())
+    un = dev(C.initial_state(cfg))
+    tight = NewtonConfig(abs_tol=0.0, rel_tol=1e-13, gmres_tol=1e-14,
+                         precond=L.STG_PRECOND_TBLOCK)
+    Ua, _, _ = op.stdg_step(0.0, cfg.dt, un, tight)
+    for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
+        Ub, _, _ = op.rk_step(form, 0.0, cfg.dt, un, tight)
+        assert rel(Ub, Ua.cpu().numpy()) <= TOL_SOLVE
+
+
 def test_burgers_fd_jvp_close_to_exact():
     cfg = C.CONFIGS["c3"].scaled((64,))
     op = SlabOperator(**cfg.kwargs())
