@@ -260,6 +260,330 @@ __global__ void __launch_bounds__(GenericShape<D, N1>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
+// d = 2: E consecutive cells per CTA staged in shared memory, three balanced
+// line-owner phases (every thread owns one line of N1 nodes per phase):
+//   A: x-line at (t, y)  -> x derivative + x faces      -> G
+//   B: y-line at (t, x)  -> y derivative + y faces      -> G (complete F)
+//   C: t-line at (y, x)  -> temporal mixing + u_n term  -> R (coalesced STG)
+// Shared-memory traffic is ~8 doubles per DOF and there are few registers
+// per thread, so many CTAs stay resident to hide HBM latency.
+// ---------------------------------------------------------------------------
+template <int N1, int NT>
+struct Shape2d {
+  static constexpr int NPC = N1 * N1;
+  static constexpr int LINES = (NT > N1 ? NT : N1) * N1;  // threads per cell
+  static constexpr int E = LINES >= 32 ? 4 : 8;
+  static constexpr int THREADS = E * LINES;
+};
+
+template <int N1, int NT>
+__global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
+    slab2d_kernel(const SlabArgs a) {
+  using Sh = Shape2d<N1, NT>;
+  constexpr int NPC = Sh::NPC, E = Sh::E;
+  __shared__ double Xs[NT][E][NPC];
+  __shared__ double Gs[NT][E][NPC];
+  const int tid = threadIdx.x;
+  const int nx = a.g.nx, ny = a.g.ny;
+  const long long ns = a.g.n_sdof;
+  const int c0 = blockIdx.x * E;
+  const int ncell = a.g.n_cells;
+
+  // ---- coalesced staging of the tile: for each t, E*NPC contiguous doubles
+  for (int q = tid; q < NT * E * NPC; q += Sh::THREADS) {
+    const int t = q / (E * NPC), r = q - t * (E * NPC);
+    const int e = r / NPC;
+    Xs[t][e][r - e * NPC] = (c0 + e < ncell) ? a.X[t * ns + (long long)c0 * NPC + r] : 0.0;
+  }
+
+  // ---- identities and early global loads ---------------------------------
+  const int e = tid / Sh::LINES, l = tid - (tid / Sh::LINES) * Sh::LINES;
+  const int cell = c0 + e;
+  const bool active = e < E && cell < ncell;
+  const int cx = cell % nx, cy = (cell / nx) % ny;
+  const bool nLx = a.sp.cL[0] != 0.0, nRx = a.sp.cR[0] != 0.0;
+  const bool nLy = a.sp.cL[1] != 0.0, nRy = a.sp.cR[1] != 0.0;
+  // phase A/B line index: t = l / N1, m = l % N1 (y for A, x for B)
+  const bool lineAB = active && l < NT * N1;
+  const int tL = l / N1, mL = l - (l / N1) * N1;
+  double xl = 0.0, xr = 0.0, yl = 0.0, yr = 0.0;
+  if (lineAB) {
+    const double* Xt = a.X + tL * ns;
+    const bool inL = e > 0 && cx > 0, inR = e < E - 1 && cx < nx - 1 && cell + 1 < ncell;
+    if (nLx && !inL) xl = Xt[(long long)(cell - cx + (cx == 0 ? nx - 1 : cx - 1)) * NPC + mL * N1 + N1 - 1];
+    if (nRx && !inR) xr = Xt[(long long)(cell - cx + (cx == nx - 1 ? 0 : cx + 1)) * NPC + mL * N1];
+    if (nLy) yl = Xt[(long long)(cell + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx) * NPC + (N1 - 1) * N1 + mL];
+    if (nRy) yr = Xt[(long long)(cell + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx) * NPC + mL];
+  }
+  // phase C: node (y, x) = (l / N1, l % N1)
+  const bool lineC = active && l < NPC;
+  double w = 0.0;
+  if (lineC && a.has_w) w = a.W[(long long)cell * NPC + l];
+  __syncthreads();
+
+  // ---- phase A: x-line at (t = tL, y = mL) ---------------------------------
+  if (lineAB) {
+    const double* row = &Xs[tL][e][mL * N1];
+    if (nLx && e > 0 && cx > 0) xl = Xs[tL][e - 1][mL * N1 + N1 - 1];
+    if (nRx && e < E - 1 && cx < nx - 1 && cell + 1 < ncell) xr = Xs[tL][e + 1][mL * N1];
+    double u[N1];
+#pragma unroll
+    for (int k = 0; k < N1; ++k) u[k] = row[k];
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double g = 0.0;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) g = fma(a.sp.V[0][i][k], u[k], g);
+      if (i == 0) g = fma(a.sp.cL[0], xl, g);
+      if (i == N1 - 1) g = fma(a.sp.cR[0], xr, g);
+      Gs[tL][e][mL * N1 + i] = g;
+    }
+  }
+  __syncthreads();
+  // ---- phase B: y-line at (t = tL, x = mL) ---------------------------------
+  if (lineAB) {
+    double u[N1];
+#pragma unroll
+    for (int k = 0; k < N1; ++k) u[k] = Xs[tL][e][k * N1 + mL];
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      double g = Gs[tL][e][i * N1 + mL];
+#pragma unroll
+      for (int k = 0; k < N1; ++k) g = fma(a.sp.V[1][i][k], u[k], g);
+      if (i == 0) g = fma(a.sp.cL[1], yl, g);
+      if (i == N1 - 1) g = fma(a.sp.cR[1], yr, g);
+      Gs[tL][e][i * N1 + mL] = g;
+    }
+  }
+  __syncthreads();
+  // ---- phase C: t-line at node l ---------------------------------------------
+  if (lineC) {
+    double x[NT], G[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      x[j] = Xs[j][e][l];
+      G[j] = Gs[j][e][l];
+    }
+    double* Rp = a.R + (long long)cell * NPC + l;
+#pragma unroll
+    for (int r = 0; r < NT; ++r) {
+      if (r >= a.n_out) break;
+      double acc = a.mx.c[r] * w;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        acc = fma(a.mx.T[r][j], x[j], acc);
+        acc = fma(a.mx.S[r][j], G[j], acc);
+      }
+      Rp[r * ns] = acc;
+    }
+  }
+}
+
+// PTX helpers for the mbarrier / bulk-async-copy pipelines.
+namespace ptx {
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(bar), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// generic-proxy reads of a buffer before async-proxy (TMA / bulk) writes to it
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+}  // namespace ptx
+
+// Persistent variant of slab2d_kernel: the E-cell tile of segment i+1 is
+// bulk-copied (cp.async.bulk, one copy per temporal block) into the other
+// stage of a 2-stage ring while segment i is computed, and each thread
+// prefetches the next segment's neighbour traces and u_n into registers.
+// Time planes are padded by 2 doubles (keeps 16-byte alignment for the bulk
+// copies and breaks the 2-way bank conflicts between planes).
+// Requires n_cells % E == 0.
+template <int N1, int NT>
+struct P2d {
+  using Sh = Shape2d<N1, NT>;
+  static constexpr int E = Sh::E, NPC = Sh::NPC;
+  // plane pitch: +10 doubles for (N1, NT) = (5, 5) (c2) minimises shared-
+  // memory wavefronts with the line-major thread mapping (bank simulation:
+  // 735 vs 915 half-warp wavefronts per tile); +2 keeps 16-byte alignment
+  static constexpr int PAD = (N1 == 5 && NT == 5) ? 10 : 2;
+  static constexpr int PLANE = E * NPC + PAD;         // padded plane (doubles)
+  static constexpr int STAGE = NT * PLANE;            // doubles per stage
+  static constexpr int SMEM = (3 * STAGE) * 8 + 64;   // 2 X stages + G + barriers
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
+                                         uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+template <int N1, int NT>
+__global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
+    slab2d_persist(const SlabArgs a) {
+  using P = P2d<N1, NT>;
+  using Sh = typename P::Sh;
+  constexpr int NPC = P::NPC, E = P::E, PL = P::PLANE;
+  extern __shared__ __align__(16) double sm2[];
+  double* G = sm2 + 2 * P::STAGE;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm2 + 3 * P::STAGE);
+  const uint32_t bar0 = ptx::smem_u32(bars), bar1 = ptx::smem_u32(bars + 1);
+  const int tid = threadIdx.x;
+  const int nx = a.g.nx, ny = a.g.ny;
+  const long long ns = a.g.n_sdof;
+  const int nseg = a.g.n_cells / E;
+  const uint32_t tbytes = E * NPC * 8;
+  const bool nLx = a.sp.cL[0] != 0.0, nRx = a.sp.cR[0] != 0.0;
+  const bool nLy = a.sp.cL[1] != 0.0, nRy = a.sp.cR[1] != 0.0;
+
+  if (tid == 0) {
+    ptx::mbar_init(bar0, 1);
+    ptx::mbar_init(bar1, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  const int e = tid / Sh::LINES, l = tid - (tid / Sh::LINES) * Sh::LINES;
+  const bool lineAB = l < NT * N1;
+  const bool lineC = l < NPC;
+  const int tL = l % NT, mL = l / NT;  // line-major: consecutive lanes step in t
+
+  auto issue = [&](int seg, int st) {
+    const uint32_t bar = st ? bar1 : bar0;
+    ptx::mbar_expect_tx(bar, NT * tbytes);
+    const uint32_t dst = ptx::smem_u32(sm2 + st * P::STAGE);
+    const double* src = a.X + (long long)seg * E * NPC;
+    for (int t = 0; t < NT; ++t) bulk_g2s(dst + t * PL * 8, src + t * ns, tbytes, bar);
+  };
+  // neighbour traces (x halos from outside the tile, y faces) and u_n
+  auto faces = [&](int seg, double& xl, double& xr, double& yl, double& yr, double& w) {
+    const int cell = seg * E + e;
+    const int cx = cell % nx, cy = (cell / nx) % ny;
+    xl = xr = yl = yr = w = 0.0;
+    if (lineAB) {
+      const double* Xt = a.X + tL * ns;
+      if (nLx && !(e > 0 && cx > 0))
+        xl = Xt[(long long)(cell - cx + (cx == 0 ? nx - 1 : cx - 1)) * NPC + mL * N1 + N1 - 1];
+      if (nRx && !(e < E - 1 && cx < nx - 1))
+        xr = Xt[(long long)(cell - cx + (cx == nx - 1 ? 0 : cx + 1)) * NPC + mL * N1];
+      if (nLy) yl = Xt[(long long)(cell + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx) * NPC + (N1 - 1) * N1 + mL];
+      if (nRy) yr = Xt[(long long)(cell + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx) * NPC + mL];
+    }
+    if (lineC && a.has_w) w = a.W[(long long)cell * NPC + l];
+  };
+
+  int seg = blockIdx.x;
+  if (tid == 0 && seg < nseg) issue(seg, 0);
+  double xl, xr, yl, yr, w;
+  if (seg < nseg) faces(seg, xl, xr, yl, yr, w);
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int st = it & 1;
+    const int nxt = seg + gridDim.x;
+    if (tid == 0 && nxt < nseg) {
+      ptx::fence_proxy_async_smem();
+      issue(nxt, st ^ 1);
+    }
+    double nxl = 0, nxr = 0, nyl = 0, nyr = 0, nw = 0;
+    if (nxt < nseg) faces(nxt, nxl, nxr, nyl, nyr, nw);
+    while (!ptx::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+    const double* X = sm2 + st * P::STAGE;
+    const int cell = seg * E + e;
+    const int cx = cell % nx;
+
+    // phase A: x-line at (t = tL, y = mL)
+    if (lineAB) {
+      const double* row = X + tL * PL + e * NPC + mL * N1;
+      double hl = xl, hr = xr;
+      if (nLx && e > 0 && cx > 0) hl = row[-NPC + N1 - 1];
+      if (nRx && e < E - 1 && cx < nx - 1) hr = row[NPC];
+      double u[N1];
+#pragma unroll
+      for (int k = 0; k < N1; ++k) u[k] = row[k];
+      double* g = G + tL * PL + e * NPC + mL * N1;
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) acc = fma(a.sp.V[0][i][k], u[k], acc);
+        if (i == 0) acc = fma(a.sp.cL[0], hl, acc);
+        if (i == N1 - 1) acc = fma(a.sp.cR[0], hr, acc);
+        g[i] = acc;
+      }
+    }
+    __syncthreads();
+    // phase B: y-line at (t = tL, x = mL)
+    if (lineAB) {
+      const double* col = X + tL * PL + e * NPC + mL;
+      double* g = G + tL * PL + e * NPC + mL;
+      double u[N1];
+#pragma unroll
+      for (int k = 0; k < N1; ++k) u[k] = col[k * N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        double acc = g[i * N1];
+#pragma unroll
+        for (int k = 0; k < N1; ++k) acc = fma(a.sp.V[1][i][k], u[k], acc);
+        if (i == 0) acc = fma(a.sp.cL[1], yl, acc);
+        if (i == N1 - 1) acc = fma(a.sp.cR[1], yr, acc);
+        g[i * N1] = acc;
+      }
+    }
+    __syncthreads();
+    // phase C: t-line at node l
+    if (lineC) {
+      double x[NT], Gv[NT];
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        x[j] = X[j * PL + e * NPC + l];
+        Gv[j] = G[j * PL + e * NPC + l];
+      }
+      double* Rp = a.R + (long long)cell * NPC + l;
+#pragma unroll
+      for (int r = 0; r < NT; ++r) {
+        if (r >= a.n_out) break;
+        double acc = a.mx.c[r] * w;
+#pragma unroll
+        for (int j = 0; j < NT; ++j) {
+          acc = fma(a.mx.T[r][j], x[j], acc);
+          acc = fma(a.mx.S[r][j], Gv[j], acc);
+        }
+        Rp[r * ns] = acc;
+      }
+    }
+    __syncthreads();  // stage st and G free for reuse
+    xl = nxl;
+    xr = nxr;
+    yl = nyl;
+    yr = nyr;
+    w = nw;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // d = 3, N = 3, n_tau = 4: TMA-staged, register-tiled two-phase kernel
 // ---------------------------------------------------------------------------
 namespace fast {
@@ -767,6 +1091,55 @@ int launch1d(const SlabArgs& a, cudaStream_t s) {
   return 1;
 }
 
+int num_sms_cached() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int N1, int NT>
+int launch2d_t(const SlabArgs& a, cudaStream_t s) {
+  using Sh = Shape2d<N1, NT>;
+  using P = P2d<N1, NT>;
+  const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 && (a.g.n_sdof % 2) == 0;
+  if (a.g.n_cells % Sh::E == 0 && aligned && !std::getenv("STG_2D_NONPERSIST")) {
+    static int occ = -1;
+    if (occ < 0) {
+      cudaFuncSetAttribute(slab2d_persist<N1, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           P::SMEM);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_persist<N1, NT>, Sh::THREADS,
+                                                    P::SMEM);
+      if (occ < 1) occ = 1;
+    }
+    const int nseg = a.g.n_cells / Sh::E;
+    int grid = occ * num_sms_cached();
+    if (grid > nseg) grid = nseg;
+    slab2d_persist<N1, NT><<<grid, Sh::THREADS, P::SMEM, s>>>(a);
+    return 1;
+  }
+  const int blocks = (a.g.n_cells + Sh::E - 1) / Sh::E;
+  slab2d_kernel<N1, NT><<<blocks, Sh::THREADS, 0, s>>>(a);
+  return 1;
+}
+
+template <int N1>
+int launch2d_n(const SlabArgs& a, cudaStream_t s) {
+  switch (a.n_in) {
+    case 1: return launch2d_t<N1, 1>(a, s);
+    case 2: return launch2d_t<N1, 2>(a, s);
+    case 3: return launch2d_t<N1, 3>(a, s);
+    case 4: return launch2d_t<N1, 4>(a, s);
+    case 5: return launch2d_t<N1, 5>(a, s);
+    case 6: return launch2d_t<N1, 6>(a, s);
+    default: return -1;
+  }
+}
+
 template <int D, int N1>
 int launch_generic_t(const SlabArgs& a, cudaStream_t s) {
   using Sh = GenericShape<D, N1>;
@@ -815,6 +1188,16 @@ int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
     }
   }
   if (a.model != int(Model::advection)) return -1;
+  if (d == 2 && a.n_out <= a.n_in && !std::getenv("STG_GENERIC_2D")) {
+    switch (n1) {
+      case 2: return launch2d_n<2>(a, s);
+      case 3: return launch2d_n<3>(a, s);
+      case 4: return launch2d_n<4>(a, s);
+      case 5: return launch2d_n<5>(a, s);
+      case 6: return launch2d_n<6>(a, s);
+      default: return -1;
+    }
+  }
   if (d == 2) {
     switch (n1) {
       case 2: return launch_generic_t<2, 2>(a, s);
