@@ -395,11 +395,34 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     R1 = torch.empty_like(U1)
     us = 1e3 * timed(lambda: op1.st_residual(0.0, c1.dt, u1, U1, out=R1),
                      torch.cuda.current_stream(), torch, 1000)
+    # the same 1000 applies captured once in a CUDA graph and replayed: the
+    # device-side cost without Python/ctypes launch overhead
+    us_graph = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            op1.st_residual(0.0, c1.dt, u1, U1, out=R1)
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(1000):
+                    op1.st_residual(0.0, c1.dt, u1, U1, out=R1)
+        torch.cuda.current_stream().wait_stream(side)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        us_graph = e0.elapsed_time(e1)  # ms for 1000 applies = us per apply
+    except Exception as e:  # capture unsupported: report why
+        us_graph = f"unavailable: {e}"
     nc1 = NewtonConfig(abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12)
     op1.stdg_step(0.0, c1.dt, u1, nc1)
     t1, (_, _, info1) = _wall(torch, lambda: op1.stdg_step(0.0, c1.dt, u1, nc1))
-    out["c1"] = {"us_per_residual_python_loop": us, "slab_solve_s": t1,
-                 "gmres_iterations": info1.linear_iterations}
+    out["c1"] = {"us_per_residual_python_loop": us, "us_per_residual_cuda_graph": us_graph,
+                 "slab_solve_s": t1, "gmres_iterations": info1.linear_iterations}
     # c3: Burgers, inexact Newton-GMRES with FD J.v (eps 1e-7), 10 slabs
     c3 = C.CONFIGS["c3"]
     op3 = SlabOperator(**c3.kwargs())

@@ -75,6 +75,10 @@ struct SlabArgs {
   const double* U;  // linearisation point (jvp && burgers), n_in blocks
   const double* W;  // spatial vector or null
   double* R;        // n_out blocks
+  // fast 3-D path only: process 8-cell segments [seg_begin, seg_end) of the
+  // mesh (seg_end == 0: all).  Used by the pipelined host-buffer entry point.
+  int seg_begin;
+  int seg_end;
 };
 
 // ---- launchers (kernels_slab.cu) -------------------------------------------

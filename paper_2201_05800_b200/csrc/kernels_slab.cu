@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(fast::THREADS, 4)
   const int tid = threadIdx.x;
   const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
   const long long ns = a.g.n_sdof;
-  const int e0 = blockIdx.x * E;  // first cell of the pencil segment
+  const int e0 = (a.seg_begin + blockIdx.x) * E;  // first cell of the pencil segment
   const int cx0 = e0 % nx;
   const int cy = (e0 / nx) % ny;
   const int cz = e0 / (nx * ny);
@@ -917,7 +917,7 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
 
   const int tid = threadIdx.x;
   const long long ns = a.g.n_sdof;
-  const int nseg = a.g.n_cells / E;
+  const int nseg = a.seg_end > 0 ? a.seg_end : a.g.n_cells / E;
   const Need nd{a.sp.cL[0] != 0.0, a.sp.cR[0] != 0.0, a.sp.cL[1] != 0.0, a.sp.cR[1] != 0.0,
                 a.sp.cL[2] != 0.0, a.sp.cR[2] != 0.0, a.has_w != 0};
 
@@ -927,7 +927,7 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
     fast::fence_mbar_init();
   }
   __syncthreads();
-  int seg = blockIdx.x;
+  int seg = a.seg_begin + blockIdx.x;
   if (tid == 0 && seg < nseg) issue(maps, a, nd, seg, base, bar0);
 
   // thread identities of the two phases
@@ -1267,7 +1267,8 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
     const cuuint64_t gstride[3] = {128, 512, tstride};
     const cuuint32_t box[4] = {16, 4, fast::E, 4};
     if (!encode(enc, &map, a.X, 4, gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_128B)) return -1;
-    const int blocks = a.g.n_cells / fast::E;
+    const int blocks = (a.seg_end > 0 ? a.seg_end : a.g.n_cells / fast::E) - a.seg_begin;
+    if (blocks <= 0) return 0;
     if (a.full_s) {
       slab3d_n4_tma<true><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
     } else {
@@ -1309,7 +1310,8 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
                          pst::SMEM_BYTES);
     attr = true;
   }
-  const int nseg = a.g.n_cells / pst::E;
+  const int nseg = (a.seg_end > 0 ? a.seg_end : a.g.n_cells / pst::E) - a.seg_begin;
+  if (nseg <= 0) return 0;
   static int per_sm = [] {
     const char* e = std::getenv("STG_FAST_CTAS_PER_SM");
     const int v = e ? std::atoi(e) : 2;

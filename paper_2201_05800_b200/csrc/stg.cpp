@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -85,9 +86,20 @@ struct stg_handle {
   DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
+  // pipelined host-buffer path: copy-in / copy-out streams and chunk events
+  static constexpr int kChunks = 8;
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_in[kChunks] = {}, ev_c[kChunks] = {};
 
   ~stg_handle() {
     if (pinned) cudaFreeHost(pinned);
+    if (s_in) cudaStreamDestroy(s_in);
+    if (s_out) cudaStreamDestroy(s_out);
+    if (ev_start) cudaEventDestroy(ev_start);
+    for (int k = 0; k < kChunks; ++k) {
+      if (ev_in[k]) cudaEventDestroy(ev_in[k]);
+      if (ev_c[k]) cudaEventDestroy(ev_c[k]);
+    }
   }
 };
 
@@ -101,8 +113,11 @@ void check_launch(stg_handle* h) {
 
 // ---- operator dispatch ----------------------------------------------------
 void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
-           const double* U, const double* W, double* R, bool jvp, bool full_s) {
+           const double* U, const double* W, double* R, bool jvp, bool full_s,
+           int seg_begin = 0, int seg_end = 0) {
   stg::SlabArgs a{};
+  a.seg_begin = seg_begin;
+  a.seg_end = seg_end;
   a.sp = h->sp;
   a.mx = mx;
   a.g = h->g;
@@ -522,6 +537,83 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
   apply(h, mix, h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false, full);
   stg::vec_axpby(Jv, -1.0 / eps, h->tmp2.p, 1.0 / eps, n, h->stream);
   h->launches++;
+}
+
+// Host-buffer R(U) with the transfers pipelined against the compute (fast
+// 3-D path): the mesh is cut into K z-chunks; chunk k's H2D (U's n_tau
+// blocks and u_n) runs on s_in, its fast-kernel launch on the compute
+// stream once chunk k (and the periodic z-neighbour layer it reads) has
+// arrived, and its D2H on s_out right after.  PCIe is full duplex, so
+// in-bound, out-bound and compute overlap.  Returns false when the fast
+// kernel does not apply (the caller then runs the plain path).
+bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
+                                const double* U_host, double* R_host) {
+  const stg::Geometry& g = h->g;
+  if (h->kernel_pref == STG_KERNEL_GENERIC || g.dim != 3 || g.nz < 2) return false;
+  int K = stg_handle::kChunks;
+  while (K > 1 && g.nz % K) --K;
+  if (K < 2) return false;
+  const long long ns = h->n_sdof, nd = h->n_dof;
+  h->host_U.ensure(size_t(nd));
+  h->host_R.ensure(size_t(nd));
+  h->host_u.ensure(size_t(ns));
+  stg::SlabArgs a{};
+  a.sp = h->sp;
+  a.mx = st_mix(h, dt, true);
+  a.g = g;
+  a.n_in = a.n_out = h->nt;
+  a.has_w = 1;
+  a.model = h->desc.model;
+  a.X = h->host_U.p;
+  a.W = h->host_u.p;
+  a.R = h->host_R.p;
+  if (!stg::slab_fast_supported(a)) return false;
+  if (!h->s_in) {
+    ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event");
+    for (int k = 0; k < stg_handle::kChunks; ++k) {
+      ck(cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&h->ev_c[k], cudaEventDisableTiming), "event");
+    }
+  }
+  const int L = g.nz / K;                              // z-layers per chunk
+  const long long layer = (long long)g.nx * g.ny * g.npc;  // doubles per layer per block
+  const int seg_per_layer = g.nx * g.ny / 8;
+  const bool needL = h->sp.cL[2] != 0.0, needR = h->sp.cR[2] != 0.0;
+  // earlier work on the compute stream may still read the device buffers
+  ck(cudaEventRecord(h->ev_start, h->stream), "event");
+  ck(cudaStreamWaitEvent(h->s_in, h->ev_start, 0), "wait");
+  const size_t pitch = sizeof(double) * size_t(ns);  // one temporal block
+  auto copy_layers = [&](int z0, int nl) {
+    const long long off = z0 * layer, cnt = nl * layer;
+    // one strided copy moves the chunk's slice of all n_tau blocks
+    ck(cudaMemcpy2DAsync(h->host_U.p + off, pitch, U_host + off, pitch, sizeof(double) * cnt,
+                         size_t(h->nt), cudaMemcpyHostToDevice, h->s_in), "H2D");
+    ck(cudaMemcpyAsync(h->host_u.p + off, un_host + off, sizeof(double) * cnt,
+                       cudaMemcpyHostToDevice, h->s_in), "H2D");
+  };
+  if (needL) copy_layers(g.nz - 1, 1);  // periodic z- neighbour of chunk 0
+  for (int k = 0; k < K; ++k) {
+    copy_layers(k * L, L);
+    ck(cudaEventRecord(h->ev_in[k], h->s_in), "event");
+  }
+  for (int k = 0; k < K; ++k) {
+    ck(cudaStreamWaitEvent(h->stream, h->ev_in[needR ? std::min(k + 1, K - 1) : k], 0), "wait");
+    a.seg_begin = k * L * seg_per_layer;
+    a.seg_end = (k + 1) * L * seg_per_layer;
+    if (stg::launch_slab_fast(a, h->stream) < 0)
+      throw std::runtime_error("fast kernel launch failed in the pipelined path");
+    h->launches++;
+    check_launch(h);
+    ck(cudaEventRecord(h->ev_c[k], h->stream), "event");
+    ck(cudaStreamWaitEvent(h->s_out, h->ev_c[k], 0), "wait");
+    const long long off = k * L * layer, cnt = L * layer;
+    ck(cudaMemcpy2DAsync(R_host + off, pitch, h->host_R.p + off, pitch, sizeof(double) * cnt,
+                         size_t(h->nt), cudaMemcpyDeviceToHost, h->s_out), "D2H");
+  }
+  ck(cudaStreamSynchronize(h->s_out), "sync");
+  return true;
 }
 
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
@@ -1003,6 +1095,8 @@ int stg_st_residual_host(stg_handle* h, double t_n, double dt, const double* u_n
     need(U, "U");
     need(R, "R");
     (void)t_n;
+    if (!std::getenv("STG_HOST_NO_PIPELINE") && st_residual_host_pipelined(h, dt, u_n, U, R))
+      return;
     h->host_U.ensure(size_t(h->n_dof));
     h->host_R.ensure(size_t(h->n_dof));
     h->host_u.ensure(size_t(h->n_sdof));

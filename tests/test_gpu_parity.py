@@ -186,8 +186,12 @@ def test_fast_and_generic_kernels_agree_full_c4():
     assert rel(a, b.cpu().numpy()) <= 1e-13
 
 
-def test_host_buffer_variant_matches_device():
-    cfg = C.CONFIGS["c4"].scaled((8, 8, 8))
+@pytest.mark.parametrize("cfg", [
+    C.CONFIGS["c4"].scaled((8, 8, 8)),
+    make(3, 3, 4, (16, 8, 6), (-0.7, 0.4, -1.1)),      # z-downwind neighbours: pipelined waits
+    make(3, 2, 3, (6, 5, 4), (1.0, 1.0, 1.0)),         # generic kernel: plain host path
+], ids=["c4small", "negvel", "generic"])
+def test_host_buffer_variant_matches_device(cfg):
     op = SlabOperator(**cfg.kwargs())
     U, un = C.random_slab(cfg), C.initial_state(cfg)
     a = op.st_residual_host(0.0, cfg.dt, un, U)
