@@ -625,6 +625,9 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t phase) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1, int c2, int c3) {
   asm volatile(
@@ -839,6 +842,38 @@ constexpr int FA_OFF = 2 * STAGE;
 constexpr int BAR_OFF = FA_OFF + MAIN;
 constexpr int SMEM_BYTES = BAR_OFF + 64 + 1024;
 
+// Runtime stage layout: only the trace buffers the velocity signs need (for
+// b > 0: y-, z- faces and the x- halo), so that three CTAs fit per SM.
+struct Layout {
+  int yl, yr, zl, zr, hl, hr;  // byte offsets within a stage (-1: not loaded)
+  int stage;                   // bytes per stage (1024-aligned)
+  int fa;                      // FA buffer offset
+  int bar;                     // mbarrier offset
+  int smem;                    // dynamic shared memory to request
+};
+
+inline Layout make_layout(bool lx, bool rx, bool ly, bool ry, bool lz, bool rz) {
+  Layout L{};
+  int off = MAIN;
+  auto take = [&](bool need, int bytes) {
+    if (!need) return -1;
+    const int o = off;
+    off += bytes;
+    return o;
+  };
+  L.yl = take(ly, FACE);
+  L.yr = take(ry, FACE);
+  L.zl = take(lz, FACE);
+  L.zr = take(rz, FACE);
+  L.hl = take(lx, HALO);
+  L.hr = take(rx, HALO);
+  L.stage = ((off + 1023) / 1024) * 1024;
+  L.fa = 2 * L.stage;
+  L.bar = L.fa + MAIN;
+  L.smem = L.bar + 64 + 1024;
+  return L;
+}
+
 struct Maps {
   CUtensorMap main;   // 4-D {16, 4, cells, 4}, box {16, 4, E, 4}, swizzle 128B
   CUtensorMap yface;  // 5-D {4, 4, 4, cells, 4}, box {4, 1, 4, E, 4}
@@ -872,8 +907,9 @@ struct Need {
 };
 
 // Issue every TMA of segment `seg` into the stage at `sbase` (one thread).
-__device__ __forceinline__ void issue(const Maps& m, const SlabArgs& a, const Need& nd, int seg,
-                                      unsigned char* sbase, uint32_t bar) {
+__device__ __forceinline__ void issue(const Maps& m, const SlabArgs& a, const Need& nd,
+                                      const Layout& L, int seg, unsigned char* sbase,
+                                      uint32_t bar) {
   const int nx = a.g.nx, ny = a.g.ny, nz = a.g.nz;
   const int e0 = seg * E;
   const int cx0 = e0 % nx, cy = (e0 / nx) % ny, cz = e0 / (nx * ny);
@@ -882,28 +918,27 @@ __device__ __forceinline__ void issue(const Maps& m, const SlabArgs& a, const Ne
   bytes += nd.ry ? FACE : 0;
   bytes += nd.lz ? FACE : 0;
   bytes += nd.rz ? FACE : 0;
-  bytes += nd.w ? WBUF : 0;
   bytes += nd.lx ? HALO : 0;
   bytes += nd.rx ? HALO : 0;
   fast::mbar_expect_tx(bar, bytes);
   const uint32_t s = fast::smem_u32(sbase);
-  fast::tma_load_4d(s, &m.main, bar, 0, 0, e0, 0);
-  if (nd.ly) tma_load_5d(s + OFF_YL, &m.yface, bar, 0, 3, 0, e0 + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx, 0);
-  if (nd.ry) tma_load_5d(s + OFF_YR, &m.yface, bar, 0, 0, 0, e0 + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx, 0);
-  if (nd.lz) tma_load_5d(s + OFF_ZL, &m.zface, bar, 0, 0, 3, e0 + ((cz == 0 ? nz - 1 : cz - 1) - cz) * nx * ny, 0);
-  if (nd.rz) tma_load_5d(s + OFF_ZR, &m.zface, bar, 0, 0, 0, e0 + ((cz == nz - 1 ? 0 : cz + 1) - cz) * nx * ny, 0);
-  if (nd.w) tma_load_2d(s + OFF_W, &m.w, bar, 0, e0);
-  if (nd.lx) tma_load_5d(s + OFF_HL, &m.halo, bar, 2, 0, 0, e0 - cx0 + (cx0 == 0 ? nx - 1 : cx0 - 1), 0);
+  fast::tma_load_4d(s, &m.main, bar, 0, 0, e0, 0);  // rows [t][cell][z]
+  if (nd.ly) tma_load_5d(s + L.yl, &m.yface, bar, 0, 3, 0, e0 + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx, 0);
+  if (nd.ry) tma_load_5d(s + L.yr, &m.yface, bar, 0, 0, 0, e0 + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx, 0);
+  if (nd.lz) tma_load_5d(s + L.zl, &m.zface, bar, 0, 0, 3, e0 + ((cz == 0 ? nz - 1 : cz - 1) - cz) * nx * ny, 0);
+  if (nd.rz) tma_load_5d(s + L.zr, &m.zface, bar, 0, 0, 0, e0 + ((cz == nz - 1 ? 0 : cz + 1) - cz) * nx * ny, 0);
+  if (nd.lx) tma_load_5d(s + L.hl, &m.halo, bar, 2, 0, 0, e0 - cx0 + (cx0 == 0 ? nx - 1 : cx0 - 1), 0);
   if (nd.rx) {
     const int cxe = cx0 + E - 1;
-    tma_load_5d(s + OFF_HR, &m.halo, bar, 0, 0, 0, e0 - cx0 + (cxe == nx - 1 ? 0 : cxe + 1), 0);
+    tma_load_5d(s + L.hr, &m.halo, bar, 0, 0, 0, e0 - cx0 + (cxe == nx - 1 ? 0 : cxe + 1), 0);
   }
 }
 }  // namespace pst
 
 template <bool FULL_S>
-__global__ void __launch_bounds__(pst::THREADS, 2)
-    slab3d_n4_persist(const __grid_constant__ pst::Maps maps, const SlabArgs a) {
+__global__ void __launch_bounds__(pst::THREADS, 3)
+    slab3d_n4_persist(const __grid_constant__ pst::Maps maps, const SlabArgs a,
+                      const pst::Layout lay) {
   using namespace pst;
   using fast::row_of;
   using fast::swz;
@@ -911,9 +946,10 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
   // align to 1024 B (128B-swizzle atoms) by integer offset so the pointer
   // keeps its shared-memory provenance (LDS/STS, not generic LD/ST)
   unsigned char* base = smem_raw + ((1024u - (fast::smem_u32(smem_raw) & 1023u)) & 1023u);
-  double* FA = reinterpret_cast<double*>(base + FA_OFF);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(base + BAR_OFF);
+  double* FA = reinterpret_cast<double*>(base + lay.fa);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + lay.bar);
   const uint32_t bar0 = fast::smem_u32(bars), bar1 = fast::smem_u32(bars + 1);
+  const int STG = lay.stage;
 
   const int tid = threadIdx.x;
   const long long ns = a.g.n_sdof;
@@ -928,30 +964,49 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
   }
   __syncthreads();
   int seg = a.seg_begin + blockIdx.x;
-  if (tid == 0 && seg < nseg) issue(maps, a, nd, seg, base, bar0);
+  if (tid == 0 && seg < nseg) issue(maps, a, nd, lay, seg, base, bar0);
 
-  // thread identities of the two phases
+  // thread identities of the two phases.  (A warp-decoupled variant -- each
+  // warp owning two cells in both phases, __syncwarp between them and
+  // per-warp `empty` mbarriers instead of the CTA barriers -- measured 36 us
+  // vs 29.7 us: the producer's empty-wait delays the next segment's TMA.)
+  auto rowc = [](int t, int e, int z) { return (t * E + e) * 4 + z; };
   const int zA = tid & 3, eA = (tid >> 2) & (E - 1), tA = tid >> 5;
   const int xB = tid & 3, yB = (tid >> 2) & 3, eB = tid >> 4;
   const int qB = yB * 4 + xB;
+  // u_n (the W term) is prefetched into registers one segment ahead
+  double w[4] = {0, 0, 0, 0};
+  if (nd.w && seg < nseg) {
+    const double* p = a.W + (long long)(seg * E + eB) * 64 + qB;
+#pragma unroll
+    for (int z = 0; z < 4; ++z) w[z] = __ldcs(p + 16 * z);
+  }
 
   for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
     const int st = it & 1;
-    unsigned char* sb = base + st * STAGE;
+    unsigned char* sb = base + st * STG;
     const double* Xs = reinterpret_cast<const double*>(sb);
+    const int nxt = seg + gridDim.x;
     if (tid == 0) {
-      const int nxt = seg + gridDim.x;
       if (nxt < nseg) {
+        // stage st^1 was last read in iteration it-1, which ended with a CTA
+        // barrier
         fence_proxy_async();
-        issue(maps, a, nd, nxt, base + (st ^ 1) * STAGE, st ? bar0 : bar1);
+        issue(maps, a, nd, lay, nxt, base + (st ^ 1) * STG, st ? bar0 : bar1);
       }
+    }
+    double wn[4] = {0, 0, 0, 0};
+    if (nd.w && nxt < nseg) {
+      const double* p = a.W + (long long)(nxt * E + eB) * 64 + qB;
+#pragma unroll
+      for (int z = 0; z < 4; ++z) wn[z] = __ldcs(p + 16 * z);
     }
     while (!fast::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
 
     // ---- phase A: x and y derivatives of the (y,x) plane at (t, e, z) -----
     {
-      const int row = row_of(tA, eA, zA);
+      const int row = rowc(tA, eA, zA);
       const int sw = row & 7;
       double u[16];
 #pragma unroll
@@ -964,35 +1019,35 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
       double yl[4] = {0, 0, 0, 0}, yr[4] = {0, 0, 0, 0};
       if (nd.lx) {
         if (eA > 0) {
-          const int rl = row_of(tA, eA - 1, zA);
+          const int rl = rowc(tA, eA - 1, zA);
 #pragma unroll
           for (int y = 0; y < 4; ++y) hl[y] = Xs[swz(rl, 4 * y + 3)];
         } else {
-          const double* H = reinterpret_cast<const double*>(sb + OFF_HL) + (tA * 4 + zA) * 8;
+          const double* H = reinterpret_cast<const double*>(sb + lay.hl) + (tA * 4 + zA) * 8;
 #pragma unroll
           for (int y = 0; y < 4; ++y) hl[y] = H[2 * y + 1];
         }
       }
       if (nd.rx) {
         if (eA < E - 1) {
-          const int rr = row_of(tA, eA + 1, zA);
+          const int rr = rowc(tA, eA + 1, zA);
 #pragma unroll
           for (int y = 0; y < 4; ++y) hr[y] = Xs[swz(rr, 4 * y)];
         } else {
-          const double* H = reinterpret_cast<const double*>(sb + OFF_HR) + (tA * 4 + zA) * 8;
+          const double* H = reinterpret_cast<const double*>(sb + lay.hr) + (tA * 4 + zA) * 8;
 #pragma unroll
           for (int y = 0; y < 4; ++y) hr[y] = H[2 * y];
         }
       }
       const int fo = ((tA * E + eA) * 4 + zA) * 4;
       if (nd.ly) {
-        const double* Y = reinterpret_cast<const double*>(sb + OFF_YL) + fo;
+        const double* Y = reinterpret_cast<const double*>(sb + lay.yl) + fo;
         const double2 v0 = *reinterpret_cast<const double2*>(Y);
         const double2 v1 = *reinterpret_cast<const double2*>(Y + 2);
         yl[0] = v0.x; yl[1] = v0.y; yl[2] = v1.x; yl[3] = v1.y;
       }
       if (nd.ry) {
-        const double* Y = reinterpret_cast<const double*>(sb + OFF_YR) + fo;
+        const double* Y = reinterpret_cast<const double*>(sb + lay.yr) + fo;
         const double2 v0 = *reinterpret_cast<const double2*>(Y);
         const double2 v1 = *reinterpret_cast<const double2*>(Y + 2);
         yr[0] = v0.x; yr[1] = v0.y; yr[2] = v1.x; yr[3] = v1.y;
@@ -1029,25 +1084,20 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
       for (int t = 0; t < 4; ++t)
 #pragma unroll
         for (int z = 0; z < 4; ++z) {
-          const int o = swz(row_of(t, eB, z), qB);
+          const int o = swz(rowc(t, eB, z), qB);
           u[t][z] = Xs[o];
           f[t][z] = FA[o];
         }
-      double zl[4] = {0, 0, 0, 0}, zr[4] = {0, 0, 0, 0}, w[4] = {0, 0, 0, 0};
+      double zl[4] = {0, 0, 0, 0}, zr[4] = {0, 0, 0, 0};
       if (nd.lz) {
-        const double* Z = reinterpret_cast<const double*>(sb + OFF_ZL) + eB * 16 + qB;
+        const double* Z = reinterpret_cast<const double*>(sb + lay.zl) + eB * 16 + qB;
 #pragma unroll
         for (int t = 0; t < 4; ++t) zl[t] = Z[t * E * 16];
       }
       if (nd.rz) {
-        const double* Z = reinterpret_cast<const double*>(sb + OFF_ZR) + eB * 16 + qB;
+        const double* Z = reinterpret_cast<const double*>(sb + lay.zr) + eB * 16 + qB;
 #pragma unroll
         for (int t = 0; t < 4; ++t) zr[t] = Z[t * E * 16];
-      }
-      if (nd.w) {
-        const double* W = reinterpret_cast<const double*>(sb + OFF_W) + eB * 64 + qB;
-#pragma unroll
-        for (int z = 0; z < 4; ++z) w[z] = W[16 * z];
       }
 #pragma unroll
       for (int t = 0; t < 4; ++t)
@@ -1077,7 +1127,9 @@ __global__ void __launch_bounds__(pst::THREADS, 2)
           Rb[r * ns + 16 * z] = acc;
         }
     }
-    __syncthreads();
+#pragma unroll
+    for (int z = 0; z < 4; ++z) w[z] = wn[z];
+    __syncthreads();  // stage st and FA free for reuse
   }
 }
 
@@ -1278,6 +1330,9 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   }
   pst::Maps m;
   {
+    // dims {yx (16), z (4), cell, t}: [t][cell][z] rows of 128 B, so each
+    // TMA streams 4 KB contiguous runs per temporal block (a cell-outermost
+    // box, [cell][t][z], measured 36 us vs 30 us: 512 B runs)
     const cuuint64_t gdim[4] = {16, 4, cells, 4};
     const cuuint64_t gstride[3] = {128, 512, tstride};
     const cuuint32_t box[4] = {16, 4, pst::E, 4};
@@ -1293,17 +1348,12 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
     if (!encode(enc, &m.zface, a.X, 5, gdim, gstride, bz, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
     if (!encode(enc, &m.halo, a.X, 5, gdim, gstride, bh, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
   }
-  if (a.has_w) {
-    if (reinterpret_cast<uintptr_t>(a.W) & 15) return -1;
-    const cuuint64_t gdim[2] = {64, cells};
-    const cuuint64_t gstride[1] = {512};
-    const cuuint32_t box[2] = {64, pst::E};
-    if (!encode(enc, &m.w, a.W, 2, gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
-  } else {
-    m.w = m.main;  // unused
-  }
+  m.w = m.main;  // u_n is prefetched into registers (no TMA box)
+  const pst::Layout lay =
+      pst::make_layout(a.sp.cL[0] != 0.0, a.sp.cR[0] != 0.0, a.sp.cL[1] != 0.0,
+                       a.sp.cR[1] != 0.0, a.sp.cL[2] != 0.0, a.sp.cR[2] != 0.0);
   static bool attr = false;
-  if (!attr) {
+  if (!attr) {  // the largest layout (every trace buffer) bounds the request
     cudaFuncSetAttribute(slab3d_n4_persist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          pst::SMEM_BYTES);
     cudaFuncSetAttribute(slab3d_n4_persist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1312,17 +1362,25 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   }
   const int nseg = (a.seg_end > 0 ? a.seg_end : a.g.n_cells / pst::E) - a.seg_begin;
   if (nseg <= 0) return 0;
-  static int per_sm = [] {
+  int occ = 0;
+  if (a.full_s)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab3d_n4_persist<true>, pst::THREADS,
+                                                  lay.smem);
+  else
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab3d_n4_persist<false>, pst::THREADS,
+                                                  lay.smem);
+  static int per_sm_cap = [] {
     const char* e = std::getenv("STG_FAST_CTAS_PER_SM");
-    const int v = e ? std::atoi(e) : 2;
-    return v < 1 ? 1 : (v > 2 ? 2 : v);
+    return e ? std::atoi(e) : 3;
   }();
-  int grid = per_sm * num_sms();
+  if (occ > per_sm_cap) occ = per_sm_cap;
+  if (occ < 1) occ = 1;
+  int grid = occ * num_sms();
   if (grid > nseg) grid = nseg;
   if (a.full_s) {
-    slab3d_n4_persist<true><<<grid, pst::THREADS, pst::SMEM_BYTES, s>>>(m, a);
+    slab3d_n4_persist<true><<<grid, pst::THREADS, lay.smem, s>>>(m, a, lay);
   } else {
-    slab3d_n4_persist<false><<<grid, pst::THREADS, pst::SMEM_BYTES, s>>>(m, a);
+    slab3d_n4_persist<false><<<grid, pst::THREADS, lay.smem, s>>>(m, a, lay);
   }
   return 1;
 }
