@@ -64,8 +64,10 @@ extern "C" {
  * defaults to a diagonal preconditioner (newton.hpp:69); point Jacobi stalls
  * on these Jacobians, so the block versions are provided:
  *   TBLOCK  temporal-block Jacobi (n_tau x n_tau per spatial node, advection)
- *   EBLOCK  element-block Jacobi (exact element-local block, d = 1)
- *   AUTO    EBLOCK for d = 1, TBLOCK otherwise. */
+ *   EBLOCK  element-block Jacobi (exact inverse of the element-local block:
+ *           d = 1 dense; d = 3 advection, degree 3, n_tau = 4, cells % 8 == 0
+ *           by fast diagonalisation)
+ *   AUTO    EBLOCK where supported, else TBLOCK (advection) / none. */
 #define STG_PRECOND_NONE 0
 #define STG_PRECOND_TBLOCK 1
 #define STG_PRECOND_EBLOCK 2
@@ -179,6 +181,11 @@ int stg_stage_jvp(stg_handle* h, int form, double t, double dt, const double* U,
 int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const double* b,
                  double* x, int restart, double tol, int max_it, int precond, int* iterations,
                  double* rel_residual);
+
+/* The right preconditioner gmres_st would use, applied once: out = P^-1 in
+ * (P = block-Jacobi part of the slab Jacobian at U; n_dof vectors). */
+int stg_st_precond_apply(stg_handle* h, double dt, const double* U, int precond,
+                         const double* in, double* out);
 
 /* stdg_step (stdg.hpp:120-143): Newton from 1 (x) u_n; U (n_dof) receives the
  * slab solution, u_next (n_sdof) its last temporal block. */

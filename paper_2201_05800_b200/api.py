@@ -227,6 +227,15 @@ class SlabOperator:
                    ctypes.byref(it), ctypes.byref(rr))
         return x, it.value, rr.value
 
+    def st_precond_apply(self, dt: float, v, U=None, precond: int = L.STG_PRECOND_AUTO,
+                         out=None):
+        """out = P^-1 v for the block-Jacobi right preconditioner gmres_st uses."""
+        out = self._new(self.n_dof) if out is None else out
+        Up = _ptr(U, self.n_dof, "U") if U is not None else None
+        self._call(self._lib.stg_st_precond_apply, float(dt), Up, int(precond),
+                   _ptr(v, self.n_dof, "in"), _ptr(out, self.n_dof, "out"))
+        return out
+
     def _step(self, fn, head, u, cfg, U, u_next, what):
         cfg = cfg or NewtonConfig()
         U = self._new(self.n_dof) if U is None else U

@@ -88,6 +88,24 @@ int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
 bool slab_fast_supported(const SlabArgs& a);
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s);
 
+// ---- element-block Jacobi by fast diagonalisation, d = 3 N = 3 n_tau = 4
+// (kernels_fdm.cu).  Complex entries are stored [re, im]; x eigen-indices are
+// kept for one member of each conjugate pair (kx = 2j, j = 0, 1).
+struct FdmCoef {
+  double FX[2][4][2];        // rows 0, 2 of Px^-1
+  double FY[4][4][2];        // Py^-1
+  double FZ[4][4][2];        // Pz^-1
+  double FT[4][4][2];        // Q^-1 S^-1
+  double IT[4][4][2];        // Q
+  double IZ[4][4][2];        // Pz
+  double IY[4][4][2];        // Py
+  double IX[4][2][2];        // columns 0, 2 of Px
+  double LI[4][4][4][2][2];  // 1 / (lt[it] + thz[iz] + thy[iy] + thx[2j])
+};
+bool fdm_supported(const Geometry& g, int n_tau);
+int launch_precond_fdm(const FdmCoef& c, const Geometry& g, const double* in, double* out,
+                       cudaStream_t s);
+
 // ---- block-Jacobi preconditioners (kernels_precond.cu) ----------------------
 // out[t][cell][k] = sum_j minv[k][t][j] in[j][cell][k]   (npc class tables)
 void precond_tblock(double* out, const double* in, const double* minv, int nt, int npc,

@@ -1,0 +1,285 @@
+// Element-block Jacobi for the d = 3, N = 3, n_tau = 4 slab / stage
+// Jacobians by fast diagonalisation (FDM).
+//
+// The element-local block of J = T (x) I + S (x) F (advection; F's
+// neighbour couplings removed) is L_e = (S (x) I)(G (x) I + I (x) K) with
+// G = S^-1 T and K = V_z (+) V_y (+) V_x (Kronecker sum of the per-axis 4x4
+// element matrices, own-face terms included).  With G = Q Lt Q^-1 and
+// V_a = P_a Th_a P_a^-1 (complex, host eig.hpp):
+//   L_e^-1 = (Q (x) Pz (x) Py (x) Px) diag(1/(lt + thz + thy + thx))
+//            (Q^-1 S^-1 (x) Pz^-1 (x) Py^-1 (x) Px^-1).
+// The input is real, so the spectrum is conjugate-symmetric and only the
+// x-eigen-indices {0, 2} (one of each conjugate pair) are kept: the data stays
+// 256 doubles per cell and the last inverse mode is 2 Re(.).  Cost ~15k FMA
+// per cell (a dense 256 x 256 inverse would be 65k) in three phases:
+//   A : forward x and y modes on the (y,x) plane at (t, cell, z)
+//   B : forward z, t modes, the 1/Lambda scaling, inverse t, z modes on the
+//       (t,z) tile at (iy, j)
+//   A': inverse y and x modes, coalesced store
+// The input tile arrives by TMA (the operator's 128B-swizzled 4-D box) in a
+// 2-stage ring; coefficient matrices are kernel parameters read as
+// constant-bank operands.  Exactness is tested against the dense inverse.
+#include <cuda.h>
+
+#include <cstdlib>
+
+#include "kernels.hpp"
+#include "ptx.cuh"
+
+namespace stg {
+namespace {
+
+constexpr int E = 8;
+constexpr int THREADS = 128;
+constexpr int TILE = 16384;
+constexpr int OFF_B1 = 2 * TILE;
+constexpr int OFF_LI = 3 * TILE;
+constexpr int OFF_BAR = OFF_LI + 2048;
+constexpr int SMEM = OFF_BAR + 64 + 1024;
+
+__device__ __forceinline__ int row_of(int t, int e, int z) { return (t * E + e) * 4 + z; }
+
+// complex helpers on (re, im) pairs
+struct C2 {
+  double r, i;
+};
+__device__ __forceinline__ void cmac(C2& acc, double ar, double ai, const C2& b) {
+  acc.r = fma(ar, b.r, fma(-ai, b.i, acc.r));
+  acc.i = fma(ar, b.i, fma(ai, b.r, acc.i));
+}
+
+__global__ void __launch_bounds__(THREADS, 3)
+    fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ FdmCoef c,
+               const Geometry g, double* __restrict__ out) {
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (ptxh::smem_u32(smem_raw) & 1023u)) & 1023u);
+  double* B1 = reinterpret_cast<double*>(base + OFF_B1);
+  double* LI = reinterpret_cast<double*>(base + OFF_LI);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + OFF_BAR);
+  const uint32_t bar0 = ptxh::smem_u32(bars), bar1 = ptxh::smem_u32(bars + 1);
+  const int tid = threadIdx.x;
+  const long long ns = g.n_sdof;
+  const int nseg = g.n_cells / E;
+
+  for (int q = tid; q < 4 * 4 * 4 * 2 * 2; q += THREADS)
+    LI[q] = (&c.LI[0][0][0][0][0])[q];
+  if (tid == 0) {
+    ptxh::mbar_init(bar0, 1);
+    ptxh::mbar_init(bar1, 1);
+    ptxh::fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int seg, int st) {
+    const uint32_t bar = st ? bar1 : bar0;
+    ptxh::mbar_expect_tx(bar, TILE);
+    ptxh::tma_load_4d(ptxh::smem_u32(base + st * TILE), &tm, bar, 0, 0, seg * E, 0);
+  };
+  int seg = blockIdx.x;
+  if (tid == 0 && seg < nseg) issue(seg, 0);
+
+  const int zA = tid & 3, eA = (tid >> 2) & (E - 1), tA = tid >> 5;
+  const int rowA = row_of(tA, eA, zA), swA = rowA & 7;
+  const int eB = tid >> 3, qB = tid & 7, iyB = qB >> 1, jB = qB & 1;
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int st = it & 1;
+    const double* Xs = reinterpret_cast<const double*>(base + st * TILE);
+    if (tid == 0 && seg + (int)gridDim.x < nseg) {
+      ptxh::fence_proxy_async_smem();
+      issue(seg + gridDim.x, st ^ 1);
+    }
+    while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+
+    // ---- phase A: forward x (kept eigen-indices j -> kx = 2j) and y modes --
+    {
+      double r[16];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const double2 v = *reinterpret_cast<const double2*>(Xs + rowA * 16 + ((q ^ swA) << 1));
+        r[2 * q] = v.x;
+        r[2 * q + 1] = v.y;
+      }
+      C2 a[4][2];
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            re = fma(c.FX[j][x][0], r[4 * y + x], re);
+            im = fma(c.FX[j][x][1], r[4 * y + x], im);
+          }
+          a[y][j] = {re, im};
+        }
+#pragma unroll
+      for (int iy = 0; iy < 4; ++iy)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          C2 b = {0.0, 0.0};
+#pragma unroll
+          for (int y = 0; y < 4; ++y) cmac(b, c.FY[iy][y][0], c.FY[iy][y][1], a[y][j]);
+          const int q = iy * 2 + j;
+          *reinterpret_cast<double2*>(B1 + rowA * 16 + ((q ^ swA) << 1)) = make_double2(b.r, b.i);
+        }
+    }
+    __syncthreads();
+
+    // ---- phase B: (t,z) tile at (iy, j): forward z, t; scale; inverse t, z -
+    if (tid < 64) {
+      C2 u[4][4];  // [t][z]
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          const int row = row_of(t, eB, z);
+          const double2 v = *reinterpret_cast<const double2*>(B1 + row * 16 + ((qB ^ (row & 7)) << 1));
+          u[t][z] = {v.x, v.y};
+        }
+      // every mode product runs in place on u with a 4-entry temporary
+      // (keeps phase B at one 16-entry complex tile: no register spills)
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {  // forward z
+        C2 s[4];
+#pragma unroll
+        for (int iz = 0; iz < 4; ++iz) {
+          s[iz] = {0.0, 0.0};
+#pragma unroll
+          for (int z = 0; z < 4; ++z) cmac(s[iz], c.FZ[iz][z][0], c.FZ[iz][z][1], u[t][z]);
+        }
+#pragma unroll
+        for (int iz = 0; iz < 4; ++iz) u[t][iz] = s[iz];
+      }
+#pragma unroll
+      for (int iz = 0; iz < 4; ++iz) {  // forward t (S^-1 folded), 1/Lambda, inverse t
+        C2 s[4];
+#pragma unroll
+        for (int it2 = 0; it2 < 4; ++it2) {
+          C2 a = {0.0, 0.0};
+#pragma unroll
+          for (int t = 0; t < 4; ++t) cmac(a, c.FT[it2][t][0], c.FT[it2][t][1], u[t][iz]);
+          const double2 l = *reinterpret_cast<const double2*>(
+              LI + ((((it2 * 4 + iz) * 4 + iyB) * 2 + jB) << 1));
+          s[it2] = {a.r * l.x - a.i * l.y, a.r * l.y + a.i * l.x};
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          C2 a = {0.0, 0.0};
+#pragma unroll
+          for (int it2 = 0; it2 < 4; ++it2) cmac(a, c.IT[t][it2][0], c.IT[t][it2][1], s[it2]);
+          u[t][iz] = a;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)  // inverse z, store
+#pragma unroll
+        for (int z = 0; z < 4; ++z) {
+          C2 s = {0.0, 0.0};
+#pragma unroll
+          for (int iz = 0; iz < 4; ++iz) cmac(s, c.IZ[z][iz][0], c.IZ[z][iz][1], u[t][iz]);
+          const int row = row_of(t, eB, z);
+          *reinterpret_cast<double2*>(B1 + row * 16 + ((qB ^ (row & 7)) << 1)) =
+              make_double2(s.r, s.i);
+        }
+    }
+    __syncthreads();
+
+    // ---- phase A': inverse y, inverse x (2 Re), store ----------------------
+    {
+      C2 h[4][2];
+#pragma unroll
+      for (int iy = 0; iy < 4; ++iy)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int q = iy * 2 + j;
+          const double2 v = *reinterpret_cast<const double2*>(B1 + rowA * 16 + ((q ^ swA) << 1));
+          h[iy][j] = {v.x, v.y};
+        }
+      double o[16];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        C2 m[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          C2 s = {0.0, 0.0};
+#pragma unroll
+          for (int iy = 0; iy < 4; ++iy) cmac(s, c.IY[y][iy][0], c.IY[y][iy][1], h[iy][j]);
+          m[j] = s;
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x) {
+          double re = 0.0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            re = fma(c.IX[x][j][0], m[j].r, fma(-c.IX[x][j][1], m[j].i, re));
+          o[4 * y + x] = 2.0 * re;
+        }
+      }
+      double* op = out + tA * ns + (long long)(seg * E + eA) * 64 + zA * 16;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<double2*>(op + 2 * q) = make_double2(o[2 * q], o[2 * q + 1]);
+    }
+    __syncthreads();  // stage st and B1 free for reuse
+  }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool fdm_supported(const Geometry& g, int n_tau) {
+  return g.dim == 3 && g.n1 == 4 && n_tau == 4 && g.n_cells % E == 0 &&
+         encode_fn() != nullptr;
+}
+
+int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in, double* out,
+                       cudaStream_t s) {
+  EncodeFn enc = encode_fn();
+  if (!enc || (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return -1;
+  CUtensorMap map;
+  const cuuint64_t gdim[4] = {16, 4, cuuint64_t(g.n_cells), 4};
+  const cuuint64_t gstride[3] = {128, 512, cuuint64_t(g.n_sdof) * 8};
+  const cuuint32_t box[4] = {16, 4, E, 4};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(in), gdim, gstride, box,
+          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(fdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fdm_kernel, THREADS, SMEM);
+    if (occ < 1) occ = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nseg = g.n_cells / E;
+  int grid = occ * sms;
+  if (grid > nseg) grid = nseg;
+  fdm_kernel<<<grid, THREADS, SMEM, s>>>(map, coef, g, out);
+  return 1;
+}
+
+}  // namespace stg

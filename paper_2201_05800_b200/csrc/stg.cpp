@@ -17,6 +17,7 @@
 
 #include "../../include/stg_cuda.h"
 #include "constants.hpp"
+#include "eig.hpp"
 #include "kernels.hpp"
 
 namespace {
@@ -646,13 +647,85 @@ void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double
   }
 }
 
+// Fast-diagonalisation factors of the d = 3 element-local Jacobian block
+// L_e = T (x) I + S (x) (V_z (+) V_y (+) V_x) (kernels_fdm.cu).  False when
+// S is singular or a factor has no accurate eigen-decomposition of the form
+// the kernel assumes (V_x: two complex-conjugate pairs).
+bool build_fdm(const stg::SpatialCoef& sp, const stg::MixCoef& mx, stg::FdmCoef& c) {
+  using stg::cplx;
+  constexpr int n = 4;
+  try {
+    std::vector<double> S(n * n), T(n * n);
+    for (int r = 0; r < n; ++r)
+      for (int j = 0; j < n; ++j) {
+        S[size_t(r) * n + j] = mx.S[r][j];
+        T[size_t(r) * n + j] = mx.T[r][j];
+      }
+    const std::vector<double> Si = stg::inverse(S, n);
+    std::vector<double> G(n * n, 0.0);
+    for (int r = 0; r < n; ++r)
+      for (int j = 0; j < n; ++j)
+        for (int q = 0; q < n; ++q) G[size_t(r) * n + j] += Si[size_t(r) * n + q] * T[size_t(q) * n + j];
+    std::vector<cplx> lt, Q, Qi, th[3], P[3], Pi[3];
+    if (!stg::eig_real(G, n, lt, Q, Qi)) return false;
+    for (int a = 0; a < 3; ++a) {
+      std::vector<double> V(n * n);
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) V[size_t(i) * n + k] = sp.V[a][i][k];
+      if (!stg::eig_real(V, n, th[a], P[a], Pi[a])) return false;
+    }
+    // x modes: keep one member of each conjugate pair (0, 2)
+    for (int j = 0; j < 2; ++j)
+      if (!(th[0][size_t(2 * j)].imag() > 0.0) ||
+          th[0][size_t(2 * j + 1)] != std::conj(th[0][size_t(2 * j)]))
+        return false;
+    auto put = [](double* dst, cplx z) {
+      dst[0] = z.real();
+      dst[1] = z.imag();
+    };
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) {
+        cplx ft = 0.0;
+        for (int m = 0; m < n; ++m) ft += Qi[size_t(r) * n + m] * Si[size_t(m) * n + q];
+        put(c.FT[r][q], ft);
+        put(c.IT[r][q], Q[size_t(r) * n + q]);
+        put(c.FZ[r][q], Pi[2][size_t(r) * n + q]);
+        put(c.IZ[r][q], P[2][size_t(r) * n + q]);
+        put(c.FY[r][q], Pi[1][size_t(r) * n + q]);
+        put(c.IY[r][q], P[1][size_t(r) * n + q]);
+      }
+    for (int j = 0; j < 2; ++j)
+      for (int x = 0; x < n; ++x) {
+        put(c.FX[j][x], Pi[0][size_t(2 * j) * n + x]);
+        put(c.IX[x][j], P[0][size_t(x) * n + 2 * j]);
+      }
+    for (int it = 0; it < n; ++it)
+      for (int iz = 0; iz < n; ++iz)
+        for (int iy = 0; iy < n; ++iy)
+          for (int j = 0; j < 2; ++j) {
+            const cplx lam = lt[size_t(it)] + th[2][size_t(iz)] + th[1][size_t(iy)] + th[0][size_t(2 * j)];
+            if (std::abs(lam) < 1e-300) return false;
+            put(c.LI[it][iz][iy][j], 1.0 / lam);
+          }
+    return true;
+  } catch (const std::exception&) {
+    return false;
+  }
+}
+
+bool fdm_ok(const stg_handle* h) {
+  return h->desc.dim == 3 && h->desc.model == STG_MODEL_ADVECTION && stg::fdm_supported(h->g, h->nt);
+}
+
 int resolve_precond(const stg_handle* h, int kind) {
   if (kind == STG_PRECOND_AUTO)
-    return h->desc.dim == 1 ? STG_PRECOND_EBLOCK
-                            : (h->desc.model == STG_MODEL_ADVECTION ? STG_PRECOND_TBLOCK
-                                                                    : STG_PRECOND_NONE);
-  if (kind == STG_PRECOND_EBLOCK && h->desc.dim != 1)
-    throw std::invalid_argument("element-block Jacobi: d = 1 only");
+    return (h->desc.dim == 1 || fdm_ok(h))
+               ? STG_PRECOND_EBLOCK
+               : (h->desc.model == STG_MODEL_ADVECTION ? STG_PRECOND_TBLOCK : STG_PRECOND_NONE);
+  if (kind == STG_PRECOND_EBLOCK && h->desc.dim != 1 && !fdm_ok(h))
+    throw std::invalid_argument(
+        "element-block Jacobi: d = 1, or d = 3 advection with degree 3, n_tau = 4 and a cell "
+        "count divisible by 8");
   if (kind == STG_PRECOND_TBLOCK && h->desc.model != STG_MODEL_ADVECTION)
     throw std::invalid_argument("temporal-block Jacobi: advection only");
   if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_AUTO)
@@ -688,6 +761,18 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream);
       h->launches++;
     };
+  }
+  if (d == 3) {  // element-block Jacobi by fast diagonalisation
+    stg::FdmCoef c;
+    if (build_fdm(h->sp, mx, c))
+      return [h, c](const double* in, double* out) {
+        if (stg::launch_precond_fdm(c, h->g, in, out, h->stream) < 0)
+          throw std::runtime_error("element-block preconditioner launch failed");
+        h->launches++;
+      };
+    if (h->desc.model != STG_MODEL_ADVECTION)
+      throw std::invalid_argument("element-block Jacobi: no factorisation");
+    return make_precond(h, STG_PRECOND_TBLOCK, mx, U);  // spectrum not of the FDM form
   }
   // element-block Jacobi, d = 1: block (r,i),(j,q) of the element-local Jacobian
   const int nb = nt * n1;
@@ -1062,6 +1147,25 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     if (!st.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
                                fmt_short(st.rel_residual));
+  });
+}
+
+int stg_st_precond_apply(stg_handle* h, double dt, const double* U, int precond,
+                         const double* in, double* out) {
+  return guarded(h, [&] {
+    need(h, "stg_st_precond_apply");
+    need(in, "in");
+    need(out, "out");
+    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
+    if (P) {
+      P(in, out);
+      check_launch(h);
+    } else {
+      stg::vec_copy(out, in, h->n_dof, h->stream);
+      h->launches++;
+      check_launch(h);
+    }
   });
 }
 

@@ -262,7 +262,7 @@ def test_burgers_newton_vs_oracle():
 
 
 @pytest.mark.parametrize("name,cells,pcs", [
-    ("c4", (8, 8, 8), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK]),
+    ("c4", (8, 8, 8), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK]),
     ("c2", (16, 16), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK]),
     ("c1", (64,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
     ("c3", (256,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
@@ -279,8 +279,48 @@ def test_preconditioners_same_solution_fewer_iterations(name, cells, pcs):
         U, u1, info = op.stdg_step(0.0, dt, un, nc)
         sols.append(U.cpu().numpy())
         its.append(info.linear_iterations)
-    assert rel(sols[1], sols[0]) <= TOL_SOLVE
-    assert its[1] < its[0], its
+    for i in range(1, len(pcs)):
+        assert rel(sols[i], sols[0]) <= TOL_SOLVE
+        assert its[i] < its[i - 1], its
+
+
+@pytest.mark.parametrize("velocity", [(1.0, 1.0, 1.0), (-0.7, 0.4, -1.1)])
+def test_fdm_element_block_is_exact_local_inverse(velocity):
+    """d = 3 EBLOCK (fast diagonalisation, kernels_fdm.cu) = the exact inverse
+    of the element-local Jacobian block, which is read off the oracle's J.v
+    (columns supported on one element; 2 x 2 x 2 periodic mesh)."""
+    cfg = make(3, 3, 4, (2, 2, 2), velocity, dt=0.02)
+    op, pr = pair(cfg)
+    ns, npc, nt = op.n_sdof, 64, 4
+    loc = np.array([t * ns + k for t in range(nt) for k in range(npc)])  # element 0
+    Lblk = np.zeros((nt * npc, nt * npc))
+    U0 = np.zeros(nt * ns)
+    for c, i in enumerate(loc):
+        e = np.zeros(nt * ns)
+        e[i] = 1.0
+        Lblk[:, c] = pr.st_jvp(0.0, cfg.dt, U0, e)[loc]
+    x = np.random.default_rng(5).standard_normal(nt * ns)
+    y = op.st_precond_apply(cfg.dt, dev(x), precond=L.STG_PRECOND_EBLOCK).cpu().numpy()
+    for cell in range(8):
+        idx = loc + cell * npc
+        ref = np.linalg.solve(Lblk, x[idx])
+        assert rel(y[idx], ref) <= 1e-11, cell
+    ya = op.st_precond_apply(cfg.dt, dev(x)).cpu().numpy()  # AUTO picks it
+    assert np.array_equal(ya, y)
+
+
+def test_fdm_eblock_stage_solves():
+    cfg = C.CONFIGS["c5"].scaled((8, 8, 8))
+    op = SlabOperator(**cfg.kwargs())
+    un = dev(C.initial_state(cfg))
+    for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
+        res = []
+        for pc in (L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK):
+            nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-13, gmres_tol=1e-14, precond=pc)
+            U, _, info = op.rk_step(form, 0.0, cfg.dt, un, nc)
+            res.append((U.cpu().numpy(), info.linear_iterations))
+        assert rel(res[1][0], res[0][0]) <= TOL_SOLVE
+        assert res[1][1] < res[0][1], (form, res[0][1], res[1][1])
 
 
 def test_preconditioned_stage_solve_matches_slab():
