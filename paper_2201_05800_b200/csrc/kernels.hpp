@@ -131,11 +131,11 @@ void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s)
 void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s);
 // U_j = u for j < nb (1 (x) u, stdg.hpp:131)
 void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t s);
-// out[j] = <V_j, w>, j < k (V_j = V + j*ldv); partial buffer >= grid*k doubles
+// out[j] = <V_j, w>, j < k <= 64 (V_j = V + j*ldv); partial buffer >= grid*k doubles
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
                   double* partial, double* out, cudaStream_t s);
-// w = (w - sum_{j<k} h[j] V_j) * s (h on device), then out2[j] = <V_j, w> (if
-// dots) and out2[k] = <w,w>; partial buffer >= grid*(k+1).  s = 1 unless
+// w = (w - sum_{j<k} h[j] V_j) * s (h on device), then out2[k] = <w,w> and,
+// if want_dots, out2[j] = <V_j, w> (an extra pass); partial buffer >= grid*(k+1).  s = 1 unless
 // scale_src = [h_0..h_{k-1}, <w,w>] is given: then s = 1/sqrt(<w,w> - sum h^2)
 // (Pythagorean norm of the projected vector), written to scale_out[0].
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
@@ -144,9 +144,9 @@ void vec_update_dot(double* w, const double* V, long long ldv, int k, const doub
 // y = x / sqrt(*nrm2)  (nrm2 on device)
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
                        cudaStream_t s);
-// x += sum_{j<k} y[j] V_j (y on device)
+// x = (accumulate ? x : 0) + sum_{j<k} y[j] V_j (y on device), k <= 64
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
-                 cudaStream_t s);
+                 cudaStream_t s, bool accumulate = true);
 // *out = max |x_i|
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s);
 // *out = <x,y>

@@ -14,7 +14,7 @@
 // per cell (a dense 256 x 256 inverse would be 65k) in three phases:
 //   A : forward x and y modes on the (y,x) plane at (t, cell, z)
 //   B : forward z, t modes, the 1/Lambda scaling, inverse t, z modes on the
-//       (t,z) tile at (iy, j)
+//       (t,z) tile at (iy, j), split over two threads (columns, then rows)
 //   A': inverse y and x modes, coalesced store
 // The input tile arrives by TMA (the operator's 128B-swizzled 4-D box) in a
 // 2-stage ring; coefficient matrices are kernel parameters read as
@@ -48,7 +48,60 @@ __device__ __forceinline__ void cmac(C2& acc, double ar, double ai, const C2& b)
   acc.i = fma(ar, b.i, fma(ai, b.r, acc.i));
 }
 
-__global__ void __launch_bounds__(THREADS, 3)
+__device__ __forceinline__ double2* tile_at(double* B1, int t, int e, int z, int q) {
+  const int row = row_of(t, e, z);
+  return reinterpret_cast<double2*>(B1 + row * 16 + ((q ^ (row & 7)) << 1));
+}
+
+// Phase B, first part, for half H of the (t,z) tile of unit (e, q = (iy, j)):
+// forward z for the z-eigen-columns iz = 2H, 2H+1, then the t modes
+// (Q^-1 S^-1, 1/Lambda, Q) on those columns.  Templated so the coefficient
+// indices stay compile-time constants (H is warp-uniform).
+template <int H>
+__device__ __forceinline__ void phase_b_cols(const FdmCoef& c, double* B1, const double* LI,
+                                             int e, int q, C2 (&w)[4][2]) {
+  const int iy = q >> 1, j = q & 1;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    C2 u[4];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const double2 v = *tile_at(B1, t, e, z, q);
+      u[z] = {v.x, v.y};
+    }
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      C2 s = {0.0, 0.0};
+#pragma unroll
+      for (int z = 0; z < 4; ++z) cmac(s, c.FZ[2 * H + k][z][0], c.FZ[2 * H + k][z][1], u[z]);
+      w[t][k] = s;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int iz = 2 * H + k;
+    C2 s[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      C2 a = {0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cmac(a, c.FT[it][t][0], c.FT[it][t][1], w[t][k]);
+      const double2 l =
+          *reinterpret_cast<const double2*>(LI + ((((it * 4 + iz) * 4 + iy) * 2 + j) << 1));
+      s[it] = {a.r * l.x - a.i * l.y, a.r * l.y + a.i * l.x};
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      C2 a = {0.0, 0.0};
+#pragma unroll
+      for (int it = 0; it < 4; ++it) cmac(a, c.IT[t][it][0], c.IT[t][it][1], s[it]);
+      w[t][k] = a;
+    }
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
     fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ FdmCoef c,
                const Geometry g, double* __restrict__ out) {
   extern __shared__ unsigned char smem_raw[];
@@ -79,7 +132,10 @@ __global__ void __launch_bounds__(THREADS, 3)
 
   const int zA = tid & 3, eA = (tid >> 2) & (E - 1), tA = tid >> 5;
   const int rowA = row_of(tA, eA, zA), swA = rowA & 7;
-  const int eB = tid >> 3, qB = tid & 7, iyB = qB >> 1, jB = qB & 1;
+  // phase B: tile unit = (cell, iy, j); the two halves of a unit sit in
+  // different warps so the half index is warp-uniform
+  const int hB = (tid >> 5) & 1, uB = (tid & 31) | ((tid >> 6) << 5);
+  const int eB = uB >> 3, qB = uB & 7;
 
   for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
     const int st = it & 1;
@@ -126,62 +182,44 @@ __global__ void __launch_bounds__(THREADS, 3)
     }
     __syncthreads();
 
-    // ---- phase B: (t,z) tile at (iy, j): forward z, t; scale; inverse t, z -
-    if (tid < 64) {
-      C2 u[4][4];  // [t][z]
+    // ---- phase B: (t,z) tile at (iy, j), two threads per tile ------------
+    {
+      C2 w[4][2];  // [t][k]: z-eigen-column 2 hB + k
+      if (hB)
+        phase_b_cols<1>(c, B1, LI, eB, qB, w);
+      else
+        phase_b_cols<0>(c, B1, LI, eB, qB, w);
+      __syncthreads();  // both halves have read the tile
 #pragma unroll
       for (int t = 0; t < 4; ++t)
 #pragma unroll
-        for (int z = 0; z < 4; ++z) {
-          const int row = row_of(t, eB, z);
-          const double2 v = *reinterpret_cast<const double2*>(B1 + row * 16 + ((qB ^ (row & 7)) << 1));
-          u[t][z] = {v.x, v.y};
-        }
-      // every mode product runs in place on u with a 4-entry temporary
-      // (keeps phase B at one 16-entry complex tile: no register spills)
+        for (int k = 0; k < 2; ++k)
+          *tile_at(B1, t, eB, 2 * hB + k, qB) = make_double2(w[t][k].r, w[t][k].i);
+      __syncthreads();
+      // inverse z on rows t = 2 hB, 2 hB + 1 (all four columns)
+      C2 o[2][4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {  // forward z
-        C2 s[4];
+      for (int tt = 0; tt < 2; ++tt) {
+        C2 m[4];
 #pragma unroll
         for (int iz = 0; iz < 4; ++iz) {
-          s[iz] = {0.0, 0.0};
-#pragma unroll
-          for (int z = 0; z < 4; ++z) cmac(s[iz], c.FZ[iz][z][0], c.FZ[iz][z][1], u[t][z]);
+          const double2 v = *tile_at(B1, 2 * hB + tt, eB, iz, qB);
+          m[iz] = {v.x, v.y};
         }
-#pragma unroll
-        for (int iz = 0; iz < 4; ++iz) u[t][iz] = s[iz];
-      }
-#pragma unroll
-      for (int iz = 0; iz < 4; ++iz) {  // forward t (S^-1 folded), 1/Lambda, inverse t
-        C2 s[4];
-#pragma unroll
-        for (int it2 = 0; it2 < 4; ++it2) {
-          C2 a = {0.0, 0.0};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) cmac(a, c.FT[it2][t][0], c.FT[it2][t][1], u[t][iz]);
-          const double2 l = *reinterpret_cast<const double2*>(
-              LI + ((((it2 * 4 + iz) * 4 + iyB) * 2 + jB) << 1));
-          s[it2] = {a.r * l.x - a.i * l.y, a.r * l.y + a.i * l.x};
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          C2 a = {0.0, 0.0};
-#pragma unroll
-          for (int it2 = 0; it2 < 4; ++it2) cmac(a, c.IT[t][it2][0], c.IT[t][it2][1], s[it2]);
-          u[t][iz] = a;
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < 4; ++t)  // inverse z, store
 #pragma unroll
         for (int z = 0; z < 4; ++z) {
           C2 s = {0.0, 0.0};
 #pragma unroll
-          for (int iz = 0; iz < 4; ++iz) cmac(s, c.IZ[z][iz][0], c.IZ[z][iz][1], u[t][iz]);
-          const int row = row_of(t, eB, z);
-          *reinterpret_cast<double2*>(B1 + row * 16 + ((qB ^ (row & 7)) << 1)) =
-              make_double2(s.r, s.i);
+          for (int iz = 0; iz < 4; ++iz) cmac(s, c.IZ[z][iz][0], c.IZ[z][iz][1], m[iz]);
+          o[tt][z] = s;
         }
+      }
+      __syncthreads();  // every column read before the results overwrite them
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+        for (int z = 0; z < 4; ++z)
+          *tile_at(B1, 2 * hB + tt, eB, z, qB) = make_double2(o[tt][z].r, o[tt][z].i);
     }
     __syncthreads();
 
@@ -266,10 +304,17 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
+  // 3 CTAs/SM (144 registers, no spills) by default; STG_FDM_MINB=4 trades a
+  // small spill for a fourth CTA
+  static const bool four = [] {
+    const char* e = std::getenv("STG_FDM_MINB");
+    return e && std::atoi(e) == 4;
+  }();
+  auto kern = four ? fdm_kernel<4> : fdm_kernel<3>;
   static int occ = -1;
   if (occ < 0) {
-    cudaFuncSetAttribute(fdm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fdm_kernel, THREADS, SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, SMEM);
     if (occ < 1) occ = 1;
   }
   int dev = 0, sms = 148;
@@ -278,7 +323,7 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
   const int nseg = g.n_cells / E;
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
-  fdm_kernel<<<grid, THREADS, SMEM, s>>>(map, coef, g, out);
+  kern<<<grid, THREADS, SMEM, s>>>(map, coef, g, out);
   return 1;
 }
 

@@ -1,12 +1,16 @@
 // HBM-bound Krylov vector kernels (GMRES inner products, norms, axpys) with
 // deterministic reductions: the grid size is a fixed function of n, every
-// block reduces its slice in a fixed order, and a single block finishes the
-// reduction in a fixed order.  No atomics, so results are bitwise
-// reproducible run to run.
+// block reduces its slice in a fixed order, and the last block to finish (the
+// only atomic is its completion counter) sums the block partials in block
+// order.  Results are bitwise reproducible run to run.
 //
-// These replace the vector work inside Eigen::GMRES (newton.hpp:68-77) with a
-// classical Gram-Schmidt Arnoldi whose passes are fused: one multi-dot pass,
-// one "update + re-dot" pass (CGS2), one "update + norm" pass.
+// These replace the vector work inside Eigen::GMRES (newton.hpp:68-77): the
+// Arnoldi step is one multi-dot pass ([V^T w, <w,w>]) and one fused
+// project + Pythagorean-normalise + norm pass (stg.cpp, gmres).
+#include <algorithm>
+#include <cstdint>
+#include <stdexcept>
+
 #include "kernels.hpp"
 
 namespace stg {
@@ -86,84 +90,114 @@ __global__ void k_scale_invsqrt(double* y, const double* x, const double* nrm2, 
     y[i] = x[i] * s;
 }
 
-// ---- multi-vector kernels: block = 8 warps x 32 lanes.  Warp g owns basis
-// vectors j = g, g+8, g+16, ... (MPW of them); per iteration the block covers
-// kU = 8 slots of 32 consecutive elements (lane l of slot u owns element
-// base + 32u + l), so every thread keeps MPW*kU independent loads in flight.
-// Every V_j entry is loaded once per pass and kept in a register for the
-// second half of a fused pass; the cross-warp sum of slot u is done by warp u
-// (balanced), in a fixed order.
-constexpr int kWarps = 8;
-constexpr int kMultiBlock = 32 * kWarps;
-constexpr int kU = 8;
-constexpr int kTile = 32 * kU;
+// ---- multi-vector kernels: thread-per-chunk.  Each thread owns W
+// consecutive elements (W = 2: one 16-byte load per vector) in a grid-stride
+// loop and walks the basis vectors in groups of 8, so a thread keeps up to 9
+// independent loads in flight and every element of every vector is loaded
+// exactly once per pass.  Block partials are reduced warp-wise in a fixed
+// order; the grid depends only on n, so sums are reproducible.
+constexpr int kGroup = 8;
+constexpr int kVecBlock = 256;
 
-int multi_grid(long long n) {
-  long long g = (n + kTile - 1) / kTile;
-  if (g < 1) g = 1;
-  if (g > 148 * 4) g = 148 * 4;
-  return int(g);
+template <int W>
+struct VecT;
+template <>
+struct VecT<1> {
+  using T = double;
+  __device__ static T ld(const double* p, long long i) { return __ldcs(p + i); }
+  __device__ static void st(double* p, long long i, T v) { __stcs(p + i, v); }
+  __device__ static double dot(T a, T b, double acc) { return fma(a, b, acc); }
+  __device__ static T axpy(double a, T x, T y) { return fma(a, x, y); }
+  __device__ static T scale(T x, double s) { return x * s; }
+  __device__ static T zero() { return 0.0; }
+};
+template <>
+struct VecT<2> {
+  using T = double2;
+  __device__ static T ld(const double* p, long long i) {
+    return __ldcs(reinterpret_cast<const double2*>(p) + i);
+  }
+  __device__ static void st(double* p, long long i, T v) {
+    __stcs(reinterpret_cast<double2*>(p) + i, v);
+  }
+  __device__ static double dot(T a, T b, double acc) { return fma(a.x, b.x, fma(a.y, b.y, acc)); }
+  __device__ static T axpy(double a, T x, T y) { return make_double2(fma(a, x.x, y.x), fma(a, x.y, y.y)); }
+  __device__ static T scale(T x, double s) { return make_double2(x.x * s, x.y * s); }
+  __device__ static T zero() { return make_double2(0.0, 0.0); }
+};
+
+// Block-reduce acc[0..cnt) (cnt <= KMAX + 1) into part[blockIdx.x*cnt + j];
+// the last block sums the partials into out[0..cnt).
+template <int NACC>
+__device__ __forceinline__ void reduce_out(const double (&acc)[NACC], int cnt, double* part,
+                                           double* out, unsigned* counter) {
+  __shared__ double red[kVecBlock / 32][NACC];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < NACC; ++j) {
+    if (j < cnt) {
+      const double s = warp_sum(acc[j]);
+      if (lane == 0) red[wp][j] = s;
+    }
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < cnt; j += kVecBlock) {
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < kVecBlock / 32; ++q) s += red[q][j];
+    part[(size_t)blockIdx.x * cnt + j] = s;
+  }
+  if (is_last_block(counter)) block_finish_sum(part, gridDim.x, cnt, out, counter);
 }
 
-// part[b*k + j] = block partial of <V_j, w>
-template <int MPW>
-__global__ void __launch_bounds__(kMultiBlock) k_multidot(const double* __restrict__ V,
-                                                          long long ldv, int k,
-                                                          const double* __restrict__ w,
-                                                          long long n, double* part,
-                                                          double* out, unsigned* counter) {
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  double acc[MPW];
+// out[j] = <V_j, w>, j < k <= KMAX
+template <int KMAX, int W>
+__global__ void __launch_bounds__(kVecBlock) k_multidot(const double* __restrict__ V,
+                                                        long long ldv, int k,
+                                                        const double* __restrict__ w,
+                                                        long long nw, double* part,
+                                                        double* out, unsigned* counter) {
+  using O = VecT<W>;
+  const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
+  double acc[KMAX];
 #pragma unroll
-  for (int m = 0; m < MPW; ++m) acc[m] = 0.0;
-  for (long long base = (long long)blockIdx.x * kTile; base < n;
-       base += (long long)gridDim.x * kTile) {
-    double wv[kU];
+  for (int j = 0; j < KMAX; ++j) acc[j] = 0.0;
+  for (long long i = blockIdx.x * (long long)kVecBlock + threadIdx.x; i < nw;
+       i += (long long)gridDim.x * kVecBlock) {
+    const typename O::T x = O::ld(w, i);
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const long long i = base + 32 * u + lane;
-      wv[u] = i < n ? w[i] : 0.0;
-    }
+    for (int g = 0; g < KMAX; g += kGroup) {
+      if (g < kk) {
+        typename O::T v[kGroup];
 #pragma unroll
-    for (int m = 0; m < MPW; ++m) {
-      const int j = g + kWarps * m;
-      if (j < k) {
-        const double* Vj = V + j * ldv;
+        for (int q = 0; q < kGroup; ++q)
+          v[q] = (g + q < KMAX && g + q < kk) ? O::ld(V + (g + q) * ldv, i) : O::zero();
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const long long i = base + 32 * u + lane;
-          if (i < n) acc[m] = fma(Vj[i], wv[u], acc[m]);
-        }
+        for (int q = 0; q < kGroup; ++q)
+          if (g + q < KMAX) acc[g + q] = O::dot(v[q], x, acc[g + q]);
       }
     }
   }
-#pragma unroll
-  for (int m = 0; m < MPW; ++m) {
-    const int j = g + kWarps * m;
-    const double s = warp_sum(acc[m]);
-    if (lane == 0 && j < k) part[(size_t)blockIdx.x * k + j] = s;
-  }
-  if (is_last_block(counter)) block_finish_sum(part, gridDim.x, k, out, counter);
+  reduce_out(acc, kk, part, out, counter);
 }
 
-// w += sign * sum_j h_j V_j; optionally dots <V_j, w_new>; always <w_new, w_new>.
-// part[b*(k+1) + j], j < k dots (0 if !dots), j = k norm^2 (part may be null).
-template <int MPW>
-__global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
-                                                        const double* __restrict__ V,
-                                                        long long ldv, int k,
-                                                        const double* __restrict__ h,
-                                                        long long n, int dots, double sign,
-                                                        double* part,
-                                                        const double* __restrict__ scale_src,
-                                                        double* scale_out, double* out,
-                                                        unsigned* counter) {
-  __shared__ double red[kWarps][kU][32];
-  __shared__ double wnew[kU][32];
-  __shared__ double hs[kWarps * MPW];
+// w = (accumulate ? w : 0) + sign * sum_{j<k} h_j V_j, times s = 1 or the
+// Pythagorean scale from scale_src; out[0] = <w_new, w_new> (part may be
+// null: no reduction).
+template <int KMAX, int W>
+__global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
+                                                      const double* __restrict__ V,
+                                                      long long ldv, int k,
+                                                      const double* __restrict__ h, long long nw,
+                                                      double sign, int accumulate, double* part,
+                                                      const double* __restrict__ scale_src,
+                                                      double* scale_out, double* out,
+                                                      unsigned* counter) {
+  using O = VecT<W>;
+  const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
+  __shared__ double hs[KMAX];
   __shared__ double sc;
-  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
-  for (int j = threadIdx.x; j < kWarps * MPW; j += blockDim.x) hs[j] = j < k ? h[j] : 0.0;
+  for (int j = threadIdx.x; j < KMAX; j += kVecBlock) hs[j] = j < k ? sign * h[j] : 0.0;
   if (threadIdx.x == 0) {
     // scale_src = [h_0..h_{k-1}, <w,w>]: normalise by the Pythagorean norm
     // sqrt(<w,w> - sum h_j^2) of the projected vector (fallback: ||w||)
@@ -180,73 +214,31 @@ __global__ void __launch_bounds__(kMultiBlock) k_update(double* __restrict__ w,
   }
   __syncthreads();
   const double s = sc;
-  double acc[MPW];
+  double hr[KMAX];  // registers: a generic store to w could alias hs
 #pragma unroll
-  for (int m = 0; m < MPW; ++m) acc[m] = 0.0;
-  double nrm = 0.0;
-  for (long long base = (long long)blockIdx.x * kTile; base < n;
-       base += (long long)gridDim.x * kTile) {
-    double v[MPW][kU];
-    double p[kU];
+  for (int j = 0; j < KMAX; ++j) hr[j] = hs[j];
+  double acc[1] = {0.0};
+  for (long long i = blockIdx.x * (long long)kVecBlock + threadIdx.x; i < nw;
+       i += (long long)gridDim.x * kVecBlock) {
+    typename O::T x = accumulate ? O::ld(w, i) : O::zero();
 #pragma unroll
-    for (int u = 0; u < kU; ++u) p[u] = 0.0;
+    for (int g = 0; g < KMAX; g += kGroup) {
+      if (g < kk) {
+        typename O::T v[kGroup];
 #pragma unroll
-    for (int m = 0; m < MPW; ++m) {
-      const int j = g + kWarps * m;
-      const double hj = hs[j];
-      const double* Vj = V + j * ldv;
+        for (int q = 0; q < kGroup; ++q)
+          v[q] = (g + q < KMAX && g + q < kk) ? O::ld(V + (g + q) * ldv, i) : O::zero();
 #pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const long long i = base + 32 * u + lane;
-        v[m][u] = (j < k && i < n) ? Vj[i] : 0.0;
-        p[u] = fma(hj, v[m][u], p[u]);
+        for (int q = 0; q < kGroup; ++q)
+          if (g + q < KMAX) x = O::axpy(hr[g + q], v[q], x);
       }
     }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) red[g][u][lane] = p[u];
-    __syncthreads();
-    {
-      // warp g finishes slot u = g
-      const long long i = base + 32 * g + lane;
-      double sum = 0.0;
-#pragma unroll
-      for (int q = 0; q < kWarps; ++q) sum += red[q][g][lane];
-      double wi = 0.0;
-      if (i < n) {
-        wi = fma(sign, sum, w[i]) * s;
-        w[i] = wi;
-      }
-      wnew[g][lane] = wi;
-      nrm = fma(wi, wi, nrm);
-    }
-    __syncthreads();
-    if (dots) {
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const double wi = wnew[u][lane];
-#pragma unroll
-        for (int m = 0; m < MPW; ++m) acc[m] = fma(v[m][u], wi, acc[m]);
-      }
-    }
+    x = O::scale(x, s);
+    O::st(w, i, x);
+    acc[0] = O::dot(x, x, acc[0]);
   }
   if (part == nullptr) return;
-  __shared__ double nr[kWarps];
-#pragma unroll
-  for (int m = 0; m < MPW; ++m) {
-    const int j = g + kWarps * m;
-    const double s = warp_sum(acc[m]);
-    if (lane == 0 && j < k) part[(size_t)blockIdx.x * (k + 1) + j] = dots ? s : 0.0;
-  }
-  const double sn = warp_sum(nrm);
-  if (lane == 0) nr[g] = sn;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-#pragma unroll
-    for (int q = 0; q < kWarps; ++q) t += nr[q];
-    part[(size_t)blockIdx.x * (k + 1) + k] = t;
-  }
-  if (is_last_block(counter)) block_finish_sum(part, gridDim.x, k + 1, out, counter);
+  reduce_out(acc, 1, part, out, counter);
 }
 
 __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x, long long n,
@@ -307,20 +299,28 @@ void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long
   k_scale_invsqrt<<<grid_for(n), kBlock, 0, s>>>(y, x, nrm2, n);
 }
 
-#define STG_DISPATCH_MPW(k, CALL)        \
-  if ((k) <= 8) {                        \
-    constexpr int MPW = 1;               \
-    CALL;                                \
-  } else if ((k) <= 16) {                \
-    constexpr int MPW = 2;               \
-    CALL;                                \
-  } else if ((k) <= 32) {                \
-    constexpr int MPW = 4;               \
-    CALL;                                \
-  } else {                               \
-    constexpr int MPW = 8;               \
-    CALL;                                \
+namespace {
+
+// Grid: enough blocks to fill every SM to the kernel's occupancy (so the
+// loads in flight cover HBM latency at small k), fewer for short vectors.
+// A fixed function of (n, kernel): reductions stay reproducible.  One cache
+// per instantiation; at most kPartialDoubles / 80 blocks.
+template <int KM, int WW, bool UPD>
+int multi_grid(long long n) {
+  static int cap = 0;
+  if (cap == 0) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (UPD)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<KM, WW>, kVecBlock, 0);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_multidot<KM, WW>, kVecBlock, 0);
+    cap = std::max(1, std::min(per_sm * sms, int(kPartialDoubles / 80)));
   }
+  long long g = (n / WW + kVecBlock - 1) / kVecBlock;
+  return int(std::max(1LL, std::min(g, (long long)cap)));
+}
 
 // The completion counter lives right after the partial-sum area (see
 // kPartialDoubles in kernels.hpp); it is zero between launches.
@@ -328,30 +328,74 @@ unsigned* counter_of(double* partial) {
   return reinterpret_cast<unsigned*>(partial + kPartialDoubles);
 }
 
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// W = 2 (16-byte accesses) when n, ldv and every base pointer allow it
+int vec_width(long long n, long long ldv, const void* a, const void* b) {
+  return (n % 2 == 0 && ldv % 2 == 0 && aligned16(a) && aligned16(b)) ? 2 : 1;
+}
+
+// k <= 8: exact-k instantiations (no predicated lanes in the loop); above:
+// runtime k up to KMAX = 16, 32, 64
+#define STG_KSWITCH(k, CALL)                                 \
+  switch (k) {                                               \
+    case 1: { constexpr int KM = 1; CALL; } break;           \
+    case 2: { constexpr int KM = 2; CALL; } break;           \
+    case 3: { constexpr int KM = 3; CALL; } break;           \
+    case 4: { constexpr int KM = 4; CALL; } break;           \
+    case 5: { constexpr int KM = 5; CALL; } break;           \
+    case 6: { constexpr int KM = 6; CALL; } break;           \
+    case 7: { constexpr int KM = 7; CALL; } break;           \
+    case 8: { constexpr int KM = 8; CALL; } break;           \
+    default:                                                 \
+      if ((k) <= 16) { constexpr int KM = 16; CALL; }        \
+      else if ((k) <= 32) { constexpr int KM = 32; CALL; }   \
+      else { constexpr int KM = 64; CALL; }                  \
+  }
+
+#define STG_DISPATCH_K(k, W, CALL)                                                \
+  do {                                                                            \
+    if ((k) < 1 || (k) > 64) throw std::invalid_argument("multi-vector kernels: 1 <= k <= 64"); \
+    if ((W) == 2) {                                                               \
+      constexpr int WW = 2;                                                       \
+      STG_KSWITCH(k, CALL)                                                        \
+    } else {                                                                      \
+      constexpr int WW = 1;                                                       \
+      STG_KSWITCH(k, CALL)                                                        \
+    }                                                                             \
+  } while (0)
+
+}  // namespace
+
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
                   double* partial, double* out, cudaStream_t s) {
-  const int g = multi_grid(n);
+  const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
-  STG_DISPATCH_MPW(k, (k_multidot<MPW><<<g, kMultiBlock, 0, s>>>(V, ldv, k, w, n, partial, out,
-                                                                 c)));
+  STG_DISPATCH_K(k, W, (k_multidot<KM, WW><<<multi_grid<KM, WW, false>(n), kVecBlock,
+                                              0, s>>>(V, ldv, k, w, n / WW, partial, out, c)));
 }
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
                     const double* scale_src, double* scale_out) {
-  const int g = multi_grid(n);
+  const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
-  STG_DISPATCH_MPW(k, (k_update<MPW><<<g, kMultiBlock, 0, s>>>(w, V, ldv, k, h, n, want_dots,
-                                                               -1.0, partial, scale_src,
-                                                               scale_out, out2, c)));
+  STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
+                           w, V, ldv, k, h, n / WW, -1.0, 1, partial, scale_src, scale_out,
+                           out2 + k, c)));
+  if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s);  // <V_j, w_new>
 }
 
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
-                 cudaStream_t s) {
-  const int g = multi_grid(n);
-  STG_DISPATCH_MPW(k, (k_update<MPW><<<g, kMultiBlock, 0, s>>>(x, V, ldv, k, y, n, 0, 1.0,
-                                                               nullptr, nullptr, nullptr, nullptr,
-                                                               nullptr)));
+                 cudaStream_t s, bool accumulate) {
+  if (k == 0) {
+    if (!accumulate) vec_fill(x, 0.0, n, s);
+    return;
+  }
+  const int W = vec_width(n, ldv, V, x);
+  STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
+                           x, V, ldv, k, y, n / WW, 1.0, accumulate ? 1 : 0, nullptr, nullptr,
+                           nullptr, nullptr, nullptr)));
 }
 
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s) {

@@ -427,11 +427,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     ck(cudaMemcpyAsync(dsm + 256, hp + 256, sizeof(double) * k, cudaMemcpyHostToDevice, s),
        "memcpy");
     if (P) {
-      stg::vec_fill(h->zc.p, 0.0, n, s);
-      stg::vec_combine(h->zc.p, V, ld, k, dsm + 256, n, s);  // t = V y
-      (*P)(h->zc.p, h->zv.p);                                // P^-1 t
-      stg::vec_axpy(x, 1.0, h->zv.p, n, s);                  // x += P^-1 V y
-      h->launches += 3;
+      stg::vec_combine(h->zc.p, V, ld, k, dsm + 256, n, s, false);  // t = V y
+      (*P)(h->zc.p, h->zv.p);                                       // P^-1 t
+      stg::vec_axpy(x, 1.0, h->zv.p, n, s);                         // x += P^-1 V y
+      h->launches += 2;
     } else {
       stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
       h->launches++;
