@@ -593,10 +593,22 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
     ck(cudaMemcpyAsync(h->host_u.p + off, un_host + off, sizeof(double) * cnt,
                        cudaMemcpyHostToDevice, h->s_in), "H2D");
   };
+  // STG_PIPE_TRACE=1: time-stamp every chunk's H2D / kernel / D2H (stderr)
+  static const bool trace = std::getenv("STG_PIPE_TRACE") != nullptr;
+  std::vector<cudaEvent_t> tev;
+  auto stamp = [&](cudaStream_t st) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    tev.push_back(e);
+  };
+  stamp(h->s_in);
   if (needL) copy_layers(g.nz - 1, 1);  // periodic z- neighbour of chunk 0
   for (int k = 0; k < K; ++k) {
     copy_layers(k * L, L);
     ck(cudaEventRecord(h->ev_in[k], h->s_in), "event");
+    stamp(h->s_in);
   }
   for (int k = 0; k < K; ++k) {
     ck(cudaStreamWaitEvent(h->stream, h->ev_in[needR ? std::min(k + 1, K - 1) : k], 0), "wait");
@@ -607,12 +619,33 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
     h->launches++;
     check_launch(h);
     ck(cudaEventRecord(h->ev_c[k], h->stream), "event");
+    stamp(h->stream);
     ck(cudaStreamWaitEvent(h->s_out, h->ev_c[k], 0), "wait");
     const long long off = k * L * layer, cnt = L * layer;
     ck(cudaMemcpy2DAsync(R_host + off, pitch, h->host_R.p + off, pitch, sizeof(double) * cnt,
                          size_t(h->nt), cudaMemcpyDeviceToHost, h->s_out), "D2H");
+    stamp(h->s_out);
   }
   ck(cudaStreamSynchronize(h->s_out), "sync");
+  if (trace) {
+    cudaDeviceSynchronize();
+    // order: start, in[0..K-1], then (kernel k, out k) pairs
+    std::fprintf(stderr, "pipe K=%d in:", K);
+    float ms = 0.f;
+    for (int k = 0; k < K; ++k) {
+      cudaEventElapsedTime(&ms, tev[0], tev[size_t(1 + k)]);
+      std::fprintf(stderr, " %.3f", ms);
+    }
+    std::fprintf(stderr, " | kern/out:");
+    for (int k = 0; k < K; ++k) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, tev[0], tev[size_t(1 + K + 2 * k)]);
+      cudaEventElapsedTime(&b, tev[0], tev[size_t(2 + K + 2 * k)]);
+      std::fprintf(stderr, " %.3f/%.3f", a, b);
+    }
+    std::fprintf(stderr, "\n");
+    for (cudaEvent_t e : tev) cudaEventDestroy(e);
+  }
   return true;
 }
 
