@@ -46,6 +46,12 @@ def lib() -> ctypes.CDLL:
         L.or_destroy.argtypes = [ctypes.c_void_p]
         L.or_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _dp, _dp, _dp,
                                 ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+        L.or_create_general.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _ip, _dp, _dp,
+                                        ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp,
+                                        ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.POINTER(ctypes.c_void_p)]
+        L.or_eta.restype = ctypes.c_double
+        L.or_eta.argtypes = [ctypes.c_void_p]
         for name in ("or_spatial_rhs",):
             getattr(L, name).argtypes = [ctypes.c_void_p, ctypes.c_double, _dp, _dp]
         L.or_spatial_jvp.argtypes = [ctypes.c_void_p, ctypes.c_double, _dp, _dp, _dp]
@@ -168,6 +174,8 @@ def lu_solve_dense(A, b):
 
 # ---- problems ---------------------------------------------------------------
 ADVECTION, BURGERS, TEST_EQUATION, ZERO_SYSTEM = 0, 1, 2, 3
+ADVDIFF, EULER = 4, 5               # general flux models (models.hpp:40-159)
+FIELD_CONSTANT, FIELD_ROTATING = 0, 1  # velocity b constant / rotating_field()
 A_FORM, A_INV_FORM = 0, 1
 AUTO, DENSE_LU, GMRES = 0, 1, 3
 
@@ -176,7 +184,11 @@ class Problem:
     """A DG space + model + temporal SBP operators (n_tau nodes)."""
 
     def __init__(self, d, p, cells, lower, upper, velocity=(0.0, 0.0, 0.0), model=ADVECTION,
-                 n_tau=None):
+                 n_tau=None, field=FIELD_CONSTANT, eps=0.0, eta=0.0, gamma=1.4):
+        """model ADVECTION / BURGERS / TEST_EQUATION / ZERO_SYSTEM, or the general
+        flux models ADVDIFF (advdiff_model: b constant or rotating_field, eps >= 0,
+        interior penalty eta; eta <= 0 -> 10 p^2) and EULER (euler_model(gamma),
+        r = 4 conservative components per node)."""
         self.d = int(d)
         self.p = int(p)
         self.n_tau = int(n_tau if n_tau is not None else p + 1)
@@ -185,11 +197,19 @@ class Problem:
         hi = _f64(list(upper) + [1.0] * (3 - len(upper)))
         b = _f64(list(velocity) + [0.0] * (3 - len(velocity)))
         h = ctypes.c_void_p()
-        _check(lib().or_create(self.d, self.p, self.n_tau, c, _p(lo), _p(hi), _p(b), int(model),
-                               ctypes.byref(h)))
+        self.r = 4 if model == EULER else 1
+        if model in (ADVDIFF, EULER):
+            _check(lib().or_create_general(self.d, self.p, self.n_tau, c, _p(lo), _p(hi),
+                                           0 if model == ADVDIFF else 1, self.r, int(field),
+                                           _p(b), float(eps), float(eta), float(gamma),
+                                           ctypes.byref(h)))
+        else:
+            _check(lib().or_create(self.d, self.p, self.n_tau, c, _p(lo), _p(hi), _p(b),
+                                   int(model), ctypes.byref(h)))
         self._h = h
         self.dof = int(lib().or_dof(h))
         self.model = model
+        self.eta = float(lib().or_eta(h))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -203,7 +223,8 @@ class Problem:
         return m
 
     def coords(self):
-        x = np.zeros((self.dof, 3))
+        """Node coordinates, one row per (cell, node) (components share a node)."""
+        x = np.zeros((self.dof // self.r, 3))
         _check(lib().or_node_coords(self._h, _p(x)))
         return x
 

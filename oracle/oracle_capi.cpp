@@ -22,8 +22,9 @@ namespace {
 thread_local std::string g_err;
 
 struct Problem {
-  int model = 0;  // 0 = advection, 1 = burgers
+  int model = 0;  // 0 = advection, 1 = burgers, 4 = general (advdiff / euler)
   Space space;
+  std::shared_ptr<GenOperator> gen;  // general models only
   System sys;
   Sbp ops;        // temporal SBP operators (n_tau)
 };
@@ -36,6 +37,9 @@ int guarded(F&& f) {
   } catch (const NonconvergenceError& e) {
     g_err = e.what();
     return 3;
+  } catch (const AdmissibilityError& e) {
+    g_err = e.what();
+    return 5;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return 1;
@@ -159,13 +163,44 @@ int or_create(int d, int p, int n_tau, const int* cells, const double* lower,
   });
 }
 
+// General flux models (models.hpp:23-192): kind 0 advdiff_model (field 0:
+// constant b, 1: rotating_field; eps >= 0), kind 1 euler_model(gamma), r = 4.
+// eta <= 0: the default 10 p^2 (spatial.hpp:366).
+int or_create_general(int d, int p, int n_tau, const int* cells, const double* lower,
+                      const double* upper, int kind, int r, int field, const double* b,
+                      double eps, double eta, double gamma, void** out) {
+  return guarded([&] {
+    auto pr = std::make_unique<Problem>();
+    pr->model = 4;
+    pr->space = make_space(d, p, cells, lower, upper);
+    GenModel m;
+    m.kind = kind;
+    m.r = r;
+    m.d = d;
+    m.field = field;
+    for (int a = 0; a < 3; ++a) m.b[a] = b[a];
+    m.eps = eps;
+    m.gamma = gamma;
+    pr->gen = std::make_shared<GenOperator>(make_gen_operator(pr->space, m, eta));
+    pr->sys = gen_system(*pr->gen);
+    pr->ops = sbp_operators(n_tau);
+    *out = pr.release();
+  });
+}
+
+double or_eta(void* h) {
+  auto* p = static_cast<Problem*>(h);
+  return p->gen ? p->gen->eta : 0.0;
+}
+
 void or_destroy(void* h) { delete static_cast<Problem*>(h); }
 
 long long or_dof(void* h) { return static_cast<Problem*>(h)->sys.dof; }
 
 int or_mass(void* h, double* m) {
   return guarded([&] {
-    const Vec v = global_mass(static_cast<Problem*>(h)->space);
+    auto* pr = static_cast<Problem*>(h);
+    const Vec v = pr->gen ? pr->gen->mass : global_mass(pr->space);
     std::memcpy(m, v.data(), sizeof(double) * v.size());
   });
 }

@@ -697,6 +697,309 @@ inline void burgers_jvp(const Burgers& op, const double* u, const double* v,
 }
 
 // --------------------------------------------------------------------------
+// General flux models with r components on d in {1, 2} (models.hpp:23-192)
+// and SpatialOperator::rhs with interior-penalty diffusion
+// (spatial.hpp:20-52, 107-266), restated in the reference's loop order.
+//   kind 0: advdiff_model(d, b, eps) -- b constant or rotating_field()
+//           (models.hpp:40-84); eps = 0 is plain advection_model
+//   kind 1: euler_model(gamma), r = 4, d = 2 (models.hpp:118-159)
+// --------------------------------------------------------------------------
+// AdmissibilityError: models.hpp:15-20
+struct AdmissibilityError : std::runtime_error {
+  Vec state;
+  AdmissibilityError(const std::string& what, Vec s)
+      : std::runtime_error(what), state(std::move(s)) {}
+};
+
+struct GenModel {
+  int kind = 0;    // 0 advdiff, 1 euler
+  int r = 1;
+  int d = 1;
+  int field = 0;   // 0 constant b, 1 rotating_field (models.hpp:73-80)
+  double b[3] = {0, 0, 0};
+  double eps = 0.0;
+  double gamma = 1.4;
+
+  bool has_diffusion() const { return kind == 0 && eps > 0; }
+  bool linear() const { return kind == 0; }
+  void velocity(const double* x, double* bv) const {
+    if (field == 1) {
+      bv[0] = -4.0 * (x[1] - 0.5);
+      bv[1] = 4.0 * (x[0] - 0.5);
+    } else {
+      for (int a = 0; a < d; ++a) bv[a] = b[a];
+    }
+  }
+  // euler_pressure / require_admissible: models.hpp:100-113
+  double pressure(const double* u) const {
+    const double rho = u[0];
+    const double kinetic = (u[1] * u[1] + u[2] * u[2]) / (2.0 * rho);
+    return (gamma - 1.0) * (u[3] - kinetic);
+  }
+  void require_admissible(const double* u) const {
+    if (!(u[0] > 0.0) || !(pressure(u) > 0.0))
+      throw AdmissibilityError("euler_model: nonphysical state", Vec(u, u + 4));
+  }
+  // F_c(u, x): r x d row-major, f[comp*d + a]  (models.hpp:46-48, 126-141)
+  void Fc(const double* u, const double* x, double* f) const {
+    if (kind == 0) {
+      double bv[3];
+      velocity(x, bv);
+      for (int a = 0; a < d; ++a) f[a] = u[0] * bv[a];
+      return;
+    }
+    require_admissible(u);
+    const double rho = u[0];
+    const double v[2] = {u[1] / rho, u[2] / rho};
+    const double P = pressure(u);
+    const double e = u[3];
+    for (int a = 0; a < 2; ++a) {
+      f[0 * 2 + a] = rho * v[a];
+      for (int i = 0; i < 2; ++i) f[(1 + i) * 2 + a] = rho * v[i] * v[a] + (i == a ? P : 0.0);
+      f[3 * 2 + a] = (e + P) * v[a];
+    }
+  }
+  // F_v(u, grad, x) = eps grad (models.hpp:70-72); zero for Euler
+  void Fv(const double* grad, double* f) const {
+    for (int k = 0; k < r * d; ++k) f[k] = kind == 0 ? eps * grad[k] : 0.0;
+  }
+  // max_wave_speed: models.hpp:55-58 (|b(x).n|), 145-156 (max |v.n| + c)
+  double max_wave_speed(const double* uL, const double* uR, const double* n,
+                        const double* x) const {
+    if (kind == 0) {
+      double bv[3];
+      velocity(x, bv);
+      double dot = 0.0;
+      for (int a = 0; a < d; ++a) dot += bv[a] * n[a];
+      return std::abs(dot);
+    }
+    double lambda = 0.0;
+    for (const double* u : {uL, uR}) {
+      require_admissible(u);
+      const double rho = u[0];
+      const double v[2] = {u[1] / rho, u[2] / rho};
+      const double c = std::sqrt(gamma * pressure(u) / rho);
+      lambda = std::max(lambda, std::abs(v[0] * n[0] + v[1] * n[1]) + c);
+    }
+    return lambda;
+  }
+};
+
+struct GenOperator {
+  Space s;       // geometry (r = 1 indexing); coefficients carry r components
+  GenModel m;
+  double eta = 1.0;
+  Vec mass;      // per coefficient (replicated across components)
+  int64_t dof() const { return s.dof() * m.r; }
+  int64_t coeff(int cell, int node, int comp) const {
+    return (int64_t(cell) * s.npc() + node) * m.r + comp;
+  }
+  // 2-D node_index(ix, iy) = iy*(p+1) + ix; 1-D: ix (mesh.hpp:70-72)
+  int node2(int ix, int iy) const { return s.d == 1 ? ix : iy * s.n1() + ix; }
+};
+
+// assemble_semidiscrete: spatial.hpp:352-373 (eta default 10 p^2)
+inline GenOperator make_gen_operator(const Space& s, const GenModel& m, double eta) {
+  if (s.d > 2) throw std::invalid_argument("general models: d in {1, 2}");
+  if (m.d != s.d) throw std::invalid_argument("assemble_semidiscrete: dimension mismatch");
+  if (m.kind == 1 && (m.r != 4 || s.d != 2))
+    throw std::invalid_argument("euler_model: r = 4, d = 2");
+  if (m.kind == 0 && m.r != 1) throw std::invalid_argument("advdiff_model: r = 1");
+  if (m.kind == 0 && m.eps < 0) throw std::invalid_argument("advdiff_model: need eps >= 0");
+  if (m.kind == 1 && !(m.gamma > 1.0)) throw std::invalid_argument("euler_model: gamma > 1");
+  GenOperator op;
+  op.s = s;
+  op.m = m;
+  op.eta = eta > 0 ? eta : 10.0 * s.p * s.p;
+  const Vec m1 = global_mass(s);
+  op.mass.resize(size_t(op.dof()));
+  for (int64_t k = 0; k < s.dof(); ++k)
+    for (int c = 0; c < m.r; ++c) op.mass[size_t(k * m.r + c)] = m1[size_t(k)];
+  return op;
+}
+
+// SpatialOperator::rhs: spatial.hpp:107-266
+inline void gen_rhs(const GenOperator& op, const double* u, double* F) {
+  const Space& s = op.s;
+  const GenModel& m = op.m;
+  const int n1 = s.n1(), p = s.p, r = m.r, d = s.d, npc = s.npc();
+  const Mat& D = s.D;
+  const Vec& w = s.rule.weights;
+  const int64_t dof = op.dof();
+  std::vector<double> Lh(size_t(dof), 0.0);
+  const bool diff = m.has_diffusion();
+  const size_t R1 = static_cast<size_t>(r), RD = static_cast<size_t>(r) * d;
+  std::vector<double> loc(static_cast<size_t>(npc) * R1), grads(static_cast<size_t>(npc) * RD),
+      flux(static_cast<size_t>(npc) * RD), fv(RD);
+  // element integrals (F_c - F_v) : grad(psi), S = 0 (spatial.hpp:117-156)
+  for (int cell = 0; cell < s.n_cells(); ++cell) {
+    for (int node = 0; node < npc; ++node)
+      for (int c = 0; c < r; ++c) loc[size_t(node) * r + c] = u[op.coeff(cell, node, c)];
+    if (diff) {  // local_grad: spatial.hpp:72-99
+      std::fill(grads.begin(), grads.end(), 0.0);
+      const double sx = 2.0 / s.h[0];
+      if (d == 1) {
+        for (int i = 0; i < n1; ++i)
+          for (int k = 0; k < n1; ++k)
+            for (int c = 0; c < r; ++c)
+              grads[(size_t(i) * r + c) * d + 0] += sx * D(i, k) * loc[size_t(k) * r + c];
+      } else {
+        const double sy = 2.0 / s.h[1];
+        for (int ix = 0; ix < n1; ++ix)
+          for (int iy = 0; iy < n1; ++iy) {
+            const int g = op.node2(ix, iy);
+            for (int k = 0; k < n1; ++k)
+              for (int c = 0; c < r; ++c) {
+                grads[(size_t(g) * r + c) * d + 0] +=
+                    sx * D(ix, k) * loc[size_t(op.node2(k, iy)) * r + c];
+                grads[(size_t(g) * r + c) * d + 1] +=
+                    sy * D(iy, k) * loc[size_t(op.node2(ix, k)) * r + c];
+              }
+          }
+      }
+    }
+    for (int node = 0; node < npc; ++node) {
+      double x[3];
+      s.node_coord(cell, node, x);
+      m.Fc(&loc[size_t(node) * r], x, &flux[size_t(node) * r * d]);
+      if (diff) {
+        m.Fv(&grads[size_t(node) * r * d], fv.data());
+        for (int k = 0; k < r * d; ++k) flux[size_t(node) * r * d + k] -= fv[size_t(k)];
+      }
+    }
+    if (d == 1) {
+      const double h = s.h[0];
+      for (int i = 0; i < n1; ++i)
+        for (int c = 0; c < r; ++c) {
+          double val = w[i] * (h / 2.0) * 0.0;
+          for (int k = 0; k < n1; ++k) val += w[k] * D(k, i) * flux[(size_t(k) * r + c) * d + 0];
+          Lh[op.coeff(cell, i, c)] += val;
+        }
+    } else {
+      const double hx = s.h[0], hy = s.h[1];
+      for (int ix = 0; ix < n1; ++ix)
+        for (int iy = 0; iy < n1; ++iy)
+          for (int c = 0; c < r; ++c) {
+            double val = w[ix] * w[iy] * (hx * hy / 4.0) * 0.0;
+            for (int k = 0; k < n1; ++k) {
+              val += w[iy] * (hy / 2.0) * w[k] * D(k, ix) *
+                     flux[(size_t(op.node2(k, iy)) * r + c) * d + 0];
+              val += w[ix] * (hx / 2.0) * w[k] * D(k, iy) *
+                     flux[(size_t(op.node2(ix, k)) * r + c) * d + 1];
+            }
+            Lh[op.coeff(cell, op.node2(ix, iy), c)] += val;
+          }
+    }
+  }
+  // facet integrals, facet-major (spatial.hpp:158-261)
+  std::vector<double> uL(R1), uR(R1), FL(RD), FR(RD), H(R1), gL(RD), gR(RD), uavg(R1), jt(RD),
+      fvL(RD), fvR(RD), fj(RD), jump(R1), avg(R1);
+  for (int axis = 0; axis < d; ++axis) {
+    const int nx = s.cells[0];
+    const int ny = d == 2 ? s.cells[1] : 1;
+    const double h_n = s.h[axis];
+    const double h_e = d == 2 ? s.h[axis] : s.h[0];
+    double nrm[2] = {0.0, 0.0};
+    nrm[axis] = 1.0;
+    for (int cy = 0; cy < ny; ++cy)
+      for (int cx = 0; cx < nx; ++cx) {
+        const int L = s.cell_index(cx, cy, 0);
+        const int R = s.neighbor(L, axis, +1);
+        const int n_trans = d == 2 ? n1 : 1;
+        for (int q = 0; q < n_trans; ++q) {
+          const int nodeL = d == 1 ? p : (axis == 0 ? op.node2(p, q) : op.node2(q, p));
+          const int nodeR = d == 1 ? 0 : (axis == 0 ? op.node2(0, q) : op.node2(q, 0));
+          double x[3] = {0.0, 0.0, 0.0};
+          {
+            int ci[3];
+            s.cell_multi(L, ci);
+            x[axis] = s.lower[axis] + (ci[axis] + 1) * s.h[axis];
+            if (d == 2) {
+              const int tangent = 1 - axis;
+              x[tangent] = s.lower[tangent] +
+                           (ci[tangent] + 0.5 * (1.0 + s.rule.nodes[q])) * s.h[tangent];
+            }
+          }
+          const double wf = d == 2 ? s.rule.weights[q] * s.h[1 - axis] / 2.0 : 1.0;
+          for (int c = 0; c < r; ++c) {
+            uL[size_t(c)] = u[op.coeff(L, nodeL, c)];
+            uR[size_t(c)] = u[op.coeff(R, nodeR, c)];
+          }
+          // llf_flux: spatial.hpp:20-25
+          const double lambda = m.max_wave_speed(uL.data(), uR.data(), nrm, x);
+          m.Fc(uL.data(), x, FL.data());
+          m.Fc(uR.data(), x, FR.data());
+          for (int c = 0; c < r; ++c) {
+            double fn = 0.0;
+            for (int a = 0; a < d; ++a)
+              fn += (FL[size_t(c) * d + a] + FR[size_t(c) * d + a]) * nrm[a];
+            H[size_t(c)] = 0.5 * fn + 0.5 * lambda * (uL[size_t(c)] - uR[size_t(c)]);
+          }
+          for (int c = 0; c < r; ++c) {
+            Lh[op.coeff(L, nodeL, c)] -= H[size_t(c)] * wf;
+            Lh[op.coeff(R, nodeR, c)] += H[size_t(c)] * wf;
+          }
+          if (!diff) continue;
+          // gradient traces (spatial.hpp:213-240)
+          std::fill(gL.begin(), gL.end(), 0.0);
+          std::fill(gR.begin(), gR.end(), 0.0);
+          const double sn = 2.0 / h_n;
+          for (int k = 0; k < n1; ++k) {
+            const int lkn = d == 1 ? k : (axis == 0 ? op.node2(k, q) : op.node2(q, k));
+            for (int c = 0; c < r; ++c) {
+              gL[size_t(c) * d + axis] += sn * D(n1 - 1, k) * u[op.coeff(L, lkn, c)];
+              gR[size_t(c) * d + axis] += sn * D(0, k) * u[op.coeff(R, lkn, c)];
+            }
+          }
+          if (d == 2) {
+            const int tangent = 1 - axis;
+            const double st = 2.0 / s.h[tangent];
+            for (int k = 0; k < n1; ++k) {
+              const int ltk = axis == 0 ? op.node2(p, k) : op.node2(k, p);
+              const int rtk = axis == 0 ? op.node2(0, k) : op.node2(k, 0);
+              for (int c = 0; c < r; ++c) {
+                gL[size_t(c) * d + tangent] += st * D(q, k) * u[op.coeff(L, ltk, c)];
+                gR[size_t(c) * d + tangent] += st * D(q, k) * u[op.coeff(R, rtk, c)];
+              }
+            }
+          }
+          // interior_penalty_surface: spatial.hpp:35-52
+          for (int c = 0; c < r; ++c) {
+            uavg[size_t(c)] = 0.5 * (uL[size_t(c)] + uR[size_t(c)]);
+            for (int a = 0; a < d; ++a) jt[size_t(c) * d + a] = (uL[size_t(c)] - uR[size_t(c)]) * nrm[a];
+          }
+          m.Fv(jt.data(), fj.data());
+          m.Fv(gL.data(), fvL.data());
+          m.Fv(gR.data(), fvR.data());
+          for (int c = 0; c < r; ++c) {
+            double jf = 0.0, af = 0.0;
+            for (int a = 0; a < d; ++a) {
+              jf += fj[size_t(c) * d + a] * nrm[a];
+              af += (fvL[size_t(c) * d + a] + fvR[size_t(c) * d + a]) * nrm[a];
+            }
+            jump[size_t(c)] = jf;
+            avg[size_t(c)] = 0.5 * af;
+          }
+          for (int c = 0; c < r; ++c) {
+            const double sym = -0.5 * jump[size_t(c)];
+            const double tL = -avg[size_t(c)] + (op.eta / h_e) * jump[size_t(c)];
+            const double tR = avg[size_t(c)] - (op.eta / h_e) * jump[size_t(c)];
+            Lh[op.coeff(L, nodeL, c)] -= tL * wf;
+            Lh[op.coeff(R, nodeR, c)] -= tR * wf;
+            // symmetry term along the normal line (spatial.hpp:248-259)
+            for (int i = 0; i < n1; ++i) {
+              const int lin = d == 1 ? i : (axis == 0 ? op.node2(i, q) : op.node2(q, i));
+              Lh[op.coeff(L, lin, c)] -= sym * D(n1 - 1, i) * sn * wf;
+              Lh[op.coeff(R, lin, c)] -= sym * D(0, i) * sn * wf;
+            }
+          }
+        }
+      }
+  }
+  for (int64_t i = 0; i < dof; ++i) F[i] = Lh[size_t(i)] / op.mass[size_t(i)];
+}
+
+// --------------------------------------------------------------------------
 // Semidiscrete system seam (system.hpp:16-23): rhs(t, u) plus a flag for
 // linearity (spatial_jacobian's exact branch, spatial.hpp:290-298).
 // --------------------------------------------------------------------------
@@ -741,6 +1044,54 @@ inline System burgers_system(const Burgers& op) {
   sys.jac = [opp](double, const double* u, const double* v, double* Jv) {
     burgers_jvp(*opp, u, v, Jv);
   };
+  return sys;
+}
+
+// advdiff: linear, J v = rhs(v) - rhs(0) (spatial.hpp:290-298, cached base);
+// euler: the reference assembles a coloured central-difference Jacobian
+// (spatial.hpp:299-320, step sqrt(eps)(1+|u_j|)); its action is restated as
+// the directional central difference with step 1e-7 (1 + ||u||_inf)/||v||_inf.
+inline System gen_system(const GenOperator& op) {
+  System sys;
+  sys.dof = op.dof();
+  sys.linear = op.m.linear();
+  auto opp = std::make_shared<GenOperator>(op);
+  sys.rhs = [opp](double, const double* u, double* F) { gen_rhs(*opp, u, F); };
+  if (sys.linear) {
+    auto base = std::make_shared<Vec>();
+    sys.jac = [opp, base](double, const double*, const double* v, double* Jv) {
+      const int64_t n = opp->dof();
+      if (base->empty()) {
+        Vec zero(static_cast<size_t>(n), 0.0);
+        base->resize(static_cast<size_t>(n));
+        gen_rhs(*opp, zero.data(), base->data());
+      }
+      gen_rhs(*opp, v, Jv);
+      for (int64_t i = 0; i < n; ++i) Jv[i] -= (*base)[size_t(i)];
+    };
+  } else {
+    sys.jac = [opp](double, const double* u, const double* v, double* Jv) {
+      const int64_t n = opp->dof();
+      double un = 0.0, vn = 0.0;
+      for (int64_t i = 0; i < n; ++i) {
+        un = std::max(un, std::abs(u[i]));
+        vn = std::max(vn, std::abs(v[i]));
+      }
+      if (vn == 0.0) {
+        for (int64_t i = 0; i < n; ++i) Jv[i] = 0.0;
+        return;
+      }
+      const double h = 1e-7 * (1.0 + un) / vn;
+      Vec up(u, u + n), um(u, u + n), Fp(static_cast<size_t>(n)), Fm(static_cast<size_t>(n));
+      for (int64_t i = 0; i < n; ++i) {
+        up[size_t(i)] += h * v[i];
+        um[size_t(i)] -= h * v[i];
+      }
+      gen_rhs(*opp, up.data(), Fp.data());
+      gen_rhs(*opp, um.data(), Fm.data());
+      for (int64_t i = 0; i < n; ++i) Jv[i] = (Fp[size_t(i)] - Fm[size_t(i)]) / (2.0 * h);
+    };
+  }
   return sys;
 }
 

@@ -136,3 +136,36 @@ def residual_bytes(cfg: Config) -> int:
 
 def jvp_bytes(cfg: Config) -> int:
     return 16 * cfg.n_dof
+
+
+# ---- initial data of the reference experiments (host side) -----------------
+def rotating_pulse_exact(t, x, y, eps=0.001):
+    """Analytic rotating-pulse solution (models.hpp:162-170), vectorised."""
+    x0, y0 = np.asarray(x) - 0.5, np.asarray(y) - 0.5
+    xq = x0 * np.cos(4.0 * t) + y0 * np.sin(4.0 * t) + 0.25
+    yq = -x0 * np.sin(4.0 * t) + y0 * np.cos(4.0 * t)
+    s2 = 0.004 + 4.0 * eps * t
+    return (0.004 / s2) * np.exp(-(xq * xq + yq * yq) / s2)
+
+
+def vortex_initial(x, y, Sv=5.0, M=0.5, gamma=1.4):
+    """Isentropic vortex conservative state (rho, rho v1, rho v2, e), evaluated
+    as printed in models.hpp:173-190; returns an (..., 4) array."""
+    x, y = np.asarray(x, dtype=np.float64), np.asarray(y, dtype=np.float64)
+    f = 1.0 - x * x - y * y
+    rho_base = 1.0 - Sv * Sv * (gamma - 1.0) * M * M * np.exp(f) / (8.0 * math.pi * math.pi)
+    if np.any(~(rho_base > 0.0)):
+        raise ValueError("vortex_initial: density formula nonpositive")
+    rho = rho_base ** (1.0 / (gamma - 1.0))
+    v1 = 1.0 - Sv * y * np.exp(f / 2.0) / (2.0 * math.pi)
+    v2 = Sv * x * np.exp(f / 2.0) / (2.0 * math.pi)
+    P = rho ** gamma / (gamma * M * M)
+    e = P / (gamma - 1.0) + 0.5 * (v1 * v1 + v2 * v2) / rho
+    return np.stack([rho, rho * v1, rho * v2, e], axis=-1)
+
+
+def grid_coords(dim, degree, cells, lower, upper) -> np.ndarray:
+    """Node coordinates (n_cells * n^d, 3) in the reference order (mesh.hpp:70-90)."""
+    cfg = Config("grid", dim, degree, 2, tuple(cells), tuple(lower), tuple(upper),
+                 (0.0,) * dim, 0.0, "none", 0)
+    return node_coords(cfg)
