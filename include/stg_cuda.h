@@ -14,13 +14,15 @@
  *   STG_ERR_RUNTIME        2  std::runtime_error      (newton.hpp:74-76)
  *   STG_ERR_NONCONVERGENCE 3  NonconvergenceError     (newton.hpp:40-48, 116-120)
  *   STG_ERR_CUDA           4  CUDA runtime failure (no CPU fallback exists)
+ *   STG_ERR_ADMISSIBILITY  5  AdmissibilityError     (models.hpp:15-20, stdg.hpp:41-50)
  *
  * Layout of every vector (unchanged from the reference, stdg.hpp:18-20,
  * mesh.hpp:22-25, mesh.hpp:70-81): temporal-node (stage) blocks outermost,
  * then cell index (x fastest: cell = (cz*ny + cy)*nx + cx), then node index
  * within the cell (x fastest: node = (iz*n + iy)*n + ix), component innermost
- * (r = 1 for every supported model).  A spatial vector has n_sdof entries, a
- * slab/stage vector n_tau * n_sdof.
+ * (r = 4 conservative components for Euler, r = 1 otherwise).  A spatial
+ * vector has n_sdof = cells * n^d * r entries, a slab/stage vector
+ * n_tau * n_sdof.
  *
  * Memory: unless a function name ends in `_host`, every double* is a DEVICE
  * pointer owned by the caller.  `_host` variants take host pointers and do
@@ -37,18 +39,29 @@
 extern "C" {
 #endif
 
-#define STG_ABI_VERSION 1
+#define STG_ABI_VERSION 2
 
 #define STG_OK 0
 #define STG_ERR_INVALID 1
 #define STG_ERR_RUNTIME 2
 #define STG_ERR_NONCONVERGENCE 3
 #define STG_ERR_CUDA 4
+#define STG_ERR_ADMISSIBILITY 5
 
 /* models: advection_model (models.hpp:40-66) with constant velocity;
- * Burgers (EXTENSION, not in the reference; d = 1 only). */
+ * Burgers (EXTENSION, not in the reference; d = 1 only);
+ * advdiff_model (models.hpp:68-76): advection with a constant or rotating
+ * (models.hpp:79-85) velocity field plus interior-penalty diffusion eps
+ * (spatial.hpp:27-52, 209-261), d in {1, 2};
+ * euler_model(gamma) (models.hpp:118-159): 2-D compressible Euler, r = 4. */
 #define STG_MODEL_ADVECTION 0
 #define STG_MODEL_BURGERS 1
+#define STG_MODEL_ADVDIFF 2
+#define STG_MODEL_EULER 3
+
+/* velocity fields of STG_MODEL_ADVDIFF */
+#define STG_FIELD_CONSTANT 0  /* b = velocity[] */
+#define STG_FIELD_ROTATING 1  /* rotating_field(): b = (-4(y-1/2), 4(x-1/2)) */
 
 /* JacobianForm (lodg.hpp:20) */
 #define STG_FORM_A 0
@@ -91,7 +104,12 @@ typedef struct stg_desc {
   int cells[3];     /* cells per axis (unused axes ignored) */
   double lower[3];  /* domain lower corner */
   double upper[3];  /* domain upper corner */
-  double velocity[3]; /* advection velocity b (advection only) */
+  double velocity[3]; /* advection velocity b (constant fields) */
+  /* ABI v2 (general models; zero-initialise for the defaults): */
+  int velocity_field; /* STG_FIELD_* (STG_MODEL_ADVDIFF) */
+  double eps;         /* diffusion coefficient >= 0 (STG_MODEL_ADVDIFF) */
+  double eta;         /* interior-penalty parameter; <= 0: 10 p^2 (spatial.hpp:366) */
+  double gamma;       /* ratio of specific heats; <= 0: 1.4 (STG_MODEL_EULER) */
 } stg_desc;
 
 /* NewtonConfig (newton.hpp:30-38) plus the finite-difference step for
@@ -104,7 +122,8 @@ typedef struct stg_newton_config {
   int gmres_restart;  /* default 30 */
   double gmres_tol;   /* default 1e-12, ||r||_2 <= tol ||b||_2 */
   int gmres_max_it;   /* default 1000 */
-  double fd_eps;      /* FD Jacobian-vector step (Burgers); <= 0: exact */
+  double fd_eps;      /* FD Jacobian-vector step; <= 0: exact (Burgers) or
+                         1e-7 (Euler, which has no exact linearisation here) */
   int precond;        /* STG_PRECOND_*; default AUTO */
 } stg_newton_config;
 

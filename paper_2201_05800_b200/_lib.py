@@ -12,7 +12,9 @@ from pathlib import Path
 LIB_PATH = Path(__file__).resolve().parent / "libstg_cuda.so"
 
 STG_OK, STG_ERR_INVALID, STG_ERR_RUNTIME, STG_ERR_NONCONVERGENCE, STG_ERR_CUDA = 0, 1, 2, 3, 4
-STG_MODEL_ADVECTION, STG_MODEL_BURGERS = 0, 1
+STG_ERR_ADMISSIBILITY = 5
+STG_MODEL_ADVECTION, STG_MODEL_BURGERS, STG_MODEL_ADVDIFF, STG_MODEL_EULER = 0, 1, 2, 3
+STG_FIELD_CONSTANT, STG_FIELD_ROTATING = 0, 1
 STG_FORM_A, STG_FORM_A_INV = 0, 1
 STG_LINEAR_AUTO, STG_LINEAR_GMRES = 0, 3
 STG_KERNEL_AUTO, STG_KERNEL_GENERIC, STG_KERNEL_FAST = 0, 1, 2
@@ -37,6 +39,8 @@ class StgDesc(ctypes.Structure):
         ("dim", ctypes.c_int), ("degree", ctypes.c_int), ("n_tau", ctypes.c_int),
         ("model", ctypes.c_int), ("cells", ctypes.c_int * 3), ("lower", ctypes.c_double * 3),
         ("upper", ctypes.c_double * 3), ("velocity", ctypes.c_double * 3),
+        ("velocity_field", ctypes.c_int), ("eps", ctypes.c_double), ("eta", ctypes.c_double),
+        ("gamma", ctypes.c_double),
     ]
 
 

@@ -11,6 +11,7 @@ Exception mapping (status code -> reference exception type):
   STG_ERR_RUNTIME        -> RuntimeError          (std::runtime_error)
   STG_ERR_NONCONVERGENCE -> NonconvergenceError   (newton.hpp:40-48)
   STG_ERR_CUDA           -> CudaError
+  STG_ERR_ADMISSIBILITY  -> AdmissibilityError    (models.hpp:15-20)
 """
 from __future__ import annotations
 
@@ -39,6 +40,11 @@ class NonconvergenceError(RuntimeError):
 
 class CudaError(RuntimeError):
     pass
+
+
+class AdmissibilityError(RuntimeError):
+    """A model was evaluated at a nonphysical state (models.hpp:15-20); the
+    message names the temporal node (stdg.hpp:41-50)."""
 
 
 class LinearMethod:  # newton.hpp:28
@@ -87,6 +93,8 @@ def _raise(h, code: int, lib) -> None:
         raise NonconvergenceError(msg)
     if code == L.STG_ERR_CUDA:
         raise CudaError(msg)
+    if code == L.STG_ERR_ADMISSIBILITY:
+        raise AdmissibilityError(msg)
     raise RuntimeError(msg)
 
 
@@ -117,7 +125,8 @@ class SlabOperator:
     def __init__(self, dim: int, degree: int, n_tau: int, cells: Sequence[int],
                  lower: Sequence[float], upper: Sequence[float],
                  velocity: Sequence[float] = (0.0, 0.0, 0.0), model: int = L.STG_MODEL_ADVECTION,
-                 kernel: int = L.STG_KERNEL_AUTO):
+                 kernel: int = L.STG_KERNEL_AUTO, velocity_field: int = L.STG_FIELD_CONSTANT,
+                 eps: float = 0.0, eta: float = 0.0, gamma: float = 0.0):
         self._lib = L.load()
         pad = lambda v, fill: list(v) + [fill] * (3 - len(v))
         d = L.StgDesc()
@@ -126,6 +135,8 @@ class SlabOperator:
         d.lower[:] = [float(x) for x in pad(lower, 0.0)]
         d.upper[:] = [float(x) for x in pad(upper, 1.0)]
         d.velocity[:] = [float(x) for x in pad(velocity, 0.0)]
+        d.velocity_field, d.eps, d.eta, d.gamma = int(velocity_field), float(eps), float(eta), \
+            float(gamma)
         h = ctypes.c_void_p()
         _raise(None, self._lib.stg_create(ctypes.byref(d), ctypes.byref(h)), self._lib)
         self._h = h

@@ -88,6 +88,34 @@ int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
 bool slab_fast_supported(const SlabArgs& a);
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s);
 
+// ---- general flux models, d in {1, 2} (kernels_general.cu) -----------------
+// r = 1: advdiff_model (constant / rotating velocity, eps >= 0, interior
+// penalty eta); r = 4: euler_model(gamma).
+struct GenCoef {
+  int r;
+  int field;      // 0 constant b, 1 rotating_field (models.hpp:79-85)
+  double b[2];
+  double eps, eta, gamma;
+  double xi[kMaxN], w[kMaxN];
+  double D[kMaxN][kMaxN];  // D[j][i] = D(j,i) = psi_i'(x_j)
+  double h[2], lower[2];
+  double vol_scale;        // prod(h) / 2^d (global_mass, mesh.hpp:125-141)
+};
+struct GenArgs {
+  GenCoef c;
+  Geometry g;     // n_sdof includes the r components
+  MixCoef mx;
+  int n_in, n_out;
+  const double* X;     // n_in blocks: F_j = F(X_j)
+  const double* Xmix;  // blocks of the T term (null: none)
+  const double* W;     // spatial vector of the c term (null: none)
+  double* F;           // workspace, n_in blocks
+  double* R;           // n_out blocks (null: only F is computed)
+  int* err;            // admissibility flag: 1 + first failing block
+};
+// Returns the number of kernels launched, or -1 if (d, n, r) is unsupported.
+int launch_general(const GenArgs& a, cudaStream_t s);
+
 // ---- element-block Jacobi by fast diagonalisation, d = 3 N = 3 n_tau = 4
 // (kernels_fdm.cu).  Complex entries are stored [re, im]; x eigen-indices are
 // kept for one member of each conjugate pair (kx = 2j, j = 0, 1).

@@ -25,6 +25,10 @@ namespace {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// AdmissibilityError (models.hpp:15-20), rethrown per temporal node (stdg.hpp:41-50)
+struct AdmissibilityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 struct NonconvergenceError : std::runtime_error {
   std::vector<double> history;
   NonconvergenceError(const std::string& w, std::vector<double> h)
@@ -62,6 +66,9 @@ struct DevBuf {
 
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
+bool general_model(int m) { return m == STG_MODEL_ADVDIFF || m == STG_MODEL_EULER; }
+bool linear_model(int m) { return m == STG_MODEL_ADVECTION || m == STG_MODEL_ADVDIFF; }
+
 }  // namespace
 
 struct stg_handle {
@@ -70,6 +77,8 @@ struct stg_handle {
   int n1 = 0, nt = 0;
   long long n_sdof = 0, n_dof = 0;
   stg::SpatialCoef sp{};
+  stg::GenCoef gc{};   // general flux models (advdiff / euler)
+  int r = 1;           // components per node
   stg::LglRule rule, trule;
   std::vector<double> D, Dt;  // row-major D(j,i) at [j*n+i]
   stg::Tableau tab;
@@ -85,6 +94,7 @@ struct stg_handle {
   DevBuf partial;  // reduction partials
   DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
   DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
+  DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
@@ -113,6 +123,43 @@ void check_launch(stg_handle* h) {
 }
 
 // ---- operator dispatch ----------------------------------------------------
+// General flux models: F(X_j) for every input block, then the mix; Euler's
+// admissibility flag is read back (one sync) and raised as AdmissibilityError
+// naming the temporal node (stdg.hpp:41-50).
+void apply_general(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
+                   const double* W, double* R) {
+  if (h->kernel_pref == STG_KERNEL_FAST)
+    throw std::invalid_argument("fast kernel requested but not applicable to this problem");
+  stg::GenArgs a{};
+  a.c = h->gc;
+  a.g = h->g;
+  a.mx = mx;
+  a.n_in = n_in;
+  a.n_out = n_out;
+  a.X = X;
+  a.Xmix = X;
+  a.W = W;
+  h->genF.ensure(size_t(n_in) * size_t(h->n_sdof));
+  a.F = h->genF.p;
+  a.R = R;
+  a.err = reinterpret_cast<int*>(h->genFlag.p);
+  const int launched = stg::launch_general(a, h->stream);
+  if (launched < 0) throw std::invalid_argument("no kernel for this (dim, degree, model)");
+  h->launches += launched;
+  check_launch(h);
+  if (h->desc.model == STG_MODEL_EULER) {
+    int* hp = reinterpret_cast<int*>(h->pinned + 1000);
+    ck(cudaMemcpyAsync(hp, a.err, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "memcpy");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    if (*hp != 0) {
+      const int node = *hp - 1;
+      ck(cudaMemsetAsync(a.err, 0, sizeof(int), h->stream), "memset");
+      throw AdmissibilityError("temporal node " + std::to_string(node) +
+                               ": euler_model: nonphysical state");
+    }
+  }
+}
+
 void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
            const double* U, const double* W, double* R, bool jvp, bool full_s,
            int seg_begin = 0, int seg_end = 0) {
@@ -132,6 +179,10 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   a.U = U;
   a.W = W;
   a.R = R;
+  if (general_model(h->desc.model)) {
+    apply_general(h, mx, n_in, n_out, X, W, R);
+    return;
+  }
   int launched = -1;
   if (h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(a)) {
     launched = stg::launch_slab_fast(a, h->stream);
@@ -197,10 +248,22 @@ void validate_desc(const stg_desc* d) {
     throw std::invalid_argument("dg_space: degree must be in [1, 5]");
   if (d->n_tau < 2 || d->n_tau > stg::kMaxT)
     throw std::invalid_argument("sbp_operators: n_tau must be in [2, 6]");
-  if (d->model != STG_MODEL_ADVECTION && d->model != STG_MODEL_BURGERS)
+  if (d->model < STG_MODEL_ADVECTION || d->model > STG_MODEL_EULER)
     throw std::invalid_argument("unknown model");
   if (d->model == STG_MODEL_BURGERS && d->dim != 1)
     throw std::invalid_argument("burgers model: d = 1 only");
+  if (d->model == STG_MODEL_ADVDIFF) {  // advdiff_model (models.hpp:68-76)
+    if (d->dim > 2) throw std::invalid_argument("advdiff_model: d in {1, 2}");
+    if (!(d->eps >= 0.0)) throw std::invalid_argument("advdiff_model: need eps >= 0");
+    if (d->velocity_field != STG_FIELD_CONSTANT && d->velocity_field != STG_FIELD_ROTATING)
+      throw std::invalid_argument("advdiff_model: unknown velocity field");
+    if (d->velocity_field == STG_FIELD_ROTATING && d->dim != 2)
+      throw std::invalid_argument("rotating_field: d = 2");
+  }
+  if (d->model == STG_MODEL_EULER) {  // euler_model (models.hpp:118-124)
+    if (d->dim != 2) throw std::invalid_argument("assemble_semidiscrete: dimension mismatch");
+    if (d->gamma > 0.0 && !(d->gamma > 1.0)) throw std::invalid_argument("euler_model: gamma > 1");
+  }
   if (d->dim == 3 && d->degree + 1 > 5)
     throw std::invalid_argument("d = 3 supports degree <= 4");
   long long cells = 1;
@@ -213,6 +276,7 @@ void validate_desc(const stg_desc* d) {
   if (cells > (1LL << 30)) throw std::invalid_argument("too many cells");
   long long npc = 1;
   for (int a = 0; a < d->dim; ++a) npc *= d->degree + 1;
+  if (d->model == STG_MODEL_EULER) npc *= 4;
   if (cells * npc >= (1LL << 31))
     throw std::invalid_argument("mesh too large: n_sdof must stay below 2^31");
 }
@@ -237,7 +301,8 @@ void build_constants(stg_handle* h) {
   g.ny = d.dim >= 2 ? d.cells[1] : 1;
   g.nz = d.dim >= 3 ? d.cells[2] : 1;
   g.n_cells = g.nx * g.ny * g.nz;
-  g.n_sdof = (long long)g.n_cells * g.npc;
+  h->r = d.model == STG_MODEL_EULER ? 4 : 1;
+  g.n_sdof = (long long)g.n_cells * g.npc * h->r;
   h->n_sdof = g.n_sdof;
   h->n_dof = g.n_sdof * h->nt;
 
@@ -265,6 +330,29 @@ void build_constants(stg_handle* h) {
       sp.inv_wN = 1.0 / w[n - 1];
       for (int i = 0; i < n; ++i)
         for (int k = 0; k < n; ++k) sp.Dm[i][k] = h->D[size_t(i) * n + k];
+    }
+  }
+  if (general_model(d.model)) {
+    stg::GenCoef& c = h->gc;
+    std::memset(&c, 0, sizeof c);
+    c.r = h->r;
+    c.field = d.velocity_field;
+    c.b[0] = d.velocity[0];
+    c.b[1] = d.velocity[1];
+    c.eps = d.model == STG_MODEL_ADVDIFF ? d.eps : 0.0;
+    c.eta = d.eta > 0.0 ? d.eta : 10.0 * d.degree * d.degree;  // spatial.hpp:366
+    c.gamma = d.gamma > 0.0 ? d.gamma : 1.4;
+    double hprod = 1.0;
+    for (int a = 0; a < d.dim; ++a) {
+      c.h[a] = (d.upper[a] - d.lower[a]) / double(d.cells[a]);
+      c.lower[a] = d.lower[a];
+      hprod *= c.h[a];
+    }
+    c.vol_scale = hprod / std::pow(2.0, d.dim);
+    for (int i = 0; i < n; ++i) {
+      c.xi[i] = h->rule.x[size_t(i)];
+      c.w[i] = w[size_t(i)];
+      for (int k = 0; k < n; ++k) c.D[i][k] = h->D[size_t(i) * n + k];
     }
   }
 }
@@ -649,9 +737,16 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
   return true;
 }
 
+// Euler has no exact linearisation here: a finite-difference step is always used
+// (the reference differences too, spatial.hpp:299-320).
+double effective_fd_eps(const stg_handle* h, double fd_eps) {
+  return h->desc.model == STG_MODEL_EULER && fd_eps <= 0.0 ? 1e-7 : fd_eps;
+}
+
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
             double fd_eps) {
-  if (h->desc.model == STG_MODEL_ADVECTION) {
+  fd_eps = effective_fd_eps(h, fd_eps);
+  if (linear_model(h->desc.model)) {
     // linear: J v = R(v) with the u_n coupling removed (stdg.hpp:79-110)
     apply(h, st_mix(h, dt, false), h->nt, h->nt, v, nullptr, nullptr, Jv, false, false);
   } else if (fd_eps <= 0.0) {
@@ -670,7 +765,8 @@ void stage_residual(stg_handle* h, int form, double dt, const double* u, const d
 void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double* v, double* Jv,
                double fd_eps) {
   const bool full = form == STG_FORM_A;
-  if (h->desc.model == STG_MODEL_ADVECTION) {
+  fd_eps = effective_fd_eps(h, fd_eps);
+  if (linear_model(h->desc.model)) {
     apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, v, nullptr, nullptr, Jv, false, full);
   } else if (fd_eps <= 0.0) {
     apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, full);
@@ -750,6 +846,10 @@ bool fdm_ok(const stg_handle* h) {
 }
 
 int resolve_precond(const stg_handle* h, int kind) {
+  if (general_model(h->desc.model)) {
+    if (kind == STG_PRECOND_AUTO || kind == STG_PRECOND_NONE) return STG_PRECOND_NONE;
+    throw std::invalid_argument("block-Jacobi preconditioners: advection / Burgers only");
+  }
   if (kind == STG_PRECOND_AUTO)
     return (h->desc.dim == 1 || fdm_ok(h))
                ? STG_PRECOND_EBLOCK
@@ -942,6 +1042,9 @@ int guarded(stg_handle* h, F&& f) {
   } catch (const CudaError& e) {
     *err = e.what();
     return STG_ERR_CUDA;
+  } catch (const AdmissibilityError& e) {
+    *err = e.what();
+    return STG_ERR_ADMISSIBILITY;
   } catch (const std::invalid_argument& e) {
     *err = e.what();
     return STG_ERR_INVALID;
@@ -990,6 +1093,10 @@ int stg_create(const stg_desc* desc, stg_handle** out) {
     h->desc = *desc;
     build_constants(h.get());
     ensure_workspace(h.get());
+    if (general_model(desc->model)) {
+      h->genFlag.ensure(1);
+      ck(cudaMemset(h->genFlag.p, 0, sizeof(double)), "cudaMemset");
+    }
     *out = h.release();
   });
 }
@@ -1105,8 +1212,28 @@ int stg_spatial_jvp(stg_handle* h, double t, const double* u, const double* v, d
     (void)t;
     stg::MixCoef m = zero_mix();
     m.S[0][0] = 1.0;
-    const bool nl = h->desc.model != STG_MODEL_ADVECTION;
+    const bool nl = !linear_model(h->desc.model);
     if (nl) need(u, "u");
+    if (h->desc.model == STG_MODEL_EULER) {  // forward difference (no exact linearisation)
+      const long long n = h->n_sdof;
+      const double vn = std::sqrt(dev_dot(h, v, v, n));
+      if (vn == 0.0) {
+        stg::vec_fill(Jv, 0.0, n, h->stream);
+        h->launches++;
+        return;
+      }
+      const double eps = 1e-7 * std::sqrt(1.0 + std::sqrt(dev_dot(h, u, u, n))) / vn;
+      h->tmp1.ensure(size_t(n));
+      h->tmp2.ensure(size_t(n));
+      stg::vec_copy(h->tmp1.p, u, n, h->stream);
+      stg::vec_axpy(h->tmp1.p, eps, v, n, h->stream);
+      h->launches += 2;
+      apply(h, m, 1, 1, h->tmp1.p, nullptr, nullptr, Jv, false, false);
+      apply(h, m, 1, 1, u, nullptr, nullptr, h->tmp2.p, false, false);
+      stg::vec_axpby(Jv, -1.0 / eps, h->tmp2.p, 1.0 / eps, n, h->stream);
+      h->launches++;
+      return;
+    }
     apply(h, m, 1, 1, v, nl ? u : nullptr, nullptr, Jv, nl, false);
   });
 }
@@ -1129,7 +1256,7 @@ int stg_st_jvp(stg_handle* h, double t_n, double dt, const double* U, const doub
     need(h, "stg_st_jvp");
     need(v, "v");
     need(Jv, "Jv");
-    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    if (!linear_model(h->desc.model)) need(U, "U");
     (void)t_n;
     st_jvp(h, dt, U, v, Jv, fd_eps);
   });
@@ -1156,7 +1283,7 @@ int stg_stage_jvp(stg_handle* h, int form, double t, double dt, const double* U,
     need(Jv, "Jv");
     (void)t;
     if (form != STG_FORM_A && form != STG_FORM_A_INV) throw std::invalid_argument("bad form");
-    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    if (!linear_model(h->desc.model)) need(U, "U");
     stage_jvp(h, form, dt, U, v, Jv, fd_eps);
   });
 }
@@ -1169,7 +1296,7 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     need(b, "b");
     need(x, "x");
     (void)t_n;
-    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    if (!linear_model(h->desc.model)) need(U, "U");
     const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
     const GmresStats st = gmres(
         h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
@@ -1188,7 +1315,7 @@ int stg_st_precond_apply(stg_handle* h, double dt, const double* U, int precond,
     need(h, "stg_st_precond_apply");
     need(in, "in");
     need(out, "out");
-    if (h->desc.model != STG_MODEL_ADVECTION) need(U, "U");
+    if (!linear_model(h->desc.model)) need(U, "U");
     const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
     if (P) {
       P(in, out);
