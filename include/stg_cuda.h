@@ -123,7 +123,7 @@ typedef struct stg_newton_config {
   double gmres_tol;   /* default 1e-12, ||r||_2 <= tol ||b||_2 */
   int gmres_max_it;   /* default 1000 */
   double fd_eps;      /* FD Jacobian-vector step; <= 0: exact (Burgers) or
-                         1e-7 (Euler, which has no exact linearisation here) */
+                         1e-5 (Euler, which has no exact linearisation here) */
   int precond;        /* STG_PRECOND_*; default AUTO */
 } stg_newton_config;
 
@@ -178,8 +178,8 @@ int stg_st_residual(stg_handle* h, double t_n, double dt, const double* u_n,
                     const double* U, double* R);
 
 /* st_jacobian (stdg.hpp:79-110) applied matrix-free: Jv = dR/dU(U) v.
- * fd_eps > 0 (nonlinear models): forward difference [R(U+h v)-R(U)]/h with
- * h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (Walker-Pernice parameter). */
+ * fd_eps > 0 (nonlinear models): central difference [R(U+h v)-R(U-h v)]/2h
+ * with h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (Walker-Pernice parameter). */
 int stg_st_jvp(stg_handle* h, double t_n, double dt, const double* U, const double* v,
                double* Jv, double fd_eps);
 

@@ -602,6 +602,7 @@ void st_residual(stg_handle* h, double dt, const double* un, const double* U, do
 
 // Forward-difference Jacobian action [R(U + h v) - R(U)] / h of the slab /
 // stage residual without its constant (u_n / u) coupling, which cancels.
+// [R0(U + h v) - R0(U - h v)] / 2h with
 // h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (the Walker-Pernice differencing
 // parameter, as in PETSc's MFFD "wp"), so the perturbation is relative to the
 // state regardless of the scaling of the Krylov vector v.
@@ -618,12 +619,15 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
   const double eps = fd_eps * std::sqrt(1.0 + un) / vn;
   h->tmp1.ensure(size_t(n));
   h->tmp2.ensure(size_t(n));
+  // central difference: the same two applies as a forward difference, O(h^2)
   stg::vec_copy(h->tmp1.p, U, n, h->stream);
   stg::vec_axpy(h->tmp1.p, eps, v, n, h->stream);
   h->launches += 2;
   apply(h, mix, h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false, full);
-  apply(h, mix, h->nt, h->nt, U, nullptr, nullptr, h->tmp2.p, false, full);
-  stg::vec_axpby(Jv, -1.0 / eps, h->tmp2.p, 1.0 / eps, n, h->stream);
+  stg::vec_axpy(h->tmp1.p, -2.0 * eps, v, n, h->stream);
+  h->launches++;
+  apply(h, mix, h->nt, h->nt, h->tmp1.p, nullptr, nullptr, h->tmp2.p, false, full);
+  stg::vec_axpby(Jv, -0.5 / eps, h->tmp2.p, 0.5 / eps, n, h->stream);
   h->launches++;
 }
 
@@ -738,9 +742,12 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
 }
 
 // Euler has no exact linearisation here: a finite-difference step is always used
-// (the reference differences too, spatial.hpp:299-320).
+// (the reference differences too, spatial.hpp:299-320).  Default fd_eps 1e-5:
+// the central difference's truncation (h^2) and rounding (eps_mach / h) errors
+// balance near h ~ eps_mach^(1/3) per entry.
+constexpr double kEulerFdEps = 1e-5;
 double effective_fd_eps(const stg_handle* h, double fd_eps) {
-  return h->desc.model == STG_MODEL_EULER && fd_eps <= 0.0 ? 1e-7 : fd_eps;
+  return h->desc.model == STG_MODEL_EULER && fd_eps <= 0.0 ? kEulerFdEps : fd_eps;
 }
 
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
@@ -1222,15 +1229,17 @@ int stg_spatial_jvp(stg_handle* h, double t, const double* u, const double* v, d
         h->launches++;
         return;
       }
-      const double eps = 1e-7 * std::sqrt(1.0 + std::sqrt(dev_dot(h, u, u, n))) / vn;
+      const double eps = kEulerFdEps * std::sqrt(1.0 + std::sqrt(dev_dot(h, u, u, n))) / vn;
       h->tmp1.ensure(size_t(n));
       h->tmp2.ensure(size_t(n));
       stg::vec_copy(h->tmp1.p, u, n, h->stream);
       stg::vec_axpy(h->tmp1.p, eps, v, n, h->stream);
       h->launches += 2;
       apply(h, m, 1, 1, h->tmp1.p, nullptr, nullptr, Jv, false, false);
-      apply(h, m, 1, 1, u, nullptr, nullptr, h->tmp2.p, false, false);
-      stg::vec_axpby(Jv, -1.0 / eps, h->tmp2.p, 1.0 / eps, n, h->stream);
+      stg::vec_axpy(h->tmp1.p, -2.0 * eps, v, n, h->stream);
+      h->launches++;
+      apply(h, m, 1, 1, h->tmp1.p, nullptr, nullptr, h->tmp2.p, false, false);
+      stg::vec_axpby(Jv, -0.5 / eps, h->tmp2.p, 0.5 / eps, n, h->stream);
       h->launches++;
       return;
     }

@@ -141,15 +141,19 @@ def test_admissibility_error_names_temporal_node():  # stdg.hpp:41-50, models.hp
     with pytest.raises(AdmissibilityError, match="temporal node 1"):
         op.st_residual(0.0, 0.01, dev(good), dev(U))
     # the handle recovers
-    assert rel(op.st_residual(0.0, 0.01, dev(good), dev(np.concatenate([good, good]))),
-               pr.st_residual(0.0, 0.01, good, np.concatenate([good, good]))) <= TOL_OP
+    v = vortex_u(pr)
+    V = np.concatenate([v, v * 1.01])
+    assert rel(op.st_residual(0.0, 0.01, dev(v), dev(V)), pr.st_residual(0.0, 0.01, v, V)) <= TOL_OP
 
 
 def test_general_models_reject_block_preconditioners():
-    op, _ = pulse_pair(4, 1)
-    un = dev(np.zeros(op.n_sdof))
-    with pytest.raises(ValueError):
-        op.stdg_step(0.0, 0.1, un, NewtonConfig(precond=L.STG_PRECOND_TBLOCK))
+    op, pr = pulse_pair(4, 1)
+    v = dev(np.ones(op.n_dof))
+    for pc in (L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK):
+        with pytest.raises(ValueError):
+            op.st_precond_apply(0.1, v, precond=pc)
+    # AUTO resolves to no preconditioner: P^-1 = I
+    assert float((op.st_precond_apply(0.1, v) - v).abs().max()) == 0.0
 
 
 def test_pulse_slab_solves_match_oracle():
