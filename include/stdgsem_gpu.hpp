@@ -11,7 +11,8 @@
 // role); each call moves them to the device once, runs there, and copies the
 // result back.  For device-resident loops use the DeviceVec overloads.
 // Status codes map back to std::invalid_argument / std::runtime_error /
-// NonconvergenceError; CUDA failures throw CudaError (there is no CPU path).
+// NonconvergenceError / AdmissibilityError; CUDA failures throw CudaError
+// (there is no CPU path).
 #pragma once
 
 #include <memory>
@@ -31,6 +32,11 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// AdmissibilityError (models.hpp:15-20); the message names the temporal node.
+struct AdmissibilityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 struct NonconvergenceError : std::runtime_error {
   Vec last_iterate;
   std::vector<double> residual_history;
@@ -45,6 +51,7 @@ inline void check(int code, const stg_handle* h) {
     case STG_ERR_INVALID: throw std::invalid_argument(msg);
     case STG_ERR_NONCONVERGENCE: throw NonconvergenceError(msg, {});
     case STG_ERR_CUDA: throw CudaError(msg);
+    case STG_ERR_ADMISSIBILITY: throw AdmissibilityError(msg);
     default: throw std::runtime_error(msg);
   }
 }
@@ -99,28 +106,73 @@ inline Mesh uniform_mesh(int d, const std::vector<double>& lower,
   return Mesh{d, lower, upper, cells};
 }
 
-struct DgSpace {  // mesh.hpp:59-91 (r = 1)
+struct DgSpace {  // mesh.hpp:59-91
   Mesh mesh;
   int p = 1;
+  int r = 1;  // components per node
   int dof() const {
     int npc = 1, nc = 1;
     for (int a = 0; a < mesh.d; ++a) {
       npc *= p + 1;
       nc *= mesh.cells[size_t(a)];
     }
-    return npc * nc;
+    return r * npc * nc;
   }
 };
-inline DgSpace dg_space(const Mesh& m, int p) { return DgSpace{m, p}; }
+inline DgSpace dg_space(const Mesh& m, int p, int r = 1) {  // mesh.hpp:93-110
+  if (p < 1) throw std::invalid_argument("dg_space: need p >= 1 (p = 0 has no LGL rule)");
+  if (r < 1) throw std::invalid_argument("dg_space: need r >= 1");
+  return DgSpace{m, p, r};
+}
 
-struct FluxModel {  // models.hpp:23-36, constant-velocity advection or Burgers
+// FluxModel (models.hpp:23-36): which of the library's models, with its data.
+struct FluxModel {
   int kind = STG_MODEL_ADVECTION;
+  std::vector<double> b;               // constant velocity
+  int field = STG_FIELD_CONSTANT;      // advdiff velocity field
+  double eps = 0.0;                    // advdiff diffusion
+  double gamma = 1.4;                  // euler
+  int r = 1;
+};
+// VelocityField (models.hpp:38): constant b, or rotating_field() (models.hpp:79-85)
+struct VelocityField {
+  int kind = STG_FIELD_CONSTANT;
   std::vector<double> b;
 };
-inline FluxModel advection_model(const std::vector<double>& b) {
-  return FluxModel{STG_MODEL_ADVECTION, b};
+inline VelocityField rotating_field() { return VelocityField{STG_FIELD_ROTATING, {0.0, 0.0}}; }
+inline VelocityField constant_field(const std::vector<double>& b) {
+  return VelocityField{STG_FIELD_CONSTANT, b};
 }
-inline FluxModel burgers_model() { return FluxModel{STG_MODEL_BURGERS, {0.0}}; }
+inline FluxModel advection_model(const std::vector<double>& b) {  // models.hpp:40-66
+  FluxModel m;
+  m.b = b;
+  return m;
+}
+inline FluxModel burgers_model() {  // EXTENSION (not in the reference)
+  FluxModel m;
+  m.kind = STG_MODEL_BURGERS;
+  m.b = {0.0};
+  return m;
+}
+inline FluxModel advdiff_model(int d, const VelocityField& b, double eps) {  // models.hpp:68-76
+  if (eps < 0) throw std::invalid_argument("advdiff_model: need eps >= 0");
+  FluxModel m;
+  m.kind = STG_MODEL_ADVDIFF;
+  m.b = b.b;
+  m.b.resize(size_t(d), 0.0);
+  m.field = b.kind;
+  m.eps = eps;
+  return m;
+}
+inline FluxModel euler_model(double gamma = 1.4) {  // models.hpp:118-159, r = 4, d = 2
+  if (!(gamma > 1.0)) throw std::invalid_argument("euler_model: gamma > 1");
+  FluxModel m;
+  m.kind = STG_MODEL_EULER;
+  m.b = {0.0, 0.0};
+  m.gamma = gamma;
+  m.r = 4;
+  return m;
+}
 
 enum class LinearMethod { auto_select = STG_LINEAR_AUTO, gmres = STG_LINEAR_GMRES };
 enum class JacobianForm { a_form = STG_FORM_A, a_inv_form = STG_FORM_A_INV };
@@ -144,12 +196,16 @@ struct NewtonConfig {  // newton.hpp:30-38
 // The slab operator for one (space, model, n_tau): owns a C-ABI handle.
 class SlabOperator {
  public:
-  SlabOperator(const DgSpace& space, const FluxModel& model, int n_tau) {
+  SlabOperator(const DgSpace& space, const FluxModel& model, int n_tau, double eta = 0.0) {
     stg_desc d{};
     d.dim = space.mesh.d;
     d.degree = space.p;
     d.n_tau = n_tau;
     d.model = model.kind;
+    d.velocity_field = model.field;
+    d.eps = model.eps;
+    d.eta = eta;
+    d.gamma = model.gamma;
     for (int a = 0; a < 3; ++a) {
       d.cells[a] = a < d.dim ? space.mesh.cells[size_t(a)] : 1;
       d.lower[a] = a < d.dim ? space.mesh.lower[size_t(a)] : 0.0;
@@ -180,13 +236,15 @@ class SlabOperator {
 // operator per number of temporal nodes.
 class SemiDiscreteSystem {
  public:
-  SemiDiscreteSystem(DgSpace space, FluxModel model)
-      : space_(std::move(space)), model_(std::move(model)) {}
+  SemiDiscreteSystem(DgSpace space, FluxModel model, double eta = 0.0)
+      : space_(std::move(space)), model_(std::move(model)), eta_(eta) {}
   int dof() const { return space_.dof(); }
+  // the interior-penalty parameter in use (spatial.hpp:366 default 10 p^2)
+  double eta() const { return eta_ > 0 ? eta_ : 10.0 * space_.p * space_.p; }
   SlabOperator& op(int n_tau) const {
     for (auto& e : ops_)
       if (e.first == n_tau) return *e.second;
-    ops_.emplace_back(n_tau, std::make_shared<SlabOperator>(space_, model_, n_tau));
+    ops_.emplace_back(n_tau, std::make_shared<SlabOperator>(space_, model_, n_tau, eta_));
     return *ops_.back().second;
   }
   // rhs(t, u) = F(u) (spatial.hpp:107-266)
@@ -200,13 +258,20 @@ class SemiDiscreteSystem {
  private:
   DgSpace space_;
   FluxModel model_;
+  double eta_ = 0.0;
   mutable std::vector<std::pair<int, std::shared_ptr<SlabOperator>>> ops_;
 };
 
-inline SemiDiscreteSystem assemble_semidiscrete(const DgSpace& space, const FluxModel& model) {
+// assemble_semidiscrete (spatial.hpp:352-385); eta <= 0: the default 10 p^2.
+inline SemiDiscreteSystem assemble_semidiscrete(const DgSpace& space, const FluxModel& model,
+                                                double eta = 0.0) {
   if (model.kind == STG_MODEL_ADVECTION && int(model.b.size()) != space.mesh.d)
     throw std::invalid_argument("assemble_semidiscrete: dimension mismatch");
-  return SemiDiscreteSystem(space, model);
+  if (model.kind == STG_MODEL_EULER && space.mesh.d != 2)
+    throw std::invalid_argument("assemble_semidiscrete: dimension mismatch");
+  if (model.r != space.r)
+    throw std::invalid_argument("assemble_semidiscrete: component mismatch");
+  return SemiDiscreteSystem(space, model, eta);
 }
 
 struct SbpOperators {  // operators.hpp:16-22 (the library builds D, M itself)

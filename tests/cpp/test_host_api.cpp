@@ -208,6 +208,39 @@ static void test_3d_free_stream() {  // EXTENSION: d = 3 (acceptance.cpp:334-343
   CHECK(maxabs(st_residual(e, Vec(size_t(4 * dof), 0.37))) <= 1e-12);
 }
 
+static void test_general_models() {  // test_spatial.cpp:67-89, models.hpp:108-113
+  auto pulse = assemble_semidiscrete(dg_space(uniform_mesh(2, {0, 0}, {1, 1}, {5, 5}), 3),
+                                     advdiff_model(2, rotating_field(), 0.001));
+  CHECK(pulse.eta() == 90.0);
+  CHECK(maxabs(pulse.rhs(0.0, Vec(size_t(pulse.dof()), -0.6))) <= 1e-12);
+  auto euler = assemble_semidiscrete(
+      dg_space(uniform_mesh(2, {-10, -10}, {10, 10}, {4, 4}), 1, 4), euler_model(1.4));
+  Vec c3(size_t(euler.dof()));
+  for (size_t i = 0; i < c3.size(); i += 4) {
+    c3[i] = 1.0;
+    c3[i + 1] = 0.3;
+    c3[i + 2] = -0.2;
+    c3[i + 3] = 2.5;
+  }
+  CHECK(maxabs(euler.rhs(0.0, c3)) <= 1e-12);
+  Vec bad = c3;
+  for (size_t i = 0; i < bad.size(); i += 4) bad[i + 1] = 4.0, bad[i + 3] = 1.0;
+  bool threw = false;
+  try {
+    euler.rhs(0.0, bad);
+  } catch (const AdmissibilityError&) {
+    threw = true;
+  }
+  CHECK(threw);
+  bool mismatch = false;
+  try {
+    assemble_semidiscrete(dg_space(uniform_mesh(1, {0}, {1}, {4}), 1, 4), euler_model());
+  } catch (const std::invalid_argument&) {
+    mismatch = true;
+  }
+  CHECK(mismatch);
+}
+
 int main() {
   test_stdg_equals_rk();
   test_st_residual_constant_and_dt();
@@ -217,6 +250,7 @@ int main() {
   test_linear_one_newton_iteration();
   test_nonconvergence_context();
   test_3d_free_stream();
+  test_general_models();
   std::printf("passed %d failed %d\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }
