@@ -584,6 +584,190 @@ __global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
 }
 
 // ---------------------------------------------------------------------------
+// d = 2, S diagonal (st_residual, J.v, A^-1-form stage residual): one thread
+// per (cell, temporal node) PLANE.  With S diagonal, F(X_t) only enters row
+// t of the mix, so the thread that owns plane t of a cell computes the whole
+// output plane R_t = sum_j T(t,j) X_j + S(t,t) F(X_t) + c_t W in registers:
+// the x and y derivatives on its n x n register tile, the temporal mix from
+// the other planes of the staged tile, no intermediate buffer and no phase
+// barrier.  E cells per segment; the tile (n_tau planes of E*n^2 doubles,
+// plus u_n when present) arrives by bulk copy in a 2-stage ring; R is staged
+// back into the consumed stage and written by bulk stores (full lines, no
+// partial-sector write traffic).  Lanes are consecutive cells: a plane stride
+// of n^2 = 25 doubles (odd) keeps the 64-bit shared accesses conflict-free.
+// ---------------------------------------------------------------------------
+template <int N1, int NT, int E>
+struct Plane2d {
+  static constexpr int NPC = N1 * N1;
+  static constexpr int THREADS = E * NT;
+  static constexpr int PLANE = E * NPC;                 // doubles per plane
+  static constexpr int STAGE = (NT + 1) * PLANE;        // NT planes + u_n
+  static constexpr int SMEM = (2 * STAGE + NT * PLANE) * 8 + 64;  // 2 stages + R staging
+  static_assert(PLANE % 2 == 0, "16-byte aligned planes");
+};
+
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<uint64_t>(dst)),
+               "r"(src), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read0() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <int N1, int NT, int E, int MINB>
+__global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
+    slab2d_plane(const SlabArgs a) {
+  using P = Plane2d<N1, NT, E>;
+  constexpr int NPC = P::NPC, PL = P::PLANE;
+  extern __shared__ __align__(16) double sm2[];
+  double* Rs = sm2 + 2 * P::STAGE;  // output staging (NT planes)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Rs + NT * PL);
+  const uint32_t bar0 = ptx::smem_u32(bars), bar1 = ptx::smem_u32(bars + 1);
+  const int tid = threadIdx.x;
+  const int e = tid % E, t = tid / E;
+  const int nx = a.g.nx, ny = a.g.ny;
+  const long long ns = a.g.n_sdof;
+  const int nseg = a.g.n_cells / E;
+  const uint32_t pbytes = PL * 8;
+  const bool hw = a.has_w != 0;
+  const uint32_t sbytes = (NT + (hw ? 1 : 0)) * pbytes;
+  const bool nLx = a.sp.cL[0] != 0.0, nRx = a.sp.cR[0] != 0.0;
+  const bool nLy = a.sp.cL[1] != 0.0, nRy = a.sp.cR[1] != 0.0;
+  double Tr[NT];  // this thread's row of the mix
+#pragma unroll
+  for (int j = 0; j < NT; ++j) Tr[j] = a.mx.T[t][j];
+  const double tt_ = a.mx.T[t][t], st_ = a.mx.S[t][t], ct_ = hw ? a.mx.c[t] : 0.0;
+
+  if (tid == 0) {
+    ptx::mbar_init(bar0, 1);
+    ptx::mbar_init(bar1, 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](int seg, int stg) {
+    const uint32_t bar = stg ? bar1 : bar0;
+    ptx::mbar_expect_tx(bar, sbytes);
+    const uint32_t dst = ptx::smem_u32(sm2 + stg * P::STAGE);
+    const double* src = a.X + (long long)seg * PL;
+    for (int j = 0; j < NT; ++j) bulk_g2s(dst + j * pbytes, src + j * ns, pbytes, bar);
+    if (hw) bulk_g2s(dst + NT * pbytes, a.W + (long long)seg * PL, pbytes, bar);
+  };
+  // neighbour traces that are not in the tile (global / L2)
+  auto faces = [&](int seg, double* xl, double* xr, double* yl, double* yr) {
+    const int cell = seg * E + e;
+    const int cx = cell % nx, cy = (cell / nx) % ny;
+    const double* Xt = a.X + t * ns;
+    if (nLx && !(e > 0 && cx > 0)) {
+      const double* q = Xt + (long long)(cell - cx + (cx == 0 ? nx - 1 : cx - 1)) * NPC + N1 - 1;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xl[k] = q[k * N1];
+    }
+    if (nRx && !(e < E - 1 && cx < nx - 1)) {
+      const double* q = Xt + (long long)(cell - cx + (cx == nx - 1 ? 0 : cx + 1)) * NPC;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xr[k] = q[k * N1];
+    }
+    if (nLy) {
+      const double* q = Xt + (long long)(cell + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx) * NPC +
+                        (N1 - 1) * N1;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) yl[k] = q[k];
+    }
+    if (nRy) {
+      const double* q = Xt + (long long)(cell + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx) * NPC;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) yr[k] = q[k];
+    }
+  };
+
+  int seg = blockIdx.x;
+  if (tid == 0 && seg < nseg) issue(seg, 0);
+  double xl[N1], xr[N1], yl[N1], yr[N1];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) xl[k] = xr[k] = yl[k] = yr[k] = 0.0;
+  if (seg < nseg) faces(seg, xl, xr, yl, yr);
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int stg = it & 1;
+    const int nxt = seg + gridDim.x;
+    if (tid == 0 && nxt < nseg) {
+      ptx::fence_proxy_async_smem();
+      issue(nxt, stg ^ 1);
+    }
+    const double* X = sm2 + stg * P::STAGE;
+    while (!ptx::mbar_try_wait(stg ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+    const int cell = seg * E + e;
+    const int cx = cell % nx;
+    const double* own = X + t * PL + e * NPC;
+    double u[NPC];
+#pragma unroll
+    for (int k = 0; k < NPC; ++k) u[k] = own[k];
+    if (nLx && e > 0 && cx > 0) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xl[k] = own[-NPC + k * N1 + N1 - 1];
+    }
+    if (nRx && e < E - 1 && cx < nx - 1) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xr[k] = own[NPC + k * N1];
+    }
+    double r[NPC];
+#pragma unroll
+    for (int iy = 0; iy < N1; ++iy)
+#pragma unroll
+      for (int ix = 0; ix < N1; ++ix) {
+        double g = 0.0;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) g = fma(a.sp.V[0][ix][k], u[iy * N1 + k], g);
+#pragma unroll
+        for (int k = 0; k < N1; ++k) g = fma(a.sp.V[1][iy][k], u[k * N1 + ix], g);
+        if (ix == 0) g = fma(a.sp.cL[0], xl[iy], g);
+        if (ix == N1 - 1) g = fma(a.sp.cR[0], xr[iy], g);
+        if (iy == 0) g = fma(a.sp.cL[1], yl[ix], g);
+        if (iy == N1 - 1) g = fma(a.sp.cR[1], yr[ix], g);
+        r[iy * N1 + ix] = fma(st_, g, tt_ * u[iy * N1 + ix]);
+      }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j == t) continue;
+      const double* pj = X + j * PL + e * NPC;
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) r[k] = fma(Tr[j], pj[k], r[k]);
+    }
+    if (hw && ct_ != 0.0) {
+      const double* pw = X + NT * PL + e * NPC;
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) r[k] = fma(ct_, pw[k], r[k]);
+    }
+    // prefetch the next segment's out-of-tile traces
+    if (nxt < nseg) faces(nxt, xl, xr, yl, yr);
+    // the previous segment's bulk stores must have read Rs before it is rewritten
+    if (tid == 0) bulk_wait_read0();
+    __syncthreads();  // also: every thread has read stage stg (it is refilled next iteration)
+    double* outp = Rs + t * PL + e * NPC;
+#pragma unroll
+    for (int k = 0; k < NPC; ++k) outp[k] = r[k];
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < NT; ++j)
+        bulk_s2g(a.R + j * ns + (long long)seg * PL, ptx::smem_u32(Rs + j * PL), pbytes);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
 // d = 3, N = 3, n_tau = 4: TMA-staged, register-tiled two-phase kernel
 // ---------------------------------------------------------------------------
 namespace fast {
@@ -1143,12 +1327,53 @@ int num_sms_cached() {
   return n;
 }
 
+// E = 32 cells per segment for the plane kernel (lanes = cells)
+static const int kPlaneEnv = [] {
+  const char* v = std::getenv("STG_2D_PLANE_E");
+  return v ? std::atoi(v) : 32;
+}();
+
+template <int N1, int NT, int E>
+bool plane2d_ok(const SlabArgs& a) {
+  using P = Plane2d<N1, NT, E>;
+  return !a.full_s && a.n_in == NT && a.n_out == NT && a.g.n_cells % E == 0 &&
+         (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 &&
+         (!a.has_w || (reinterpret_cast<uintptr_t>(a.W) & 15) == 0) && a.g.n_sdof % 2 == 0 &&
+         P::SMEM <= 227 * 1024 && !std::getenv("STG_2D_V1");
+}
+
+template <int N1, int NT, int E, int MINB>
+int launch_plane2d(const SlabArgs& a, cudaStream_t s) {
+  using Q = Plane2d<N1, NT, E>;
+  static int occ = -1;
+  if (occ < 0) {
+    cudaFuncSetAttribute(slab2d_plane<N1, NT, E, MINB>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane<N1, NT, E, MINB>,
+                                                  Q::THREADS, Q::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  const int nseg = a.g.n_cells / E;
+  int grid = occ * num_sms_cached();
+  if (grid > nseg) grid = nseg;
+  slab2d_plane<N1, NT, E, MINB><<<grid, Q::THREADS, Q::SMEM, s>>>(a);
+  return 1;
+}
+
 template <int N1, int NT>
 int launch2d_t(const SlabArgs& a, cudaStream_t s) {
   using Sh = Shape2d<N1, NT>;
   using P = P2d<N1, NT>;
-  const bool aligned = (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 && (a.g.n_sdof % 2) == 0;
-  if (a.g.n_cells % Sh::E == 0 && aligned && !std::getenv("STG_2D_NONPERSIST")) {
+  if constexpr (N1 <= 5) {  // n = 6 would spill the register tile
+    if (kPlaneEnv == 16 && plane2d_ok<N1, NT, 16>(a)) return launch_plane2d<N1, NT, 16, 3>(a, s);
+    if (kPlaneEnv == 33 && plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 1>(a, s);
+    // 2 CTAs/SM: caps the tile kernel at 200 registers (202 would round to
+    // 6656 per warp and leave room for one 160-thread CTA only)
+    if (plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 2>(a, s);
+  }
+  if (a.g.n_cells % Sh::E == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
+      (a.g.n_sdof % 2) == 0 && !std::getenv("STG_2D_NONPERSIST")) {
     static int occ = -1;
     if (occ < 0) {
       cudaFuncSetAttribute(slab2d_persist<N1, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
