@@ -22,7 +22,7 @@ LIB = PKG / "libstg_cuda.so"
 OBJDIR = PKG / "build_obj"
 
 SOURCES = ["kernels_slab.cu", "kernels_vec.cu", "kernels_precond.cu", "kernels_fdm.cu",
-           "kernels_general.cu", "stg.cpp"]
+           "kernels_general.cu", "kernels_small.cu", "stg.cpp"]
 HEADERS = ["kernels.hpp", "constants.hpp", "eig.hpp", "ptx.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",

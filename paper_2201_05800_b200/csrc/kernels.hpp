@@ -116,6 +116,33 @@ struct GenArgs {
 // Returns the number of kernels launched, or -1 if (d, n, r) is unsupported.
 int launch_general(const GenArgs& a, cudaStream_t s);
 
+// ---- fused small-problem Newton-GMRES (kernels_small.cu) -------------------
+constexpr int kSmallMaxRestart = 30;
+#define STG_MAX_HISTORY_DEV 64
+struct SmallSolveOut {
+  int status;  // 0 ok, 1 Newton did not converge, 2 GMRES did not converge
+  int newton_iterations, linear_iterations, n_history;
+  double final_residual, gmres_rel;
+  double history[STG_MAX_HISTORY_DEV];
+};
+struct SmallSolveArgs {
+  SpatialCoef sp;
+  MixCoef mx_res, mx_jac, mx_next;  // residual (with W), Jacobian, rk u_next
+  int n, K, nt, n1;                  // n = nt * ns
+  long long ns, ld;                  // spatial size, basis leading dimension
+  int restart, max_it, max_iter, rk;
+  double tol, abs_tol, rel_tol;
+  const double* W;    // u_n (stdg) or u (rk)
+  const double* B;    // element-block inverse (nt*n1)^2 or null (no preconditioner)
+  double* V;          // basis workspace, (restart + 1) * ld (vectors not held in smem)
+  int basis_in_smem;  // set by the launcher
+  double* U_out;      // n
+  double* u_next;     // ns or null
+  SmallSolveOut* out;
+};
+bool small_solve_supported(const Geometry& g, int nt, int model, int restart);
+int launch_small_solve(SmallSolveArgs a, cudaStream_t s);
+
 // ---- element-block Jacobi by fast diagonalisation, d = 3 N = 3 n_tau = 4
 // (kernels_fdm.cu).  Complex entries are stored [re, im]; x eigen-indices are
 // kept for one member of each conjugate pair (kx = 2j, j = 0, 1).

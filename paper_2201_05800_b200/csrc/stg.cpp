@@ -95,6 +95,7 @@ struct stg_handle {
   DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
   DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
   DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
+  DevBuf small_out;      // fused small-solve result record
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
@@ -600,9 +601,8 @@ void st_residual(stg_handle* h, double dt, const double* un, const double* U, do
   apply(h, st_mix(h, dt, un != nullptr), h->nt, h->nt, U, nullptr, un, R, false, false);
 }
 
-// Forward-difference Jacobian action [R(U + h v) - R(U)] / h of the slab /
-// stage residual without its constant (u_n / u) coupling, which cancels.
-// [R0(U + h v) - R0(U - h v)] / 2h with
+// Central-difference Jacobian action of the slab / stage residual without its
+// constant (u_n / u) coupling, which cancels: [R0(U + h v) - R0(U - h v)] / 2h with
 // h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (the Walker-Pernice differencing
 // parameter, as in PETSc's MFFD "wp"), so the perturbation is relative to the
 // state regardless of the scaling of the Krylov vector v.
@@ -872,6 +872,26 @@ int resolve_precond(const stg_handle* h, int kind) {
   return kind;
 }
 
+// Inverse of the (shared) element block of the d = 1 advection Jacobian with
+// temporal mixing (T, S): rows / columns (r, i), (j, q) of the element-local
+// block T (x) I + S (x) V.  Uploaded to h->ptab; returns the device pointer.
+const double* eblock_table_1d(stg_handle* h, const stg::MixCoef& mx) {
+  const int nt = h->nt, n1 = h->n1, nb = nt * n1;
+  std::vector<double> B(size_t(nb) * nb);
+  for (int r = 0; r < nt; ++r)
+    for (int i = 0; i < n1; ++i)
+      for (int j = 0; j < nt; ++j)
+        for (int q = 0; q < n1; ++q)
+          B[size_t(r * n1 + i) * nb + size_t(j * n1 + q)] =
+              (i == q ? mx.T[r][j] : 0.0) + mx.S[r][j] * h->sp.V[0][i][q];
+  const std::vector<double> Bi = stg::inverse(B, nb);
+  h->ptab.ensure(Bi.size());
+  ck(cudaMemcpyAsync(h->ptab.p, Bi.data(), sizeof(double) * Bi.size(), cudaMemcpyHostToDevice,
+                     h->stream), "H2D");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  return h->ptab.p;
+}
+
 // Right preconditioner for the Jacobian with temporal mixing (T, S) at the
 // linearisation point U (used by the Burgers element blocks only).
 Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U) {
@@ -918,18 +938,7 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
   const int ncells = h->g.n_cells;
   long long bstride = 0;
   if (h->desc.model == STG_MODEL_ADVECTION) {
-    std::vector<double> B(size_t(nb) * nb);
-    for (int r = 0; r < nt; ++r)
-      for (int i = 0; i < n1; ++i)
-        for (int j = 0; j < nt; ++j)
-          for (int q = 0; q < n1; ++q)
-            B[size_t(r * n1 + i) * nb + size_t(j * n1 + q)] =
-                (i == q ? mx.T[r][j] : 0.0) + mx.S[r][j] * h->sp.V[0][i][q];
-    const std::vector<double> Bi = stg::inverse(B, nb);
-    h->ptab.ensure(Bi.size());
-    ck(cudaMemcpyAsync(h->ptab.p, Bi.data(), sizeof(double) * Bi.size(), cudaMemcpyHostToDevice,
-                       h->stream), "H2D");
-    ck(cudaStreamSynchronize(h->stream), "sync");
+    eblock_table_1d(h, mx);
   } else {
     stg::SlabArgs a{};
     a.sp = h->sp;
@@ -961,6 +970,76 @@ stg_newton_config effective_cfg(const stg_newton_config* cfg) {
   return c;
 }
 
+// Whole Newton-GMRES solve in one single-CTA kernel (kernels_small.cu) for
+// small d = 1 advection problems (c1); false when not applicable.  Same
+// Newton / GMRES control flow, tolerances and error behaviour as the
+// host-driven path.
+bool small_solve(stg_handle* h, bool rk, const stg::MixCoef& mres, const stg::MixCoef& mjac,
+                 const stg::MixCoef& mnext, const double* W, const stg_newton_config& cfg,
+                 double* U, double* u_next, stg_solve_info* info, const std::string& ctx) {
+  static const bool off = std::getenv("STG_NO_FUSED_SMALL") != nullptr;
+  if (off || h->desc.model != STG_MODEL_ADVECTION || h->kernel_pref != STG_KERNEL_AUTO ||
+      !stg::small_solve_supported(h->g, h->nt, h->desc.model, cfg.gmres_restart))
+    return false;
+  const int kind = resolve_precond(h, cfg.precond);
+  if (kind != STG_PRECOND_NONE && kind != STG_PRECOND_EBLOCK) return false;
+  ensure_workspace(h);
+  stg::SmallSolveArgs a{};
+  a.sp = h->sp;
+  a.mx_res = mres;
+  a.mx_jac = mjac;
+  a.mx_next = mnext;
+  a.n = int(h->n_dof);
+  a.K = h->g.n_cells;
+  a.nt = h->nt;
+  a.n1 = h->n1;
+  a.ns = h->n_sdof;
+  a.ld = round_up(h->n_dof, 32);
+  a.restart = cfg.gmres_restart;
+  a.max_it = cfg.gmres_max_it;
+  a.max_iter = cfg.max_iter;
+  a.rk = rk ? 1 : 0;
+  a.tol = cfg.gmres_tol;
+  a.abs_tol = cfg.abs_tol;
+  a.rel_tol = cfg.rel_tol;
+  a.W = W;
+  a.B = kind == STG_PRECOND_EBLOCK ? eblock_table_1d(h, mjac) : nullptr;
+  h->basis.ensure(size_t(a.ld) * (a.restart + 1));
+  a.V = h->basis.p;
+  a.U_out = U;
+  a.u_next = u_next;
+  const size_t out_doubles = (sizeof(stg::SmallSolveOut) + 7) / 8;
+  h->small_out.ensure(out_doubles);
+  a.out = reinterpret_cast<stg::SmallSolveOut*>(h->small_out.p);
+  if (stg::launch_small_solve(a, h->stream) < 0) return false;
+  h->launches++;
+  check_launch(h);
+  stg::SmallSolveOut* o = reinterpret_cast<stg::SmallSolveOut*>(h->pinned + 512);
+  ck(cudaMemcpyAsync(o, a.out, sizeof(stg::SmallSolveOut), cudaMemcpyDeviceToHost, h->stream),
+     "memcpy");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  if (std::getenv("STG_SMALL_TRACE"))
+    std::fprintf(stderr, "small trace: res %.0f prec %.0f jac %.0f dots %.0f upd+norm %.0f cycles\n",
+                 o->history[40], o->history[41], o->history[42], o->history[43], o->history[44]);
+  NewtonOut out;
+  out.iterations = o->newton_iterations;
+  out.linear_iterations = o->linear_iterations;
+  out.final_residual = o->final_residual;
+  out.history.assign(o->history, o->history + o->n_history);
+  if (o->status == 1) {
+    fill_info(info, out);
+    throw NonconvergenceError(ctx + ": newton_solve: no convergence in " +
+                                  std::to_string(cfg.max_iter) + " iterations, residual " +
+                                  fmt_short(o->final_residual),
+                              out.history);
+  }
+  if (o->status == 2)
+    throw std::runtime_error("linear_solve: GMRES did not converge, error " +
+                             fmt_short(o->gmres_rel));
+  fill_info(info, out);
+  return true;
+}
+
 void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
                   const stg_newton_config* cfgp, double* U, double* u_next,
                   stg_solve_info* info) {
@@ -968,6 +1047,10 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
   if (!(dt > 0)) throw std::invalid_argument("stdg_step: dt > 0 required");
   const stg_newton_config cfg = effective_cfg(cfgp);
   const long long n = h->n_dof;
+  if (small_solve(h, false, st_mix(h, dt, true), st_mix(h, dt, false), zero_mix(), u_n, cfg, U,
+                  u_next, info,
+                  "stdg_step element at t=" + fmt_short(t_n) + ", dt=" + fmt_short(dt)))
+    return;
   stg::vec_broadcast(U, u_n, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u_n (stdg.hpp:131)
   h->launches++;
   const double eps = cfg.fd_eps;
@@ -1003,6 +1086,14 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
   if (form != STG_FORM_A && form != STG_FORM_A_INV) throw std::invalid_argument("bad form");
   const stg_newton_config cfg = effective_cfg(cfgp);
   const long long n = h->n_dof;
+  {
+    stg::MixCoef mn = zero_mix();  // u_next = u + dt sum_j b_j F(U_j)  (lodg.hpp:142-145)
+    for (int j = 0; j < h->nt; ++j) mn.S[0][j] = dt * h->tab.b[size_t(j)];
+    mn.c[0] = 1.0;
+    if (small_solve(h, true, stage_mix(h, form, dt, true), stage_mix(h, form, dt, false), mn, u,
+                    cfg, U, u_next, info, "rk_step at t=" + fmt_short(t) + ", dt=" + fmt_short(dt)))
+      return;
+  }
   stg::vec_broadcast(U, u, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u (lodg.hpp:131)
   h->launches++;
   const double eps = cfg.fd_eps;

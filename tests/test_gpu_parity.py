@@ -370,3 +370,45 @@ def test_launch_counter_counts_native_kernels():
     n0 = op.kernel_launches()
     op.st_residual(0.0, cfg.dt, dev(C.initial_state(cfg)), dev(C.random_slab(cfg)))
     assert op.kernel_launches() == n0 + 1
+
+
+@pytest.mark.parametrize("cells,degree,n_tau,vel", [((64,), 3, 4, (1.0,)), ((16,), 2, 3, (-0.8,)),
+                                                    ((40,), 4, 5, (1.3,))])
+def test_fused_small_solve_matches_host_driven(cells, degree, n_tau, vel):
+    """kernels_small.cu (one-CTA Newton-GMRES, AUTO) == the host-driven solver
+    (STG_KERNEL_GENERIC) for slab and stage solves, both preconditioners."""
+    cfg = make(1, degree, n_tau, cells, vel, dt=0.005)
+    fused = SlabOperator(**cfg.kwargs())
+    host = SlabOperator(**cfg.kwargs(), kernel=L.STG_KERNEL_GENERIC)
+    pr = O.Problem(1, degree, list(cells), [0.0], [1.0], list(vel), n_tau=n_tau)
+    un = C.initial_state(cfg)
+    for pc in (L.STG_PRECOND_AUTO, L.STG_PRECOND_NONE):
+        nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12, precond=pc)
+        Uf, uf, inf_f = fused.stdg_step(0.0, cfg.dt, dev(un), nc)
+        Uh, uh, inf_h = host.stdg_step(0.0, cfg.dt, dev(un), nc)
+        assert rel(Uf, Uh.cpu().numpy()) <= TOL_SOLVE
+        assert rel(uf, uh.cpu().numpy()) <= TOL_SOLVE
+        assert inf_f.newton_iterations == inf_h.newton_iterations
+        assert abs(inf_f.linear_iterations - inf_h.linear_iterations) <= 1
+        Uo, _, _, _ = pr.stdg_step(0.0, cfg.dt, un, linear=O.DENSE_LU if pr.dof * n_tau < 600
+                                   else O.GMRES, abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-13)
+        assert rel(Uf, Uo) <= TOL_SOLVE
+        if n_tau in (2, 3, 4):
+            for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
+                Uf, uf, _ = fused.rk_step(form, 0.0, cfg.dt, dev(un), nc)
+                Uh, uh, _ = host.rk_step(form, 0.0, cfg.dt, dev(un), nc)
+                assert rel(Uf, Uh.cpu().numpy()) <= TOL_SOLVE
+                assert rel(uf, uh.cpu().numpy()) <= TOL_SOLVE
+
+
+def test_fused_small_solve_errors_match():
+    cfg = C.CONFIGS["c1"]
+    op = SlabOperator(**cfg.kwargs())
+    un = dev(C.initial_state(cfg))
+    with pytest.raises(NonconvergenceError) as e:
+        op.stdg_step(0.5, cfg.dt, un, NewtonConfig(max_iter=0))
+    assert "stdg_step element at t=0.5" in str(e.value)
+    assert len(e.value.residual_history) == 1
+    with pytest.raises(RuntimeError, match="GMRES did not converge"):
+        op.stdg_step(0.0, cfg.dt, un, NewtonConfig(gmres_max_it=1, gmres_tol=1e-14,
+                                                   precond=L.STG_PRECOND_NONE))
