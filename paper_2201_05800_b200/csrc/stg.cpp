@@ -477,15 +477,17 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       for (int j = 0; j <= k; ++j) Hat(j, k) = hp[j];
       double hn = sigma;
       if (!(ww - hh > 1e-4 * ww) || std::abs(hp[64 + kk] - 1.0) > 1e-10) {
-        // re-orthogonalise the stored (scaled) vector: g2 = V^T vn, vn -= V g2
-        stg::vec_multidot(V, ld, kk, vn, n, h->partial.p, dsm + 128, s);
-        stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s);
-        stg::vec_scale_invsqrt(vn, vn, dsm + 64 + kk, n, s);
-        h->launches += 3;
+        // re-orthogonalise the stored (scaled) vector in two passes:
+        // [g2, <vn,vn>] = [V, vn]^T vn (vn is the basis slot after V_k), then
+        // vn = (vn - V g2) / sqrt(<vn,vn> - |g2|^2) (Pythagorean scale)
+        stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm + 128, s);
+        stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s, dsm + 128,
+                            dsm + 191);
+        h->launches += 2;
         ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
         ck(cudaStreamSynchronize(s), "sync");
         for (int j = 0; j <= k; ++j) Hat(j, k) += sigma * hp[128 + j];
-        hn = sigma * std::sqrt(hp[64 + kk]);
+        hn = sigma / hp[191];  // hp[191] = 1 / ||vn - V g2||
         h->reorth++;
       }
       if (!(ww > 0.0)) hn = 0.0;  // exact breakdown: A P^-1 v_k = 0
@@ -1018,9 +1020,6 @@ bool small_solve(stg_handle* h, bool rk, const stg::MixCoef& mres, const stg::Mi
   ck(cudaMemcpyAsync(o, a.out, sizeof(stg::SmallSolveOut), cudaMemcpyDeviceToHost, h->stream),
      "memcpy");
   ck(cudaStreamSynchronize(h->stream), "sync");
-  if (std::getenv("STG_SMALL_TRACE"))
-    std::fprintf(stderr, "small trace: res %.0f prec %.0f jac %.0f dots %.0f upd+norm %.0f cycles\n",
-                 o->history[40], o->history[41], o->history[42], o->history[43], o->history[44]);
   NewtonOut out;
   out.iterations = o->newton_iterations;
   out.linear_iterations = o->linear_iterations;
