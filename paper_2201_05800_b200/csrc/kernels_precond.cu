@@ -82,105 +82,139 @@ __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
 // Build and invert the element blocks of the 1-D Burgers slab / stage Jacobian
 // at U: column (j, q) = element response to a unit input at temporal node j,
 // node q (neighbour inputs zero; neighbour STATES enter through the exact
-// linearisation).  One thread per element; Gauss-Jordan with partial
-// pivoting on a thread-private (local-memory) nb x 2nb tableau.
-template <int N1>
+// linearisation).  One warp per element: lane l < NB owns row l = (r, i) of
+// the block and of the identity, in registers.  Gauss-Jordan with partial
+// pivoting WITHOUT row exchanges: at column `col` the unused lane with the
+// largest |a[col]| (lowest lane on ties) becomes the pivot; its normalised
+// row is broadcast by shuffles and eliminated from every other lane.  At the
+// end the pivot lane of column col holds row col of the inverse.
+template <int N1, int NT>
 __global__ void __launch_bounds__(128) k_build_burgers_eblock(double* __restrict__ Binv,
                                                               const double* __restrict__ U,
                                                               const SlabArgs a) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  constexpr int NB = N1 * NT;
+  static_assert(NB <= 32, "one lane per block row");
+  const int lane = threadIdx.x & 31;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int K = a.g.nx;
-  if (c >= K) return;
-  const int nt = a.n_in;
-  const int nb = nt * N1;
+  if (c >= K) return;  // warp-uniform
   const long long ns = a.g.n_sdof;
   const int cl = c == 0 ? K - 1 : c - 1, cr = c == K - 1 ? 0 : c + 1;
-  double* M = Binv + (size_t)c * nb * nb;  // built in place, then inverted
-  double aug[kMaxT * N1][kMaxT * N1];       // local memory
-  // J_F(U_j) restricted to the element, for every temporal node j
-  double jf[kMaxT][N1][N1];
-  for (int j = 0; j < nt; ++j) {
+  const bool act = lane < NB;
+  const int r = act ? lane / N1 : 0, i = act ? lane - (lane / N1) * N1 : 0;
+  double row[NB], inv[NB];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) {
     double u[N1];
-    for (int i = 0; i < N1; ++i) u[i] = U[j * ns + (long long)c * N1 + i];
+#pragma unroll
+    for (int k = 0; k < N1; ++k) u[k] = U[j * ns + (long long)c * N1 + k];
     const double ul = U[j * ns + (long long)cl * N1 + N1 - 1];
     const double ur = U[j * ns + (long long)cr * N1];
+#pragma unroll
     for (int q = 0; q < N1; ++q) {
-      // derivative of F_i w.r.t. u_q (own element; neighbours held fixed)
-      for (int i = 0; i < N1; ++i) {
-        double vol = 0.0;
-        for (int k = 0; k < N1; ++k) {
-          const double dvi = (i == q ? 1.0 : 0.0), dvk = (k == q ? 1.0 : 0.0);
-          vol += 2.0 * a.sp.Dm[i][k] *
-                 ((2.0 * u[i] + u[k]) * dvi + (u[i] + 2.0 * u[k]) * dvk) / 6.0;
-        }
-        double g = -a.sp.sc * vol;
-        if (i == N1 - 1 && q == N1 - 1) {
-          // d/duL of LLF(uL, ur) - f(uL) at the right face
-          const double aL = fabs(u[N1 - 1]), aR = fabs(ur);
-          double dH;
-          if (aL >= aR)
-            dH = 0.5 * u[N1 - 1] + 0.5 * (u[N1 - 1] >= 0 ? 1.0 : -1.0) * (u[N1 - 1] - ur) + 0.5 * aL;
-          else
-            dH = 0.5 * u[N1 - 1] + 0.5 * aR;
-          g -= a.sp.sc * (dH - u[N1 - 1]) * a.sp.inv_wN;
-        }
-        if (i == 0 && q == 0) {
-          // d/duR of LLF(ul, uR) - f(uR) at the left face
-          const double aL = fabs(ul), aR = fabs(u[0]);
-          double dH;
-          if (aL >= aR)
-            dH = 0.5 * u[0] - 0.5 * aL;
-          else
-            dH = 0.5 * u[0] + 0.5 * (u[0] >= 0 ? 1.0 : -1.0) * (ul - u[0]) - 0.5 * aR;
-          g += a.sp.sc * (dH - u[0]) * a.sp.inv_w0;
-        }
-        jf[j][i][q] = g;
+      // d F_i(U_j) / d u_q: own element, neighbour states fixed
+      double vol = 0.0;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) {
+        const double dvi = (i == q ? 1.0 : 0.0), dvk = (k == q ? 1.0 : 0.0);
+        vol += 2.0 * a.sp.Dm[i][k] * ((2.0 * u[i] + u[k]) * dvi + (u[i] + 2.0 * u[k]) * dvk) / 6.0;
+      }
+      double g = -a.sp.sc * vol;
+      if (i == N1 - 1 && q == N1 - 1) {  // d/duL of LLF(uL, ur) - f(uL), right face
+        const double aL = fabs(u[N1 - 1]), aR = fabs(ur);
+        const double dH = aL >= aR
+                              ? 0.5 * u[N1 - 1] + 0.5 * (u[N1 - 1] >= 0 ? 1.0 : -1.0) *
+                                                      (u[N1 - 1] - ur) + 0.5 * aL
+                              : 0.5 * u[N1 - 1] + 0.5 * aR;
+        g -= a.sp.sc * (dH - u[N1 - 1]) * a.sp.inv_wN;
+      }
+      if (i == 0 && q == 0) {  // d/duR of LLF(ul, uR) - f(uR), left face
+        const double aL = fabs(ul), aR = fabs(u[0]);
+        const double dH = aL >= aR ? 0.5 * u[0] - 0.5 * aL
+                                   : 0.5 * u[0] + 0.5 * (u[0] >= 0 ? 1.0 : -1.0) * (ul - u[0]) -
+                                         0.5 * aR;
+        g += a.sp.sc * (dH - u[0]) * a.sp.inv_w0;
+      }
+      row[j * N1 + q] = act ? (i == q ? a.mx.T[r][j] : 0.0) + a.mx.S[r][j] * g : 0.0;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NB; ++q) inv[q] = (q == lane) ? 1.0 : 0.0;
+  bool used = !act;
+  int my_col = 0;
+#pragma unroll
+  for (int col = 0; col < NB; ++col) {
+    // pivot lane: max |row[col]| among unused lanes, lowest lane on ties
+    double v = used ? -1.0 : fabs(row[col]);
+    int idx = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (v2 > v || (v2 == v && i2 < idx)) {
+        v = v2;
+        idx = i2;
+      }
+    }
+    const int p = idx;
+    const double ip = 1.0 / __shfl_sync(0xffffffffu, row[col], p);
+    if (lane == p) {
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        row[q] *= ip;
+        inv[q] *= ip;
+      }
+      used = true;
+      my_col = col;
+    }
+    const double f = row[col];
+#pragma unroll
+    for (int q = 0; q < NB; ++q) {
+      const double pr = __shfl_sync(0xffffffffu, row[q], p);
+      const double pi = __shfl_sync(0xffffffffu, inv[q], p);
+      if (lane != p) {
+        row[q] = fma(-f, pr, row[q]);
+        inv[q] = fma(-f, pi, inv[q]);
       }
     }
   }
-  // block (r,i),(j,q) = T(r,j) delta_iq + S(r,j) jf[j][i][q]
-  for (int r = 0; r < nt; ++r)
-    for (int i = 0; i < N1; ++i)
-      for (int j = 0; j < nt; ++j)
-        for (int q = 0; q < N1; ++q) {
-          aug[r * N1 + i][j * N1 + q] =
-              (i == q ? a.mx.T[r][j] : 0.0) + a.mx.S[r][j] * jf[j][i][q];
-        }
-  // invert in place (Gauss-Jordan, partial pivoting), result to M
-  double inv[kMaxT * N1][kMaxT * N1];
-  for (int r = 0; r < nb; ++r)
-    for (int q = 0; q < nb; ++q) inv[r][q] = r == q ? 1.0 : 0.0;
-  for (int col = 0; col < nb; ++col) {
-    int p = col;
-    for (int r = col + 1; r < nb; ++r)
-      if (fabs(aug[r][col]) > fabs(aug[p][col])) p = r;
-    if (p != col)
-      for (int q = 0; q < nb; ++q) {
-        double t0 = aug[col][q];
-        aug[col][q] = aug[p][q];
-        aug[p][q] = t0;
-        t0 = inv[col][q];
-        inv[col][q] = inv[p][q];
-        inv[p][q] = t0;
-      }
-    const double piv = aug[col][col];
-    const double ip = 1.0 / piv;
-    for (int q = 0; q < nb; ++q) {
-      aug[col][q] *= ip;
-      inv[col][q] *= ip;
-    }
-    for (int r = 0; r < nb; ++r) {
-      if (r == col) continue;
-      const double f = aug[r][col];
-      if (f == 0.0) continue;
-      for (int q = 0; q < nb; ++q) {
-        aug[r][q] = fma(-f, aug[col][q], aug[r][q]);
-        inv[r][q] = fma(-f, inv[col][q], inv[r][q]);
-      }
-    }
+  if (act) {
+    double* M = Binv + (size_t)c * NB * NB + (size_t)my_col * NB;
+#pragma unroll
+    for (int q = 0; q < NB; ++q) M[q] = inv[q];
   }
-  for (int r = 0; r < nb; ++r)
-    for (int q = 0; q < nb; ++q) M[(size_t)r * nb + q] = inv[r][q];
+}
+
+// Per-element blocks (bstride > 0), nb <= 16: two elements per warp, lane
+// (h, r) computes row r of element 2w + h; x is exchanged by shuffles and
+// the block row is read with 16-byte loads.
+template <int NB>
+__global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
+                                                 const double* __restrict__ in,
+                                                 const double* __restrict__ B, int n1,
+                                                 int ncells, long long ns) {
+  static_assert(NB <= 16 && NB % 2 == 0, "two elements per warp");
+  const int lane = threadIdx.x & 31, h = lane >> 4, r = lane & 15;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long pair = warp; pair * 2 < ncells; pair += nwarps) {
+    const long long c = pair * 2 + h;
+    const bool act = r < NB && c < ncells;
+    const int t = r / n1, k = r - (r / n1) * n1;
+    const double x = act ? in[t * ns + c * n1 + k] : 0.0;
+    const double2* Br =
+        reinterpret_cast<const double2*>(B + (size_t)(act ? c : 0) * NB * NB + (size_t)(act ? r : 0) * NB);
+    double acc = 0.0;
+#pragma unroll
+    for (int q2 = 0; q2 < NB / 2; ++q2) {
+      const double2 b = act ? __ldcs(Br + q2) : make_double2(0.0, 0.0);
+      const double x0 = __shfl_sync(0xffffffffu, x, (h << 4) + 2 * q2);
+      const double x1 = __shfl_sync(0xffffffffu, x, (h << 4) + 2 * q2 + 1);
+      acc = fma(b.x, x0, acc);
+      acc = fma(b.y, x1, acc);
+    }
+    if (act) out[t * ns + c * n1 + k] = acc;
+  }
 }
 
 int pgrid(long long n) {
@@ -207,17 +241,45 @@ void precond_tblock(double* out, const double* in, const double* minv, int nt, i
 
 void precond_eblock(double* out, const double* in, const double* B, long long bstride, int nt,
                     int n1, int ncells, long long ns, cudaStream_t s) {
+  const int nb = nt * n1;
+  if (bstride == (long long)nb * nb && nb <= 16 && nb % 2 == 0) {
+    long long g = ((ncells + 1) / 2 + 7) / 8;  // 8 warps per block, 2 elements per warp
+    if (g > 148 * 16) g = 148 * 16;
+    switch (nb) {
+      case 4: k_eblock2<4><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      case 6: k_eblock2<6><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      case 8: k_eblock2<8><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      case 10: k_eblock2<10><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      case 12: k_eblock2<12><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      case 14: k_eblock2<14><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      case 16: k_eblock2<16><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+      default: break;
+    }
+  }
   int g = (ncells + 7) / 8;
   if (g > 148 * 16) g = 148 * 16;
   k_eblock<kMaxT * kMaxN><<<g, 256, 0, s>>>(out, in, B, bstride, nt, n1, ncells, ns);
 }
 
+template <int N1>
+bool build_nt(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
+  const long long threads = (long long)a.g.nx * 32;  // one warp per element
+  const int blocks = int((threads + 127) / 128);
+  switch (a.n_in) {
+    case 2: k_build_burgers_eblock<N1, 2><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    case 3: k_build_burgers_eblock<N1, 3><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    case 4: k_build_burgers_eblock<N1, 4><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    case 5: k_build_burgers_eblock<N1, 5><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    case 6: k_build_burgers_eblock<N1, 6><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    default: return false;
+  }
+}
+
 bool build_burgers_eblock(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
-  const int blocks = (a.g.nx + 127) / 128;
   switch (a.g.n1) {
-    case 2: k_build_burgers_eblock<2><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
-    case 3: k_build_burgers_eblock<3><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
-    case 4: k_build_burgers_eblock<4><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    case 2: return build_nt<2>(Binv, U, a, s);
+    case 3: return build_nt<3>(Binv, U, a, s);
+    case 4: return build_nt<4>(Binv, U, a, s);
     default: return false;
   }
 }

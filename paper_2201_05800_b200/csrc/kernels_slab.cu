@@ -24,6 +24,7 @@
 #include <cuda.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -160,6 +161,71 @@ __global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
       }
       a.R[r * ns + oc + i] = acc;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// d = 1, large meshes (c3): one lane per (element, temporal block).  The
+// NT lanes of an element compute their block's F(X_j) (or Burgers' exact
+// J_F(U_j) X_j) and exchange X_j, G_j by shuffles for the temporal mix; lane
+// j writes output block j.  32 / NT elements per warp: 4x the threads of
+// slab1d_kernel and short per-lane chains.
+// ---------------------------------------------------------------------------
+template <int N1, int NT>
+__global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
+  constexpr int EPW = 32 / NT;  // elements per warp
+  const int lane = threadIdx.x & 31;
+  const int e = lane / NT, j = lane - (lane / NT) * NT;
+  const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int K = a.g.nx;
+  const long long c0 = warp * EPW + e;
+  const bool act = e < EPW && c0 < K;
+  const int c = act ? int(c0) : 0;
+  const long long ns = a.g.n_sdof;
+  const int cl = wrap_m(c, K), cr = wrap_p(c, K);
+  const long long oc = (long long)c * N1, ol = (long long)cl * N1 + (N1 - 1),
+                  orr = (long long)cr * N1;
+  double x[N1], G[N1];
+#pragma unroll
+  for (int i = 0; i < N1; ++i) x[i] = G[i] = 0.0;
+  if (act && j < a.n_in) {
+    const double* Xj = a.X + j * ns;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) x[i] = Xj[oc + i];
+    const double xl = Xj[ol], xr = Xj[orr];
+    if (a.model == int(Model::advection)) {
+      advection_line<N1>(a.sp, x, xl, xr, G);
+    } else if (!a.jvp) {
+      burgers_line<N1>(a.sp, x, xl, xr, G);
+    } else {
+      const double* Uj = a.U + j * ns;
+      double u[N1];
+#pragma unroll
+      for (int i = 0; i < N1; ++i) u[i] = Uj[oc + i];
+      burgers_jvp_line<N1>(a.sp, u, Uj[ol], Uj[orr], x, xl, xr, G);
+    }
+  }
+  const int base = e * NT;  // first lane of this element's group
+  double acc[N1];
+  const bool out_lane = act && j < a.n_out;
+  const double cr_ = out_lane ? a.mx.c[j] : 0.0;
+#pragma unroll
+  for (int i = 0; i < N1; ++i) acc[i] = out_lane && a.has_w ? cr_ * a.W[oc + i] : 0.0;
+#pragma unroll
+  for (int jj = 0; jj < NT; ++jj) {
+    const double tr = out_lane ? a.mx.T[j][jj] : 0.0, sr = out_lane ? a.mx.S[j][jj] : 0.0;
+    const int src = base + jj < 32 ? base + jj : lane;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      const double xv = __shfl_sync(0xffffffffu, x[i], src);
+      const double gv = __shfl_sync(0xffffffffu, G[i], src);
+      acc[i] = fma(tr, xv, acc[i]);
+      acc[i] = fma(sr, gv, acc[i]);
+    }
+  }
+  if (out_lane) {
+#pragma unroll
+    for (int i = 0; i < N1; ++i) a.R[j * ns + oc + i] = acc[i];
   }
 }
 
@@ -1311,6 +1377,26 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
 // ---------------------------------------------------------------------------
 template <int N1>
 int launch1d(const SlabArgs& a, cudaStream_t s) {
+  // large meshes: one lane per (element, temporal block) when n_in == n_tau
+  // covers the mix (n_out <= n_in) and the lanes fill a warp evenly
+  if (a.g.nx >= 4096 && a.n_out <= a.n_in && !std::getenv("STG_1D_V1")) {
+    auto go = [&](auto nt_tag) {
+      constexpr int NT = decltype(nt_tag)::value;
+      constexpr int EPW = 32 / NT;
+      const long long warps = (a.g.nx + EPW - 1) / EPW;
+      const int blocks = int((warps * 32 + 255) / 256);
+      slab1d_lane_kernel<N1, NT><<<blocks, 256, 0, s>>>(a);
+      return 1;
+    };
+    switch (a.n_in) {
+      case 2: return go(std::integral_constant<int, 2>{});
+      case 3: return go(std::integral_constant<int, 3>{});
+      case 4: return go(std::integral_constant<int, 4>{});
+      case 5: return go(std::integral_constant<int, 5>{});
+      case 6: return go(std::integral_constant<int, 6>{});
+      default: break;
+    }
+  }
   const int blocks = (a.g.nx + kThreads1d - 1) / kThreads1d;
   slab1d_kernel<N1><<<blocks, kThreads1d, 0, s>>>(a);
   return 1;

@@ -96,6 +96,10 @@ struct stg_handle {
   DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
   DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
   DevBuf small_out;      // fused small-solve result record
+  // Burgers element blocks: built at the first Newton iteration of a step and
+  // reused for the rest of it (a lagged preconditioner; STG_PRECOND_REBUILD=1
+  // rebuilds every iteration)
+  bool eblock_valid = false;
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
@@ -608,8 +612,9 @@ void st_residual(stg_handle* h, double dt, const double* un, const double* U, do
 // h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (the Walker-Pernice differencing
 // parameter, as in PETSc's MFFD "wp"), so the perturbation is relative to the
 // state regardless of the scaling of the Krylov vector v.
+// un2 >= 0: ||U||_2 already known (U is fixed during a Newton linear solve)
 void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, const double* v,
-            double* Jv, double fd_eps) {
+            double* Jv, double fd_eps, double un2 = -1.0) {
   const long long n = h->n_dof;
   const double vn = std::sqrt(dev_dot(h, v, v, n));
   if (vn == 0.0) {
@@ -617,7 +622,7 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
     h->launches++;
     return;
   }
-  const double un = std::sqrt(dev_dot(h, U, U, n));
+  const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
   const double eps = fd_eps * std::sqrt(1.0 + un) / vn;
   h->tmp1.ensure(size_t(n));
   h->tmp2.ensure(size_t(n));
@@ -752,8 +757,14 @@ double effective_fd_eps(const stg_handle* h, double fd_eps) {
   return h->desc.model == STG_MODEL_EULER && fd_eps <= 0.0 ? kEulerFdEps : fd_eps;
 }
 
+// whether the Jacobian action of this handle differences (Burgers with
+// fd_eps > 0, Euler always)
+bool uses_fd(const stg_handle* h, double fd_eps) {
+  return !linear_model(h->desc.model) && effective_fd_eps(h, fd_eps) > 0.0;
+}
+
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
-            double fd_eps) {
+            double fd_eps, double un2 = -1.0) {
   fd_eps = effective_fd_eps(h, fd_eps);
   if (linear_model(h->desc.model)) {
     // linear: J v = R(v) with the u_n coupling removed (stdg.hpp:79-110)
@@ -761,7 +772,7 @@ void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* 
   } else if (fd_eps <= 0.0) {
     apply(h, st_mix(h, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, false);
   } else {
-    fd_jvp(h, st_mix(h, dt, false), false, U, v, Jv, fd_eps);
+    fd_jvp(h, st_mix(h, dt, false), false, U, v, Jv, fd_eps, un2);
   }
 }
 
@@ -772,7 +783,7 @@ void stage_residual(stg_handle* h, int form, double dt, const double* u, const d
 }
 
 void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double* v, double* Jv,
-               double fd_eps) {
+               double fd_eps, double un2 = -1.0) {
   const bool full = form == STG_FORM_A;
   fd_eps = effective_fd_eps(h, fd_eps);
   if (linear_model(h->desc.model)) {
@@ -780,7 +791,7 @@ void stage_jvp(stg_handle* h, int form, double dt, const double* U, const double
   } else if (fd_eps <= 0.0) {
     apply(h, stage_mix(h, form, dt, false), h->nt, h->nt, v, U, nullptr, Jv, true, full);
   } else {
-    fd_jvp(h, stage_mix(h, form, dt, false), full, U, v, Jv, fd_eps);
+    fd_jvp(h, stage_mix(h, form, dt, false), full, U, v, Jv, fd_eps, un2);
   }
 }
 
@@ -948,11 +959,15 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     a.g = h->g;
     a.n_in = nt;
     a.n_out = nt;
-    h->ptab.ensure(size_t(ncells) * nb * nb);
-    if (!stg::build_burgers_eblock(h->ptab.p, U, a, h->stream))
-      throw std::invalid_argument("element-block Jacobi: degree <= 3 for Burgers");
-    h->launches++;
-    check_launch(h);
+    static const bool rebuild = std::getenv("STG_PRECOND_REBUILD") != nullptr;
+    if (!h->eblock_valid || rebuild) {
+      h->ptab.ensure(size_t(ncells) * nb * nb);
+      if (!stg::build_burgers_eblock(h->ptab.p, U, a, h->stream))
+        throw std::invalid_argument("element-block Jacobi: degree <= 3 for Burgers");
+      h->launches++;
+      check_launch(h);
+      h->eblock_valid = true;
+    }
     bstride = (long long)nb * nb;
   }
   const double* tab = h->ptab.p;
@@ -1050,6 +1065,7 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
                   u_next, info,
                   "stdg_step element at t=" + fmt_short(t_n) + ", dt=" + fmt_short(dt)))
     return;
+  h->eblock_valid = false;
   stg::vec_broadcast(U, u_n, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u_n (stdg.hpp:131)
   h->launches++;
   const double eps = cfg.fd_eps;
@@ -1059,7 +1075,10 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
         h, [&](const double* X, double* R) { st_residual(h, dt, u_n, X, R); },
         [&](const double* X) -> LinSys {
           LinSys L;
-          L.A = [h, dt, X, eps](const double* v, double* Jv) { st_jvp(h, dt, X, v, Jv, eps); };
+          const double un2 = uses_fd(h, eps) ? std::sqrt(dev_dot(h, X, X, n)) : -1.0;
+          L.A = [h, dt, X, eps, un2](const double* v, double* Jv) {
+            st_jvp(h, dt, X, v, Jv, eps, un2);
+          };
           L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
           return L;
         },
@@ -1093,6 +1112,7 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
                     cfg, U, u_next, info, "rk_step at t=" + fmt_short(t) + ", dt=" + fmt_short(dt)))
       return;
   }
+  h->eblock_valid = false;
   stg::vec_broadcast(U, u, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u (lodg.hpp:131)
   h->launches++;
   const double eps = cfg.fd_eps;
@@ -1102,8 +1122,9 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
         h, [&](const double* X, double* R) { stage_residual(h, form, dt, u, X, R); },
         [&](const double* X) -> LinSys {
           LinSys L;
-          L.A = [h, form, dt, X, eps](const double* v, double* Jv) {
-            stage_jvp(h, form, dt, X, v, Jv, eps);
+          const double un2 = uses_fd(h, eps) ? std::sqrt(dev_dot(h, X, X, n)) : -1.0;
+          L.A = [h, form, dt, X, eps, un2](const double* v, double* Jv) {
+            stage_jvp(h, form, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
           return L;
@@ -1396,6 +1417,7 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     need(x, "x");
     (void)t_n;
     if (!linear_model(h->desc.model)) need(U, "U");
+    h->eblock_valid = false;
     const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
     const GmresStats st = gmres(
         h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
@@ -1415,6 +1437,7 @@ int stg_st_precond_apply(stg_handle* h, double dt, const double* U, int precond,
     need(in, "in");
     need(out, "out");
     if (!linear_model(h->desc.model)) need(U, "U");
+    h->eblock_valid = false;
     const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
     if (P) {
       P(in, out);

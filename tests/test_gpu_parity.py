@@ -412,3 +412,32 @@ def test_fused_small_solve_errors_match():
     with pytest.raises(RuntimeError, match="GMRES did not converge"):
         op.stdg_step(0.0, cfg.dt, un, NewtonConfig(gmres_max_it=1, gmres_tol=1e-14,
                                                    precond=L.STG_PRECOND_NONE))
+
+
+@pytest.mark.parametrize("model,n_tau,degree", [(L.STG_MODEL_ADVECTION, 4, 3),
+                                                (L.STG_MODEL_BURGERS, 4, 3),
+                                                (L.STG_MODEL_BURGERS, 3, 2),
+                                                (L.STG_MODEL_ADVECTION, 5, 1)])
+def test_large_1d_lane_kernel_parity(model, n_tau, degree):
+    """slab1d_lane_kernel (d = 1, >= 4096 elements): R(U), J.v (exact and FD
+    paths), stage residuals vs the oracle."""
+    cfg = make(1, degree, n_tau, (5003,), (0.9,), model=model, dt=1e-3)
+    op, pr = pair(cfg)
+    rng = np.random.default_rng(11)
+    un = C.initial_state(cfg)
+    U = np.concatenate([un + 0.05 * rng.uniform(-1, 1, un.size) for _ in range(n_tau)])
+    v = rng.uniform(-1, 1, U.size)
+    assert rel(op.st_residual(0.0, cfg.dt, dev(un), dev(U)), pr.st_residual(0.0, cfg.dt, un, U)) <= TOL_OP
+    assert rel(op.st_jvp(0.0, cfg.dt, dev(U), dev(v)), pr.st_jvp(0.0, cfg.dt, U, v)) <= TOL_OP
+    if n_tau in (2, 3, 4):
+        for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
+            got = op.stage_residual(form, 0.0, cfg.dt, dev(un), dev(U))
+            assert rel(got, pr.stage_residual(n_tau, form, 0.0, cfg.dt, un, U)) <= TOL_OP
+
+
+def test_full_c3_residual_parity():
+    cfg = C.CONFIGS["c3"]
+    op, pr = pair(cfg)
+    un = C.initial_state(cfg)
+    U = np.concatenate([un] * cfg.n_tau) + 0.01 * np.random.default_rng(2).uniform(-1, 1, cfg.n_dof)
+    assert rel(op.st_residual(0.0, cfg.dt, dev(un), dev(U)), pr.st_residual(0.0, cfg.dt, un, U)) <= TOL_OP
