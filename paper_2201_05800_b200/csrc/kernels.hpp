@@ -168,6 +168,9 @@ void precond_tblock(double* out, const double* in, const double* minv, int nt, i
 // out_e = B_e in_e, B_e = B + e * bstride (bstride 0: one shared block), d = 1
 void precond_eblock(double* out, const double* in, const double* B, long long bstride, int nt,
                     int n1, int ncells, long long ns, cudaStream_t s);
+// d = 2: out_e = B in_e with ONE shared dense block B ((n_tau*npc)^2, <= 128^2)
+bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
+                          int ncells, long long ns, cudaStream_t s);
 // per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U
 bool build_burgers_eblock(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s);
 

@@ -261,6 +261,88 @@ void precond_eblock(double* out, const double* in, const double* B, long long bs
   k_eblock<kMaxT * kMaxN><<<g, 256, 0, s>>>(out, in, B, bstride, nt, n1, ncells, ns);
 }
 
+// ---- d = 2 element-block Jacobi with one shared dense block ----------------
+// Y = B X for every element, B (nb x nb, nb = n_tau * n^2 <= kDenseMax) the
+// inverse of the element-local Jacobian block.  It is a GEMM
+// (nb x nb) x (nb x n_cells) on the stage-major layout: a CTA stages B^T in
+// shared memory once, then loops over tiles of TE = 32 elements -- gather the
+// tile transposed into shared memory, a 4 x 4 register tile per thread
+// (rows x elements), the result staged back through shared memory and
+// written coalesced.  FP64-pipe bound (nb FMAs per DOF).
+constexpr int kDenseMax = 128;
+constexpr int kTE = 64;            // elements per tile
+constexpr int kTEp = kTE + 1;      // odd row pitch: conflict-free transposed staging
+constexpr int kDenseThreads = 32 * (kTE / 4);  // 32 row groups x 16 element groups
+
+__global__ void __launch_bounds__(kDenseThreads, 1)
+    k_eblock_dense(double* __restrict__ out, const double* __restrict__ in,
+                   const double* __restrict__ B, int nb, int npc, int nt, int ncells,
+                   long long ns) {
+  extern __shared__ double sm[];
+  constexpr int NBP = 128;                  // padded row count of B^T (4 rows x 32 groups)
+  double* Bt = sm;                          // [nb][NBP]: Bt[k][row] = B[row][k]
+  double* Xs = Bt + (size_t)nb * NBP;       // [NBP][kTEp]: input tile, then output tile
+  const int tid = threadIdx.x;
+  for (int q = tid; q < nb * NBP; q += kDenseThreads) {
+    const int k = q / NBP, row = q - (q / NBP) * NBP;
+    Bt[q] = row < nb ? B[(size_t)row * nb + k] : 0.0;
+  }
+  const int rg = tid & 31, eg = tid >> 5;  // rows 4rg..4rg+3, elements 4eg..4eg+3
+  const int ntile = (ncells + kTE - 1) / kTE;
+  for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    const int e0 = tile * kTE;
+    const int ne = min(kTE, ncells - e0);
+    __syncthreads();  // Bt ready / previous tile's output drained
+    for (int t = 0; t < nt; ++t) {  // gather: Xs[t*npc + node][e]
+      const double* src = in + t * ns + (long long)e0 * npc;
+      for (int q = tid; q < kTE * npc; q += kDenseThreads) {
+        const int e = q / npc, node = q - (q / npc) * npc;
+        Xs[(t * npc + node) * kTEp + e] = e < ne ? __ldcs(src + q) : 0.0;
+      }
+    }
+    __syncthreads();
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    const double* bcol = Bt + 4 * rg;
+    const double* xrow = Xs + 4 * eg;
+#pragma unroll 5
+    for (int k = 0; k < nb; ++k) {
+      const double2 b01 = *reinterpret_cast<const double2*>(bcol + (size_t)k * NBP);
+      const double2 b23 = *reinterpret_cast<const double2*>(bcol + (size_t)k * NBP + 2);
+      const double x0 = xrow[k * kTEp + 0], x1 = xrow[k * kTEp + 1],
+                   x2 = xrow[k * kTEp + 2], x3 = xrow[k * kTEp + 3];
+      const double bb[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        acc[i][0] = fma(bb[i], x0, acc[i][0]);
+        acc[i][1] = fma(bb[i], x1, acc[i][1]);
+        acc[i][2] = fma(bb[i], x2, acc[i][2]);
+        acc[i][3] = fma(bb[i], x3, acc[i][3]);
+      }
+    }
+    __syncthreads();  // every thread has read the input tile
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int row = 4 * rg + i;
+      if (row < nb) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) Xs[row * kTEp + 4 * eg + j] = acc[i][j];
+      }
+    }
+    __syncthreads();
+    for (int t = 0; t < nt; ++t) {  // coalesced write-back
+      double* dst = out + t * ns + (long long)e0 * npc;
+      for (int q = tid; q < ne * npc; q += kDenseThreads) {
+        const int e = q / npc, node = q - (q / npc) * npc;
+        dst[q] = Xs[(t * npc + node) * kTEp + e];
+      }
+    }
+  }
+}
+
 template <int N1>
 bool build_nt(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   const long long threads = (long long)a.g.nx * 32;  // one warp per element
@@ -273,6 +355,26 @@ bool build_nt(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) 
     case 6: k_build_burgers_eblock<N1, 6><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
     default: return false;
   }
+}
+
+bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
+                          int ncells, long long ns, cudaStream_t s) {
+  const int nb = nt * npc;
+  if (nb > kDenseMax) return false;
+  const size_t smem = sizeof(double) * ((size_t)nb * 128 + (size_t)128 * kTEp);
+  if (smem > 227 * 1024) return false;
+  static size_t set = 0;
+  if (smem > set) {
+    cudaFuncSetAttribute(k_eblock_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    set = smem;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int ntile = (ncells + kTE - 1) / kTE;
+  const int grid = ntile < sms ? ntile : sms;
+  k_eblock_dense<<<grid, kDenseThreads, smem, s>>>(out, in, B, nb, npc, nt, ncells, ns);
+  return true;
 }
 
 bool build_burgers_eblock(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {

@@ -861,6 +861,12 @@ bool build_fdm(const stg::SpatialCoef& sp, const stg::MixCoef& mx, stg::FdmCoef&
   }
 }
 
+// d = 2 advection: one shared dense element block, n_tau * n^2 <= 128
+bool dense2d_ok(const stg_handle* h) {
+  return h->desc.dim == 2 && h->desc.model == STG_MODEL_ADVECTION &&
+         h->nt * h->g.npc <= 128;
+}
+
 bool fdm_ok(const stg_handle* h) {
   return h->desc.dim == 3 && h->desc.model == STG_MODEL_ADVECTION && stg::fdm_supported(h->g, h->nt);
 }
@@ -871,10 +877,10 @@ int resolve_precond(const stg_handle* h, int kind) {
     throw std::invalid_argument("block-Jacobi preconditioners: advection / Burgers only");
   }
   if (kind == STG_PRECOND_AUTO)
-    return (h->desc.dim == 1 || fdm_ok(h))
+    return (h->desc.dim == 1 || fdm_ok(h) || dense2d_ok(h))
                ? STG_PRECOND_EBLOCK
                : (h->desc.model == STG_MODEL_ADVECTION ? STG_PRECOND_TBLOCK : STG_PRECOND_NONE);
-  if (kind == STG_PRECOND_EBLOCK && h->desc.dim != 1 && !fdm_ok(h))
+  if (kind == STG_PRECOND_EBLOCK && h->desc.dim != 1 && !fdm_ok(h) && !dense2d_ok(h))
     throw std::invalid_argument(
         "element-block Jacobi: d = 1, or d = 3 advection with degree 3, n_tau = 4 and a cell "
         "count divisible by 8");
@@ -931,6 +937,34 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     const double* dt = h->ptab.p;
     return [h, dt, nt, npc, ns](const double* in, double* out) {
       stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream);
+      h->launches++;
+    };
+  }
+  if (d == 2) {  // one shared dense element block (advection)
+    const int nbd = nt * npc;
+    std::vector<double> B(size_t(nbd) * nbd, 0.0);
+    for (int r = 0; r < nt; ++r)
+      for (int node = 0; node < npc; ++node) {
+        const int iy = node / n1, ix = node % n1;
+        for (int j = 0; j < nt; ++j)
+          for (int node2 = 0; node2 < npc; ++node2) {
+            const int jy = node2 / n1, jx = node2 % n1;
+            const double K = (iy == jy ? h->sp.V[0][ix][jx] : 0.0) +
+                             (ix == jx ? h->sp.V[1][iy][jy] : 0.0);
+            B[size_t(r * npc + node) * nbd + size_t(j * npc + node2)] =
+                (node == node2 ? mx.T[r][j] : 0.0) + mx.S[r][j] * K;
+          }
+      }
+    const std::vector<double> Bi = stg::inverse(B, nbd);
+    h->ptab.ensure(Bi.size());
+    ck(cudaMemcpyAsync(h->ptab.p, Bi.data(), sizeof(double) * Bi.size(), cudaMemcpyHostToDevice,
+                       h->stream), "H2D");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    const double* tab = h->ptab.p;
+    const int ncells = h->g.n_cells;
+    return [h, tab, nt, npc, ncells, ns](const double* in, double* out) {
+      if (!stg::precond_eblock_dense(out, in, tab, nt, npc, ncells, ns, h->stream))
+        throw std::runtime_error("element-block preconditioner launch failed");
       h->launches++;
     };
   }

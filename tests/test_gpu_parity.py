@@ -263,7 +263,7 @@ def test_burgers_newton_vs_oracle():
 
 @pytest.mark.parametrize("name,cells,pcs", [
     ("c4", (8, 8, 8), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK]),
-    ("c2", (16, 16), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK]),
+    ("c2", (16, 16), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK]),
     ("c1", (64,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
     ("c3", (256,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
 ])
@@ -441,3 +441,23 @@ def test_full_c3_residual_parity():
     un = C.initial_state(cfg)
     U = np.concatenate([un] * cfg.n_tau) + 0.01 * np.random.default_rng(2).uniform(-1, 1, cfg.n_dof)
     assert rel(op.st_residual(0.0, cfg.dt, dev(un), dev(U)), pr.st_residual(0.0, cfg.dt, un, U)) <= TOL_OP
+
+
+def test_dense_2d_element_block_is_exact_local_inverse():
+    """d = 2 EBLOCK (one shared dense block, kernels_precond.cu) = the exact
+    inverse of the element-local block read off the oracle's J.v."""
+    cfg = make(2, 4, 5, (4, 3), (1.0, -0.5), dt=0.003)
+    op, pr = pair(cfg)
+    ns, npc, nt = op.n_sdof, 25, 5
+    loc = np.array([t * ns + k for t in range(nt) for k in range(npc)])  # element 0
+    Lblk = np.zeros((nt * npc, nt * npc))
+    U0 = np.zeros(nt * ns)
+    for c, i in enumerate(loc):
+        e = np.zeros(nt * ns)
+        e[i] = 1.0
+        Lblk[:, c] = pr.st_jvp(0.0, cfg.dt, U0, e)[loc]
+    x = np.random.default_rng(9).standard_normal(nt * ns)
+    y = op.st_precond_apply(cfg.dt, dev(x), precond=L.STG_PRECOND_EBLOCK).cpu().numpy()
+    for cell in range(12):
+        idx = loc + cell * npc
+        assert rel(y[idx], np.linalg.solve(Lblk, x[idx])) <= 1e-11, cell
