@@ -78,8 +78,9 @@ extern "C" {
  * on these Jacobians, so the block versions are provided:
  *   TBLOCK  temporal-block Jacobi (n_tau x n_tau per spatial node, advection)
  *   EBLOCK  element-block Jacobi (exact inverse of the element-local block:
- *           d = 1 dense; d = 3 advection, degree 3, n_tau = 4, cells % 8 == 0
- *           by fast diagonalisation)
+ *           d = 1 dense; d = 2 advection with n_tau * (N+1)^2 <= 128 one
+ *           shared dense block; d = 3 advection, degree 3, n_tau = 4,
+ *           cells % 8 == 0 by fast diagonalisation)
  *   AUTO    EBLOCK where supported, else TBLOCK (advection) / none. */
 #define STG_PRECOND_NONE 0
 #define STG_PRECOND_TBLOCK 1
