@@ -273,6 +273,7 @@ constexpr int kDenseMax = 128;
 constexpr int kTE = 64;            // elements per tile
 constexpr int kTEp = kTE + 1;      // odd row pitch: conflict-free transposed staging
 constexpr int kDenseThreads = 32 * (kTE / 4);  // 32 row groups x 16 element groups
+constexpr int kPre = 128 * kTE / kDenseThreads;  // prefetched doubles per thread
 
 __global__ void __launch_bounds__(kDenseThreads, 1)
     k_eblock_dense(double* __restrict__ out, const double* __restrict__ in,
@@ -289,18 +290,38 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
   }
   const int rg = tid & 31, eg = tid >> 5;  // rows 4rg..4rg+3, elements 4eg..4eg+3
   const int ntile = (ncells + kTE - 1) / kTE;
+  const int per_tile = nt * kTE * npc;  // <= 128 * kTE = kPre * kDenseThreads
+  // the next tile is gathered into registers while the current one is
+  // computed (loads first, then the transposed shared stores)
+  double pre[kPre];
+  auto load_tile = [&](int tile) {
+    const int e0 = tile * kTE, ne = min(kTE, ncells - e0);
+#pragma unroll
+    for (int c = 0; c < kPre; ++c) {
+      const int q = tid + c * kDenseThreads;
+      pre[c] = 0.0;
+      if (q < per_tile) {
+        const int t = q / (kTE * npc), r = q - t * (kTE * npc);
+        if (r / npc < ne) pre[c] = __ldcs(in + t * ns + (long long)e0 * npc + r);
+      }
+    }
+  };
+  if (blockIdx.x < ntile) load_tile(blockIdx.x);
   for (int tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
     const int e0 = tile * kTE;
     const int ne = min(kTE, ncells - e0);
     __syncthreads();  // Bt ready / previous tile's output drained
-    for (int t = 0; t < nt; ++t) {  // gather: Xs[t*npc + node][e]
-      const double* src = in + t * ns + (long long)e0 * npc;
-      for (int q = tid; q < kTE * npc; q += kDenseThreads) {
-        const int e = q / npc, node = q - (q / npc) * npc;
-        Xs[(t * npc + node) * kTEp + e] = e < ne ? __ldcs(src + q) : 0.0;
+#pragma unroll
+    for (int c = 0; c < kPre; ++c) {
+      const int q = tid + c * kDenseThreads;
+      if (q < per_tile) {
+        const int t = q / (kTE * npc), r = q - t * (kTE * npc);
+        const int e = r / npc, node = r - (r / npc) * npc;
+        Xs[(t * npc + node) * kTEp + e] = pre[c];
       }
     }
     __syncthreads();
+    if (tile + (int)gridDim.x < ntile) load_tile(tile + gridDim.x);
     double acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
