@@ -104,6 +104,10 @@ struct stg_handle {
   DevBuf dtab;
   stg::MixCoef dense_mix{};
   bool dense_valid = false;
+  // d = 3 fast-diagonalisation factors and the mix they belong to
+  stg::FdmCoef fdm{};
+  stg::MixCoef fdm_mix{};
+  bool fdm_valid = false;
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
@@ -987,7 +991,15 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
   }
   if (d == 3) {  // element-block Jacobi by fast diagonalisation
     stg::FdmCoef c;
-    if (build_fdm(h->sp, mx, c))
+    bool ok = h->fdm_valid && std::memcmp(&h->fdm_mix, &mx, sizeof mx) == 0;
+    if (ok) {
+      c = h->fdm;
+    } else if (build_fdm(h->sp, mx, c)) {
+      h->fdm = c;
+      h->fdm_mix = mx;
+      h->fdm_valid = ok = true;
+    }
+    if (ok)
       return [h, c](const double* in, double* out) {
         if (stg::launch_precond_fdm(c, h->g, in, out, h->stream) < 0)
           throw std::runtime_error("element-block preconditioner launch failed");
