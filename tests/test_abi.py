@@ -52,6 +52,35 @@ def test_invalid_descriptor_rejected_before_cuda(lib):
     assert lib.stg_create(ctypes.byref(d), ctypes.byref(h)) == L.STG_ERR_INVALID
 
 
+@pytest.mark.parametrize("field,msg", [
+    (dict(model=L.STG_MODEL_ADVDIFF, dim=3), b"d in {1, 2}"),
+    (dict(model=L.STG_MODEL_ADVDIFF, eps=-1e-3), b"eps >= 0"),
+    (dict(model=L.STG_MODEL_ADVDIFF, velocity_field=7), b"velocity field"),
+    (dict(model=L.STG_MODEL_ADVDIFF, dim=1, velocity_field=L.STG_FIELD_ROTATING), b"d = 2"),
+    (dict(model=L.STG_MODEL_EULER, dim=1), b"dimension mismatch"),
+    (dict(model=L.STG_MODEL_EULER, gamma=0.9), b"gamma > 1"),
+    (dict(model=9), b"unknown model"),
+    (dict(cells=[1 << 15, 1 << 14, 1]), b"2^31"),
+    (dict(cells=[1 << 16, 1 << 15, 1]), b"too many cells"),
+])
+def test_invalid_v2_descriptors(lib, field, msg):  # models.hpp:68-124, mesh.hpp:39
+    """ABI v2 descriptor validation (general models, size guard) happens before
+    any CUDA call, so it runs on CPU too."""
+    d = L.StgDesc()
+    d.dim, d.degree, d.n_tau, d.model = 2, 3, 4, L.STG_MODEL_ADVECTION
+    d.cells[:] = [4, 4, 1]
+    d.lower[:] = [0, 0, 0]
+    d.upper[:] = [1, 1, 1]
+    for k, v in field.items():
+        if k == "cells":
+            d.cells[:] = v
+        else:
+            setattr(d, k, v)
+    h = ctypes.c_void_p()
+    assert lib.stg_create(ctypes.byref(d), ctypes.byref(h)) == L.STG_ERR_INVALID
+    assert msg in lib.stg_last_error(None), lib.stg_last_error(None)
+
+
 def test_no_cpu_fallback_without_device(lib):
     from conftest import cuda_available
     if cuda_available():

@@ -63,6 +63,15 @@ CASES = [
     make(1, 2, 3, (9,), (-1.5,)),
     make(1, 5, 6, (7,), (0.8,)),
     make(3, 4, 5, (3, 2, 2), (1.0, -1.0, 0.5)),
+    # 2-D plane kernel (cells % 32 == 0): negative / zero velocities, and
+    # single-cell axes (a cell is its own periodic neighbour)
+    make(2, 4, 5, (16, 4), (-0.8, -0.3)),
+    make(2, 2, 3, (8, 4), (0.0, -1.2)),
+    make(2, 3, 4, (1, 32), (0.7, 0.4)),
+    make(2, 3, 4, (32, 1), (-0.7, 0.4)),
+    # fast 3-D kernel with one-cell y / z axes
+    make(3, 3, 4, (8, 1, 1), (1.0, 0.5, -0.5)),
+    make(3, 3, 4, (8, 2, 1), (-1.0, 1.0, 1.0)),
 ]
 IDS = [c.name if c.name[0] == "c" else f"d{c.dim}p{c.degree}nt{c.n_tau}{c.cells}" for c in CASES]
 
