@@ -488,6 +488,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       const double sigma = 1.0 / hp[190];  // norm used to scale the stored vector
       for (int j = 0; j <= k; ++j) Hat(j, k) = hp[j];
       double hn = sigma;
+      static const bool trace = std::getenv("STG_GMRES_TRACE") != nullptr;
+      if (trace)  // Arnoldi cancellation / normalisation diagnostics
+        std::fprintf(stderr, "arnoldi k=%d cancel=%.3e nv2-1=%.3e\n", k, (ww - hh) / ww,
+                     hp[64 + kk] - 1.0);
       if (!(ww - hh > 1e-4 * ww) || std::abs(hp[64 + kk] - 1.0) > 1e-10) {
         // re-orthogonalise the stored (scaled) vector in two passes:
         // [g2, <vn,vn>] = [V, vn]^T vn (vn is the basis slot after V_k), then
