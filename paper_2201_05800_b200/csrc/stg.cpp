@@ -101,6 +101,9 @@ struct stg_handle {
   // rebuilds every iteration)
   bool eblock_valid = false;
   // d = 2 dense element block: the uploaded inverse and the mix it belongs to
+  DevBuf etab;  // d = 1 advection element block (shared), keyed by mix
+  stg::MixCoef etab_mix{};
+  bool etab_valid = false;
   DevBuf dtab;
   stg::MixCoef dense_mix{};
   bool dense_valid = false;
@@ -908,6 +911,7 @@ int resolve_precond(const stg_handle* h, int kind) {
 // block T (x) I + S (x) V.  Uploaded to h->ptab; returns the device pointer.
 const double* eblock_table_1d(stg_handle* h, const stg::MixCoef& mx) {
   const int nt = h->nt, n1 = h->n1, nb = nt * n1;
+  if (h->etab_valid && std::memcmp(&h->etab_mix, &mx, sizeof mx) == 0) return h->etab.p;
   std::vector<double> B(size_t(nb) * nb);
   for (int r = 0; r < nt; ++r)
     for (int i = 0; i < n1; ++i)
@@ -916,11 +920,13 @@ const double* eblock_table_1d(stg_handle* h, const stg::MixCoef& mx) {
           B[size_t(r * n1 + i) * nb + size_t(j * n1 + q)] =
               (i == q ? mx.T[r][j] : 0.0) + mx.S[r][j] * h->sp.V[0][i][q];
   const std::vector<double> Bi = stg::inverse(B, nb);
-  h->ptab.ensure(Bi.size());
-  ck(cudaMemcpyAsync(h->ptab.p, Bi.data(), sizeof(double) * Bi.size(), cudaMemcpyHostToDevice,
+  h->etab.ensure(Bi.size());
+  ck(cudaMemcpyAsync(h->etab.p, Bi.data(), sizeof(double) * Bi.size(), cudaMemcpyHostToDevice,
                      h->stream), "H2D");
   ck(cudaStreamSynchronize(h->stream), "sync");
-  return h->ptab.p;
+  h->etab_mix = mx;
+  h->etab_valid = true;
+  return h->etab.p;
 }
 
 // Right preconditioner for the Jacobian with temporal mixing (T, S) at the
@@ -1017,8 +1023,9 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
   const int nb = nt * n1;
   const int ncells = h->g.n_cells;
   long long bstride = 0;
+  const double* tab = nullptr;
   if (h->desc.model == STG_MODEL_ADVECTION) {
-    eblock_table_1d(h, mx);
+    tab = eblock_table_1d(h, mx);
   } else {
     stg::SlabArgs a{};
     a.sp = h->sp;
@@ -1036,8 +1043,8 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       h->eblock_valid = true;
     }
     bstride = (long long)nb * nb;
+    tab = h->ptab.p;
   }
-  const double* tab = h->ptab.p;
   return [h, tab, bstride, nt, n1, ncells, ns](const double* in, double* out) {
     stg::precond_eblock(out, in, tab, bstride, nt, n1, ncells, ns, h->stream);
     h->launches++;
