@@ -101,8 +101,17 @@ __device__ __noinline__ double block_maxabs(const double* x, int n, double (*red
 
 // R = sum_j T X_j + sum_j S F(X_j) + c W over n_out blocks (1-D advection);
 // one thread per (cell, node).  X, R may live in shared or global memory.
+// Coefficients staged in shared memory: V (N1 x N1), cL, cR of axis 0 and the
+// three mixes T / S / c (kernel parameters indexed by lane-divergent values
+// would serialise in the constant cache).
+struct SmallCoef {
+  double V[kMaxN][kMaxN];
+  double cL, cR;
+  MixCoef mx[3];  // residual, Jacobian, rk u_next
+};
+
 template <int N1>
-__device__ __noinline__ void apply_1d(const SpatialCoef& sp, const MixCoef& mx, int nt, int n_out,
+__device__ __noinline__ void apply_1d(const SmallCoef& sc, const MixCoef& mx, int nt, int n_out,
                          const double* X, const double* W, double* R, int K, long long ns) {
   for (int q = threadIdx.x; q < K * N1; q += kSmallThreads) {
     const int c = q / N1, i = q - (q / N1) * N1;
@@ -115,9 +124,9 @@ __device__ __noinline__ void apply_1d(const SpatialCoef& sp, const MixCoef& mx, 
         double g = 0.0;
         if (mx.S[r][j] != 0.0) {  // F(X_j) at node i (recomputed per output row)
 #pragma unroll
-          for (int k = 0; k < N1; ++k) g = fma(sp.V[0][i][k], Xj[c * N1 + k], g);
-          if (i == 0) g = fma(sp.cL[0], Xj[cl * N1 + N1 - 1], g);
-          if (i == N1 - 1) g = fma(sp.cR[0], Xj[cr * N1], g);
+          for (int k = 0; k < N1; ++k) g = fma(sc.V[i][k], Xj[c * N1 + k], g);
+          if (i == 0) g = fma(sc.cL, Xj[cl * N1 + N1 - 1], g);
+          if (i == N1 - 1) g = fma(sc.cR, Xj[cr * N1], g);
         }
         acc = fma(mx.T[r][j], Xj[c * N1 + i], acc);
         acc = fma(mx.S[r][j], g, acc);
@@ -142,7 +151,7 @@ __device__ __noinline__ void precond_1d(const double* B, int nt, const double* i
     double acc = 0.0;
     for (int col = 0; col < nb; ++col) {
       const int j = col / N1, k = col - (col / N1) * N1;
-      acc = fma(B[row * nb + col], in[j * ns + c * N1 + k], acc);
+      acc = fma(B[row * (nb + 1) + col], in[j * ns + c * N1 + k], acc);  // odd pitch
     }
     out[r * ns + c * N1 + i] = acc;
   }
@@ -170,26 +179,37 @@ __global__ void __launch_bounds__(kSmallThreads)
   s.B = a.B ? s.W + ns : nullptr;
   // basis: as many vectors as fit in the rest of the dynamic shared memory
   Basis V;
-  V.sm = s.W + ns + (a.B ? (nt * N1) * (nt * N1) : 0);
+  V.sm = s.W + ns + (a.B ? (nt * N1) * (nt * N1 + 1) : 0);
   V.gl = a.V;
   V.in_smem = a.basis_in_smem;
   V.n = n;
   V.ld = a.ld;
   const int nb = nt * N1;
+  __shared__ SmallCoef sc;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < N1; ++i)
+      for (int k = 0; k < N1; ++k) sc.V[i][k] = a.sp.V[0][i][k];
+    sc.cL = a.sp.cL[0];
+    sc.cR = a.sp.cR[0];
+    sc.mx[0] = a.mx_res;
+    sc.mx[1] = a.mx_jac;
+    sc.mx[2] = a.mx_next;
+  }
   for (int i = threadIdx.x; i < ns; i += kSmallThreads) s.W[i] = a.W[i];
   if (s.B)
-    for (int i = threadIdx.x; i < nb * nb; i += kSmallThreads) s.B[i] = a.B[i];
+    for (int i = threadIdx.x; i < nb * nb; i += kSmallThreads)
+      s.B[(i / nb) * (nb + 1) + i % nb] = a.B[i];
   // initial guess 1 (x) W (stdg.hpp:131, lodg.hpp:131)
   for (int i = threadIdx.x; i < n; i += kSmallThreads) s.U[i] = a.W[i % ns];
   __syncthreads();
 
   auto residual = [&]() {
-    apply_1d<N1>(a.sp, a.mx_res, nt, nt, s.U, s.W, s.R, K, ns);
+    apply_1d<N1>(sc, sc.mx[0], nt, nt, s.U, s.W, s.R, K, ns);
     __syncthreads();
   };
   // Jacobian action w = J x (the mix without the constant coupling)
   auto jac = [&](const double* x, double* y) {
-    apply_1d<N1>(a.sp, a.mx_jac, nt, nt, x, nullptr, y, K, ns);
+    apply_1d<N1>(sc, sc.mx[1], nt, nt, x, nullptr, y, K, ns);
     __syncthreads();
   };
 
@@ -350,7 +370,7 @@ __global__ void __launch_bounds__(kSmallThreads)
   for (int i = threadIdx.x; i < n; i += kSmallThreads) a.U_out[i] = s.U[i];
   if (a.u_next) {
     if (a.rk) {  // u_next = u + dt sum_j b_j F(U_j)  (lodg.hpp:142-145)
-      apply_1d<N1>(a.sp, a.mx_next, nt, 1, s.U, s.W, a.u_next, K, ns);
+      apply_1d<N1>(sc, sc.mx[2], nt, 1, s.U, s.W, a.u_next, K, ns);
     } else {
       for (int i = threadIdx.x; i < ns; i += kSmallThreads) a.u_next[i] = s.U[(nt - 1) * ns + i];
     }
@@ -368,7 +388,7 @@ __global__ void __launch_bounds__(kSmallThreads)
 }  // namespace
 
 size_t small_solve_smem(int n, long long ns, int nb, bool precond) {
-  return sizeof(double) * (5 * size_t(n) + size_t(ns) + (precond ? size_t(nb) * nb : 0));
+  return sizeof(double) * (5 * size_t(n) + size_t(ns) + (precond ? size_t(nb) * (nb + 1) : 0));
 }
 constexpr size_t kSmallDynMax = 200 * 1024;  // dynamic shared memory budget
 
