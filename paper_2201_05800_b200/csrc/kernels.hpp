@@ -79,7 +79,16 @@ struct SlabArgs {
   // mesh (seg_end == 0: all).  Used by the pipelined host-buffer entry point.
   int seg_begin;
   int seg_end;
+  // fused central-difference Jacobian action (d = 1 lane kernel): when fdv is
+  // set, X is the linearisation point U and the kernel returns
+  // T v + S [F(U + e v) - F(U - e v)] / (2e), e = fd_c / sqrt(*fd_vv)
+  // (fd_vv = <v,v> on the device: no host round trip)
+  const double* fdv;
+  const double* fd_vv;
+  double fd_c;
 };
+// true if the d = 1 lane kernel handles fused FD Jacobian actions for a
+bool fd_fused_supported(const SlabArgs& a);
 
 // ---- launchers (kernels_slab.cu) -------------------------------------------
 // Returns the number of kernels launched (>= 1) or -1 if no kernel fits.

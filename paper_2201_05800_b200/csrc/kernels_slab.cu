@@ -188,7 +188,26 @@ __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
   double x[N1], G[N1];
 #pragma unroll
   for (int i = 0; i < N1; ++i) x[i] = G[i] = 0.0;
-  if (act && j < a.n_in) {
+  if (act && j < a.n_in && a.fdv) {
+    // fused central difference: x <- v, G <- [F(U + e v) - F(U - e v)] / 2e
+    const double vv = *a.fd_vv;
+    const double e = vv > 0.0 ? a.fd_c / sqrt(vv) : 1.0;
+    const double* Uj = a.X + j * ns;
+    const double* vj = a.fdv + j * ns;
+    double up[N1], um[N1], Gp[N1], Gm[N1];
+#pragma unroll
+    for (int i = 0; i < N1; ++i) {
+      x[i] = vj[oc + i];
+      up[i] = fma(e, x[i], Uj[oc + i]);
+      um[i] = fma(-e, x[i], Uj[oc + i]);
+    }
+    const double vl = vj[ol], vr = vj[orr];
+    burgers_line<N1>(a.sp, up, fma(e, vl, Uj[ol]), fma(e, vr, Uj[orr]), Gp);
+    burgers_line<N1>(a.sp, um, fma(-e, vl, Uj[ol]), fma(-e, vr, Uj[orr]), Gm);
+    const double inv = 0.5 / e;
+#pragma unroll
+    for (int i = 0; i < N1; ++i) G[i] = (Gp[i] - Gm[i]) * inv;
+  } else if (act && j < a.n_in) {
     const double* Xj = a.X + j * ns;
 #pragma unroll
     for (int i = 0; i < N1; ++i) x[i] = Xj[oc + i];
@@ -1570,6 +1589,12 @@ int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
     }
   }
   return -1;
+}
+
+bool fd_fused_supported(const SlabArgs& a) {
+  return a.g.dim == 1 && a.model == int(Model::burgers) && a.g.nx >= 4096 &&
+         a.n_out <= a.n_in && a.n_in >= 2 && a.n_in <= 6 && a.g.n1 >= 2 && a.g.n1 <= 6 &&
+         !std::getenv("STG_1D_V1");
 }
 
 bool slab_fast_supported(const SlabArgs& a) {

@@ -631,6 +631,31 @@ void st_residual(stg_handle* h, double dt, const double* un, const double* U, do
 void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, const double* v,
             double* Jv, double fd_eps, double un2 = -1.0) {
   const long long n = h->n_dof;
+  if (h->desc.model == STG_MODEL_BURGERS && h->kernel_pref == STG_KERNEL_AUTO) {
+    // fused: <v,v> on the device, then ONE kernel forms U +- e v per lane
+    stg::SlabArgs a{};
+    a.sp = h->sp;
+    a.mx = mix;
+    a.g = h->g;
+    a.n_in = a.n_out = h->nt;
+    a.full_s = full ? 1 : 0;
+    a.model = h->desc.model;
+    a.X = U;
+    a.R = Jv;
+    a.fdv = v;
+    if (stg::fd_fused_supported(a)) {
+      const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
+      double* vv = h->small.p + 1000;
+      stg::vec_dot(v, v, n, h->partial.p, vv, h->stream);
+      a.fd_vv = vv;
+      a.fd_c = fd_eps * std::sqrt(1.0 + un);
+      if (stg::launch_slab_generic(a, h->stream) < 0)
+        throw std::runtime_error("fused FD Jacobian launch failed");
+      h->launches += 2;
+      check_launch(h);
+      return;
+    }
+  }
   const double vn = std::sqrt(dev_dot(h, v, v, n));
   if (vn == 0.0) {
     stg::vec_fill(Jv, 0.0, n, h->stream);

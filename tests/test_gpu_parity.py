@@ -470,3 +470,38 @@ def test_dense_2d_element_block_is_exact_local_inverse():
     for cell in range(12):
         idx = loc + cell * npc
         assert rel(y[idx], np.linalg.solve(Lblk, x[idx])) <= 1e-11, cell
+
+
+def test_fused_fd_jvp_matches_host_driven_and_exact():
+    """d = 1 Burgers, >= 4096 elements: the fused central difference (one lane
+    kernel, <v,v> on the device) agrees with the host-driven difference and
+    with the exact linearisation to FD accuracy; slab and both stage forms."""
+    cfg = make(1, 3, 4, (5003,), (0.0,), model=L.STG_MODEL_BURGERS, dt=1e-4)
+    fused = SlabOperator(**cfg.kwargs())
+    host = SlabOperator(**cfg.kwargs(), kernel=L.STG_KERNEL_GENERIC)
+    rng = np.random.default_rng(4)
+    un = C.initial_state(cfg)
+    U = dev(np.concatenate([un + 0.05 * rng.uniform(-1, 1, un.size) for _ in range(4)]))
+    v = dev(rng.uniform(-1, 1, cfg.n_dof))
+    a = fused.st_jvp(0.0, cfg.dt, U, v, fd_eps=1e-7).cpu().numpy()
+    b = host.st_jvp(0.0, cfg.dt, U, v, fd_eps=1e-7).cpu().numpy()
+    ex = fused.st_jvp(0.0, cfg.dt, U, v).cpu().numpy()  # exact linearisation
+    assert rel(a, b) <= 1e-7
+    assert rel(a, ex) <= 1e-6
+    for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
+        a = fused.stage_jvp(form, 0.0, cfg.dt, U, v, fd_eps=1e-7).cpu().numpy()
+        ex = fused.stage_jvp(form, 0.0, cfg.dt, U, v).cpu().numpy()
+        assert rel(a, ex) <= 1e-6
+
+
+def test_c3_fused_solve_matches_host_driven():
+    cfg = C.CONFIGS["c3"]
+    fused = SlabOperator(**cfg.kwargs())
+    host = SlabOperator(**cfg.kwargs(), kernel=L.STG_KERNEL_GENERIC)
+    u = dev(C.initial_state(cfg))
+    nc = NewtonConfig(abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-6, fd_eps=1e-7)
+    _, uf, inf_f = fused.stdg_step(0.0, cfg.dt, u, nc)
+    _, uh, inf_h = host.stdg_step(0.0, cfg.dt, u, nc)
+    # inexact Newton to ||R||_inf <= 1e-12: both land on the same solution
+    assert rel(uf, uh.cpu().numpy()) <= 1e-9
+    assert inf_f.newton_iterations == inf_h.newton_iterations
