@@ -180,8 +180,13 @@ void precond_eblock(double* out, const double* in, const double* B, long long bs
 // d = 2: out_e = B in_e with ONE shared dense block B ((n_tau*npc)^2, <= 128^2)
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
                           int ncells, long long ns, cudaStream_t s);
-// per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U
-bool build_burgers_eblock(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s);
+// per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U,
+// stored in fp32 (a preconditioner; applied in fp64 arithmetic)
+bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s);
+// out_e = B_e in_e with per-element fp32 blocks, nt*n1 <= 16 and even
+bool eblock_f32_supported(int nt, int n1);
+void precond_eblock_f32(double* out, const double* in, const float* B, int nt, int n1,
+                        int ncells, long long ns, cudaStream_t s);
 
 // ---- vector kernels (kernels_vec.cu) ----------------------------------------
 // All reductions are deterministic: fixed grid for a given n, fixed-order

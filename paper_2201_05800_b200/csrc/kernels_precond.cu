@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
 // row is broadcast by shuffles and eliminated from every other lane.  At the
 // end the pivot lane of column col holds row col of the inverse.
 template <int N1, int NT>
-__global__ void __launch_bounds__(128) k_build_burgers_eblock(double* __restrict__ Binv,
+__global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict__ Binv,
                                                               const double* __restrict__ U,
                                                               const SlabArgs a) {
   constexpr int NB = N1 * NT;
@@ -178,10 +178,10 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(double* __restrict
       }
     }
   }
-  if (act) {
-    double* M = Binv + (size_t)c * NB * NB + (size_t)my_col * NB;
+  if (act) {  // stored in fp32: a preconditioner; GMRES itself stays fp64
+    float* M = Binv + (size_t)c * NB * NB + (size_t)my_col * NB;
 #pragma unroll
-    for (int q = 0; q < NB; ++q) M[q] = inv[q];
+    for (int q = 0; q < NB; ++q) M[q] = float(inv[q]);
   }
 }
 
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(double* __restrict
 template <int NB>
 __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
                                                  const double* __restrict__ in,
-                                                 const double* __restrict__ B, int n1,
+                                                 const float* __restrict__ B, int n1,
                                                  int ncells, long long ns) {
   static_assert(NB <= 16 && NB % 2 == 0, "two elements per warp");
   const int lane = threadIdx.x & 31, h = lane >> 4, r = lane & 15;
@@ -202,12 +202,13 @@ __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
     const bool act = r < NB && c < ncells;
     const int t = r / n1, k = r - (r / n1) * n1;
     const double x = act ? in[t * ns + c * n1 + k] : 0.0;
-    const double2* Br =
-        reinterpret_cast<const double2*>(B + (size_t)(act ? c : 0) * NB * NB + (size_t)(act ? r : 0) * NB);
+    const float2* Br =
+        reinterpret_cast<const float2*>(B + (size_t)(act ? c : 0) * NB * NB + (size_t)(act ? r : 0) * NB);
     double acc = 0.0;
 #pragma unroll
     for (int q2 = 0; q2 < NB / 2; ++q2) {
-      const double2 b = act ? __ldcs(Br + q2) : make_double2(0.0, 0.0);
+      const float2 bf = act ? __ldg(Br + q2) : make_float2(0.f, 0.f);
+      const double2 b = make_double2(double(bf.x), double(bf.y));
       const double x0 = __shfl_sync(0xffffffffu, x, (h << 4) + 2 * q2);
       const double x1 = __shfl_sync(0xffffffffu, x, (h << 4) + 2 * q2 + 1);
       acc = fma(b.x, x0, acc);
@@ -241,21 +242,6 @@ void precond_tblock(double* out, const double* in, const double* minv, int nt, i
 
 void precond_eblock(double* out, const double* in, const double* B, long long bstride, int nt,
                     int n1, int ncells, long long ns, cudaStream_t s) {
-  const int nb = nt * n1;
-  if (bstride == (long long)nb * nb && nb <= 16 && nb % 2 == 0) {
-    long long g = ((ncells + 1) / 2 + 7) / 8;  // 8 warps per block, 2 elements per warp
-    if (g > 148 * 16) g = 148 * 16;
-    switch (nb) {
-      case 4: k_eblock2<4><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      case 6: k_eblock2<6><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      case 8: k_eblock2<8><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      case 10: k_eblock2<10><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      case 12: k_eblock2<12><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      case 14: k_eblock2<14><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      case 16: k_eblock2<16><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-      default: break;
-    }
-  }
   int g = (ncells + 7) / 8;
   if (g > 148 * 16) g = 148 * 16;
   k_eblock<kMaxT * kMaxN><<<g, 256, 0, s>>>(out, in, B, bstride, nt, n1, ncells, ns);
@@ -365,7 +351,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 }
 
 template <int N1>
-bool build_nt(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
+bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   const long long threads = (long long)a.g.nx * 32;  // one warp per element
   const int blocks = int((threads + 127) / 128);
   switch (a.n_in) {
@@ -398,7 +384,29 @@ bool precond_eblock_dense(double* out, const double* in, const double* B, int nt
   return true;
 }
 
-bool build_burgers_eblock(double* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
+void precond_eblock_f32(double* out, const double* in, const float* B, int nt, int n1,
+                        int ncells, long long ns, cudaStream_t s) {
+  const int nb = nt * n1;
+  long long g = ((ncells + 1) / 2 + 7) / 8;  // 8 warps per block, 2 elements per warp
+  if (g > 148 * 16) g = 148 * 16;
+  switch (nb) {
+    case 4: k_eblock2<4><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 6: k_eblock2<6><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 8: k_eblock2<8><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 10: k_eblock2<10><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 12: k_eblock2<12><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 14: k_eblock2<14><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 16: k_eblock2<16><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    default: break;
+  }
+}
+
+bool eblock_f32_supported(int nt, int n1) {
+  const int nb = nt * n1;
+  return nb <= 16 && nb % 2 == 0;
+}
+
+bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   switch (a.g.n1) {
     case 2: return build_nt<2>(Binv, U, a, s);
     case 3: return build_nt<3>(Binv, U, a, s);

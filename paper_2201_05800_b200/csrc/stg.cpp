@@ -916,6 +916,8 @@ int resolve_precond(const stg_handle* h, int kind) {
     if (kind == STG_PRECOND_AUTO || kind == STG_PRECOND_NONE) return STG_PRECOND_NONE;
     throw std::invalid_argument("block-Jacobi preconditioners: advection / Burgers only");
   }
+  if (kind == STG_PRECOND_AUTO && h->desc.dim == 1 && h->desc.model == STG_MODEL_BURGERS)
+    return stg::eblock_f32_supported(h->nt, h->n1) ? STG_PRECOND_EBLOCK : STG_PRECOND_NONE;
   if (kind == STG_PRECOND_AUTO)
     return (h->desc.dim == 1 || fdm_ok(h) || dense2d_ok(h))
                ? STG_PRECOND_EBLOCK
@@ -1058,17 +1060,23 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     a.g = h->g;
     a.n_in = nt;
     a.n_out = nt;
+    if (!stg::eblock_f32_supported(nt, n1))
+      throw std::invalid_argument("element-block Jacobi (Burgers): n_tau * (N+1) <= 16 and even");
     static const bool rebuild = std::getenv("STG_PRECOND_REBUILD") != nullptr;
+    float* fb = reinterpret_cast<float*>(h->ptab.p);
     if (!h->eblock_valid || rebuild) {
-      h->ptab.ensure(size_t(ncells) * nb * nb);
-      if (!stg::build_burgers_eblock(h->ptab.p, U, a, h->stream))
+      h->ptab.ensure((size_t(ncells) * nb * nb + 1) / 2);  // fp32 blocks
+      fb = reinterpret_cast<float*>(h->ptab.p);
+      if (!stg::build_burgers_eblock(fb, U, a, h->stream))
         throw std::invalid_argument("element-block Jacobi: degree <= 3 for Burgers");
       h->launches++;
       check_launch(h);
       h->eblock_valid = true;
     }
-    bstride = (long long)nb * nb;
-    tab = h->ptab.p;
+    return [h, fb, nt, n1, ncells, ns](const double* in, double* out) {
+      stg::precond_eblock_f32(out, in, fb, nt, n1, ncells, ns, h->stream);
+      h->launches++;
+    };
   }
   return [h, tab, bstride, nt, n1, ncells, ns](const double* in, double* out) {
     stg::precond_eblock(out, in, tab, bstride, nt, n1, ncells, ns, h->stream);
