@@ -5,7 +5,8 @@ Plain nvcc (no torch JIT cache): every translation unit is compiled with
 library next to this file, so the built artefact travels with the repo
 snapshot to the GPU box.  The static CUDA runtime is linked in; the driver API
 entry point for TMA descriptors is resolved at run time through
-``cudaGetDriverEntryPoint`` (no -lcuda).
+``cudaGetDriverEntryPoint`` (no -lcuda).  cuBLAS is linked for one plain
+GEMM (the d = 2 dense element-block preconditioner).
 """
 from __future__ import annotations
 
@@ -67,7 +68,10 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         subprocess.run(cmd, check=True)
         objs.append(str(o))
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = cc + ARCH + ["-shared", "-o", str(tmp)] + objs
+    # cuBLAS: the plain DGEMM of the d = 2 dense element-block preconditioner
+    cudalib = Path(nvcc()).resolve().parent.parent / "lib64"
+    cmd = cc + ARCH + ["-shared", "-o", str(tmp)] + objs + [
+        f"-L{cudalib}", "-lcublas", "-Xlinker", f"-rpath={cudalib}"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

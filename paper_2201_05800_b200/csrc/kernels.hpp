@@ -180,6 +180,10 @@ void precond_eblock(double* out, const double* in, const double* B, long long bs
 // d = 2: out_e = B in_e with ONE shared dense block B ((n_tau*npc)^2, <= 128^2)
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
                           int ncells, long long ns, cudaStream_t s);
+// stage-major [t][cell][node] <-> element-major [cell][t][node] (n = nt * ns)
+void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s);
+void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
+                       cudaStream_t s);
 // per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U,
 // stored in fp32 (a preconditioner; applied in fp64 arithmetic)
 bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s);

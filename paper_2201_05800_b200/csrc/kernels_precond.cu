@@ -364,6 +364,38 @@ bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   }
 }
 
+// stage-major [t][cell][node] <-> element-major [cell][t][node]
+__global__ void k_to_elem(double* __restrict__ Xp, const double* __restrict__ X, int nt, int npc,
+                          long long n, long long ns) {
+  const long long nb = (long long)nt * npc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long e = i / nb, r = i - e * nb;
+    const int t = int(r / npc), node = int(r - (long long)t * npc);
+    Xp[i] = __ldcs(X + t * ns + e * npc + node);
+  }
+}
+__global__ void k_from_elem(double* __restrict__ Y, const double* __restrict__ Yp, int nt,
+                            int npc, long long n, long long ns) {
+  const long long nb = (long long)nt * npc;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long t = i / ns, rem = i - t * ns;
+    const long long e = rem / npc, node = rem - e * npc;
+    Y[i] = __ldcs(Yp + e * nb + t * npc + node);
+  }
+}
+
+void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s) {
+  const long long n = ns * nt;
+  k_to_elem<<<pgrid(n), kPB, 0, s>>>(Xp, X, nt, npc, n, ns);
+}
+void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
+                       cudaStream_t s) {
+  const long long n = ns * nt;
+  k_from_elem<<<pgrid(n), kPB, 0, s>>>(Y, Yp, nt, npc, n, ns);
+}
+
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
                           int ncells, long long ns, cudaStream_t s) {
   const int nb = nt * npc;

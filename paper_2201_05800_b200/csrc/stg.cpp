@@ -2,6 +2,7 @@
 // dispatch, device-resident GMRES(m), Newton and the STDG / LoDG steps.
 // Control flow follows the reference drivers (stdg.hpp:120-143,
 // lodg.hpp:89-149, newton.hpp:102-130); all vector work is on the device.
+#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -104,7 +105,8 @@ struct stg_handle {
   DevBuf etab;  // d = 1 advection element block (shared), keyed by mix
   stg::MixCoef etab_mix{};
   bool etab_valid = false;
-  DevBuf dtab;
+  DevBuf dtab, pz1, pz2;  // d = 2 dense block; element-major work vectors
+  cublasHandle_t cublas = nullptr;
   stg::MixCoef dense_mix{};
   bool dense_valid = false;
   // d = 3 fast-diagonalisation factors and the mix they belong to
@@ -119,6 +121,7 @@ struct stg_handle {
   cudaEvent_t ev_start = nullptr, ev_in[kChunks] = {}, ev_c[kChunks] = {};
 
   ~stg_handle() {
+    if (cublas) cublasDestroy(cublas);
     if (pinned) cudaFreeHost(pinned);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
@@ -933,6 +936,37 @@ int resolve_precond(const stg_handle* h, int kind) {
   return kind;
 }
 
+// d = 2 dense element block: out = B in for every element.  A plain GEMM
+// (nb x nb) x (nb x n_cells) on the element-major copy of the vector: permute
+// (own kernel), cuBLAS DGEMM, permute back.  STG_DENSE_OWN_KERNEL=1 uses the
+// hand-written smem-tiled kernel instead (kernels_precond.cu).
+Op dense_op(stg_handle* h, const double* tab, int nt, int npc, int ncells, long long ns) {
+  return [h, tab, nt, npc, ncells, ns](const double* in, double* out) {
+    static const bool own = std::getenv("STG_DENSE_OWN_KERNEL") != nullptr;
+    if (own) {
+      if (!stg::precond_eblock_dense(out, in, tab, nt, npc, ncells, ns, h->stream))
+        throw std::runtime_error("element-block preconditioner launch failed");
+      h->launches++;
+      return;
+    }
+    const int nb = nt * npc;
+    const size_t n = size_t(ns) * nt;
+    h->pz1.ensure(n);
+    h->pz2.ensure(n);
+    if (!h->cublas && cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasCreate failed");
+    cublasSetStream(h->cublas, h->stream);
+    stg::permute_to_elem(h->pz1.p, in, nt, npc, ns, h->stream);
+    const double one = 1.0, zero = 0.0;
+    // column-major: Yp (nb x cells) = B Xp; the row-major B is op(T) of its buffer
+    if (cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, nb, ncells, nb, &one, tab, nb, h->pz1.p,
+                    nb, &zero, h->pz2.p, nb) != CUBLAS_STATUS_SUCCESS)
+      throw CudaError("cublasDgemm failed");
+    stg::permute_from_elem(out, h->pz2.p, nt, npc, ns, h->stream);
+    h->launches += 3;
+  };
+}
+
 // Inverse of the (shared) element block of the d = 1 advection Jacobian with
 // temporal mixing (T, S): rows / columns (r, i), (j, q) of the element-local
 // block T (x) I + S (x) V.  Uploaded to h->ptab; returns the device pointer.
@@ -992,11 +1026,7 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     if (h->dense_valid && std::memcmp(&h->dense_mix, &mx, sizeof mx) == 0) {
       const double* tab = h->dtab.p;
       const int ncells = h->g.n_cells;
-      return [h, tab, nt, npc, ncells, ns](const double* in, double* out) {
-        if (!stg::precond_eblock_dense(out, in, tab, nt, npc, ncells, ns, h->stream))
-          throw std::runtime_error("element-block preconditioner launch failed");
-        h->launches++;
-      };
+      return dense_op(h, tab, nt, npc, ncells, ns);
     }
     std::vector<double> B(size_t(nbd) * nbd, 0.0);
     for (int r = 0; r < nt; ++r)
@@ -1020,11 +1050,7 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     h->dense_valid = true;
     const double* tab = h->dtab.p;
     const int ncells = h->g.n_cells;
-    return [h, tab, nt, npc, ncells, ns](const double* in, double* out) {
-      if (!stg::precond_eblock_dense(out, in, tab, nt, npc, ncells, ns, h->stream))
-        throw std::runtime_error("element-block preconditioner launch failed");
-      h->launches++;
-    };
+    return dense_op(h, tab, nt, npc, ncells, ns);
   }
   if (d == 3) {  // element-block Jacobi by fast diagonalisation
     stg::FdmCoef c;
