@@ -692,7 +692,11 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
                                 const double* U_host, double* R_host) {
   const stg::Geometry& g = h->g;
   if (h->kernel_pref == STG_KERNEL_GENERIC || g.dim != 3 || g.nz < 2) return false;
-  int K = stg_handle::kChunks;
+  static const int kenv = [] {
+    const char* e = std::getenv("STG_PIPE_K");
+    return e ? std::atoi(e) : 0;
+  }();
+  int K = kenv > 0 && kenv <= stg_handle::kChunks ? kenv : stg_handle::kChunks;
   while (K > 1 && g.nz % K) --K;
   if (K < 2) return false;
   const long long ns = h->n_sdof, nd = h->n_dof;
@@ -727,11 +731,17 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
   ck(cudaEventRecord(h->ev_start, h->stream), "event");
   ck(cudaStreamWaitEvent(h->s_in, h->ev_start, 0), "wait");
   const size_t pitch = sizeof(double) * size_t(ns);  // one temporal block
+  static const bool one_d = std::getenv("STG_PIPE_1D") != nullptr;
   auto copy_layers = [&](int z0, int nl) {
     const long long off = z0 * layer, cnt = nl * layer;
-    // one strided copy moves the chunk's slice of all n_tau blocks
-    ck(cudaMemcpy2DAsync(h->host_U.p + off, pitch, U_host + off, pitch, sizeof(double) * cnt,
-                         size_t(h->nt), cudaMemcpyHostToDevice, h->s_in), "H2D");
+    if (one_d) {  // one contiguous copy per temporal block
+      for (int t = 0; t < h->nt; ++t)
+        ck(cudaMemcpyAsync(h->host_U.p + t * ns + off, U_host + t * ns + off,
+                           sizeof(double) * cnt, cudaMemcpyHostToDevice, h->s_in), "H2D");
+    } else {  // one strided copy moves the chunk's slice of all n_tau blocks
+      ck(cudaMemcpy2DAsync(h->host_U.p + off, pitch, U_host + off, pitch, sizeof(double) * cnt,
+                           size_t(h->nt), cudaMemcpyHostToDevice, h->s_in), "H2D");
+    }
     ck(cudaMemcpyAsync(h->host_u.p + off, un_host + off, sizeof(double) * cnt,
                        cudaMemcpyHostToDevice, h->s_in), "H2D");
   };
@@ -764,8 +774,14 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
     stamp(h->stream);
     ck(cudaStreamWaitEvent(h->s_out, h->ev_c[k], 0), "wait");
     const long long off = k * L * layer, cnt = L * layer;
-    ck(cudaMemcpy2DAsync(R_host + off, pitch, h->host_R.p + off, pitch, sizeof(double) * cnt,
-                         size_t(h->nt), cudaMemcpyDeviceToHost, h->s_out), "D2H");
+    if (one_d) {
+      for (int t = 0; t < h->nt; ++t)
+        ck(cudaMemcpyAsync(R_host + t * ns + off, h->host_R.p + t * ns + off,
+                           sizeof(double) * cnt, cudaMemcpyDeviceToHost, h->s_out), "D2H");
+    } else {
+      ck(cudaMemcpy2DAsync(R_host + off, pitch, h->host_R.p + off, pitch, sizeof(double) * cnt,
+                           size_t(h->nt), cudaMemcpyDeviceToHost, h->s_out), "D2H");
+    }
     stamp(h->s_out);
   }
   ck(cudaStreamSynchronize(h->s_out), "sync");
