@@ -374,6 +374,73 @@ def _wall(torch, fn):
     return time.perf_counter() - t0, r
 
 
+def rank3_experiments(torch, dev, args):
+    """run_advdiff (N = 16, n_tau = 3, STDG and LoDG to T = 1) and
+    run_euler_vortex (16^2, p = 1, LoDG n_tau = 2, dt 0.05, 10 steps) on the
+    device: wall time and the reference's error measures; the CPU oracle's
+    time for the vortex run beside it."""
+    import math
+    import numpy as np
+    from paper_2201_05800_b200 import configs as C
+    from paper_2201_05800_b200 import _lib as L
+    from paper_2201_05800_b200.api import NewtonConfig, SlabOperator
+    res = {}
+    N, nt = 16, 3
+    op = SlabOperator(2, nt - 1, nt, (N, N), (0.0, 0.0), (1.0, 1.0), model=L.STG_MODEL_ADVDIFF,
+                      velocity_field=L.STG_FIELD_ROTATING, eps=0.001)
+    X = C.grid_coords(2, nt - 1, (N, N), (0.0, 0.0), (1.0, 1.0))
+    h = 1.0 / N
+    _, w, _ = op.constants()  # LGL weights of the spatial rule
+    m = np.outer(w, w).reshape(-1) * (h * h / 4.0)  # global_mass, mesh.hpp:125-141
+    mass = np.tile(m, N * N)
+    exact = C.rotating_pulse_exact(1.0, X[:, 0], X[:, 1])
+    nc = NewtonConfig(gmres_tol=1e-12, gmres_max_it=5000)
+    for method in ("stdg", "lodg"):
+        u = torch.as_tensor(C.rotating_pulse_exact(0.0, X[:, 0], X[:, 1]), device=dev)
+        op.stdg_step(0.0, h, u, nc) if method == "stdg" else op.rk_step(L.STG_FORM_A, 0.0, h, u, nc)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for k in range(N):
+            if method == "stdg":
+                _, u, _ = op.stdg_step(k * h, h, u, nc)
+            else:
+                _, u, _ = op.rk_step(L.STG_FORM_A, k * h, h, u, nc)
+        torch.cuda.synchronize()
+        d = u.cpu().numpy() - exact
+        res[f"pulse_{method}_ntau3_N16"] = {
+            "seconds": time.perf_counter() - t0,
+            "l2_error": math.sqrt(float(np.dot(mass, d * d))),
+            "reference_l2_error": 5.38e-3 if method == "stdg" else 5.36e-3}
+    eo = SlabOperator(2, 1, 2, (16, 16), (-10.0, -10.0), (10.0, 10.0), model=L.STG_MODEL_EULER)
+    Xe = C.grid_coords(2, 1, (16, 16), (-10.0, -10.0), (10.0, 10.0))
+    u0 = C.vortex_initial(Xe[:, 0], Xe[:, 1]).reshape(-1)
+    nce = NewtonConfig(gmres_tol=1e-8, gmres_max_it=5000)
+    u = torch.as_tensor(u0, device=dev)
+    eo.rk_step(L.STG_FORM_A, 0.0, 0.05, u, nce)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    newton = 0
+    for k in range(10):
+        _, u, info = eo.rk_step(L.STG_FORM_A, 0.05 * k, 0.05, u, nce)
+        newton = max(newton, info.newton_iterations)
+    torch.cuda.synchronize()
+    res["euler_vortex_16x16_10steps"] = {"seconds": time.perf_counter() - t0,
+                                         "min_density": float(u[0::4].min()),
+                                         "max_newton_per_step": newton}
+    if not args.no_cpu:
+        import oracle as O
+        pr = O.Problem(2, 1, [16, 16], [-10.0, -10.0], [10.0, 10.0], model=O.EULER, n_tau=2)
+        uc = u0.copy()
+        t0 = time.perf_counter()
+        for k in range(10):
+            _, uc, _, _ = pr.rk_step(2, 0, 0.05 * k, 0.05, uc, linear=O.GMRES, gmres_tol=1e-8,
+                                     gmres_max_it=5000)
+        res["euler_vortex_16x16_10steps"]["cpu_oracle_seconds"] = time.perf_counter() - t0
+        res["euler_vortex_16x16_10steps"]["max_rel_gap_to_cpu"] = float(
+            np.abs(u.cpu().numpy() - uc).max() / np.abs(uc).max())
+    return res
+
+
 def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     """Slab solves of every BASELINE config (device-resident u_n, from guess
     1 (x) u_n, wall time with a CUDA sync on both sides), the c5 stage system
@@ -464,6 +531,13 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
         return uu
     t3, _ = _wall(torch, ten)
     out["c3_10_slabs"] = {"seconds": t3, "per_slab_s": t3 / 10, "newton_gmres": its}
+    # rank 3: the reference's own experiments on the device --
+    # rotating pulse (acceptance criterion 6, experiments.hpp:133-175) and the
+    # Euler vortex (criterion 9, experiments.hpp:188-262)
+    try:
+        out["rank3"] = rank3_experiments(torch, dev, args)
+    except Exception as e:  # report, do not fail the bench
+        out["rank3"] = f"unavailable: {e}"
     # CPU reference (oracle) solves beside them
     if not args.no_cpu:
         try:
