@@ -505,3 +505,43 @@ def test_c3_fused_solve_matches_host_driven():
     # inexact Newton to ||R||_inf <= 1e-12: both land on the same solution
     assert rel(uf, uh.cpu().numpy()) <= 1e-9
     assert inf_f.newton_iterations == inf_h.newton_iterations
+
+
+def _random_configs(n, seed=2024):
+    rng = np.random.default_rng(seed)
+    out = []
+    while len(out) < n:
+        d = int(rng.integers(1, 4))
+        p = int(rng.integers(1, 5 if d < 3 else 5))
+        nt = int(rng.integers(2, 7))
+        if d == 1:
+            cells = (int(rng.choice([1, 2, 3, 7, 16, 33, 64])),)
+        elif d == 2:
+            cells = tuple(int(x) for x in rng.choice([1, 2, 3, 4, 5, 8, 16, 32], 2))
+        else:
+            cells = tuple(int(x) for x in rng.choice([1, 2, 3, 4, 8], 3))
+        vel = tuple(float(v) for v in rng.choice([-1.3, -0.4, 0.0, 0.6, 1.1], d))
+        out.append(make(d, p, nt, cells, vel, dt=float(rng.uniform(1e-3, 5e-2))))
+    return out
+
+
+SWEEP = _random_configs(40)
+
+
+@pytest.mark.parametrize("cfg", SWEEP, ids=[f"{c.dim}d-p{c.degree}-nt{c.n_tau}-{c.cells}"
+                                            for c in SWEEP])
+def test_random_sweep_parity(cfg):
+    """Seeded sweep over (d, N, n_tau, mesh, velocity signs incl. 0): R(U),
+    J.v and both stage residuals vs the oracle, with whatever kernel AUTO
+    selects for the shape."""
+    op, pr = pair(cfg)
+    rng = np.random.default_rng(7)
+    un = rng.uniform(-1, 1, cfg.n_sdof)
+    U = rng.uniform(-1, 1, cfg.n_dof)
+    v = rng.uniform(-1, 1, cfg.n_dof)
+    assert rel(op.st_residual(0.0, cfg.dt, dev(un), dev(U)), pr.st_residual(0.0, cfg.dt, un, U)) <= TOL_OP
+    assert rel(op.st_jvp(0.0, cfg.dt, None, dev(v)), pr.st_jvp(0.0, cfg.dt, U, v)) <= TOL_OP
+    if cfg.n_tau in (2, 3, 4):
+        for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
+            got = op.stage_residual(form, 0.0, cfg.dt, dev(un), dev(U))
+            assert rel(got, pr.stage_residual(cfg.n_tau, form, 0.0, cfg.dt, un, U)) <= TOL_OP
