@@ -366,17 +366,30 @@ inline StdgTrajectory stdg_integrate(const SemiDiscreteSystem& system, const Sbp
                                      double t0, const Vec& u0, double t_end, int n_steps,
                                      const NewtonConfig& cfg = {}) {
   if (n_steps < 1) throw std::invalid_argument("stdg_integrate: n_steps >= 1 required");
+  SlabOperator& o = system.op(ops.n);
+  if (u0.size() != o.n_sdof()) throw std::invalid_argument("stdg_integrate: u0 size mismatch");
   StdgTrajectory traj;
   traj.times.resize(size_t(n_steps) + 1);
   for (int k = 0; k <= n_steps; ++k) traj.times[size_t(k)] = t0 + (t_end - t0) * k / n_steps;
-  traj.states.push_back(u0);
-  const double dt = (t_end - t0) / n_steps;
-  for (int k = 0; k < n_steps; ++k) {
-    StdgStepResult st = stdg_step(system, ops, traj.times[size_t(k)], traj.states.back(), dt, cfg);
-    traj.states.push_back(std::move(st.u_next));
-    traj.element_solutions.push_back(std::move(st.U));
-    traj.total_newton_iterations += st.newton_iterations;
-  }
+  // marched on the device (stg_stdg_integrate), one download at the end
+  DeviceVec du(u0), uf(o.n_sdof()), st((size_t(n_steps) + 1) * o.n_sdof()),
+      sol(size_t(n_steps) * o.n_dof());
+  const stg_newton_config c = cfg.c();
+  stg_solve_info info{};
+  const int code = stg_stdg_integrate(o.handle(), t0, du.data(), t_end, n_steps, &c, uf.data(),
+                                      st.data(), sol.data(), &info);
+  if (code == STG_ERR_NONCONVERGENCE)
+    throw NonconvergenceError(stg_last_error(o.handle()),
+                              Vec(info.residual_history, info.residual_history + info.n_history));
+  check(code, o.handle());
+  const Vec all = st.download(), sols = sol.download();
+  for (int k = 0; k <= n_steps; ++k)
+    traj.states.emplace_back(all.begin() + long(size_t(k) * o.n_sdof()),
+                             all.begin() + long(size_t(k + 1) * o.n_sdof()));
+  for (int k = 0; k < n_steps; ++k)
+    traj.element_solutions.emplace_back(sols.begin() + long(size_t(k) * o.n_dof()),
+                                        sols.begin() + long(size_t(k + 1) * o.n_dof()));
+  traj.total_newton_iterations = info.newton_iterations;
   return traj;
 }
 

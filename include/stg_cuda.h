@@ -213,6 +213,23 @@ int stg_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
                   const stg_newton_config* cfg, double* U, double* u_next,
                   stg_solve_info* info);
 
+/* stdg_integrate (stdg.hpp:152-173), device-resident: n_steps sequential slabs
+ * from u0 over [t0, t_end] (t_k = t0 + (t_end - t0) k / n_steps, as the
+ * reference), no host round trip between slabs.  u_final (n_sdof) receives the
+ * last state; states (optional, (n_steps + 1) * n_sdof) every state incl. u0;
+ * U_slabs (optional, n_steps * n_dof) every slab solution.  info: Newton and
+ * GMRES iterations summed over the slabs (total_newton_iterations,
+ * stdg.hpp:150), the last slab's residual and history. */
+int stg_stdg_integrate(stg_handle* h, double t0, const double* u0, double t_end, int n_steps,
+                       const stg_newton_config* cfg, double* u_final, double* states,
+                       double* U_slabs, stg_solve_info* info);
+
+/* integrate (lodg.hpp:158-181), device-resident: n_steps rk_steps of the
+ * n_tau-stage Lobatto IIIC scheme; U_stages (optional, n_steps * n_dof). */
+int stg_rk_integrate(stg_handle* h, int form, double t0, const double* u0, double t_end,
+                     int n_steps, const stg_newton_config* cfg, double* u_final, double* states,
+                     double* U_stages, stg_solve_info* info);
+
 /* rk_step (lodg.hpp:89-149): Newton on the stage system from 1 (x) u, then
  * u_next = u + dt sum_j b_j F(t + c_j dt, U_j).  U: s*n_sdof stages. */
 int stg_rk_step(stg_handle* h, int form, double t, double dt, const double* u,

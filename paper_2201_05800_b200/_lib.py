@@ -27,7 +27,7 @@ EXPORTS = (
     "stg_set_stream", "stg_set_kernel", "stg_sizes", "stg_constants",
     "stg_spatial_rhs", "stg_spatial_jvp", "stg_st_residual", "stg_st_jvp",
     "stg_stage_residual", "stg_stage_jvp", "stg_gmres_st", "stg_st_precond_apply",
-    "stg_stdg_step", "stg_rk_step",
+    "stg_stdg_step", "stg_rk_step", "stg_stdg_integrate", "stg_rk_integrate",
     "stg_st_residual_host", "stg_stdg_step_host", "stg_rk_step_host", "stg_kernel_launches",
     "stg_lgl_rule", "stg_diff_matrix", "stg_lobatto_tableau",
     "stg_device_alloc", "stg_device_free", "stg_memcpy", "stg_device_synchronize",
@@ -96,6 +96,8 @@ def load() -> ctypes.CDLL:
     L.stg_stage_residual.argtypes = [_vp, _i, _d, _d, _vp, _vp, _vp]
     L.stg_stage_jvp.argtypes = [_vp, _i, _d, _d, _vp, _vp, _vp, _d]
     L.stg_st_precond_apply.argtypes = [_vp, _d, _vp, _i, _vp, _vp]
+    L.stg_stdg_integrate.argtypes = [_vp, _d, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp]
+    L.stg_rk_integrate.argtypes = [_vp, _i, _d, _vp, _d, _i, _vp, _vp, _vp, _vp, _vp]
     L.stg_gmres_st.argtypes = [_vp, _d, _d, _vp, _vp, _vp, _i, _d, _i, _i, ctypes.POINTER(_i),
                                ctypes.POINTER(_d)]
     cfgp = ctypes.POINTER(StgNewtonConfig)

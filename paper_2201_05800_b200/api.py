@@ -262,6 +262,43 @@ class SlabOperator:
         _raise(self._h, code, self._lib)
         return U, u_next, _info(info)
 
+    def _integrate(self, fn, head, u0, t_end, n_steps, cfg, keep_states, keep_solutions):
+        cfg = cfg or NewtonConfig()
+        u_final = self._new(self.n_sdof)
+        states = self._new((n_steps + 1) * self.n_sdof) if keep_states else None
+        sols = self._new(n_steps * self.n_dof) if keep_solutions else None
+        info = L.StgSolveInfo()
+        c = cfg.to_c()
+        self._lib.stg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        code = fn(self._h, *head, _ptr(u0, self.n_sdof, "u0"), float(t_end), int(n_steps),
+                  ctypes.byref(c), _ptr(u_final, self.n_sdof, "u_final"),
+                  None if states is None else states.data_ptr(),
+                  None if sols is None else sols.data_ptr(), ctypes.byref(info))
+        if code == L.STG_ERR_NONCONVERGENCE:
+            raise NonconvergenceError(self._lib.stg_last_error(self._h).decode(),
+                                      _info(info).residual_history)
+        _raise(self._h, code, self._lib)
+        if states is not None:
+            states = states.view(n_steps + 1, self.n_sdof)
+        if sols is not None:
+            sols = sols.view(n_steps, self.n_dof)
+        return u_final, states, sols, _info(info)
+
+    def stdg_integrate(self, t0: float, u0, t_end: float, n_steps: int,
+                       cfg: Optional[NewtonConfig] = None, keep_states: bool = False,
+                       keep_solutions: bool = False):
+        """stdg_integrate (stdg.hpp:152-173), marched on the device: returns
+        (u_final, states or None, slab solutions or None, SolveInfo totals)."""
+        return self._integrate(self._lib.stg_stdg_integrate, (float(t0),), u0, t_end, n_steps,
+                               cfg, keep_states, keep_solutions)
+
+    def rk_integrate(self, form: int, t0: float, u0, t_end: float, n_steps: int,
+                     cfg: Optional[NewtonConfig] = None, keep_states: bool = False,
+                     keep_solutions: bool = False):
+        """integrate (lodg.hpp:158-181), marched on the device."""
+        return self._integrate(self._lib.stg_rk_integrate, (int(form), float(t0)), u0, t_end,
+                               n_steps, cfg, keep_states, keep_solutions)
+
     def stdg_step(self, t_n: float, dt: float, u_n, cfg: Optional[NewtonConfig] = None, U=None,
                   u_next=None):
         """stdg_step (stdg.hpp:120-143): returns (U, u_next, SolveInfo)."""
@@ -474,14 +511,11 @@ def stdg_integrate(system, ops, t0, u0, t_end, n_steps, cfg=None) -> StdgTraject
     if n_steps < 1:
         raise ValueError("stdg_integrate: n_steps >= 1 required")
     times = [t0 + (t_end - t0) * k / n_steps for k in range(n_steps + 1)]
-    dt = (t_end - t0) / n_steps
-    tr = StdgTrajectory(times, [u0], [])
-    for k in range(n_steps):
-        st = stdg_step(system, ops, times[k], tr.states[-1], dt, cfg)
-        tr.states.append(st.u_next)
-        tr.element_solutions.append(st.U)
-        tr.total_newton_iterations += st.newton_iterations
-    return tr
+    # marched on the device (stg_stdg_integrate): no host round trip per slab
+    _, states, sols, info = system.op(ops.n).stdg_integrate(t0, u0, t_end, n_steps, cfg,
+                                                            keep_states=True, keep_solutions=True)
+    return StdgTrajectory(times, [states[k] for k in range(n_steps + 1)],
+                          [sols[k] for k in range(n_steps)], info.newton_iterations)
 
 
 @dataclass
@@ -515,11 +549,8 @@ def integrate(system, tab, t0, u0, t_end, n_steps, cfg=None, jac_form=JacobianFo
     if n_steps < 1:
         raise ValueError("integrate: n_steps >= 1 required")
     times = [t0 + (t_end - t0) * k / n_steps for k in range(n_steps + 1)]
-    dt = (t_end - t0) / n_steps
-    tr = RkTrajectory(times, [u0], [])
-    for k in range(n_steps):
-        st = rk_step(system, tab, times[k], tr.states[-1], dt, cfg, jac_form)
-        tr.states.append(st.u_next)
-        tr.stage_solutions.append(st.stages)
-        tr.total_newton_iterations += st.newton_iterations
-    return tr
+    # marched on the device (stg_rk_integrate)
+    _, states, sols, info = system.op(tab.s).rk_integrate(jac_form, t0, u0, t_end, n_steps, cfg,
+                                                          keep_states=True, keep_solutions=True)
+    return RkTrajectory(times, [states[k] for k in range(n_steps + 1)],
+                        [sols[k] for k in range(n_steps)], info.newton_iterations)

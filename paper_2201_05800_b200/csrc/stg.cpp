@@ -97,6 +97,7 @@ struct stg_handle {
   DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
   DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
   DevBuf small_out;      // fused small-solve result record
+  DevBuf march;          // integrate: ping-pong states
   // Burgers element blocks: built at the first Newton iteration of a step and
   // reused for the rest of it (a lagged preconditioner; STG_PRECOND_REBUILD=1
   // rebuilds every iteration)
@@ -1325,6 +1326,42 @@ void need(const void* p, const char* what) {
   if (!p) throw std::invalid_argument(std::string(what) + ": null pointer");
 }
 
+// march n_steps with `step(t_k, dt, u_k, U_k, u_{k+1}, info_k)` on the device
+template <class Step>
+void integrate_impl(stg_handle* h, double t0, const double* u0, double t_end, int n_steps,
+                    double* u_final, double* states, double* U_all, stg_solve_info* info,
+                    const char* who, Step&& step) {
+  if (n_steps < 1) throw std::invalid_argument(std::string(who) + ": n_steps >= 1 required");
+  const long long ns = h->n_sdof, nd = h->n_dof;
+  const double dt = (t_end - t0) / n_steps;
+  if (!(dt > 0)) throw std::invalid_argument(std::string(who) + ": t_end > t0 required");
+  h->Ustage.ensure(size_t(nd));
+  h->march.ensure(size_t(2 * ns));  // ping-pong states when `states` is not given
+  if (states) {
+    ck(cudaMemcpyAsync(states, u0, sizeof(double) * ns, cudaMemcpyDeviceToDevice, h->stream),
+       "memcpy");
+  }
+  const double* cur = u0;
+  stg_solve_info acc{};
+  for (int k = 0; k < n_steps; ++k) {
+    const double tk = t0 + (t_end - t0) * k / n_steps;  // stdg.hpp:160-161
+    double* next = states ? states + (k + 1) * ns
+                          : (k + 1 == n_steps ? u_final : h->march.p + (k % 2) * ns);
+    double* Uk = U_all ? U_all + (long long)k * nd : h->Ustage.p;
+    stg_solve_info ik{};
+    step(tk, dt, cur, Uk, next, &ik);
+    acc.newton_iterations += ik.newton_iterations;
+    acc.linear_iterations += ik.linear_iterations;
+    acc.final_residual = ik.final_residual;
+    acc.n_history = ik.n_history;
+    std::memcpy(acc.residual_history, ik.residual_history, sizeof acc.residual_history);
+    cur = next;
+  }
+  if (states && u_final)
+    ck(cudaMemcpyAsync(u_final, states + (long long)n_steps * ns, sizeof(double) * ns,
+                       cudaMemcpyDeviceToDevice, h->stream), "memcpy");
+  if (info) *info = acc;
+}
 }  // namespace
 
 extern "C" {
@@ -1607,6 +1644,33 @@ int stg_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
     need(u_n, "u_n");
     need(U, "U");
     do_stdg_step(h, t_n, dt, u_n, cfg, U, u_next, info);
+  });
+}
+
+
+int stg_stdg_integrate(stg_handle* h, double t0, const double* u0, double t_end, int n_steps,
+                       const stg_newton_config* cfg, double* u_final, double* states,
+                       double* U_slabs, stg_solve_info* info) {
+  return guarded(h, [&] {
+    need(h, "stg_stdg_integrate");
+    need(u0, "u0");
+    need(u_final, "u_final");
+    integrate_impl(h, t0, u0, t_end, n_steps, u_final, states, U_slabs, info, "stdg_integrate",
+                   [&](double tk, double dt, const double* uk, double* Uk, double* un,
+                       stg_solve_info* ik) { do_stdg_step(h, tk, dt, uk, cfg, Uk, un, ik); });
+  });
+}
+
+int stg_rk_integrate(stg_handle* h, int form, double t0, const double* u0, double t_end,
+                     int n_steps, const stg_newton_config* cfg, double* u_final, double* states,
+                     double* U_stages, stg_solve_info* info) {
+  return guarded(h, [&] {
+    need(h, "stg_rk_integrate");
+    need(u0, "u0");
+    need(u_final, "u_final");
+    integrate_impl(h, t0, u0, t_end, n_steps, u_final, states, U_stages, info, "integrate",
+                   [&](double tk, double dt, const double* uk, double* Uk, double* un,
+                       stg_solve_info* ik) { do_rk_step(h, form, tk, dt, uk, cfg, Uk, un, ik); });
   });
 }
 

@@ -545,3 +545,31 @@ def test_random_sweep_parity(cfg):
         for form in (L.STG_FORM_A, L.STG_FORM_A_INV):
             got = op.stage_residual(form, 0.0, cfg.dt, dev(un), dev(U))
             assert rel(got, pr.stage_residual(cfg.n_tau, form, 0.0, cfg.dt, un, U)) <= TOL_OP
+
+
+@pytest.mark.parametrize("name", ["c1", "c4@8"])
+def test_device_integrate_matches_step_loop(name):
+    """stg_stdg_integrate / stg_rk_integrate (stdg.hpp:152-173, lodg.hpp:158-181)
+    march on the device and reproduce a host loop of steps bit for bit."""
+    cfg = C.CONFIGS["c1"] if name == "c1" else C.CONFIGS["c4"].scaled((8, 8, 8))
+    op = SlabOperator(**cfg.kwargs())
+    u0 = dev(C.initial_state(cfg))
+    nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-10, gmres_tol=1e-11)
+    n, t0, t1 = 3, 0.1, 0.1 + 3 * cfg.dt
+    uf, states, sols, info = op.stdg_integrate(t0, u0, t1, n, nc, keep_states=True,
+                                               keep_solutions=True)
+    u, tot = u0, 0
+    for k in range(n):
+        U, u, inf = op.stdg_step(t0 + (t1 - t0) * k / n, (t1 - t0) / n, u, nc)
+        assert torch.equal(states[k + 1], u)
+        assert torch.equal(sols[k], U)
+        tot += inf.newton_iterations
+    assert torch.equal(uf, u) and torch.equal(states[0], u0)
+    assert info.newton_iterations == tot
+    uf2, _, _, _ = op.rk_integrate(L.STG_FORM_A_INV, t0, u0, t1, n, nc)
+    u = u0
+    for k in range(n):
+        _, u, _ = op.rk_step(L.STG_FORM_A_INV, t0 + (t1 - t0) * k / n, (t1 - t0) / n, u, nc)
+    assert torch.equal(uf2, u)
+    with pytest.raises(ValueError):
+        op.stdg_integrate(0.0, u0, 1.0, 0, nc)
