@@ -80,7 +80,8 @@ extern "C" {
  *   EBLOCK  element-block Jacobi (exact inverse of the element-local block:
  *           d = 1 dense; d = 2 advection with n_tau * (N+1)^2 <= 128 one
  *           shared dense block; d = 3 advection, degree 3, n_tau = 4,
- *           cells % 8 == 0 by fast diagonalisation)
+ *           cells % 8 == 0 by fast diagonalisation; advdiff (linear general
+ *           model) with n_tau * (N+1)^d <= 32 by coloured probing)
  *   AUTO    EBLOCK where supported, else TBLOCK (advection) / none. */
 #define STG_PRECOND_NONE 0
 #define STG_PRECOND_TBLOCK 1

@@ -180,6 +180,15 @@ void precond_eblock(double* out, const double* in, const double* B, long long bs
 // d = 2: out_e = B in_e with ONE shared dense block B ((n_tau*npc)^2, <= 128^2)
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
                           int ncells, long long ns, cudaStream_t s);
+// element blocks of the general linear models by coloured probing
+// (ndl = element-local DOFs per temporal block = npc * r)
+void probe_set(double* P, int ndl, int col, int nx, int ny, int sx, int sy, int cx0, int cy0,
+               int ncells, cudaStream_t s);
+void probe_extract(double* K, const double* F, int ndl, int col, int nx, int sx, int sy, int cx0,
+                   int cy0, int ncells, cudaStream_t s);
+// Binv_e = (T (x) I + S (x) K_e)^-1 per element (nt * ndl <= 32)
+bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt, int ndl,
+                       int ncells, cudaStream_t s);
 // stage-major [t][cell][node] <-> element-major [cell][t][node] (n = nt * ns)
 void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s);
 void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,

@@ -350,6 +350,101 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
   }
 }
 
+// ---- element blocks of the general (linear) models by coloured probing -----
+// P = unit entry `col` in every cell of colour (cx0, cy0); after F = F(P) the
+// cells of that colour read column `col` of their local Jacobian K_e off
+// their own rows (same-colour cells are >= 3 apart: neighbour couplings never
+// reach them).  Then B_e = T (x) I + S (x) K_e is inverted per element.
+__global__ void k_probe_set(double* __restrict__ P, int ndl, int col, int nx, int ny, int sx,
+                            int sy, int cx0, int cy0, int ncells) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+    const int cx = c % nx, cy = c / nx;
+    const bool on = (cx % sx) == cx0 && (cy % sy) == cy0;
+    for (int k = 0; k < ndl; ++k) P[(long long)c * ndl + k] = (on && k == col) ? 1.0 : 0.0;
+  }
+}
+__global__ void k_probe_extract(double* __restrict__ K, const double* __restrict__ F, int ndl,
+                                int col, int nx, int sx, int sy, int cx0, int cy0, int ncells) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
+    const int cx = c % nx, cy = c / nx;
+    if ((cx % sx) != cx0 || (cy % sy) != cy0) continue;
+    for (int i = 0; i < ndl; ++i)
+      K[((long long)c * ndl + i) * ndl + col] = F[(long long)c * ndl + i];
+  }
+}
+
+// one warp per element: lane l < nb owns row l = (t, i) of [B_e | I];
+// Gauss-Jordan with partial pivoting without row exchanges (see
+// k_build_burgers_eblock); B_e = T(t,j) delta_ik + S(t,j) K_e(i,k)
+__global__ void __launch_bounds__(128) k_gen_eblock(double* __restrict__ Binv,
+                                                    const double* __restrict__ K,
+                                                    const MixCoef mx, int nt, int ndl,
+                                                    int ncells) {
+  constexpr int MAXB = 32;
+  const int lane = threadIdx.x & 31;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (c >= ncells) return;  // warp-uniform
+  const int nb = nt * ndl;
+  const bool act = lane < nb;
+  const int t = act ? lane / ndl : 0, i = act ? lane - (lane / ndl) * ndl : 0;
+  const double* Kc = K + (size_t)c * ndl * ndl;
+  double row[MAXB], inv[MAXB];
+#pragma unroll
+  for (int q = 0; q < MAXB; ++q) {
+    double v = 0.0;
+    if (act && q < nb) {
+      const int j = q / ndl, k = q - (q / ndl) * ndl;
+      v = (i == k ? mx.T[t][j] : 0.0) + mx.S[t][j] * Kc[i * ndl + k];
+    }
+    row[q] = v;
+    inv[q] = (q == lane && act) ? 1.0 : 0.0;
+  }
+  bool used = !act;
+  int my_col = 0;
+#pragma unroll
+  for (int col = 0; col < MAXB; ++col) {
+    if (col >= nb) break;  // uniform
+    double v = used ? -1.0 : fabs(row[col]);
+    int idx = lane;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
+      if (v2 > v || (v2 == v && i2 < idx)) {
+        v = v2;
+        idx = i2;
+      }
+    }
+    const int p = idx;
+    const double ip = 1.0 / __shfl_sync(0xffffffffu, row[col], p);
+    if (lane == p) {
+#pragma unroll
+      for (int q = 0; q < MAXB; ++q) {
+        row[q] *= ip;
+        inv[q] *= ip;
+      }
+      used = true;
+      my_col = col;
+    }
+    const double f = row[col];
+#pragma unroll
+    for (int q = 0; q < MAXB; ++q) {
+      const double pr = __shfl_sync(0xffffffffu, row[q], p);
+      const double pi = __shfl_sync(0xffffffffu, inv[q], p);
+      if (lane != p) {
+        row[q] = fma(-f, pr, row[q]);
+        inv[q] = fma(-f, pi, inv[q]);
+      }
+    }
+  }
+  if (act) {
+    double* M = Binv + (size_t)c * nb * nb + (size_t)my_col * nb;
+#pragma unroll
+    for (int q = 0; q < MAXB; ++q)
+      if (q < nb) M[q] = inv[q];
+  }
+}
+
 template <int N1>
 bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   const long long threads = (long long)a.g.nx * 32;  // one warp per element
@@ -413,6 +508,22 @@ bool precond_eblock_dense(double* out, const double* in, const double* B, int nt
   const int ntile = (ncells + kTE - 1) / kTE;
   const int grid = ntile < sms ? ntile : sms;
   k_eblock_dense<<<grid, kDenseThreads, smem, s>>>(out, in, B, nb, npc, nt, ncells, ns);
+  return true;
+}
+
+void probe_set(double* P, int ndl, int col, int nx, int ny, int sx, int sy, int cx0, int cy0,
+               int ncells, cudaStream_t s) {
+  k_probe_set<<<pgrid(ncells), kPB, 0, s>>>(P, ndl, col, nx, ny, sx, sy, cx0, cy0, ncells);
+}
+void probe_extract(double* K, const double* F, int ndl, int col, int nx, int sx, int sy, int cx0,
+                   int cy0, int ncells, cudaStream_t s) {
+  k_probe_extract<<<pgrid(ncells), kPB, 0, s>>>(K, F, ndl, col, nx, sx, sy, cx0, cy0, ncells);
+}
+bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt, int ndl,
+                       int ncells, cudaStream_t s) {
+  if (nt * ndl > 32) return false;
+  const long long threads = (long long)ncells * 32;
+  k_gen_eblock<<<int((threads + 127) / 128), 128, 0, s>>>(Binv, K, mx, nt, ndl, ncells);
   return true;
 }
 

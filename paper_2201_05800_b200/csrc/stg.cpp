@@ -98,6 +98,11 @@ struct stg_handle {
   DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
   DevBuf small_out;      // fused small-solve result record
   DevBuf march;          // integrate: ping-pong states
+  // general linear models: element-local Jacobians K_e (probed once) and the
+  // inverted element blocks for the last mix
+  DevBuf gK, gProbe, gBinv;
+  bool gK_valid = false, gB_valid = false;
+  stg::MixCoef g_mix{};
   // Burgers element blocks: built at the first Newton iteration of a step and
   // reused for the rest of it (a lagged preconditioner; STG_PRECOND_REBUILD=1
   // rebuilds every iteration)
@@ -931,10 +936,19 @@ bool fdm_ok(const stg_handle* h) {
   return h->desc.dim == 3 && h->desc.model == STG_MODEL_ADVECTION && stg::fdm_supported(h->g, h->nt);
 }
 
+// general linear models (advdiff): element blocks n_tau * npc * r <= 32
+bool gen_eblock_ok(const stg_handle* h) {
+  return h->desc.model == STG_MODEL_ADVDIFF && h->nt * h->g.npc * h->r <= 32;
+}
+
 int resolve_precond(const stg_handle* h, int kind) {
   if (general_model(h->desc.model)) {
-    if (kind == STG_PRECOND_AUTO || kind == STG_PRECOND_NONE) return STG_PRECOND_NONE;
-    throw std::invalid_argument("block-Jacobi preconditioners: advection / Burgers only");
+    if (kind == STG_PRECOND_NONE) return STG_PRECOND_NONE;
+    if (kind == STG_PRECOND_AUTO) return gen_eblock_ok(h) ? STG_PRECOND_EBLOCK : STG_PRECOND_NONE;
+    if (kind == STG_PRECOND_EBLOCK && gen_eblock_ok(h)) return STG_PRECOND_EBLOCK;
+    throw std::invalid_argument(
+        "block-Jacobi preconditioners for the general models: element blocks of the linear "
+        "advdiff model with n_tau * (N+1)^d <= 32 only");
   }
   if (kind == STG_PRECOND_AUTO && h->desc.dim == 1 && h->desc.model == STG_MODEL_BURGERS)
     return stg::eblock_f32_supported(h->nt, h->n1) ? STG_PRECOND_EBLOCK : STG_PRECOND_NONE;
@@ -1009,9 +1023,68 @@ const double* eblock_table_1d(stg_handle* h, const stg::MixCoef& mx) {
 
 // Right preconditioner for the Jacobian with temporal mixing (T, S) at the
 // linearisation point U (used by the Burgers element blocks only).
+// smallest divisor >= 3 of n (n itself when n <= 2 or prime): same-coloured
+// cells on the periodic lattice are >= 3 apart (spatial.hpp color_stride)
+int color_stride(int n) {
+  if (n <= 2) return n;
+  for (int m = 3; m < n; ++m)
+    if (n % m == 0) return m;
+  return n;
+}
+
+// element-block Jacobi of a general linear model: K_e by coloured probing of
+// the spatial operator (once per handle: linear, time independent), then the
+// blocks T (x) I + S (x) K_e inverted on the device (once per mix)
+Op general_eblock(stg_handle* h, const stg::MixCoef& mx) {
+  const stg::Geometry& g = h->g;
+  const int ndl = g.npc * h->r, nt = h->nt, nb = nt * ndl, nc = g.n_cells;
+  const long long ns = h->n_sdof;
+  if (!h->gK_valid) {
+    h->gK.ensure(size_t(nc) * ndl * ndl);
+    h->gProbe.ensure(size_t(ns));
+    h->genF.ensure(size_t(ns));
+    const int sx = color_stride(g.nx), sy = g.dim == 2 ? color_stride(g.ny) : 1;
+    stg::GenArgs a{};
+    a.c = h->gc;
+    a.g = g;
+    a.n_in = 1;
+    a.X = h->gProbe.p;
+    a.F = h->genF.p;
+    a.R = nullptr;
+    a.err = reinterpret_cast<int*>(h->genFlag.p);
+    for (int cy0 = 0; cy0 < sy; ++cy0)
+      for (int cx0 = 0; cx0 < sx; ++cx0)
+        for (int col = 0; col < ndl; ++col) {
+          stg::probe_set(h->gProbe.p, ndl, col, g.nx, g.ny, sx, sy, cx0, cy0, nc, h->stream);
+          if (stg::launch_general(a, h->stream) < 0)
+            throw std::invalid_argument("no kernel for this (dim, degree, model)");
+          stg::probe_extract(h->gK.p, h->genF.p, ndl, col, g.nx, sx, sy, cx0, cy0, nc,
+                             h->stream);
+          h->launches += 3;
+        }
+    check_launch(h);
+    h->gK_valid = true;
+  }
+  if (!h->gB_valid || std::memcmp(&h->g_mix, &mx, sizeof mx) != 0) {
+    h->gBinv.ensure(size_t(nc) * nb * nb);
+    if (!stg::gen_eblock_invert(h->gBinv.p, h->gK.p, mx, nt, ndl, nc, h->stream))
+      throw std::invalid_argument("element block too large");
+    h->launches++;
+    check_launch(h);
+    h->g_mix = mx;
+    h->gB_valid = true;
+  }
+  const double* tab = h->gBinv.p;
+  return [h, tab, nb, nt, ndl, nc, ns](const double* in, double* out) {
+    stg::precond_eblock(out, in, tab, (long long)nb * nb, nt, ndl, nc, ns, h->stream);
+    h->launches++;
+  };
+}
+
 Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U) {
   kind = resolve_precond(h, kind);
   if (kind == STG_PRECOND_NONE) return Op();
+  if (general_model(h->desc.model)) return general_eblock(h, mx);
   const int nt = h->nt, n1 = h->n1, npc = h->g.npc, d = h->desc.dim;
   const long long ns = h->n_sdof;
   if (kind == STG_PRECOND_TBLOCK) {

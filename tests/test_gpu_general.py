@@ -146,14 +146,55 @@ def test_admissibility_error_names_temporal_node():  # stdg.hpp:41-50, models.hp
     assert rel(op.st_residual(0.0, 0.01, dev(v), dev(V)), pr.st_residual(0.0, 0.01, v, V)) <= TOL_OP
 
 
-def test_general_models_reject_block_preconditioners():
+def test_general_model_preconditioner_resolution():
     op, pr = pulse_pair(4, 1)
     v = dev(np.ones(op.n_dof))
-    for pc in (L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK):
-        with pytest.raises(ValueError):
-            op.st_precond_apply(0.1, v, precond=pc)
-    # AUTO resolves to no preconditioner: P^-1 = I
-    assert float((op.st_precond_apply(0.1, v) - v).abs().max()) == 0.0
+    with pytest.raises(ValueError):  # temporal blocks: constant-velocity advection only
+        op.st_precond_apply(0.1, v, precond=L.STG_PRECOND_TBLOCK)
+    a = op.st_precond_apply(0.1, v)  # AUTO -> element blocks for advdiff
+    b = op.st_precond_apply(0.1, v, precond=L.STG_PRECOND_EBLOCK)
+    assert torch.equal(a, b)
+    eo, _ = euler_pair(4, 1)  # nonlinear Euler: no block preconditioner (AUTO = identity)
+    ve = dev(np.ones(eo.n_dof))
+    assert float((eo.st_precond_apply(0.1, ve, dev(np.tile([1.0, 0.3, -0.2, 2.5], eo.n_dof // 4)))
+                  - ve).abs().max()) == 0.0
+    with pytest.raises(ValueError):
+        eo.st_precond_apply(0.1, ve, dev(np.ones(eo.n_dof)), precond=L.STG_PRECOND_EBLOCK)
+
+
+@pytest.mark.parametrize("cells,p,nt,field,vel", [(6, 2, 3, L.STG_FIELD_ROTATING, (0.0, 0.0)),
+                                                  (5, 1, 2, L.STG_FIELD_CONSTANT, (0.7, -1.1))])
+def test_general_eblock_is_exact_local_inverse(cells, p, nt, field, vel):
+    """advdiff element blocks (coloured probing, kernels_precond.cu) = the exact
+    inverse of each element's local Jacobian block, read off the oracle's J.v."""
+    op, pr = pulse_pair(cells, p, n_tau=nt, field=field, vel=vel, eps=0.01)
+    ns, npc = op.n_sdof, (p + 1) ** 2
+    dt = 0.03
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(nt * ns)
+    y = op.st_precond_apply(dt, dev(x), precond=L.STG_PRECOND_EBLOCK).cpu().numpy()
+    U0 = np.zeros(nt * ns)
+    for cell in (0, cells + 1, cells * cells - 1):  # the velocity field varies per cell
+        loc = np.array([t * ns + cell * npc + k for t in range(nt) for k in range(npc)])
+        Lblk = np.zeros((loc.size, loc.size))
+        for c, i in enumerate(loc):
+            e = np.zeros(nt * ns)
+            e[i] = 1.0
+            Lblk[:, c] = pr.st_jvp(0.0, dt, U0, e)[loc]
+        assert rel(y[loc], np.linalg.solve(Lblk, x[loc])) <= 1e-11, cell
+
+
+def test_pulse_eblock_same_solution_fewer_iterations():
+    op, pr = pulse_pair(16, 2)
+    u = dev(pulse_u(pr))
+    res = {}
+    for pc in (L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK):
+        nc = NewtonConfig(abs_tol=1e-13, rel_tol=1e-13, gmres_tol=1e-13, gmres_max_it=5000,
+                          precond=pc)
+        U, u1, info = op.stdg_step(0.0, 1.0 / 16, u, nc)
+        res[pc] = (U.cpu().numpy(), info.linear_iterations)
+    assert rel(res[L.STG_PRECOND_EBLOCK][0], res[L.STG_PRECOND_NONE][0]) <= TOL_SOLVE
+    assert res[L.STG_PRECOND_EBLOCK][1] * 5 < res[L.STG_PRECOND_NONE][1], res
 
 
 def test_pulse_slab_solves_match_oracle():
