@@ -425,7 +425,7 @@ struct GmresStats {
 // ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at newton.hpp:68-77).
 // x holds the initial guess.
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
-                 double tol, int max_it, const Op* P = nullptr) {
+                 double tol, int max_it, const Op* P = nullptr, bool x_zero = false) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > 60) throw std::invalid_argument("gmres: restart <= 60");
@@ -443,7 +443,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   double* hp = h->pinned;
   cudaStream_t s = h->stream;
 
-  const double bnorm = std::sqrt(dev_dot(h, b, b, n));
+  const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[0]
+  const double bnorm = std::sqrt(bb);
+  ck(cudaMemcpyAsync(h->small.p + 200, h->small.p, sizeof(double), cudaMemcpyDeviceToDevice,
+                     h->stream), "memcpy");
   if (bnorm == 0.0) {
     stg::vec_fill(x, 0.0, n, s);
     h->launches++;
@@ -453,17 +456,27 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   std::vector<double> H(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m);
   auto Hat = [&](int i, int j) -> double& { return H[size_t(i) * m + j]; };
   int total = 0;
+  bool first = true;
   while (true) {
-    A(x, w);                                   // w = A x
-    stg::vec_axpby(w, 1.0, b, -1.0, n, s);     // w = b - A x
-    h->launches++;
-    stg::vec_multidot(w, 0, 1, w, n, h->partial.p, dsm + 200, s);
-    h->launches += 1;
-    ck(cudaMemcpyAsync(hp + 200, dsm + 200, sizeof(double), cudaMemcpyDeviceToHost, s), "memcpy");
-    stg::vec_scale_invsqrt(V, w, dsm + 200, n, s);  // V_0 = r / ||r||
-    h->launches++;
-    ck(cudaStreamSynchronize(s), "sync");
-    const double beta = std::sqrt(hp[200]);
+    double beta;
+    if (first && x_zero) {  // x = 0: r = b and ||r|| = ||b|| (no operator apply, no sync)
+      stg::vec_scale_invsqrt(V, b, dsm + 200, n, s);  // V_0 = b / ||b|| (dsm[200] = <b,b>)
+      h->launches++;
+      beta = bnorm;
+    } else {
+      A(x, w);                                   // w = A x
+      stg::vec_axpby(w, 1.0, b, -1.0, n, s);     // w = b - A x
+      h->launches++;
+      stg::vec_multidot(w, 0, 1, w, n, h->partial.p, dsm + 200, s);
+      h->launches += 1;
+      ck(cudaMemcpyAsync(hp + 200, dsm + 200, sizeof(double), cudaMemcpyDeviceToHost, s),
+         "memcpy");
+      stg::vec_scale_invsqrt(V, w, dsm + 200, n, s);  // V_0 = r / ||r||
+      h->launches++;
+      ck(cudaStreamSynchronize(s), "sync");
+      beta = std::sqrt(hp[200]);
+    }
+    first = false;
     st.rel_residual = beta / bnorm;
     if (st.rel_residual <= tol) {
       st.converged = true;
@@ -554,7 +567,8 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
       h->launches++;
     }
-    ck(cudaStreamSynchronize(s), "sync");  // hp+256 reused next cycle
+    // no sync here: hp+256 is rewritten only after the next cycle's first
+    // host read, which follows this H2D in stream order
   }
   st.iterations = total;
   check_launch(h);
@@ -601,7 +615,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     stg::vec_fill(du, 0.0, n, h->stream);
     h->launches += 2;
     const GmresStats gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
-                                cfg.gmres_max_it, J.P ? &J.P : nullptr);
+                                cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true);
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
