@@ -459,6 +459,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   bool first = true;
   while (true) {
     double beta;
+    double est_rel = -1.0;  // >= 0: the Givens residual estimate met tol
     if (first && x_zero) {  // x = 0: r = b and ||r|| = ||b|| (no operator apply, no sync)
       stg::vec_scale_invsqrt(V, b, dsm + 200, n, s);  // V_0 = b / ||b|| (dsm[200] = <b,b>)
       h->launches++;
@@ -545,7 +546,12 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       Hat(k + 1, k) = 0.0;
       g[k + 1] = -sn[k] * g[k];
       g[k] = cs[k] * g[k];
-      if (std::abs(g[k + 1]) / bnorm <= tol || hn == 0.0 || !std::isfinite(hn)) {
+      if (std::abs(g[k + 1]) / bnorm <= tol) {  // residual estimate converged
+        est_rel = std::abs(g[k + 1]) / bnorm;
+        ++k;
+        break;
+      }
+      if (hn == 0.0 || !std::isfinite(hn)) {
         ++k;
         break;
       }
@@ -566,6 +572,14 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     } else {
       stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
       h->launches++;
+    }
+    if (est_rel >= 0.0) {
+      // stop on the Arnoldi residual estimate, as Eigen's GMRES does; the
+      // re-orthogonalised basis keeps it close to the true residual (the
+      // Newton residual that follows is computed exactly)
+      st.converged = true;
+      st.rel_residual = est_rel;
+      break;
     }
     // no sync here: hp+256 is rewritten only after the next cycle's first
     // host read, which follows this H2D in stream order
