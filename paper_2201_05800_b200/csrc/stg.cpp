@@ -419,11 +419,13 @@ struct GmresStats {
 };
 
 // Restarted GMRES(m), right-preconditioned (A P^-1 y = b, x = P^-1 y; P null:
-// unpreconditioned), classical Gram-Schmidt with one full
-// re-orthogonalisation (CGS2) in three fused passes, Givens rotations on the
-// host.  Right preconditioning keeps the stopping test on the true residual,
-// ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at newton.hpp:68-77).
-// x holds the initial guess.
+// unpreconditioned), classical Gram-Schmidt in two fused passes per Arnoldi
+// step (multidot incl. <w,w>; project + Pythagorean normalise) with a second
+// pass only on heavy cancellation (DGKS-style), Givens rotations on the host.
+// Stopping test ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at
+// newton.hpp:68-77) on the Arnoldi residual estimate, which with right
+// preconditioning is the unpreconditioned residual; the true residual is
+// recomputed at each restart.  x holds the initial guess (x_zero: known 0).
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false) {
   ensure_workspace(h);
