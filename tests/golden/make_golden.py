@@ -80,7 +80,46 @@ def c1_fixture():
     )
 
 
+def small_fixtures():
+    """Oracle outputs for small cases of the other model families (kept small
+    so the npz stays a few hundred KB):
+      c4p  -- c4 physics (d = 3, N = 3, n_tau = 4, b = (1,1,1)) on 2 x 2 x 2 cells
+      c2p  -- c2 physics (d = 2, N = 4, n_tau = 5, b = (1, 0.5)) on 4 x 4 cells
+      pulse -- rotating pulse (advdiff, rotating field, eps 1e-3) 4 x 4, p = 2
+      euler -- 2-D Euler (gamma 1.4) 4 x 4 on [-10,10]^2, p = 1, vortex data
+    For each: the inputs (seeded PCG64) and R(U), J.v (linear models),
+    F(u)."""
+    out = {}
+    rng = np.random.default_rng(20261019)
+    for name, cfg in (("c4p", C.CONFIGS["c4"].scaled((2, 2, 2))),
+                      ("c2p", C.CONFIGS["c2"].scaled((4, 4)))):
+        pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
+                       list(cfg.velocity), n_tau=cfg.n_tau)
+        U = rng.uniform(-1, 1, cfg.n_dof)
+        un = rng.uniform(-1, 1, cfg.n_sdof)
+        v = rng.uniform(-1, 1, cfg.n_dof)
+        out.update({f"{name}_U": U, f"{name}_un": un, f"{name}_v": v,
+                    f"{name}_R": pr.st_residual(0.0, cfg.dt, un, U),
+                    f"{name}_Jv": pr.st_jvp(0.0, cfg.dt, U, v)})
+    pu = O.Problem(2, 2, [4, 4], [0.0, 0.0], [1.0, 1.0], model=O.ADVDIFF,
+                   field=O.FIELD_ROTATING, eps=0.001, n_tau=3)
+    X = pu.coords()
+    u = C.rotating_pulse_exact(0.0, X[:, 0], X[:, 1]) + 0.05 * rng.uniform(-1, 1, pu.dof)
+    U = np.concatenate([u, 0.9 * u, 1.1 * u])
+    out.update({"pulse_u": u, "pulse_F": pu.rhs(u), "pulse_U": U,
+                "pulse_R": pu.st_residual(0.0, 0.02, u, U)})
+    eu = O.Problem(2, 1, [4, 4], [-10.0, -10.0], [10.0, 10.0], model=O.EULER, n_tau=2)
+    X = eu.coords()
+    u = C.vortex_initial(X[:, 0], X[:, 1]).reshape(-1) * (1 + 0.01 * rng.uniform(-1, 1, eu.dof))
+    U = np.concatenate([u, 1.001 * u])
+    out.update({"euler_u": u, "euler_F": eu.rhs(u), "euler_U": U,
+                "euler_R": eu.st_residual(0.0, 0.05, u, U)})
+    return out
+
+
 if __name__ == "__main__":
     (HERE / "reference_kats.json").write_text(json.dumps(kats(), indent=1))
     np.savez_compressed(HERE / "c1_seed0.npz", **c1_fixture())
-    print("wrote", HERE / "reference_kats.json", HERE / "c1_seed0.npz")
+    np.savez_compressed(HERE / "small_cases.npz", **small_fixtures())
+    print("wrote", HERE / "reference_kats.json", HERE / "c1_seed0.npz",
+          HERE / "small_cases.npz")

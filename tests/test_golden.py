@@ -81,3 +81,50 @@ def test_cuda_matches_c1_fixture():
     assert rel(op.st_jvp(0.0, cfg.dt, d(f["U"]), d(f["v"])), f["Jv"]) <= 1e-12
     assert rel(op.stage_residual(0, 0.0, cfg.dt, d(f["u_n"]), d(f["U"])), f["stage_a"]) <= 1e-12
     assert rel(op.stage_residual(1, 0.0, cfg.dt, d(f["u_n"]), d(f["U"])), f["stage_ainv"]) <= 1e-12
+
+
+SMALL = G / "small_cases.npz"
+
+
+def _small_problems():
+    c4p, c2p = C.CONFIGS["c4"].scaled((2, 2, 2)), C.CONFIGS["c2"].scaled((4, 4))
+    return c4p, c2p
+
+
+def test_oracle_reproduces_small_fixtures():
+    """Regression pin of the oracle on the small 3-D / 2-D / pulse / Euler cases."""
+    f = np.load(SMALL)
+    c4p, c2p = _small_problems()
+    for name, cfg in (("c4p", c4p), ("c2p", c2p)):
+        pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
+                       list(cfg.velocity), n_tau=cfg.n_tau)
+        R = pr.st_residual(0.0, cfg.dt, f[f"{name}_un"], f[f"{name}_U"])
+        assert np.abs(R - f[f"{name}_R"]).max() <= 1e-14 * np.abs(f[f"{name}_R"]).max()
+    pu = O.Problem(2, 2, [4, 4], [0.0, 0.0], [1.0, 1.0], model=O.ADVDIFF,
+                   field=O.FIELD_ROTATING, eps=0.001, n_tau=3)
+    assert np.abs(pu.rhs(f["pulse_u"]) - f["pulse_F"]).max() <= 1e-13 * np.abs(f["pulse_F"]).max()
+    eu = O.Problem(2, 1, [4, 4], [-10.0, -10.0], [10.0, 10.0], model=O.EULER, n_tau=2)
+    assert np.abs(eu.rhs(f["euler_u"]) - f["euler_F"]).max() <= 1e-13 * np.abs(f["euler_F"]).max()
+
+
+@pytest.mark.gpu
+def test_cuda_matches_small_fixtures():
+    import torch
+    from paper_2201_05800_b200 import _lib as L
+    from paper_2201_05800_b200.api import SlabOperator
+    f = np.load(SMALL)
+    d = lambda a: torch.as_tensor(a, device="cuda")
+    rel = lambda a, b: np.abs(a.cpu().numpy() - b).max() / np.abs(b).max()
+    c4p, c2p = _small_problems()
+    for name, cfg in (("c4p", c4p), ("c2p", c2p)):
+        op = SlabOperator(**cfg.kwargs())
+        assert rel(op.st_residual(0.0, cfg.dt, d(f[f"{name}_un"]), d(f[f"{name}_U"])),
+                   f[f"{name}_R"]) <= 1e-12
+        assert rel(op.st_jvp(0.0, cfg.dt, None, d(f[f"{name}_v"])), f[f"{name}_Jv"]) <= 1e-12
+    pu = SlabOperator(2, 2, 3, (4, 4), (0.0, 0.0), (1.0, 1.0), model=L.STG_MODEL_ADVDIFF,
+                      velocity_field=L.STG_FIELD_ROTATING, eps=0.001)
+    assert rel(pu.spatial_rhs(d(f["pulse_u"])), f["pulse_F"]) <= 1e-12
+    assert rel(pu.st_residual(0.0, 0.02, d(f["pulse_u"]), d(f["pulse_U"])), f["pulse_R"]) <= 1e-12
+    eu = SlabOperator(2, 1, 2, (4, 4), (-10.0, -10.0), (10.0, 10.0), model=L.STG_MODEL_EULER)
+    assert rel(eu.spatial_rhs(d(f["euler_u"])), f["euler_F"]) <= 1e-12
+    assert rel(eu.st_residual(0.0, 0.05, d(f["euler_u"]), d(f["euler_U"])), f["euler_R"]) <= 1e-12
