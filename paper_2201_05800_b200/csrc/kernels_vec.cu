@@ -159,6 +159,9 @@ __global__ void __launch_bounds__(kVecBlock) k_multidot(const double* __restrict
                                                         double* out, unsigned* counter) {
   using O = VecT<W>;
   const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
+  // the last "basis vector" is often w itself (<w,w> in the Arnoldi pass, or
+  // a plain norm): use the loaded x instead of reading w twice
+  const int self = (V + (long long)(kk - 1) * ldv == w) ? kk - 1 : -1;
   double acc[KMAX];
 #pragma unroll
   for (int j = 0; j < KMAX; ++j) acc[j] = 0.0;
@@ -171,7 +174,9 @@ __global__ void __launch_bounds__(kVecBlock) k_multidot(const double* __restrict
         typename O::T v[kGroup];
 #pragma unroll
         for (int q = 0; q < kGroup; ++q)
-          v[q] = (g + q < KMAX && g + q < kk) ? O::ld(V + (g + q) * ldv, i) : O::zero();
+          v[q] = (g + q < KMAX && g + q < kk)
+                     ? (g + q == self ? x : O::ld(V + (g + q) * ldv, i))
+                     : O::zero();
 #pragma unroll
         for (int q = 0; q < kGroup; ++q)
           if (g + q < KMAX) acc[g + q] = O::dot(v[q], x, acc[g + q]);
