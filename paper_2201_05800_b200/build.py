@@ -59,14 +59,18 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     OBJDIR.mkdir(exist_ok=True)
     cc = [nvcc()] + _host_compiler()
-    objs = []
-    for s in SOURCES:
-        o = OBJDIR / (s + ".o")
-        cmd = cc + NVFLAGS + ["-c", str(CSRC / s), "-o", str(o)]
+    objs = [str(OBJDIR / (s + ".o")) for s in SOURCES]
+
+    def compile_one(s: str) -> None:
+        cmd = cc + NVFLAGS + ["-c", str(CSRC / s), "-o", str(OBJDIR / (s + ".o"))]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-        objs.append(str(o))
+
+    # translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+        list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     # cuBLAS: the plain DGEMM of the d = 2 dense element-block preconditioner
     cudalib = Path(nvcc()).resolve().parent.parent / "lib64"

@@ -197,20 +197,26 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
                                                       double sign, int accumulate, double* part,
                                                       const double* __restrict__ scale_src,
                                                       double* scale_out, double* out,
-                                                      unsigned* counter) {
+                                                      unsigned* counter,
+                                                      const double* __restrict__ hn2) {
   using O = VecT<W>;
   const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
   __shared__ double hs[KMAX];
   __shared__ double sc;
-  for (int j = threadIdx.x; j < KMAX; j += kVecBlock) hs[j] = j < k ? sign * h[j] : 0.0;
+  // hn2 (optional) = ||V_j||^2: the basis vectors are stored unnormalised
+  // (exact norms tracked instead of a rescaling pass), so the projection
+  // coefficient of <V_j, w> is <V_j, w> / ||V_j||^2
+  for (int j = threadIdx.x; j < KMAX; j += kVecBlock)
+    hs[j] = j < k ? sign * (hn2 ? h[j] / hn2[j] : h[j]) : 0.0;
   if (threadIdx.x == 0) {
     // scale_src = [h_0..h_{k-1}, <w,w>]: normalise by the Pythagorean norm
-    // sqrt(<w,w> - sum h_j^2) of the projected vector (fallback: ||w||)
+    // sqrt(<w,w> - sum h_j^2 / ||V_j||^2) of the projected vector (fallback: ||w||)
     double s = 1.0;
     if (scale_src) {
       const double ww = scale_src[k];
       double hh = 0.0;
-      for (int j = 0; j < k; ++j) hh = fma(scale_src[j], scale_src[j], hh);
+      for (int j = 0; j < k; ++j)
+        hh = fma(scale_src[j], hn2 ? scale_src[j] / hn2[j] : scale_src[j], hh);
       const double est = ww - hh;
       s = est > 1e-28 * ww ? 1.0 / sqrt(est) : (ww > 0.0 ? 1.0 / sqrt(ww) : 1.0);
       if (scale_out && blockIdx.x == 0) scale_out[0] = s;
@@ -382,12 +388,12 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
-                    const double* scale_src, double* scale_out) {
+                    const double* scale_src, double* scale_out, const double* hn2) {
   const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
   STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
                            w, V, ldv, k, h, n / WW, -1.0, 1, partial, scale_src, scale_out,
-                           out2 + k, c)));
+                           out2 + k, c, hn2)));
   if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s);  // <V_j, w_new>
 }
 
@@ -400,7 +406,7 @@ void vec_combine(double* x, const double* V, long long ldv, int k, const double*
   const int W = vec_width(n, ldv, V, x);
   STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
                            x, V, ldv, k, y, n / WW, 1.0, accumulate ? 1 : 0, nullptr, nullptr,
-                           nullptr, nullptr, nullptr)));
+                           nullptr, nullptr, nullptr, nullptr)));
 }
 
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s) {

@@ -455,7 +455,16 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     st.converged = true;
     return st;
   }
-  std::vector<double> H(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m);
+  std::vector<double> H(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), cn(m + 1, 1.0);
+  // ||V_0||^2 = 1 (V_0 = r / ||r||); the Arnoldi update pass fills dsm[64 + j], j >= 1
+  hp[400] = 1.0;
+  ck(cudaMemcpyAsync(dsm + 64, hp + 400, sizeof(double), cudaMemcpyHostToDevice, s), "memcpy");
+  // re-orthogonalise when ||w - V h||^2 <= reorth_tol ||w||^2 (orthogonality
+  // loss of the single pass ~ eps * sqrt(1 / reorth_tol) = 2e-12 at 1e-8)
+  static const double reorth_tol = [] {
+    const char* e = std::getenv("STG_GMRES_REORTH_TOL");
+    return e ? std::atof(e) : 1e-8;
+  }();
   auto Hat = [&](int i, int j) -> double& { return H[size_t(i) * m + j]; };
   int total = 0;
   bool first = true;
@@ -495,8 +504,8 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       // basis slot; one pass computes h = V^T w and <w,w>; one fused pass
       // projects and normalises with the Pythagorean norm.  A second
       // (classical) Gram-Schmidt pass runs only if that norm shows heavy
-      // cancellation (||w - V h||^2 < 1e-4 ||w||^2, DGKS-style), which keeps
-      // the orthogonality loss per step near 1e-14 at two passes per step.
+      // cancellation (||w - V h||^2 <= reorth_tol ||w||^2, DGKS-style), which
+      // keeps the orthogonality loss per step near 1e-12 at two passes per step.
       double* vn = V + size_t(k + 1) * ld;
       if (P) {
         (*P)(V + size_t(k) * ld, h->zv.p);  // z = P^-1 v_k
@@ -505,35 +514,47 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
         A(V + size_t(k) * ld, vn);
       }
       const int kk = k + 1;  // vectors V_0..V_k
-      stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s);  // [h_0..h_k, <w,w>]
-      stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190);
+      // The stored basis vectors S_j are not exactly unit length: the
+      // Pythagorean scale is an estimate, and instead of a rescaling pass the
+      // update pass measures ||S_{k+1}||^2 exactly (dsm[64 + k + 1]) and the
+      // normalisation is carried as c_j = 1 / ||S_j|| (true basis v_j = c_j S_j).
+      // Raw dots d_j = <S_j, A P^-1 S_k> give H(j,k) = c_k c_j d_j; the update
+      // kernel divides by ||S_j||^2 itself (hn2 = dsm + 64).
+      stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s);  // [d_0..d_k, <w,w>]
+      stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190,
+                          dsm + 64);
       h->launches += 2;
       ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
       ck(cudaStreamSynchronize(s), "sync");
+      const double ckk = cn[size_t(k)];
       const double ww = hp[kk];
       double hh = 0.0;
-      for (int j = 0; j <= k; ++j) hh += hp[j] * hp[j];
-      const double sigma = 1.0 / hp[190];  // norm used to scale the stored vector
-      for (int j = 0; j <= k; ++j) Hat(j, k) = hp[j];
-      double hn = sigma;
+      for (int j = 0; j <= k; ++j) hh += hp[j] * hp[j] / hp[64 + j];
+      const double sc1 = hp[190];  // scale applied to the projected vector
+      for (int j = 0; j <= k; ++j) Hat(j, k) = ckk * cn[size_t(j)] * hp[j];
+      double n2 = hp[64 + kk];     // ||S_{k+1}||^2
+      double hn = ckk * std::sqrt(n2) / sc1;
       static const bool trace = std::getenv("STG_GMRES_TRACE") != nullptr;
       if (trace)  // Arnoldi cancellation / normalisation diagnostics
         std::fprintf(stderr, "arnoldi k=%d cancel=%.3e nv2-1=%.3e\n", k, (ww - hh) / ww,
-                     hp[64 + kk] - 1.0);
-      if (!(ww - hh > 1e-4 * ww) || std::abs(hp[64 + kk] - 1.0) > 1e-10) {
-        // re-orthogonalise the stored (scaled) vector in two passes:
-        // [g2, <vn,vn>] = [V, vn]^T vn (vn is the basis slot after V_k), then
-        // vn = (vn - V g2) / sqrt(<vn,vn> - |g2|^2) (Pythagorean scale)
+                     n2 - 1.0);
+      if (!(ww - hh > reorth_tol * ww) || !(n2 > 0.0)) {
+        // heavy cancellation (the single classical pass leaves an
+        // orthogonality loss ~ eps ||w|| / ||w - V h||): re-orthogonalise the
+        // stored vector in two more passes, [g2, <S,S>] = [V, S]^T S, then
+        // S' = (S - sum g2_j / ||S_j||^2 S_j) * Pythagorean scale
         stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm + 128, s);
         stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s, dsm + 128,
-                            dsm + 191);
+                            dsm + 191, dsm + 64);
         h->launches += 2;
         ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
         ck(cudaStreamSynchronize(s), "sync");
-        for (int j = 0; j <= k; ++j) Hat(j, k) += sigma * hp[128 + j];
-        hn = sigma / hp[191];  // hp[191] = 1 / ||vn - V g2||
+        for (int j = 0; j <= k; ++j) Hat(j, k) += ckk * cn[size_t(j)] * hp[128 + j] / sc1;
+        n2 = hp[64 + kk];
+        hn = ckk * std::sqrt(n2) / (sc1 * hp[191]);
         h->reorth++;
       }
+      cn[size_t(k + 1)] = n2 > 0.0 ? 1.0 / std::sqrt(n2) : 0.0;
       if (!(ww > 0.0)) hn = 0.0;  // exact breakdown: A P^-1 v_k = 0
       Hat(k + 1, k) = hn;
       for (int j = 0; j < k; ++j) {
@@ -563,7 +584,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       for (int j = i + 1; j < k; ++j) acc -= Hat(i, j) * y[j];
       y[i] = acc / Hat(i, i);
     }
-    std::memcpy(hp + 256, y.data(), sizeof(double) * k);
+    for (int j = 0; j < k; ++j) hp[256 + j] = y[size_t(j)] * cn[size_t(j)];  // x += sum y_j c_j S_j
     ck(cudaMemcpyAsync(dsm + 256, hp + 256, sizeof(double) * k, cudaMemcpyHostToDevice, s),
        "memcpy");
     if (P) {

@@ -1,6 +1,7 @@
 """Kernel busy time vs wall time of one warm slab solve (torch profiler /
 CUPTI timestamps): how much of the solve is GPU idle between launches."""
 import json
+import re
 import sys
 import time
 from pathlib import Path
@@ -31,8 +32,10 @@ busy = sum(e.device_time_total for e in kern) / 1e3  # us -> ms
 span = (max(e.time_range.end for e in kern) - min(e.time_range.start for e in kern)) / 1e3
 by = {}
 for e in kern:
-    k = e.name.split("(")[0].split("<")[0][-40:]
+    k = re.sub(r"^void |\(anonymous namespace\)::|stg::", "", e.name).split("(")[0][:48]
     by[k] = by.get(k, 0.0) + e.device_time_total / 1e3
 print(json.dumps({"config": name, "wall_ms": 1e3 * wall, "kernel_busy_ms": busy,
                   "first_to_last_kernel_ms": span, "launches": len(kern),
-                  "top": dict(sorted(by.items(), key=lambda x: -x[1])[:8])}))
+                  "top": dict(sorted(by.items(), key=lambda x: -x[1])[:12]),
+                  "counts": {k: sum(1 for e in kern if re.sub(r"^void |\(anonymous namespace\)::|stg::", "", e.name).split("(")[0][:48] == k)
+                             for k in by}}))
