@@ -61,6 +61,50 @@ struct Geometry {
 
 enum class Model : int { advection = 0, burgers = 1 };
 
+// Device-side cancellation of queued work.  The GMRES driver enqueues the
+// next Arnoldi step before it has read the outcome of the current one; every
+// kernel of a step carries a Skip and returns at entry unless *flag == run
+// (flag null: always run).  The flag is written by an earlier kernel on the
+// same stream, so stream order makes it visible.
+struct Skip {
+  const int* flag = nullptr;
+  int run = 0;
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ bool skip_now(const Skip& s) {
+  return s.flag != nullptr && *reinterpret_cast<const volatile int*>(s.flag) != s.run;
+}
+#endif
+
+// Device state of one GMRES(m) cycle (stg.cpp, gmres): the Hessenberg matrix
+// reduced by Givens rotations, the rotations, the rotated right-hand side g,
+// the inverse norms c_j = 1/||S_j|| of the stored basis vectors, and the
+// cycle status: 0 running, 1 residual estimate <= tol_abs, 2 breakdown,
+// 3 the last step needs a second Gram-Schmidt pass.
+constexpr int kGmresMaxRestart = 60;
+struct GmresDev {
+  double H[(kGmresMaxRestart + 1) * kGmresMaxRestart];  // H(i,j) at i*m + j
+  double cs[kGmresMaxRestart], sn[kGmresMaxRestart];
+  double g[kGmresMaxRestart + 1];
+  double cn[kGmresMaxRestart + 1];
+  double tol_abs, reorth_tol, est;
+  int m, status, k_done, pad;
+};
+// The Givens step of Arnoldi step k, run by the last block of the update
+// pass: pass 0 after the first projection (raw dots d1 = <S_j, w>, j <= k,
+// and d1[k+1] = <w,w>), pass 1 after a re-orthogonalisation (raw dots d2).
+// The step's status is mirrored to host-mapped memory (host[k]).
+struct GivensArgs {
+  GmresDev* G = nullptr;
+  int k = 0;
+  int pass = 0;
+  const double* d1 = nullptr;
+  const double* sc1 = nullptr;  // scale applied by pass 0 (pass 1 reads it)
+  int* host = nullptr;          // mapped pinned per-step status slots
+};
+void gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol, double* hn2_0,
+                cudaStream_t s);
+
 struct SlabArgs {
   SpatialCoef sp;
   MixCoef mx;
@@ -86,6 +130,7 @@ struct SlabArgs {
   const double* fdv;
   const double* fd_vv;
   double fd_c;
+  Skip skip;
 };
 // true if the d = 1 lane kernel handles fused FD Jacobian actions for a
 bool fd_fused_supported(const SlabArgs& a);
@@ -168,15 +213,15 @@ struct FdmCoef {
 };
 bool fdm_supported(const Geometry& g, int n_tau);
 int launch_precond_fdm(const FdmCoef& c, const Geometry& g, const double* in, double* out,
-                       cudaStream_t s);
+                       cudaStream_t s, Skip skip = {});
 
 // ---- block-Jacobi preconditioners (kernels_precond.cu) ----------------------
 // out[t][cell][k] = sum_j minv[k][t][j] in[j][cell][k]   (npc class tables)
 void precond_tblock(double* out, const double* in, const double* minv, int nt, int npc,
-                    long long ns, cudaStream_t s);
+                    long long ns, cudaStream_t s, Skip skip = {});
 // out_e = B_e in_e, B_e = B + e * bstride (bstride 0: one shared block), d = 1
 void precond_eblock(double* out, const double* in, const double* B, long long bstride, int nt,
-                    int n1, int ncells, long long ns, cudaStream_t s);
+                    int n1, int ncells, long long ns, cudaStream_t s, Skip skip = {});
 // d = 2: out_e = B in_e with ONE shared dense block B ((n_tau*npc)^2, <= 128^2)
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
                           int ncells, long long ns, cudaStream_t s);
@@ -190,16 +235,17 @@ void probe_extract(double* K, const double* F, int ndl, int col, int nx, int sx,
 bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt, int ndl,
                        int ncells, cudaStream_t s);
 // stage-major [t][cell][node] <-> element-major [cell][t][node] (n = nt * ns)
-void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s);
+void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s,
+                     Skip skip = {});
 void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
-                       cudaStream_t s);
+                       cudaStream_t s, Skip skip = {});
 // per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U,
 // stored in fp32 (a preconditioner; applied in fp64 arithmetic)
 bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s);
 // out_e = B_e in_e with per-element fp32 blocks, nt*n1 <= 16 and even
 bool eblock_f32_supported(int nt, int n1);
 void precond_eblock_f32(double* out, const double* in, const float* B, int nt, int n1,
-                        int ncells, long long ns, cudaStream_t s);
+                        int ncells, long long ns, cudaStream_t s, Skip skip = {});
 
 // ---- vector kernels (kernels_vec.cu) ----------------------------------------
 // All reductions are deterministic: fixed grid for a given n, fixed-order
@@ -218,7 +264,7 @@ void vec_axpby(double* y, double a, const double* x, double b, long long n, cuda
 void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t s);
 // out[j] = <V_j, w>, j < k <= 64 (V_j = V + j*ldv); partial buffer >= grid*k doubles
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
-                  double* partial, double* out, cudaStream_t s);
+                  double* partial, double* out, cudaStream_t s, Skip skip = {});
 // w = (w - sum_{j<k} h[j] V_j) * s (h on device), then out2[k] = <w,w> and,
 // if want_dots, out2[j] = <V_j, w> (an extra pass); partial buffer >= grid*(k+1).  s = 1 unless
 // scale_src = [h_0..h_{k-1}, <w,w>] is given: then s = 1/sqrt(<w,w> - sum h^2)
@@ -228,7 +274,7 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
                     const double* scale_src = nullptr, double* scale_out = nullptr,
-                    const double* hn2 = nullptr);
+                    const double* hn2 = nullptr, Skip skip = {}, GivensArgs gv = {});
 // y = x / sqrt(*nrm2)  (nrm2 on device)
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
                        cudaStream_t s);
@@ -239,6 +285,6 @@ void vec_combine(double* x, const double* V, long long ldv, int k, const double*
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s);
 // *out = <x,y>
 void vec_dot(const double* x, const double* y, long long n, double* partial, double* out,
-             cudaStream_t s);
+             cudaStream_t s, Skip skip = {});
 
 }  // namespace stg

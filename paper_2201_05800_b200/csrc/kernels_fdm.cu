@@ -103,7 +103,8 @@ __device__ __forceinline__ void phase_b_cols(const FdmCoef& c, double* B1, const
 template <int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ FdmCoef c,
-               const Geometry g, double* __restrict__ out) {
+               const Geometry g, double* __restrict__ out, const Skip skip) {
+  if (skip_now(skip)) return;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (ptxh::smem_u32(smem_raw) & 1023u)) & 1023u);
   double* B1 = reinterpret_cast<double*>(base + OFF_B1);
@@ -291,7 +292,7 @@ bool fdm_supported(const Geometry& g, int n_tau) {
 }
 
 int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in, double* out,
-                       cudaStream_t s) {
+                       cudaStream_t s, Skip skip) {
   EncodeFn enc = encode_fn();
   if (!enc || (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return -1;
@@ -323,7 +324,7 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
   const int nseg = g.n_cells / E;
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
-  kern<<<grid, THREADS, SMEM, s>>>(map, coef, g, out);
+  kern<<<grid, THREADS, SMEM, s>>>(map, coef, g, out, skip);
   return 1;
 }
 

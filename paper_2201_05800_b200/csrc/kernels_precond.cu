@@ -26,7 +26,8 @@ template <int NT>
 __global__ void __launch_bounds__(kPB) k_tblock(double* __restrict__ out,
                                                 const double* __restrict__ in,
                                                 const double* __restrict__ minv, int npc,
-                                                int ncells, long long ns) {
+                                                int ncells, long long ns, Skip skip) {
+  if (skip_now(skip)) return;
   // smem layout [t][j][k]: consecutive nodes (threads) read consecutive words
   // (the global table is [k][t][j]; a [k]-major smem copy would be a 32-way
   // bank conflict for npc = 64)
@@ -58,7 +59,9 @@ template <int NB>
 __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
                                                 const double* __restrict__ in,
                                                 const double* __restrict__ B, long long bstride,
-                                                int nt, int n1, int ncells, long long ns) {
+                                                int nt, int n1, int ncells, long long ns,
+                                                Skip skip) {
+  if (skip_now(skip)) return;
   __shared__ double xs[8][NB];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nb = nt * n1;
@@ -192,7 +195,8 @@ template <int NB>
 __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
                                                  const double* __restrict__ in,
                                                  const float* __restrict__ B, int n1,
-                                                 int ncells, long long ns) {
+                                                 int ncells, long long ns, Skip skip) {
+  if (skip_now(skip)) return;
   static_assert(NB <= 16 && NB % 2 == 0, "two elements per warp");
   const int lane = threadIdx.x & 31, h = lane >> 4, r = lane & 15;
   const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -227,24 +231,24 @@ int pgrid(long long n) {
 }  // namespace
 
 void precond_tblock(double* out, const double* in, const double* minv, int nt, int npc,
-                    long long ns, cudaStream_t s) {
+                    long long ns, cudaStream_t s, Skip skip) {
   const int ncells = int(ns / npc);  // ns < 2^31 for every supported mesh (validate_desc)
   const size_t smem = size_t(npc) * nt * nt * sizeof(double);
   const int g = pgrid(ns);
   switch (nt) {
-    case 2: k_tblock<2><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns); break;
-    case 3: k_tblock<3><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns); break;
-    case 4: k_tblock<4><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns); break;
-    case 5: k_tblock<5><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns); break;
-    default: k_tblock<6><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns); break;
+    case 2: k_tblock<2><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
+    case 3: k_tblock<3><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
+    case 4: k_tblock<4><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
+    case 5: k_tblock<5><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
+    default: k_tblock<6><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
   }
 }
 
 void precond_eblock(double* out, const double* in, const double* B, long long bstride, int nt,
-                    int n1, int ncells, long long ns, cudaStream_t s) {
+                    int n1, int ncells, long long ns, cudaStream_t s, Skip skip) {
   int g = (ncells + 7) / 8;
   if (g > 148 * 16) g = 148 * 16;
-  k_eblock<kMaxT * kMaxN><<<g, 256, 0, s>>>(out, in, B, bstride, nt, n1, ncells, ns);
+  k_eblock<kMaxT * kMaxN><<<g, 256, 0, s>>>(out, in, B, bstride, nt, n1, ncells, ns, skip);
 }
 
 // ---- d = 2 element-block Jacobi with one shared dense block ----------------
@@ -461,7 +465,8 @@ bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
 
 // stage-major [t][cell][node] <-> element-major [cell][t][node]
 __global__ void k_to_elem(double* __restrict__ Xp, const double* __restrict__ X, int nt, int npc,
-                          long long n, long long ns) {
+                          long long n, long long ns, Skip skip) {
+  if (skip_now(skip)) return;
   const long long nb = (long long)nt * npc;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -471,7 +476,8 @@ __global__ void k_to_elem(double* __restrict__ Xp, const double* __restrict__ X,
   }
 }
 __global__ void k_from_elem(double* __restrict__ Y, const double* __restrict__ Yp, int nt,
-                            int npc, long long n, long long ns) {
+                            int npc, long long n, long long ns, Skip skip) {
+  if (skip_now(skip)) return;
   const long long nb = (long long)nt * npc;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
@@ -481,14 +487,15 @@ __global__ void k_from_elem(double* __restrict__ Y, const double* __restrict__ Y
   }
 }
 
-void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s) {
+void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s,
+                     Skip skip) {
   const long long n = ns * nt;
-  k_to_elem<<<pgrid(n), kPB, 0, s>>>(Xp, X, nt, npc, n, ns);
+  k_to_elem<<<pgrid(n), kPB, 0, s>>>(Xp, X, nt, npc, n, ns, skip);
 }
 void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
-                       cudaStream_t s) {
+                       cudaStream_t s, Skip skip) {
   const long long n = ns * nt;
-  k_from_elem<<<pgrid(n), kPB, 0, s>>>(Y, Yp, nt, npc, n, ns);
+  k_from_elem<<<pgrid(n), kPB, 0, s>>>(Y, Yp, nt, npc, n, ns, skip);
 }
 
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
@@ -528,18 +535,18 @@ bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt,
 }
 
 void precond_eblock_f32(double* out, const double* in, const float* B, int nt, int n1,
-                        int ncells, long long ns, cudaStream_t s) {
+                        int ncells, long long ns, cudaStream_t s, Skip skip) {
   const int nb = nt * n1;
   long long g = ((ncells + 1) / 2 + 7) / 8;  // 8 warps per block, 2 elements per warp
   if (g > 148 * 16) g = 148 * 16;
   switch (nb) {
-    case 4: k_eblock2<4><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-    case 6: k_eblock2<6><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-    case 8: k_eblock2<8><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-    case 10: k_eblock2<10><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-    case 12: k_eblock2<12><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-    case 14: k_eblock2<14><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
-    case 16: k_eblock2<16><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns); return;
+    case 4: k_eblock2<4><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 6: k_eblock2<6><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 8: k_eblock2<8><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 10: k_eblock2<10><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 12: k_eblock2<12><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 14: k_eblock2<14><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 16: k_eblock2<16><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
     default: break;
   }
 }

@@ -111,6 +111,7 @@ __device__ __forceinline__ void burgers_jvp_line(const SpatialCoef& sp, const do
 // ---------------------------------------------------------------------------
 template <int N1>
 __global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int K = a.g.nx;
   if (c >= K) return;
@@ -173,6 +174,7 @@ __global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
 // ---------------------------------------------------------------------------
 template <int N1, int NT>
 __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   constexpr int EPW = 32 / NT;  // elements per warp
   const int lane = threadIdx.x & 31;
   const int e = lane / NT, j = lane - (lane / NT) * NT;
@@ -261,6 +263,7 @@ struct GenericShape {
 template <int D, int N1>
 __global__ void __launch_bounds__(GenericShape<D, N1>::THREADS)
     slab_generic_kernel(const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   using Sh = GenericShape<D, N1>;
   constexpr int NPC = Sh::NPC;
   constexpr int E = Sh::E;
@@ -364,6 +367,7 @@ struct Shape2d {
 template <int N1, int NT>
 __global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
     slab2d_kernel(const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   using Sh = Shape2d<N1, NT>;
   constexpr int NPC = Sh::NPC, E = Sh::E;
   __shared__ double Xs[NT][E][NPC];
@@ -528,6 +532,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 template <int N1, int NT>
 __global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
     slab2d_persist(const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   using P = P2d<N1, NT>;
   using Sh = typename P::Sh;
   constexpr int NPC = P::NPC, E = P::E, PL = P::PLANE;
@@ -710,6 +715,7 @@ __device__ __forceinline__ void bulk_wait0() {
 template <int N1, int NT, int E, int MINB>
 __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
     slab2d_plane(const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   using P = Plane2d<N1, NT, E>;
   constexpr int NPC = P::NPC, PL = P::PLANE;
   extern __shared__ __align__(16) double sm2[];
@@ -910,6 +916,7 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 template <bool FULL_S>
 __global__ void __launch_bounds__(fast::THREADS, 4)
     slab3d_n4_tma(const __grid_constant__ CUtensorMap tmX, const SlabArgs a) {
+  if (skip_now(a.skip)) return;
   using namespace fast;
   extern __shared__ unsigned char smem_raw[];
   // align to 1024 B (128B-swizzle atoms) by integer offset so the pointer
@@ -1197,6 +1204,7 @@ template <bool FULL_S>
 __global__ void __launch_bounds__(pst::THREADS, 3)
     slab3d_n4_persist(const __grid_constant__ pst::Maps maps, const SlabArgs a,
                       const pst::Layout lay) {
+  if (skip_now(a.skip)) return;
   using namespace pst;
   using fast::row_of;
   using fast::swz;

@@ -129,7 +129,7 @@ struct VecT<2> {
 // Block-reduce acc[0..cnt) (cnt <= KMAX + 1) into part[blockIdx.x*cnt + j];
 // the last block sums the partials into out[0..cnt).
 template <int NACC>
-__device__ __forceinline__ void reduce_out(const double (&acc)[NACC], int cnt, double* part,
+__device__ __forceinline__ bool reduce_out(const double (&acc)[NACC], int cnt, double* part,
                                            double* out, unsigned* counter) {
   __shared__ double red[kVecBlock / 32][NACC];
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
@@ -147,7 +147,68 @@ __device__ __forceinline__ void reduce_out(const double (&acc)[NACC], int cnt, d
     for (int q = 0; q < kVecBlock / 32; ++q) s += red[q][j];
     part[(size_t)blockIdx.x * cnt + j] = s;
   }
-  if (is_last_block(counter)) block_finish_sum(part, gridDim.x, cnt, out, counter);
+  if (!is_last_block(counter)) return false;
+  block_finish_sum(part, gridDim.x, cnt, out, counter);
+  return true;
+}
+
+// Arnoldi step k's Givens update (thread 0 of the update pass's last block;
+// n2 = ||S_{k+1}||^2 just reduced, sc = the scale this pass applied).  The
+// same arithmetic as the host loop it replaces: H(j,k) = c_k c_j d_j with
+// c_j = 1/||S_j||, h_{k+1,k} = c_k ||S_{k+1}|| / scale, then the previous
+// rotations, a new rotation, and the residual estimate |g_{k+1}|.
+__device__ __noinline__ void gmres_givens(const GivensArgs& a, const double* d, double sc,
+                                          const double* hn2, double n2) {
+  GmresDev* G = a.G;
+  const int m = G->m, k = a.k, kk = k + 1;
+  const double* d1 = a.d1;
+  const double ckk = G->cn[k];
+  double* Hc = G->H;  // column k: Hc[i * m + k]
+  double hn;
+  if (a.pass == 0) {
+    const double ww = d1[kk];
+    double hh = 0.0;
+    for (int j = 0; j <= k; ++j) hh += d1[j] * d1[j] / hn2[j];
+    if (!(ww - hh > G->reorth_tol * ww) || !(n2 > 0.0)) {
+      // heavy cancellation: the host enqueues a second pass for this step
+      G->status = 3;
+      reinterpret_cast<volatile int*>(a.host)[k] = 3;
+      __threadfence_system();
+      return;
+    }
+    for (int j = 0; j <= k; ++j) Hc[j * m + k] = ckk * G->cn[j] * d1[j];
+    hn = ckk * sqrt(n2) / sc;
+    if (!(ww > 0.0)) hn = 0.0;  // exact breakdown: A P^-1 v_k = 0
+  } else {
+    const double sc1 = *a.sc1;
+    for (int j = 0; j <= k; ++j) Hc[j * m + k] = ckk * G->cn[j] * (d1[j] + d[j] / sc1);
+    hn = ckk * sqrt(n2) / (sc1 * sc);
+    if (!(d1[kk] > 0.0)) hn = 0.0;
+  }
+  G->cn[kk] = n2 > 0.0 ? 1.0 / sqrt(n2) : 0.0;
+  for (int j = 0; j < k; ++j) {
+    const double a0 = Hc[j * m + k], a1 = Hc[(j + 1) * m + k];
+    Hc[j * m + k] = G->cs[j] * a0 + G->sn[j] * a1;
+    Hc[(j + 1) * m + k] = -G->sn[j] * a0 + G->cs[j] * a1;
+  }
+  const double hk = Hc[k * m + k];
+  const double den = hypot(hk, hn);
+  const double c = den == 0.0 ? 1.0 : hk / den;
+  const double sn = den == 0.0 ? 0.0 : hn / den;
+  G->cs[k] = c;
+  G->sn[k] = sn;
+  Hc[k * m + k] = den;
+  Hc[kk * m + k] = 0.0;
+  const double gk = G->g[k];
+  G->g[kk] = -sn * gk;
+  G->g[k] = c * gk;
+  const double est = fabs(G->g[kk]);
+  G->est = est;
+  G->k_done = kk;
+  const int st = est <= G->tol_abs ? 1 : ((hn == 0.0 || !isfinite(hn)) ? 2 : 0);
+  G->status = st;
+  reinterpret_cast<volatile int*>(a.host)[k] = st;
+  __threadfence_system();
 }
 
 // out[j] = <V_j, w>, j < k <= KMAX
@@ -156,7 +217,9 @@ __global__ void __launch_bounds__(kVecBlock) k_multidot(const double* __restrict
                                                         long long ldv, int k,
                                                         const double* __restrict__ w,
                                                         long long nw, double* part,
-                                                        double* out, unsigned* counter) {
+                                                        double* out, unsigned* counter,
+                                                        Skip skip) {
+  if (skip_now(skip)) return;
   using O = VecT<W>;
   const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
   // the last "basis vector" is often w itself (<w,w> in the Arnoldi pass, or
@@ -198,7 +261,9 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
                                                       const double* __restrict__ scale_src,
                                                       double* scale_out, double* out,
                                                       unsigned* counter,
-                                                      const double* __restrict__ hn2) {
+                                                      const double* __restrict__ hn2, Skip skip,
+                                                      GivensArgs gv) {
+  if (skip_now(skip)) return;
   using O = VecT<W>;
   const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
   __shared__ double hs[KMAX];
@@ -249,7 +314,22 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
     acc[0] = O::dot(x, x, acc[0]);
   }
   if (part == nullptr) return;
-  reduce_out(acc, 1, part, out, counter);
+  if (reduce_out(acc, 1, part, out, counter) && gv.G && threadIdx.x == 0)
+    gmres_givens(gv, scale_src, s, hn2, out[0]);
+}
+
+__global__ void k_gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol,
+                             double* hn2_0) {
+  G->m = m;
+  G->status = 0;
+  G->k_done = 0;
+  G->est = beta;
+  G->tol_abs = tol_abs;
+  G->reorth_tol = reorth_tol;
+  G->g[0] = beta;
+  for (int j = 1; j <= m; ++j) G->g[j] = 0.0;
+  G->cn[0] = 1.0;
+  if (hn2_0) *hn2_0 = 1.0;  // ||S_0||^2 = 1 (S_0 = r / ||r||)
 }
 
 __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x, long long n,
@@ -379,22 +459,29 @@ int vec_width(long long n, long long ldv, const void* a, const void* b) {
 }  // namespace
 
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
-                  double* partial, double* out, cudaStream_t s) {
+                  double* partial, double* out, cudaStream_t s, Skip skip) {
   const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
   STG_DISPATCH_K(k, W, (k_multidot<KM, WW><<<multi_grid<KM, WW, false>(n), kVecBlock,
-                                              0, s>>>(V, ldv, k, w, n / WW, partial, out, c)));
+                                              0, s>>>(V, ldv, k, w, n / WW, partial, out, c,
+                                                      skip)));
+}
+
+void gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol, double* hn2_0,
+                cudaStream_t s) {
+  k_gmres_init<<<1, 1, 0, s>>>(G, m, beta, tol_abs, reorth_tol, hn2_0);
 }
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
-                    const double* scale_src, double* scale_out, const double* hn2) {
+                    const double* scale_src, double* scale_out, const double* hn2, Skip skip,
+                    GivensArgs gv) {
   const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
   STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
                            w, V, ldv, k, h, n / WW, -1.0, 1, partial, scale_src, scale_out,
-                           out2 + k, c, hn2)));
-  if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s);  // <V_j, w_new>
+                           out2 + k, c, hn2, skip, gv)));
+  if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s, skip);  // <V_j, w_new>
 }
 
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
@@ -406,7 +493,7 @@ void vec_combine(double* x, const double* V, long long ldv, int k, const double*
   const int W = vec_width(n, ldv, V, x);
   STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
                            x, V, ldv, k, y, n / WW, 1.0, accumulate ? 1 : 0, nullptr, nullptr,
-                           nullptr, nullptr, nullptr, nullptr)));
+                           nullptr, nullptr, nullptr, nullptr, Skip{}, GivensArgs{})));
 }
 
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s) {
@@ -415,8 +502,8 @@ void vec_maxabs(const double* x, long long n, double* partial, double* out, cuda
 }
 
 void vec_dot(const double* x, const double* y, long long n, double* partial, double* out,
-             cudaStream_t s) {
-  vec_multidot(x, 0, 1, y, n, partial, out, s);
+             cudaStream_t s, Skip skip) {
+  vec_multidot(x, 0, 1, y, n, partial, out, s, skip);
 }
 
 }  // namespace stg

@@ -121,6 +121,15 @@ struct stg_handle {
   bool fdm_valid = false;
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
+  // GMRES cycle state on the device, its pinned host copy, the host-mapped
+  // [status, k_done] word pair the Givens step publishes, and the skip flag
+  // the operator / preconditioner launchers attach to their kernels while an
+  // Arnoldi step is being enqueued speculatively
+  DevBuf gstate;
+  stg::GmresDev* gpin = nullptr;
+  int* mapped = nullptr;
+  cudaEvent_t ev_step[2] = {}, ev_re = nullptr;
+  stg::Skip skip{};
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
   static constexpr int kChunks = 8;
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -129,6 +138,11 @@ struct stg_handle {
   ~stg_handle() {
     if (cublas) cublasDestroy(cublas);
     if (pinned) cudaFreeHost(pinned);
+    if (gpin) cudaFreeHost(gpin);
+    if (mapped) cudaFreeHost(mapped);
+    for (cudaEvent_t e : ev_step)
+      if (e) cudaEventDestroy(e);
+    if (ev_re) cudaEventDestroy(ev_re);
     if (s_in) cudaStreamDestroy(s_in);
     if (s_out) cudaStreamDestroy(s_out);
     if (ev_start) cudaEventDestroy(ev_start);
@@ -204,6 +218,7 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   a.U = U;
   a.W = W;
   a.R = R;
+  a.skip = h->skip;
   if (general_model(h->desc.model)) {
     apply_general(h, mx, n_in, n_out, X, W, R);
     return;
@@ -412,6 +427,14 @@ double dev_dot(stg_handle* h, const double* x, const double* y, long long n) {
   return h->pinned[0];
 }
 
+// attaches a skip flag to every kernel the operator / preconditioner
+// launchers enqueue while in scope
+struct SkipScope {
+  stg_handle* h;
+  SkipScope(stg_handle* hh, stg::Skip s) : h(hh) { h->skip = s; }
+  ~SkipScope() { h->skip = stg::Skip{}; }
+};
+
 struct GmresStats {
   int iterations = 0;
   double rel_residual = 0.0;
@@ -421,16 +444,26 @@ struct GmresStats {
 // Restarted GMRES(m), right-preconditioned (A P^-1 y = b, x = P^-1 y; P null:
 // unpreconditioned), classical Gram-Schmidt in two fused passes per Arnoldi
 // step (multidot incl. <w,w>; project + Pythagorean normalise) with a second
-// pass only on heavy cancellation (DGKS-style), Givens rotations on the host.
-// Stopping test ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at
-// newton.hpp:68-77) on the Arnoldi residual estimate, which with right
-// preconditioning is the unpreconditioned residual; the true residual is
-// recomputed at each restart.  x holds the initial guess (x_zero: known 0).
+// pass only on heavy cancellation (DGKS-style).  Stopping test
+// ||b - A x||_2 <= tol ||b||_2 (Eigen's criterion at newton.hpp:68-77) on the
+// Arnoldi residual estimate, which with right preconditioning is the
+// unpreconditioned residual; the true residual is recomputed at each restart.
+// x holds the initial guess (x_zero: known 0).
+//
+// The Hessenberg column, the Givens rotations and the stopping test of each
+// step run on the device (the last block of the update pass, kernels_vec.cu
+// gmres_givens), so the host never waits inside a step: it enqueues step k+1
+// before reading step k's outcome (lag 1).  Every kernel of a step carries a
+// skip flag (the cycle status), so the speculative step is a string of empty
+// launches once step k has converged or broken down, or needs a second
+// Gram-Schmidt pass -- which the host then enqueues before re-enqueueing step
+// k+1.  lag 0 (pipelined = false, or STG_GMRES_SYNC=1) waits after every step.
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
-                 double tol, int max_it, const Op* P = nullptr, bool x_zero = false) {
+                 double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
+                 bool pipelined = true) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
-  if (m > 60) throw std::invalid_argument("gmres: restart <= 60");
+  if (m > stg::kGmresMaxRestart) throw std::invalid_argument("gmres: restart <= 60");
   GmresStats st;
   const long long ld = round_up(n, 32);
   h->basis.ensure(size_t(ld) * (m + 1));
@@ -439,11 +472,34 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     h->zv.ensure(size_t(n));
     h->zc.ensure(size_t(n));
   }
+  if (!h->gpin) {
+    h->gstate.ensure((sizeof(stg::GmresDev) + 7) / 8);
+    ck(cudaMallocHost(&h->gpin, sizeof(stg::GmresDev)), "cudaMallocHost");
+    ck(cudaHostAlloc(&h->mapped, (stg::kGmresMaxRestart + 2) * sizeof(int), cudaHostAllocMapped),
+       "cudaHostAlloc");
+    for (cudaEvent_t& e : h->ev_step)
+      ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    ck(cudaEventCreateWithFlags(&h->ev_re, cudaEventDisableTiming), "event");
+  }
+  stg::GmresDev* G = reinterpret_cast<stg::GmresDev*>(h->gstate.p);
+  int* mapped_dev = nullptr;
+  ck(cudaHostGetDevicePointer(reinterpret_cast<void**>(&mapped_dev), h->mapped, 0),
+     "cudaHostGetDevicePointer");
+  volatile int* mapped = h->mapped;
   double* V = h->basis.p;
   double* w = h->wv.p;
-  double* dsm = h->small.p;  // [0..m+1] h1, [64..] h2/norm, [128..] h3/norm, [256..] y
+  double* dsm = h->small.p;  // [0..m+1] raw dots, [64..] ||S_j||^2, [128..] 2nd-pass dots,
+                             // [190] / [191] pass scales, [200] <b,b> / <r,r>, [256..] y
   double* hp = h->pinned;
   cudaStream_t s = h->stream;
+  static const bool force_sync = std::getenv("STG_GMRES_SYNC") != nullptr;
+  const int lag = (pipelined && !force_sync) ? 1 : 0;
+  // re-orthogonalise when ||w - V h||^2 <= reorth_tol ||w||^2 (orthogonality
+  // loss of the single pass ~ eps * sqrt(1 / reorth_tol) = 2e-12 at 1e-8)
+  static const double reorth_tol = [] {
+    const char* e = std::getenv("STG_GMRES_REORTH_TOL");
+    return e ? std::atof(e) : 1e-8;
+  }();
 
   const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[0]
   const double bnorm = std::sqrt(bb);
@@ -455,24 +511,60 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     st.converged = true;
     return st;
   }
-  std::vector<double> H(size_t(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), y(m), cn(m + 1, 1.0);
-  // ||V_0||^2 = 1 (V_0 = r / ||r||); the Arnoldi update pass fills dsm[64 + j], j >= 1
-  hp[400] = 1.0;
-  ck(cudaMemcpyAsync(dsm + 64, hp + 400, sizeof(double), cudaMemcpyHostToDevice, s), "memcpy");
-  // re-orthogonalise when ||w - V h||^2 <= reorth_tol ||w||^2 (orthogonality
-  // loss of the single pass ~ eps * sqrt(1 / reorth_tol) = 2e-12 at 1e-8)
-  static const double reorth_tol = [] {
-    const char* e = std::getenv("STG_GMRES_REORTH_TOL");
-    return e ? std::atof(e) : 1e-8;
-  }();
-  auto Hat = [&](int i, int j) -> double& { return H[size_t(i) * m + j]; };
+  const stg::Skip run0{&G->status, 0}, run_re{&G->status, 3};
+  // Arnoldi step k: S_{k+1} <- A P^-1 S_k, then the two fused passes; the
+  // update pass's last block runs the Givens step and publishes the status
+  auto enqueue_step = [&](int k) {
+    double* vn = V + size_t(k + 1) * ld;
+    {
+      SkipScope scope(h, run0);
+      if (P) {
+        (*P)(V + size_t(k) * ld, h->zv.p);  // z = P^-1 S_k
+        A(h->zv.p, vn);
+      } else {
+        A(V + size_t(k) * ld, vn);
+      }
+    }
+    const int kk = k + 1;  // vectors S_0..S_k
+    stg::GivensArgs gv;
+    gv.G = G;
+    gv.k = k;
+    gv.pass = 0;
+    gv.d1 = dsm;
+    gv.host = mapped_dev;
+    stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s, run0);  // [d_0..d_k, <w,w>]
+    stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190,
+                        dsm + 64, run0, gv);
+    h->launches += 2;
+    ck(cudaEventRecord(h->ev_step[k & 1], s), "event");
+  };
+  // second classical pass on S_{k+1}: [g2, <S,S>] = [V, S]^T S, then
+  // S' = (S - sum g2_j / ||S_j||^2 S_j) * Pythagorean scale; runs only while
+  // the status says "re-orthogonalise" (3)
+  auto enqueue_reorth = [&](int k) {
+    double* vn = V + size_t(k + 1) * ld;
+    const int kk = k + 1;
+    stg::GivensArgs gv;
+    gv.G = G;
+    gv.k = k;
+    gv.pass = 1;
+    gv.d1 = dsm;
+    gv.sc1 = dsm + 190;
+    gv.host = mapped_dev;
+    stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm + 128, s, run_re);
+    stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s, dsm + 128,
+                        dsm + 191, dsm + 64, run_re, gv);
+    h->launches += 2;
+    ck(cudaEventRecord(h->ev_re, s), "event");
+  };
+
+  std::vector<double> y(static_cast<size_t>(m), 0.0);
   int total = 0;
   bool first = true;
   while (true) {
     double beta;
-    double est_rel = -1.0;  // >= 0: the Givens residual estimate met tol
     if (first && x_zero) {  // x = 0: r = b and ||r|| = ||b|| (no operator apply, no sync)
-      stg::vec_scale_invsqrt(V, b, dsm + 200, n, s);  // V_0 = b / ||b|| (dsm[200] = <b,b>)
+      stg::vec_scale_invsqrt(V, b, dsm + 200, n, s);  // S_0 = b / ||b|| (dsm[200] = <b,b>)
       h->launches++;
       beta = bnorm;
     } else {
@@ -483,7 +575,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       h->launches += 1;
       ck(cudaMemcpyAsync(hp + 200, dsm + 200, sizeof(double), cudaMemcpyDeviceToHost, s),
          "memcpy");
-      stg::vec_scale_invsqrt(V, w, dsm + 200, n, s);  // V_0 = r / ||r||
+      stg::vec_scale_invsqrt(V, w, dsm + 200, n, s);  // S_0 = r / ||r||
       h->launches++;
       ck(cudaStreamSynchronize(s), "sync");
       beta = std::sqrt(hp[200]);
@@ -495,96 +587,42 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       break;
     }
     if (total >= max_it) break;
-    std::fill(g.begin(), g.end(), 0.0);
-    g[0] = beta;
-    int k = 0;
-    for (; k < m && total < max_it; ++k) {
-      ++total;
-      // Arnoldi step: the operator writes A P^-1 v_k straight into the next
-      // basis slot; one pass computes h = V^T w and <w,w>; one fused pass
-      // projects and normalises with the Pythagorean norm.  A second
-      // (classical) Gram-Schmidt pass runs only if that norm shows heavy
-      // cancellation (||w - V h||^2 <= reorth_tol ||w||^2, DGKS-style), which
-      // keeps the orthogonality loss per step near 1e-12 at two passes per step.
-      double* vn = V + size_t(k + 1) * ld;
-      if (P) {
-        (*P)(V + size_t(k) * ld, h->zv.p);  // z = P^-1 v_k
-        A(h->zv.p, vn);
-      } else {
-        A(V + size_t(k) * ld, vn);
+    stg::gmres_init(G, m, beta, tol * bnorm, reorth_tol, dsm + 64, s);
+    h->launches++;
+    for (int j = 0; j <= m; ++j) mapped[j] = -1;  // per-step status slots
+    auto can_enqueue = [&](int j) { return j < m && total + j < max_it; };
+    int k = 0, enq = 0, status = 0;
+    while (true) {
+      while (enq <= k + lag && can_enqueue(enq)) {  // step k and, speculatively, k + lag
+        enqueue_step(enq);
+        ++enq;
       }
-      const int kk = k + 1;  // vectors V_0..V_k
-      // The stored basis vectors S_j are not exactly unit length: the
-      // Pythagorean scale is an estimate, and instead of a rescaling pass the
-      // update pass measures ||S_{k+1}||^2 exactly (dsm[64 + k + 1]) and the
-      // normalisation is carried as c_j = 1 / ||S_j|| (true basis v_j = c_j S_j).
-      // Raw dots d_j = <S_j, A P^-1 S_k> give H(j,k) = c_k c_j d_j; the update
-      // kernel divides by ||S_j||^2 itself (hn2 = dsm + 64).
-      stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s);  // [d_0..d_k, <w,w>]
-      stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190,
-                          dsm + 64);
-      h->launches += 2;
-      ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
-      ck(cudaStreamSynchronize(s), "sync");
-      const double ckk = cn[size_t(k)];
-      const double ww = hp[kk];
-      double hh = 0.0;
-      for (int j = 0; j <= k; ++j) hh += hp[j] * hp[j] / hp[64 + j];
-      const double sc1 = hp[190];  // scale applied to the projected vector
-      for (int j = 0; j <= k; ++j) Hat(j, k) = ckk * cn[size_t(j)] * hp[j];
-      double n2 = hp[64 + kk];     // ||S_{k+1}||^2
-      double hn = ckk * std::sqrt(n2) / sc1;
-      static const bool trace = std::getenv("STG_GMRES_TRACE") != nullptr;
-      if (trace)  // Arnoldi cancellation / normalisation diagnostics
-        std::fprintf(stderr, "arnoldi k=%d cancel=%.3e nv2-1=%.3e\n", k, (ww - hh) / ww,
-                     n2 - 1.0);
-      if (!(ww - hh > reorth_tol * ww) || !(n2 > 0.0)) {
-        // heavy cancellation (the single classical pass leaves an
-        // orthogonality loss ~ eps ||w|| / ||w - V h||): re-orthogonalise the
-        // stored vector in two more passes, [g2, <S,S>] = [V, S]^T S, then
-        // S' = (S - sum g2_j / ||S_j||^2 S_j) * Pythagorean scale
-        stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm + 128, s);
-        stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s, dsm + 128,
-                            dsm + 191, dsm + 64);
-        h->launches += 2;
-        ck(cudaMemcpyAsync(hp, dsm, sizeof(double) * 192, cudaMemcpyDeviceToHost, s), "memcpy");
-        ck(cudaStreamSynchronize(s), "sync");
-        for (int j = 0; j <= k; ++j) Hat(j, k) += ckk * cn[size_t(j)] * hp[128 + j] / sc1;
-        n2 = hp[64 + kk];
-        hn = ckk * std::sqrt(n2) / (sc1 * hp[191]);
+      if (k >= enq) break;  // end of the cycle (restart length or max_it)
+      ck(cudaEventSynchronize(h->ev_step[k & 1]), "sync");  // step k done
+      status = mapped[k];
+      if (status == 3) {  // step k needs a second Gram-Schmidt pass
+        enqueue_reorth(k);
         h->reorth++;
+        ck(cudaEventSynchronize(h->ev_re), "sync");
+        status = mapped[k];
+        if (status == 0) enq = k + 1;  // a speculative step k+1 was skipped: enqueue it again
       }
-      cn[size_t(k + 1)] = n2 > 0.0 ? 1.0 / std::sqrt(n2) : 0.0;
-      if (!(ww > 0.0)) hn = 0.0;  // exact breakdown: A P^-1 v_k = 0
-      Hat(k + 1, k) = hn;
-      for (int j = 0; j < k; ++j) {
-        const double t0 = cs[j] * Hat(j, k) + sn[j] * Hat(j + 1, k);
-        Hat(j + 1, k) = -sn[j] * Hat(j, k) + cs[j] * Hat(j + 1, k);
-        Hat(j, k) = t0;
-      }
-      const double den = std::hypot(Hat(k, k), Hat(k + 1, k));
-      cs[k] = den == 0.0 ? 1.0 : Hat(k, k) / den;
-      sn[k] = den == 0.0 ? 0.0 : Hat(k + 1, k) / den;
-      Hat(k, k) = den;
-      Hat(k + 1, k) = 0.0;
-      g[k + 1] = -sn[k] * g[k];
-      g[k] = cs[k] * g[k];
-      if (std::abs(g[k + 1]) / bnorm <= tol) {  // residual estimate converged
-        est_rel = std::abs(g[k + 1]) / bnorm;
-        ++k;
-        break;
-      }
-      if (hn == 0.0 || !std::isfinite(hn)) {
-        ++k;
-        break;
-      }
+      if (status < 0 || status > 2) throw std::runtime_error("gmres: Arnoldi step status lost");
+      ++k;
+      if (status != 0) break;  // converged (1) or breakdown (2) at step k - 1
     }
+    // stream order: any speculative launches after step k - 1 are no-ops
+    total += k;
+    ck(cudaMemcpyAsync(h->gpin, G, sizeof(stg::GmresDev), cudaMemcpyDeviceToHost, s), "memcpy");
+    ck(cudaStreamSynchronize(s), "sync");
+    const stg::GmresDev& Gh = *h->gpin;
+    if (Gh.k_done != k) throw std::runtime_error("gmres: device step count mismatch");
     for (int i = k - 1; i >= 0; --i) {
-      double acc = g[i];
-      for (int j = i + 1; j < k; ++j) acc -= Hat(i, j) * y[j];
-      y[i] = acc / Hat(i, i);
+      double acc = Gh.g[i];
+      for (int j = i + 1; j < k; ++j) acc -= Gh.H[size_t(i) * m + j] * y[size_t(j)];
+      y[size_t(i)] = acc / Gh.H[size_t(i) * m + i];
     }
-    for (int j = 0; j < k; ++j) hp[256 + j] = y[size_t(j)] * cn[size_t(j)];  // x += sum y_j c_j S_j
+    for (int j = 0; j < k; ++j) hp[256 + j] = y[size_t(j)] * Gh.cn[j];  // x += sum y_j c_j S_j
     ck(cudaMemcpyAsync(dsm + 256, hp + 256, sizeof(double) * k, cudaMemcpyHostToDevice, s),
        "memcpy");
     if (P) {
@@ -596,12 +634,12 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
       h->launches++;
     }
-    if (est_rel >= 0.0) {
+    if (status == 1) {
       // stop on the Arnoldi residual estimate, as Eigen's GMRES does; the
-      // re-orthogonalised basis keeps it close to the true residual (the
-      // Newton residual that follows is computed exactly)
+      // basis orthogonality keeps it close to the true residual (the Newton
+      // residual that follows is computed exactly)
       st.converged = true;
-      st.rel_residual = est_rel;
+      st.rel_residual = Gh.est / bnorm;
       break;
     }
     // no sync here: hp+256 is rewritten only after the next cycle's first
@@ -652,7 +690,8 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     stg::vec_fill(du, 0.0, n, h->stream);
     h->launches += 2;
     const GmresStats gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
-                                cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true);
+                                cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
+                                /*pipelined=*/!general_model(h->desc.model));
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
@@ -703,10 +742,11 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
     a.X = U;
     a.R = Jv;
     a.fdv = v;
+    a.skip = h->skip;
     if (stg::fd_fused_supported(a)) {
       const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
       double* vv = h->small.p + 1000;
-      stg::vec_dot(v, v, n, h->partial.p, vv, h->stream);
+      stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
       a.fd_vv = vv;
       a.fd_c = fd_eps * std::sqrt(1.0 + un);
       if (stg::launch_slab_generic(a, h->stream) < 0)
@@ -1038,13 +1078,13 @@ Op dense_op(stg_handle* h, const double* tab, int nt, int npc, int ncells, long 
     if (!h->cublas && cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS)
       throw CudaError("cublasCreate failed");
     cublasSetStream(h->cublas, h->stream);
-    stg::permute_to_elem(h->pz1.p, in, nt, npc, ns, h->stream);
+    stg::permute_to_elem(h->pz1.p, in, nt, npc, ns, h->stream, h->skip);
     const double one = 1.0, zero = 0.0;
     // column-major: Yp (nb x cells) = B Xp; the row-major B is op(T) of its buffer
     if (cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, nb, ncells, nb, &one, tab, nb, h->pz1.p,
                     nb, &zero, h->pz2.p, nb) != CUBLAS_STATUS_SUCCESS)
       throw CudaError("cublasDgemm failed");
-    stg::permute_from_elem(out, h->pz2.p, nt, npc, ns, h->stream);
+    stg::permute_from_elem(out, h->pz2.p, nt, npc, ns, h->stream, h->skip);
     h->launches += 3;
   };
 }
@@ -1127,7 +1167,7 @@ Op general_eblock(stg_handle* h, const stg::MixCoef& mx) {
   }
   const double* tab = h->gBinv.p;
   return [h, tab, nb, nt, ndl, nc, ns](const double* in, double* out) {
-    stg::precond_eblock(out, in, tab, (long long)nb * nb, nt, ndl, nc, ns, h->stream);
+    stg::precond_eblock(out, in, tab, (long long)nb * nb, nt, ndl, nc, ns, h->stream, h->skip);
     h->launches++;
   };
 }
@@ -1156,7 +1196,7 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     ck(cudaStreamSynchronize(h->stream), "sync");
     const double* dt = h->ptab.p;
     return [h, dt, nt, npc, ns](const double* in, double* out) {
-      stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream);
+      stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream, h->skip);
       h->launches++;
     };
   }
@@ -1205,7 +1245,7 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     }
     if (ok)
       return [h, c](const double* in, double* out) {
-        if (stg::launch_precond_fdm(c, h->g, in, out, h->stream) < 0)
+        if (stg::launch_precond_fdm(c, h->g, in, out, h->stream, h->skip) < 0)
           throw std::runtime_error("element-block preconditioner launch failed");
         h->launches++;
       };
@@ -1241,12 +1281,12 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       h->eblock_valid = true;
     }
     return [h, fb, nt, n1, ncells, ns](const double* in, double* out) {
-      stg::precond_eblock_f32(out, in, fb, nt, n1, ncells, ns, h->stream);
+      stg::precond_eblock_f32(out, in, fb, nt, n1, ncells, ns, h->stream, h->skip);
       h->launches++;
     };
   }
   return [h, tab, bstride, nt, n1, ncells, ns](const double* in, double* out) {
-    stg::precond_eblock(out, in, tab, bstride, nt, n1, ncells, ns, h->stream);
+    stg::precond_eblock(out, in, tab, bstride, nt, n1, ncells, ns, h->stream, h->skip);
     h->launches++;
   };
 }
@@ -1731,7 +1771,8 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
     const GmresStats st = gmres(
         h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
-        restart, tol, max_it, P ? &P : nullptr);
+        restart, tol, max_it, P ? &P : nullptr, /*x_zero=*/false,
+        /*pipelined=*/!general_model(h->desc.model));
     if (iterations) *iterations = st.iterations;
     if (rel_residual) *rel_residual = st.rel_residual;
     if (!st.converged)

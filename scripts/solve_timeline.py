@@ -39,3 +39,11 @@ print(json.dumps({"config": name, "wall_ms": 1e3 * wall, "kernel_busy_ms": busy,
                   "top": dict(sorted(by.items(), key=lambda x: -x[1])[:12]),
                   "counts": {k: sum(1 for e in kern if re.sub(r"^void |\(anonymous namespace\)::|stg::", "", e.name).split("(")[0][:48] == k)
                              for k in by}}))
+if "--seq" in sys.argv:  # per-launch sequence: gap before each kernel, duration
+    ks = sorted(kern, key=lambda e: e.time_range.start)
+    prev = None
+    for e in ks:
+        gap = (e.time_range.start - prev) if prev is not None else 0.0
+        nm = re.sub(r"^void |\(anonymous namespace\)::|stg::", "", e.name).split("(")[0][:40]
+        print(f"  gap {gap:7.1f} us  dur {e.device_time_total:7.1f} us  {nm}")
+        prev = e.time_range.end
