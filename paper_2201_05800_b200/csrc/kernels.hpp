@@ -17,6 +17,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 
 #include <cuda_runtime.h>
 
@@ -74,6 +75,39 @@ struct Skip {
 __device__ __forceinline__ bool skip_now(const Skip& s) {
   return s.flag != nullptr && *reinterpret_cast<const volatile int*>(s.flag) != s.run;
 }
+
+// Programmatic dependent launch.  The hot kernels are launched with
+// programmatic stream serialisation (launch_pdl) and start with pdl_entry():
+// wait until the preceding kernel has completed and its writes are visible
+// (griddepcontrol.wait -- before ANY global read, the skip flag included),
+// then let the next kernel be scheduled at once, so its launch and prologue
+// overlap this kernel's tail instead of following it.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// kernel classes for STG_PDL_MASK (A/B measurements; default: all on;
+// STG_NO_PDL: all off)
+enum PdlClass : int { kPdlSlab = 1, kPdlFdm = 2, kPdlVec = 4, kPdlPrecond = 8 };
+bool pdl_enabled(int cls);
+
+template <typename... KArgs, typename... Args>
+inline void launch_ex(int pdl_cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled(pdl_cls) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 #endif
 
 // Device state of one GMRES(m) cycle (stg.cpp, gmres): the Hessenberg matrix
@@ -131,6 +165,9 @@ struct SlabArgs {
   const double* fd_vv;
   double fd_c;
   Skip skip;
+  // launch without programmatic serialisation (the launch follows a
+  // cross-stream event wait, which PDL must not relax)
+  int no_pdl;
 };
 // true if the d = 1 lane kernel handles fused FD Jacobian actions for a
 bool fd_fused_supported(const SlabArgs& a);

@@ -104,6 +104,7 @@ template <int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ FdmCoef c,
                const Geometry g, double* __restrict__ out, const Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (ptxh::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -324,7 +325,7 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
   const int nseg = g.n_cells / E;
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
-  kern<<<grid, THREADS, SMEM, s>>>(map, coef, g, out, skip);
+  launch_ex(kPdlFdm, kern, grid, THREADS, SMEM, s, map, coef, g, out, skip);
   return 1;
 }
 

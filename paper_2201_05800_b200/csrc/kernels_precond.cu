@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(kPB) k_tblock(double* __restrict__ out,
                                                 const double* __restrict__ in,
                                                 const double* __restrict__ minv, int npc,
                                                 int ncells, long long ns, Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   // smem layout [t][j][k]: consecutive nodes (threads) read consecutive words
   // (the global table is [k][t][j]; a [k]-major smem copy would be a 32-way
@@ -61,6 +62,7 @@ __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
                                                 const double* __restrict__ B, long long bstride,
                                                 int nt, int n1, int ncells, long long ns,
                                                 Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   __shared__ double xs[8][NB];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -95,6 +97,7 @@ template <int N1, int NT>
 __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict__ Binv,
                                                               const double* __restrict__ U,
                                                               const SlabArgs a) {
+  pdl_entry();
   constexpr int NB = N1 * NT;
   static_assert(NB <= 32, "one lane per block row");
   const int lane = threadIdx.x & 31;
@@ -196,6 +199,7 @@ __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
                                                  const double* __restrict__ in,
                                                  const float* __restrict__ B, int n1,
                                                  int ncells, long long ns, Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   static_assert(NB <= 16 && NB % 2 == 0, "two elements per warp");
   const int lane = threadIdx.x & 31, h = lane >> 4, r = lane & 15;
@@ -236,11 +240,11 @@ void precond_tblock(double* out, const double* in, const double* minv, int nt, i
   const size_t smem = size_t(npc) * nt * nt * sizeof(double);
   const int g = pgrid(ns);
   switch (nt) {
-    case 2: k_tblock<2><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
-    case 3: k_tblock<3><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
-    case 4: k_tblock<4><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
-    case 5: k_tblock<5><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
-    default: k_tblock<6><<<g, kPB, smem, s>>>(out, in, minv, npc, ncells, ns, skip); break;
+    case 2: launch_ex(kPdlPrecond, k_tblock<2>, g, kPB, smem, s, out, in, minv, npc, ncells, ns, skip); break;
+    case 3: launch_ex(kPdlPrecond, k_tblock<3>, g, kPB, smem, s, out, in, minv, npc, ncells, ns, skip); break;
+    case 4: launch_ex(kPdlPrecond, k_tblock<4>, g, kPB, smem, s, out, in, minv, npc, ncells, ns, skip); break;
+    case 5: launch_ex(kPdlPrecond, k_tblock<5>, g, kPB, smem, s, out, in, minv, npc, ncells, ns, skip); break;
+    default: launch_ex(kPdlPrecond, k_tblock<6>, g, kPB, smem, s, out, in, minv, npc, ncells, ns, skip); break;
   }
 }
 
@@ -248,7 +252,7 @@ void precond_eblock(double* out, const double* in, const double* B, long long bs
                     int n1, int ncells, long long ns, cudaStream_t s, Skip skip) {
   int g = (ncells + 7) / 8;
   if (g > 148 * 16) g = 148 * 16;
-  k_eblock<kMaxT * kMaxN><<<g, 256, 0, s>>>(out, in, B, bstride, nt, n1, ncells, ns, skip);
+  launch_ex(kPdlPrecond, k_eblock<kMaxT * kMaxN>, g, 256, 0, s, out, in, B, bstride, nt, n1, ncells, ns, skip);
 }
 
 // ---- d = 2 element-block Jacobi with one shared dense block ----------------
@@ -269,6 +273,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
     k_eblock_dense(double* __restrict__ out, const double* __restrict__ in,
                    const double* __restrict__ B, int nb, int npc, int nt, int ncells,
                    long long ns) {
+  pdl_entry();
   extern __shared__ double sm[];
   constexpr int NBP = 128;                  // padded row count of B^T (4 rows x 32 groups)
   double* Bt = sm;                          // [nb][NBP]: Bt[k][row] = B[row][k]
@@ -361,6 +366,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1)
 // reach them).  Then B_e = T (x) I + S (x) K_e is inverted per element.
 __global__ void k_probe_set(double* __restrict__ P, int ndl, int col, int nx, int ny, int sx,
                             int sy, int cx0, int cy0, int ncells) {
+  pdl_entry();
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
     const int cx = c % nx, cy = c / nx;
     const bool on = (cx % sx) == cx0 && (cy % sy) == cy0;
@@ -369,6 +375,7 @@ __global__ void k_probe_set(double* __restrict__ P, int ndl, int col, int nx, in
 }
 __global__ void k_probe_extract(double* __restrict__ K, const double* __restrict__ F, int ndl,
                                 int col, int nx, int sx, int sy, int cx0, int cy0, int ncells) {
+  pdl_entry();
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < ncells; c += gridDim.x * blockDim.x) {
     const int cx = c % nx, cy = c / nx;
     if ((cx % sx) != cx0 || (cy % sy) != cy0) continue;
@@ -384,6 +391,7 @@ __global__ void __launch_bounds__(128) k_gen_eblock(double* __restrict__ Binv,
                                                     const double* __restrict__ K,
                                                     const MixCoef mx, int nt, int ndl,
                                                     int ncells) {
+  pdl_entry();
   constexpr int MAXB = 32;
   const int lane = threadIdx.x & 31;
   const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -454,11 +462,11 @@ bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   const long long threads = (long long)a.g.nx * 32;  // one warp per element
   const int blocks = int((threads + 127) / 128);
   switch (a.n_in) {
-    case 2: k_build_burgers_eblock<N1, 2><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
-    case 3: k_build_burgers_eblock<N1, 3><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
-    case 4: k_build_burgers_eblock<N1, 4><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
-    case 5: k_build_burgers_eblock<N1, 5><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
-    case 6: k_build_burgers_eblock<N1, 6><<<blocks, 128, 0, s>>>(Binv, U, a); return true;
+    case 2: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 2>, blocks, 128, 0, s, Binv, U, a); return true;
+    case 3: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 3>, blocks, 128, 0, s, Binv, U, a); return true;
+    case 4: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 4>, blocks, 128, 0, s, Binv, U, a); return true;
+    case 5: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 5>, blocks, 128, 0, s, Binv, U, a); return true;
+    case 6: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 6>, blocks, 128, 0, s, Binv, U, a); return true;
     default: return false;
   }
 }
@@ -466,6 +474,7 @@ bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
 // stage-major [t][cell][node] <-> element-major [cell][t][node]
 __global__ void k_to_elem(double* __restrict__ Xp, const double* __restrict__ X, int nt, int npc,
                           long long n, long long ns, Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   const long long nb = (long long)nt * npc;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -477,6 +486,7 @@ __global__ void k_to_elem(double* __restrict__ Xp, const double* __restrict__ X,
 }
 __global__ void k_from_elem(double* __restrict__ Y, const double* __restrict__ Yp, int nt,
                             int npc, long long n, long long ns, Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   const long long nb = (long long)nt * npc;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -490,12 +500,12 @@ __global__ void k_from_elem(double* __restrict__ Y, const double* __restrict__ Y
 void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s,
                      Skip skip) {
   const long long n = ns * nt;
-  k_to_elem<<<pgrid(n), kPB, 0, s>>>(Xp, X, nt, npc, n, ns, skip);
+  launch_ex(kPdlPrecond, k_to_elem, pgrid(n), kPB, 0, s, Xp, X, nt, npc, n, ns, skip);
 }
 void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
                        cudaStream_t s, Skip skip) {
   const long long n = ns * nt;
-  k_from_elem<<<pgrid(n), kPB, 0, s>>>(Y, Yp, nt, npc, n, ns, skip);
+  launch_ex(kPdlPrecond, k_from_elem, pgrid(n), kPB, 0, s, Y, Yp, nt, npc, n, ns, skip);
 }
 
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
@@ -514,23 +524,23 @@ bool precond_eblock_dense(double* out, const double* in, const double* B, int nt
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntile = (ncells + kTE - 1) / kTE;
   const int grid = ntile < sms ? ntile : sms;
-  k_eblock_dense<<<grid, kDenseThreads, smem, s>>>(out, in, B, nb, npc, nt, ncells, ns);
+  launch_ex(kPdlPrecond, k_eblock_dense, grid, kDenseThreads, smem, s, out, in, B, nb, npc, nt, ncells, ns);
   return true;
 }
 
 void probe_set(double* P, int ndl, int col, int nx, int ny, int sx, int sy, int cx0, int cy0,
                int ncells, cudaStream_t s) {
-  k_probe_set<<<pgrid(ncells), kPB, 0, s>>>(P, ndl, col, nx, ny, sx, sy, cx0, cy0, ncells);
+  launch_ex(kPdlPrecond, k_probe_set, pgrid(ncells), kPB, 0, s, P, ndl, col, nx, ny, sx, sy, cx0, cy0, ncells);
 }
 void probe_extract(double* K, const double* F, int ndl, int col, int nx, int sx, int sy, int cx0,
                    int cy0, int ncells, cudaStream_t s) {
-  k_probe_extract<<<pgrid(ncells), kPB, 0, s>>>(K, F, ndl, col, nx, sx, sy, cx0, cy0, ncells);
+  launch_ex(kPdlPrecond, k_probe_extract, pgrid(ncells), kPB, 0, s, K, F, ndl, col, nx, sx, sy, cx0, cy0, ncells);
 }
 bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt, int ndl,
                        int ncells, cudaStream_t s) {
   if (nt * ndl > 32) return false;
   const long long threads = (long long)ncells * 32;
-  k_gen_eblock<<<int((threads + 127) / 128), 128, 0, s>>>(Binv, K, mx, nt, ndl, ncells);
+  launch_ex(kPdlPrecond, k_gen_eblock, int((threads + 127) / 128), 128, 0, s, Binv, K, mx, nt, ndl, ncells);
   return true;
 }
 
@@ -540,13 +550,13 @@ void precond_eblock_f32(double* out, const double* in, const float* B, int nt, i
   long long g = ((ncells + 1) / 2 + 7) / 8;  // 8 warps per block, 2 elements per warp
   if (g > 148 * 16) g = 148 * 16;
   switch (nb) {
-    case 4: k_eblock2<4><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
-    case 6: k_eblock2<6><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
-    case 8: k_eblock2<8><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
-    case 10: k_eblock2<10><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
-    case 12: k_eblock2<12><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
-    case 14: k_eblock2<14><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
-    case 16: k_eblock2<16><<<int(g), 256, 0, s>>>(out, in, B, n1, ncells, ns, skip); return;
+    case 4: launch_ex(kPdlPrecond, k_eblock2<4>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
+    case 6: launch_ex(kPdlPrecond, k_eblock2<6>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
+    case 8: launch_ex(kPdlPrecond, k_eblock2<8>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
+    case 10: launch_ex(kPdlPrecond, k_eblock2<10>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
+    case 12: launch_ex(kPdlPrecond, k_eblock2<12>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
+    case 14: launch_ex(kPdlPrecond, k_eblock2<14>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
+    case 16: launch_ex(kPdlPrecond, k_eblock2<16>, int(g), 256, 0, s, out, in, B, n1, ncells, ns, skip); return;
     default: break;
   }
 }

@@ -111,6 +111,7 @@ __device__ __forceinline__ void burgers_jvp_line(const SpatialCoef& sp, const do
 // ---------------------------------------------------------------------------
 template <int N1>
 __global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   const int K = a.g.nx;
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
 // ---------------------------------------------------------------------------
 template <int N1, int NT>
 __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   constexpr int EPW = 32 / NT;  // elements per warp
   const int lane = threadIdx.x & 31;
@@ -263,6 +265,7 @@ struct GenericShape {
 template <int D, int N1>
 __global__ void __launch_bounds__(GenericShape<D, N1>::THREADS)
     slab_generic_kernel(const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   using Sh = GenericShape<D, N1>;
   constexpr int NPC = Sh::NPC;
@@ -367,6 +370,7 @@ struct Shape2d {
 template <int N1, int NT>
 __global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
     slab2d_kernel(const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   using Sh = Shape2d<N1, NT>;
   constexpr int NPC = Sh::NPC, E = Sh::E;
@@ -532,6 +536,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 template <int N1, int NT>
 __global__ void __launch_bounds__(Shape2d<N1, NT>::THREADS)
     slab2d_persist(const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   using P = P2d<N1, NT>;
   using Sh = typename P::Sh;
@@ -715,6 +720,7 @@ __device__ __forceinline__ void bulk_wait0() {
 template <int N1, int NT, int E, int MINB>
 __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
     slab2d_plane(const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   using P = Plane2d<N1, NT, E>;
   constexpr int NPC = P::NPC, PL = P::PLANE;
@@ -916,6 +922,7 @@ __device__ __forceinline__ double2 ldg2(const double* p) {
 template <bool FULL_S>
 __global__ void __launch_bounds__(fast::THREADS, 4)
     slab3d_n4_tma(const __grid_constant__ CUtensorMap tmX, const SlabArgs a) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   using namespace fast;
   extern __shared__ unsigned char smem_raw[];
@@ -1204,6 +1211,7 @@ template <bool FULL_S>
 __global__ void __launch_bounds__(pst::THREADS, 3)
     slab3d_n4_persist(const __grid_constant__ pst::Maps maps, const SlabArgs a,
                       const pst::Layout lay) {
+  pdl_entry();
   if (skip_now(a.skip)) return;
   using namespace pst;
   using fast::row_of;
@@ -1412,7 +1420,7 @@ int launch1d(const SlabArgs& a, cudaStream_t s) {
       constexpr int EPW = 32 / NT;
       const long long warps = (a.g.nx + EPW - 1) / EPW;
       const int blocks = int((warps * 32 + 255) / 256);
-      slab1d_lane_kernel<N1, NT><<<blocks, 256, 0, s>>>(a);
+      launch_ex(kPdlSlab, slab1d_lane_kernel<N1, NT>, blocks, 256, 0, s, a);
       return 1;
     };
     switch (a.n_in) {
@@ -1425,7 +1433,7 @@ int launch1d(const SlabArgs& a, cudaStream_t s) {
     }
   }
   const int blocks = (a.g.nx + kThreads1d - 1) / kThreads1d;
-  slab1d_kernel<N1><<<blocks, kThreads1d, 0, s>>>(a);
+  launch_ex(kPdlSlab, slab1d_kernel<N1>, blocks, kThreads1d, 0, s, a);
   return 1;
 }
 
@@ -1470,7 +1478,7 @@ int launch_plane2d(const SlabArgs& a, cudaStream_t s) {
   const int nseg = a.g.n_cells / E;
   int grid = occ * num_sms_cached();
   if (grid > nseg) grid = nseg;
-  slab2d_plane<N1, NT, E, MINB><<<grid, Q::THREADS, Q::SMEM, s>>>(a);
+  launch_ex(kPdlSlab, slab2d_plane<N1, NT, E, MINB>, grid, Q::THREADS, Q::SMEM, s, a);
   return 1;
 }
 
@@ -1498,11 +1506,11 @@ int launch2d_t(const SlabArgs& a, cudaStream_t s) {
     const int nseg = a.g.n_cells / Sh::E;
     int grid = occ * num_sms_cached();
     if (grid > nseg) grid = nseg;
-    slab2d_persist<N1, NT><<<grid, Sh::THREADS, P::SMEM, s>>>(a);
+    launch_ex(kPdlSlab, slab2d_persist<N1, NT>, grid, Sh::THREADS, P::SMEM, s, a);
     return 1;
   }
   const int blocks = (a.g.n_cells + Sh::E - 1) / Sh::E;
-  slab2d_kernel<N1, NT><<<blocks, Sh::THREADS, 0, s>>>(a);
+  launch_ex(kPdlSlab, slab2d_kernel<N1, NT>, blocks, Sh::THREADS, 0, s, a);
   return 1;
 }
 
@@ -1528,7 +1536,7 @@ int launch_generic_t(const SlabArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(slab_generic_kernel<D, N1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
   }
-  slab_generic_kernel<D, N1><<<blocks, Sh::THREADS, smem, s>>>(a);
+  launch_ex(kPdlSlab, slab_generic_kernel<D, N1>, blocks, Sh::THREADS, smem, s, a);
   return 1;
 }
 
@@ -1655,9 +1663,9 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
     const int blocks = (a.seg_end > 0 ? a.seg_end : a.g.n_cells / fast::E) - a.seg_begin;
     if (blocks <= 0) return 0;
     if (a.full_s) {
-      slab3d_n4_tma<true><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+      launch_ex(kPdlSlab, slab3d_n4_tma<true>, blocks, fast::THREADS, fast::SMEM_BYTES, s, map, a);
     } else {
-      slab3d_n4_tma<false><<<blocks, fast::THREADS, fast::SMEM_BYTES, s>>>(map, a);
+      launch_ex(kPdlSlab, slab3d_n4_tma<false>, blocks, fast::THREADS, fast::SMEM_BYTES, s, map, a);
     }
     return 1;
   }
@@ -1711,9 +1719,9 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   int grid = occ * num_sms();
   if (grid > nseg) grid = nseg;
   if (a.full_s) {
-    slab3d_n4_persist<true><<<grid, pst::THREADS, lay.smem, s>>>(m, a, lay);
+    launch_ex(a.no_pdl ? 0 : kPdlSlab, slab3d_n4_persist<true>, grid, pst::THREADS, lay.smem, s, m, a, lay);
   } else {
-    slab3d_n4_persist<false><<<grid, pst::THREADS, lay.smem, s>>>(m, a, lay);
+    launch_ex(a.no_pdl ? 0 : kPdlSlab, slab3d_n4_persist<false>, grid, pst::THREADS, lay.smem, s, m, a, lay);
   }
   return 1;
 }

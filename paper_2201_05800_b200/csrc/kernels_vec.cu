@@ -9,6 +9,7 @@
 // project + Pythagorean-normalise + norm pass (stg.cpp, gmres).
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -56,27 +57,32 @@ __device__ __forceinline__ void block_finish_sum(const double* part, int nblocks
 }
 
 __global__ void k_fill(double* x, double v, long long n) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     x[i] = v;
 }
 __global__ void k_copy(double* __restrict__ y, const double* __restrict__ x, long long n) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] = x[i];
 }
 __global__ void k_axpby(double* y, double a, const double* x, double b, long long n) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] = fma(a, x[i], b * y[i]);
 }
 __global__ void k_axpy(double* y, double a, const double* x, long long n) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
     y[i] = fma(a, x[i], y[i]);
 }
 __global__ void k_broadcast(double* __restrict__ U, const double* __restrict__ u, int nb,
                             long long n) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const double v = u[i];
@@ -84,6 +90,7 @@ __global__ void k_broadcast(double* __restrict__ U, const double* __restrict__ u
   }
 }
 __global__ void k_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n) {
+  pdl_entry();
   const double s = 1.0 / sqrt(nrm2[0]);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
@@ -219,6 +226,7 @@ __global__ void __launch_bounds__(kVecBlock) k_multidot(const double* __restrict
                                                         long long nw, double* part,
                                                         double* out, unsigned* counter,
                                                         Skip skip) {
+  pdl_entry();
   if (skip_now(skip)) return;
   using O = VecT<W>;
   const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
@@ -263,6 +271,7 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
                                                       unsigned* counter,
                                                       const double* __restrict__ hn2, Skip skip,
                                                       GivensArgs gv) {
+  pdl_entry();
   if (skip_now(skip)) return;
   using O = VecT<W>;
   const int kk = KMAX <= kGroup ? KMAX : k;  // KMAX <= 8: instantiated for k == KMAX
@@ -320,6 +329,7 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
 
 __global__ void k_gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol,
                              double* hn2_0) {
+  pdl_entry();
   G->m = m;
   G->status = 0;
   G->k_done = 0;
@@ -335,6 +345,7 @@ __global__ void k_gmres_init(GmresDev* G, int m, double beta, double tol_abs, do
 __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x, long long n,
                                                    double* part, double* out,
                                                    unsigned* counter) {
+  pdl_entry();
   __shared__ double red[kBlock / 32];
   double m = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -370,24 +381,38 @@ int grid_for(long long n) {
 
 int reduce_grid(long long n) { return grid_for(n); }
 
+// Vector kernels use PDL only below 4 Mi elements: there the launch latency
+// it hides is a large share of the kernel; on the 64 MiB c4 vectors it
+// measured slower (c4 solve 2.09 -> 2.20 ms, c3 8.2 -> 7.9 ms with it on)
+int vec_pdl(long long n) { return n < (4LL << 20) ? kPdlVec : 0; }
+
+bool pdl_enabled(int cls) {
+  static const int mask = [] {
+    if (std::getenv("STG_NO_PDL")) return 0;
+    const char* e = std::getenv("STG_PDL_MASK");
+    return e ? std::atoi(e) : kPdlSlab | kPdlFdm | kPdlVec | kPdlPrecond;
+  }();
+  return (mask & cls) != 0;
+}
+
 void vec_fill(double* x, double v, long long n, cudaStream_t s) {
-  k_fill<<<grid_for(n), kBlock, 0, s>>>(x, v, n);
+  launch_ex(vec_pdl(n), k_fill, grid_for(n), kBlock, 0, s, x, v, n);
 }
 void vec_copy(double* y, const double* x, long long n, cudaStream_t s) {
-  k_copy<<<grid_for(n), kBlock, 0, s>>>(y, x, n);
+  launch_ex(vec_pdl(n), k_copy, grid_for(n), kBlock, 0, s, y, x, n);
 }
 void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s) {
-  k_axpy<<<grid_for(n), kBlock, 0, s>>>(y, a, x, n);
+  launch_ex(vec_pdl(n), k_axpy, grid_for(n), kBlock, 0, s, y, a, x, n);
 }
 void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s) {
-  k_axpby<<<grid_for(n), kBlock, 0, s>>>(y, a, x, b, n);
+  launch_ex(vec_pdl(n), k_axpby, grid_for(n), kBlock, 0, s, y, a, x, b, n);
 }
 void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t s) {
-  k_broadcast<<<grid_for(n), kBlock, 0, s>>>(U, u, nb, n);
+  launch_ex(vec_pdl(n), k_broadcast, grid_for(n), kBlock, 0, s, U, u, nb, n);
 }
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
                        cudaStream_t s) {
-  k_scale_invsqrt<<<grid_for(n), kBlock, 0, s>>>(y, x, nrm2, n);
+  launch_ex(vec_pdl(n), k_scale_invsqrt, grid_for(n), kBlock, 0, s, y, x, nrm2, n);
 }
 
 namespace {
@@ -462,14 +487,14 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
                   double* partial, double* out, cudaStream_t s, Skip skip) {
   const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
-  STG_DISPATCH_K(k, W, (k_multidot<KM, WW><<<multi_grid<KM, WW, false>(n), kVecBlock,
-                                              0, s>>>(V, ldv, k, w, n / WW, partial, out, c,
+  STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_multidot<KM, WW>, multi_grid<KM, WW, false>(n), kVecBlock,
+                                              0, s, V, ldv, k, w, n / WW, partial, out, c,
                                                       skip)));
 }
 
 void gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol, double* hn2_0,
                 cudaStream_t s) {
-  k_gmres_init<<<1, 1, 0, s>>>(G, m, beta, tol_abs, reorth_tol, hn2_0);
+  launch_ex(kPdlVec, k_gmres_init, 1, 1, 0, s, G, m, beta, tol_abs, reorth_tol, hn2_0);
 }
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
@@ -478,7 +503,7 @@ void vec_update_dot(double* w, const double* V, long long ldv, int k, const doub
                     GivensArgs gv) {
   const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
-  STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
+  STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_update<KM, WW>, multi_grid<KM, WW, true>(n), kVecBlock, 0, s, 
                            w, V, ldv, k, h, n / WW, -1.0, 1, partial, scale_src, scale_out,
                            out2 + k, c, hn2, skip, gv)));
   if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s, skip);  // <V_j, w_new>
@@ -491,14 +516,14 @@ void vec_combine(double* x, const double* V, long long ldv, int k, const double*
     return;
   }
   const int W = vec_width(n, ldv, V, x);
-  STG_DISPATCH_K(k, W, (k_update<KM, WW><<<multi_grid<KM, WW, true>(n), kVecBlock, 0, s>>>(
+  STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_update<KM, WW>, multi_grid<KM, WW, true>(n), kVecBlock, 0, s, 
                            x, V, ldv, k, y, n / WW, 1.0, accumulate ? 1 : 0, nullptr, nullptr,
                            nullptr, nullptr, nullptr, nullptr, Skip{}, GivensArgs{})));
 }
 
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s) {
   const int g = grid_for(n);
-  k_maxabs<<<g, kBlock, 0, s>>>(x, n, partial, out, counter_of(partial));
+  launch_ex(vec_pdl(n), k_maxabs, g, kBlock, 0, s, x, n, partial, out, counter_of(partial));
 }
 
 void vec_dot(const double* x, const double* y, long long n, double* partial, double* out,

@@ -810,6 +810,7 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
   a.X = h->host_U.p;
   a.W = h->host_u.p;
   a.R = h->host_R.p;
+  a.no_pdl = 1;  // each chunk's launch follows an H2D event wait
   if (!stg::slab_fast_supported(a)) return false;
   if (!h->s_in) {
     ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
