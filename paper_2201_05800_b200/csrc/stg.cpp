@@ -94,7 +94,8 @@ struct stg_handle {
   DevBuf small;    // device scalars / Hessenberg columns
   DevBuf partial;  // reduction partials
   DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
-  DevBuf zv, zc, ptab;  // preconditioner work vectors and block tables
+  DevBuf ptab;          // preconditioner block tables
+  DevBuf zbasis;        // flexible GMRES: preconditioned basis Z_k = P^-1 S_k
   DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
   DevBuf small_out;      // fused small-solve result record
   DevBuf march;          // integrate: ping-pong states
@@ -468,10 +469,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   const long long ld = round_up(n, 32);
   h->basis.ensure(size_t(ld) * (m + 1));
   h->wv.ensure(size_t(n));
-  if (P) {
-    h->zv.ensure(size_t(n));
-    h->zc.ensure(size_t(n));
-  }
+  // flexible GMRES: Z_k = P^-1 S_k is kept, x += sum y_j c_j Z_j (no final
+  // preconditioner apply, and P need not be the same linear map every step)
+  if (P) h->zbasis.ensure(size_t(ld) * m);
+  double* Z = P ? h->zbasis.p : nullptr;
   if (!h->gpin) {
     h->gstate.ensure((sizeof(stg::GmresDev) + 7) / 8);
     ck(cudaMallocHost(&h->gpin, sizeof(stg::GmresDev)), "cudaMallocHost");
@@ -519,8 +520,9 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     {
       SkipScope scope(h, run0);
       if (P) {
-        (*P)(V + size_t(k) * ld, h->zv.p);  // z = P^-1 S_k
-        A(h->zv.p, vn);
+        double* zk = Z + size_t(k) * ld;
+        (*P)(V + size_t(k) * ld, zk);  // Z_k = P^-1 S_k
+        A(zk, vn);
       } else {
         A(V + size_t(k) * ld, vn);
       }
@@ -561,6 +563,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   std::vector<double> y(static_cast<size_t>(m), 0.0);
   int total = 0;
   bool first = true;
+  bool x_set = !x_zero;  // x_zero: x is written (not accumulated) by the first update
   while (true) {
     double beta;
     if (first && x_zero) {  // x = 0: r = b and ||r|| = ||b|| (no operator apply, no sync)
@@ -625,15 +628,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     for (int j = 0; j < k; ++j) hp[256 + j] = y[size_t(j)] * Gh.cn[j];  // x += sum y_j c_j S_j
     ck(cudaMemcpyAsync(dsm + 256, hp + 256, sizeof(double) * k, cudaMemcpyHostToDevice, s),
        "memcpy");
-    if (P) {
-      stg::vec_combine(h->zc.p, V, ld, k, dsm + 256, n, s, false);  // t = V y
-      (*P)(h->zc.p, h->zv.p);                                       // P^-1 t
-      stg::vec_axpy(x, 1.0, h->zv.p, n, s);                         // x += P^-1 V y
-      h->launches += 2;
-    } else {
-      stg::vec_combine(x, V, ld, k, dsm + 256, n, s);  // x += V y
-      h->launches++;
-    }
+    // x (+)= sum y_j c_j Z_j (flexible) or sum y_j c_j S_j
+    stg::vec_combine(x, P ? Z : V, ld, k, dsm + 256, n, s, x_set);
+    h->launches++;
+    x_set = true;
     if (status == 1) {
       // stop on the Arnoldi residual estimate, as Eigen's GMRES does; the
       // basis orthogonality keeps it close to the true residual (the Newton
@@ -644,6 +642,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     }
     // no sync here: hp+256 is rewritten only after the next cycle's first
     // host read, which follows this H2D in stream order
+  }
+  if (!x_set) {  // no Arnoldi step ran (max_it = 0 or r = 0): x = 0
+    stg::vec_fill(x, 0.0, n, s);
+    h->launches++;
   }
   st.iterations = total;
   check_launch(h);
@@ -687,8 +689,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
                                 out.history);
     const LinSys J = jacobian(u);
     stg::vec_axpby(r, 0.0, r, -1.0, n, h->stream);  // r = -r
-    stg::vec_fill(du, 0.0, n, h->stream);
-    h->launches += 2;
+    h->launches++;  // du needs no zero fill: gmres(x_zero) writes it
     const GmresStats gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
                                 cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
                                 /*pipelined=*/!general_model(h->desc.model));
