@@ -24,7 +24,7 @@ OBJDIR = PKG / "build_obj"
 
 SOURCES = ["kernels_slab.cu", "kernels_vec.cu", "kernels_precond.cu", "kernels_fdm.cu",
            "kernels_general.cu", "kernels_small.cu", "stg.cpp"]
-HEADERS = ["kernels.hpp", "constants.hpp", "eig.hpp", "ptx.cuh"]
+HEADERS = ["kernels.hpp", "constants.hpp", "eig.hpp", "ptx.cuh", "krylov.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}"]

@@ -100,6 +100,114 @@ __device__ __forceinline__ void phase_b_cols(const FdmCoef& c, double* B1, const
   }
 }
 
+// ---- the three phases, shared by the standalone apply and the fused
+// Arnoldi-update kernel.  Thread tid owns tile row rowA = tid = (t, e, z) in
+// phases A / A' and the half hB of tile unit (eB, qB) in phase B.
+// Phase A: forward x (kept eigen-indices j -> kx = 2j) and y modes of the
+// thread's (y,x) plane r, into the complex tile B1.
+__device__ __forceinline__ void fdm_phase_a(const FdmCoef& c, const double (&r)[16], double* B1,
+                                            int rowA, int swA) {
+  C2 a[4][2];
+#pragma unroll
+  for (int y = 0; y < 4; ++y)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        re = fma(c.FX[j][x][0], r[4 * y + x], re);
+        im = fma(c.FX[j][x][1], r[4 * y + x], im);
+      }
+      a[y][j] = {re, im};
+    }
+#pragma unroll
+  for (int iy = 0; iy < 4; ++iy)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      C2 b = {0.0, 0.0};
+#pragma unroll
+      for (int y = 0; y < 4; ++y) cmac(b, c.FY[iy][y][0], c.FY[iy][y][1], a[y][j]);
+      const int q = iy * 2 + j;
+      *reinterpret_cast<double2*>(B1 + rowA * 16 + ((q ^ swA) << 1)) = make_double2(b.r, b.i);
+    }
+}
+
+// Phase B: (t,z) tile at (iy, j), two threads per tile: forward z and t
+// modes, 1/Lambda, inverse t and z modes, in place in B1.  Contains CTA
+// barriers: every thread calls it.
+__device__ __forceinline__ void fdm_phase_b(const FdmCoef& c, double* B1, const double* LI,
+                                            int hB, int eB, int qB) {
+  C2 w[4][2];  // [t][k]: z-eigen-column 2 hB + k
+  if (hB)
+    phase_b_cols<1>(c, B1, LI, eB, qB, w);
+  else
+    phase_b_cols<0>(c, B1, LI, eB, qB, w);
+  __syncthreads();  // both halves have read the tile
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int k = 0; k < 2; ++k)
+      *tile_at(B1, t, eB, 2 * hB + k, qB) = make_double2(w[t][k].r, w[t][k].i);
+  __syncthreads();
+  // inverse z on rows t = 2 hB, 2 hB + 1 (all four columns)
+  C2 o[2][4];
+#pragma unroll
+  for (int tt = 0; tt < 2; ++tt) {
+    C2 m[4];
+#pragma unroll
+    for (int iz = 0; iz < 4; ++iz) {
+      const double2 v = *tile_at(B1, 2 * hB + tt, eB, iz, qB);
+      m[iz] = {v.x, v.y};
+    }
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      C2 s = {0.0, 0.0};
+#pragma unroll
+      for (int iz = 0; iz < 4; ++iz) cmac(s, c.IZ[z][iz][0], c.IZ[z][iz][1], m[iz]);
+      o[tt][z] = s;
+    }
+  }
+  __syncthreads();  // every column read before the results overwrite them
+#pragma unroll
+  for (int tt = 0; tt < 2; ++tt)
+#pragma unroll
+    for (int z = 0; z < 4; ++z)
+      *tile_at(B1, 2 * hB + tt, eB, z, qB) = make_double2(o[tt][z].r, o[tt][z].i);
+}
+
+// Phase A': inverse y and x modes (2 Re) of the thread's row into o.
+__device__ __forceinline__ void fdm_phase_a2(const FdmCoef& c, const double* B1, int rowA,
+                                             int swA, double (&o)[16]) {
+  C2 h[4][2];
+#pragma unroll
+  for (int iy = 0; iy < 4; ++iy)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int q = iy * 2 + j;
+      const double2 v = *reinterpret_cast<const double2*>(B1 + rowA * 16 + ((q ^ swA) << 1));
+      h[iy][j] = {v.x, v.y};
+    }
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    C2 m[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      C2 s = {0.0, 0.0};
+#pragma unroll
+      for (int iy = 0; iy < 4; ++iy) cmac(s, c.IY[y][iy][0], c.IY[y][iy][1], h[iy][j]);
+      m[j] = s;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      double re = 0.0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+        re = fma(c.IX[x][j][0], m[j].r, fma(-c.IX[x][j][1], m[j].i, re));
+      o[4 * y + x] = 2.0 * re;
+    }
+  }
+}
+
 template <int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
     fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ FdmCoef c,
@@ -148,8 +256,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
-
-    // ---- phase A: forward x (kept eigen-indices j -> kx = 2j) and y modes --
     {
       double r[16];
 #pragma unroll
@@ -158,104 +264,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
         r[2 * q] = v.x;
         r[2 * q + 1] = v.y;
       }
-      C2 a[4][2];
-#pragma unroll
-      for (int y = 0; y < 4; ++y)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          double re = 0.0, im = 0.0;
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            re = fma(c.FX[j][x][0], r[4 * y + x], re);
-            im = fma(c.FX[j][x][1], r[4 * y + x], im);
-          }
-          a[y][j] = {re, im};
-        }
-#pragma unroll
-      for (int iy = 0; iy < 4; ++iy)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          C2 b = {0.0, 0.0};
-#pragma unroll
-          for (int y = 0; y < 4; ++y) cmac(b, c.FY[iy][y][0], c.FY[iy][y][1], a[y][j]);
-          const int q = iy * 2 + j;
-          *reinterpret_cast<double2*>(B1 + rowA * 16 + ((q ^ swA) << 1)) = make_double2(b.r, b.i);
-        }
+      fdm_phase_a(c, r, B1, rowA, swA);
     }
     __syncthreads();
-
-    // ---- phase B: (t,z) tile at (iy, j), two threads per tile ------------
-    {
-      C2 w[4][2];  // [t][k]: z-eigen-column 2 hB + k
-      if (hB)
-        phase_b_cols<1>(c, B1, LI, eB, qB, w);
-      else
-        phase_b_cols<0>(c, B1, LI, eB, qB, w);
-      __syncthreads();  // both halves have read the tile
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-#pragma unroll
-        for (int k = 0; k < 2; ++k)
-          *tile_at(B1, t, eB, 2 * hB + k, qB) = make_double2(w[t][k].r, w[t][k].i);
-      __syncthreads();
-      // inverse z on rows t = 2 hB, 2 hB + 1 (all four columns)
-      C2 o[2][4];
-#pragma unroll
-      for (int tt = 0; tt < 2; ++tt) {
-        C2 m[4];
-#pragma unroll
-        for (int iz = 0; iz < 4; ++iz) {
-          const double2 v = *tile_at(B1, 2 * hB + tt, eB, iz, qB);
-          m[iz] = {v.x, v.y};
-        }
-#pragma unroll
-        for (int z = 0; z < 4; ++z) {
-          C2 s = {0.0, 0.0};
-#pragma unroll
-          for (int iz = 0; iz < 4; ++iz) cmac(s, c.IZ[z][iz][0], c.IZ[z][iz][1], m[iz]);
-          o[tt][z] = s;
-        }
-      }
-      __syncthreads();  // every column read before the results overwrite them
-#pragma unroll
-      for (int tt = 0; tt < 2; ++tt)
-#pragma unroll
-        for (int z = 0; z < 4; ++z)
-          *tile_at(B1, 2 * hB + tt, eB, z, qB) = make_double2(o[tt][z].r, o[tt][z].i);
-    }
+    fdm_phase_b(c, B1, LI, hB, eB, qB);
     __syncthreads();
-
-    // ---- phase A': inverse y, inverse x (2 Re), store ----------------------
     {
-      C2 h[4][2];
-#pragma unroll
-      for (int iy = 0; iy < 4; ++iy)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int q = iy * 2 + j;
-          const double2 v = *reinterpret_cast<const double2*>(B1 + rowA * 16 + ((q ^ swA) << 1));
-          h[iy][j] = {v.x, v.y};
-        }
       double o[16];
-#pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        C2 m[2];
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          C2 s = {0.0, 0.0};
-#pragma unroll
-          for (int iy = 0; iy < 4; ++iy) cmac(s, c.IY[y][iy][0], c.IY[y][iy][1], h[iy][j]);
-          m[j] = s;
-        }
-#pragma unroll
-        for (int x = 0; x < 4; ++x) {
-          double re = 0.0;
-#pragma unroll
-          for (int j = 0; j < 2; ++j)
-            re = fma(c.IX[x][j][0], m[j].r, fma(-c.IX[x][j][1], m[j].i, re));
-          o[4 * y + x] = 2.0 * re;
-        }
-      }
+      fdm_phase_a2(c, B1, rowA, swA, o);
       double* op = out + tA * ns + (long long)(seg * E + eA) * 64 + zA * 16;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
