@@ -410,22 +410,26 @@ void ensure_workspace(stg_handle* h) {
 }
 
 // ---- device reductions returning to the host --------------------------------
+// Slot of `small` / `pinned` for these scalars: clear of the GMRES step data
+// ([0, 320): dots, norms, scales, y), which an operator that reduces (the FD
+// Jacobian action) must not overwrite while a step is in flight.
+constexpr int kScalarSlot = 960;
 double dev_maxabs(stg_handle* h, const double* x, long long n) {
-  stg::vec_maxabs(x, n, h->partial.p, h->small.p, h->stream);
+  stg::vec_maxabs(x, n, h->partial.p, h->small.p + kScalarSlot, h->stream);
   h->launches += 1;  // fused last-block reduction
-  ck(cudaMemcpyAsync(h->pinned, h->small.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream),
-     "memcpy");
+  ck(cudaMemcpyAsync(h->pinned + kScalarSlot, h->small.p + kScalarSlot, sizeof(double),
+                     cudaMemcpyDeviceToHost, h->stream), "memcpy");
   ck(cudaStreamSynchronize(h->stream), "sync");
-  return h->pinned[0];
+  return h->pinned[kScalarSlot];
 }
 
 double dev_dot(stg_handle* h, const double* x, const double* y, long long n) {
-  stg::vec_dot(x, y, n, h->partial.p, h->small.p, h->stream);
+  stg::vec_dot(x, y, n, h->partial.p, h->small.p + kScalarSlot, h->stream);
   h->launches += 1;
-  ck(cudaMemcpyAsync(h->pinned, h->small.p, sizeof(double), cudaMemcpyDeviceToHost, h->stream),
-     "memcpy");
+  ck(cudaMemcpyAsync(h->pinned + kScalarSlot, h->small.p + kScalarSlot, sizeof(double),
+                     cudaMemcpyDeviceToHost, h->stream), "memcpy");
   ck(cudaStreamSynchronize(h->stream), "sync");
-  return h->pinned[0];
+  return h->pinned[kScalarSlot];
 }
 
 // attaches a skip flag to every kernel the operator / preconditioner
@@ -502,10 +506,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     return e ? std::atof(e) : 1e-8;
   }();
 
-  const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[0]
+  const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[kScalarSlot]
   const double bnorm = std::sqrt(bb);
-  ck(cudaMemcpyAsync(h->small.p + 200, h->small.p, sizeof(double), cudaMemcpyDeviceToDevice,
-                     h->stream), "memcpy");
+  ck(cudaMemcpyAsync(h->small.p + 200, h->small.p + kScalarSlot, sizeof(double),
+                     cudaMemcpyDeviceToDevice, h->stream), "memcpy");
   if (bnorm == 0.0) {
     stg::vec_fill(x, 0.0, n, s);
     h->launches++;
@@ -664,6 +668,9 @@ struct NewtonOut {
 struct LinSys {
   Op A;
   Op P;
+  // every kernel A and P launch honours the skip flag and neither waits on
+  // the host: GMRES may enqueue Arnoldi steps speculatively
+  bool speculative = false;
 };
 
 // newton_solve (newton.hpp:102-130) on device vectors; u holds u0 on entry.
@@ -692,7 +699,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     h->launches++;  // du needs no zero fill: gmres(x_zero) writes it
     const GmresStats gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
                                 cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                                /*pipelined=*/!general_model(h->desc.model));
+                                /*pipelined=*/J.speculative);
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
@@ -919,6 +926,19 @@ double effective_fd_eps(const stg_handle* h, double fd_eps) {
 // fd_eps > 0, Euler always)
 bool uses_fd(const stg_handle* h, double fd_eps) {
   return !linear_model(h->desc.model) && effective_fd_eps(h, fd_eps) > 0.0;
+}
+
+// whether the Jacobian action is skip-aware and host-wait free (LinSys):
+// the slab kernels are; the general-model kernels and the unfused FD action
+// (host-side norms, plain vector kernels) are not
+bool jvp_speculative(const stg_handle* h, double fd_eps) {
+  if (general_model(h->desc.model)) return false;
+  if (!uses_fd(h, fd_eps)) return true;
+  stg::SlabArgs a{};
+  a.g = h->g;
+  a.model = h->desc.model;
+  a.n_in = a.n_out = h->nt;
+  return h->kernel_pref == STG_KERNEL_AUTO && stg::fd_fused_supported(a);
 }
 
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
@@ -1396,6 +1416,7 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
             st_jvp(h, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
+          L.speculative = jvp_speculative(h, eps);
           return L;
         },
         U, n, cfg);
@@ -1443,6 +1464,7 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
             stage_jvp(h, form, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
+          L.speculative = jvp_speculative(h, eps);
           return L;
         },
         U, n, cfg);
@@ -1774,7 +1796,7 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     const GmresStats st = gmres(
         h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
         restart, tol, max_it, P ? &P : nullptr, /*x_zero=*/false,
-        /*pipelined=*/!general_model(h->desc.model));
+        /*pipelined=*/jvp_speculative(h, 0.0));
     if (iterations) *iterations = st.iterations;
     if (rel_residual) *rel_residual = st.rel_residual;
     if (!st.converged)
