@@ -13,6 +13,7 @@
 //    the state and are rebuilt per Newton iteration from the exact
 //    linearisation.
 #include <algorithm>
+#include <type_traits>
 
 #include "kernels.hpp"
 
@@ -89,33 +90,40 @@ __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
 // Build and invert the element blocks of the 1-D Burgers slab / stage Jacobian
 // at U: column (j, q) = element response to a unit input at temporal node j,
 // node q (neighbour inputs zero; neighbour STATES enter through the exact
-// linearisation).  One warp per element: lane l < NB owns row l = (r, i) of
-// the block and of the identity, in registers.  Gauss-Jordan with partial
-// pivoting WITHOUT row exchanges: at column `col` the unused lane with the
-// largest |a[col]| (lowest lane on ties) becomes the pivot; its normalised
-// row is broadcast by shuffles and eliminated from every other lane.  At the
-// end the pivot lane of column col holds row col of the inverse.
+// linearisation).  Two elements per warp: lane (h, l) with l < NB owns row
+// l = (r, i) of element 2w + h's block and of the identity, in registers.
+// Gauss-Jordan with partial pivoting WITHOUT row exchanges: at column `col`
+// the unused lane of the half with the largest |a[col]| (lowest lane on
+// ties) becomes the pivot, normalises its row and publishes it through
+// shared memory (one 16-byte load per two entries for the other lanes,
+// instead of two 32-bit shuffles per entry); every other lane eliminates it.
+// At the end the pivot lane of column col holds row col of the inverse.
+// (One element per warp with shuffled rows took 853 us for the 65,536 c3
+// blocks.)
 template <int N1, int NT>
 __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict__ Binv,
                                                               const double* __restrict__ U,
                                                               const SlabArgs a) {
   pdl_entry();
   constexpr int NB = N1 * NT;
-  static_assert(NB <= 32, "one lane per block row");
-  const int lane = threadIdx.x & 31;
-  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  static_assert(NB <= 16 && NB % 2 == 0, "two elements per warp, even block size");
+  constexpr int PS = 2 * NB + 4;  // published-row stride (doubles): halves on different banks
+  __shared__ __align__(16) double pub[4][2][PS];
+  const int lane = threadIdx.x & 31, h = lane >> 4, l = lane & 15, wib = threadIdx.x >> 5;
   const int K = a.g.nx;
-  if (c >= K) return;  // warp-uniform
+  const int c = int(((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5) * 2 + h);
+  const bool live = c < K;
+  const int ce = live ? c : K - 1;  // dead half-warps mirror a live element (no stores)
   const long long ns = a.g.n_sdof;
-  const int cl = c == 0 ? K - 1 : c - 1, cr = c == K - 1 ? 0 : c + 1;
-  const bool act = lane < NB;
-  const int r = act ? lane / N1 : 0, i = act ? lane - (lane / N1) * N1 : 0;
+  const int cl = ce == 0 ? K - 1 : ce - 1, cr = ce == K - 1 ? 0 : ce + 1;
+  const bool act = l < NB;
+  const int r = act ? l / N1 : 0, i = act ? l - (l / N1) * N1 : 0;
   double row[NB], inv[NB];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     double u[N1];
 #pragma unroll
-    for (int k = 0; k < N1; ++k) u[k] = U[j * ns + (long long)c * N1 + k];
+    for (int k = 0; k < N1; ++k) u[k] = U[j * ns + (long long)ce * N1 + k];
     const double ul = U[j * ns + (long long)cl * N1 + N1 - 1];
     const double ur = U[j * ns + (long long)cr * N1];
 #pragma unroll
@@ -125,7 +133,7 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
 #pragma unroll
       for (int k = 0; k < N1; ++k) {
         const double dvi = (i == q ? 1.0 : 0.0), dvk = (k == q ? 1.0 : 0.0);
-        vol += 2.0 * a.sp.Dm[i][k] * ((2.0 * u[i] + u[k]) * dvi + (u[i] + 2.0 * u[k]) * dvk) / 6.0;
+        vol += a.sp.Dm[i][k] * ((2.0 * u[i] + u[k]) * dvi + (u[i] + 2.0 * u[k]) * dvk) * (1.0 / 3.0);
       }
       double g = -a.sp.sc * vol;
       if (i == N1 - 1 && q == N1 - 1) {  // d/duL of LLF(uL, ur) - f(uL), right face
@@ -147,16 +155,17 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
     }
   }
 #pragma unroll
-  for (int q = 0; q < NB; ++q) inv[q] = (q == lane) ? 1.0 : 0.0;
+  for (int q = 0; q < NB; ++q) inv[q] = (q == l) ? 1.0 : 0.0;
   bool used = !act;
   int my_col = 0;
+  double* P = pub[wib][h];
 #pragma unroll
   for (int col = 0; col < NB; ++col) {
-    // pivot lane: max |row[col]| among unused lanes, lowest lane on ties
+    // pivot lane of this half: max |row[col]| among unused lanes, lowest lane on ties
     double v = used ? -1.0 : fabs(row[col]);
-    int idx = lane;
+    int idx = l;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 8; o > 0; o >>= 1) {
       const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
       const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
       if (v2 > v || (v2 == v && i2 < idx)) {
@@ -164,32 +173,40 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
         idx = i2;
       }
     }
-    const int p = idx;
-    const double ip = 1.0 / __shfl_sync(0xffffffffu, row[col], p);
-    if (lane == p) {
+    const double f = row[col];
+    if (l == idx) {
+      const double ip = 1.0 / f;
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
         row[q] *= ip;
         inv[q] *= ip;
       }
+#pragma unroll
+      for (int q = 0; q < NB; q += 2) {
+        *reinterpret_cast<double2*>(P + q) = make_double2(row[q], row[q + 1]);
+        *reinterpret_cast<double2*>(P + NB + q) = make_double2(inv[q], inv[q + 1]);
+      }
       used = true;
       my_col = col;
     }
-    const double f = row[col];
+    __syncwarp();
+    if (l != idx) {
 #pragma unroll
-    for (int q = 0; q < NB; ++q) {
-      const double pr = __shfl_sync(0xffffffffu, row[q], p);
-      const double pi = __shfl_sync(0xffffffffu, inv[q], p);
-      if (lane != p) {
-        row[q] = fma(-f, pr, row[q]);
-        inv[q] = fma(-f, pi, inv[q]);
+      for (int q = 0; q < NB; q += 2) {
+        const double2 pr = *reinterpret_cast<const double2*>(P + q);
+        const double2 pi = *reinterpret_cast<const double2*>(P + NB + q);
+        row[q] = fma(-f, pr.x, row[q]);
+        row[q + 1] = fma(-f, pr.y, row[q + 1]);
+        inv[q] = fma(-f, pi.x, inv[q]);
+        inv[q + 1] = fma(-f, pi.y, inv[q + 1]);
       }
     }
+    __syncwarp();  // the published row is consumed before the next pivot writes
   }
-  if (act) {  // stored in fp32: a preconditioner; GMRES itself stays fp64
+  if (act && live) {  // stored in fp32: a preconditioner; GMRES itself stays fp64
     float* M = Binv + (size_t)c * NB * NB + (size_t)my_col * NB;
 #pragma unroll
-    for (int q = 0; q < NB; ++q) M[q] = float(inv[q]);
+    for (int q = 0; q < NB; q += 2) *reinterpret_cast<float2*>(M + q) = make_float2(float(inv[q]), float(inv[q + 1]));
   }
 }
 
@@ -461,14 +478,23 @@ __global__ void __launch_bounds__(128) k_gen_eblock(double* __restrict__ Binv,
 
 template <int N1>
 bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
-  const long long threads = (long long)a.g.nx * 32;  // one warp per element
-  const int blocks = int((threads + 127) / 128);
+  const long long warps = ((long long)a.g.nx + 1) / 2;  // two elements per warp
+  const int blocks = int((warps * 32 + 127) / 128);
+  auto go = [&](auto nt_tag) {
+    constexpr int NT = decltype(nt_tag)::value;
+    if constexpr (N1 * NT <= 16 && (N1 * NT) % 2 == 0) {
+      launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, NT>, blocks, 128, 0, s, Binv, U, a);
+      return true;
+    } else {
+      return false;  // the fp32 block apply takes n_tau * (N+1) <= 16, even
+    }
+  };
   switch (a.n_in) {
-    case 2: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 2>, blocks, 128, 0, s, Binv, U, a); return true;
-    case 3: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 3>, blocks, 128, 0, s, Binv, U, a); return true;
-    case 4: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 4>, blocks, 128, 0, s, Binv, U, a); return true;
-    case 5: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 5>, blocks, 128, 0, s, Binv, U, a); return true;
-    case 6: launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, 6>, blocks, 128, 0, s, Binv, U, a); return true;
+    case 2: return go(std::integral_constant<int, 2>{});
+    case 3: return go(std::integral_constant<int, 3>{});
+    case 4: return go(std::integral_constant<int, 4>{});
+    case 5: return go(std::integral_constant<int, 5>{});
+    case 6: return go(std::integral_constant<int, 6>{});
     default: return false;
   }
 }
