@@ -168,6 +168,9 @@ struct SlabArgs {
   // launch without programmatic serialisation (the launch follows a
   // cross-stream event wait, which PDL must not relax)
   int no_pdl;
+  // X and R in element-major order [cell][t][node] (d = 2 plane kernel only;
+  // the dense element-block preconditioner's layout)
+  int em;
 };
 // true if the d = 1 lane kernel handles fused FD Jacobian actions for a
 bool fd_fused_supported(const SlabArgs& a);
@@ -175,6 +178,8 @@ bool fd_fused_supported(const SlabArgs& a);
 // ---- launchers (kernels_slab.cu) -------------------------------------------
 // Returns the number of kernels launched (>= 1) or -1 if no kernel fits.
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
+// whether the element-major (a.em) variant applies to these arguments
+bool slab_em_supported(const SlabArgs& a);
 // Fast TMA path: d = 3, n = 4, n_in = n_out = 4, advection, nx % 8 == 0.
 bool slab_fast_supported(const SlabArgs& a);
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s);

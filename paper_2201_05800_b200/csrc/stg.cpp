@@ -131,6 +131,10 @@ struct stg_handle {
   int* mapped = nullptr;
   cudaEvent_t ev_step[2] = {}, ev_re = nullptr;
   stg::Skip skip{};
+  // slab vectors handed to the operator / preconditioner are element-major
+  // (set around a d = 2 GMRES solve with the dense element block, see newton)
+  int em = 0;
+  DevBuf emb, emx;  // element-major right-hand side and solution
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
   static constexpr int kChunks = 8;
   cudaStream_t s_in = nullptr, s_out = nullptr;
@@ -220,6 +224,7 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   a.W = W;
   a.R = R;
   a.skip = h->skip;
+  a.em = h->em;
   if (general_model(h->desc.model)) {
     apply_general(h, mx, n_in, n_out, X, W, R);
     return;
@@ -671,6 +676,17 @@ struct LinSys {
   // every kernel A and P launch honours the skip flag and neither waits on
   // the host: GMRES may enqueue Arnoldi steps speculatively
   bool speculative = false;
+  // A and P also run on element-major vectors (d = 2 dense element block):
+  // the solve is done in that layout, with one permute each way
+  bool element_major = false;
+};
+
+// sets the handle's element-major mode for the operator / preconditioner
+// launches made while in scope
+struct EmScope {
+  stg_handle* h;
+  explicit EmScope(stg_handle* hh) : h(hh) { h->em = 1; }
+  ~EmScope() { h->em = 0; }
 };
 
 // newton_solve (newton.hpp:102-130) on device vectors; u holds u0 on entry.
@@ -697,9 +713,25 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     const LinSys J = jacobian(u);
     stg::vec_axpby(r, 0.0, r, -1.0, n, h->stream);  // r = -r
     h->launches++;  // du needs no zero fill: gmres(x_zero) writes it
-    const GmresStats gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol,
-                                cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                                /*pipelined=*/J.speculative);
+    GmresStats gs;
+    if (J.element_major) {  // solve in the preconditioner's layout
+      const int nt = h->nt, npc = h->g.npc;
+      const long long ns = h->n_sdof;
+      h->emb.ensure(size_t(n));
+      h->emx.ensure(size_t(n));
+      stg::permute_to_elem(h->emb.p, r, nt, npc, ns, h->stream);
+      {
+        EmScope scope(h);
+        gs = gmres(h, J.A, h->emb.p, h->emx.p, n, cfg.gmres_restart, cfg.gmres_tol,
+                   cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
+                   /*pipelined=*/J.speculative);
+      }
+      stg::permute_from_elem(du, h->emx.p, nt, npc, ns, h->stream);
+      h->launches += 2;
+    } else {
+      gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
+                 J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/J.speculative);
+    }
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
@@ -1080,6 +1112,25 @@ int resolve_precond(const stg_handle* h, int kind) {
   return kind;
 }
 
+// whether a d = 2 linear solve can run element-major: the dense element
+// block preconditioner with the plane kernel for the Jacobian action
+// (S diagonal: the slab and A^-1-form stage Jacobians)
+bool element_major_ok(const stg_handle* h, int precond, bool full_s) {
+  static const bool off = std::getenv("STG_NO_ELEMENT_MAJOR") != nullptr ||
+                          std::getenv("STG_DENSE_OWN_KERNEL") != nullptr;
+  if (off || h->desc.dim != 2 || h->desc.model != STG_MODEL_ADVECTION || full_s) return false;
+  if (!dense2d_ok(h) || resolve_precond(h, precond) != STG_PRECOND_EBLOCK) return false;
+  stg::SlabArgs a{};
+  a.g = h->g;
+  a.model = h->desc.model;
+  a.n_in = a.n_out = h->nt;
+  static double aligned_probe[2] __attribute__((aligned(16)));  // only its alignment is read
+  a.X = aligned_probe;
+  a.R = aligned_probe;
+  a.em = 1;
+  return stg::slab_em_supported(a);
+}
+
 // d = 2 dense element block: out = B in for every element.  A plain GEMM
 // (nb x nb) x (nb x n_cells) on the element-major copy of the vector: permute
 // (own kernel), cuBLAS DGEMM, permute back.  STG_DENSE_OWN_KERNEL=1 uses the
@@ -1095,14 +1146,21 @@ Op dense_op(stg_handle* h, const double* tab, int nt, int npc, int ncells, long 
     }
     const int nb = nt * npc;
     const size_t n = size_t(ns) * nt;
-    h->pz1.ensure(n);
-    h->pz2.ensure(n);
     if (!h->cublas && cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS)
       throw CudaError("cublasCreate failed");
     cublasSetStream(h->cublas, h->stream);
-    stg::permute_to_elem(h->pz1.p, in, nt, npc, ns, h->stream, h->skip);
     const double one = 1.0, zero = 0.0;
     // column-major: Yp (nb x cells) = B Xp; the row-major B is op(T) of its buffer
+    if (h->em) {  // vectors already element-major: the GEMM alone
+      if (cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, nb, ncells, nb, &one, tab, nb, in, nb,
+                      &zero, out, nb) != CUBLAS_STATUS_SUCCESS)
+        throw CudaError("cublasDgemm failed");
+      h->launches++;
+      return;
+    }
+    h->pz1.ensure(n);
+    h->pz2.ensure(n);
+    stg::permute_to_elem(h->pz1.p, in, nt, npc, ns, h->stream, h->skip);
     if (cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, nb, ncells, nb, &one, tab, nb, h->pz1.p,
                     nb, &zero, h->pz2.p, nb) != CUBLAS_STATUS_SUCCESS)
       throw CudaError("cublasDgemm failed");
@@ -1417,6 +1475,7 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
           };
           L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
           L.speculative = jvp_speculative(h, eps);
+          L.element_major = element_major_ok(h, cfg.precond, false);
           return L;
         },
         U, n, cfg);
@@ -1465,6 +1524,7 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
           };
           L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
           L.speculative = jvp_speculative(h, eps);
+          L.element_major = element_major_ok(h, cfg.precond, form == STG_FORM_A);
           return L;
         },
         U, n, cfg);

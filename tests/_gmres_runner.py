@@ -28,6 +28,18 @@ def main(out: str) -> None:
         U, _, info = op.stdg_step(0.0, cfg.dt, un, nc)
         res[name] = U.cpu().numpy()
         res[name + "_its"] = np.array([info.newton_iterations, info.linear_iterations])
+    # c2 physics on 32 x 8 cells: the dense element block, solved element-major
+    c2 = C.CONFIGS["c2"].scaled((32, 8))
+    op2 = SlabOperator(**c2.kwargs())
+    u2 = torch.as_tensor(C.initial_state(c2), device="cuda")
+    U2, _, info2 = op2.stdg_step(0.0, c2.dt, u2, NewtonConfig(abs_tol=0.0, rel_tol=1e-11,
+                                                             gmres_tol=1e-12))
+    res["c2"] = U2.cpu().numpy()
+    res["c2_its"] = np.array([info2.newton_iterations, info2.linear_iterations])
+    U2s, _, _ = op2.rk_step(L.STG_FORM_A_INV, 0.0, c2.dt, u2,
+                            NewtonConfig(abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12))
+    res["c2rk"] = U2s.cpu().numpy()
+    res["c2rk_its"] = np.array([0, 0])
     # plain linear solve through the ABI entry (non-zero initial guess)
     rng = np.random.default_rng(5)
     b = torch.as_tensor(rng.uniform(-1, 1, cfg.n_dof), device="cuda")

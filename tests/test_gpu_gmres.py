@@ -11,7 +11,9 @@ tests check the mechanisms one by one:
   and with programmatic dependent launch off (STG_NO_PDL=1): neither changes
   any arithmetic;
 * forcing the second Gram-Schmidt pass on every step
-  (STG_GMRES_REORTH_TOL=0.5) gives the same converged solutions.
+  (STG_GMRES_REORTH_TOL=0.5) gives the same converged solutions;
+* the element-major d = 2 solve (dense element block) matches the
+  stage-major one (STG_NO_ELEMENT_MAJOR=1) and the oracle.
 The knobs are read once per process, so each variant is a subprocess
 (tests/_gmres_runner.py).  The forced-second-pass run found a real bug: a
 Jacobian action that reduces into the step's scratch (the unfused FD J.v)
@@ -33,7 +35,7 @@ pytestmark = pytest.mark.gpu
 
 RUNNER = Path(__file__).with_name("_gmres_runner.py")
 TOL_SOLVE = 1e-10
-KEYS = ["fdm30", "fdm3", "tblock4", "none30", "gmres_st", "c3", "c3f"]
+KEYS = ["fdm30", "fdm3", "tblock4", "none30", "gmres_st", "c3", "c3f", "c2", "c2rk"]
 
 
 def run(tmp_path_factory, **env):
@@ -100,3 +102,22 @@ def test_forced_reorthogonalisation_same_solutions(base, tmp_path_factory):
     other = run(tmp_path_factory, STG_GMRES_REORTH_TOL="0.5")
     for k in KEYS:
         assert rel(other[k], base[k]) <= TOL_SOLVE, k
+
+
+def test_element_major_solve_matches_stage_major(base, tmp_path_factory):
+    # d = 2 with the dense element block solves in element-major order (one
+    # permute each way per Newton step instead of two per preconditioner
+    # apply); the stage-major path is the reference
+    other = run(tmp_path_factory, STG_NO_ELEMENT_MAJOR="1")
+    for k in ["c2", "c2rk"]:
+        assert rel(other[k], base[k]) <= TOL_SOLVE, k
+    assert base["c2_its"][1] == other["c2_its"][1]
+
+
+def test_c2_solve_matches_oracle(base):
+    cfg = C.CONFIGS["c2"].scaled((32, 8))
+    pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
+                   list(cfg.velocity), n_tau=cfg.n_tau)
+    Uo, _, _, _ = pr.stdg_step(0.0, cfg.dt, C.initial_state(cfg), linear=O.GMRES, abs_tol=0.0,
+                               rel_tol=1e-12, gmres_tol=1e-13)
+    assert rel(base["c2"], Uo) <= TOL_SOLVE
