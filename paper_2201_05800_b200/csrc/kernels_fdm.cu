@@ -210,8 +210,8 @@ __device__ __forceinline__ void fdm_phase_a2(const FdmCoef& c, const double* B1,
 
 template <int MINB>
 __global__ void __launch_bounds__(THREADS, MINB)
-    fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ FdmCoef c,
-               const Geometry g, double* __restrict__ out, const Skip skip) {
+    fdm_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_out,
+               const __grid_constant__ FdmCoef c, const Geometry g, const Skip skip) {
   pdl_entry();
   if (skip_now(skip)) return;
   extern __shared__ unsigned char smem_raw[];
@@ -221,7 +221,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + OFF_BAR);
   const uint32_t bar0 = ptxh::smem_u32(bars), bar1 = ptxh::smem_u32(bars + 1);
   const int tid = threadIdx.x;
-  const long long ns = g.n_sdof;
   const int nseg = g.n_cells / E;
 
   for (int q = tid; q < 4 * 4 * 4 * 2 * 2; q += THREADS)
@@ -249,8 +248,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
 
   for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
     const int st = it & 1;
-    const double* Xs = reinterpret_cast<const double*>(base + st * TILE);
+    double* Xs = reinterpret_cast<double*>(base + st * TILE);
     if (tid == 0 && seg + (int)gridDim.x < nseg) {
+      // stage st^1 last held the previous segment's result: its bulk store
+      // must have read it before the next load overwrites it
+      ptxh::bulk_wait_read0();
       ptxh::fence_proxy_async_smem();
       issue(seg + gridDim.x, st ^ 1);
     }
@@ -270,15 +272,25 @@ __global__ void __launch_bounds__(THREADS, MINB)
     fdm_phase_b(c, B1, LI, hB, eB, qB);
     __syncthreads();
     {
+      // the result row goes back into the (consumed) input stage, in the
+      // same swizzled box layout, and leaves by one TMA tensor store: full
+      // 128-byte lines instead of 16-byte stores 128 bytes apart (which made
+      // the L2 fetch every output sector from DRAM before merging)
       double o[16];
       fdm_phase_a2(c, B1, rowA, swA, o);
-      double* op = out + tA * ns + (long long)(seg * E + eA) * 64 + zA * 16;
 #pragma unroll
       for (int q = 0; q < 8; ++q)
-        *reinterpret_cast<double2*>(op + 2 * q) = make_double2(o[2 * q], o[2 * q + 1]);
+        *reinterpret_cast<double2*>(Xs + rowA * 16 + ((q ^ swA) << 1)) =
+            make_double2(o[2 * q], o[2 * q + 1]);
     }
-    __syncthreads();  // stage st and B1 free for reuse
+    ptxh::fence_proxy_async_smem();
+    __syncthreads();  // result tile complete; B1 free for reuse
+    if (tid == 0) {
+      ptxh::tma_store_4d(&tm_out, ptxh::smem_u32(Xs), 0, 0, seg * E, 0);
+      ptxh::bulk_commit();
+    }
   }
+  if (tid == 0) ptxh::bulk_wait0();
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -322,6 +334,11 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
+  CUtensorMap map_out;
+  if (enc(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, out, gdim, gstride, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
   // 3 CTAs/SM (144 registers, no spills) by default; STG_FDM_MINB=4 trades a
   // small spill for a fourth CTA
   static const bool four = [] {
@@ -341,7 +358,7 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
   const int nseg = g.n_cells / E;
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
-  launch_ex(kPdlFdm, kern, grid, THREADS, SMEM, s, map, coef, g, out, skip);
+  launch_ex(kPdlFdm, kern, grid, THREADS, SMEM, s, map, map_out, coef, g, skip);
   return 1;
 }
 
