@@ -114,14 +114,14 @@ inline void launch_ex(int pdl_cls, void (*kernel)(KArgs...), dim3 grid, dim3 blo
 // reduced by Givens rotations, the rotations, the rotated right-hand side g,
 // the inverse norms c_j = 1/||S_j|| of the stored basis vectors, and the
 // cycle status: 0 running, 1 residual estimate <= tol_abs, 2 breakdown,
-// 3 the last step needs a second Gram-Schmidt pass.
+// 3 the last step needs a second Gram-Schmidt pass, 4 nothing to do (b = 0).
 constexpr int kGmresMaxRestart = 60;
 struct GmresDev {
   double H[(kGmresMaxRestart + 1) * kGmresMaxRestart];  // H(i,j) at i*m + j
   double cs[kGmresMaxRestart], sn[kGmresMaxRestart];
   double g[kGmresMaxRestart + 1];
   double cn[kGmresMaxRestart + 1];
-  double tol_abs, reorth_tol, est;
+  double tol_abs, reorth_tol, est, bnorm;
   int m, status, k_done, pad;
 };
 // The Givens step of Arnoldi step k, run by the last block of the update
@@ -136,8 +136,11 @@ struct GivensArgs {
   const double* sc1 = nullptr;  // scale applied by pass 0 (pass 1 reads it)
   int* host = nullptr;          // mapped pinned per-step status slots
 };
-void gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol, double* hn2_0,
-                cudaStream_t s);
+// bb != null: beta = sqrt(*bb) on the device and tol is relative (first
+// cycle from x = 0, no host round trip); else beta and tol_abs = tol given.
+// beta = 0 sets status 4 ("no work") and writes it to every host slot.
+void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,
+                double* hn2_0, int* host, cudaStream_t s);
 
 struct SlabArgs {
   SpatialCoef sp;
@@ -317,9 +320,9 @@ void vec_update_dot(double* w, const double* V, long long ldv, int k, const doub
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
                     const double* scale_src = nullptr, double* scale_out = nullptr,
                     const double* hn2 = nullptr, Skip skip = {}, GivensArgs gv = {});
-// y = x / sqrt(*nrm2)  (nrm2 on device)
+// y = sign * x / sqrt(*nrm2)  (nrm2 on device)
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
-                       cudaStream_t s);
+                       cudaStream_t s, double sign = 1.0);
 // x = (accumulate ? x : 0) + sum_{j<k} y[j] V_j (y on device), k <= 64
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
                  cudaStream_t s, bool accumulate = true);

@@ -60,12 +60,23 @@ __global__ void k_broadcast(double* __restrict__ U, const double* __restrict__ u
     for (int j = 0; j < nb; ++j) U[j * n + i] = v;
   }
 }
-__global__ void k_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n) {
+__global__ void k_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
+                                double sign, int vec2) {
   pdl_entry();
-  const double s = 1.0 / sqrt(nrm2[0]);
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    y[i] = x[i] * s;
+  const double s = sign / sqrt(nrm2[0]);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (vec2) {  // 16-byte accesses (both vectors 16-byte aligned)
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    double2* y2 = reinterpret_cast<double2*>(y);
+    for (long long i = i0; i < n / 2; i += stride) {
+      const double2 v = __ldcs(x2 + i);
+      __stcs(y2 + i, make_double2(v.x * s, v.y * s));
+    }
+    if (i0 == 0 && (n & 1)) y[n - 1] = x[n - 1] * s;
+  } else {
+    for (long long i = i0; i < n; i += stride) y[i] = x[i] * s;
+  }
 }
 
 // ---- multi-vector kernels: thread-per-chunk.  Each thread owns W
@@ -239,11 +250,22 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
     gmres_givens(gv, scale_src, s, hn2, out[0]);
 }
 
-__global__ void k_gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol,
-                             double* hn2_0) {
+__global__ void k_gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol,
+                             double reorth_tol, double* hn2_0, int* host) {
   pdl_entry();
+  double tol_abs = tol;
+  if (bb) {  // first cycle from x = 0: ||r|| = ||b|| is only known here
+    beta = sqrt(*bb);
+    G->bnorm = beta;
+    tol_abs = tol * beta;
+  }
   G->m = m;
   G->status = 0;
+  if (!(beta > 0.0)) {  // b = 0: nothing to do; every step slot reads "no work"
+    G->status = 4;
+    for (int j = 0; j <= m; ++j) reinterpret_cast<volatile int*>(host)[j] = 4;
+    __threadfence_system();
+  }
   G->k_done = 0;
   G->est = beta;
   G->tol_abs = tol_abs;
@@ -323,8 +345,10 @@ void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t
   launch_ex(vec_pdl(n), k_broadcast, grid_for(n), kBlock, 0, s, U, u, nb, n);
 }
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
-                       cudaStream_t s) {
-  launch_ex(vec_pdl(n), k_scale_invsqrt, grid_for(n), kBlock, 0, s, y, x, nrm2, n);
+                       cudaStream_t s, double sign) {
+  const int v2 = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15) == 0;
+  launch_ex(vec_pdl(n), k_scale_invsqrt, grid_for(v2 ? n / 2 + 1 : n), kBlock, 0, s, y, x, nrm2,
+            n, sign, v2);
 }
 
 namespace {
@@ -404,9 +428,9 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
                                                       skip)));
 }
 
-void gmres_init(GmresDev* G, int m, double beta, double tol_abs, double reorth_tol, double* hn2_0,
-                cudaStream_t s) {
-  launch_ex(kPdlVec, k_gmres_init, 1, 1, 0, s, G, m, beta, tol_abs, reorth_tol, hn2_0);
+void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,
+                double* hn2_0, int* host, cudaStream_t s) {
+  launch_ex(kPdlVec, k_gmres_init, 1, 1, 0, s, G, m, bb, beta, tol, reorth_tol, hn2_0, host);
 }
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,

@@ -470,7 +470,7 @@ struct GmresStats {
 // k+1.  lag 0 (pipelined = false, or STG_GMRES_SYNC=1) waits after every step.
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
-                 bool pipelined = true) {
+                 bool pipelined = true, double b_sign = 1.0) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > stg::kGmresMaxRestart) throw std::invalid_argument("gmres: restart <= 60");
@@ -511,15 +511,26 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     return e ? std::atof(e) : 1e-8;
   }();
 
-  const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[kScalarSlot]
-  const double bnorm = std::sqrt(bb);
-  ck(cudaMemcpyAsync(h->small.p + 200, h->small.p + kScalarSlot, sizeof(double),
-                     cudaMemcpyDeviceToDevice, h->stream), "memcpy");
-  if (bnorm == 0.0) {
-    stg::vec_fill(x, 0.0, n, s);
+  // The right-hand side is b_sign * b.  From x = 0 with tol < 1, ||b|| stays
+  // on the device for the first cycle (S_0 = b / ||b|| and the stopping
+  // threshold are formed there): no host round trip before the first step.
+  // Otherwise it is read back here.
+  const bool defer = x_zero && tol < 1.0;
+  double bnorm = -1.0;  // < 0: not known on the host yet
+  if (defer) {
+    stg::vec_dot(b, b, n, h->partial.p, dsm + 200, s);
     h->launches++;
-    st.converged = true;
-    return st;
+  } else {
+    const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[kScalarSlot]
+    bnorm = std::sqrt(bb);
+    ck(cudaMemcpyAsync(h->small.p + 200, h->small.p + kScalarSlot, sizeof(double),
+                       cudaMemcpyDeviceToDevice, h->stream), "memcpy");
+    if (bnorm == 0.0) {
+      stg::vec_fill(x, 0.0, n, s);
+      h->launches++;
+      st.converged = true;
+      return st;
+    }
   }
   const stg::Skip run0{&G->status, 0}, run_re{&G->status, 3};
   // Arnoldi step k: S_{k+1} <- A P^-1 S_k, then the two fused passes; the
@@ -574,14 +585,14 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   bool first = true;
   bool x_set = !x_zero;  // x_zero: x is written (not accumulated) by the first update
   while (true) {
-    double beta;
+    double beta = -1.0;  // < 0: on the device only (deferred first cycle)
     if (first && x_zero) {  // x = 0: r = b and ||r|| = ||b|| (no operator apply, no sync)
-      stg::vec_scale_invsqrt(V, b, dsm + 200, n, s);  // S_0 = b / ||b|| (dsm[200] = <b,b>)
+      stg::vec_scale_invsqrt(V, b, dsm + 200, n, s, b_sign);  // S_0 = b / ||b|| (dsm[200] = <b,b>)
       h->launches++;
-      beta = bnorm;
+      if (!defer) beta = bnorm;
     } else {
       A(x, w);                                   // w = A x
-      stg::vec_axpby(w, 1.0, b, -1.0, n, s);     // w = b - A x
+      stg::vec_axpby(w, b_sign, b, -1.0, n, s);  // w = b - A x
       h->launches++;
       stg::vec_multidot(w, 0, 1, w, n, h->partial.p, dsm + 200, s);
       h->launches += 1;
@@ -593,15 +604,20 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       beta = std::sqrt(hp[200]);
     }
     first = false;
-    st.rel_residual = beta / bnorm;
-    if (st.rel_residual <= tol) {
-      st.converged = true;
-      break;
+    if (beta >= 0.0) {
+      st.rel_residual = beta / bnorm;
+      if (st.rel_residual <= tol) {
+        st.converged = true;
+        break;
+      }
     }
     if (total >= max_it) break;
-    stg::gmres_init(G, m, beta, tol * bnorm, reorth_tol, dsm + 64, s);
-    h->launches++;
     for (int j = 0; j <= m; ++j) mapped[j] = -1;  // per-step status slots
+    if (beta >= 0.0)
+      stg::gmres_init(G, m, nullptr, beta, tol * bnorm, reorth_tol, dsm + 64, mapped_dev, s);
+    else
+      stg::gmres_init(G, m, dsm + 200, 0.0, tol, reorth_tol, dsm + 64, mapped_dev, s);
+    h->launches++;
     auto can_enqueue = [&](int j) { return j < m && total + j < max_it; };
     int k = 0, enq = 0, status = 0;
     while (true) {
@@ -612,6 +628,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       if (k >= enq) break;  // end of the cycle (restart length or max_it)
       ck(cudaEventSynchronize(h->ev_step[k & 1]), "sync");  // step k done
       status = mapped[k];
+      if (status == 4) break;  // b = 0 (deferred norm): no step ran
       if (status == 3) {  // step k needs a second Gram-Schmidt pass
         enqueue_reorth(k);
         h->reorth++;
@@ -628,6 +645,12 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     ck(cudaMemcpyAsync(h->gpin, G, sizeof(stg::GmresDev), cudaMemcpyDeviceToHost, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");
     const stg::GmresDev& Gh = *h->gpin;
+    if (bnorm < 0.0) bnorm = Gh.bnorm;  // deferred first cycle
+    if (status == 4 || bnorm == 0.0) {   // b = 0: x = 0
+      st.converged = true;
+      st.rel_residual = 0.0;
+      break;
+    }
     if (Gh.k_done != k) throw std::runtime_error("gmres: device step count mismatch");
     for (int i = k - 1; i >= 0; --i) {
       double acc = Gh.g[i];
@@ -711,8 +734,8 @@ NewtonOut newton(stg_handle* h, const Op& residual,
                                     fmt_short(norm),
                                 out.history);
     const LinSys J = jacobian(u);
-    stg::vec_axpby(r, 0.0, r, -1.0, n, h->stream);  // r = -r
-    h->launches++;  // du needs no zero fill: gmres(x_zero) writes it
+    // J du = -r: the sign is folded into GMRES (b_sign = -1); du needs no
+    // zero fill (gmres with x_zero writes it)
     GmresStats gs;
     if (J.element_major) {  // solve in the preconditioner's layout
       const int nt = h->nt, npc = h->g.npc;
@@ -724,13 +747,14 @@ NewtonOut newton(stg_handle* h, const Op& residual,
         EmScope scope(h);
         gs = gmres(h, J.A, h->emb.p, h->emx.p, n, cfg.gmres_restart, cfg.gmres_tol,
                    cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                   /*pipelined=*/J.speculative);
+                   /*pipelined=*/J.speculative, /*b_sign=*/-1.0);
       }
       stg::permute_from_elem(du, h->emx.p, nt, npc, ns, h->stream);
       h->launches += 2;
     } else {
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
-                 J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/J.speculative);
+                 J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/J.speculative,
+                 /*b_sign=*/-1.0);
     }
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
