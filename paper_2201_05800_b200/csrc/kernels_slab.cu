@@ -247,8 +247,16 @@ __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
     }
   }
   if (out_lane) {
+    double* Rj = a.R + j * ns + oc;
+    if (N1 % 2 == 0 && (reinterpret_cast<uintptr_t>(Rj) & 15) == 0) {
+      // 16-byte stores: each lane's row is one or more whole 32-byte sectors
 #pragma unroll
-    for (int i = 0; i < N1; ++i) a.R[j * ns + oc + i] = acc[i];
+      for (int i = 0; i + 1 < N1; i += 2)
+        *reinterpret_cast<double2*>(Rj + i) = make_double2(acc[i], acc[i + 1]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < N1; ++i) Rj[i] = acc[i];
+    }
   }
 }
 
