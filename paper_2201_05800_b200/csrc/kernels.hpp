@@ -141,6 +141,8 @@ struct GivensArgs {
 // beta = 0 sets status 4 ("no work") and writes it to every host slot.
 void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,
                 double* hn2_0, int* host, cudaStream_t s);
+// out[j] = y_j c_j, y = R^-1 g over the first k columns (the cycle's update)
+void gmres_backsub(const GmresDev* G, int k, double* out, cudaStream_t s);
 
 struct SlabArgs {
   SpatialCoef sp;
@@ -167,6 +169,9 @@ struct SlabArgs {
   const double* fdv;
   const double* fd_vv;
   double fd_c;
+  // fd_uu != null: e = fd_c * sqrt(1 + sqrt(*fd_uu)) / sqrt(*fd_vv), with
+  // fd_uu = <U,U> also on the device (fd_c then holds fd_eps)
+  const double* fd_uu;
   Skip skip;
   // launch without programmatic serialisation (the launch follows a
   // cross-stream event wait, which PDL must not relax)

@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
   if (act && j < a.n_in && a.fdv) {
     // fused central difference: x <- v, G <- [F(U + e v) - F(U - e v)] / 2e
     const double vv = *a.fd_vv;
-    const double e = vv > 0.0 ? a.fd_c / sqrt(vv) : 1.0;
+    const double c = a.fd_uu ? a.fd_c * sqrt(1.0 + sqrt(*a.fd_uu)) : a.fd_c;
+    const double e = vv > 0.0 ? c / sqrt(vv) : 1.0;
     const double* Uj = a.X + j * ns;
     const double* vj = a.fdv + j * ns;
     double up[N1], um[N1], Gp[N1], Gm[N1];

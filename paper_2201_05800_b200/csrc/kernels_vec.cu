@@ -276,6 +276,21 @@ __global__ void k_gmres_init(GmresDev* G, int m, const double* bb, double beta, 
   if (hn2_0) *hn2_0 = 1.0;  // ||S_0||^2 = 1 (S_0 = r / ||r||)
 }
 
+// y = R^-1 g over the first k Givens-reduced Hessenberg columns, scaled by
+// the basis norms (out[j] = y_j c_j: x += sum out_j S_j); one thread, k <= 60
+__global__ void k_gmres_backsub(const GmresDev* G, int k, double* out) {
+  pdl_entry();
+  if (threadIdx.x != 0) return;
+  const int m = G->m;
+  double y[kGmresMaxRestart];
+  for (int i = k - 1; i >= 0; --i) {
+    double acc = G->g[i];
+    for (int j = i + 1; j < k; ++j) acc -= G->H[i * m + j] * y[j];
+    y[i] = acc / G->H[i * m + i];
+  }
+  for (int j = 0; j < k; ++j) out[j] = y[j] * G->cn[j];
+}
+
 __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x, long long n,
                                                    double* part, double* out,
                                                    unsigned* counter) {
@@ -426,6 +441,10 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
   STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_multidot<KM, WW>, multi_grid<KM, WW, false>(n), kVecBlock,
                                               0, s, V, ldv, k, w, n / WW, partial, out, c,
                                                       skip)));
+}
+
+void gmres_backsub(const GmresDev* G, int k, double* out, cudaStream_t s) {
+  launch_ex(kPdlVec, k_gmres_backsub, 1, 32, 0, s, G, k, out);
 }
 
 void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,

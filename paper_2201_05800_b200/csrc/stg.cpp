@@ -470,7 +470,7 @@ struct GmresStats {
 // k+1.  lag 0 (pipelined = false, or STG_GMRES_SYNC=1) waits after every step.
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
-                 bool pipelined = true, double b_sign = 1.0) {
+                 bool pipelined = true, double b_sign = 1.0, bool want_rel = true) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > stg::kGmresMaxRestart) throw std::invalid_argument("gmres: restart <= 60");
@@ -642,6 +642,17 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     }
     // stream order: any speculative launches after step k - 1 are no-ops
     total += k;
+    if (status == 1 && !want_rel) {
+      // converged and the caller does not read the residual estimate: the
+      // back substitution and the update run on the device, no round trip
+      stg::gmres_backsub(G, k, dsm + 256, s);
+      stg::vec_combine(x, P ? Z : V, ld, k, dsm + 256, n, s, x_set);
+      h->launches += 2;
+      x_set = true;
+      st.converged = true;
+      st.rel_residual = -1.0;  // not read back
+      break;
+    }
     ck(cudaMemcpyAsync(h->gpin, G, sizeof(stg::GmresDev), cudaMemcpyDeviceToHost, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");
     const stg::GmresDev& Gh = *h->gpin;
@@ -747,14 +758,14 @@ NewtonOut newton(stg_handle* h, const Op& residual,
         EmScope scope(h);
         gs = gmres(h, J.A, h->emb.p, h->emx.p, n, cfg.gmres_restart, cfg.gmres_tol,
                    cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                   /*pipelined=*/J.speculative, /*b_sign=*/-1.0);
+                   /*pipelined=*/J.speculative, /*b_sign=*/-1.0, /*want_rel=*/false);
       }
       stg::permute_from_elem(du, h->emx.p, nt, npc, ns, h->stream);
       h->launches += 2;
     } else {
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
                  J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/J.speculative,
-                 /*b_sign=*/-1.0);
+                 /*b_sign=*/-1.0, /*want_rel=*/false);
     }
     out.linear_iterations += gs.iterations;
     if (!gs.converged)
@@ -790,7 +801,10 @@ void st_residual(stg_handle* h, double dt, const double* un, const double* U, do
 // h = fd_eps * sqrt(1 + ||U||_2) / ||v||_2 (the Walker-Pernice differencing
 // parameter, as in PETSc's MFFD "wp"), so the perturbation is relative to the
 // state regardless of the scaling of the Krylov vector v.
-// un2 >= 0: ||U||_2 already known (U is fixed during a Newton linear solve)
+// un2 >= 0: ||U||_2 already known (U is fixed during a Newton linear solve);
+// un2 == kUUOnDevice: <U,U> sits in small[kUUSlot] (fused path only)
+constexpr double kUUOnDevice = -2.0;
+constexpr int kUUSlot = 1001;
 void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, const double* v,
             double* Jv, double fd_eps, double un2 = -1.0) {
   const long long n = h->n_dof;
@@ -808,11 +822,16 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
     a.fdv = v;
     a.skip = h->skip;
     if (stg::fd_fused_supported(a)) {
-      const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
       double* vv = h->small.p + 1000;
+      if (un2 == kUUOnDevice) {
+        a.fd_uu = h->small.p + kUUSlot;
+        a.fd_c = fd_eps;
+      } else {
+        const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
+        a.fd_c = fd_eps * std::sqrt(1.0 + un);
+      }
       stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
       a.fd_vv = vv;
-      a.fd_c = fd_eps * std::sqrt(1.0 + un);
       if (stg::launch_slab_generic(a, h->stream) < 0)
         throw std::runtime_error("fused FD Jacobian launch failed");
       h->launches += 2;
@@ -996,6 +1015,19 @@ bool jvp_speculative(const stg_handle* h, double fd_eps) {
   a.n_in = a.n_out = h->nt;
   return h->kernel_pref == STG_KERNEL_AUTO && stg::fd_fused_supported(a);
 }
+
+// ||U||_2 for the FD Jacobian action at U: left on the device (no host
+// round trip) when the fused action consumes it there, else read back
+double fd_norm(stg_handle* h, double fd_eps, const double* U, long long n) {
+  if (!uses_fd(h, fd_eps)) return -1.0;
+  if (jvp_speculative(h, fd_eps)) {  // the fused lane-kernel action
+    stg::vec_dot(U, U, n, h->partial.p, h->small.p + kUUSlot, h->stream);
+    h->launches++;
+    return kUUOnDevice;
+  }
+  return std::sqrt(dev_dot(h, U, U, n));
+}
+
 
 void st_jvp(stg_handle* h, double dt, const double* U, const double* v, double* Jv,
             double fd_eps, double un2 = -1.0) {
@@ -1493,7 +1525,7 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
         h, [&](const double* X, double* R) { st_residual(h, dt, u_n, X, R); },
         [&](const double* X) -> LinSys {
           LinSys L;
-          const double un2 = uses_fd(h, eps) ? std::sqrt(dev_dot(h, X, X, n)) : -1.0;
+          const double un2 = fd_norm(h, eps, X, n);
           L.A = [h, dt, X, eps, un2](const double* v, double* Jv) {
             st_jvp(h, dt, X, v, Jv, eps, un2);
           };
@@ -1542,7 +1574,7 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
         h, [&](const double* X, double* R) { stage_residual(h, form, dt, u, X, R); },
         [&](const double* X) -> LinSys {
           LinSys L;
-          const double un2 = uses_fd(h, eps) ? std::sqrt(dev_dot(h, X, X, n)) : -1.0;
+          const double un2 = fd_norm(h, eps, X, n);
           L.A = [h, form, dt, X, eps, un2](const double* v, double* Jv) {
             stage_jvp(h, form, dt, X, v, Jv, eps, un2);
           };
