@@ -216,6 +216,7 @@ struct GenArgs {
   double* F;           // workspace, n_in blocks
   double* R;           // n_out blocks (null: only F is computed)
   int* err;            // admissibility flag: 1 + first failing block
+  Skip skip;
 };
 // Returns the number of kernels launched, or -1 if (d, n, r) is unsupported.
 int launch_general(const GenArgs& a, cudaStream_t s);
@@ -331,6 +332,13 @@ void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long
 // x = (accumulate ? x : 0) + sum_{j<k} y[j] V_j (y on device), k <= 64
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
                  cudaStream_t s, bool accumulate = true);
+// Central-difference Jacobian action on the device, no host scalars:
+// e = c * sqrt(1 + sqrt(*uu)) / sqrt(*vv) (uu null: e = c / sqrt(*vv); e = 1
+// if <v,v> = 0).  fd_pm: Up = U + e v, Um = U - e v.  fd_diff: Jv = (Jv - Fm) / 2e.
+void vec_fd_pm(double* Up, double* Um, const double* U, const double* v, long long n,
+               const double* vv, const double* uu, double c, cudaStream_t s, Skip skip = {});
+void vec_fd_diff(double* Jv, const double* Fm, long long n, const double* vv, const double* uu,
+                 double c, cudaStream_t s, Skip skip = {});
 // *out = max |x_i|
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s);
 // *out = <x,y>

@@ -94,7 +94,9 @@ __device__ __forceinline__ double wave_speed(const GenCoef& c, const double* uL,
 template <int D, int N1, int R>
 __global__ void __launch_bounds__(kThreads)
     gen_rhs_kernel(const GenCoef c, const Geometry g, const double* __restrict__ X,
-                   double* __restrict__ F, int n_in, int* err) {
+                   double* __restrict__ F, int n_in, int* err, const Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
   constexpr int NPC = D == 1 ? N1 : N1 * N1;
   const long long per_block = (long long)g.n_cells * NPC;
   const long long total = per_block * n_in;
@@ -234,7 +236,9 @@ __global__ void __launch_bounds__(kThreads)
 __global__ void __launch_bounds__(kThreads)
     gen_mix_kernel(const MixCoef mx, int n_in, int n_out, const double* __restrict__ X,
                    const double* __restrict__ F, const double* __restrict__ W,
-                   double* __restrict__ R, long long ns) {
+                   double* __restrict__ R, long long ns, const Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
   for (long long k = blockIdx.x * (long long)kThreads + threadIdx.x; k < ns;
        k += (long long)gridDim.x * kThreads) {
     double xv[kMaxT], fv[kMaxT];
@@ -259,7 +263,8 @@ void launch_rhs(const GenArgs& a, cudaStream_t s) {
   const long long total = (long long)a.g.n_cells * NPC * a.n_in;
   long long grid = (total + kThreads - 1) / kThreads;
   if (grid > 148 * 16) grid = 148 * 16;
-  gen_rhs_kernel<D, N1, R><<<int(grid), kThreads, 0, s>>>(a.c, a.g, a.X, a.F, a.n_in, a.err);
+  launch_ex(kPdlSlab, gen_rhs_kernel<D, N1, R>, int(grid), kThreads, 0, s, a.c, a.g, a.X, a.F,
+            a.n_in, a.err, a.skip);
 }
 
 template <int D, int R>
@@ -288,8 +293,8 @@ int launch_general(const GenArgs& a, cudaStream_t s) {
   if (a.R == nullptr) return 1;  // F only (spatial rhs into a.F)
   long long grid = (a.g.n_sdof + kThreads - 1) / kThreads;
   if (grid > 148 * 16) grid = 148 * 16;
-  gen_mix_kernel<<<int(grid), kThreads, 0, s>>>(a.mx, a.n_in, a.n_out, a.Xmix, a.F, a.W, a.R,
-                                                a.g.n_sdof);
+  launch_ex(kPdlSlab, gen_mix_kernel, int(grid), kThreads, 0, s, a.mx, a.n_in, a.n_out, a.Xmix,
+            a.F, a.W, a.R, a.g.n_sdof, a.skip);
   return 2;
 }
 

@@ -276,6 +276,33 @@ __global__ void k_gmres_init(GmresDev* G, int m, const double* bb, double beta, 
   if (hn2_0) *hn2_0 = 1.0;  // ||S_0||^2 = 1 (S_0 = r / ||r||)
 }
 
+__device__ __forceinline__ double fd_step(const double* vv, const double* uu, double c) {
+  const double e = uu ? c * sqrt(1.0 + sqrt(*uu)) : c;
+  return *vv > 0.0 ? e / sqrt(*vv) : 1.0;
+}
+__global__ void k_fd_pm(double* __restrict__ Up, double* __restrict__ Um,
+                        const double* __restrict__ U, const double* __restrict__ v, long long n,
+                        const double* vv, const double* uu, double c, Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  const double e = fd_step(vv, uu, c);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double u = U[i], d = e * v[i];
+    Up[i] = u + d;
+    Um[i] = u - d;
+  }
+}
+__global__ void k_fd_diff(double* __restrict__ Jv, const double* __restrict__ Fm, long long n,
+                          const double* vv, const double* uu, double c, Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  const double h = 0.5 / fd_step(vv, uu, c);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    Jv[i] = (Jv[i] - Fm[i]) * h;
+}
+
 // y = R^-1 g over the first k Givens-reduced Hessenberg columns, scaled by
 // the basis norms (out[j] = y_j c_j: x += sum out_j S_j); one thread, k <= 60
 __global__ void k_gmres_backsub(const GmresDev* G, int k, double* out) {
@@ -441,6 +468,15 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
   STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_multidot<KM, WW>, multi_grid<KM, WW, false>(n), kVecBlock,
                                               0, s, V, ldv, k, w, n / WW, partial, out, c,
                                                       skip)));
+}
+
+void vec_fd_pm(double* Up, double* Um, const double* U, const double* v, long long n,
+               const double* vv, const double* uu, double c, cudaStream_t s, Skip skip) {
+  launch_ex(vec_pdl(n), k_fd_pm, grid_for(n), kBlock, 0, s, Up, Um, U, v, n, vv, uu, c, skip);
+}
+void vec_fd_diff(double* Jv, const double* Fm, long long n, const double* vv, const double* uu,
+                 double c, cudaStream_t s, Skip skip) {
+  launch_ex(vec_pdl(n), k_fd_diff, grid_for(n), kBlock, 0, s, Jv, Fm, n, vv, uu, c, skip);
 }
 
 void gmres_backsub(const GmresDev* G, int k, double* out, cudaStream_t s) {

@@ -131,6 +131,9 @@ struct stg_handle {
   int* mapped = nullptr;
   cudaEvent_t ev_step[2] = {}, ev_re = nullptr;
   stg::Skip skip{};
+  // Euler admissibility: a flag may be set on the device (pending) and the
+  // check is deferred while a Newton solve runs (apply_general)
+  bool adm_pending = false, adm_defer = false;
   // slab vectors handed to the operator / preconditioner are element-major
   // (set around a d = 2 GMRES solve with the dense element block, see newton)
   int em = 0;
@@ -167,9 +170,36 @@ void check_launch(stg_handle* h) {
 }
 
 // ---- operator dispatch ----------------------------------------------------
-// General flux models: F(X_j) for every input block, then the mix; Euler's
-// admissibility flag is read back (one sync) and raised as AdmissibilityError
-// naming the temporal node (stdg.hpp:41-50).
+// Euler's admissibility flag (1 + first failing temporal block, set by the
+// rhs kernel) is raised as AdmissibilityError naming the temporal node
+// (stdg.hpp:41-50).  Outside a solve every apply checks it (one sync); inside
+// newton() the check is deferred to the Newton step's own sync points, so no
+// Arnoldi step waits on the host (the step that went nonphysical still throws,
+// a few kernels later).
+void check_admissibility(stg_handle* h) {
+  if (!h->adm_pending) return;
+  h->adm_pending = false;
+  int* hp = reinterpret_cast<int*>(h->pinned + 1000);
+  int* flag = reinterpret_cast<int*>(h->genFlag.p);
+  ck(cudaMemcpyAsync(hp, flag, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "memcpy");
+  ck(cudaStreamSynchronize(h->stream), "sync");
+  if (*hp != 0) {
+    const int node = *hp - 1;
+    ck(cudaMemsetAsync(flag, 0, sizeof(int), h->stream), "memset");
+    throw AdmissibilityError("temporal node " + std::to_string(node) +
+                             ": euler_model: nonphysical state");
+  }
+}
+
+// while in scope, admissibility checks wait for check_admissibility()
+struct AdmDefer {
+  stg_handle* h;
+  bool prev;
+  explicit AdmDefer(stg_handle* hh) : h(hh), prev(hh->adm_defer) { h->adm_defer = true; }
+  ~AdmDefer() { h->adm_defer = prev; }
+};
+
+// General flux models: F(X_j) for every input block, then the mix.
 void apply_general(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
                    const double* W, double* R) {
   if (h->kernel_pref == STG_KERNEL_FAST)
@@ -187,20 +217,14 @@ void apply_general(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, c
   a.F = h->genF.p;
   a.R = R;
   a.err = reinterpret_cast<int*>(h->genFlag.p);
+  a.skip = h->skip;
   const int launched = stg::launch_general(a, h->stream);
   if (launched < 0) throw std::invalid_argument("no kernel for this (dim, degree, model)");
   h->launches += launched;
   check_launch(h);
   if (h->desc.model == STG_MODEL_EULER) {
-    int* hp = reinterpret_cast<int*>(h->pinned + 1000);
-    ck(cudaMemcpyAsync(hp, a.err, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "memcpy");
-    ck(cudaStreamSynchronize(h->stream), "sync");
-    if (*hp != 0) {
-      const int node = *hp - 1;
-      ck(cudaMemsetAsync(a.err, 0, sizeof(int), h->stream), "memset");
-      throw AdmissibilityError("temporal node " + std::to_string(node) +
-                               ": euler_model: nonphysical state");
-    }
+    h->adm_pending = true;
+    if (!h->adm_defer) check_admissibility(h);
   }
 }
 
@@ -655,6 +679,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     }
     ck(cudaMemcpyAsync(h->gpin, G, sizeof(stg::GmresDev), cudaMemcpyDeviceToHost, s), "memcpy");
     ck(cudaStreamSynchronize(s), "sync");
+    check_admissibility(h);  // a nonphysical Euler state stops the solve here
     const stg::GmresDev& Gh = *h->gpin;
     if (bnorm < 0.0) bnorm = Gh.bnorm;  // deferred first cycle
     if (status == 4 || bnorm == 0.0) {   // b = 0: x = 0
@@ -707,9 +732,6 @@ struct NewtonOut {
 struct LinSys {
   Op A;
   Op P;
-  // every kernel A and P launch honours the skip flag and neither waits on
-  // the host: GMRES may enqueue Arnoldi steps speculatively
-  bool speculative = false;
   // A and P also run on element-major vectors (d = 2 dense element block):
   // the solve is done in that layout, with one permute each way
   bool element_major = false;
@@ -733,8 +755,10 @@ NewtonOut newton(stg_handle* h, const Op& residual,
   double* r = h->res.p;
   double* du = h->delta.p;
   NewtonOut out;
+  AdmDefer defer(h);
   residual(u, r);
   double norm = dev_maxabs(h, r, n);
+  check_admissibility(h);
   const double norm0 = norm;
   out.history.push_back(norm);
   auto converged = [&](double v) { return v <= cfg.abs_tol || v <= cfg.rel_tol * norm0; };
@@ -758,16 +782,17 @@ NewtonOut newton(stg_handle* h, const Op& residual,
         EmScope scope(h);
         gs = gmres(h, J.A, h->emb.p, h->emx.p, n, cfg.gmres_restart, cfg.gmres_tol,
                    cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                   /*pipelined=*/J.speculative, /*b_sign=*/-1.0, /*want_rel=*/false);
+                   /*pipelined=*/true, /*b_sign=*/-1.0, /*want_rel=*/false);
       }
       stg::permute_from_elem(du, h->emx.p, nt, npc, ns, h->stream);
       h->launches += 2;
     } else {
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
-                 J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/J.speculative,
+                 J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/true,
                  /*b_sign=*/-1.0, /*want_rel=*/false);
     }
     out.linear_iterations += gs.iterations;
+    check_admissibility(h);
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
                                fmt_short(gs.rel_residual));
@@ -776,6 +801,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     ++out.iterations;
     residual(u, r);
     norm = dev_maxabs(h, r, n);
+    check_admissibility(h);
     out.history.push_back(norm);
   }
   out.final_residual = norm;
@@ -839,25 +865,25 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
       return;
     }
   }
-  const double vn = std::sqrt(dev_dot(h, v, v, n));
-  if (vn == 0.0) {
-    stg::vec_fill(Jv, 0.0, n, h->stream);
-    h->launches++;
-    return;
+  // central difference, the same two applies as a forward difference, O(h^2);
+  // the step h is formed on the device from <v,v> (and <U,U>): no host sync
+  double* vv = h->small.p + 1000;
+  stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
+  const double* uu = nullptr;
+  double c = fd_eps;
+  if (un2 == kUUOnDevice) {
+    uu = h->small.p + kUUSlot;
+  } else {
+    const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
+    c = fd_eps * std::sqrt(1.0 + un);
   }
-  const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
-  const double eps = fd_eps * std::sqrt(1.0 + un) / vn;
   h->tmp1.ensure(size_t(n));
   h->tmp2.ensure(size_t(n));
-  // central difference: the same two applies as a forward difference, O(h^2)
-  stg::vec_copy(h->tmp1.p, U, n, h->stream);
-  stg::vec_axpy(h->tmp1.p, eps, v, n, h->stream);
+  stg::vec_fd_pm(h->tmp1.p, h->tmp2.p, U, v, n, vv, uu, c, h->stream, h->skip);
   h->launches += 2;
   apply(h, mix, h->nt, h->nt, h->tmp1.p, nullptr, nullptr, Jv, false, full);
-  stg::vec_axpy(h->tmp1.p, -2.0 * eps, v, n, h->stream);
-  h->launches++;
-  apply(h, mix, h->nt, h->nt, h->tmp1.p, nullptr, nullptr, h->tmp2.p, false, full);
-  stg::vec_axpby(Jv, -0.5 / eps, h->tmp2.p, 0.5 / eps, n, h->stream);
+  apply(h, mix, h->nt, h->nt, h->tmp2.p, nullptr, nullptr, h->tmp1.p, false, full);
+  stg::vec_fd_diff(Jv, h->tmp1.p, n, vv, uu, c, h->stream, h->skip);
   h->launches++;
 }
 
@@ -1003,29 +1029,13 @@ bool uses_fd(const stg_handle* h, double fd_eps) {
   return !linear_model(h->desc.model) && effective_fd_eps(h, fd_eps) > 0.0;
 }
 
-// whether the Jacobian action is skip-aware and host-wait free (LinSys):
-// the slab kernels are; the general-model kernels and the unfused FD action
-// (host-side norms, plain vector kernels) are not
-bool jvp_speculative(const stg_handle* h, double fd_eps) {
-  if (general_model(h->desc.model)) return false;
-  if (!uses_fd(h, fd_eps)) return true;
-  stg::SlabArgs a{};
-  a.g = h->g;
-  a.model = h->desc.model;
-  a.n_in = a.n_out = h->nt;
-  return h->kernel_pref == STG_KERNEL_AUTO && stg::fd_fused_supported(a);
-}
-
-// ||U||_2 for the FD Jacobian action at U: left on the device (no host
-// round trip) when the fused action consumes it there, else read back
+// <U,U> for the FD Jacobian action at U, left on the device: both FD
+// actions form their step there (no host round trip inside GMRES)
 double fd_norm(stg_handle* h, double fd_eps, const double* U, long long n) {
   if (!uses_fd(h, fd_eps)) return -1.0;
-  if (jvp_speculative(h, fd_eps)) {  // the fused lane-kernel action
-    stg::vec_dot(U, U, n, h->partial.p, h->small.p + kUUSlot, h->stream);
-    h->launches++;
-    return kUUOnDevice;
-  }
-  return std::sqrt(dev_dot(h, U, U, n));
+  stg::vec_dot(U, U, n, h->partial.p, h->small.p + kUUSlot, h->stream);
+  h->launches++;
+  return kUUOnDevice;
 }
 
 
@@ -1530,7 +1540,6 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
             st_jvp(h, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
-          L.speculative = jvp_speculative(h, eps);
           L.element_major = element_major_ok(h, cfg.precond, false);
           return L;
         },
@@ -1579,7 +1588,6 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
             stage_jvp(h, form, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
-          L.speculative = jvp_speculative(h, eps);
           L.element_major = element_major_ok(h, cfg.precond, form == STG_FORM_A);
           return L;
         },
@@ -1605,22 +1613,34 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
 template <class F>
 int guarded(stg_handle* h, F&& f) {
   std::string* err = h ? &h->err : &g_create_error;
+  // a failed call leaves no deferred admissibility flag behind
+  auto clear = [h] {
+    if (h && h->adm_pending) {
+      h->adm_pending = false;
+      cudaMemsetAsync(h->genFlag.p, 0, sizeof(int), h->stream);
+    }
+  };
   try {
     f();
     return STG_OK;
   } catch (const NonconvergenceError& e) {
+    clear();
     *err = e.what();
     return STG_ERR_NONCONVERGENCE;
   } catch (const CudaError& e) {
+    clear();
     *err = e.what();
     return STG_ERR_CUDA;
   } catch (const AdmissibilityError& e) {
+    clear();
     *err = e.what();
     return STG_ERR_ADMISSIBILITY;
   } catch (const std::invalid_argument& e) {
+    clear();
     *err = e.what();
     return STG_ERR_INVALID;
   } catch (const std::exception& e) {
+    clear();
     *err = e.what();
     return STG_ERR_RUNTIME;
   }
@@ -1912,7 +1932,7 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     const GmresStats st = gmres(
         h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
         restart, tol, max_it, P ? &P : nullptr, /*x_zero=*/false,
-        /*pipelined=*/jvp_speculative(h, 0.0));
+        /*pipelined=*/true);
     if (iterations) *iterations = st.iterations;
     if (rel_residual) *rel_residual = st.rel_residual;
     if (!st.converged)
