@@ -18,3 +18,10 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     --csv --log-file gpurun_out/ncu_c4_solve_launches.csv python scripts/prof_solve.py c4 \
     > gpurun_out/ncu_solve.log 2>&1
 echo "ncu solve exit $?" >> gpurun_out/ncu_solve.log
+ncu -k regex:fdm_kernel --set full --clock-control none --import-source on -c 1 \
+    -o gpurun_out/fdm_full python scripts/prof_solve.py c4 > gpurun_out/ncu_fdm.log 2>&1
+ncu -i gpurun_out/fdm_full.ncu-rep --page raw --csv > gpurun_out/fdm_full_raw.csv 2>&1
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    --csv --log-file gpurun_out/ncu_c3_solve_launches.csv python scripts/prof_solve.py c3 \
+    > gpurun_out/ncu_c3.log 2>&1
+python bench.py --impl reference --steps 100 --warmup 2 > gpurun_out/ref.json 2>/dev/null
