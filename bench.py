@@ -456,6 +456,13 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     out["c4_slab_solve"] = {"seconds": t, "gmres_tol": 1e-10, "newton": info.newton_iterations,
                             "gmres_iterations": info.linear_iterations,
                             "final_residual_inf": info.final_residual}
+    # c4 marched over 10 slabs on the device (stg_stdg_integrate, stdg.hpp:152-173)
+    op.stdg_integrate(0.0, un, 2 * cfg.dt, 2, nc)  # warm
+    t10, (_, _, _, info10) = _wall(
+        torch, lambda: op.stdg_integrate(0.0, un, 10 * cfg.dt, 10, nc))
+    out["c4_10_slab_march"] = {"seconds": t10, "per_slab_s": t10 / 10,
+                               "newton": info10.newton_iterations,
+                               "gmres_iterations": info10.linear_iterations}
     # c5: Lobatto IIIC s=4 stage system (A^-1 form) on the c4 mesh, vs the c4 slab
     c5 = C.CONFIGS["c5"]
     op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, un, nc)  # warm (lazy module load of its kernels)
