@@ -229,18 +229,32 @@ __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
     const bool act = r < NB && c < ncells;
     const int t = r / n1, k = r - (r / n1) * n1;
     const double x = act ? in[t * ns + c * n1 + k] : 0.0;
-    const float2* Br =
-        reinterpret_cast<const float2*>(B + (size_t)(act ? c : 0) * NB * NB + (size_t)(act ? r : 0) * NB);
+    const float* Brow = B + (size_t)(act ? c : 0) * NB * NB + (size_t)(act ? r : 0) * NB;
+    // the row as 16-byte loads where it is 16-byte aligned (NB % 4 == 0)
+    float bv[NB];
+    if (NB % 4 == 0) {
+#pragma unroll
+      for (int q4 = 0; q4 < NB / 4; ++q4) {
+        const float4 v = act ? __ldg(reinterpret_cast<const float4*>(Brow) + q4)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+        bv[4 * q4] = v.x;
+        bv[4 * q4 + 1] = v.y;
+        bv[4 * q4 + 2] = v.z;
+        bv[4 * q4 + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q2 = 0; q2 < NB / 2; ++q2) {
+        const float2 v = act ? __ldg(reinterpret_cast<const float2*>(Brow) + q2)
+                             : make_float2(0.f, 0.f);
+        bv[2 * q2] = v.x;
+        bv[2 * q2 + 1] = v.y;
+      }
+    }
     double acc = 0.0;
 #pragma unroll
-    for (int q2 = 0; q2 < NB / 2; ++q2) {
-      const float2 bf = act ? __ldg(Br + q2) : make_float2(0.f, 0.f);
-      const double2 b = make_double2(double(bf.x), double(bf.y));
-      const double x0 = __shfl_sync(0xffffffffu, x, (h << 4) + 2 * q2);
-      const double x1 = __shfl_sync(0xffffffffu, x, (h << 4) + 2 * q2 + 1);
-      acc = fma(b.x, x0, acc);
-      acc = fma(b.y, x1, acc);
-    }
+    for (int q = 0; q < NB; ++q)
+      acc = fma(double(bv[q]), __shfl_sync(0xffffffffu, x, (h << 4) + q), acc);
     if (act) out[t * ns + c * n1 + k] = acc;
   }
 }
