@@ -57,7 +57,6 @@ __device__ __forceinline__ void advection_line(const SpatialCoef& sp, const doub
 // entropy-conservative two-point flux f#(a,b) = (a^2+ab+b^2)/6, LLF
 // interface flux with lambda = max(|uL|,|uR|), SAT lifting.
 __device__ __forceinline__ double bf(double u) { return 0.5 * u * u; }
-__device__ __forceinline__ double bec(double a, double b) { return (a * a + a * b + b * b) / 6.0; }
 __device__ __forceinline__ double bllf(double uL, double uR) {
   const double lam = fmax(fabs(uL), fabs(uR));
   return 0.5 * (bf(uL) + bf(uR)) + 0.5 * lam * (uL - uR);
@@ -78,12 +77,14 @@ __device__ __forceinline__ double dbllf(double uL, double uR, double vL, double 
 template <int N1>
 __device__ __forceinline__ void burgers_line(const SpatialCoef& sp, const double* u, double ul,
                                              double ur, double* G) {
+  // sum_k 2 D(i,k) f#(u_i,u_k), f#(a,b) = (a^2+ab+b^2)/6, with the 2/6 = 1/3
+  // factored out of the sum: no division per pair
 #pragma unroll
   for (int i = 0; i < N1; ++i) {
     double vol = 0.0;
 #pragma unroll
-    for (int k = 0; k < N1; ++k) vol += 2.0 * sp.Dm[i][k] * bec(u[i], u[k]);
-    G[i] = -sp.sc * vol;
+    for (int k = 0; k < N1; ++k) vol = fma(sp.Dm[i][k], fma(u[i], u[i] + u[k], u[k] * u[k]), vol);
+    G[i] = -sp.sc * vol * (1.0 / 3.0);
   }
   G[N1 - 1] -= sp.sc * (bllf(u[N1 - 1], ur) - bf(u[N1 - 1])) * sp.inv_wN;
   G[0] += sp.sc * (bllf(ul, u[0]) - bf(u[0])) * sp.inv_w0;
@@ -98,9 +99,8 @@ __device__ __forceinline__ void burgers_jvp_line(const SpatialCoef& sp, const do
     double vol = 0.0;
 #pragma unroll
     for (int k = 0; k < N1; ++k)
-      vol += 2.0 * sp.Dm[i][k] *
-             ((2.0 * u[i] + u[k]) * v[i] + (u[i] + 2.0 * u[k]) * v[k]) / 6.0;
-    G[i] = -sp.sc * vol;
+      vol = fma(sp.Dm[i][k], (2.0 * u[i] + u[k]) * v[i] + (u[i] + 2.0 * u[k]) * v[k], vol);
+    G[i] = -sp.sc * vol * (1.0 / 3.0);
   }
   G[N1 - 1] -= sp.sc * (dbllf(u[N1 - 1], ur, v[N1 - 1], vr) - u[N1 - 1] * v[N1 - 1]) * sp.inv_wN;
   G[0] += sp.sc * (dbllf(ul, u[0], vl, v[0]) - u[0] * v[0]) * sp.inv_w0;
