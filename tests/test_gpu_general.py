@@ -146,6 +146,22 @@ def test_admissibility_error_names_temporal_node():  # stdg.hpp:41-50, models.hp
     assert rel(op.st_residual(0.0, 0.01, dev(v), dev(V)), pr.st_residual(0.0, 0.01, v, V)) <= TOL_OP
 
 
+def test_admissibility_error_inside_a_solve():
+    # inside stdg_step the flag is checked at the Newton step's sync points
+    # (not after every apply): the same error surfaces from the same call,
+    # and the handle solves normally afterwards
+    op, pr = euler_pair(2, 1)
+    bad = np.tile([1.0, 4.0, 0.0, 1.0], op.n_sdof // 4)  # negative pressure
+    nc = NewtonConfig(abs_tol=1e-10, rel_tol=1e-10, gmres_tol=1e-12)
+    with pytest.raises(AdmissibilityError, match="temporal node"):
+        op.stdg_step(0.0, 0.01, dev(bad), nc)
+    v = vortex_u(pr)
+    U, u1, info = op.stdg_step(0.0, 0.01, dev(v), nc)
+    assert info.newton_iterations >= 1
+    Uo, _, _, _ = pr.stdg_step(0.0, 0.01, v, abs_tol=1e-10, rel_tol=1e-10, linear=O.DENSE_LU)
+    assert rel(U, Uo) <= 1e-8
+
+
 def test_general_model_preconditioner_resolution():
     op, pr = pulse_pair(4, 1)
     v = dev(np.ones(op.n_dof))
