@@ -174,16 +174,19 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
       }
     }
     const double f = row[col];
+    // block columns <= col are finished (never read again), so only the
+    // entries right of the pivot column and the identity part are updated
+    const int qa = (col + 1) & ~1;  // first updated pair (col: unrolled constant)
     if (l == idx) {
       const double ip = 1.0 / f;
 #pragma unroll
       for (int q = 0; q < NB; ++q) {
-        row[q] *= ip;
+        if (q > col) row[q] *= ip;
         inv[q] *= ip;
       }
 #pragma unroll
       for (int q = 0; q < NB; q += 2) {
-        *reinterpret_cast<double2*>(P + q) = make_double2(row[q], row[q + 1]);
+        if (q >= qa) *reinterpret_cast<double2*>(P + q) = make_double2(row[q], row[q + 1]);
         *reinterpret_cast<double2*>(P + NB + q) = make_double2(inv[q], inv[q + 1]);
       }
       used = true;
@@ -193,10 +196,12 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
     if (l != idx) {
 #pragma unroll
       for (int q = 0; q < NB; q += 2) {
-        const double2 pr = *reinterpret_cast<const double2*>(P + q);
+        if (q >= qa) {
+          const double2 pr = *reinterpret_cast<const double2*>(P + q);
+          row[q] = fma(-f, pr.x, row[q]);
+          row[q + 1] = fma(-f, pr.y, row[q + 1]);
+        }
         const double2 pi = *reinterpret_cast<const double2*>(P + NB + q);
-        row[q] = fma(-f, pr.x, row[q]);
-        row[q + 1] = fma(-f, pr.y, row[q + 1]);
         inv[q] = fma(-f, pi.x, inv[q]);
         inv[q + 1] = fma(-f, pi.y, inv[q + 1]);
       }
