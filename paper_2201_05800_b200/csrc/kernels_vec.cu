@@ -304,18 +304,30 @@ __global__ void k_fd_diff(double* __restrict__ Jv, const double* __restrict__ Fm
 }
 
 // y = R^-1 g over the first k Givens-reduced Hessenberg columns, scaled by
-// the basis norms (out[j] = y_j c_j: x += sum out_j S_j); one thread, k <= 60
-__global__ void k_gmres_backsub(const GmresDev* G, int k, double* out) {
+// the basis norms (out[j] = y_j c_j: x += sum out_j S_j), k <= 60.  The
+// block stages R's upper triangle, g and c in shared memory (independent
+// loads), then one thread substitutes from there.
+__global__ void __launch_bounds__(128) k_gmres_backsub(const GmresDev* G, int k, double* out) {
   pdl_entry();
-  if (threadIdx.x != 0) return;
+  __shared__ double Rs[kGmresMaxRestart * kGmresMaxRestart];
+  __shared__ double gs[kGmresMaxRestart], cs[kGmresMaxRestart], y[kGmresMaxRestart];
   const int m = G->m;
-  double y[kGmresMaxRestart];
-  for (int i = k - 1; i >= 0; --i) {
-    double acc = G->g[i];
-    for (int j = i + 1; j < k; ++j) acc -= G->H[i * m + j] * y[j];
-    y[i] = acc / G->H[i * m + i];
+  for (int q = threadIdx.x; q < k * k; q += blockDim.x) {
+    const int i = q / k, j = q - i * k;
+    if (j >= i) Rs[q] = G->H[i * m + j];
   }
-  for (int j = 0; j < k; ++j) out[j] = y[j] * G->cn[j];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    gs[j] = G->g[j];
+    cs[j] = G->cn[j];
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  for (int i = k - 1; i >= 0; --i) {
+    double acc = gs[i];
+    for (int j = i + 1; j < k; ++j) acc -= Rs[i * k + j] * y[j];
+    y[i] = acc / Rs[i * k + i];
+  }
+  for (int j = 0; j < k; ++j) out[j] = y[j] * cs[j];
 }
 
 __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x, long long n,
@@ -480,7 +492,7 @@ void vec_fd_diff(double* Jv, const double* Fm, long long n, const double* vv, co
 }
 
 void gmres_backsub(const GmresDev* G, int k, double* out, cudaStream_t s) {
-  launch_ex(kPdlVec, k_gmres_backsub, 1, 32, 0, s, G, k, out);
+  launch_ex(kPdlVec, k_gmres_backsub, 1, 128, 0, s, G, k, out);
 }
 
 void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,
