@@ -179,7 +179,17 @@ struct SlabArgs {
   // X and R in element-major order [cell][t][node] (d = 2 plane kernel only;
   // the dense element-block preconditioner's layout)
   int em;
+  // fused reductions of R (fast 3-D kernel; red_done reports whether the
+  // launched kernel produced them): *red_max = max |R_i| as the bit pattern
+  // of a non-negative double (zeroed beforehand), *red_ss = <R,R> summed in
+  // fixed order over per-CTA partials (red_part, with its completion counter
+  // right after kPartialDoubles doubles)
+  unsigned long long* red_max;
+  double* red_ss;
+  double* red_part;
 };
+// whether launch_slab_fast computes the fused R reductions for these args
+bool slab_fast_reduces(const SlabArgs& a);
 // true if the d = 1 lane kernel handles fused FD Jacobian actions for a
 bool fd_fused_supported(const SlabArgs& a);
 

@@ -27,6 +27,7 @@
 #include <type_traits>
 
 #include "kernels.hpp"
+#include "krylov.cuh"
 
 namespace stg {
 namespace {
@@ -1230,7 +1231,9 @@ __device__ __forceinline__ void issue(const Maps& m, const SlabArgs& a, const Ne
 }
 }  // namespace pst
 
-template <bool FULL_S>
+// RED: also max |R_i| and <R,R> (the Newton residual norm and the next
+// GMRES right-hand side's norm), so no separate reduction pass reads R again
+template <bool FULL_S, bool RED = false>
 __global__ void __launch_bounds__(pst::THREADS, 3)
     slab3d_n4_persist(const __grid_constant__ pst::Maps maps, const SlabArgs a,
                       const pst::Layout lay) {
@@ -1271,6 +1274,7 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
   const int zA = tid & 3, eA = (tid >> 2) & (E - 1), tA = tid >> 5;
   const int xB = tid & 3, yB = (tid >> 2) & 3, eB = tid >> 4;
   const int qB = yB * 4 + xB;
+  double rmax = 0.0, rss = 0.0;  // RED
   // u_n (the W term) is prefetched into registers one segment ahead
   double w[4] = {0, 0, 0, 0};
   if (nd.w && seg < nseg) {
@@ -1422,11 +1426,41 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
             acc = fma(a.mx.S[r][r], f[r][z], acc);
           }
           Rb[r * ns + 16 * z] = acc;
+          if (RED) {
+            rmax = nan_max(rmax, fabs(acc));
+            rss = fma(acc, acc, rss);
+          }
         }
     }
 #pragma unroll
     for (int z = 0; z < 4; ++z) w[z] = wn[z];
     __syncthreads();  // stage st and FA free for reuse
+  }
+  if (RED) {
+    __shared__ double red_m[pst::THREADS / 32], red_s[pst::THREADS / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rmax = nan_max(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
+      rss += __shfl_down_sync(0xffffffffu, rss, o);
+    }
+    if ((tid & 31) == 0) {
+      red_m[tid >> 5] = rmax;
+      red_s[tid >> 5] = rss;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < pst::THREADS / 32; ++q) {
+        m = nan_max(m, red_m[q]);
+        s2 += red_s[q];
+      }
+      // non-negative doubles order like their bit patterns
+      atomicMax(a.red_max, static_cast<unsigned long long>(__double_as_longlong(m)));
+      a.red_part[blockIdx.x] = s2;
+    }
+    unsigned* counter = reinterpret_cast<unsigned*>(a.red_part + kPartialDoubles);
+    if (is_last_block(counter)) block_finish_sum(a.red_part, gridDim.x, 1, a.red_ss, counter);
   }
 }
 
@@ -1701,6 +1735,11 @@ int fast_variant() {
 }
 }  // namespace
 
+bool slab_fast_reduces(const SlabArgs& a) {
+  return a.red_max != nullptr && a.red_ss != nullptr && a.red_part != nullptr &&
+         a.seg_end == 0 && slab_fast_supported(a) && fast_variant() != 1;
+}
+
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   EncodeFn enc = get_encode();
   if (!enc) return -1;
@@ -1745,23 +1784,20 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   const pst::Layout lay =
       pst::make_layout(a.sp.cL[0] != 0.0, a.sp.cR[0] != 0.0, a.sp.cL[1] != 0.0,
                        a.sp.cR[1] != 0.0, a.sp.cL[2] != 0.0, a.sp.cR[2] != 0.0);
+  const bool red = slab_fast_reduces(a);
+  auto kern = a.full_s ? (red ? slab3d_n4_persist<true, true> : slab3d_n4_persist<true, false>)
+                       : (red ? slab3d_n4_persist<false, true> : slab3d_n4_persist<false, false>);
   static bool attr = false;
   if (!attr) {  // the largest layout (every trace buffer) bounds the request
-    cudaFuncSetAttribute(slab3d_n4_persist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         pst::SMEM_BYTES);
-    cudaFuncSetAttribute(slab3d_n4_persist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         pst::SMEM_BYTES);
+    for (auto k : {slab3d_n4_persist<true, false>, slab3d_n4_persist<false, false>,
+                   slab3d_n4_persist<true, true>, slab3d_n4_persist<false, true>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, pst::SMEM_BYTES);
     attr = true;
   }
   const int nseg = (a.seg_end > 0 ? a.seg_end : a.g.n_cells / pst::E) - a.seg_begin;
   if (nseg <= 0) return 0;
   int occ = 0;
-  if (a.full_s)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab3d_n4_persist<true>, pst::THREADS,
-                                                  lay.smem);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab3d_n4_persist<false>, pst::THREADS,
-                                                  lay.smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, pst::THREADS, lay.smem);
   static int per_sm_cap = [] {
     const char* e = std::getenv("STG_FAST_CTAS_PER_SM");
     return e ? std::atoi(e) : 3;
@@ -1770,11 +1806,8 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   if (occ < 1) occ = 1;
   int grid = occ * num_sms();
   if (grid > nseg) grid = nseg;
-  if (a.full_s) {
-    launch_ex(a.no_pdl ? 0 : kPdlSlab, slab3d_n4_persist<true>, grid, pst::THREADS, lay.smem, s, m, a, lay);
-  } else {
-    launch_ex(a.no_pdl ? 0 : kPdlSlab, slab3d_n4_persist<false>, grid, pst::THREADS, lay.smem, s, m, a, lay);
-  }
+  if (red) cudaMemsetAsync(a.red_max, 0, sizeof(unsigned long long), s);
+  launch_ex(a.no_pdl ? 0 : kPdlSlab, kern, grid, pst::THREADS, lay.smem, s, m, a, lay);
   return 1;
 }
 

@@ -23,7 +23,7 @@ constexpr int kMaxGrid = 148 * 8;
 
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  for (int o = 16; o > 0; o >>= 1) v = nan_max(v, __shfl_down_sync(0xffffffffu, v, o));
   return v;
 }
 
@@ -338,18 +338,18 @@ __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x,
   double m = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
-    m = fmax(m, fabs(x[i]));
+    m = nan_max(m, fabs(x[i]));
   m = warp_max(m);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
     double r = 0.0;
-    for (int w = 0; w < kBlock / 32; ++w) r = fmax(r, red[w]);
+    for (int w = 0; w < kBlock / 32; ++w) r = nan_max(r, red[w]);
     part[blockIdx.x] = r;
   }
   if (is_last_block(counter) && threadIdx.x < 32) {
     double r = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) r = fmax(r, __ldcg(part + b));
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) r = nan_max(r, __ldcg(part + b));
     r = warp_max(r);
     if (threadIdx.x == 0) {
       out[0] = r;

@@ -8,6 +8,10 @@
 namespace stg {
 namespace {
 
+// max that propagates NaN (fmax drops it): a NaN residual must not read as
+// converged (the reference's inf-norm of a NaN vector is NaN)
+__device__ __forceinline__ double nan_max(double a, double b) { return (b > a || b != b) ? b : a; }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);

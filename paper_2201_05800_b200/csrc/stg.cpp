@@ -134,6 +134,9 @@ struct stg_handle {
   // Euler admissibility: a flag may be set on the device (pending) and the
   // check is deferred while a Newton solve runs (apply_general)
   bool adm_pending = false, adm_defer = false;
+  // fused residual reductions (fast 3-D kernel): requested by newton() for
+  // its residual applies; red_done: the last apply produced them
+  bool red = false, red_done = false;
   // slab vectors handed to the operator / preconditioner are element-major
   // (set around a d = 2 GMRES solve with the dense element block, see newton)
   int em = 0;
@@ -170,6 +173,10 @@ void check_launch(stg_handle* h) {
 }
 
 // ---- operator dispatch ----------------------------------------------------
+// slots of `small` for the fused residual reductions (clear of the GMRES
+// step data; kRedSsSlot is where the deferred first GMRES cycle reads <b,b>)
+constexpr int kRedMaxSlot = 1010;
+constexpr int kRedSsSlot = 200;
 // Euler's admissibility flag (1 + first failing temporal block, set by the
 // rhs kernel) is raised as AdmissibilityError naming the temporal node
 // (stdg.hpp:41-50).  Outside a solve every apply checks it (one sync); inside
@@ -231,6 +238,7 @@ void apply_general(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, c
 void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
            const double* U, const double* W, double* R, bool jvp, bool full_s,
            int seg_begin = 0, int seg_end = 0) {
+  h->red_done = false;
   stg::SlabArgs a{};
   a.seg_begin = seg_begin;
   a.seg_end = seg_end;
@@ -249,12 +257,18 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   a.R = R;
   a.skip = h->skip;
   a.em = h->em;
+  if (h->red) {  // max |R| and <R,R> from the apply itself (fast 3-D kernel)
+    a.red_max = reinterpret_cast<unsigned long long*>(h->small.p + kRedMaxSlot);
+    a.red_ss = h->small.p + kRedSsSlot;
+    a.red_part = h->partial.p;
+  }
   if (general_model(h->desc.model)) {
     apply_general(h, mx, n_in, n_out, X, W, R);
     return;
   }
   int launched = -1;
   if (h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(a)) {
+    h->red_done = h->red && stg::slab_fast_reduces(a);
     launched = stg::launch_slab_fast(a, h->stream);
   } else if (h->kernel_pref == STG_KERNEL_FAST) {
     throw std::invalid_argument("fast kernel requested but not applicable to this problem");
@@ -494,7 +508,8 @@ struct GmresStats {
 // k+1.  lag 0 (pipelined = false, or STG_GMRES_SYNC=1) waits after every step.
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
-                 bool pipelined = true, double b_sign = 1.0, bool want_rel = true) {
+                 bool pipelined = true, double b_sign = 1.0, bool want_rel = true,
+                 bool bb_ready = false) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > stg::kGmresMaxRestart) throw std::invalid_argument("gmres: restart <= 60");
@@ -542,8 +557,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   const bool defer = x_zero && tol < 1.0;
   double bnorm = -1.0;  // < 0: not known on the host yet
   if (defer) {
-    stg::vec_dot(b, b, n, h->partial.p, dsm + 200, s);
-    h->launches++;
+    if (!bb_ready) {  // else the residual kernel left <b,b> in dsm[200] (kRedSsSlot)
+      stg::vec_dot(b, b, n, h->partial.p, dsm + 200, s);
+      h->launches++;
+    }
   } else {
     const double bb = dev_dot(h, b, b, n);  // leaves <b,b> in small[kScalarSlot]
     bnorm = std::sqrt(bb);
@@ -756,8 +773,24 @@ NewtonOut newton(stg_handle* h, const Op& residual,
   double* du = h->delta.p;
   NewtonOut out;
   AdmDefer defer(h);
-  residual(u, r);
-  double norm = dev_maxabs(h, r, n);
+  // the residual apply computes max |r| and <r,r> itself where it can
+  // (fast 3-D kernel); otherwise a reduction pass reads r back
+  auto residual_norm = [&]() -> double {
+    h->red = true;
+    try {
+      residual(u, r);
+    } catch (...) {
+      h->red = false;
+      throw;
+    }
+    h->red = false;
+    if (!h->red_done) return dev_maxabs(h, r, n);
+    ck(cudaMemcpyAsync(h->pinned + kRedMaxSlot, h->small.p + kRedMaxSlot, sizeof(double),
+                       cudaMemcpyDeviceToHost, h->stream), "memcpy");
+    ck(cudaStreamSynchronize(h->stream), "sync");
+    return h->pinned[kRedMaxSlot];  // the bits of a non-negative double
+  };
+  double norm = residual_norm();
   check_admissibility(h);
   const double norm0 = norm;
   out.history.push_back(norm);
@@ -768,7 +801,11 @@ NewtonOut newton(stg_handle* h, const Op& residual,
                                     std::to_string(cfg.max_iter) + " iterations, residual " +
                                     fmt_short(norm),
                                 out.history);
+    const bool red_r = h->red_done;  // <r,r> already in small[kRedSsSlot]
     const LinSys J = jacobian(u);
+    // (an operator apply inside jacobian() clears red_done; nothing there
+    // writes small[kRedSsSlot])
+    const bool bb_ready = red_r && h->red_done;
     // J du = -r: the sign is folded into GMRES (b_sign = -1); du needs no
     // zero fill (gmres with x_zero writes it)
     GmresStats gs;
@@ -782,14 +819,15 @@ NewtonOut newton(stg_handle* h, const Op& residual,
         EmScope scope(h);
         gs = gmres(h, J.A, h->emb.p, h->emx.p, n, cfg.gmres_restart, cfg.gmres_tol,
                    cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                   /*pipelined=*/true, /*b_sign=*/-1.0, /*want_rel=*/false);
+                   /*pipelined=*/true, /*b_sign=*/-1.0, /*want_rel=*/false,
+                   /*bb_ready=*/bb_ready);
       }
       stg::permute_from_elem(du, h->emx.p, nt, npc, ns, h->stream);
       h->launches += 2;
     } else {
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
                  J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/true,
-                 /*b_sign=*/-1.0, /*want_rel=*/false);
+                 /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready);
     }
     out.linear_iterations += gs.iterations;
     check_admissibility(h);
@@ -799,8 +837,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     stg::vec_axpy(u, 1.0, du, n, h->stream);
     h->launches++;
     ++out.iterations;
-    residual(u, r);
-    norm = dev_maxabs(h, r, n);
+    norm = residual_norm();
     check_admissibility(h);
     out.history.push_back(norm);
   }
