@@ -188,8 +188,10 @@ struct SlabArgs {
   double* red_ss;
   double* red_part;
 };
-// whether launch_slab_fast computes the fused R reductions for these args
+// whether launch_slab_fast / launch_slab_generic compute the fused R
+// reductions for these args (fast 3-D kernel / d = 2 plane kernel)
 bool slab_fast_reduces(const SlabArgs& a);
+bool slab_generic_reduces(const SlabArgs& a);
 // true if the d = 1 lane kernel handles fused FD Jacobian actions for a
 bool fd_fused_supported(const SlabArgs& a);
 

@@ -730,6 +730,35 @@ __device__ __forceinline__ void bulk_wait0() {
 // EM: slab vectors in element-major order [cell][t][node] (X and R; u_n is
 // a spatial vector either way) -- the layout the d = 2 dense element-block
 // preconditioner works in, so GMRES can run without per-apply permutes.
+// CTA + grid reduction of the fused residual norms (RED kernels): max via
+// atomic max on the bit patterns of non-negative doubles, the sum of squares
+// via per-CTA partials added in fixed order by the last CTA
+__device__ __forceinline__ void block_reduce_r(const SlabArgs& a, double rmax, double rss) {
+  __shared__ double red_m[32], red_s[32];
+  const int tid = threadIdx.x, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rmax = nan_max(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
+    rss += __shfl_down_sync(0xffffffffu, rss, o);
+  }
+  if ((tid & 31) == 0) {
+    red_m[tid >> 5] = rmax;
+    red_s[tid >> 5] = rss;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0, s2 = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      m = nan_max(m, red_m[q]);
+      s2 += red_s[q];
+    }
+    atomicMax(a.red_max, static_cast<unsigned long long>(__double_as_longlong(m)));
+    a.red_part[blockIdx.x] = s2;
+  }
+  unsigned* counter = reinterpret_cast<unsigned*>(a.red_part + kPartialDoubles);
+  if (is_last_block(counter)) block_finish_sum(a.red_part, gridDim.x, 1, a.red_ss, counter);
+}
+
 template <int N1, int NT, int E, int MINB, bool EM>
 __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
     slab2d_plane(const SlabArgs a) {
@@ -1436,32 +1465,7 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
     for (int z = 0; z < 4; ++z) w[z] = wn[z];
     __syncthreads();  // stage st and FA free for reuse
   }
-  if (RED) {
-    __shared__ double red_m[pst::THREADS / 32], red_s[pst::THREADS / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      rmax = nan_max(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
-      rss += __shfl_down_sync(0xffffffffu, rss, o);
-    }
-    if ((tid & 31) == 0) {
-      red_m[tid >> 5] = rmax;
-      red_s[tid >> 5] = rss;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      double m = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int q = 0; q < pst::THREADS / 32; ++q) {
-        m = nan_max(m, red_m[q]);
-        s2 += red_s[q];
-      }
-      // non-negative doubles order like their bit patterns
-      atomicMax(a.red_max, static_cast<unsigned long long>(__double_as_longlong(m)));
-      a.red_part[blockIdx.x] = s2;
-    }
-    unsigned* counter = reinterpret_cast<unsigned*>(a.red_part + kPartialDoubles);
-    if (is_last_block(counter)) block_finish_sum(a.red_part, gridDim.x, 1, a.red_ss, counter);
-  }
+  if (RED) block_reduce_r(a, rmax, rss);
 }
 
 // ---------------------------------------------------------------------------
@@ -1535,10 +1539,8 @@ int launch_plane2d(const SlabArgs& a, cudaStream_t s) {
   const int nseg = a.g.n_cells / E;
   int grid = occ * num_sms_cached();
   if (grid > nseg) grid = nseg;
-  if (a.em)
-    launch_ex(kPdlSlab, slab2d_plane<N1, NT, E, MINB, true>, grid, Q::THREADS, Q::SMEM, s, a);
-  else
-    launch_ex(kPdlSlab, slab2d_plane<N1, NT, E, MINB, false>, grid, Q::THREADS, Q::SMEM, s, a);
+  auto k = a.em ? slab2d_plane<N1, NT, E, MINB, true> : slab2d_plane<N1, NT, E, MINB, false>;
+  launch_ex(kPdlSlab, k, grid, Q::THREADS, Q::SMEM, s, a);
   return 1;
 }
 
@@ -1622,6 +1624,10 @@ EncodeFn get_encode() {
 }
 
 }  // namespace
+
+// the generic launchers compute no fused R reductions (measured: the d = 2
+// plane kernel's reducing instance spilled and gained nothing on c2)
+bool slab_generic_reduces(const SlabArgs&) { return false; }
 
 bool slab_em_supported(const SlabArgs& a) {
   if (a.g.dim != 2 || a.model != int(Model::advection) || a.n_in != a.n_out || kPlaneEnv != 32 ||

@@ -268,12 +268,15 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   }
   int launched = -1;
   if (h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(a)) {
-    h->red_done = h->red && stg::slab_fast_reduces(a);
     launched = stg::launch_slab_fast(a, h->stream);
+    if (launched >= 0) h->red_done = h->red && stg::slab_fast_reduces(a);
   } else if (h->kernel_pref == STG_KERNEL_FAST) {
     throw std::invalid_argument("fast kernel requested but not applicable to this problem");
   }
-  if (launched < 0) launched = stg::launch_slab_generic(a, h->stream);
+  if (launched < 0) {
+    launched = stg::launch_slab_generic(a, h->stream);
+    h->red_done = h->red && launched >= 0 && stg::slab_generic_reduces(a);
+  }
   if (launched < 0) throw std::invalid_argument("no kernel for this (dim, degree, model)");
   h->launches += launched;
   check_launch(h);
