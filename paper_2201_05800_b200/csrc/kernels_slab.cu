@@ -174,7 +174,37 @@ __global__ void __launch_bounds__(kThreads1d) slab1d_kernel(const SlabArgs a) {
 // j writes output block j.  32 / NT elements per warp: 4x the threads of
 // slab1d_kernel and short per-lane chains.
 // ---------------------------------------------------------------------------
-template <int N1, int NT>
+// CTA + grid reduction of the fused residual norms (RED kernels): max via
+// atomic max on the bit patterns of non-negative doubles, the sum of squares
+// via per-CTA partials added in fixed order by the last CTA
+__device__ __forceinline__ void block_reduce_r(const SlabArgs& a, double rmax, double rss) {
+  __shared__ double red_m[32], red_s[32];
+  const int tid = threadIdx.x, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rmax = nan_max(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
+    rss += __shfl_down_sync(0xffffffffu, rss, o);
+  }
+  if ((tid & 31) == 0) {
+    red_m[tid >> 5] = rmax;
+    red_s[tid >> 5] = rss;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0, s2 = 0.0;
+    for (int q = 0; q < nw; ++q) {
+      m = nan_max(m, red_m[q]);
+      s2 += red_s[q];
+    }
+    atomicMax(a.red_max, static_cast<unsigned long long>(__double_as_longlong(m)));
+    a.red_part[blockIdx.x] = s2;
+  }
+  unsigned* counter = reinterpret_cast<unsigned*>(a.red_part + kPartialDoubles);
+  if (is_last_block(counter)) block_finish_sum(a.red_part, gridDim.x, 1, a.red_ss, counter);
+}
+
+// RED: also max |R_i| and <R,R> (the Newton residual, see slab3d_n4_persist)
+template <int N1, int NT, bool RED = false>
 __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
   pdl_entry();
   if (skip_now(a.skip)) return;
@@ -247,6 +277,17 @@ __global__ void __launch_bounds__(256) slab1d_lane_kernel(const SlabArgs a) {
       acc[i] = fma(tr, xv, acc[i]);
       acc[i] = fma(sr, gv, acc[i]);
     }
+  }
+  if (RED) {
+    double rmax = 0.0, rss = 0.0;
+    if (out_lane) {
+#pragma unroll
+      for (int i = 0; i < N1; ++i) {
+        rmax = nan_max(rmax, fabs(acc[i]));
+        rss = fma(acc[i], acc[i], rss);
+      }
+    }
+    block_reduce_r(a, rmax, rss);
   }
   if (out_lane) {
     double* Rj = a.R + j * ns + oc;
@@ -730,34 +771,6 @@ __device__ __forceinline__ void bulk_wait0() {
 // EM: slab vectors in element-major order [cell][t][node] (X and R; u_n is
 // a spatial vector either way) -- the layout the d = 2 dense element-block
 // preconditioner works in, so GMRES can run without per-apply permutes.
-// CTA + grid reduction of the fused residual norms (RED kernels): max via
-// atomic max on the bit patterns of non-negative doubles, the sum of squares
-// via per-CTA partials added in fixed order by the last CTA
-__device__ __forceinline__ void block_reduce_r(const SlabArgs& a, double rmax, double rss) {
-  __shared__ double red_m[32], red_s[32];
-  const int tid = threadIdx.x, nw = (blockDim.x + 31) >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    rmax = nan_max(rmax, __shfl_down_sync(0xffffffffu, rmax, o));
-    rss += __shfl_down_sync(0xffffffffu, rss, o);
-  }
-  if ((tid & 31) == 0) {
-    red_m[tid >> 5] = rmax;
-    red_s[tid >> 5] = rss;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double m = 0.0, s2 = 0.0;
-    for (int q = 0; q < nw; ++q) {
-      m = nan_max(m, red_m[q]);
-      s2 += red_s[q];
-    }
-    atomicMax(a.red_max, static_cast<unsigned long long>(__double_as_longlong(m)));
-    a.red_part[blockIdx.x] = s2;
-  }
-  unsigned* counter = reinterpret_cast<unsigned*>(a.red_part + kPartialDoubles);
-  if (is_last_block(counter)) block_finish_sum(a.red_part, gridDim.x, 1, a.red_ss, counter);
-}
 
 template <int N1, int NT, int E, int MINB, bool EM>
 __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
@@ -1471,6 +1484,12 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
 // ---------------------------------------------------------------------------
 // host-side launch helpers
 // ---------------------------------------------------------------------------
+// the Newton residual's fused reductions requested (and not an FD action)
+bool lane_reduces(const SlabArgs& a) {
+  return a.red_max != nullptr && a.red_ss != nullptr && a.red_part != nullptr &&
+         a.fdv == nullptr;
+}
+
 template <int N1>
 int launch1d(const SlabArgs& a, cudaStream_t s) {
   // large meshes: one lane per (element, temporal block) when n_in == n_tau
@@ -1481,7 +1500,12 @@ int launch1d(const SlabArgs& a, cudaStream_t s) {
       constexpr int EPW = 32 / NT;
       const long long warps = (a.g.nx + EPW - 1) / EPW;
       const int blocks = int((warps * 32 + 255) / 256);
-      launch_ex(kPdlSlab, slab1d_lane_kernel<N1, NT>, blocks, 256, 0, s, a);
+      if (lane_reduces(a)) {
+        cudaMemsetAsync(a.red_max, 0, sizeof(unsigned long long), s);
+        launch_ex(kPdlSlab, slab1d_lane_kernel<N1, NT, true>, blocks, 256, 0, s, a);
+      } else {
+        launch_ex(kPdlSlab, slab1d_lane_kernel<N1, NT, false>, blocks, 256, 0, s, a);
+      }
       return 1;
     };
     switch (a.n_in) {
@@ -1625,9 +1649,12 @@ EncodeFn get_encode() {
 
 }  // namespace
 
-// the generic launchers compute no fused R reductions (measured: the d = 2
+// the generic launchers reduce R only in the d = 1 lane kernel (the d = 2
 // plane kernel's reducing instance spilled and gained nothing on c2)
-bool slab_generic_reduces(const SlabArgs&) { return false; }
+bool slab_generic_reduces(const SlabArgs& a) {
+  return a.g.dim == 1 && lane_reduces(a) && a.g.nx >= 4096 && a.n_out <= a.n_in &&
+         a.n_in >= 2 && a.n_in <= 6 && a.g.n1 >= 2 && a.g.n1 <= 6 && !std::getenv("STG_1D_V1");
+}
 
 bool slab_em_supported(const SlabArgs& a) {
   if (a.g.dim != 2 || a.model != int(Model::advection) || a.n_in != a.n_out || kPlaneEnv != 32 ||
