@@ -490,6 +490,7 @@ struct GmresStats {
   int iterations = 0;
   double rel_residual = 0.0;
   bool converged = false;
+  bool added = false;  // the solution was added into add_to instead of written to x
 };
 
 // Restarted GMRES(m), right-preconditioned (A P^-1 y = b, x = P^-1 y; P null:
@@ -512,7 +513,7 @@ struct GmresStats {
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
                  bool pipelined = true, double b_sign = 1.0, bool want_rel = true,
-                 bool bb_ready = false) {
+                 bool bb_ready = false, double* add_to = nullptr) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > stg::kGmresMaxRestart) throw std::invalid_argument("gmres: restart <= 60");
@@ -688,9 +689,16 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     total += k;
     if (status == 1 && !want_rel) {
       // converged and the caller does not read the residual estimate: the
-      // back substitution and the update run on the device, no round trip
+      // back substitution and the update run on the device, no round trip.
+      // add_to (first cycle from x = 0): the solution goes straight into the
+      // caller's vector (Newton's u += du without du)
       stg::gmres_backsub(G, k, dsm + 256, s);
-      stg::vec_combine(x, P ? Z : V, ld, k, dsm + 256, n, s, x_set);
+      if (add_to && !x_set) {
+        stg::vec_combine(add_to, P ? Z : V, ld, k, dsm + 256, n, s, true);
+        st.added = true;
+      } else {
+        stg::vec_combine(x, P ? Z : V, ld, k, dsm + 256, n, s, x_set);
+      }
       h->launches += 2;
       x_set = true;
       st.converged = true;
@@ -830,15 +838,17 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     } else {
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
                  J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/true,
-                 /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready);
+                 /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready, /*add_to=*/u);
     }
     out.linear_iterations += gs.iterations;
     check_admissibility(h);
     if (!gs.converged)
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
                                fmt_short(gs.rel_residual));
-    stg::vec_axpy(u, 1.0, du, n, h->stream);
-    h->launches++;
+    if (!gs.added) {  // (gmres added the correction into u itself otherwise)
+      stg::vec_axpy(u, 1.0, du, n, h->stream);
+      h->launches++;
+    }
     ++out.iterations;
     norm = residual_norm();
     check_admissibility(h);
