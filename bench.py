@@ -38,6 +38,55 @@ METRIC = "fp64 space-time DG-SEM operator DOF/s & % HBM roofline; solve time/sla
 UNIT = "DOF/s"
 WORKLOAD = "c4"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
+NSETS = 3  # rotating input/output sets (each > 126 MB L2 at c2 / c4)
+
+# The bench workloads restated for the reference arm, which must not import
+# or load the product (paper_2201_05800_b200): the same numbers as
+# configs.CONFIGS (tests/test_bench_contract.py checks they agree).  u_n is
+# interpolated at the oracle's own node coordinates (bitwise equal to the
+# product's, tests/test_host_helpers.py); U is numpy PCG64(seed) uniform[-1,1).
+REF_WORKLOADS = {
+    "c4": dict(dim=3, degree=3, n_tau=4, cells=(32, 32, 32), lower=(0.0,) * 3, upper=(1.0,) * 3,
+               velocity=(1.0, 1.0, 1.0), dt=0.002, seed=3,
+               u0=lambda x, y, z: np.sin(2.0 * np.pi * (x + y + z)),
+               note="3-D + t advection N=3 (the north-star target)"),
+    "c2": dict(dim=2, degree=4, n_tau=5, cells=(256, 256), lower=(0.0,) * 2, upper=(1.0,) * 2,
+               velocity=(1.0, 0.5), dt=0.001, seed=1,
+               u0=lambda x, y, z: np.sin(2.0 * np.pi * x) * np.sin(2.0 * np.pi * y),
+               note="2-D advection N=4: 8,192,000 DOF per slab"),
+}
+
+
+def workload_sizes(w):
+    cells = int(np.prod(w["cells"]))
+    n_sdof = cells * (w["degree"] + 1) ** w["dim"]
+    return n_sdof, w["n_tau"] * n_sdof
+
+
+def bench_config(name, ws):
+    """The `config` object of both arms (identical by construction)."""
+    w = REF_WORKLOADS[name]
+    n_sdof, n_dof = workload_sizes(w)
+    return {"workload": f"{name}: {w['note']}", "op": "st_residual R(U)", "n_dof": n_dof,
+            "cells": list(w["cells"]), "degree": w["degree"], "n_tau": w["n_tau"],
+            "parallelism": f"replicas{ws}",
+            "l2": f"{NSETS} rotating (U,u_n,R) sets of "
+                  f"{(2 * n_dof + n_sdof) * 8 / 2**20:.0f} MiB (> 126 MB L2)"}
+
+
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_desc(O, threads):
+    return {"cpu_model": cpu_model(), "nproc": os.cpu_count(), "threads": threads,
+            "build": f"oracle {O.flags()} -ffp-contract=off"}
 
 
 def dist_env():
@@ -80,8 +129,13 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.marks = {}
         self._stop = threading.Event()
         self._t = None
+
+    def mark(self, name: str):
+        """Sample index at which a phase starts ("timed", "end")."""
+        self.marks[name] = len(self.samples)
 
     def _run_nvml(self):
         """NVML reads the same clock / event-reason counters as nvidia-smi, in
@@ -130,6 +184,10 @@ class ClockSampler:
         self._t.join(timeout=10)
 
     def summary(self):
+        """Median SM clock and the active event reasons over the samples taken
+        under load: the clock pre-roll, the warm-up and the timed region (the
+        same kernel throughout); `samples_timed` counts those inside the
+        timed region itself."""
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
@@ -137,68 +195,85 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
+        t0, t1 = self.marks.get("timed", 0), self.marks.get("end", len(self.samples))
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples), "samples_timed": max(0, t1 - t0),
+                "window": "clock pre-roll + warm-up + timed region (same kernel)"}
 
 
-def cpu_baseline(cfg, threads: int, budget_s: float):
+def oracle_inputs(name, O):
+    """(oracle Problem, U, u_n) of a bench workload, built from the oracle and
+    numpy alone (no product code)."""
+    w = REF_WORKLOADS[name]
+    pr = O.Problem(w["dim"], w["degree"], list(w["cells"]), list(w["lower"]), list(w["upper"]),
+                   list(w["velocity"]), n_tau=w["n_tau"])
+    _, n_dof = workload_sizes(w)
+    U = np.random.default_rng(w["seed"]).uniform(-1.0, 1.0, n_dof)
+    un = pr.interpolate(w["u0"])
+    return pr, U, un
+
+
+def cpu_baseline(name, threads: int, budget_s: float):
     """Oracle R(U) on the host cores (bounded sample: whole applies until budget)."""
     import oracle as O
+    O.use_native()
     O.set_threads(threads)
-    pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
-                   list(cfg.velocity), n_tau=cfg.n_tau)
-    from paper_2201_05800_b200 import configs as C
-    U = C.random_slab(cfg)
-    un = C.initial_state(cfg)
-    pr.st_residual(0.0, cfg.dt, un, U)  # warm-up
+    pr, U, un = oracle_inputs(name, O)
+    dt = REF_WORKLOADS[name]["dt"]
+    n_dof = U.size
+    pr.st_residual(0.0, dt, un, U)  # warm-up
     n = 0
     t0 = time.perf_counter()
     while True:
-        pr.st_residual(0.0, cfg.dt, un, U)
+        pr.st_residual(0.0, dt, un, U)
         n += 1
         if time.perf_counter() - t0 >= budget_s:
             break
     el = time.perf_counter() - t0
-    return n * cfg.n_dof / el, n, el
+    return n * n_dof / el, n, el, cpu_desc(O, threads)
 
 
 def run_reference(args):
-    from paper_2201_05800_b200 import configs as C
+    """The reference's CPU path (its restatement: the reference needs Eigen3,
+    absent here) with all host threads on the same workload, config, metric
+    and warm-up; rank 0 only.  Loads oracle/build/liboracle_native.so and
+    nothing of the product."""
     import oracle as O
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    cfg = C.CONFIGS[args.workload]
+    name = args.workload
+    O.use_native()
     threads = O.max_threads()
     O.set_threads(threads)
-    pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
-                   list(cfg.velocity), n_tau=cfg.n_tau)
-    U = C.random_slab(cfg)
-    un = C.initial_state(cfg)
-    for _ in range(min(args.warmup, 2)):
-        pr.st_residual(0.0, cfg.dt, un, U)
-    budget = float(os.environ.get("STG_REF_BUDGET_S", "60"))
+    pr, U, un = oracle_inputs(name, O)
+    dt = REF_WORKLOADS[name]["dt"]
+    n_dof = U.size
+    for _ in range(args.warmup):
+        pr.st_residual(0.0, dt, un, U)
+    budget = float(os.environ.get("STG_REF_BUDGET_S", "120"))
     n = 0
     t0 = time.perf_counter()
     while n < args.steps:
-        pr.st_residual(0.0, cfg.dt, un, U)
+        pr.st_residual(0.0, dt, un, U)
         n += 1
         if time.perf_counter() - t0 >= budget:
             break
     el = time.perf_counter() - t0
-    value = n * cfg.n_dof / el
+    value = n * n_dof / el
+    desc = cpu_desc(O, threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
-        "steps": n, "warmup": min(args.warmup, 2), "ms_per_step": 1e3 * el / n,
+        "steps": n, "warmup": args.warmup, "ms_per_step": 1e3 * el / n,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.note}", "n_dof": cfg.n_dof,
-                   "cells": list(cfg.cells), "degree": cfg.degree, "n_tau": cfg.n_tau},
+        "data": "synthetic", "config": bench_config(name, ws),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"{n} full R(U) applies of {cfg.name} (capped at "
-                                   f"{budget:.0f} s or --steps); reference unbuildable here "
-                                   "(Eigen3 absent), oracle restatement timed instead"},
+                         "sample": f"{n} full R(U) applies of {name} on {threads} threads "
+                                   f"({desc['cpu_model']}; capped at {budget:.0f} s or --steps); "
+                                   "the reference needs Eigen3 (absent), so its restatement "
+                                   "oracle/stdg_oracle.hpp is timed",
+                         **desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -225,32 +300,42 @@ def run_ours(args):
 
     # inputs resident in HBM; rotate NSETS (U, u_n, R) sets so consecutive
     # applies never hit L2 (each set is 144 MiB > 126 MB L2)
-    nsets = 3
     U0 = torch.as_tensor(C.random_slab(cfg), device=dev)
     un0 = torch.as_tensor(C.initial_state(cfg), device=dev)
-    Us = [U0.clone() for _ in range(nsets)]
-    uns = [un0.clone() for _ in range(nsets)]
-    Rs = [torch.empty(cfg.n_dof, dtype=torch.float64, device=dev) for _ in range(nsets)]
+    Us = [U0.clone() for _ in range(NSETS)]
+    uns = [un0.clone() for _ in range(NSETS)]
+    Rs = [torch.empty(cfg.n_dof, dtype=torch.float64, device=dev) for _ in range(NSETS)]
 
     def step(i):
-        k = i % nsets
+        k = i % NSETS
         op.st_residual(0.0, cfg.dt, uns[k], Us[k], out=Rs[k])
 
-    for i in range(args.warmup):
-        step(i)
-    torch.cuda.synchronize()
-
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = op.kernel_launches()
     with ClockSampler(dev.index) as clk:
+        # clock pre-roll: the same apply for >= preroll_s before the warm-up,
+        # so the clocks are at steady state and sampled even when the timed
+        # region itself is shorter than one NVML sample (20 steps = 0.6 ms)
+        t0 = time.perf_counter()
+        i = 0
+        while time.perf_counter() - t0 < args.preroll_s:
+            for _ in range(200):
+                step(i)
+                i += 1
+            torch.cuda.synchronize()
+        for i in range(args.warmup):
+            step(i)
+        torch.cuda.synchronize()
+        launches0 = op.kernel_launches()
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+        clk.mark("timed")
         ev0.record(stream)
         for i in range(args.steps):
             step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
+        clk.mark("end")
         if dist:
             dist.barrier()
     launches = op.kernel_launches() - launches0
@@ -261,11 +346,13 @@ def run_ours(args):
     hbm, hbm_src = peaks()
     alg = C.residual_bytes(cfg)
     achieved = alg / (ms_step / 1e3) / 1e9
-    traffic = None
+    traffic, traffic_src = None, None
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get("slab3d_n4_persist")
+            tj = json.loads(tf.read_text())
+            traffic = tj.get("slab3d_n4_persist")
+            traffic_src = tj.get("_source")
         except Exception:
             traffic = None
 
@@ -289,6 +376,17 @@ def run_ours(args):
     torch.cuda.synchronize()
     e2e_ms = reduce_max(ev0.elapsed_time(ev1), dist, dev)
     e2e_val = whole_job_value(ws, cfg.n_dof, e2e_steps, e2e_ms)
+    # the host path's output is the device path's output, bit for bit
+    e2e_exact = bool(np.array_equal(npR, Rs[0].cpu().numpy())) if NSETS else None
+    # the same call from pageable host memory (what a caller's std::vector is)
+    pgU, pgun, pgR = np.array(npU), np.array(npun), np.empty(cfg.n_dof)
+    op.st_residual_host(0.0, cfg.dt, pgun, pgU, out=pgR)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(max(3, e2e_steps // 5)):
+        op.st_residual_host(0.0, cfg.dt, pgun, pgU, out=pgR)
+    torch.cuda.synchronize()
+    pg_s = (time.perf_counter() - t0) / max(3, e2e_steps // 5)
 
     extra = {}
     if not args.no_extra and rank == 0:
@@ -297,10 +395,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         try:
-            v, n, el = cpu_baseline(cfg, 1, args.cpu_budget)
+            v, n, el, desc = cpu_baseline(args.workload, 1, args.cpu_budget)
             cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"{n} full R(U) applies of {cfg.name} ({el:.1f} s, 1 thread; the "
-                             "reference is single-threaded, SPEC.md:426)"}
+                   "sample": f"{n} full R(U) applies of {cfg.name} ({el:.1f} s, 1 thread of "
+                             f"{desc['cpu_model']}; the reference is single-threaded, "
+                             "SPEC.md:426)", **desc}
         except Exception as e:  # oracle missing on the box: report, do not fake
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "port",
                    "sample": f"unavailable: {e}"}
@@ -310,20 +409,18 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: {cfg.note}", "op": "st_residual R(U)",
-                       "n_dof": cfg.n_dof, "cells": list(cfg.cells), "degree": cfg.degree,
-                       "n_tau": cfg.n_tau, "parallelism": f"replicas{ws}",
-                       "l2": f"{nsets} rotating (U,u_n,R) sets of "
-                             f"{(2 * cfg.n_dof + cfg.n_sdof) * 8 / 2**20:.0f} MiB (> 126 MB L2)"},
+            "config": bench_config(args.workload, ws),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic,
-                         "peak_source": hbm_src,
+                         "traffic_source": traffic_src, "peak_source": hbm_src,
                          "algorithmic_bytes_per_launch": alg},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "steps": e2e_steps,
                     "h2d_bytes_per_step": 8 * (cfg.n_dof + cfg.n_sdof),
                     "d2h_bytes_per_step": 8 * cfg.n_dof,
-                    "path": "stg_st_residual_host (pinned host buffers)"},
+                    "path": "stg_st_residual_host (pinned host buffers)",
+                    "output_bitwise_equal_device": e2e_exact,
+                    "pageable_dof_per_s": cfg.n_dof / pg_s},
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "extra": extra,
@@ -335,33 +432,63 @@ def run_ours(args):
 
 
 def timed(fn, stream, torch, reps):
+    """ms per call of fn(i) over reps calls (CUDA events on the stream), after
+    one warm call; fn rotates its own buffer sets by i."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fn()
+    fn(0)
     torch.cuda.synchronize()
     e0.record(stream)
-    for _ in range(reps):
-        fn()
+    for i in range(reps):
+        fn(i)
     e1.record(stream)
     torch.cuda.synchronize()
     return e0.elapsed_time(e1) / reps
 
 
-def extras(op, cfg, C, NewtonConfig, torch, dev, args):
-    """J.v and stage-apply throughput and the slab-solve time (not the headline)."""
+def rotating_sets(cfg, C, torch, dev, seed0):
+    """NSETS (U, v, u_n, out) sets for the apply rates, each set > 126 MB of
+    L2 at c2 / c4 (c3's 8 MiB vectors are L2-resident by nature)."""
+    sets = []
+    for k in range(NSETS):
+        sets.append((torch.as_tensor(C.random_slab(cfg, seed0 + k), device=dev),
+                     torch.as_tensor(C.random_slab(cfg, seed0 + 50 + k), device=dev),
+                     torch.as_tensor(C.initial_state(cfg), device=dev),
+                     torch.empty(cfg.n_dof, dtype=torch.float64, device=dev)))
+    return sets
+
+
+def apply_rates(op, cfg, C, torch, dev, reps, fd_eps=0.0):
+    """R(U), J.v and both stage residuals, rotating NSETS buffer sets."""
     stream = torch.cuda.current_stream()
-    out = {}
-    U = torch.as_tensor(C.random_slab(cfg), device=dev)
-    v = torch.as_tensor(C.random_slab(cfg, 99), device=dev)
-    un = torch.as_tensor(C.initial_state(cfg), device=dev)
-    R = torch.empty_like(U)
     hbm, _ = peaks()
-    ms = timed(lambda: op.st_jvp(0.0, cfg.dt, None, v, out=R), stream, torch, 50)
-    out["jvp"] = {"dof_per_s": cfg.n_dof / (ms / 1e3), "ms": ms,
-                  "hbm_frac": C.jvp_bytes(cfg) / (ms / 1e3) / 1e9 / hbm}
+    S = rotating_sets(cfg, C, torch, dev, 1000)
+    if cfg.model == 1:  # Burgers: states near u0
+        S = [(un.repeat(cfg.n_tau) + 0.01 * U, v, un, R) for (U, v, un, R) in S]
+    out = {}
+
+    def rate(ms, nbytes):
+        return {"dof_per_s": cfg.n_dof / (ms / 1e3), "ms": ms,
+                "hbm_frac": nbytes / (ms / 1e3) / 1e9 / hbm}
+    ms = timed(lambda i: op.st_residual(0.0, cfg.dt, S[i % NSETS][2], S[i % NSETS][0],
+                                        out=S[i % NSETS][3]), stream, torch, reps)
+    out["residual"] = rate(ms, C.residual_bytes(cfg))
+    Uarg = (lambda k: S[k][0]) if cfg.model == 1 else (lambda k: None)
+    ms = timed(lambda i: op.st_jvp(0.0, cfg.dt, Uarg(i % NSETS), S[i % NSETS][1], fd_eps=fd_eps,
+                                   out=S[i % NSETS][3]), stream, torch, reps)
+    out["jvp"] = rate(ms, C.jvp_bytes(cfg) + (8 * cfg.n_dof if cfg.model == 1 else 0))
+    if cfg.model == 1:
+        out["jvp"]["note"] = f"fused central-difference J.v, fd_eps={fd_eps}: reads U and v"
     for form, name in ((1, "stage_residual_a_inv"), (0, "stage_residual_a")):
-        ms = timed(lambda: op.stage_residual(form, 0.0, cfg.dt, un, U, out=R), stream, torch, 50)
-        out[name] = {"dof_per_s": cfg.n_dof / (ms / 1e3), "ms": ms,
-                     "hbm_frac": C.residual_bytes(cfg) / (ms / 1e3) / 1e9 / hbm}
+        ms = timed(lambda i: op.stage_residual(form, 0.0, cfg.dt, S[i % NSETS][2], S[i % NSETS][0],
+                                               out=S[i % NSETS][3]), stream, torch, reps)
+        out[name] = rate(ms, C.residual_bytes(cfg))
+    out["buffers"] = f"{NSETS} rotating sets"
+    return out
+
+
+def extras(op, cfg, C, NewtonConfig, torch, dev, args):
+    """Apply rates of every config, the slab-solve times (not the headline)."""
+    out = {"c4_applies": apply_rates(op, cfg, C, torch, dev, 60)}
     out.update(solves(op, cfg, C, NewtonConfig, torch, dev, args))
     return out
 
@@ -441,21 +568,83 @@ def rank3_experiments(torch, dev, args):
     return res
 
 
+def _best_wall(torch, fn, reps=3):
+    """min wall time of reps calls (CUDA sync on both sides) and the last result"""
+    best, r = None, None
+    for _ in range(reps):
+        t, r = _wall(torch, fn)
+        best = t if best is None else min(best, t)
+    return best, r
+
+
+def cpp_mirror_e2e(cfg):
+    """Time the C++ mirror's stdg_step (include/stdgsem_gpu.hpp, std::vector
+    in and out: pageable host memory) on the c4 slab; compiled here with g++
+    against libstg_cuda.so (scripts/e2e_solve_cpp.cpp)."""
+    import shutil
+    src = ROOT / "scripts" / "e2e_solve_cpp.cpp"
+    libdir = ROOT / "paper_2201_05800_b200"
+    exe = Path("/tmp") / f"stg_e2e_solve_{os.getpid()}"
+    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else shutil.which("g++")
+    subprocess.run([cxx, "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(src), f"-L{libdir}",
+                    "-lstg_cuda", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True,
+                   capture_output=True, timeout=300)
+    try:
+        r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600, check=True)
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    finally:
+        exe.unlink(missing_ok=True)
+
+
 def solves(op, cfg, C, NewtonConfig, torch, dev, args):
-    """Slab solves of every BASELINE config (device-resident u_n, from guess
-    1 (x) u_n, wall time with a CUDA sync on both sides), the c5 stage system
-    against the c4 slab, and the CPU oracle's c4 / c1 solve times beside them."""
+    """Slab solves of every BASELINE config (wall time with a CUDA sync on both
+    sides, best of 3), from device-resident u_n and end to end from host
+    buffers; the c5 stage system against the c4 slab; the CPU oracle's solves
+    beside them (same NewtonConfig; the oracle's GMRES is unpreconditioned, so
+    the device also runs unpreconditioned for a like-for-like pair)."""
     from paper_2201_05800_b200.api import SlabOperator
     from paper_2201_05800_b200 import _lib as L
     out = {}
     un = torch.as_tensor(C.initial_state(cfg), device=dev)
     # c4: one Newton step, GMRES(30) to rel tol 1e-10 (||r||_2 <= 1e-10 ||b||_2)
-    nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10, gmres_restart=30)
-    op.stdg_step(0.0, cfg.dt, un, nc)  # warm (workspace allocation)
-    t, (U4, u4, info) = _wall(torch, lambda: op.stdg_step(0.0, cfg.dt, un, nc))
-    out["c4_slab_solve"] = {"seconds": t, "gmres_tol": 1e-10, "newton": info.newton_iterations,
-                            "gmres_iterations": info.linear_iterations,
-                            "final_residual_inf": info.final_residual}
+    kw = dict(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10, gmres_restart=30)
+    c4 = {}
+    for pname, pc in (("auto_fdm_eblock", L.STG_PRECOND_AUTO), ("none", L.STG_PRECOND_NONE),
+                      ("jacobi_eigen_default", L.STG_PRECOND_JACOBI),
+                      ("tblock", L.STG_PRECOND_TBLOCK)):
+        nc = NewtonConfig(precond=pc, **kw)
+        op.stdg_step(0.0, cfg.dt, un, nc)  # warm (workspace allocation)
+        t, (U4x, _, info) = _best_wall(torch, lambda: op.stdg_step(0.0, cfg.dt, un, nc))
+        c4[pname] = {"seconds": t, "newton": info.newton_iterations,
+                     "gmres_iterations": info.linear_iterations,
+                     "final_residual_inf": info.final_residual}
+        if pc == L.STG_PRECOND_AUTO:
+            U4 = U4x
+    out["c4_slab_solve"] = {"gmres_tol": 1e-10, "by_preconditioner": c4,
+                            "seconds": c4["auto_fdm_eblock"]["seconds"]}
+    # c4 end to end from host buffers: stg_stdg_step_host (H2D of u_n, solve,
+    # D2H of U and u_next inside the call), pinned and pageable
+    nc = NewtonConfig(**kw)
+    un_h = C.initial_state(cfg)
+    pin_un = torch.empty(cfg.n_sdof, dtype=torch.float64, pin_memory=True)
+    pin_U = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    pin_u1 = torch.empty(cfg.n_sdof, dtype=torch.float64, pin_memory=True)
+    pin_un.numpy()[:] = un_h
+    e2e = {}
+    for mem, (a, b, c) in (("pinned", (pin_un.numpy(), pin_U.numpy(), pin_u1.numpy())),
+                           ("pageable", (np.array(un_h), np.empty(cfg.n_dof),
+                                         np.empty(cfg.n_sdof)))):
+        op.stdg_step_host(0.0, cfg.dt, a, nc, U=b, u_next=c)
+        t, _ = _best_wall(torch, lambda: op.stdg_step_host(0.0, cfg.dt, a, nc, U=b, u_next=c))
+        e2e[mem] = {"seconds": t, "exact_vs_device": bool(np.array_equal(b, U4.cpu().numpy()))}
+    e2e["h2d_bytes"] = 8 * cfg.n_sdof
+    e2e["d2h_bytes"] = 8 * (cfg.n_dof + cfg.n_sdof)
+    e2e["path"] = "stg_stdg_step_host via ctypes"
+    try:
+        e2e["cpp_mirror"] = cpp_mirror_e2e(cfg)
+    except Exception as e:
+        e2e["cpp_mirror"] = f"unavailable: {e}"
+    out["c4_slab_solve_e2e"] = e2e
     # c4 marched over 10 slabs on the device (stg_stdg_integrate, stdg.hpp:152-173)
     op.stdg_integrate(0.0, un, 2 * cfg.dt, 2, nc)  # warm
     t10, (_, _, _, info10) = _wall(
@@ -466,33 +655,32 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     # c5: Lobatto IIIC s=4 stage system (A^-1 form) on the c4 mesh, vs the c4 slab
     c5 = C.CONFIGS["c5"]
     op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, un, nc)  # warm (lazy module load of its kernels)
-    t, (U5, u5, info5) = _wall(torch, lambda: op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, un, nc))
+    t, (U5, u5, info5) = _best_wall(torch, lambda: op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, un, nc))
     gap = float((U5 - U4).abs().max() / U4.abs().max())
     out["c5_stage_solve"] = {"seconds": t, "newton": info5.newton_iterations,
                              "gmres_iterations": info5.linear_iterations,
                              "max_rel_gap_to_c4_slab": gap}
-    # c2: 2-D N=4, R(U) rate and slab solve
+    del U5, u5
+    # c2: 2-D N=4 apply rates and slab solve
     c2 = C.CONFIGS["c2"]
     op2 = SlabOperator(**c2.kwargs())
-    U2 = torch.as_tensor(C.random_slab(c2), device=dev)
     u2 = torch.as_tensor(C.initial_state(c2), device=dev)
-    R2 = torch.empty_like(U2)
-    ms = timed(lambda: op2.st_residual(0.0, c2.dt, u2, U2, out=R2), torch.cuda.current_stream(),
-               torch, 30)
-    hbm, _ = peaks()
-    op2.stdg_step(0.0, c2.dt, u2, nc)
-    t, (_, _, info2) = _wall(torch, lambda: op2.stdg_step(0.0, c2.dt, u2, nc))
-    out["c2"] = {"residual_dof_per_s": c2.n_dof / (ms / 1e3),
-                 "residual_hbm_frac": C.residual_bytes(c2) / (ms / 1e3) / 1e9 / hbm,
-                 "slab_solve_s": t, "gmres_iterations": info2.linear_iterations}
-    del op2, U2, u2, R2
+    out["c2"] = {"applies": apply_rates(op2, c2, C, torch, dev, 40)}
+    for pname, pc in (("auto_dense_eblock", L.STG_PRECOND_AUTO), ("none", L.STG_PRECOND_NONE)):
+        nc2 = NewtonConfig(precond=pc, **kw)
+        op2.stdg_step(0.0, c2.dt, u2, nc2)
+        t, (_, _, info2) = _best_wall(torch, lambda: op2.stdg_step(0.0, c2.dt, u2, nc2))
+        out["c2"][f"slab_solve_{pname}"] = {"seconds": t,
+                                            "gmres_iterations": info2.linear_iterations}
+    out["c2"]["slab_solve_s"] = out["c2"]["slab_solve_auto_dense_eblock"]["seconds"]
+    del op2, u2
     # c1: 1000 R(U) applies (launch-latency bound) and the GMRES slab solve at 1e-12
     c1 = C.CONFIGS["c1"]
     op1 = SlabOperator(**c1.kwargs())
     u1 = torch.as_tensor(C.initial_state(c1), device=dev)
     U1 = torch.as_tensor(C.random_slab(c1), device=dev)
     R1 = torch.empty_like(U1)
-    us = 1e3 * timed(lambda: op1.st_residual(0.0, c1.dt, u1, U1, out=R1),
+    us = 1e3 * timed(lambda i: op1.st_residual(0.0, c1.dt, u1, U1, out=R1),
                      torch.cuda.current_stream(), torch, 1000)
     # the same 1000 applies captured once in a CUDA graph and replayed: the
     # device-side cost without Python/ctypes launch overhead
@@ -519,25 +707,28 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
         us_graph = f"unavailable: {e}"
     nc1 = NewtonConfig(abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12)
     op1.stdg_step(0.0, c1.dt, u1, nc1)
-    t1, (_, _, info1) = _wall(torch, lambda: op1.stdg_step(0.0, c1.dt, u1, nc1))
+    t1, (_, _, info1) = _best_wall(torch, lambda: op1.stdg_step(0.0, c1.dt, u1, nc1))
     out["c1"] = {"us_per_residual_python_loop": us, "us_per_residual_cuda_graph": us_graph,
                  "slab_solve_s": t1, "gmres_iterations": info1.linear_iterations}
-    # c3: Burgers, inexact Newton-GMRES with FD J.v (eps 1e-7), 10 slabs
+    # c3: Burgers, apply rates, inexact Newton-GMRES with FD J.v (eps 1e-7), 10 slabs
     c3 = C.CONFIGS["c3"]
     op3 = SlabOperator(**c3.kwargs())
+    out["c3_applies"] = apply_rates(op3, c3, C, torch, dev, 200, fd_eps=1e-7)
+    out["c3_applies"]["buffers"] += " (8 MiB vectors: L2-resident)"
     u = torch.as_tensor(C.initial_state(c3), device=dev)
     nc3 = NewtonConfig(abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-6, fd_eps=1e-7)
     op3.stdg_step(0.0, c3.dt, u, nc3)  # warm
     its = []
 
     def ten():
+        its.clear()
         uu = u
         for k in range(10):
             _, uu, inf = op3.stdg_step(k * c3.dt, c3.dt, uu, nc3)
             its.append([inf.newton_iterations, inf.linear_iterations])
         return uu
-    t3, _ = _wall(torch, ten)
-    out["c3_10_slabs"] = {"seconds": t3, "per_slab_s": t3 / 10, "newton_gmres": its}
+    t3, _ = _best_wall(torch, ten, 2)
+    out["c3_10_slabs"] = {"seconds": t3, "per_slab_s": t3 / 10, "newton_gmres": list(its)}
     # rank 3: the reference's own experiments on the device --
     # rotating pulse (acceptance criterion 6, experiments.hpp:133-175) and the
     # Euler vortex (criterion 9, experiments.hpp:188-262)
@@ -545,26 +736,42 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
         out["rank3"] = rank3_experiments(torch, dev, args)
     except Exception as e:  # report, do not fail the bench
         out["rank3"] = f"unavailable: {e}"
-    # CPU reference (oracle) solves beside them
+    # CPU reference (oracle, -march=native) solves beside them, same NewtonConfig
     if not args.no_cpu:
         try:
             import oracle as O
+            O.use_native()
             thr = O.max_threads()
             O.set_threads(thr)
-            pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
-                           list(cfg.velocity), n_tau=cfg.n_tau)
+            cpu = {**cpu_desc(O, thr), "kind": "port (unpreconditioned MGS GMRES(30))"}
+            pr, _, un_c = oracle_inputs("c4", O)
             t0 = time.perf_counter()
-            _, _, nit, lin = pr.stdg_step(0.0, cfg.dt, C.initial_state(cfg), linear=O.GMRES,
+            _, _, nit, lin = pr.stdg_step(0.0, cfg.dt, un_c, linear=O.GMRES,
                                           abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10)
-            out["cpu_c4_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": thr,
-                                        "gmres_iterations": lin, "kind": "port (MGS GMRES)"}
+            cpu["c4_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": thr,
+                                    "gmres_iterations": lin, "newton": nit}
+            pr2, _, un2 = oracle_inputs("c2", O)
+            t0 = time.perf_counter()
+            _, _, nit2, lin2 = pr2.stdg_step(0.0, c2.dt, un2, linear=O.GMRES,
+                                             abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10)
+            cpu["c2_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": thr,
+                                    "gmres_iterations": lin2, "newton": nit2}
+            del pr, pr2
+            p3 = O.Problem(1, 3, [65536], [0.0], [2 * np.pi], [0.0], model=O.BURGERS, n_tau=4)
+            t0 = time.perf_counter()
+            _, _, nit3, lin3 = p3.stdg_step(0.0, c3.dt, C.initial_state(c3), linear=O.GMRES,
+                                            abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-6)
+            cpu["c3_first_slab"] = {"seconds": time.perf_counter() - t0, "threads": thr,
+                                    "newton": nit3, "gmres_iterations": lin3,
+                                    "note": "exact Burgers Jacobian action"}
             O.set_threads(1)
             p1 = O.Problem(1, 3, [64], [0.0], [1.0], [1.0], n_tau=4)
             t0 = time.perf_counter()
             _, _, _, lin1 = p1.stdg_step(0.0, c1.dt, C.initial_state(c1), linear=O.GMRES,
                                          abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-12)
-            out["cpu_c1_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": 1,
-                                        "gmres_iterations": lin1}
+            cpu["c1_slab_solve"] = {"seconds": time.perf_counter() - t0, "threads": 1,
+                                    "gmres_iterations": lin1}
+            out["cpu_solves"] = cpu
         except Exception as e:
             out["cpu_solves"] = f"unavailable: {e}"
     return out
@@ -581,6 +788,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
+    ap.add_argument("--preroll-s", type=float, default=0.5)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -15,6 +15,7 @@
 // (there is no CPU path).
 #pragma once
 
+#include <cmath>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -37,19 +38,27 @@ struct AdmissibilityError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
+// NonconvergenceError (newton.hpp:40-48): the last Newton iterate and the
+// residual history, rethrown with the step context (stdg.hpp:132-137).
 struct NonconvergenceError : std::runtime_error {
   Vec last_iterate;
   std::vector<double> residual_history;
-  NonconvergenceError(const std::string& what, std::vector<double> history)
-      : std::runtime_error(what), residual_history(std::move(history)) {}
+  NonconvergenceError(const std::string& what, Vec u, std::vector<double> history)
+      : std::runtime_error(what),
+        last_iterate(std::move(u)),
+        residual_history(std::move(history)) {}
 };
+
+inline std::vector<double> history_of(const stg_solve_info& info) {
+  return std::vector<double>(info.residual_history, info.residual_history + info.n_history);
+}
 
 inline void check(int code, const stg_handle* h) {
   if (code == STG_OK) return;
   const std::string msg = stg_last_error(h);
   switch (code) {
     case STG_ERR_INVALID: throw std::invalid_argument(msg);
-    case STG_ERR_NONCONVERGENCE: throw NonconvergenceError(msg, {});
+    case STG_ERR_NONCONVERGENCE: throw NonconvergenceError(msg, {}, {});
     case STG_ERR_CUDA: throw CudaError(msg);
     case STG_ERR_ADMISSIBILITY: throw AdmissibilityError(msg);
     default: throw std::runtime_error(msg);
@@ -123,6 +132,125 @@ inline DgSpace dg_space(const Mesh& m, int p, int r = 1) {  // mesh.hpp:93-110
   if (p < 1) throw std::invalid_argument("dg_space: need p >= 1 (p = 0 has no LGL rule)");
   if (r < 1) throw std::invalid_argument("dg_space: need r >= 1");
   return DgSpace{m, p, r};
+}
+
+// ---- host-side field helpers (mesh.hpp:82-90, 113-181) -----------------------
+// Same index map as the library: cell = (cz*ny + cy)*nx + cx, node x-fastest,
+// coefficient (cell * npc + node) * r + comp (mesh.hpp:70-81; d = 3 extended).
+inline Vec lgl_nodes(int n) {  // lgl_rule(n).nodes (quadrature.hpp:66-105)
+  Vec x(static_cast<size_t>(n)), w(static_cast<size_t>(n));
+  check(stg_lgl_rule(n, x.data(), w.data()), nullptr);
+  return x;
+}
+inline Vec lgl_weights(int n) {
+  Vec x(static_cast<size_t>(n)), w(static_cast<size_t>(n));
+  check(stg_lgl_rule(n, x.data(), w.data()), nullptr);
+  return w;
+}
+inline int nodes_per_cell(const DgSpace& s) {
+  int npc = 1;
+  for (int a = 0; a < s.mesh.d; ++a) npc *= s.p + 1;
+  return npc;
+}
+inline int n_cells(const Mesh& m) {
+  int nc = 1;
+  for (int a = 0; a < m.d; ++a) nc *= m.cells[size_t(a)];
+  return nc;
+}
+
+// node_coord (mesh.hpp:82-90): x_a = lower_a + (c_a + (1 + xi_{i_a}) / 2) h_a,
+// evaluated in the reference's operation order (bitwise equal)
+inline Vec node_coord(const DgSpace& s, const Vec& xi, int cell, int node) {
+  const int n = s.p + 1;
+  int ci[3] = {0, 0, 0}, ni[3] = {0, 0, 0};
+  int c = cell, q = node;
+  for (int a = 0; a < s.mesh.d; ++a) {
+    ci[a] = c % s.mesh.cells[size_t(a)];
+    c /= s.mesh.cells[size_t(a)];
+    ni[a] = q % n;
+    q /= n;
+  }
+  Vec x(size_t(s.mesh.d));
+  for (int a = 0; a < s.mesh.d; ++a) {
+    const double h = (s.mesh.upper[size_t(a)] - s.mesh.lower[size_t(a)]) / s.mesh.cells[size_t(a)];
+    x[size_t(a)] = s.mesh.lower[size_t(a)] + (ci[a] + 0.5 * (1.0 + xi[size_t(ni[a])])) * h;
+  }
+  return x;
+}
+inline Vec node_coord(const DgSpace& s, int cell, int node) {
+  return node_coord(s, lgl_nodes(s.p + 1), cell, node);
+}
+
+struct DiscreteField {  // mesh.hpp:113-117
+  DgSpace space;
+  Vec coeffs;
+  double time_tag = 0.0;
+};
+
+// interpolate (mesh.hpp:145-157): f maps a point to r component values
+template <class F>
+DiscreteField interpolate(const DgSpace& s, F&& f, double t = 0.0) {
+  DiscreteField field{s, Vec(size_t(s.dof())), t};
+  const Vec xi = lgl_nodes(s.p + 1);
+  const int npc = nodes_per_cell(s), nc = n_cells(s.mesh);
+  for (int cell = 0; cell < nc; ++cell)
+    for (int node = 0; node < npc; ++node) {
+      const Vec val = f(node_coord(s, xi, cell, node));
+      for (int comp = 0; comp < s.r; ++comp)
+        field.coeffs[(size_t(cell) * npc + node) * s.r + comp] = val[size_t(comp)];
+    }
+  return field;
+}
+
+// interpolate_scalar (mesh.hpp:159-165)
+template <class F>
+DiscreteField interpolate_scalar(const DgSpace& s, F&& f, double t = 0.0) {
+  return interpolate(s, [&](const Vec& x) { return Vec{f(x)}; }, t);
+}
+
+struct GlobalMassDiagonal {  // mesh.hpp:121-124
+  DgSpace space;
+  Vec diag;
+};
+
+// global_mass (mesh.hpp:125-141): cell volume / 2^d times tensor LGL weights,
+// replicated across the r components
+inline GlobalMassDiagonal global_mass(const DgSpace& s) {
+  GlobalMassDiagonal m{s, Vec(size_t(s.dof()))};
+  double vol = 1.0;
+  for (int a = 0; a < s.mesh.d; ++a)
+    vol *= (s.mesh.upper[size_t(a)] - s.mesh.lower[size_t(a)]) / s.mesh.cells[size_t(a)];
+  double pw = 1.0;
+  for (int a = 0; a < s.mesh.d; ++a) pw *= 2.0;
+  const double vol_scale = vol / pw;
+  const Vec w = lgl_weights(s.p + 1);
+  const int n = s.p + 1, npc = nodes_per_cell(s), nc = n_cells(s.mesh);
+  for (int cell = 0; cell < nc; ++cell)
+    for (int node = 0; node < npc; ++node) {
+      double wn = w[size_t(node % n)];
+      if (s.mesh.d >= 2) wn *= w[size_t((node / n) % n)];
+      if (s.mesh.d == 3) wn *= w[size_t(node / (n * n))];
+      for (int comp = 0; comp < s.r; ++comp)
+        m.diag[(size_t(cell) * npc + node) * s.r + comp] = vol_scale * wn;
+    }
+  return m;
+}
+
+// l2_norm (mesh.hpp:167-172): one square root of the mass-weighted sum
+inline double l2_norm(const DiscreteField& f) {
+  const Vec d = global_mass(f.space).diag;
+  double acc = 0.0;
+  for (size_t i = 0; i < d.size(); ++i) acc += f.coeffs[i] * f.coeffs[i] * d[i];
+  return std::sqrt(acc);
+}
+
+// l2_error (mesh.hpp:174-181): exact(x, t) returns the r component values
+template <class F>
+double l2_error(const DiscreteField& field, F&& exact, double t) {
+  DiscreteField diff = interpolate(field.space, [&](const Vec& x) { return exact(x, t); }, t);
+  for (size_t i = 0; i < diff.coeffs.size(); ++i)
+    diff.coeffs[i] = field.coeffs[i] - diff.coeffs[i];
+  return l2_norm(diff);
 }
 
 // FluxModel (models.hpp:23-36): which of the library's models, with its data.
@@ -344,10 +472,8 @@ inline StdgStepResult stdg_step(const SemiDiscreteSystem& system, const SbpOpera
   const stg_newton_config c = cfg.c();
   const int code = stg_stdg_step_host(o.handle(), t_n, dt, u_n.data(), &c, r.U.data(),
                                       r.u_next.data(), &info);
-  if (code == STG_ERR_NONCONVERGENCE)
-    throw NonconvergenceError(stg_last_error(o.handle()),
-                              std::vector<double>(info.residual_history,
-                                                  info.residual_history + info.n_history));
+  if (code == STG_ERR_NONCONVERGENCE)  // the library left the last iterate in U
+    throw NonconvergenceError(stg_last_error(o.handle()), std::move(r.U), history_of(info));
   check(code, o.handle());
   r.newton_iterations = info.newton_iterations;
   r.linear_iterations = info.linear_iterations;
@@ -378,9 +504,15 @@ inline StdgTrajectory stdg_integrate(const SemiDiscreteSystem& system, const Sbp
   stg_solve_info info{};
   const int code = stg_stdg_integrate(o.handle(), t0, du.data(), t_end, n_steps, &c, uf.data(),
                                       st.data(), sol.data(), &info);
-  if (code == STG_ERR_NONCONVERGENCE)
-    throw NonconvergenceError(stg_last_error(o.handle()),
-                              Vec(info.residual_history, info.residual_history + info.n_history));
+  if (code == STG_ERR_NONCONVERGENCE) {  // the failing slab's last iterate is in its slot
+    Vec last;
+    if (info.failed_step >= 0) {
+      const Vec sols = sol.download();
+      last.assign(sols.begin() + long(size_t(info.failed_step) * o.n_dof()),
+                  sols.begin() + long(size_t(info.failed_step + 1) * o.n_dof()));
+    }
+    throw NonconvergenceError(stg_last_error(o.handle()), std::move(last), history_of(info));
+  }
   check(code, o.handle());
   const Vec all = st.download(), sols = sol.download();
   for (int k = 0; k <= n_steps; ++k)
@@ -413,10 +545,8 @@ inline RkStepResult rk_step(const SemiDiscreteSystem& system, const ButcherTable
   const stg_newton_config c = cfg.c();
   const int code = stg_rk_step_host(o.handle(), int(jac_form), t, dt, u.data(), &c, U.data(),
                                     r.u_next.data(), &info);
-  if (code == STG_ERR_NONCONVERGENCE)
-    throw NonconvergenceError(stg_last_error(o.handle()),
-                              std::vector<double>(info.residual_history,
-                                                  info.residual_history + info.n_history));
+  if (code == STG_ERR_NONCONVERGENCE)  // the library left the last iterate in U
+    throw NonconvergenceError(stg_last_error(o.handle()), std::move(U), history_of(info));
   check(code, o.handle());
   const size_t ns = o.n_sdof();
   for (int j = 0; j < tab.s; ++j)

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define STG_ABI_VERSION 2
+#define STG_ABI_VERSION 3
 
 #define STG_OK 0
 #define STG_ERR_INVALID 1
@@ -87,6 +87,13 @@ extern "C" {
 #define STG_PRECOND_TBLOCK 1
 #define STG_PRECOND_EBLOCK 2
 #define STG_PRECOND_AUTO 3
+/* ABI v3: Eigen's default DiagonalPreconditioner -- P = diag(J), with 1 in
+ * place of a zero diagonal entry (Eigen's documented rule).  The slab
+ * Jacobian's diagonal is exactly zero at interior nodes
+ * (test_experiments.cpp:109-111), so this is mostly the identity there;
+ * provided so the device solve can run the reference's own algorithm.
+ * Advection only. */
+#define STG_PRECOND_JACOBI 4
 
 /* Kernel selection (for tests / benchmarking; AUTO picks the fastest valid). */
 #define STG_KERNEL_AUTO 0
@@ -130,13 +137,20 @@ typedef struct stg_newton_config {
 } stg_newton_config;
 
 #define STG_MAX_HISTORY 64
-/* NewtonResult (newton.hpp:93-98) plus Krylov statistics. */
+/* NewtonResult (newton.hpp:93-98) plus Krylov statistics.
+ * On STG_ERR_NONCONVERGENCE (NonconvergenceError, newton.hpp:40-48) the
+ * record describes the failed solve: the Newton / GMRES iterations done, the
+ * last residual norm and the residual history; the solver's last iterate is
+ * left in the caller's U (the step's U, or the failing step's slot of
+ * U_slabs / U_stages in the integrators -- `failed_step` names it). */
 typedef struct stg_solve_info {
   int newton_iterations;
   int linear_iterations;   /* total GMRES iterations over all Newton steps */
   double final_residual;   /* ||res||_inf */
   int n_history;
   double residual_history[STG_MAX_HISTORY];
+  int failed_step;         /* ABI v3: integrators, index of the step that did not
+                              converge; -1 otherwise */
 } stg_solve_info;
 
 /* Defaults of NewtonConfig (newton.hpp:30-38). */

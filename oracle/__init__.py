@@ -17,6 +17,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 LIB_PATH = HERE / "build" / "liboracle.so"
+NATIVE_PATH = HERE / "build" / "liboracle_native.so"
 
 _dp = ctypes.POINTER(ctypes.c_double)
 _ip = ctypes.POINTER(ctypes.c_int)
@@ -33,13 +34,35 @@ def build(force: bool = False) -> Path:
 
 
 _LIB = None
+_USE_NATIVE = False
+
+
+def use_native() -> bool:
+    """Switch to the -march=native build (the CPU-baseline legs of bench.py;
+    BASELINE.md), compiled on this host.  Must run before the first lib()
+    call; returns False (portable build kept) if the native build fails."""
+    global _USE_NATIVE
+    if _LIB is not None:
+        return _USE_NATIVE
+    try:
+        subprocess.run(["make", "-B", "-C", str(HERE), "-s", "native"], check=True,
+                       capture_output=True, timeout=600)
+        _USE_NATIVE = NATIVE_PATH.exists()
+    except Exception:
+        _USE_NATIVE = False
+    return _USE_NATIVE
+
+
+def flags() -> str:
+    return "-O3 -march=native" if _USE_NATIVE else "-O3 -march=x86-64-v3"
 
 
 def lib() -> ctypes.CDLL:
     global _LIB
     if _LIB is None:
-        build()
-        L = ctypes.CDLL(str(LIB_PATH))
+        if not _USE_NATIVE:
+            build()
+        L = ctypes.CDLL(str(NATIVE_PATH if _USE_NATIVE else LIB_PATH))
         L.or_last_error.restype = ctypes.c_char_p
         L.or_dof.restype = ctypes.c_longlong
         L.or_dof.argtypes = [ctypes.c_void_p]

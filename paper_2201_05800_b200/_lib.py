@@ -19,6 +19,7 @@ STG_FORM_A, STG_FORM_A_INV = 0, 1
 STG_LINEAR_AUTO, STG_LINEAR_GMRES = 0, 3
 STG_KERNEL_AUTO, STG_KERNEL_GENERIC, STG_KERNEL_FAST = 0, 1, 2
 STG_PRECOND_NONE, STG_PRECOND_TBLOCK, STG_PRECOND_EBLOCK, STG_PRECOND_AUTO = 0, 1, 2, 3
+STG_PRECOND_JACOBI = 4
 STG_MAX_HISTORY = 64
 
 # every symbol include/stg_cuda.h declares
@@ -57,6 +58,7 @@ class StgSolveInfo(ctypes.Structure):
         ("newton_iterations", ctypes.c_int), ("linear_iterations", ctypes.c_int),
         ("final_residual", ctypes.c_double), ("n_history", ctypes.c_int),
         ("residual_history", ctypes.c_double * STG_MAX_HISTORY),
+        ("failed_step", ctypes.c_int),
     ]
 
 

@@ -31,11 +31,14 @@ except Exception:  # pragma: no cover
 
 
 class NonconvergenceError(RuntimeError):
-    """newton.hpp:40-48: carries the residual history."""
+    """newton.hpp:40-48: carries the last Newton iterate and the residual
+    history (rethrown with the slab / step context, stdg.hpp:132-137,
+    lodg.hpp:132-137)."""
 
-    def __init__(self, what: str, residual_history=()):
+    def __init__(self, what: str, residual_history=(), last_iterate=None):
         super().__init__(what)
         self.residual_history = list(residual_history)
+        self.last_iterate = last_iterate
 
 
 class CudaError(RuntimeError):
@@ -110,6 +113,16 @@ def _ptr(t, n: Optional[int] = None, what: str = "tensor") -> int:
 
 def _np(a, n: int, what: str) -> np.ndarray:
     a = np.ascontiguousarray(a, dtype=np.float64)
+    if a.size != n:
+        raise ValueError(f"{what}: expected {n} entries, got {a.size}")
+    return a
+
+
+def _out(a, n: int, what: str) -> np.ndarray:
+    """A caller-owned host output buffer: written in place, so no copies."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous \
+            or not a.flags.writeable:
+        raise ValueError(f"{what}: expected a writable contiguous float64 array")
     if a.size != n:
         raise ValueError(f"{what}: expected {n} entries, got {a.size}")
     return a
@@ -256,9 +269,9 @@ class SlabOperator:
         self._lib.stg_set_stream(self._h, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
         code = fn(self._h, *head, _ptr(u, self.n_sdof, what), ctypes.byref(c),
                   _ptr(U, self.n_dof, "U"), _ptr(u_next, self.n_sdof, "u_next"), ctypes.byref(info))
-        if code == L.STG_ERR_NONCONVERGENCE:
+        if code == L.STG_ERR_NONCONVERGENCE:  # U holds the last iterate
             raise NonconvergenceError(self._lib.stg_last_error(self._h).decode(),
-                                      _info(info).residual_history)
+                                      _info(info).residual_history, U)
         _raise(self._h, code, self._lib)
         return U, u_next, _info(info)
 
@@ -274,7 +287,7 @@ class SlabOperator:
                   ctypes.byref(c), _ptr(u_final, self.n_sdof, "u_final"),
                   None if states is None else states.data_ptr(),
                   None if sols is None else sols.data_ptr(), ctypes.byref(info))
-        if code == L.STG_ERR_NONCONVERGENCE:
+        if code == L.STG_ERR_NONCONVERGENCE:  # the failing step's last iterate is in sols
             raise NonconvergenceError(self._lib.stg_last_error(self._h).decode(),
                                       _info(info).residual_history)
         _raise(self._h, code, self._lib)
@@ -321,20 +334,33 @@ class SlabOperator:
                                                        out.ctypes.data), self._lib)
         return out
 
-    def stdg_step_host(self, t_n: float, dt: float, u_n, cfg: Optional[NewtonConfig] = None):
-        u_n = _np(u_n, self.n_sdof, "u_n")
-        U = np.empty(self.n_dof)
-        un1 = np.empty(self.n_sdof)
+    def _step_host(self, fn, head, u, cfg, U, u_next, what):
+        u = _np(u, self.n_sdof, what)
+        U = np.empty(self.n_dof) if U is None else _out(U, self.n_dof, "U")
+        u_next = np.empty(self.n_sdof) if u_next is None else _out(u_next, self.n_sdof, "u_next")
         info = L.StgSolveInfo()
         c = (cfg or NewtonConfig()).to_c()
-        code = self._lib.stg_stdg_step_host(self._h, float(t_n), float(dt), u_n.ctypes.data,
-                                            ctypes.byref(c), U.ctypes.data, un1.ctypes.data,
-                                            ctypes.byref(info))
-        if code == L.STG_ERR_NONCONVERGENCE:
+        code = fn(self._h, *head, u.ctypes.data, ctypes.byref(c), U.ctypes.data,
+                  u_next.ctypes.data, ctypes.byref(info))
+        if code == L.STG_ERR_NONCONVERGENCE:  # U holds the last iterate
             raise NonconvergenceError(self._lib.stg_last_error(self._h).decode(),
-                                      _info(info).residual_history)
+                                      _info(info).residual_history, U)
         _raise(self._h, code, self._lib)
-        return U, un1, _info(info)
+        return U, u_next, _info(info)
+
+    def stdg_step_host(self, t_n: float, dt: float, u_n, cfg: Optional[NewtonConfig] = None,
+                       U=None, u_next=None):
+        """stdg_step from host buffers (stg_stdg_step_host): H2D of u_n, the
+        device solve, D2H of U and u_next, all inside the call.  U / u_next
+        may be caller-owned (pinned or pageable) float64 arrays."""
+        return self._step_host(self._lib.stg_stdg_step_host, (float(t_n), float(dt)), u_n, cfg,
+                               U, u_next, "u_n")
+
+    def rk_step_host(self, form: int, t: float, dt: float, u, cfg: Optional[NewtonConfig] = None,
+                     U=None, u_next=None):
+        """rk_step from host buffers (stg_rk_step_host)."""
+        return self._step_host(self._lib.stg_rk_step_host, (int(form), float(t), float(dt)), u,
+                               cfg, U, u_next, "u")
 
 
 def _info(i: L.StgSolveInfo) -> SolveInfo:
@@ -383,9 +409,9 @@ class DgSpace:  # mesh.hpp:59-91
 def dg_space(mesh: Mesh, p: int, r: int = 1) -> DgSpace:  # mesh.hpp:93-110
     if p < 1:
         raise ValueError("dg_space: the GPU path needs p >= 1")
-    if r != 1:
-        raise ValueError("dg_space: scalar models only (r = 1)")
-    return DgSpace(mesh, int(p), 1)
+    if r < 1:
+        raise ValueError("dg_space: need r >= 1")
+    return DgSpace(mesh, int(p), int(r))
 
 
 @dataclass
@@ -427,6 +453,8 @@ class SemiDiscreteSystem:
 
 
 def assemble_semidiscrete(space: DgSpace, model: FluxModel) -> SemiDiscreteSystem:
+    if space.r != 1:
+        raise ValueError("assemble_semidiscrete: component mismatch (scalar models, r = 1)")
     if model.kind == L.STG_MODEL_ADVECTION and len(model.velocity) != space.mesh.d:
         raise ValueError("assemble_semidiscrete: dimension mismatch")
     if model.kind == L.STG_MODEL_BURGERS and space.mesh.d != 1:
@@ -554,3 +582,67 @@ def integrate(system, tab, t0, u0, t_end, n_steps, cfg=None, jac_form=JacobianFo
                                                           keep_states=True, keep_solutions=True)
     return RkTrajectory(times, [states[k] for k in range(n_steps + 1)],
                         [sols[k] for k in range(n_steps)], info.newton_iterations)
+
+
+# ---------------------------------------------------------------------------
+# Host-side field helpers (mesh.hpp:82-90, 113-181); layout as the library:
+# cell x-fastest (d = 3 extended), node x-fastest, component innermost
+# ---------------------------------------------------------------------------
+@dataclass
+class DiscreteField:  # mesh.hpp:113-117
+    space: DgSpace
+    coeffs: np.ndarray
+    time_tag: float = 0.0
+
+
+def node_coords(space: DgSpace) -> np.ndarray:
+    """node_coord (mesh.hpp:82-90) of every (cell, node): (n_cells * n^d, 3),
+    evaluated as lower + (c + 0.5 (1 + xi)) h in the reference's operation
+    order (bitwise equal to it)."""
+    from . import configs as C
+    m = space.mesh
+    return C.grid_coords(m.d, space.p, m.cells, m.lower, m.upper)
+
+
+def interpolate(space: DgSpace, f, t: float = 0.0) -> DiscreteField:
+    """interpolate (mesh.hpp:145-157): f(X) maps the (n_nodes, 3) coordinate
+    array to (n_nodes,) or (n_nodes, r) values."""
+    X = node_coords(space)
+    val = np.asarray(f(X), dtype=np.float64).reshape(X.shape[0], -1)
+    if val.shape[1] != space.r:
+        raise ValueError(f"interpolate: f returned {val.shape[1]} components, space has r = {space.r}")
+    return DiscreteField(space, np.ascontiguousarray(val.reshape(-1)), float(t))
+
+
+def interpolate_scalar(space: DgSpace, f, t: float = 0.0) -> DiscreteField:
+    """interpolate_scalar (mesh.hpp:159-165)."""
+    return interpolate(space, lambda X: np.asarray(f(X), dtype=np.float64).reshape(-1, 1), t)
+
+
+def global_mass(space: DgSpace) -> np.ndarray:
+    """global_mass (mesh.hpp:125-141): cell volume / 2^d times the tensor LGL
+    weights, replicated across the r components."""
+    m = space.mesh
+    n = space.p + 1
+    lib = L.load()
+    x, w = np.zeros(n), np.zeros(n)
+    if lib.stg_lgl_rule(n, x.ctypes.data, w.ctypes.data) != 0:
+        raise ValueError("lgl_rule failed")
+    vol = 1.0
+    for a in range(m.d):
+        vol *= (m.upper[a] - m.lower[a]) / m.cells[a]
+    vol_scale = vol / 2.0 ** m.d
+    wn = w.copy()
+    for _ in range(1, m.d):  # node x-fastest: w[ix] * w[iy] (* w[iz])
+        wn = np.multiply.outer(w, wn).reshape(-1)
+    cell = np.repeat(vol_scale * wn, space.r)
+    return np.tile(cell, int(np.prod(m.cells)))
+
+
+def l2_norm(field: DiscreteField) -> float:  # mesh.hpp:167-172
+    return float(np.sqrt(np.dot(field.coeffs * field.coeffs, global_mass(field.space))))
+
+
+def l2_error(field: DiscreteField, exact, t: float) -> float:  # mesh.hpp:174-181
+    ref = interpolate(field.space, lambda X: exact(X, t), t)
+    return l2_norm(DiscreteField(field.space, field.coeffs - ref.coeffs, t))

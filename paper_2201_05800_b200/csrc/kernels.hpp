@@ -92,6 +92,16 @@ __device__ __forceinline__ void pdl_entry() {
 enum PdlClass : int { kPdlSlab = 1, kPdlFdm = 2, kPdlVec = 4, kPdlPrecond = 8 };
 bool pdl_enabled(int cls);
 
+// Per-device caches of launch attributes (occupancy, SM count, the max
+// dynamic shared memory attribute) are indexed by the current device: a
+// handle may be used on any GPU, and cudaFuncSetAttribute is per device.
+constexpr int kMaxDevices = 64;
+inline int device_slot() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d >= 0 && d < kMaxDevices ? d : kMaxDevices - 1;
+}
+
 template <typename... KArgs, typename... Args>
 inline void launch_ex(int pdl_cls, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t s, Args&&... args) {
@@ -114,7 +124,8 @@ inline void launch_ex(int pdl_cls, void (*kernel)(KArgs...), dim3 grid, dim3 blo
 // reduced by Givens rotations, the rotations, the rotated right-hand side g,
 // the inverse norms c_j = 1/||S_j|| of the stored basis vectors, and the
 // cycle status: 0 running, 1 residual estimate <= tol_abs, 2 breakdown,
-// 3 the last step needs a second Gram-Schmidt pass, 4 nothing to do (b = 0).
+// 3 the last step needs a second Gram-Schmidt pass, 4 nothing to do (b = 0),
+// 5 the initial residual norm is NaN / infinite (the solve fails).
 constexpr int kGmresMaxRestart = 60;
 struct GmresDev {
   double H[(kGmresMaxRestart + 1) * kGmresMaxRestart];  // H(i,j) at i*m + j

@@ -346,8 +346,9 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
     return e && std::atoi(e) == 4;
   }();
   auto kern = four ? fdm_kernel<4> : fdm_kernel<3>;
-  static int occ = -1;
-  if (occ < 0) {
+  static int occ_dev[kMaxDevices];  // 0: not set up on that device yet
+  int& occ = occ_dev[device_slot()];
+  if (occ <= 0) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, THREADS, SMEM);
     if (occ < 1) occ = 1;

@@ -581,7 +581,8 @@ bool precond_eblock_dense(double* out, const double* in, const double* B, int nt
   if (nb > kDenseMax) return false;
   const size_t smem = sizeof(double) * ((size_t)nb * 128 + (size_t)128 * kTEp);
   if (smem > 227 * 1024) return false;
-  static size_t set = 0;
+  static size_t set_dev[kMaxDevices];
+  size_t& set = set_dev[device_slot()];
   if (smem > set) {
     cudaFuncSetAttribute(k_eblock_dense, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     set = smem;

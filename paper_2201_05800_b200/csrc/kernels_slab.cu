@@ -1484,10 +1484,21 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
 // ---------------------------------------------------------------------------
 // host-side launch helpers
 // ---------------------------------------------------------------------------
-// the Newton residual's fused reductions requested (and not an FD action)
+// blocks of the lane kernel: one lane per (element, temporal block), 32 / NT
+// elements per warp, 8 warps per block
+long long lane_blocks(long long nx, int nt) {
+  const long long epw = 32 / nt;
+  const long long warps = (nx + epw - 1) / epw;
+  return (warps * 32 + 255) / 256;
+}
+
+// the Newton residual's fused reductions requested (and not an FD action);
+// the reducing instance writes one partial per block, so its grid must fit
+// the kPartialDoubles slots in front of the completion counter -- larger
+// meshes take the plain kernel plus a separate reduction pass
 bool lane_reduces(const SlabArgs& a) {
   return a.red_max != nullptr && a.red_ss != nullptr && a.red_part != nullptr &&
-         a.fdv == nullptr;
+         a.fdv == nullptr && a.n_in >= 1 && lane_blocks(a.g.nx, a.n_in) <= kPartialDoubles;
 }
 
 template <int N1>
@@ -1497,9 +1508,7 @@ int launch1d(const SlabArgs& a, cudaStream_t s) {
   if (a.g.nx >= 4096 && a.n_out <= a.n_in && !std::getenv("STG_1D_V1")) {
     auto go = [&](auto nt_tag) {
       constexpr int NT = decltype(nt_tag)::value;
-      constexpr int EPW = 32 / NT;
-      const long long warps = (a.g.nx + EPW - 1) / EPW;
-      const int blocks = int((warps * 32 + 255) / 256);
+      const int blocks = int(lane_blocks(a.g.nx, NT));
       if (lane_reduces(a)) {
         cudaMemsetAsync(a.red_max, 0, sizeof(unsigned long long), s);
         launch_ex(kPdlSlab, slab1d_lane_kernel<N1, NT, true>, blocks, 256, 0, s, a);
@@ -1523,12 +1532,13 @@ int launch1d(const SlabArgs& a, cudaStream_t s) {
 }
 
 int num_sms_cached() {
-  static int n = 0;
+  static int cache[kMaxDevices];
+  const int dev = device_slot();
+  int& n = cache[dev];
   if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n = v > 0 ? v : 148;
   }
   return n;
 }
@@ -1552,8 +1562,9 @@ bool plane2d_ok(const SlabArgs& a) {
 template <int N1, int NT, int E, int MINB>
 int launch_plane2d(const SlabArgs& a, cudaStream_t s) {
   using Q = Plane2d<N1, NT, E>;
-  static int occ = -1;
-  if (occ < 0) {
+  static int occ_dev[kMaxDevices];  // 0: not set up on that device yet
+  int& occ = occ_dev[device_slot()];
+  if (occ <= 0) {
     for (auto k : {slab2d_plane<N1, NT, E, MINB, false>, slab2d_plane<N1, NT, E, MINB, true>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane<N1, NT, E, MINB, false>,
@@ -1582,8 +1593,9 @@ int launch2d_t(const SlabArgs& a, cudaStream_t s) {
   if (a.em) return -1;  // element-major vectors: the plane kernel only
   if (a.g.n_cells % Sh::E == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
       (a.g.n_sdof % 2) == 0 && !std::getenv("STG_2D_NONPERSIST")) {
-    static int occ = -1;
-    if (occ < 0) {
+    static int occ_dev[kMaxDevices];
+    int& occ = occ_dev[device_slot()];
+    if (occ <= 0) {
       cudaFuncSetAttribute(slab2d_persist<N1, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            P::SMEM);
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_persist<N1, NT>, Sh::THREADS,
@@ -1747,16 +1759,7 @@ bool encode(EncodeFn enc, CUtensorMap* map, const double* base, int rank, const 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int num_sms() { return num_sms_cached(); }
 
 int fast_variant() {
   static int v = -1;
@@ -1820,7 +1823,8 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   const bool red = slab_fast_reduces(a);
   auto kern = a.full_s ? (red ? slab3d_n4_persist<true, true> : slab3d_n4_persist<true, false>)
                        : (red ? slab3d_n4_persist<false, true> : slab3d_n4_persist<false, false>);
-  static bool attr = false;
+  static bool attr_dev[kMaxDevices];
+  bool& attr = attr_dev[device_slot()];
   if (!attr) {  // the largest layout (every trace buffer) bounds the request
     for (auto k : {slab3d_n4_persist<true, false>, slab3d_n4_persist<false, false>,
                    slab3d_n4_persist<true, true>, slab3d_n4_persist<false, true>})

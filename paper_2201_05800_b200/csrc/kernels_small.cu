@@ -235,8 +235,11 @@ __global__ void __launch_bounds__(kSmallThreads)
     const double bnorm = sqrt(bc[0]);
     int total = 0;
     bool conv = bnorm == 0.0;
-    double rel = 0.0;
-    while (!conv) {
+    // a NaN / infinite residual fails the linear solve at once (the
+    // reference's GMRES does not converge on it, newton.hpp:74-76)
+    const bool finite = isfinite(bnorm);
+    double rel = finite ? 0.0 : bnorm;
+    while (!conv && finite) {
       // r = b - J du  -> V_0 = r / ||r||
       jac(s.du, s.w);
       for (int i = threadIdx.x; i < n; i += kSmallThreads) s.w[i] = s.R[i] - s.w[i];

@@ -261,9 +261,13 @@ __global__ void k_gmres_init(GmresDev* G, int m, const double* bb, double beta, 
   }
   G->m = m;
   G->status = 0;
-  if (!(beta > 0.0)) {  // b = 0: nothing to do; every step slot reads "no work"
-    G->status = 4;
-    for (int j = 0; j <= m; ++j) reinterpret_cast<volatile int*>(host)[j] = 4;
+  // b = 0: nothing to do (4).  A NaN / infinite ||r|| is a failure (5), not
+  // "b = 0": the reference's Eigen GMRES does not converge on it and
+  // linear_solve throws (newton.hpp:74-76).  Every step slot reads the status.
+  const int st0 = beta == 0.0 ? 4 : (!(beta > 0.0) || isinf(beta) ? 5 : 0);
+  if (st0 != 0) {
+    G->status = st0;
+    for (int j = 0; j <= m; ++j) reinterpret_cast<volatile int*>(host)[j] = st0;
     __threadfence_system();
   }
   G->k_done = 0;
@@ -413,10 +417,11 @@ namespace {
 // per instantiation; at most kPartialDoubles / 80 blocks.
 template <int KM, int WW, bool UPD>
 int multi_grid(long long n) {
-  static int cap = 0;
+  static int cap_dev[kMaxDevices];
+  const int dev = device_slot();
+  int& cap = cap_dev[dev];
   if (cap == 0) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
+    int sms = 0, per_sm = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (UPD)
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update<KM, WW>, kVecBlock, 0);

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -30,10 +31,14 @@ struct CudaError : std::runtime_error {
 struct AdmissibilityError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// NonconvergenceError (newton.hpp:40-48).  The last iterate stays in the
+// caller's U (Newton updates it in place); the residual history and the
+// linear-iteration count travel with the exception into stg_solve_info.
 struct NonconvergenceError : std::runtime_error {
   std::vector<double> history;
-  NonconvergenceError(const std::string& w, std::vector<double> h)
-      : std::runtime_error(w), history(std::move(h)) {}
+  int linear_iterations = 0;
+  NonconvergenceError(const std::string& w, std::vector<double> h, int lin = 0)
+      : std::runtime_error(w), history(std::move(h)), linear_iterations(lin) {}
 };
 
 void ck(cudaError_t e, const char* what) {
@@ -570,6 +575,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     bnorm = std::sqrt(bb);
     ck(cudaMemcpyAsync(h->small.p + 200, h->small.p + kScalarSlot, sizeof(double),
                        cudaMemcpyDeviceToDevice, h->stream), "memcpy");
+    if (!std::isfinite(bnorm)) {  // NaN / inf right-hand side: not converged
+      st.rel_residual = bnorm;
+      return st;
+    }
     if (bnorm == 0.0) {
       stg::vec_fill(x, 0.0, n, s);
       h->launches++;
@@ -674,6 +683,11 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       ck(cudaEventSynchronize(h->ev_step[k & 1]), "sync");  // step k done
       status = mapped[k];
       if (status == 4) break;  // b = 0 (deferred norm): no step ran
+      if (status == 5) {       // ||r|| NaN / inf: no step ran, the solve failed
+        st.iterations = total;
+        st.rel_residual = std::numeric_limits<double>::quiet_NaN();
+        return st;
+      }
       if (status == 3) {  // step k needs a second Gram-Schmidt pass
         enqueue_reorth(k);
         h->reorth++;
@@ -811,7 +825,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
       throw NonconvergenceError("newton_solve: no convergence in " +
                                     std::to_string(cfg.max_iter) + " iterations, residual " +
                                     fmt_short(norm),
-                                out.history);
+                                out.history, out.linear_iterations);
     const bool red_r = h->red_done;  // <r,r> already in small[kRedSsSlot]
     const LinSys J = jacobian(u);
     // (an operator apply inside jacobian() clears red_done; nothing there
@@ -858,8 +872,20 @@ NewtonOut newton(stg_handle* h, const Op& residual,
   return out;
 }
 
+// stg_solve_info of a solve that stopped with NonconvergenceError: the
+// iterations done so far and the residual history (newton.hpp:116-120)
+NewtonOut partial_out(const NonconvergenceError& e) {
+  NewtonOut p;
+  p.history = e.history;
+  p.iterations = e.history.empty() ? 0 : int(e.history.size()) - 1;
+  p.linear_iterations = e.linear_iterations;
+  p.final_residual = e.history.empty() ? 0.0 : e.history.back();
+  return p;
+}
+
 void fill_info(stg_solve_info* info, const NewtonOut& o) {
   if (!info) return;
+  info->failed_step = -1;
   info->newton_iterations = o.iterations;
   info->linear_iterations = o.linear_iterations;
   info->final_residual = o.final_residual;
@@ -1205,6 +1231,8 @@ bool gen_eblock_ok(const stg_handle* h) {
 int resolve_precond(const stg_handle* h, int kind) {
   if (general_model(h->desc.model)) {
     if (kind == STG_PRECOND_NONE) return STG_PRECOND_NONE;
+    if (kind == STG_PRECOND_JACOBI)
+      throw std::invalid_argument("diagonal (Jacobi) preconditioner: advection only");
     if (kind == STG_PRECOND_AUTO) return gen_eblock_ok(h) ? STG_PRECOND_EBLOCK : STG_PRECOND_NONE;
     if (kind == STG_PRECOND_EBLOCK && gen_eblock_ok(h)) return STG_PRECOND_EBLOCK;
     throw std::invalid_argument(
@@ -1223,7 +1251,9 @@ int resolve_precond(const stg_handle* h, int kind) {
         "count divisible by 8");
   if (kind == STG_PRECOND_TBLOCK && h->desc.model != STG_MODEL_ADVECTION)
     throw std::invalid_argument("temporal-block Jacobi: advection only");
-  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_AUTO)
+  if (kind == STG_PRECOND_JACOBI && h->desc.model != STG_MODEL_ADVECTION)
+    throw std::invalid_argument("diagonal (Jacobi) preconditioner: advection only");
+  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_JACOBI)
     throw std::invalid_argument("unknown preconditioner");
   return kind;
 }
@@ -1374,15 +1404,24 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
   if (general_model(h->desc.model)) return general_eblock(h, mx);
   const int nt = h->nt, n1 = h->n1, npc = h->g.npc, d = h->desc.dim;
   const long long ns = h->n_sdof;
-  if (kind == STG_PRECOND_TBLOCK) {
-    // block of node class k: T + v_k S with v_k = sum_a V_a(i_a, i_a)
-    std::vector<double> tab(size_t(npc) * nt * nt), B(size_t(nt) * nt);
+  if (kind == STG_PRECOND_TBLOCK || kind == STG_PRECOND_JACOBI) {
+    // block of node class k: T + v_k S with v_k = sum_a V_a(i_a, i_a); the
+    // diagonal preconditioner keeps its diagonal, inverted entry by entry
+    // with Eigen's DiagonalPreconditioner rule (a zero entry -> 1)
+    std::vector<double> tab(size_t(npc) * nt * nt, 0.0), B(size_t(nt) * nt);
     for (int k = 0; k < npc; ++k) {
       const int idx[3] = {k % n1, (k / n1) % n1, k / (n1 * n1)};
       double v = 0.0;
       for (int a = 0; a < d; ++a) v += h->sp.V[a][idx[a]][idx[a]];
       for (int r = 0; r < nt; ++r)
         for (int j = 0; j < nt; ++j) B[size_t(r) * nt + j] = mx.T[r][j] + v * mx.S[r][j];
+      if (kind == STG_PRECOND_JACOBI) {
+        for (int r = 0; r < nt; ++r) {
+          const double dr = B[size_t(r) * nt + r];
+          tab[size_t(k) * nt * nt + size_t(r) * nt + r] = dr != 0.0 ? 1.0 / dr : 1.0;
+        }
+        continue;
+      }
       const std::vector<double> Bi = stg::inverse(B, nt);
       std::copy(Bi.begin(), Bi.end(), tab.begin() + long(size_t(k) * nt * nt));
     }
@@ -1555,7 +1594,7 @@ bool small_solve(stg_handle* h, bool rk, const stg::MixCoef& mres, const stg::Mi
     throw NonconvergenceError(ctx + ": newton_solve: no convergence in " +
                                   std::to_string(cfg.max_iter) + " iterations, residual " +
                                   fmt_short(o->final_residual),
-                              out.history);
+                              out.history, out.linear_iterations);
   }
   if (o->status == 2)
     throw std::runtime_error("linear_solve: GMRES did not converge, error " +
@@ -1595,12 +1634,12 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
         },
         U, n, cfg);
   } catch (const NonconvergenceError& e) {
-    NewtonOut partial;
-    partial.history = e.history;  // residual history travels back (newton.hpp:40-48)
-    fill_info(info, partial);
+    // stdg.hpp:132-137: rethrown with the slab context; U holds the last
+    // iterate, info the history (newton.hpp:40-48)
+    fill_info(info, partial_out(e));
     throw NonconvergenceError("stdg_step element at t=" + fmt_short(t_n) + ", dt=" + fmt_short(dt) +
                                   ": " + e.what(),
-                              e.history);
+                              e.history, e.linear_iterations);
   }
   if (u_next) {
     stg::vec_copy(u_next, U + (h->nt - 1) * h->n_sdof, h->n_sdof, h->stream);
@@ -1643,12 +1682,10 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
         },
         U, n, cfg);
   } catch (const NonconvergenceError& e) {
-    NewtonOut partial;
-    partial.history = e.history;
-    fill_info(info, partial);
+    fill_info(info, partial_out(e));  // lodg.hpp:132-137; U holds the last iterate
     throw NonconvergenceError("rk_step at t=" + fmt_short(t) + ", dt=" + fmt_short(dt) + ": " +
                                   e.what(),
-                              e.history);
+                              e.history, e.linear_iterations);
   }
   if (u_next) {
     // u_next = u + dt sum_j b_j F(U_j)  (lodg.hpp:142-145)
@@ -1723,7 +1760,19 @@ void integrate_impl(stg_handle* h, double t0, const double* u0, double t_end, in
                           : (k + 1 == n_steps ? u_final : h->march.p + (k % 2) * ns);
     double* Uk = U_all ? U_all + (long long)k * nd : h->Ustage.p;
     stg_solve_info ik{};
-    step(tk, dt, cur, Uk, next, &ik);
+    try {
+      step(tk, dt, cur, Uk, next, &ik);
+    } catch (const NonconvergenceError&) {
+      // totals so far plus the failing step's partial record (its last
+      // iterate is in Uk)
+      if (info) {
+        *info = ik;
+        info->newton_iterations += acc.newton_iterations;
+        info->linear_iterations += acc.linear_iterations;
+        info->failed_step = k;
+      }
+      throw;
+    }
     acc.newton_iterations += ik.newton_iterations;
     acc.linear_iterations += ik.linear_iterations;
     acc.final_residual = ik.final_residual;
@@ -1734,6 +1783,7 @@ void integrate_impl(stg_handle* h, double t0, const double* u0, double t_end, in
   if (states && u_final)
     ck(cudaMemcpyAsync(u_final, states + (long long)n_steps * ns, sizeof(double) * ns,
                        cudaMemcpyDeviceToDevice, h->stream), "memcpy");
+  acc.failed_step = -1;
   if (info) *info = acc;
 }
 }  // namespace
@@ -2096,7 +2146,14 @@ int stg_stdg_step_host(stg_handle* h, double t_n, double dt, const double* u_n,
     cudaStream_t s = h->stream;
     ck(cudaMemcpyAsync(h->host_u.p, u_n, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
        "H2D");
-    do_stdg_step(h, t_n, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
+    try {
+      do_stdg_step(h, t_n, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
+    } catch (const NonconvergenceError&) {  // the last iterate goes back to U
+      ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s),
+         "D2H");
+      ck(cudaStreamSynchronize(s), "sync");
+      throw;
+    }
     ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
     if (u_next)
       ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,
@@ -2119,7 +2176,14 @@ int stg_rk_step_host(stg_handle* h, int form, double t, double dt, const double*
     cudaStream_t s = h->stream;
     ck(cudaMemcpyAsync(h->host_u.p, u, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
        "H2D");
-    do_rk_step(h, form, t, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
+    try {
+      do_rk_step(h, form, t, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
+    } catch (const NonconvergenceError&) {  // the last iterate goes back to U
+      ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s),
+         "D2H");
+      ck(cudaStreamSynchronize(s), "sync");
+      throw;
+    }
     ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
     if (u_next)
       ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,

@@ -43,15 +43,79 @@ static SemiDiscreteSystem advection_1d(int cells, int p) {  // test_stdg.cpp:23-
                                advection_model({1.0}));
 }
 
-// LGL nodes of the space (for interpolate_scalar, mesh.hpp:145-165)
+// interpolate_scalar of a 1-D profile on [0, 1] (mesh.hpp:145-165)
 static Vec interp_1d(int cells, int p, double (*f)(double)) {
-  std::vector<double> x(size_t(p) + 1), w(size_t(p) + 1);
-  stg_lgl_rule(p + 1, x.data(), w.data());
-  Vec u;
-  const double h = 1.0 / cells;
-  for (int c = 0; c < cells; ++c)
-    for (int i = 0; i <= p; ++i) u.push_back(f((c + 0.5 * (1.0 + x[size_t(i)])) * h));
-  return u;
+  const DgSpace s = dg_space(uniform_mesh(1, {0.0}, {1.0}, {cells}), p);
+  return interpolate_scalar(s, [&](const Vec& x) { return f(x[0]); }).coeffs;
+}
+
+static bool near(double a, double b, double eps) {  // doctest::Approx(b).epsilon(eps)
+  return std::abs(a - b) <= eps * (1.0 + std::max(std::abs(a), std::abs(b)));
+}
+static DgSpace unit_interval(int n, int p, int r = 1) {
+  return dg_space(uniform_mesh(1, {0.0}, {1.0}, {n}), p, r);
+}
+static DgSpace unit_square(int n, int p, int r = 1) {
+  return dg_space(uniform_mesh(2, {0.0, 0.0}, {1.0, 1.0}, {n, n}), p, r);
+}
+
+// ---- host-side field helpers: test_mesh.cpp:70-190 (no device needed) --------
+static void test_node_coords() {  // test_mesh.cpp:70-86
+  CHECK(near(node_coord(unit_interval(10, 1), 3, 0)[0], 0.3, 1e-14));
+  CHECK(near(node_coord(unit_interval(10, 1), 3, 1)[0], 0.4, 1e-14));
+  CHECK(near(node_coord(unit_interval(10, 2), 0, 1)[0], 0.05, 1e-14));
+  const DgSpace s3 = unit_square(4, 2, 3);
+  CHECK(s3.dof() == 3 * 16 * 9);
+  const Vec x = node_coord(s3, /*cell (1,0)*/ 1, /*node (2,0)*/ 2);
+  CHECK(near(x[0], 0.5, 1e-14) && near(x[1], 0.0, 1e-14));
+  // d = 3 extension: cell (cz*ny + cy)*nx + cx, node (iz*n + iy)*n + ix
+  const DgSpace c = dg_space(uniform_mesh(3, {0, 0, 0}, {1, 2, 4}, {2, 2, 2}), 1);
+  const Vec y = node_coord(c, (1 * 2 + 0) * 2 + 1, (1 * 2 + 0) * 2 + 1);
+  CHECK(near(y[0], 1.0, 1e-15) && near(y[1], 0.0, 1e-15) && near(y[2], 4.0, 1e-15));
+}
+
+static void test_global_mass() {  // test_mesh.cpp:98-113
+  for (int p : {1, 2, 3}) {
+    const auto m1 = global_mass(unit_interval(8, p));
+    double s1 = 0.0, mn = 1.0;
+    for (double v : m1.diag) s1 += v, mn = std::min(mn, v);
+    CHECK(mn > 0.0 && near(s1, 1.0, 1e-12));
+    const auto m2 = global_mass(unit_square(5, p, 4));
+    double s2 = 0.0;
+    for (double v : m2.diag) s2 += v;
+    CHECK(near(s2, 4.0, 1e-12));
+    const auto m3 = global_mass(dg_space(uniform_mesh(3, {0, 0, 0}, {1, 1, 2}, {3, 2, 2}), p));
+    double s3 = 0.0;
+    for (double v : m3.diag) s3 += v;
+    CHECK(near(s3, 2.0, 1e-12));
+  }
+  const DgSpace s = unit_square(2, 2);
+  CHECK(near(global_mass(s).diag[size_t(1 * 3 + 1)], 0.0625 * 16.0 / 9.0, 1e-14));
+}
+
+static void test_interpolate_and_l2() {  // test_mesh.cpp:115-190
+  const auto constant = interpolate_scalar(unit_interval(1, 1), [](const Vec&) { return 3.0; });
+  CHECK(constant.coeffs[0] == 3.0 && constant.coeffs[1] == 3.0);
+  const auto lin = interpolate_scalar(unit_interval(1, 1), [](const Vec& x) { return x[0]; });
+  CHECK(near(lin.coeffs[0], 0.0, 1e-14) && near(lin.coeffs[1], 1.0, 1e-14));
+  CHECK(l2_norm(interpolate_scalar(unit_interval(4, 2), [](const Vec&) { return 0.0; })) == 0.0);
+  CHECK(near(l2_norm(interpolate_scalar(unit_interval(4, 2), [](const Vec&) { return 1.0; })),
+             1.0, 1e-13));
+  for (int p : {1, 2, 3})
+    CHECK(near(l2_norm(interpolate_scalar(unit_square(3, p), [](const Vec&) { return 2.0; })),
+               2.0, 1e-13));
+  auto exact = [](const Vec& x, double t) { return Vec{std::cos(x[0] + t)}; };
+  const DgSpace s = unit_interval(6, 2);
+  const auto field = interpolate(s, [&](const Vec& x) { return exact(x, 0.75); }, 0.75);
+  CHECK(l2_error(field, exact, 0.75) <= 1e-14);
+  const auto flat = interpolate_scalar(s, [](const Vec&) { return 1.0; });
+  CHECK(near(l2_error(flat, [](const Vec&, double) { return Vec{1.125}; }, 0.0), 0.125, 1e-13));
+  // r = 4 (component-innermost coefficients, test_mesh.cpp:88-96)
+  const auto f4 = interpolate(unit_square(2, 1, 4),
+                              [](const Vec& x) { return Vec{1.0, x[0], x[1], 2.0}; });
+  CHECK(f4.coeffs.size() == size_t(4 * 4 * 4));
+  CHECK(f4.coeffs[4 * 1 + 1] == node_coord(unit_square(2, 1, 4), 0, 1)[0]);
+  CHECK(f4.coeffs[3] == 2.0);
 }
 
 static void test_stdg_equals_rk() {  // test_stdg.cpp:111-135
@@ -182,8 +246,38 @@ static void test_nonconvergence_context() {  // test_lodg.cpp:179-194
     threw = true;
     CHECK(std::string(e.what()).find("rk_step at t=0.5") != std::string::npos);
     CHECK(e.residual_history.size() == 1);
+    // newton.hpp:40-48: the last iterate is the initial guess 1 (x) u here
+    CHECK(e.last_iterate.size() == 2 * u0.size());
+    CHECK(maxdiff(Vec(e.last_iterate.begin(), e.last_iterate.begin() + long(u0.size())), u0) == 0.0);
   }
   CHECK(threw);
+  // one Newton step allowed on a 3-D slab (host-driven path): the last
+  // iterate is that step's result, and its residual is the history's tail
+  {
+    auto sys = assemble_semidiscrete(
+        dg_space(uniform_mesh(3, {0, 0, 0}, {1, 1, 1}, {8, 4, 4}), 3), advection_model({1, 1, 1}));
+    const DgSpace& sp = dg_space(uniform_mesh(3, {0, 0, 0}, {1, 1, 1}, {8, 4, 4}), 3);
+    const Vec un = interpolate_scalar(sp, [](const Vec& x) {
+                     return std::sin(2 * M_PI * (x[0] + x[1] + x[2]));
+                   }).coeffs;
+    NewtonConfig one;
+    one.max_iter = 1;
+    one.abs_tol = 0.0;
+    one.rel_tol = 1e-30;  // unreachable after one step
+    one.gmres_tol = 1e-3;
+    bool t3 = false;
+    try {
+      stdg_step(sys, sbp_operators(4), 0.0, un, 0.002, one);
+    } catch (const NonconvergenceError& e) {
+      t3 = true;
+      CHECK(e.residual_history.size() == 2);
+      TimeElementSystem el{sys, sbp_operators(4), 0.0, 0.002, un};
+      CHECK(e.last_iterate.size() == 4 * un.size());
+      if (e.last_iterate.size() == 4 * un.size())
+        CHECK(near(maxabs(st_residual(el, e.last_iterate)), e.residual_history[1], 1e-12));
+    }
+    CHECK(t3);
+  }
   bool inv = false;
   try {
     uniform_mesh(4, {0, 0, 0, 0}, {1, 1, 1, 1}, {2, 2, 2, 2});
@@ -241,7 +335,14 @@ static void test_general_models() {  // test_spatial.cpp:67-89, models.hpp:108-1
   CHECK(mismatch);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  test_node_coords();
+  test_global_mass();
+  test_interpolate_and_l2();
+  if (argc > 1 && std::string(argv[1]) == "--host-only") {  // no device needed
+    std::printf("passed %d failed %d\n", g_pass, g_fail);
+    return g_fail == 0 ? 0 : 1;
+  }
   test_stdg_equals_rk();
   test_st_residual_constant_and_dt();
   test_st_jacobian_fd();

@@ -28,6 +28,15 @@ def test_cpp_host_api_compiles(tmp_path):
     assert exe.exists()
 
 
+def test_cpp_host_field_helpers_run_on_cpu(tmp_path):
+    """node_coord / interpolate / global_mass / l2_error of the C++ mirror
+    (test_mesh.cpp:70-190 ported): host-only, no device."""
+    exe = _build(tmp_path)
+    r = subprocess.run([str(exe), "--host-only"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "failed 0" in r.stdout
+
+
 @pytest.mark.gpu
 def test_cpp_host_api_runs(tmp_path):
     exe = _build(tmp_path)

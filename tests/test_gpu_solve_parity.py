@@ -1,0 +1,186 @@
+"""Solve-level parity at the BASELINE.json config sizes (the north star's
+1e-10 gate on the converged slab solution), against the CPU oracle.
+
+Each case runs the device solver and the oracle's restatement of the
+reference solver (newton_solve + GMRES, newton.hpp:102-130, 68-77;
+stdg_step stdg.hpp:120-143; rk_step lodg.hpp:89-149) on the same inputs and
+the same NewtonConfig, at the full configuration size, and compares the
+converged solutions in the max norm (acceptance.cpp:236-237):
+
+  c4  32^3, N = 3, n_tau = 4   stdg_step, GMRES to 1e-13
+  c2  256^2, N = 4, n_tau = 5  stdg_step, GMRES to 1e-13
+  c5  32^3 Lobatto IIIC s = 4  rk_step A^-1 form vs the oracle AND vs the c4 slab
+  c3  65,536 cells Burgers     10 sequential slabs of inexact Newton-GMRES (device:
+                               FD J.v, eps 1e-7; oracle: exact J) under one config
+
+The device preconditions (element-block Jacobi) and the oracle does not, so
+iteration counts differ; the converged solutions may not.  The stage apply at
+32^3 and the pipelined host-buffer path at full c4 are checked here too.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2201_05800_b200 import configs as C
+from paper_2201_05800_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2201_05800_b200.api import NewtonConfig, SlabOperator  # noqa: E402
+
+TOL_OP = 1e-12
+TOL_SOLVE = 1e-10
+
+
+def rel(a, b):
+    a = a.detach().cpu().numpy() if hasattr(a, "detach") else np.asarray(a)
+    b = b.detach().cpu().numpy() if hasattr(b, "detach") else np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def dev(x):
+    return torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device="cuda")
+
+
+def pair(cfg):
+    O.set_threads(O.max_threads())
+    op = SlabOperator(**cfg.kwargs())
+    pr = O.Problem(cfg.dim, cfg.degree, list(cfg.cells), list(cfg.lower), list(cfg.upper),
+                   list(cfg.velocity), model=cfg.model, n_tau=cfg.n_tau)
+    return op, pr
+
+
+# the same NewtonConfig on both sides: a linear slab converges in one or two
+# Newton steps (newton.hpp:102-130), GMRES to 1e-13 relative
+LIN = dict(abs_tol=0.0, rel_tol=1e-11, gmres_tol=1e-13, restart=30)
+
+
+def dev_cfg(**kw):
+    kw = dict(kw)
+    kw["gmres_restart"] = kw.pop("restart", 30)
+    return NewtonConfig(**kw)
+
+
+@pytest.mark.parametrize("name", ["c4", "c2"])
+def test_full_size_slab_solve_vs_oracle(name):
+    cfg = C.CONFIGS[name]
+    op, pr = pair(cfg)
+    un = C.initial_state(cfg)
+    Uo, uo, nit_o, lin_o = pr.stdg_step(0.0, cfg.dt, un, linear=O.GMRES, **LIN)
+    U, un1, info = op.stdg_step(0.0, cfg.dt, dev(un), dev_cfg(**LIN))
+    assert rel(U, Uo) <= TOL_SOLVE, (rel(U, Uo), info, lin_o)
+    assert rel(un1, uo) <= TOL_SOLVE
+    # both sides satisfy the same Newton stopping test on the oracle's residual
+    r = pr.st_residual(0.0, cfg.dt, un, U.cpu().numpy())
+    r0 = pr.st_residual(0.0, cfg.dt, un, np.tile(un, cfg.n_tau))
+    assert np.abs(r).max() <= 1e-11 * np.abs(r0).max()
+    assert info.newton_iterations == nit_o
+
+
+def test_full_size_c5_stage_solve_vs_oracle_and_c4_slab():
+    c5, c4 = C.CONFIGS["c5"], C.CONFIGS["c4"]
+    op, pr = pair(c5)
+    un = C.initial_state(c5)
+    Uo, uo, _, _ = pr.rk_step(c5.n_tau, L.STG_FORM_A_INV, 0.0, c5.dt, un, linear=O.GMRES, **LIN)
+    U5, u5, info = op.rk_step(L.STG_FORM_A_INV, 0.0, c5.dt, dev(un), dev_cfg(**LIN))
+    assert rel(U5, Uo) <= TOL_SOLVE
+    assert rel(u5, uo) <= TOL_SOLVE
+    # the stage solution is the slab solution (R_ST = (dt/2)(M (x) I) R_A^-1)
+    U4, u4, _ = op.stdg_step(0.0, c4.dt, dev(un), dev_cfg(**LIN))
+    assert rel(U5, U4) <= TOL_SOLVE
+    assert rel(u5, u4) <= TOL_SOLVE
+
+
+@pytest.mark.parametrize("form", [L.STG_FORM_A, L.STG_FORM_A_INV])
+def test_full_size_c5_stage_apply_vs_oracle(form):
+    cfg = C.CONFIGS["c5"]
+    op, pr = pair(cfg)
+    U = C.random_slab(cfg)
+    u = C.initial_state(cfg)
+    v = np.random.default_rng(cfg.seed + 7).uniform(-1, 1, cfg.n_dof)
+    ref = pr.stage_residual(cfg.n_tau, form, 0.0, cfg.dt, u, U)
+    assert rel(op.stage_residual(form, 0.0, cfg.dt, dev(u), dev(U)), ref) <= TOL_OP
+    ref = pr.stage_jvp(cfg.n_tau, form, 0.0, cfg.dt, U, v)
+    assert rel(op.stage_jvp(form, 0.0, cfg.dt, dev(U), dev(v)), ref) <= TOL_OP
+
+
+def test_full_size_c3_ten_slab_march_vs_oracle():
+    """10 sequential Burgers slabs (stdg_integrate, stdg.hpp:152-173) under
+    one NewtonConfig: abs 1e-12, rel 1e-10, GMRES 1e-6 (inexact Newton).  The
+    device differences J.v (eps 1e-7, fused) and preconditions; the oracle
+    uses the exact linearisation.  Both drive ||R||_inf below the same bound,
+    slab by slab."""
+    cfg = C.CONFIGS["c3"]
+    op, pr = pair(cfg)
+    u0 = C.initial_state(cfg)
+    kw = dict(abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-6)
+    u_dev = dev(u0)
+    u_cpu = u0.copy()
+    worst = 0.0
+    for k in range(10):
+        t = k * cfg.dt
+        _, u_dev, info = op.stdg_step(t, cfg.dt, u_dev, NewtonConfig(fd_eps=1e-7, **kw))
+        _, u_cpu, nit, lin = pr.stdg_step(t, cfg.dt, u_cpu, linear=O.GMRES, **kw)
+        worst = max(worst, rel(u_dev, u_cpu))
+        assert info.final_residual <= 1e-12 or info.final_residual <= 1e-10 * info.residual_history[0]
+    assert worst <= TOL_SOLVE, worst
+
+
+def test_full_c4_host_buffer_paths_bitwise_equal_device():
+    """The reference-facing host-buffer calls the bench times end to end
+    (stg_st_residual_host: 8 pipelined z-chunks; stg_stdg_step_host) return
+    exactly the device-resident results at full c4, from pinned and from
+    pageable host memory."""
+    cfg = C.CONFIGS["c4"]
+    op = SlabOperator(**cfg.kwargs())
+    U, un = C.random_slab(cfg), C.initial_state(cfg)
+    Rd = op.st_residual(0.0, cfg.dt, dev(un), dev(U)).cpu().numpy()
+    assert np.array_equal(op.st_residual_host(0.0, cfg.dt, un, U), Rd)  # pageable
+    pU = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    pu = torch.empty(cfg.n_sdof, dtype=torch.float64, pin_memory=True)
+    pR = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    pU.numpy()[:] = U
+    pu.numpy()[:] = un
+    op.st_residual_host(0.0, cfg.dt, pu.numpy(), pU.numpy(), out=pR.numpy())
+    assert np.array_equal(pR.numpy(), Rd)
+    nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10)
+    Ud, ud, _ = op.stdg_step(0.0, cfg.dt, dev(un), nc)
+    Uh, uh, _ = op.stdg_step_host(0.0, cfg.dt, un, nc)
+    assert np.array_equal(Uh, Ud.cpu().numpy()) and np.array_equal(uh, ud.cpu().numpy())
+
+
+@pytest.mark.parametrize("name,cells", [("c4", (8, 8, 8)), ("c3", (8192,)), ("c1", (64,)),
+                                        ("c2", (32, 32))])
+def test_nan_state_fails_the_linear_solve(name, cells):
+    """A NaN in u_n makes the Newton residual NaN: the linear solve fails with
+    the reference's error (linear_solve: GMRES did not converge,
+    newton.hpp:74-76) instead of reading as b = 0 / converged."""
+    cfg = C.CONFIGS[name].scaled(cells)
+    op = SlabOperator(**cfg.kwargs())
+    un = C.initial_state(cfg)
+    un[5] = np.nan
+    nc = NewtonConfig(fd_eps=1e-7 if name == "c3" else 0.0)
+    with pytest.raises(RuntimeError, match="GMRES did not converge"):
+        op.stdg_step(0.0, cfg.dt, dev(un), nc)
+
+
+def test_nonconvergence_returns_last_iterate():
+    """newton.hpp:40-48 / stdg.hpp:132-137: the exception carries the last
+    iterate; here one Newton step on c4@8^3 with an unreachable tolerance."""
+    from paper_2201_05800_b200.api import NonconvergenceError
+    cfg = C.CONFIGS["c4"].scaled((8, 8, 8))
+    op, pr = pair(cfg)
+    un = C.initial_state(cfg)
+    nc = NewtonConfig(max_iter=1, abs_tol=0.0, rel_tol=1e-30, gmres_tol=1e-4)
+    with pytest.raises(NonconvergenceError) as e:
+        op.stdg_step(0.0, cfg.dt, dev(un), nc)
+    last = e.value.last_iterate.cpu().numpy()
+    hist = e.value.residual_history
+    assert len(hist) == 2
+    r = pr.st_residual(0.0, cfg.dt, un, last)
+    assert abs(np.abs(r).max() - hist[1]) <= 1e-12 * hist[0]
+    with pytest.raises(NonconvergenceError) as eh:
+        op.stdg_step_host(0.0, cfg.dt, un, nc)
+    assert np.array_equal(eh.value.last_iterate, last)
