@@ -289,6 +289,30 @@ bool fdm_supported(const Geometry& g, int n_tau);
 int launch_precond_fdm(const FdmCoef& c, const Geometry& g, const double* in, double* out,
                        cudaStream_t s, Skip skip = {});
 
+// FDM with a direct temporal solve per spatial mode (kernels_fdm.cu,
+// fdm3_kernel): L_e^-1 = (I (x) Pz (x) Py (x) Px) blockdiag_theta((T + theta S)^-1)
+// (I (x) Pz^-1 (x) Py^-1 (x) Px^-1), theta = thz + thy + thx over the kept
+// modes -- no eigen-decomposition of the temporal operator, and S need not be
+// invertible.  The per-mode n_tau x n_tau complex inverses live in device
+// memory, [iz][it][t][q] with q = iy * 2 + j fastest (M).
+// One device block, copied to shared memory by one bulk copy per CTA:
+// the spatial factors (complex [re, im]) followed by the temporal table.
+struct FdmCoef3 {
+  double FX[2][4][2];  // rows 0, 2 of Px^-1 (one of each conjugate pair)
+  double FY[4][4][2];  // Py^-1
+  double FZ[4][4][2];  // Pz^-1
+  double IZ[4][4][2];  // Pz
+  double IY[4][4][2];  // Py
+  double IX[4][2][2];  // 2 x columns 0, 2 of Px (the factor 2 of 2 Re(.) folded in)
+  double M[4][4][4][8][2];  // [iz][it][t][q]: (T + theta S)^-1, q = iy * 2 + j
+};
+static_assert(sizeof(FdmCoef3) % 16 == 0, "bulk-copied block");
+bool fdm3_supported(const Geometry& g, int n_tau);
+// coef: a device copy of host_coef (the kernel reads its spatial factors as
+// parameters and bulk-copies the temporal table)
+int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const Geometry& g,
+                        const double* in, double* out, cudaStream_t s, Skip skip = {});
+
 // ---- block-Jacobi preconditioners (kernels_precond.cu) ----------------------
 // out[t][cell][k] = sum_j minv[k][t][j] in[j][cell][k]   (npc class tables)
 void precond_tblock(double* out, const double* in, const double* minv, int nt, int npc,

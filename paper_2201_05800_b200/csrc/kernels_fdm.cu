@@ -293,6 +293,264 @@ __global__ void __launch_bounds__(THREADS, MINB)
   if (tid == 0) ptxh::bulk_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// fdm3_kernel: the same element-block inverse with the temporal direction
+// solved directly per spatial mode, M_theta = (T + theta S)^-1 (4 x 4
+// complex), instead of Q^-1 S^-1, 1/Lambda and Q: 12.3k FMA per cell instead
+// of 15k.  16 cells per segment and one thread per (cell, iy, j) unit in
+// phase B, so every phase is one pass over the tile: three CTA barriers per
+// 16 cells (the two-half phase B above needs six per 8).  The complex tile
+// lives in place of the real one (a (t, z) row of 16 reals becomes 8 complex
+// (iy, j) values).  All factors (FdmCoef3, 9.5 KB) arrive with the first tile
+// by one bulk copy and are read from shared memory: warp-uniform addresses
+// (broadcast) for the spatial factors, one 128-byte wavefront per table read
+// (q fastest) -- kernel-parameter operands had the compiler keep ~100 of them
+// in uniform registers and spill those.
+namespace f3 {
+constexpr int E = 16;              // cells per segment
+constexpr int THREADS = 128;
+constexpr int TILE = E * 256 * 8;  // 32 KB: [t][cell][z] rows of 16 doubles
+constexpr int COEF = int(sizeof(FdmCoef3));
+constexpr int OFF_C = 2 * TILE;
+constexpr int OFF_BAR = OFF_C + COEF;
+constexpr int SMEM = OFF_BAR + 64 + 1024;  // + 1024 B alignment slack
+__device__ __forceinline__ int row_of(int t, int e, int z) { return (t * E + e) * 4 + z; }
+__device__ __forceinline__ double2* at(double* X, int row, int q) {
+  return reinterpret_cast<double2*>(X + row * 16 + ((q ^ (row & 7)) << 1));
+}
+__device__ __forceinline__ C2 ld(const double (&a)[2]) {
+  const double2 v = *reinterpret_cast<const double2*>(a);
+  return {v.x, v.y};
+}
+// a spatial factor: a kernel-parameter (constant bank) operand or a shared load
+template <bool PARAM>
+__device__ __forceinline__ C2 cf(const double (&a)[2]) {
+  if constexpr (PARAM) return {a[0], a[1]};
+  return ld(a);
+}
+__device__ __forceinline__ void mac(C2& acc, const C2& a, const C2& b) {
+  acc.r = fma(a.r, b.r, fma(-a.i, b.i, acc.r));
+  acc.i = fma(a.r, b.i, fma(a.i, b.r, acc.i));
+}
+}  // namespace f3
+
+// phase A on one (t, cell, z) row: forward x (kept modes j) and y, in place
+template <bool PARAM>
+__device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int row) {
+  const int sw = row & 7;
+  double r[16];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double2 v = *reinterpret_cast<const double2*>(X + row * 16 + ((q ^ sw) << 1));
+    r[2 * q] = v.x;
+    r[2 * q + 1] = v.y;
+  }
+  C2 a[4][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    C2 fx[4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x) fx[x] = f3::cf<PARAM>(c.FX[j][x]);
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      double re = 0.0, im = 0.0;
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        re = fma(fx[x].r, r[4 * y + x], re);
+        im = fma(fx[x].i, r[4 * y + x], im);
+      }
+      a[y][j] = {re, im};
+    }
+  }
+#pragma unroll
+  for (int iy = 0; iy < 4; ++iy) {
+    C2 fy[4];
+#pragma unroll
+    for (int y = 0; y < 4; ++y) fy[y] = f3::cf<PARAM>(c.FY[iy][y]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      C2 b = {0.0, 0.0};
+#pragma unroll
+      for (int y = 0; y < 4; ++y) f3::mac(b, fy[y], a[y][j]);
+      *reinterpret_cast<double2*>(X + row * 16 + (((iy * 2 + j) ^ sw) << 1)) =
+          make_double2(b.r, b.i);
+    }
+  }
+}
+
+// phase A' on one row: inverse y and x (2 Re, the 2 folded into IX), in place
+template <bool PARAM>
+__device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int row) {
+  const int sw = row & 7;
+  C2 h[4][2];
+#pragma unroll
+  for (int iy = 0; iy < 4; ++iy)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double2 v =
+          *reinterpret_cast<const double2*>(X + row * 16 + (((iy * 2 + j) ^ sw) << 1));
+      h[iy][j] = {v.x, v.y};
+    }
+  double o[16];
+#pragma unroll
+  for (int y = 0; y < 4; ++y) {
+    C2 iyc[4];
+#pragma unroll
+    for (int iy = 0; iy < 4; ++iy) iyc[iy] = f3::cf<PARAM>(c.IY[y][iy]);
+    C2 m[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      C2 sacc = {0.0, 0.0};
+#pragma unroll
+      for (int iy = 0; iy < 4; ++iy) f3::mac(sacc, iyc[iy], h[iy][j]);
+      m[j] = sacc;
+    }
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      double re = 0.0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const C2 ix = f3::cf<PARAM>(c.IX[x][j]);
+        re = fma(ix.r, m[j].r, fma(-ix.i, m[j].i, re));
+      }
+      o[4 * y + x] = re;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    *reinterpret_cast<double2*>(X + row * 16 + ((q ^ sw) << 1)) = make_double2(o[2 * q], o[2 * q + 1]);
+}
+
+// phase B on unit (cell e, q = (iy, j)): forward z, the per-mode temporal
+// solve, inverse z, in place on the unit's 16 complex (t, z) values
+template <bool PARAM>
+__device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs, double* X, int e,
+                                          int q) {
+  C2 v[4][4];  // [t][z] -> [t][iz] -> [it][iz] -> [t][z], in place
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+#pragma unroll
+    for (int z = 0; z < 4; ++z) {
+      const double2 d = *f3::at(X, f3::row_of(t, e, z), q);
+      v[t][z] = {d.x, d.y};
+    }
+#pragma unroll
+  for (int iz = 0; iz < 4; ++iz) {  // forward z, then the temporal solve of mode (iz, q)
+    C2 fz[4];
+#pragma unroll
+    for (int z = 0; z < 4; ++z) fz[z] = f3::cf<PARAM>(c.FZ[iz][z]);
+    C2 w[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      C2 acc = {0.0, 0.0};
+#pragma unroll
+      for (int z = 0; z < 4; ++z) f3::mac(acc, fz[z], v[t][z]);
+      w[t] = acc;
+    }
+    C2 y[4];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      C2 acc = {0.0, 0.0};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) f3::mac(acc, f3::ld(cs.M[iz][it][t][q]), w[t]);
+      y[it] = acc;
+    }
+    // park mode iz's result in the tile (this unit's own slots; the z values
+    // are all in registers already)
+#pragma unroll
+    for (int it = 0; it < 4; ++it)
+      *f3::at(X, f3::row_of(it, e, iz), q) = make_double2(y[it].r, y[it].i);
+  }
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+#pragma unroll
+    for (int iz = 0; iz < 4; ++iz) {
+      const double2 d = *f3::at(X, f3::row_of(t, e, iz), q);
+      v[t][iz] = {d.x, d.y};
+    }
+  }
+#pragma unroll
+  for (int z = 0; z < 4; ++z) {  // inverse z, stored
+    C2 iz_c[4];
+#pragma unroll
+    for (int iz = 0; iz < 4; ++iz) iz_c[iz] = f3::cf<PARAM>(c.IZ[z][iz]);
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      C2 acc = {0.0, 0.0};
+#pragma unroll
+      for (int iz = 0; iz < 4; ++iz) f3::mac(acc, iz_c[iz], v[t][iz]);
+      *f3::at(X, f3::row_of(t, e, z), q) = make_double2(acc.r, acc.i);
+    }
+  }
+}
+
+// PARAM: the spatial factors are read as kernel-parameter operands (cp is
+// the FdmCoef3 by value); otherwise from the shared copy.  The temporal
+// table is always read from shared memory (per-lane addresses).
+template <bool PARAM>
+__global__ void __launch_bounds__(f3::THREADS, 3)
+    fdm3_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_out,
+                const FdmCoef3* __restrict__ coef, const __grid_constant__ FdmCoef3 cp,
+                const Geometry g, const Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* base = smem_raw + ((1024u - (ptxh::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const FdmCoef3& cs = *reinterpret_cast<const FdmCoef3*>(base + f3::OFF_C);
+  const FdmCoef3& c = PARAM ? cp : cs;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + f3::OFF_BAR);
+  const uint32_t bar0 = ptxh::smem_u32(bars), bar1 = ptxh::smem_u32(bars + 1);
+  const int tid = threadIdx.x;
+  const int nseg = g.n_cells / f3::E;
+  if (tid == 0) {
+    ptxh::mbar_init(bar0, 1);
+    ptxh::mbar_init(bar1, 1);
+    ptxh::fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int seg, int st, uint32_t extra) {
+    const uint32_t bar = st ? bar1 : bar0;
+    ptxh::mbar_expect_tx(bar, f3::TILE + extra);
+    ptxh::tma_load_4d(ptxh::smem_u32(base + st * f3::TILE), &tm, bar, 0, 0, seg * f3::E, 0);
+  };
+  int seg = blockIdx.x;
+  if (tid == 0 && seg < nseg) {  // the factors ride on the first tile's barrier
+    issue(seg, 0, f3::COEF);
+    ptxh::bulk_g2s_1d(ptxh::smem_u32(base + f3::OFF_C), coef, f3::COEF, bar0);
+  }
+  // phase B unit: q = (iy, j) fastest across the lanes (conflict-free tile
+  // reads, one 128-byte wavefront per table read), 4 cells per warp
+  const int qB = tid & 7, eB = tid >> 3;
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int st = it & 1;
+    double* X = reinterpret_cast<double*>(base + st * f3::TILE);
+    if (tid == 0 && seg + (int)gridDim.x < nseg) {
+      // stage st^1 last held the previous segment's result: its bulk store
+      // must have read it before the next load overwrites it
+      ptxh::bulk_wait_read0();
+      ptxh::fence_proxy_async_smem();
+      issue(seg + gridDim.x, st ^ 1, 0);
+    }
+    while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) fdm3_fwd_row<PARAM>(c, X, tid + k * f3::THREADS);
+    __syncthreads();
+    fdm3_unit<PARAM>(c, cs, X, eB, qB);
+    __syncthreads();
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) fdm3_inv_row<PARAM>(c, X, tid + k * f3::THREADS);
+    ptxh::fence_proxy_async_smem();
+    __syncthreads();  // result tile complete
+    if (tid == 0) {
+      ptxh::tma_store_4d(&tm_out, ptxh::smem_u32(X), 0, 0, seg * f3::E, 0);
+      ptxh::bulk_commit();
+    }
+  }
+  if (tid == 0) ptxh::bulk_wait0();
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -360,6 +618,49 @@ int launch_precond_fdm(const FdmCoef& coef, const Geometry& g, const double* in,
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
   launch_ex(kPdlFdm, kern, grid, THREADS, SMEM, s, map, map_out, coef, g, skip);
+  return 1;
+}
+
+bool fdm3_supported(const Geometry& g, int n_tau) {
+  return g.dim == 3 && g.n1 == 4 && n_tau == 4 && g.n_cells % f3::E == 0 &&
+         encode_fn() != nullptr && !std::getenv("STG_FDM_V1");
+}
+
+int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const Geometry& g,
+                        const double* in, double* out, cudaStream_t s, Skip skip) {
+  EncodeFn enc = encode_fn();
+  if (!enc || (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return -1;
+  const cuuint64_t gdim[4] = {16, 4, cuuint64_t(g.n_cells), 4};
+  const cuuint64_t gstride[3] = {128, 512, cuuint64_t(g.n_sdof) * 8};
+  const cuuint32_t box[4] = {16, 4, f3::E, 4};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUtensorMap map, map_out;
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(in), gdim, gstride, box,
+          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  if (enc(&map_out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, out, gdim, gstride, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return -1;
+  static const bool smem_coef = std::getenv("STG_FDM3_SMEMC") != nullptr;
+  auto kern = smem_coef ? fdm3_kernel<false> : fdm3_kernel<true>;
+  static int occ_dev[kMaxDevices];
+  const int dev = device_slot();
+  int& occ = occ_dev[dev];
+  if (occ <= 0) {
+    for (auto k : {fdm3_kernel<false>, fdm3_kernel<true>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, f3::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::THREADS, f3::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nseg = g.n_cells / f3::E;
+  int grid = occ * sms;
+  if (grid > nseg) grid = nseg;
+  launch_ex(kPdlFdm, kern, grid, f3::THREADS, f3::SMEM, s, map, map_out, coef, host_coef, g, skip);
   return 1;
 }
 

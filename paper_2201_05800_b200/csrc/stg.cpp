@@ -100,6 +100,8 @@ struct stg_handle {
   DevBuf partial;  // reduction partials
   DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
   DevBuf ptab;          // preconditioner block tables
+  int ptab_kind = -1;   // TBLOCK / JACOBI table in ptab and its mix (-1: none)
+  stg::MixCoef ptab_mix{};
   DevBuf zbasis;        // flexible GMRES: preconditioned basis Z_k = P^-1 S_k
   DevBuf genF, genFlag;  // general models: F(X_j) blocks; admissibility flag (int)
   DevBuf small_out;      // fused small-solve result record
@@ -125,6 +127,10 @@ struct stg_handle {
   stg::FdmCoef fdm{};
   stg::MixCoef fdm_mix{};
   bool fdm_valid = false;
+  stg::MixCoef fdm3_mix{};
+  bool fdm3_valid = false;
+  DevBuf fdm3M;  // device copy of the fdm3_kernel factors (stg::FdmCoef3)
+  std::unique_ptr<stg::FdmCoef3> fdm3_host;  // and the host copy (kernel parameters)
   double* pinned = nullptr;  // pinned host mirror of `small`
   static constexpr int kSmall = 1024;
   // GMRES cycle state on the device, its pinned host copy, the host-mapped
@@ -1213,6 +1219,61 @@ bool build_fdm(const stg::SpatialCoef& sp, const stg::MixCoef& mx, stg::FdmCoef&
   }
 }
 
+// Factors of fdm3_kernel (kernels_fdm.cu): the complex eigen-decompositions
+// of the per-axis element matrices V_a = P_a Th_a P_a^-1 and, per kept spatial
+// mode theta = thz + thy + thx, the temporal inverse (T + theta S)^-1, written
+// to M ([iz][it][t][q] complex, q = iy * 2 + j).  False when V_x does not have
+// two complex-conjugate pairs, an eigen-decomposition is inaccurate or a
+// temporal block is singular.
+bool build_fdm3(const stg::SpatialCoef& sp, const stg::MixCoef& mx, stg::FdmCoef3& c) {
+  using stg::cplx;
+  constexpr int n = 4;
+  try {
+    std::vector<cplx> th[3], P[3], Pi[3];
+    for (int a = 0; a < 3; ++a) {
+      std::vector<double> V(n * n);
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) V[size_t(i) * n + k] = sp.V[a][i][k];
+      if (!stg::eig_real(V, n, th[a], P[a], Pi[a])) return false;
+    }
+    for (int j = 0; j < 2; ++j)  // x modes: one member of each conjugate pair (0, 2)
+      if (!(th[0][size_t(2 * j)].imag() > 0.0) ||
+          th[0][size_t(2 * j + 1)] != std::conj(th[0][size_t(2 * j)]))
+        return false;
+    auto put = [](double* dst, cplx z) {
+      dst[0] = z.real();
+      dst[1] = z.imag();
+    };
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) {
+        put(c.FZ[r][q], Pi[2][size_t(r) * n + q]);
+        put(c.IZ[r][q], P[2][size_t(r) * n + q]);
+        put(c.FY[r][q], Pi[1][size_t(r) * n + q]);
+        put(c.IY[r][q], P[1][size_t(r) * n + q]);
+      }
+    for (int j = 0; j < 2; ++j)
+      for (int x = 0; x < n; ++x) {
+        put(c.FX[j][x], Pi[0][size_t(2 * j) * n + x]);
+        put(c.IX[x][j], 2.0 * P[0][size_t(x) * n + 2 * j]);  // 2 Re(.) of the kept half
+      }
+    std::vector<cplx> A(n * n), Ai;
+    for (int iz = 0; iz < n; ++iz)
+      for (int iy = 0; iy < n; ++iy)
+        for (int j = 0; j < 2; ++j) {
+          const cplx theta = th[2][size_t(iz)] + th[1][size_t(iy)] + th[0][size_t(2 * j)];
+          for (int r = 0; r < n; ++r)
+            for (int t = 0; t < n; ++t) A[size_t(r) * n + t] = mx.T[r][t] + theta * mx.S[r][t];
+          if (!stg::cinverse(A, Ai, n)) return false;
+          const int q = iy * 2 + j;
+          for (int it = 0; it < n; ++it)
+            for (int t = 0; t < n; ++t) put(c.M[iz][it][t][q], Ai[size_t(it) * n + t]);
+        }
+    return true;
+  } catch (const std::exception&) {
+    return false;
+  }
+}
+
 // d = 2 advection: one shared dense element block, n_tau * n^2 <= 128
 bool dense2d_ok(const stg_handle* h) {
   return h->desc.dim == 2 && h->desc.model == STG_MODEL_ADVECTION &&
@@ -1220,7 +1281,8 @@ bool dense2d_ok(const stg_handle* h) {
 }
 
 bool fdm_ok(const stg_handle* h) {
-  return h->desc.dim == 3 && h->desc.model == STG_MODEL_ADVECTION && stg::fdm_supported(h->g, h->nt);
+  return h->desc.dim == 3 && h->desc.model == STG_MODEL_ADVECTION &&
+         (stg::fdm3_supported(h->g, h->nt) || stg::fdm_supported(h->g, h->nt));
 }
 
 // general linear models (advdiff): element blocks n_tau * npc * r <= 32
@@ -1404,6 +1466,14 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
   if (general_model(h->desc.model)) return general_eblock(h, mx);
   const int nt = h->nt, n1 = h->n1, npc = h->g.npc, d = h->desc.dim;
   const long long ns = h->n_sdof;
+  if ((kind == STG_PRECOND_TBLOCK || kind == STG_PRECOND_JACOBI) && h->ptab_kind == kind &&
+      std::memcmp(&h->ptab_mix, &mx, sizeof mx) == 0) {  // the table of this mix is uploaded
+    const double* dt = h->ptab.p;
+    return [h, dt, nt, npc, ns](const double* in, double* out) {
+      stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream, h->skip);
+      h->launches++;
+    };
+  }
   if (kind == STG_PRECOND_TBLOCK || kind == STG_PRECOND_JACOBI) {
     // block of node class k: T + v_k S with v_k = sum_a V_a(i_a, i_a); the
     // diagonal preconditioner keeps its diagonal, inverted entry by entry
@@ -1429,6 +1499,8 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     ck(cudaMemcpyAsync(h->ptab.p, tab.data(), sizeof(double) * tab.size(),
                        cudaMemcpyHostToDevice, h->stream), "H2D");
     ck(cudaStreamSynchronize(h->stream), "sync");
+    h->ptab_kind = kind;
+    h->ptab_mix = mx;
     const double* dt = h->ptab.p;
     return [h, dt, nt, npc, ns](const double* in, double* out) {
       stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream, h->skip);
@@ -1467,6 +1539,31 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     const double* tab = h->dtab.p;
     const int ncells = h->g.n_cells;
     return dense_op(h, tab, nt, npc, ncells, ns);
+  }
+  if (d == 3 && stg::fdm3_supported(h->g, nt)) {  // fast diagonalisation, direct t solve
+    bool ok = h->fdm3_valid && std::memcmp(&h->fdm3_mix, &mx, sizeof mx) == 0;
+    if (!ok) {
+      auto c = std::make_unique<stg::FdmCoef3>();
+      if (build_fdm3(h->sp, mx, *c)) {
+        h->fdm3M.ensure(sizeof(stg::FdmCoef3) / sizeof(double));
+        ck(cudaMemcpyAsync(h->fdm3M.p, c.get(), sizeof(stg::FdmCoef3), cudaMemcpyHostToDevice,
+                           h->stream), "H2D");
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        h->fdm3_mix = mx;
+        h->fdm3_host = std::move(c);
+        h->fdm3_valid = ok = true;
+      }
+    }
+    if (ok) {
+      const stg::FdmCoef3* c = reinterpret_cast<const stg::FdmCoef3*>(h->fdm3M.p);
+      const stg::FdmCoef3* hc = h->fdm3_host.get();
+      return [h, c, hc](const double* in, double* out) {
+        if (stg::launch_precond_fdm3(c, *hc, h->g, in, out, h->stream, h->skip) < 0)
+          throw std::runtime_error("element-block preconditioner launch failed");
+        h->launches++;
+      };
+    }
+    return make_precond(h, STG_PRECOND_TBLOCK, mx, U);  // spectrum not of the FDM form
   }
   if (d == 3) {  // element-block Jacobi by fast diagonalisation
     stg::FdmCoef c;
@@ -1507,6 +1604,7 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     static const bool rebuild = std::getenv("STG_PRECOND_REBUILD") != nullptr;
     float* fb = reinterpret_cast<float*>(h->ptab.p);
     if (!h->eblock_valid || rebuild) {
+      h->ptab_kind = -1;  // ptab now holds Burgers blocks
       h->ptab.ensure((size_t(ncells) * nb * nb + 1) / 2);  // fp32 blocks
       fb = reinterpret_cast<float*>(h->ptab.p);
       if (!stg::build_burgers_eblock(fb, U, a, h->stream))

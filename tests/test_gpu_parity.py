@@ -294,11 +294,14 @@ def test_preconditioners_same_solution_fewer_iterations(name, cells, pcs):
 
 
 @pytest.mark.parametrize("velocity", [(1.0, 1.0, 1.0), (-0.7, 0.4, -1.1)])
-def test_fdm_element_block_is_exact_local_inverse(velocity):
+@pytest.mark.parametrize("cells", [(2, 2, 2), (4, 2, 2), (2, 2, 8)])
+def test_fdm_element_block_is_exact_local_inverse(velocity, cells):
     """d = 3 EBLOCK (fast diagonalisation, kernels_fdm.cu) = the exact inverse
     of the element-local Jacobian block, which is read off the oracle's J.v
-    (columns supported on one element; 2 x 2 x 2 periodic mesh)."""
-    cfg = make(3, 3, 4, (2, 2, 2), velocity, dt=0.02)
+    (columns supported on one element; periodic meshes of 8 cells: the
+    two-half kernel, and 16 / 32 cells: fdm3_kernel with the direct temporal
+    solve)."""
+    cfg = make(3, 3, 4, cells, velocity, dt=0.02)
     op, pr = pair(cfg)
     ns, npc, nt = op.n_sdof, 64, 4
     loc = np.array([t * ns + k for t in range(nt) for k in range(npc)])  # element 0
@@ -310,7 +313,7 @@ def test_fdm_element_block_is_exact_local_inverse(velocity):
         Lblk[:, c] = pr.st_jvp(0.0, cfg.dt, U0, e)[loc]
     x = np.random.default_rng(5).standard_normal(nt * ns)
     y = op.st_precond_apply(cfg.dt, dev(x), precond=L.STG_PRECOND_EBLOCK).cpu().numpy()
-    for cell in range(8):
+    for cell in range(int(np.prod(cells))):
         idx = loc + cell * npc
         ref = np.linalg.solve(Lblk, x[idx])
         assert rel(y[idx], ref) <= 1e-11, cell
