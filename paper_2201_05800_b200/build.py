@@ -5,8 +5,8 @@ Plain nvcc (no torch JIT cache): every translation unit is compiled with
 library next to this file, so the built artefact travels with the repo
 snapshot to the GPU box.  The static CUDA runtime is linked in; the driver API
 entry point for TMA descriptors is resolved at run time through
-``cudaGetDriverEntryPoint`` (no -lcuda).  cuBLAS is linked for one plain
-GEMM (the d = 2 dense element-block preconditioner).
+``cudaGetDriverEntryPoint`` (no -lcuda).  No CUDA libraries (cuBLAS etc.)
+are linked: every kernel on the path is in csrc/.
 """
 from __future__ import annotations
 
@@ -72,10 +72,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
         list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
-    # cuBLAS: the plain DGEMM of the d = 2 dense element-block preconditioner
-    cudalib = Path(nvcc()).resolve().parent.parent / "lib64"
-    cmd = cc + ARCH + ["-shared", "-o", str(tmp)] + objs + [
-        f"-L{cudalib}", "-lcublas", "-Xlinker", f"-rpath={cudalib}"]
+    # no library kernels: static CUDA runtime only
+    cmd = cc + ARCH + ["-shared", "-o", str(tmp)] + objs
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

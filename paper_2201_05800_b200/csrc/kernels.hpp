@@ -313,6 +313,28 @@ bool fdm3_supported(const Geometry& g, int n_tau);
 int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const Geometry& g,
                         const double* in, double* out, cudaStream_t s, Skip skip = {});
 
+// d = 2 element-block inverse by fast diagonalisation (kernels_fdm.cu,
+// fdm2_kernel): L_e^-1 = (I (x) Py (x) Px) blockdiag_theta((T + theta S)^-1)
+// (I (x) Py^-1 (x) Px^-1) over the kept spatial modes theta = thy + thx, x
+// modes: the NR real eigenvalues of V_x (real eigenvectors) then one member
+// of each of the NP complex-conjugate pairs.  One device block per mix;
+// complex entries [re, im]; sized for n <= 5, n_tau <= 5.
+constexpr int kFdm2MaxN = 5;
+struct FdmCoef2 {
+  double FX[kFdm2MaxN][kFdm2MaxN][2];  // kept rows of Px^-1 ([kept k][x])
+  double FY[kFdm2MaxN][kFdm2MaxN][2];  // Py^-1 ([iy][y])
+  double IY[kFdm2MaxN][kFdm2MaxN][2];  // Py ([y][iy])
+  double IX[kFdm2MaxN][kFdm2MaxN][2];  // kept columns of Px, x2 for pair members ([x][k])
+  // [m = iy * KX + k][it][t]: (T + theta_m S)^-1
+  double M[kFdm2MaxN * kFdm2MaxN][kFdm2MaxN][kFdm2MaxN][2];
+};
+static_assert(sizeof(FdmCoef2) % 16 == 0, "bulk-copied block");
+// n1 / n_tau / (real, pair) x-mode counts the kernel is instantiated for
+bool fdm2_supported(const Geometry& g, int n_tau, int nr, int np);
+int launch_precond_fdm2(const FdmCoef2* coef, const FdmCoef2& host_coef, const Geometry& g,
+                        int n_tau, int nr, int np, const double* in, double* out, cudaStream_t s,
+                        Skip skip = {});
+
 // ---- block-Jacobi preconditioners (kernels_precond.cu) ----------------------
 // out[t][cell][k] = sum_j minv[k][t][j] in[j][cell][k]   (npc class tables)
 void precond_tblock(double* out, const double* in, const double* minv, int nt, int npc,
@@ -322,7 +344,7 @@ void precond_eblock(double* out, const double* in, const double* B, long long bs
                     int n1, int ncells, long long ns, cudaStream_t s, Skip skip = {});
 // d = 2: out_e = B in_e with ONE shared dense block B ((n_tau*npc)^2, <= 128^2)
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
-                          int ncells, long long ns, cudaStream_t s);
+                          int ncells, long long ns, cudaStream_t s, Skip skip = {});
 // element blocks of the general linear models by coloured probing
 // (ndl = element-local DOFs per temporal block = npc * r)
 void probe_set(double* P, int ndl, int col, int nx, int ny, int sx, int sy, int cx0, int cy0,

@@ -551,6 +551,208 @@ __global__ void __launch_bounds__(f3::THREADS, 3)
   if (tid == 0) ptxh::bulk_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// fdm2_kernel: the d = 2 element-block inverse (c2: n = 5, n_tau = 5) by the
+// same fast diagonalisation, on the stage-major vectors directly (no
+// element-major permutes).  A segment is 32 consecutive cells: n_tau bulk
+// copies of 32 * n^2 contiguous doubles.  Phases (one thread per (t, cell)
+// plane in A / A', lanes = cells; one warp per kept spatial mode in B):
+//   A : forward x (NR real modes with real factors + NP pair members) and y
+//   B : (T + theta_m S)^-1 on the n_tau values of each (cell, mode)
+//   A': inverse y and x (2 Re for the pair members), in place, bulk store.
+// ~5.3k FMA per cell at c2 (a dense 125 x 125 block is 15.6k).
+namespace f2 {
+constexpr int E = 32;
+template <int N1, int NT, int NR, int NP>
+struct Shape {
+  static constexpr int NPC = N1 * N1;
+  static constexpr int KX = NR + NP;         // kept x modes
+  static constexpr int KM = N1 * KX;         // kept spatial modes
+  static constexpr int THREADS = NT * E;
+  static constexpr int NW = THREADS / 32;
+  static constexpr int STAGE = NT * E * NPC;  // doubles
+  static constexpr int OFF_C = 2 * STAGE * 8;
+  static constexpr int OFF_M = OFF_C + NT * KM * E * 16;
+  static constexpr int MBYTES = int(sizeof(((FdmCoef2*)nullptr)->M));
+  static constexpr int OFF_BAR = OFF_M + MBYTES;
+  static constexpr int SMEM = OFF_BAR + 64;
+  static_assert(N1 <= kFdm2MaxN && NT <= kFdm2MaxN && NR + 2 * NP == N1, "shape");
+  static_assert((E * NPC * 8) % 16 == 0, "bulk copy granularity");
+};
+}  // namespace f2
+
+template <int N1, int NT, int NR, int NP>
+__global__ void __launch_bounds__(f2::Shape<N1, NT, NR, NP>::THREADS)
+    fdm2_kernel(const double* __restrict__ in, double* __restrict__ out,
+                const FdmCoef2* __restrict__ coef, const __grid_constant__ FdmCoef2 c,
+                const Geometry g, const Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  using S = f2::Shape<N1, NT, NR, NP>;
+  constexpr int NPC = S::NPC, KX = S::KX, KM = S::KM, E = f2::E;
+  extern __shared__ __align__(128) unsigned char smem2[];
+  double* st0 = reinterpret_cast<double*>(smem2);
+  double2* Ct = reinterpret_cast<double2*>(smem2 + S::OFF_C);  // [t][m][e]
+  const double2* Ms = reinterpret_cast<const double2*>(smem2 + S::OFF_M);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem2 + S::OFF_BAR);
+  const uint32_t bar0 = ptxh::smem_u32(bars), bar1 = ptxh::smem_u32(bars + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tA = tid / E, eA = tid % E;
+  const long long ns = g.n_sdof;
+  const int nseg = g.n_cells / E;
+  constexpr uint32_t PB = E * NPC * 8;  // bytes of one temporal block of a segment
+  if (tid == 0) {
+    ptxh::mbar_init(bar0, 1);
+    ptxh::mbar_init(bar1, 1);
+    ptxh::fence_mbar_init();
+  }
+  __syncthreads();
+  auto issue = [&](int seg, int st, bool with_m) {
+    const uint32_t bar = st ? bar1 : bar0;
+    ptxh::mbar_expect_tx(bar, NT * PB + (with_m ? S::MBYTES : 0));
+    const uint32_t dst = ptxh::smem_u32(st0 + st * S::STAGE);
+    const double* src = in + (long long)seg * E * NPC;
+    for (int t = 0; t < NT; ++t) ptxh::bulk_g2s_1d(dst + t * PB, src + t * ns, PB, bar);
+    if (with_m) ptxh::bulk_g2s_1d(ptxh::smem_u32(Ms), coef->M, S::MBYTES, bar);
+  };
+  int seg = blockIdx.x;
+  if (tid == 0 && seg < nseg) issue(seg, 0, true);
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int st = it & 1;
+    double* X = st0 + st * S::STAGE;
+    if (tid == 0 && seg + (int)gridDim.x < nseg) {
+      ptxh::bulk_wait_read0();  // stage st^1's previous result has been stored
+      ptxh::fence_proxy_async_smem();
+      issue(seg + gridDim.x, st ^ 1, false);
+    }
+    while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+    // ---- phase A: forward x, y on plane (tA, eA) ---------------------------
+    {
+      const double* pl = X + (tA * E + eA) * NPC;
+      double u[NPC];
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) u[k] = pl[k];
+      double ar[N1][NR > 0 ? NR : 1];
+      C2 ac[N1][NP];
+#pragma unroll
+      for (int y = 0; y < N1; ++y) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          double sacc = 0.0;
+#pragma unroll
+          for (int x = 0; x < N1; ++x) sacc = fma(c.FX[k][x][0], u[y * N1 + x], sacc);
+          ar[y][k] = sacc;
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int x = 0; x < N1; ++x) {
+            re = fma(c.FX[NR + p][x][0], u[y * N1 + x], re);
+            im = fma(c.FX[NR + p][x][1], u[y * N1 + x], im);
+          }
+          ac[y][p] = {re, im};
+        }
+      }
+#pragma unroll
+      for (int iy = 0; iy < N1; ++iy) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int y = 0; y < N1; ++y) {
+            re = fma(c.FY[iy][y][0], ar[y][k], re);
+            im = fma(c.FY[iy][y][1], ar[y][k], im);
+          }
+          Ct[(tA * KM + iy * KX + k) * E + eA] = make_double2(re, im);
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          C2 b = {0.0, 0.0};
+#pragma unroll
+          for (int y = 0; y < N1; ++y) cmac(b, c.FY[iy][y][0], c.FY[iy][y][1], ac[y][p]);
+          Ct[(tA * KM + iy * KX + NR + p) * E + eA] = make_double2(b.r, b.i);
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase B: temporal solve per (cell, mode); the mode is warp-uniform --
+#pragma unroll 1
+    for (int m = warp; m < KM; m += S::NW) {
+      C2 v[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const double2 d = Ct[(t * KM + m) * E + lane];
+        v[t] = {d.x, d.y};
+      }
+#pragma unroll
+      for (int q = 0; q < NT; ++q) {
+        C2 acc = {0.0, 0.0};
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const double2 mm = Ms[(m * kFdm2MaxN + q) * kFdm2MaxN + t];
+          cmac(acc, mm.x, mm.y, v[t]);
+        }
+        Ct[(q * KM + m) * E + lane] = make_double2(acc.r, acc.i);
+      }
+    }
+    __syncthreads();
+    // ---- phase A': inverse y, x, in place ----------------------------------
+    {
+      double* pl = X + (tA * E + eA) * NPC;
+      C2 h[N1][KX];
+#pragma unroll
+      for (int iy = 0; iy < N1; ++iy)
+#pragma unroll
+        for (int k = 0; k < KX; ++k) {
+          const double2 d = Ct[(tA * KM + iy * KX + k) * E + eA];
+          h[iy][k] = {d.x, d.y};
+        }
+#pragma unroll
+      for (int y = 0; y < N1; ++y) {
+        double mr[NR > 0 ? NR : 1];
+        C2 mc[NP];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {  // real x mode: the real part is the value
+          double re = 0.0;
+#pragma unroll
+          for (int iy = 0; iy < N1; ++iy)
+            re = fma(c.IY[y][iy][0], h[iy][k].r, fma(-c.IY[y][iy][1], h[iy][k].i, re));
+          mr[k] = re;
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          C2 b = {0.0, 0.0};
+#pragma unroll
+          for (int iy = 0; iy < N1; ++iy) cmac(b, c.IY[y][iy][0], c.IY[y][iy][1], h[iy][NR + p]);
+          mc[p] = b;
+        }
+#pragma unroll
+        for (int x = 0; x < N1; ++x) {
+          double o = 0.0;
+#pragma unroll
+          for (int k = 0; k < NR; ++k) o = fma(c.IX[x][k][0], mr[k], o);
+#pragma unroll
+          for (int p = 0; p < NP; ++p)
+            o = fma(c.IX[x][NR + p][0], mc[p].r, fma(-c.IX[x][NR + p][1], mc[p].i, o));
+          pl[y * N1 + x] = o;
+        }
+      }
+    }
+    ptxh::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t src = ptxh::smem_u32(X);
+      double* dst = out + (long long)seg * E * NPC;
+      for (int t = 0; t < NT; ++t) ptxh::bulk_s2g_1d(dst + t * ns, src + t * PB, PB);
+      ptxh::bulk_commit();
+    }
+  }
+  if (tid == 0) ptxh::bulk_wait0();
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -662,6 +864,51 @@ int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const G
   if (grid > nseg) grid = nseg;
   launch_ex(kPdlFdm, kern, grid, f3::THREADS, f3::SMEM, s, map, map_out, coef, host_coef, g, skip);
   return 1;
+}
+
+namespace {
+// (n1, n_tau, nr, np) instances: c2 (5, 5, 1, 2) and the n = 4 / 3 analogues
+template <int N1, int NT, int NR, int NP>
+int launch_fdm2_t(const FdmCoef2* coef, const FdmCoef2& hc, const Geometry& g, const double* in,
+                  double* out, cudaStream_t s, Skip skip) {
+  using S = f2::Shape<N1, NT, NR, NP>;
+  static int occ_dev[kMaxDevices];
+  const int dev = device_slot();
+  int& occ = occ_dev[dev];
+  if (occ <= 0) {
+    cudaFuncSetAttribute(fdm2_kernel<N1, NT, NR, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fdm2_kernel<N1, NT, NR, NP>, S::THREADS,
+                                                  S::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nseg = g.n_cells / f2::E;
+  int grid = occ * sms;
+  if (grid > nseg) grid = nseg;
+  launch_ex(kPdlFdm, fdm2_kernel<N1, NT, NR, NP>, grid, S::THREADS, S::SMEM, s, in, out, coef, hc,
+            g, skip);
+  return 1;
+}
+}  // namespace
+
+bool fdm2_supported(const Geometry& g, int n_tau, int nr, int np) {
+  if (g.dim != 2 || g.n_cells % f2::E != 0 || (g.n_sdof * 8) % 16 != 0 || std::getenv("STG_NO_FDM2"))
+    return false;
+  return (g.n1 == 5 && n_tau == 5 && nr == 1 && np == 2) ||
+         (g.n1 == 4 && n_tau == 4 && nr == 0 && np == 2) ||
+         (g.n1 == 3 && n_tau == 3 && nr == 1 && np == 1);
+}
+
+int launch_precond_fdm2(const FdmCoef2* coef, const FdmCoef2& hc, const Geometry& g, int n_tau,
+                        int nr, int np, const double* in, double* out, cudaStream_t s, Skip skip) {
+  if (!fdm2_supported(g, n_tau, nr, np) || (reinterpret_cast<uintptr_t>(in) & 15) ||
+      (reinterpret_cast<uintptr_t>(out) & 15))
+    return -1;
+  if (g.n1 == 5) return launch_fdm2_t<5, 5, 1, 2>(coef, hc, g, in, out, s, skip);
+  if (g.n1 == 4) return launch_fdm2_t<4, 4, 0, 2>(coef, hc, g, in, out, s, skip);
+  return launch_fdm2_t<3, 3, 1, 1>(coef, hc, g, in, out, s, skip);
 }
 
 }  // namespace stg

@@ -310,8 +310,9 @@ constexpr int kPre = 128 * kTE / kDenseThreads;  // prefetched doubles per threa
 __global__ void __launch_bounds__(kDenseThreads, 1)
     k_eblock_dense(double* __restrict__ out, const double* __restrict__ in,
                    const double* __restrict__ B, int nb, int npc, int nt, int ncells,
-                   long long ns) {
+                   long long ns, Skip skip) {
   pdl_entry();
+  if (skip_now(skip)) return;
   extern __shared__ double sm[];
   constexpr int NBP = 128;                  // padded row count of B^T (4 rows x 32 groups)
   double* Bt = sm;                          // [nb][NBP]: Bt[k][row] = B[row][k]
@@ -576,7 +577,7 @@ void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long n
 }
 
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
-                          int ncells, long long ns, cudaStream_t s) {
+                          int ncells, long long ns, cudaStream_t s, Skip skip) {
   const int nb = nt * npc;
   if (nb > kDenseMax) return false;
   const size_t smem = sizeof(double) * ((size_t)nb * 128 + (size_t)128 * kTEp);
@@ -592,7 +593,8 @@ bool precond_eblock_dense(double* out, const double* in, const double* B, int nt
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int ntile = (ncells + kTE - 1) / kTE;
   const int grid = ntile < sms ? ntile : sms;
-  launch_ex(kPdlPrecond, k_eblock_dense, grid, kDenseThreads, smem, s, out, in, B, nb, npc, nt, ncells, ns);
+  launch_ex(kPdlPrecond, k_eblock_dense, grid, kDenseThreads, smem, s, out, in, B, nb, npc, nt,
+            ncells, ns, skip);
   return true;
 }
 

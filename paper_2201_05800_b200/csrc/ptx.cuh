@@ -74,5 +74,12 @@ __device__ __forceinline__ void bulk_g2s_1d(uint32_t dst, const void* src, uint3
       : "memory");
 }
 
+// 1-D bulk copy shared -> global (bulk-group completion; bytes % 16 == 0)
+__device__ __forceinline__ void bulk_s2g_1d(void* dst, uint32_t src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(src), "r"(bytes)
+               : "memory");
+}
+
 }  // namespace ptxh
 }  // namespace stg

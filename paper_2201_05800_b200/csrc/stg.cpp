@@ -2,7 +2,6 @@
 // dispatch, device-resident GMRES(m), Newton and the STDG / LoDG steps.
 // Control flow follows the reference drivers (stdg.hpp:120-143,
 // lodg.hpp:89-149, newton.hpp:102-130); all vector work is on the device.
-#include <cublas_v2.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -119,10 +118,14 @@ struct stg_handle {
   DevBuf etab;  // d = 1 advection element block (shared), keyed by mix
   stg::MixCoef etab_mix{};
   bool etab_valid = false;
-  DevBuf dtab, pz1, pz2;  // d = 2 dense block; element-major work vectors
-  cublasHandle_t cublas = nullptr;
+  DevBuf dtab;  // d = 2 dense block (fallback of the d = 2 FDM)
   stg::MixCoef dense_mix{};
   bool dense_valid = false;
+  DevBuf fdm2M;  // device copy of the fdm2_kernel factors (stg::FdmCoef2)
+  std::unique_ptr<stg::FdmCoef2> fdm2_host;
+  stg::MixCoef fdm2_mix{};
+  bool fdm2_valid = false;
+  int fdm2_nr = 0, fdm2_np = 0;
   // d = 3 fast-diagonalisation factors and the mix they belong to
   stg::FdmCoef fdm{};
   stg::MixCoef fdm_mix{};
@@ -148,17 +151,12 @@ struct stg_handle {
   // fused residual reductions (fast 3-D kernel): requested by newton() for
   // its residual applies; red_done: the last apply produced them
   bool red = false, red_done = false;
-  // slab vectors handed to the operator / preconditioner are element-major
-  // (set around a d = 2 GMRES solve with the dense element block, see newton)
-  int em = 0;
-  DevBuf emb, emx;  // element-major right-hand side and solution
   // pipelined host-buffer path: copy-in / copy-out streams and chunk events
   static constexpr int kChunks = 8;
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_start = nullptr, ev_in[kChunks] = {}, ev_c[kChunks] = {};
 
   ~stg_handle() {
-    if (cublas) cublasDestroy(cublas);
     if (pinned) cudaFreeHost(pinned);
     if (gpin) cudaFreeHost(gpin);
     if (mapped) cudaFreeHost(mapped);
@@ -267,7 +265,6 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   a.W = W;
   a.R = R;
   a.skip = h->skip;
-  a.em = h->em;
   if (h->red) {  // max |R| and <R,R> from the apply itself (fast 3-D kernel)
     a.red_max = reinterpret_cast<unsigned long long*>(h->small.p + kRedMaxSlot);
     a.red_ss = h->small.p + kRedSsSlot;
@@ -780,17 +777,6 @@ struct NewtonOut {
 struct LinSys {
   Op A;
   Op P;
-  // A and P also run on element-major vectors (d = 2 dense element block):
-  // the solve is done in that layout, with one permute each way
-  bool element_major = false;
-};
-
-// sets the handle's element-major mode for the operator / preconditioner
-// launches made while in scope
-struct EmScope {
-  stg_handle* h;
-  explicit EmScope(stg_handle* hh) : h(hh) { h->em = 1; }
-  ~EmScope() { h->em = 0; }
 };
 
 // newton_solve (newton.hpp:102-130) on device vectors; u holds u0 on entry.
@@ -840,22 +826,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     // J du = -r: the sign is folded into GMRES (b_sign = -1); du needs no
     // zero fill (gmres with x_zero writes it)
     GmresStats gs;
-    if (J.element_major) {  // solve in the preconditioner's layout
-      const int nt = h->nt, npc = h->g.npc;
-      const long long ns = h->n_sdof;
-      h->emb.ensure(size_t(n));
-      h->emx.ensure(size_t(n));
-      stg::permute_to_elem(h->emb.p, r, nt, npc, ns, h->stream);
-      {
-        EmScope scope(h);
-        gs = gmres(h, J.A, h->emb.p, h->emx.p, n, cfg.gmres_restart, cfg.gmres_tol,
-                   cfg.gmres_max_it, J.P ? &J.P : nullptr, /*x_zero=*/true,
-                   /*pipelined=*/true, /*b_sign=*/-1.0, /*want_rel=*/false,
-                   /*bb_ready=*/bb_ready);
-      }
-      stg::permute_from_elem(du, h->emx.p, nt, npc, ns, h->stream);
-      h->launches += 2;
-    } else {
+    {
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
                  J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/true,
                  /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready, /*add_to=*/u);
@@ -1320,61 +1291,102 @@ int resolve_precond(const stg_handle* h, int kind) {
   return kind;
 }
 
-// whether a d = 2 linear solve can run element-major: the dense element
-// block preconditioner with the plane kernel for the Jacobian action
-// (S diagonal: the slab and A^-1-form stage Jacobians)
-bool element_major_ok(const stg_handle* h, int precond, bool full_s) {
-  static const bool off = std::getenv("STG_NO_ELEMENT_MAJOR") != nullptr ||
-                          std::getenv("STG_DENSE_OWN_KERNEL") != nullptr;
-  if (off || h->desc.dim != 2 || h->desc.model != STG_MODEL_ADVECTION || full_s) return false;
-  if (!dense2d_ok(h) || resolve_precond(h, precond) != STG_PRECOND_EBLOCK) return false;
-  stg::SlabArgs a{};
-  a.g = h->g;
-  a.model = h->desc.model;
-  a.n_in = a.n_out = h->nt;
-  static double aligned_probe[2] __attribute__((aligned(16)));  // only its alignment is read
-  a.X = aligned_probe;
-  a.R = aligned_probe;
-  a.em = 1;
-  return stg::slab_em_supported(a);
-}
-
-// d = 2 dense element block: out = B in for every element.  A plain GEMM
-// (nb x nb) x (nb x n_cells) on the element-major copy of the vector: permute
-// (own kernel), cuBLAS DGEMM, permute back.  STG_DENSE_OWN_KERNEL=1 uses the
-// hand-written smem-tiled kernel instead (kernels_precond.cu).
+// d = 2 dense element block (the fallback of the d = 2 FDM: meshes whose cell
+// count is not a multiple of 32, other (n, n_tau)): out = B in for every
+// element, hand-written shared-memory-tiled kernel (kernels_precond.cu)
 Op dense_op(stg_handle* h, const double* tab, int nt, int npc, int ncells, long long ns) {
   return [h, tab, nt, npc, ncells, ns](const double* in, double* out) {
-    static const bool own = std::getenv("STG_DENSE_OWN_KERNEL") != nullptr;
-    if (own) {
-      if (!stg::precond_eblock_dense(out, in, tab, nt, npc, ncells, ns, h->stream))
-        throw std::runtime_error("element-block preconditioner launch failed");
-      h->launches++;
-      return;
-    }
-    const int nb = nt * npc;
-    const size_t n = size_t(ns) * nt;
-    if (!h->cublas && cublasCreate(&h->cublas) != CUBLAS_STATUS_SUCCESS)
-      throw CudaError("cublasCreate failed");
-    cublasSetStream(h->cublas, h->stream);
-    const double one = 1.0, zero = 0.0;
-    // column-major: Yp (nb x cells) = B Xp; the row-major B is op(T) of its buffer
-    if (h->em) {  // vectors already element-major: the GEMM alone
-      if (cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, nb, ncells, nb, &one, tab, nb, in, nb,
-                      &zero, out, nb) != CUBLAS_STATUS_SUCCESS)
-        throw CudaError("cublasDgemm failed");
-      h->launches++;
-      return;
-    }
-    h->pz1.ensure(n);
-    h->pz2.ensure(n);
-    stg::permute_to_elem(h->pz1.p, in, nt, npc, ns, h->stream, h->skip);
-    if (cublasDgemm(h->cublas, CUBLAS_OP_T, CUBLAS_OP_N, nb, ncells, nb, &one, tab, nb, h->pz1.p,
-                    nb, &zero, h->pz2.p, nb) != CUBLAS_STATUS_SUCCESS)
-      throw CudaError("cublasDgemm failed");
-    stg::permute_from_elem(out, h->pz2.p, nt, npc, ns, h->stream, h->skip);
-    h->launches += 3;
+    if (!stg::precond_eblock_dense(out, in, tab, nt, npc, ncells, ns, h->stream, h->skip))
+      throw std::runtime_error("element-block preconditioner launch failed");
+    h->launches++;
   };
+}
+
+// Factors of fdm2_kernel (kernels_fdm.cu) for the d = 2 element-local block
+// L_e = T (x) I + S (x) (V_y (+) V_x): complex eigen-decompositions of V_x
+// (its real eigenvectors made real) and V_y, and per kept spatial mode
+// theta = thy + thx the temporal inverse (T + theta S)^-1.  nr / np: real x
+// eigenvalues and complex-conjugate pairs.  False when an eigen-
+// decomposition is inaccurate or a temporal block singular.
+bool build_fdm2(const stg::SpatialCoef& sp, const stg::MixCoef& mx, int n, int nt,
+                stg::FdmCoef2& c, int& nr, int& np) {
+  using stg::cplx;
+  try {
+    std::vector<cplx> th[2], P[2], Pi[2];
+    for (int a = 0; a < 2; ++a) {
+      std::vector<double> V(size_t(n) * n);
+      for (int i = 0; i < n; ++i)
+        for (int k = 0; k < n; ++k) V[size_t(i) * n + k] = sp.V[a][i][k];
+      if (!stg::eig_real(V, n, th[a], P[a], Pi[a])) return false;
+    }
+    // x: real eigenvalues (made-real eigenvectors) first, then one member
+    // (Im > 0) of each conjugate pair
+    std::vector<int> kept;
+    nr = np = 0;
+    for (int k = 0; k < n; ++k)
+      if (th[0][size_t(k)].imag() == 0.0) {
+        cplx big = 0.0;
+        for (int r = 0; r < n; ++r)
+          if (std::abs(P[0][size_t(r) * n + k]) > std::abs(big)) big = P[0][size_t(r) * n + k];
+        const cplx ph = std::conj(big) / std::abs(big);
+        for (int r = 0; r < n; ++r)
+          P[0][size_t(r) * n + k] = cplx((P[0][size_t(r) * n + k] * ph).real(), 0.0);
+        kept.push_back(k);
+        ++nr;
+      }
+    for (int k = 0; k < n; ++k)
+      if (th[0][size_t(k)].imag() > 0.0) {
+        kept.push_back(k);
+        ++np;
+      }
+    if (nr + 2 * np != n) return false;
+    if (!stg::cinverse(P[0], Pi[0], n)) return false;
+    double err = 0.0, mxv = 0.0;  // the rephased factorisation still reproduces V_x
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) {
+        cplx acc = 0.0;
+        for (int k = 0; k < n; ++k)
+          acc += P[0][size_t(r) * n + k] * th[0][size_t(k)] * Pi[0][size_t(k) * n + q];
+        err = std::max(err, std::abs(acc - sp.V[0][r][q]));
+        mxv = std::max(mxv, std::abs(sp.V[0][r][q]));
+      }
+    if (!(err <= 1e-11 * std::max(mxv, 1e-300))) return false;
+    std::memset(&c, 0, sizeof c);
+    auto put = [](double* dst, cplx z) {
+      dst[0] = z.real();
+      dst[1] = z.imag();
+    };
+    const int kx = nr + np;
+    for (int j = 0; j < kx; ++j) {
+      const int k = kept[size_t(j)];
+      const bool real_mode = j < nr;
+      for (int x = 0; x < n; ++x) {
+        cplx f = Pi[0][size_t(k) * n + x];
+        if (real_mode) f = cplx(f.real(), 0.0);
+        put(c.FX[j][x], f);
+        put(c.IX[x][j], (real_mode ? 1.0 : 2.0) * P[0][size_t(x) * n + k]);
+      }
+    }
+    for (int r = 0; r < n; ++r)
+      for (int q = 0; q < n; ++q) {
+        put(c.FY[r][q], Pi[1][size_t(r) * n + q]);
+        put(c.IY[r][q], P[1][size_t(r) * n + q]);
+      }
+    std::vector<cplx> A(size_t(nt) * nt), Ai;
+    for (int iy = 0; iy < n; ++iy)
+      for (int j = 0; j < kx; ++j) {
+        const cplx theta = th[1][size_t(iy)] + th[0][size_t(kept[size_t(j)])];
+        for (int r = 0; r < nt; ++r)
+          for (int t = 0; t < nt; ++t) A[size_t(r) * nt + t] = mx.T[r][t] + theta * mx.S[r][t];
+        if (!stg::cinverse(A, Ai, nt)) return false;
+        const int m = iy * kx + j;
+        for (int it = 0; it < nt; ++it)
+          for (int t = 0; t < nt; ++t) put(c.M[m][it][t], Ai[size_t(it) * nt + t]);
+      }
+    return true;
+  } catch (const std::exception&) {
+    return false;
+  }
 }
 
 // Inverse of the (shared) element block of the d = 1 advection Jacobian with
@@ -1506,6 +1518,34 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream, h->skip);
       h->launches++;
     };
+  }
+  if (d == 2 && n1 <= stg::kFdm2MaxN && nt <= stg::kFdm2MaxN) {  // d = 2 FDM
+    bool ok = h->fdm2_valid && std::memcmp(&h->fdm2_mix, &mx, sizeof mx) == 0;
+    if (!ok) {
+      auto c = std::make_unique<stg::FdmCoef2>();
+      int nr = 0, np = 0;
+      if (build_fdm2(h->sp, mx, n1, nt, *c, nr, np) && stg::fdm2_supported(h->g, nt, nr, np)) {
+        h->fdm2M.ensure(sizeof(stg::FdmCoef2) / sizeof(double));
+        ck(cudaMemcpyAsync(h->fdm2M.p, c.get(), sizeof(stg::FdmCoef2), cudaMemcpyHostToDevice,
+                           h->stream), "H2D");
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        h->fdm2_host = std::move(c);
+        h->fdm2_mix = mx;
+        h->fdm2_nr = nr;
+        h->fdm2_np = np;
+        h->fdm2_valid = ok = true;
+      }
+    }
+    if (ok) {
+      const stg::FdmCoef2* c = reinterpret_cast<const stg::FdmCoef2*>(h->fdm2M.p);
+      const stg::FdmCoef2* hc = h->fdm2_host.get();
+      const int nr = h->fdm2_nr, np = h->fdm2_np;
+      return [h, c, hc, nt, nr, np](const double* in, double* out) {
+        if (stg::launch_precond_fdm2(c, *hc, h->g, nt, nr, np, in, out, h->stream, h->skip) < 0)
+          throw std::runtime_error("element-block preconditioner launch failed");
+        h->launches++;
+      };
+    }
   }
   if (d == 2) {  // one shared dense element block (advection)
     const int nbd = nt * npc;
@@ -1727,7 +1767,6 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
             st_jvp(h, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
-          L.element_major = element_major_ok(h, cfg.precond, false);
           return L;
         },
         U, n, cfg);
@@ -1775,7 +1814,6 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
             stage_jvp(h, form, dt, X, v, Jv, eps, un2);
           };
           L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
-          L.element_major = element_major_ok(h, cfg.precond, form == STG_FORM_A);
           return L;
         },
         U, n, cfg);

@@ -8,3 +8,5 @@ python scripts/fdm_graph_bench.py c4 > gpurun_out/fdm_ab_param.json 2>&1
 STG_FDM3_SMEMC=1 python scripts/fdm_graph_bench.py c4 > gpurun_out/fdm_ab_smemc.json 2>&1
 STG_FDM_V1=1 python scripts/fdm_graph_bench.py c4 > gpurun_out/fdm_ab_v1.json 2>&1
 python scripts/fdm_graph_bench.py c4 1 > gpurun_out/fdm_ab_tblock.json 2>&1
+python scripts/fdm_graph_bench.py c2 > gpurun_out/fdm_ab_c2_fdm2.json 2>&1
+STG_NO_FDM2=1 python scripts/fdm_graph_bench.py c2 > gpurun_out/fdm_ab_c2_dense.json 2>&1

@@ -28,7 +28,7 @@ def main(out: str) -> None:
         U, _, info = op.stdg_step(0.0, cfg.dt, un, nc)
         res[name] = U.cpu().numpy()
         res[name + "_its"] = np.array([info.newton_iterations, info.linear_iterations])
-    # c2 physics on 32 x 8 cells: the dense element block, solved element-major
+    # c2 physics on 32 x 8 cells: the d = 2 element block (FDM; dense with STG_NO_FDM2=1)
     c2 = C.CONFIGS["c2"].scaled((32, 8))
     op2 = SlabOperator(**c2.kwargs())
     u2 = torch.as_tensor(C.initial_state(c2), device="cuda")

@@ -12,8 +12,9 @@ tests check the mechanisms one by one:
   any arithmetic;
 * forcing the second Gram-Schmidt pass on every step
   (STG_GMRES_REORTH_TOL=0.5) gives the same converged solutions;
-* the element-major d = 2 solve (dense element block) matches the
-  stage-major one (STG_NO_ELEMENT_MAJOR=1) and the oracle.
+* the d = 2 solve with the fast-diagonalisation element block (fdm2_kernel,
+  default) matches the one with the dense element block (STG_NO_FDM2=1) and
+  the oracle.
 The knobs are read once per process, so each variant is a subprocess
 (tests/_gmres_runner.py).  The forced-second-pass run found a real bug: a
 Jacobian action that reduces into the step's scratch (the unfused FD J.v)
@@ -104,11 +105,11 @@ def test_forced_reorthogonalisation_same_solutions(base, tmp_path_factory):
         assert rel(other[k], base[k]) <= TOL_SOLVE, k
 
 
-def test_element_major_solve_matches_stage_major(base, tmp_path_factory):
-    # d = 2 with the dense element block solves in element-major order (one
-    # permute each way per Newton step instead of two per preconditioner
-    # apply); the stage-major path is the reference
-    other = run(tmp_path_factory, STG_NO_ELEMENT_MAJOR="1")
+def test_fdm2_solve_matches_dense_element_block(base, tmp_path_factory):
+    # d = 2: the element-block inverse by fast diagonalisation (fdm2_kernel)
+    # and by the dense block (k_eblock_dense) are the same operator, so the
+    # solves agree and take the same number of GMRES iterations
+    other = run(tmp_path_factory, STG_NO_FDM2="1")
     for k in ["c2", "c2rk"]:
         assert rel(other[k], base[k]) <= TOL_SOLVE, k
     assert base["c2_its"][1] == other["c2_its"][1]

@@ -457,12 +457,22 @@ def test_full_c3_residual_parity():
     assert rel(op.st_residual(0.0, cfg.dt, dev(un), dev(U)), pr.st_residual(0.0, cfg.dt, un, U)) <= TOL_OP
 
 
-def test_dense_2d_element_block_is_exact_local_inverse():
-    """d = 2 EBLOCK (one shared dense block, kernels_precond.cu) = the exact
-    inverse of the element-local block read off the oracle's J.v."""
-    cfg = make(2, 4, 5, (4, 3), (1.0, -0.5), dt=0.003)
+@pytest.mark.parametrize("cells,velocity,degree", [
+    ((4, 3), (1.0, -0.5), 4),      # 12 cells: the dense block (kernels_precond.cu)
+    ((8, 4), (1.0, -0.5), 4),      # 32 cells: fdm2_kernel <5, 5, 1, 2>
+    ((16, 4), (-0.8, 0.3), 4),
+    ((8, 8), (1.0, 0.5), 4),
+    ((8, 4), (0.0, 0.7), 4),       # b_x = 0: V_x has no FDM form -> dense block
+    ((8, 4), (0.6, -1.1), 3),      # n = 4, n_tau = 4: fdm2_kernel <4, 4, 0, 2>
+    ((16, 2), (1.0, 1.0), 2),      # n = 3, n_tau = 3: fdm2_kernel <3, 3, 1, 1>
+])
+def test_2d_element_block_is_exact_local_inverse(cells, velocity, degree):
+    """d = 2 EBLOCK (fast diagonalisation, kernels_fdm.cu fdm2_kernel, or the
+    shared dense block) = the exact inverse of the element-local block read
+    off the oracle's J.v."""
+    cfg = make(2, degree, degree + 1, cells, velocity, dt=0.003)
     op, pr = pair(cfg)
-    ns, npc, nt = op.n_sdof, 25, 5
+    ns, npc, nt = op.n_sdof, (degree + 1) ** 2, degree + 1
     loc = np.array([t * ns + k for t in range(nt) for k in range(npc)])  # element 0
     Lblk = np.zeros((nt * npc, nt * npc))
     U0 = np.zeros(nt * ns)
@@ -472,7 +482,7 @@ def test_dense_2d_element_block_is_exact_local_inverse():
         Lblk[:, c] = pr.st_jvp(0.0, cfg.dt, U0, e)[loc]
     x = np.random.default_rng(9).standard_normal(nt * ns)
     y = op.st_precond_apply(cfg.dt, dev(x), precond=L.STG_PRECOND_EBLOCK).cpu().numpy()
-    for cell in range(12):
+    for cell in range(int(np.prod(cells))):
         idx = loc + cell * npc
         assert rel(y[idx], np.linalg.solve(Lblk, x[idx])) <= 1e-11, cell
 
