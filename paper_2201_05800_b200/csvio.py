@@ -32,16 +32,20 @@ def _lgl_weights(n: int) -> np.ndarray:
 
 
 class Grid:
-    """Uniform periodic mesh + LGL nodes (mesh.hpp:14-91), r = 1."""
+    """Uniform periodic mesh + LGL nodes (mesh.hpp:14-91), r components per
+    node, component innermost (coeff_index, mesh.hpp:78-81)."""
 
     def __init__(self, d: int, p: int, cells: Sequence[int], lower: Sequence[float],
-                 upper: Sequence[float]):
-        self.d, self.p = int(d), int(p)
+                 upper: Sequence[float], r: int = 1):
+        self.d, self.p, self.r = int(d), int(p), int(r)
         self.cells, self.lower, self.upper = list(cells), list(lower), list(upper)
         self.n1 = self.p + 1
         self.npc = self.n1 ** self.d
         self.n_cells = int(np.prod(self.cells))
-        self.dof = self.n_cells * self.npc
+        self.dof = self.n_cells * self.npc * self.r
+
+    def index(self, cell: int, node: int, comp: int) -> int:
+        return (cell * self.npc + node) * self.r + comp
 
     def coord_header(self) -> str:
         return {1: "x", 2: "x,y", 3: "x,y,z"}[self.d]
@@ -74,7 +78,9 @@ def write_field_csv(g: Grid, coeffs, path: str, label: str = "field") -> None:
     with _open(path, label) as f:
         f.write(f"{g.coord_header()},component,value\n")
         for cell, node, x in g.coords():
-            f.write(",".join(fmt_g(v) for v in x) + f",0,{fmt_g(u[cell * g.npc + node])}\n")
+            xs = ",".join(fmt_g(v) for v in x)
+            for comp in range(g.r):
+                f.write(f"{xs},{comp},{fmt_g(u[g.index(cell, node, comp)])}\n")
 
 
 def write_trajectory_csv(g: Grid, times, states, path: str, label: str = "trajectory") -> None:
@@ -87,25 +93,31 @@ def write_trajectory_csv(g: Grid, times, states, path: str, label: str = "trajec
         hprod *= (g.upper[a] - g.lower[a]) / float(g.cells[a])
     vol_scale = hprod / math.pow(2.0, g.d)
     with _open(path, label) as f:
-        f.write("step,t,norm_c0\n")
+        f.write("step,t" + "".join(f",norm_c{c}" for c in range(g.r)) + "\n")
         for k, st in enumerate(states):
             u = _host(st)
-            acc = 0.0
-            for cell in range(g.n_cells):  # the reference's summation order
-                for node in range(g.npc):
-                    wn = w[node % g.n1]
-                    if g.d >= 2:
-                        wn *= w[(node // g.n1) % g.n1]
-                    if g.d >= 3:
-                        wn *= w[node // (g.n1 * g.n1)]
-                    v = u[cell * g.npc + node]
-                    acc += vol_scale * wn * v * v
-            f.write(f"{k},{fmt_g(times[k])},{fmt_g(math.sqrt(acc))}\n")
+            if u.size != g.dof:
+                raise ValueError("write_trajectory_csv: state size mismatch")
+            row = f"{k},{fmt_g(times[k])}"
+            for comp in range(g.r):
+                acc = 0.0
+                for cell in range(g.n_cells):  # the reference's summation order
+                    for node in range(g.npc):
+                        wn = w[node % g.n1]
+                        if g.d >= 2:
+                            wn *= w[(node // g.n1) % g.n1]
+                        if g.d >= 3:
+                            wn *= w[node // (g.n1 * g.n1)]
+                        v = u[g.index(cell, node, comp)]
+                        acc += vol_scale * wn * v * v
+                row += f",{fmt_g(math.sqrt(acc))}"
+            f.write(row + "\n")
 
 
 def write_elements_csv(g: Grid, n_tau: int, times, element_solutions, path: str,
                        label: str = "elements") -> None:
-    """write_elements_csv (csv.hpp:77-109): one row per (element, stage, node)."""
+    """write_elements_csv (csv.hpp:77-109): one row per (element, stage, node,
+    component)."""
     if len(element_solutions) + 1 != len(times):
         raise ValueError("write_elements_csv: size mismatch")
     tau = lgl_nodes(n_tau)
@@ -119,5 +131,7 @@ def write_elements_csv(g: Grid, n_tau: int, times, element_solutions, path: str,
                 t = times[n] + 0.5 * dt * (1.0 + tau[j])
                 head = f"{n},{j},{fmt_g(tau[j])},{fmt_g(t)},"
                 for cell, node, x in coords:
-                    val = U[j * g.dof + cell * g.npc + node]
-                    f.write(head + ",".join(fmt_g(v) for v in x) + f",0,{fmt_g(val)}\n")
+                    xs = ",".join(fmt_g(v) for v in x)
+                    for comp in range(g.r):
+                        val = U[j * g.dof + g.index(cell, node, comp)]
+                        f.write(f"{head}{xs},{comp},{fmt_g(val)}\n")

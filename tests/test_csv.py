@@ -44,12 +44,13 @@ CPP = r'''
 using namespace stdgsem::gpu::csv;
 int main(int argc, char** argv) {
   const std::string dir = argv[1];
-  struct C { int d, p; std::vector<int> cells; };
-  const C cases[] = {{1, 3, {5}}, {2, 2, {3, 2}}, {3, 1, {2, 3, 2}}};
+  struct C { int d, p; std::vector<int> cells; int r; };
+  const C cases[] = {{1, 3, {5}, 1}, {2, 2, {3, 2}, 1}, {3, 1, {2, 3, 2}, 1}, {2, 1, {3, 2}, 4},
+                     {1, 2, {3}, 2}};
   int i = 0;
   for (const C& c : cases) {
     Grid g;
-    g.d = c.d; g.p = c.p; g.cells = c.cells;
+    g.d = c.d; g.p = c.p; g.cells = c.cells; g.r = c.r;
     g.lower.assign(size_t(c.d), 0.25); g.upper.assign(size_t(c.d), 1.75);
     std::vector<double> u(static_cast<size_t>(g.dof()));
     for (size_t k = 0; k < u.size(); ++k) u[k] = std::sin(0.37 * double(k)) * 1e-3 + 1.0 / (k + 3);
@@ -76,9 +77,10 @@ def test_cpp_and_python_writers_agree(tmp_path):
     subprocess.run([cxx, "-std=c++17", "-O2", f"-I{ROOT / 'include'}", str(src), f"-L{lib}",
                     "-lstg_cuda", f"-Wl,-rpath,{lib}", "-o", str(exe)], check=True)
     subprocess.run([str(exe), str(tmp_path)], check=True)
-    cases = [(1, 3, [5]), (2, 2, [3, 2]), (3, 1, [2, 3, 2])]
-    for i, (d, p, cells) in enumerate(cases):
-        g = csvio.Grid(d, p, cells, [0.25] * d, [1.75] * d)
+    cases = [(1, 3, [5], 1), (2, 2, [3, 2], 1), (3, 1, [2, 3, 2], 1), (2, 1, [3, 2], 4),
+             (1, 2, [3], 2)]
+    for i, (d, p, cells, r) in enumerate(cases):
+        g = csvio.Grid(d, p, cells, [0.25] * d, [1.75] * d, r=r)
         k = np.arange(g.dof, dtype=np.float64)
         u = np.sin(0.37 * k) * 1e-3 + 1.0 / (k + 3)
         kk = np.arange(3 * g.dof, dtype=np.float64)
@@ -91,3 +93,24 @@ def test_cpp_and_python_writers_agree(tmp_path):
             a = (tmp_path / f"cpp{i}_{kind}.csv").read_bytes()
             b = Path(f"{s}_{kind}.csv").read_bytes()
             assert a == b, (d, kind)
+
+
+def test_multicomponent_rows_and_header(tmp_path):
+    """r > 1 (Euler, r = 4): every row carries its component index in
+    coeff_index order (csv.hpp:39-44, 57-71, 97-104) and the trajectory has a
+    norm per component.  The 1-cell, p = 1, r = 2 case written out by hand."""
+    g = csvio.Grid(1, 1, [1], [0.0], [1.0], r=2)
+    u = np.array([1.0, -2.0, 3.0, 0.5])  # (node 0: c0, c1), (node 1: c0, c1)
+    csvio.write_field_csv(g, u, tmp_path / "f.csv")
+    assert (tmp_path / "f.csv").read_text() == (
+        "# stdgsem-csv v1 field\nx,component,value\n0,0,1\n0,1,-2\n1,0,3\n1,1,0.5\n")
+    csvio.write_trajectory_csv(g, [0.0], [u], tmp_path / "t.csv")
+    # global mass: w = (1, 1), vol_scale = 1/2 -> norms sqrt((1 + 9)/2), sqrt((4 + 0.25)/2)
+    assert (tmp_path / "t.csv").read_text() == (
+        "# stdgsem-csv v1 trajectory\nstep,t,norm_c0,norm_c1\n"
+        f"0,0,{csvio.fmt_g(np.sqrt(5.0))},{csvio.fmt_g(np.sqrt(2.125))}\n")
+    U = np.arange(8.0)
+    csvio.write_elements_csv(g, 2, [0.0, 1.0], [U], tmp_path / "e.csv")
+    lines = (tmp_path / "e.csv").read_text().splitlines()
+    assert lines[2:6] == ["0,0,-1,0,0,0,0", "0,0,-1,0,0,1,1", "0,0,-1,0,1,0,2", "0,0,-1,0,1,1,3"]
+    assert lines[6] == "0,1,1,1,0,0,4" and len(lines) == 10
