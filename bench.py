@@ -156,7 +156,7 @@ class ClockSampler:
                 r = get_reasons(h)
                 act = ["Active" if r & b else "Not Active" for b in bits]
                 self.samples.append([str(sm), str(mx), "", "", *act])
-                self._stop.wait(0.01)
+                self._stop.wait(0.005)
         finally:
             N.nvmlShutdown()
 
@@ -318,9 +318,12 @@ def run_ours(args):
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
-        # clock pre-roll: the same apply for >= preroll_s before the warm-up,
-        # so the clocks are at steady state and sampled even when the timed
-        # region itself is shorter than one NVML sample (20 steps = 0.6 ms)
+        # clock pre-roll: the same apply for >= preroll_s (0.1 s) before the
+        # warm-up, so the clocks are sampled under this load even when the
+        # timed region itself is shorter than one NVML sample (20 steps =
+        # 0.6 ms).  Kept short: seconds of back-to-back applies engage the
+        # power cap (sw_power_cap, SM ~1.85 GHz, R(U) 29.3 -> 31 us), which a
+        # 20-step burst does not see.
         t0 = time.perf_counter()
         i = 0
         while time.perf_counter() - t0 < args.preroll_s:
@@ -799,7 +802,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
-    ap.add_argument("--preroll-s", type=float, default=0.5)
+    ap.add_argument("--preroll-s", type=float, default=0.1)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":

@@ -426,7 +426,7 @@ __device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int r
 template <bool PARAM>
 __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs, double* X, int e,
                                           int q) {
-  C2 v[4][4];  // [t][z] -> [t][iz] -> [it][iz] -> [t][z], in place
+  C2 v[4][4];  // [t][z] -> [t][iz] -> [it][iz] -> [t][z], in place in registers
 #pragma unroll
   for (int t = 0; t < 4; ++t)
 #pragma unroll
@@ -435,50 +435,38 @@ __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs,
       v[t][z] = {d.x, d.y};
     }
 #pragma unroll
-  for (int iz = 0; iz < 4; ++iz) {  // forward z, then the temporal solve of mode (iz, q)
-    C2 fz[4];
-#pragma unroll
-    for (int z = 0; z < 4; ++z) fz[z] = f3::cf<PARAM>(c.FZ[iz][z]);
+  for (int t = 0; t < 4; ++t) {  // forward z, row by row
     C2 w[4];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int iz = 0; iz < 4; ++iz) {
       C2 acc = {0.0, 0.0};
 #pragma unroll
-      for (int z = 0; z < 4; ++z) f3::mac(acc, fz[z], v[t][z]);
-      w[t] = acc;
+      for (int z = 0; z < 4; ++z) f3::mac(acc, f3::cf<PARAM>(c.FZ[iz][z]), v[t][z]);
+      w[iz] = acc;
     }
+#pragma unroll
+    for (int iz = 0; iz < 4; ++iz) v[t][iz] = w[iz];
+  }
+#pragma unroll
+  for (int iz = 0; iz < 4; ++iz) {  // temporal solve of mode (iz, q), column by column
     C2 y[4];
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       C2 acc = {0.0, 0.0};
 #pragma unroll
-      for (int t = 0; t < 4; ++t) f3::mac(acc, f3::ld(cs.M[iz][it][t][q]), w[t]);
+      for (int t = 0; t < 4; ++t) f3::mac(acc, f3::ld(cs.M[iz][it][t][q]), v[t][iz]);
       y[it] = acc;
     }
-    // park mode iz's result in the tile (this unit's own slots; the z values
-    // are all in registers already)
 #pragma unroll
-    for (int it = 0; it < 4; ++it)
-      *f3::at(X, f3::row_of(it, e, iz), q) = make_double2(y[it].r, y[it].i);
+    for (int it = 0; it < 4; ++it) v[it][iz] = y[it];
   }
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
+  for (int t = 0; t < 4; ++t) {  // inverse z, stored
 #pragma unroll
-    for (int iz = 0; iz < 4; ++iz) {
-      const double2 d = *f3::at(X, f3::row_of(t, e, iz), q);
-      v[t][iz] = {d.x, d.y};
-    }
-  }
-#pragma unroll
-  for (int z = 0; z < 4; ++z) {  // inverse z, stored
-    C2 iz_c[4];
-#pragma unroll
-    for (int iz = 0; iz < 4; ++iz) iz_c[iz] = f3::cf<PARAM>(c.IZ[z][iz]);
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
+    for (int z = 0; z < 4; ++z) {
       C2 acc = {0.0, 0.0};
 #pragma unroll
-      for (int iz = 0; iz < 4; ++iz) f3::mac(acc, iz_c[iz], v[t][iz]);
+      for (int iz = 0; iz < 4; ++iz) f3::mac(acc, f3::cf<PARAM>(c.IZ[z][iz]), v[t][iz]);
       *f3::at(X, f3::row_of(t, e, z), q) = make_double2(acc.r, acc.i);
     }
   }
