@@ -7,6 +7,7 @@ paper_2201_05800_b200.build`` (``__graft_entry__.build()`` does this).
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libstg_cuda.so"
@@ -73,11 +74,12 @@ def load() -> ctypes.CDLL:
     global _LIB
     if _LIB is not None:
         return _LIB
-    if not LIB_PATH.exists():
+    path = Path(os.environ.get("STG_CUDA_LIB") or LIB_PATH)  # A/B builds (scripts/variants)
+    if not path.exists():
         raise RuntimeError(
-            f"{LIB_PATH} is missing: build the CUDA extension first "
+            f"{path} is missing: build the CUDA extension first "
             "(python -m paper_2201_05800_b200.build); there is no CPU fallback")
-    L = ctypes.CDLL(str(LIB_PATH))
+    L = ctypes.CDLL(str(path))
     L.stg_last_error.restype = ctypes.c_char_p
     L.stg_last_error.argtypes = [_vp]
     L.stg_newton_config_default.argtypes = [ctypes.POINTER(StgNewtonConfig)]

@@ -187,9 +187,6 @@ struct SlabArgs {
   // launch without programmatic serialisation (the launch follows a
   // cross-stream event wait, which PDL must not relax)
   int no_pdl;
-  // X and R in element-major order [cell][t][node] (d = 2 plane kernel only;
-  // the dense element-block preconditioner's layout)
-  int em;
   // fused reductions of R (fast 3-D kernel; red_done reports whether the
   // launched kernel produced them): *red_max = max |R_i| as the bit pattern
   // of a non-negative double (zeroed beforehand), *red_ss = <R,R> summed in
@@ -209,8 +206,6 @@ bool fd_fused_supported(const SlabArgs& a);
 // ---- launchers (kernels_slab.cu) -------------------------------------------
 // Returns the number of kernels launched (>= 1) or -1 if no kernel fits.
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
-// whether the element-major (a.em) variant applies to these arguments
-bool slab_em_supported(const SlabArgs& a);
 // Fast TMA path: d = 3, n = 4, n_in = n_out = 4, advection, nx % 8 == 0.
 bool slab_fast_supported(const SlabArgs& a);
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s);
@@ -354,11 +349,6 @@ void probe_extract(double* K, const double* F, int ndl, int col, int nx, int sx,
 // Binv_e = (T (x) I + S (x) K_e)^-1 per element (nt * ndl <= 32)
 bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt, int ndl,
                        int ncells, cudaStream_t s);
-// stage-major [t][cell][node] <-> element-major [cell][t][node] (n = nt * ns)
-void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s,
-                     Skip skip = {});
-void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
-                       cudaStream_t s, Skip skip = {});
 // per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U,
 // stored in fp32 (a preconditioner; applied in fp64 arithmetic)
 bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s);

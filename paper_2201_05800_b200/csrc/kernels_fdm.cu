@@ -475,8 +475,17 @@ __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs,
 // PARAM: the spatial factors are read as kernel-parameter operands (cp is
 // the FdmCoef3 by value); otherwise from the shared copy.  The temporal
 // table is always read from shared memory (per-lane addresses).
+#ifndef STG_FDM3_MINB
+#define STG_FDM3_MINB 3
+#endif
+#ifndef STG_FDM3_ROW_UNROLL
+#define STG_FDM3_ROW_UNROLL 1
+#endif
+namespace f3 {
+constexpr int kRowUnroll = STG_FDM3_ROW_UNROLL;
+}
 template <bool PARAM>
-__global__ void __launch_bounds__(f3::THREADS, 3)
+__global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
     fdm3_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_out,
                 const FdmCoef3* __restrict__ coef, const __grid_constant__ FdmCoef3 cp,
                 const Geometry g, const Skip skip) {
@@ -522,12 +531,12 @@ __global__ void __launch_bounds__(f3::THREADS, 3)
     }
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
-#pragma unroll 1
+#pragma unroll(f3::kRowUnroll)
     for (int k = 0; k < 2; ++k) fdm3_fwd_row<PARAM>(c, X, tid + k * f3::THREADS);
     __syncthreads();
     fdm3_unit<PARAM>(c, cs, X, eB, qB);
     __syncthreads();
-#pragma unroll 1
+#pragma unroll(f3::kRowUnroll)
     for (int k = 0; k < 2; ++k) fdm3_inv_row<PARAM>(c, X, tid + k * f3::THREADS);
     ptxh::fence_proxy_async_smem();
     __syncthreads();  // result tile complete

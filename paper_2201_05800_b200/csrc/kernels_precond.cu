@@ -519,62 +519,6 @@ bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
   }
 }
 
-// stage-major [t][cell][node] <-> element-major [cell][t][node], through a
-// shared-memory tile of kPermCells cells: both the global reads and the
-// global writes are contiguous runs (the per-element gather of the previous
-// version did a 64-bit division per element and reached ~3.2 TB/s).
-constexpr int kPermCells = 32;
-constexpr int kPermMaxNb = kMaxT * 25;  // nt * npc <= 150 (d = 2, N <= 4)
-template <bool TO_ELEM>
-__global__ void __launch_bounds__(kPB) k_permute(double* __restrict__ Y,
-                                                  const double* __restrict__ X, int nt,
-                                                  int npc, int ncells, long long ns, Skip skip) {
-  pdl_entry();
-  if (skip_now(skip)) return;
-  __shared__ double tile[kPermCells * kPermMaxNb];
-  const int nb = nt * npc;
-  for (int c0 = blockIdx.x * kPermCells; c0 < ncells; c0 += gridDim.x * kPermCells) {
-    const int nc = min(kPermCells, ncells - c0);
-    const int run = nc * npc;  // contiguous doubles per temporal block
-    if (TO_ELEM) {
-      for (int t = 0; t < nt; ++t) {
-        const double* src = X + t * ns + (long long)c0 * npc;
-        for (int i = threadIdx.x; i < run; i += kPB) {
-          const int e = i / npc, node = i - e * npc;
-          tile[e * nb + t * npc + node] = __ldcs(src + i);
-        }
-      }
-      __syncthreads();
-      double* dst = Y + (long long)c0 * nb;
-      for (int i = threadIdx.x; i < nc * nb; i += kPB) __stcs(dst + i, tile[i]);
-    } else {
-      const double* src = X + (long long)c0 * nb;
-      for (int i = threadIdx.x; i < nc * nb; i += kPB) tile[i] = __ldcs(src + i);
-      __syncthreads();
-      for (int t = 0; t < nt; ++t) {
-        double* dst = Y + t * ns + (long long)c0 * npc;
-        for (int i = threadIdx.x; i < run; i += kPB) {
-          const int e = i / npc, node = i - e * npc;
-          __stcs(dst + i, tile[e * nb + t * npc + node]);
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
-void permute_to_elem(double* Xp, const double* X, int nt, int npc, long long ns, cudaStream_t s,
-                     Skip skip) {
-  const int ncells = int(ns / npc);
-  const int g = std::min((ncells + kPermCells - 1) / kPermCells, 148 * 8);
-  launch_ex(kPdlPrecond, k_permute<true>, g, kPB, 0, s, Xp, X, nt, npc, ncells, ns, skip);
-}
-void permute_from_elem(double* Y, const double* Yp, int nt, int npc, long long ns,
-                       cudaStream_t s, Skip skip) {
-  const int ncells = int(ns / npc);
-  const int g = std::min((ncells + kPermCells - 1) / kPermCells, 148 * 8);
-  launch_ex(kPdlPrecond, k_permute<false>, g, kPB, 0, s, Y, Yp, nt, npc, ncells, ns, skip);
-}
 
 bool precond_eblock_dense(double* out, const double* in, const double* B, int nt, int npc,
                           int ncells, long long ns, cudaStream_t s, Skip skip) {

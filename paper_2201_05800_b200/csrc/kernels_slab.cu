@@ -768,20 +768,16 @@ __device__ __forceinline__ void bulk_wait0() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-// EM: slab vectors in element-major order [cell][t][node] (X and R; u_n is
-// a spatial vector either way) -- the layout the d = 2 dense element-block
-// preconditioner works in, so GMRES can run without per-apply permutes.
-
-template <int N1, int NT, int E, int MINB, bool EM>
+template <int N1, int NT, int E, int MINB>
 __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
     slab2d_plane(const SlabArgs a) {
   pdl_entry();
   if (skip_now(a.skip)) return;
   using P = Plane2d<N1, NT, E>;
   constexpr int NPC = P::NPC, PL = P::PLANE;
-  // plane j of segment cell c inside a staged tile / in the global vector
-  auto tp = [](int j, int c) { return EM ? c * NT * NPC + j * NPC : j * PL + c * NPC; };
-  constexpr long long CS = EM ? NT * NPC : NPC;  // global stride between cells
+  // plane j of segment cell c inside a staged tile
+  auto tp = [](int j, int c) { return j * PL + c * NPC; };
+  constexpr long long CS = NPC;  // global stride between cells
   extern __shared__ __align__(16) double sm2[];
   double* Rs = sm2 + 2 * P::STAGE;  // output staging (NT planes)
   uint64_t* bars = reinterpret_cast<uint64_t*>(Rs + NT * PL);
@@ -812,19 +808,15 @@ __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
     const uint32_t bar = stg ? bar1 : bar0;
     ptx::mbar_expect_tx(bar, sbytes);
     const uint32_t dst = ptx::smem_u32(sm2 + stg * P::STAGE);
-    if (EM) {
-      bulk_g2s(dst, a.X + (long long)seg * NT * PL, NT * pbytes, bar);
-    } else {
-      const double* src = a.X + (long long)seg * PL;
-      for (int j = 0; j < NT; ++j) bulk_g2s(dst + j * pbytes, src + j * ns, pbytes, bar);
-    }
+    const double* src = a.X + (long long)seg * PL;
+    for (int j = 0; j < NT; ++j) bulk_g2s(dst + j * pbytes, src + j * ns, pbytes, bar);
     if (hw) bulk_g2s(dst + NT * pbytes, a.W + (long long)seg * PL, pbytes, bar);
   };
   // neighbour traces that are not in the tile (global / L2)
   auto faces = [&](int seg, double* xl, double* xr, double* yl, double* yr) {
     const int cell = seg * E + e;
     const int cx = cell % nx, cy = (cell / nx) % ny;
-    const double* Xt = a.X + (EM ? (long long)t * NPC : t * ns);
+    const double* Xt = a.X + t * ns;
     if (nLx && !(e > 0 && cx > 0)) {
       const double* q = Xt + (long long)(cell - cx + (cx == 0 ? nx - 1 : cx - 1)) * CS + N1 - 1;
 #pragma unroll
@@ -918,12 +910,8 @@ __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
     ptx::fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      if (EM) {
-        bulk_s2g(a.R + (long long)seg * NT * PL, ptx::smem_u32(Rs), NT * pbytes);
-      } else {
-        for (int j = 0; j < NT; ++j)
-          bulk_s2g(a.R + j * ns + (long long)seg * PL, ptx::smem_u32(Rs + j * PL), pbytes);
-      }
+      for (int j = 0; j < NT; ++j)
+        bulk_s2g(a.R + j * ns + (long long)seg * PL, ptx::smem_u32(Rs + j * PL), pbytes);
       bulk_commit();
     }
   }
@@ -1565,17 +1553,16 @@ int launch_plane2d(const SlabArgs& a, cudaStream_t s) {
   static int occ_dev[kMaxDevices];  // 0: not set up on that device yet
   int& occ = occ_dev[device_slot()];
   if (occ <= 0) {
-    for (auto k : {slab2d_plane<N1, NT, E, MINB, false>, slab2d_plane<N1, NT, E, MINB, true>})
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane<N1, NT, E, MINB, false>,
+    cudaFuncSetAttribute(slab2d_plane<N1, NT, E, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Q::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane<N1, NT, E, MINB>,
                                                   Q::THREADS, Q::SMEM);
     if (occ < 1) occ = 1;
   }
   const int nseg = a.g.n_cells / E;
   int grid = occ * num_sms_cached();
   if (grid > nseg) grid = nseg;
-  auto k = a.em ? slab2d_plane<N1, NT, E, MINB, true> : slab2d_plane<N1, NT, E, MINB, false>;
-  launch_ex(kPdlSlab, k, grid, Q::THREADS, Q::SMEM, s, a);
+  launch_ex(kPdlSlab, slab2d_plane<N1, NT, E, MINB>, grid, Q::THREADS, Q::SMEM, s, a);
   return 1;
 }
 
@@ -1590,7 +1577,6 @@ int launch2d_t(const SlabArgs& a, cudaStream_t s) {
     // 6656 per warp and leave room for one 160-thread CTA only)
     if (plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 2>(a, s);
   }
-  if (a.em) return -1;  // element-major vectors: the plane kernel only
   if (a.g.n_cells % Sh::E == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
       (a.g.n_sdof % 2) == 0 && !std::getenv("STG_2D_NONPERSIST")) {
     static int occ_dev[kMaxDevices];
@@ -1668,33 +1654,8 @@ bool slab_generic_reduces(const SlabArgs& a) {
          a.n_in >= 2 && a.n_in <= 6 && a.g.n1 >= 2 && a.g.n1 <= 6 && !std::getenv("STG_1D_V1");
 }
 
-bool slab_em_supported(const SlabArgs& a) {
-  if (a.g.dim != 2 || a.model != int(Model::advection) || a.n_in != a.n_out || kPlaneEnv != 32 ||
-      std::getenv("STG_GENERIC_2D"))
-    return false;
-  auto by_nt = [&](auto n1_tag) -> bool {
-    constexpr int N1 = decltype(n1_tag)::value;
-    switch (a.n_in) {
-      case 2: return plane2d_ok<N1, 2, 32>(a);
-      case 3: return plane2d_ok<N1, 3, 32>(a);
-      case 4: return plane2d_ok<N1, 4, 32>(a);
-      case 5: return plane2d_ok<N1, 5, 32>(a);
-      case 6: return plane2d_ok<N1, 6, 32>(a);
-      default: return false;
-    }
-  };
-  switch (a.g.n1) {
-    case 2: return by_nt(std::integral_constant<int, 2>{});
-    case 3: return by_nt(std::integral_constant<int, 3>{});
-    case 4: return by_nt(std::integral_constant<int, 4>{});
-    case 5: return by_nt(std::integral_constant<int, 5>{});
-    default: return false;
-  }
-}
-
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
   const int d = a.g.dim, n1 = a.g.n1;
-  if (a.em && !slab_em_supported(a)) return -1;
   if (d == 1) {
     switch (n1) {
       case 2: return launch1d<2>(a, s);

@@ -15,6 +15,8 @@ from paper_2201_05800_b200.api import SlabOperator  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 pc = int(sys.argv[2]) if len(sys.argv) > 2 else L.STG_PRECOND_EBLOCK
 cfg = C.CONFIGS[name]
+if len(sys.argv) > 3:  # another mesh with the config's physics, e.g. 32x24x37
+    cfg = cfg.scaled(tuple(int(c) for c in sys.argv[3].split("x")))
 op = SlabOperator(**cfg.kwargs())
 X = [torch.as_tensor(C.random_slab(cfg, k), device="cuda") for k in range(3)]
 Y = [torch.empty_like(x) for x in X]
@@ -41,5 +43,6 @@ for _ in range(5):
     e1.record()
     torch.cuda.synchronize()
     best = min(best, e0.elapsed_time(e1) / reps)
-print(json.dumps({"config": name, "precond": pc, "us_per_apply": 1e3 * best,
+print(json.dumps({"config": cfg.name, "precond": pc, "us_per_apply": 1e3 * best,
+                  "ns_per_cell": 1e6 * best / cfg.n_cells,
                   "gbs": 16 * cfg.n_dof / (best * 1e-3) / 1e9}))
