@@ -680,13 +680,13 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     op2 = SlabOperator(**c2.kwargs())
     u2 = torch.as_tensor(C.initial_state(c2), device=dev)
     out["c2"] = {"applies": apply_rates(op2, c2, C, torch, dev, 40)}
-    for pname, pc in (("auto_dense_eblock", L.STG_PRECOND_AUTO), ("none", L.STG_PRECOND_NONE)):
+    for pname, pc in (("auto_fdm2_eblock", L.STG_PRECOND_AUTO), ("none", L.STG_PRECOND_NONE)):
         nc2 = NewtonConfig(precond=pc, **kw)
         op2.stdg_step(0.0, c2.dt, u2, nc2)
         t, (_, _, info2) = _best_wall(torch, lambda: op2.stdg_step(0.0, c2.dt, u2, nc2))
         out["c2"][f"slab_solve_{pname}"] = {"seconds": t,
                                             "gmres_iterations": info2.linear_iterations}
-    out["c2"]["slab_solve_s"] = out["c2"]["slab_solve_auto_dense_eblock"]["seconds"]
+    out["c2"]["slab_solve_s"] = out["c2"]["slab_solve_auto_fdm2_eblock"]["seconds"]
     del op2, u2
     # c1: 1000 R(U) applies (launch-latency bound) and the GMRES slab solve at 1e-12
     c1 = C.CONFIGS["c1"]
