@@ -489,8 +489,6 @@ __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
     fdm3_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_out,
                 const FdmCoef3* __restrict__ coef, const __grid_constant__ FdmCoef3 cp,
                 const Geometry g, const Skip skip) {
-  pdl_entry();
-  if (skip_now(skip)) return;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (ptxh::smem_u32(smem_raw) & 1023u)) & 1023u);
   const FdmCoef3& cs = *reinterpret_cast<const FdmCoef3*>(base + f3::OFF_C);
@@ -499,22 +497,38 @@ __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
   const uint32_t bar0 = ptxh::smem_u32(bars), bar1 = ptxh::smem_u32(bars + 1);
   const int tid = threadIdx.x;
   const int nseg = g.n_cells / f3::E;
+  int seg = blockIdx.x;
+  // prologue before the programmatic-dependency wait (it overlaps the
+  // previous kernel's tail): the barriers and the factor block, which no
+  // kernel of the stream writes (uploaded once per mix).  The factors ride
+  // on the first tile's barrier phase (expect_tx without arrival; the tile
+  // issue below arrives).
   if (tid == 0) {
     ptxh::mbar_init(bar0, 1);
     ptxh::mbar_init(bar1, 1);
     ptxh::fence_mbar_init();
+    if (seg < nseg) {
+      ptxh::mbar_expect_tx_only(bar0, f3::COEF);
+      ptxh::bulk_g2s_1d(ptxh::smem_u32(base + f3::OFF_C), coef, f3::COEF, bar0);
+    }
   }
+  pdl_entry();
   __syncthreads();
-  auto issue = [&](int seg, int st, uint32_t extra) {
+  auto issue = [&](int sg, int st) {
     const uint32_t bar = st ? bar1 : bar0;
-    ptxh::mbar_expect_tx(bar, f3::TILE + extra);
-    ptxh::tma_load_4d(ptxh::smem_u32(base + st * f3::TILE), &tm, bar, 0, 0, seg * f3::E, 0);
+    ptxh::mbar_expect_tx(bar, f3::TILE);
+    ptxh::tma_load_4d(ptxh::smem_u32(base + st * f3::TILE), &tm, bar, 0, 0, sg * f3::E, 0);
   };
-  int seg = blockIdx.x;
-  if (tid == 0 && seg < nseg) {  // the factors ride on the first tile's barrier
-    issue(seg, 0, f3::COEF);
-    ptxh::bulk_g2s_1d(ptxh::smem_u32(base + f3::OFF_C), coef, f3::COEF, bar0);
+  if (skip_now(skip)) {
+    // the factor copy is in flight: it must land before the CTA exits
+    if (seg < nseg) {
+      if (tid == 0) ptxh::mbar_arrive(bar0);
+      while (!ptxh::mbar_try_wait(bar0, 0)) {
+      }
+    }
+    return;
   }
+  if (tid == 0 && seg < nseg) issue(seg, 0);
   // phase B unit: q = (iy, j) fastest across the lanes (conflict-free tile
   // reads, one 128-byte wavefront per table read), 4 cells per warp
   const int qB = tid & 7, eB = tid >> 3;
@@ -527,7 +541,7 @@ __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
       // must have read it before the next load overwrites it
       ptxh::bulk_wait_read0();
       ptxh::fence_proxy_async_smem();
-      issue(seg + gridDim.x, st ^ 1, 0);
+      issue(seg + gridDim.x, st ^ 1);
     }
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
@@ -583,8 +597,6 @@ __global__ void __launch_bounds__(f2::Shape<N1, NT, NR, NP>::THREADS)
     fdm2_kernel(const double* __restrict__ in, double* __restrict__ out,
                 const FdmCoef2* __restrict__ coef, const __grid_constant__ FdmCoef2 c,
                 const Geometry g, const Skip skip) {
-  pdl_entry();
-  if (skip_now(skip)) return;
   using S = f2::Shape<N1, NT, NR, NP>;
   constexpr int NPC = S::NPC, KX = S::KX, KM = S::KM, E = f2::E;
   extern __shared__ __align__(128) unsigned char smem2[];
@@ -598,22 +610,37 @@ __global__ void __launch_bounds__(f2::Shape<N1, NT, NR, NP>::THREADS)
   const long long ns = g.n_sdof;
   const int nseg = g.n_cells / E;
   constexpr uint32_t PB = E * NPC * 8;  // bytes of one temporal block of a segment
+  int seg = blockIdx.x;
+  // prologue before the programmatic-dependency wait: the barriers and the
+  // temporal table (uploaded once per mix, no kernel writes it), which rides
+  // on the first segment's barrier phase (expect_tx without arrival)
   if (tid == 0) {
     ptxh::mbar_init(bar0, 1);
     ptxh::mbar_init(bar1, 1);
     ptxh::fence_mbar_init();
+    if (seg < nseg) {
+      ptxh::mbar_expect_tx_only(bar0, S::MBYTES);
+      ptxh::bulk_g2s_1d(ptxh::smem_u32(Ms), coef->M, S::MBYTES, bar0);
+    }
   }
+  pdl_entry();
   __syncthreads();
-  auto issue = [&](int seg, int st, bool with_m) {
+  if (skip_now(skip)) {  // the table copy must land before the CTA exits
+    if (seg < nseg) {
+      if (tid == 0) ptxh::mbar_arrive(bar0);
+      while (!ptxh::mbar_try_wait(bar0, 0)) {
+      }
+    }
+    return;
+  }
+  auto issue = [&](int sg, int st) {
     const uint32_t bar = st ? bar1 : bar0;
-    ptxh::mbar_expect_tx(bar, NT * PB + (with_m ? S::MBYTES : 0));
+    ptxh::mbar_expect_tx(bar, NT * PB);
     const uint32_t dst = ptxh::smem_u32(st0 + st * S::STAGE);
-    const double* src = in + (long long)seg * E * NPC;
+    const double* src = in + (long long)sg * E * NPC;
     for (int t = 0; t < NT; ++t) ptxh::bulk_g2s_1d(dst + t * PB, src + t * ns, PB, bar);
-    if (with_m) ptxh::bulk_g2s_1d(ptxh::smem_u32(Ms), coef->M, S::MBYTES, bar);
   };
-  int seg = blockIdx.x;
-  if (tid == 0 && seg < nseg) issue(seg, 0, true);
+  if (tid == 0 && seg < nseg) issue(seg, 0);
 
   for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
     const int st = it & 1;
@@ -621,7 +648,7 @@ __global__ void __launch_bounds__(f2::Shape<N1, NT, NR, NP>::THREADS)
     if (tid == 0 && seg + (int)gridDim.x < nseg) {
       ptxh::bulk_wait_read0();  // stage st^1's previous result has been stored
       ptxh::fence_proxy_async_smem();
-      issue(seg + gridDim.x, st ^ 1, false);
+      issue(seg + gridDim.x, st ^ 1);
     }
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
