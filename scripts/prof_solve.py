@@ -1,4 +1,5 @@
-"""ncu driver: one warm slab solve inside cudaProfilerStart/Stop."""
+"""ncu driver: one warm slab solve inside cudaProfilerStart/Stop (run ncu with
+--profile-from-start off).  c3 uses its inexact Newton-GMRES config."""
 import sys
 import time
 from pathlib import Path
@@ -13,7 +14,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c4"
 cfg = C.CONFIGS[name]
 op = SlabOperator(**cfg.kwargs())
 un = torch.as_tensor(C.initial_state(cfg), device="cuda")
-nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10)
+nc = (NewtonConfig(abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-6, fd_eps=1e-7) if name == "c3"
+      else NewtonConfig(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10))
 op.stdg_step(0.0, cfg.dt, un, nc)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
