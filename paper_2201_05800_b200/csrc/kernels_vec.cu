@@ -352,8 +352,17 @@ __global__ void __launch_bounds__(kBlock) k_maxabs(const double* __restrict__ x,
     part[blockIdx.x] = r;
   }
   if (is_last_block(counter) && threadIdx.x < 32) {
-    double r = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) r = nan_max(r, __ldcg(part + b));
+    double a[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // 8 loads in flight per lane
+    int b = threadIdx.x;
+    for (; b + 7 * 32 < (int)gridDim.x; b += 8 * 32) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = nan_max(a[q], __ldcg(part + b + q * 32));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (b + q * 32 < (int)gridDim.x) a[q] = nan_max(a[q], __ldcg(part + b + q * 32));
+    double r = nan_max(nan_max(nan_max(a[0], a[1]), nan_max(a[2], a[3])),
+                       nan_max(nan_max(a[4], a[5]), nan_max(a[6], a[7])));
     r = warp_max(r);
     if (threadIdx.x == 0) {
       out[0] = r;
