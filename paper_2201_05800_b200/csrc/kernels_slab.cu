@@ -919,6 +919,174 @@ __global__ void __launch_bounds__(Plane2d<N1, NT, E>::THREADS, MINB)
 }
 
 // ---------------------------------------------------------------------------
+// slab2d_plane3: the plane kernel with a 3-stage ring.  R is written back
+// into the consumed stage and leaves by bulk stores from there (no separate
+// output staging), and u_n rides in a 2-slot ring of its own, so a stage is
+// the n_tau planes: 3 x 32 KB + 2 x 6.4 KB at c2, 2 CTAs per SM.  The load
+// for segment it+2 is issued after the compute of segment it (by then the
+// store of it-1, which last used that stage, has long read it).
+// ---------------------------------------------------------------------------
+template <int N1, int NT, int E>
+struct Plane3 {
+  static constexpr int NPC = N1 * N1;
+  static constexpr int THREADS = E * NT;
+  static constexpr int PLANE = E * NPC;
+  static constexpr int STAGE = NT * PLANE;
+  static constexpr int SMEM = (3 * STAGE + 2 * PLANE) * 8 + 64;
+};
+
+template <int N1, int NT, int E>
+__global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
+    slab2d_plane3(const SlabArgs a) {
+  pdl_entry();
+  if (skip_now(a.skip)) return;
+  using P = Plane3<N1, NT, E>;
+  constexpr int NPC = P::NPC, PL = P::PLANE;
+  auto tp = [](int j, int c) { return j * PL + c * NPC; };
+  constexpr long long CS = NPC;
+  extern __shared__ __align__(16) double sm3[];
+  double* Ws = sm3 + 3 * P::STAGE;  // u_n ring, 2 slots
+  uint64_t* bars = reinterpret_cast<uint64_t*>(Ws + 2 * PL);
+  const int tid = threadIdx.x;
+  const int e = tid % E, t = tid / E;
+  const int nx = a.g.nx, ny = a.g.ny;
+  const long long ns = a.g.n_sdof;
+  const int nseg = a.g.n_cells / E;
+  const uint32_t pbytes = PL * 8;
+  const bool nLx = a.sp.cL[0] != 0.0, nRx = a.sp.cR[0] != 0.0;
+  const bool nLy = a.sp.cL[1] != 0.0, nRy = a.sp.cR[1] != 0.0;
+  double Tr[NT];
+#pragma unroll
+  for (int j = 0; j < NT; ++j) Tr[j] = a.mx.T[t][j];
+  const double tt_ = a.mx.T[t][t], st_ = a.mx.S[t][t];
+  const bool hw = a.has_w != 0;
+  const double ct_ = hw ? a.mx.c[t] : 0.0;
+
+  if (tid == 0) {
+    for (int q = 0; q < 3; ++q) ptx::mbar_init(ptx::smem_u32(bars + q), 1);
+    ptx::fence_mbar_init();
+  }
+  __syncthreads();
+  // segment sg into X stage stg and u_n slot wsl, on the stage's barrier
+  auto issue = [&](int sg, int stg, int wsl) {
+    const uint32_t bar = ptx::smem_u32(bars + stg);
+    ptx::mbar_expect_tx(bar, (NT + (hw ? 1 : 0)) * pbytes);
+    const uint32_t dst = ptx::smem_u32(sm3 + stg * P::STAGE);
+    const double* src = a.X + (long long)sg * PL;
+    for (int j = 0; j < NT; ++j) bulk_g2s(dst + j * pbytes, src + j * ns, pbytes, bar);
+    if (hw) bulk_g2s(ptx::smem_u32(Ws + wsl * PL), a.W + (long long)sg * PL, pbytes, bar);
+  };
+  auto faces = [&](int sg, double* xl, double* xr, double* yl, double* yr) {
+    const int cell = sg * E + e;
+    const int cx = cell % nx, cy = (cell / nx) % ny;
+    const double* Xt = a.X + t * ns;
+    if (nLx && !(e > 0 && cx > 0)) {
+      const double* q = Xt + (long long)(cell - cx + (cx == 0 ? nx - 1 : cx - 1)) * CS + N1 - 1;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xl[k] = q[k * N1];
+    }
+    if (nRx && !(e < E - 1 && cx < nx - 1)) {
+      const double* q = Xt + (long long)(cell - cx + (cx == nx - 1 ? 0 : cx + 1)) * CS;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xr[k] = q[k * N1];
+    }
+    if (nLy) {
+      const double* q = Xt + (long long)(cell + ((cy == 0 ? ny - 1 : cy - 1) - cy) * nx) * CS +
+                        (N1 - 1) * N1;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) yl[k] = q[k];
+    }
+    if (nRy) {
+      const double* q = Xt + (long long)(cell + ((cy == ny - 1 ? 0 : cy + 1) - cy) * nx) * CS;
+#pragma unroll
+      for (int k = 0; k < N1; ++k) yr[k] = q[k];
+    }
+  };
+
+  int seg = blockIdx.x;
+  if (tid == 0) {
+    if (seg < nseg) issue(seg, 0, 0);
+    if (seg + (int)gridDim.x < nseg) issue(seg + gridDim.x, 1, 1);
+  }
+  double xl[N1], xr[N1], yl[N1], yr[N1];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) xl[k] = xr[k] = yl[k] = yr[k] = 0.0;
+  if (seg < nseg) faces(seg, xl, xr, yl, yr);
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int stg = it % 3;
+    const int nxt = seg + gridDim.x;
+    double* X = sm3 + stg * P::STAGE;
+    while (!ptx::mbar_try_wait(ptx::smem_u32(bars + stg), (it / 3) & 1)) {
+    }
+    const int cell = seg * E + e;
+    const int cx = cell % nx;
+    const double* own = X + tp(t, e);
+    double u[NPC];
+#pragma unroll
+    for (int k = 0; k < NPC; ++k) u[k] = own[k];
+    if (nLx && e > 0 && cx > 0) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xl[k] = own[-CS + k * N1 + N1 - 1];
+    }
+    if (nRx && e < E - 1 && cx < nx - 1) {
+#pragma unroll
+      for (int k = 0; k < N1; ++k) xr[k] = own[CS + k * N1];
+    }
+    double r[NPC];
+#pragma unroll
+    for (int iy = 0; iy < N1; ++iy)
+#pragma unroll
+      for (int ix = 0; ix < N1; ++ix) {
+        double g = 0.0;
+#pragma unroll
+        for (int k = 0; k < N1; ++k) g = fma(a.sp.V[0][ix][k], u[iy * N1 + k], g);
+#pragma unroll
+        for (int k = 0; k < N1; ++k) g = fma(a.sp.V[1][iy][k], u[k * N1 + ix], g);
+        if (ix == 0) g = fma(a.sp.cL[0], xl[iy], g);
+        if (ix == N1 - 1) g = fma(a.sp.cR[0], xr[iy], g);
+        if (iy == 0) g = fma(a.sp.cL[1], yl[ix], g);
+        if (iy == N1 - 1) g = fma(a.sp.cR[1], yr[ix], g);
+        r[iy * N1 + ix] = fma(st_, g, tt_ * u[iy * N1 + ix]);
+      }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      if (j == t) continue;
+      const double* pj = X + tp(j, e);
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) r[k] = fma(Tr[j], pj[k], r[k]);
+    }
+    if (hw && ct_ != 0.0) {
+      const double* pw = Ws + (it & 1) * PL + e * NPC;
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) r[k] = fma(ct_, pw[k], r[k]);
+    }
+    // next segment's out-of-tile traces
+    if (nxt < nseg) faces(nxt, xl, xr, yl, yr);
+    __syncthreads();  // every thread has read stage stg and u_n slot it & 1
+    if (tid == 0 && nxt + (int)gridDim.x < nseg) {
+      // stage (it+2)%3 last held segment it-1, stored at the end of the
+      // previous iteration: its bulk store must have read it; u_n slot it&1
+      // was read by this iteration (barrier above)
+      bulk_wait_read0();
+      ptx::fence_proxy_async_smem();
+      issue(nxt + gridDim.x, (it + 2) % 3, it & 1);
+    }
+    double* outp = X + tp(t, e);
+#pragma unroll
+    for (int k = 0; k < NPC; ++k) outp[k] = r[k];
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < NT; ++j)
+        bulk_s2g(a.R + j * ns + (long long)seg * PL, ptx::smem_u32(X + j * PL), pbytes);
+      bulk_commit();
+    }
+  }
+  if (tid == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------
 // d = 3, N = 3, n_tau = 4: TMA-staged, register-tiled two-phase kernel
 // ---------------------------------------------------------------------------
 namespace fast {
@@ -1547,6 +1715,33 @@ bool plane2d_ok(const SlabArgs& a) {
          P::SMEM <= 227 * 1024 && !std::getenv("STG_2D_V1");
 }
 
+template <int N1, int NT, int E>
+bool plane3_ok(const SlabArgs& a) {
+  return !a.full_s && a.n_in == NT && a.n_out == NT && a.g.n_cells % E == 0 &&
+         (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
+         (reinterpret_cast<uintptr_t>(a.R) & 15) == 0 && a.g.n_sdof % 2 == 0 &&
+         Plane3<N1, NT, E>::SMEM <= 113 * 1024;
+}
+
+template <int N1, int NT, int E>
+int launch_plane3(const SlabArgs& a, cudaStream_t s) {
+  using Q = Plane3<N1, NT, E>;
+  static int occ_dev[kMaxDevices];
+  int& occ = occ_dev[device_slot()];
+  if (occ <= 0) {
+    cudaFuncSetAttribute(slab2d_plane3<N1, NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Q::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane3<N1, NT, E>, Q::THREADS,
+                                                  Q::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  const int nseg = a.g.n_cells / E;
+  int grid = occ * num_sms_cached();
+  if (grid > nseg) grid = nseg;
+  launch_ex(kPdlSlab, slab2d_plane3<N1, NT, E>, grid, Q::THREADS, Q::SMEM, s, a);
+  return 1;
+}
+
 template <int N1, int NT, int E, int MINB>
 int launch_plane2d(const SlabArgs& a, cudaStream_t s) {
   using Q = Plane2d<N1, NT, E>;
@@ -1575,6 +1770,10 @@ int launch2d_t(const SlabArgs& a, cudaStream_t s) {
     if (kPlaneEnv == 33 && plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 1>(a, s);
     // 2 CTAs/SM: caps the tile kernel at 200 registers (202 would round to
     // 6656 per warp and leave room for one 160-thread CTA only)
+    // default: the 3-stage in-place plane kernel (c2 R(U) 31.9 -> 29.6 us);
+    // STG_2D_PLANE2=1 keeps the 2-stage kernel with its output staging
+    static const bool p2 = std::getenv("STG_2D_PLANE2") != nullptr;
+    if (!p2 && kPlaneEnv == 32 && plane3_ok<N1, NT, 32>(a)) return launch_plane3<N1, NT, 32>(a, s);
     if (plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 2>(a, s);
   }
   if (a.g.n_cells % Sh::E == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
