@@ -184,3 +184,29 @@ def test_nonconvergence_returns_last_iterate():
     with pytest.raises(NonconvergenceError) as eh:
         op.stdg_step_host(0.0, cfg.dt, un, nc)
     assert np.array_equal(eh.value.last_iterate, last)
+
+
+def test_large_1d_mesh_newton_residual_norm():
+    """The d = 1 lane kernel reduces max |R| and <R,R> for Newton's residual in
+    the same launch, one partial per block.  Above ~6M cells at n_tau = 4 its
+    grid exceeds the partial-sum slots, so those meshes must take the plain
+    kernel plus a reduction pass (the reducing instance used to
+    overrun its buffer there).  8M cells: the residual norm Newton reports
+    equals max |R(1 (x) u_n)| computed by a separate apply."""
+    from paper_2201_05800_b200.api import NonconvergenceError
+    K = 8 * 1024 * 1024
+    op = SlabOperator(1, 3, 4, (K,), (0.0,), (1.0,), (1.0,))
+    x = torch.linspace(0.0, 1.0, op.n_sdof, dtype=torch.float64, device="cuda")
+    un = torch.sin(2 * np.pi * x)
+    with pytest.raises(NonconvergenceError) as e:
+        op.stdg_step(0.0, 1e-4, un, NewtonConfig(max_iter=0))
+    R = op.st_residual(0.0, 1e-4, un, un.repeat(4))
+    assert e.value.residual_history[0] == R.abs().max().item()
+    # a mesh whose grid still fits keeps the fused reduction: same contract
+    op2 = SlabOperator(1, 3, 4, (1 << 20,), (0.0,), (1.0,), (1.0,))
+    u2 = torch.sin(2 * np.pi * torch.linspace(0.0, 1.0, op2.n_sdof, dtype=torch.float64,
+                                              device="cuda"))
+    with pytest.raises(NonconvergenceError) as e2:
+        op2.stdg_step(0.0, 1e-4, u2, NewtonConfig(max_iter=0))
+    R2 = op2.st_residual(0.0, 1e-4, u2, u2.repeat(4))
+    assert e2.value.residual_history[0] == R2.abs().max().item()
