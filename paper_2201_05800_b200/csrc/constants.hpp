@@ -7,7 +7,8 @@
 //   lagrange_basis  quadrature.hpp:107-124
 //   diff_matrix     quadrature.hpp:128-144
 //   lobatto_tableau operators.hpp:76-112
-// and tests/test_constants.py checks it is bitwise equal to the oracle's.
+// and tests/test_abi.py (test_constants_bitwise_equal_to_oracle) checks it is
+// bitwise equal to the oracle's.
 #pragma once
 
 #include <cmath>
