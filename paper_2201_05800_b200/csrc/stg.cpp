@@ -956,8 +956,31 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
     return e ? std::atoi(e) : 0;
   }();
   int K = kenv > 0 && kenv <= stg_handle::kChunks ? kenv : stg_handle::kChunks;
-  while (K > 1 && g.nz % K) --K;
+  if (K > g.nz) K = g.nz;
   if (K < 2) return false;
+  // chunk sizes in z-layers: a geometric ramp up and down (1, 2, 4, 8, 8, 4,
+  // 2, 1 relative) so the first H2D before any compute and the last D2H after
+  // it are small; STG_PIPE_UNIFORM=1 uses equal chunks
+  static const bool uniform = std::getenv("STG_PIPE_UNIFORM") != nullptr;
+  int zb[stg_handle::kChunks + 1];
+  {
+    double wsum = 0.0, w[stg_handle::kChunks];
+    for (int k = 0; k < K; ++k) {
+      const int d = std::min(k, K - 1 - k);
+      w[k] = uniform ? 1.0 : double(1 << std::min(d, 3));
+      wsum += w[k];
+    }
+    int acc = 0;
+    double cw = 0.0;
+    zb[0] = 0;
+    for (int k = 0; k < K; ++k) {
+      cw += w[k];
+      int b = k + 1 == K ? g.nz : int(std::lround(g.nz * cw / wsum));
+      b = std::max(b, acc + 1);                // every chunk has a layer
+      b = std::min(b, g.nz - (K - 1 - k));     // and leaves one for each later chunk
+      zb[k + 1] = acc = b;
+    }
+  }
   const long long ns = h->n_sdof, nd = h->n_dof;
   h->host_U.ensure(size_t(nd));
   h->host_R.ensure(size_t(nd));
@@ -983,7 +1006,6 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
       ck(cudaEventCreateWithFlags(&h->ev_c[k], cudaEventDisableTiming), "event");
     }
   }
-  const int L = g.nz / K;                              // z-layers per chunk
   const long long layer = (long long)g.nx * g.ny * g.npc;  // doubles per layer per block
   const int seg_per_layer = g.nx * g.ny / 8;
   const bool needL = h->sp.cL[2] != 0.0, needR = h->sp.cR[2] != 0.0;
@@ -1018,14 +1040,14 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
   stamp(h->s_in);
   if (needL) copy_layers(g.nz - 1, 1);  // periodic z- neighbour of chunk 0
   for (int k = 0; k < K; ++k) {
-    copy_layers(k * L, L);
+    copy_layers(zb[k], zb[k + 1] - zb[k]);
     ck(cudaEventRecord(h->ev_in[k], h->s_in), "event");
     stamp(h->s_in);
   }
   for (int k = 0; k < K; ++k) {
     ck(cudaStreamWaitEvent(h->stream, h->ev_in[needR ? std::min(k + 1, K - 1) : k], 0), "wait");
-    a.seg_begin = k * L * seg_per_layer;
-    a.seg_end = (k + 1) * L * seg_per_layer;
+    a.seg_begin = zb[k] * seg_per_layer;
+    a.seg_end = zb[k + 1] * seg_per_layer;
     if (stg::launch_slab_fast(a, h->stream) < 0)
       throw std::runtime_error("fast kernel launch failed in the pipelined path");
     h->launches++;
@@ -1033,7 +1055,7 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
     ck(cudaEventRecord(h->ev_c[k], h->stream), "event");
     stamp(h->stream);
     ck(cudaStreamWaitEvent(h->s_out, h->ev_c[k], 0), "wait");
-    const long long off = k * L * layer, cnt = L * layer;
+    const long long off = zb[k] * layer, cnt = (zb[k + 1] - zb[k]) * layer;
     if (one_d) {
       for (int t = 0; t < h->nt; ++t)
         ck(cudaMemcpyAsync(R_host + t * ns + off, h->host_R.p + t * ns + off,
