@@ -324,6 +324,30 @@ struct FdmCoef2 {
   double M[kFdm2MaxN * kFdm2MaxN][kFdm2MaxN][kFdm2MaxN][2];
 };
 static_assert(sizeof(FdmCoef2) % 16 == 0, "bulk-copied block");
+// fdm2i_kernel (odd n: 3, 5): the same inverse computed IN PLACE in the
+// input stage.  The y-transform of a real x-mode column is real data, so it
+// keeps one member of each y conjugate pair too: per (t, cell) plane the
+// transformed values take exactly n^2 doubles (NR real x-modes x (NR reals +
+// NP complex) + NP complex x-modes x n complex), no separate complex tile,
+// 3 CTAs/SM, and NR*NR + NR*NP + NP*n temporal solves per cell (13 at n = 5
+// instead of 15).  y-modes are ordered [real (NR), pair members with
+// Im > 0 (NP), their conjugates (NP)].
+struct FdmCoef2i {
+  double FX[kFdm2MaxN][kFdm2MaxN][2];   // kept x rows of Px^-1 ([k][x]; real modes: im 0)
+  double FY[kFdm2MaxN][kFdm2MaxN][2];   // Py^-1 rows in y-mode order ([ky][y])
+  double IY[kFdm2MaxN][kFdm2MaxN][2];   // Py columns in y-mode order ([y][ky])
+  double IYW[kFdm2MaxN][kFdm2MaxN][2];  // real x-mode columns: IY x (1 real / 2 pair) ([y][ky < NR+NP])
+  double IX[kFdm2MaxN][kFdm2MaxN][2];   // kept x columns of Px, x (1 / 2) ([x][k])
+  // [m][it][t]: (T + theta_m S)^-1 in phase-B mode order: real x-modes
+  // (j < NR) x y-modes ky < NR+NP, then complex x-modes x all n y-modes
+  double M[kFdm2MaxN * kFdm2MaxN][kFdm2MaxN][kFdm2MaxN][2];
+};
+static_assert(sizeof(FdmCoef2i) % 16 == 0, "bulk-copied block");
+bool fdm2i_supported(const Geometry& g, int n_tau, int nr, int np);
+int launch_precond_fdm2i(const FdmCoef2i* coef, const FdmCoef2i& host_coef, const Geometry& g,
+                         int n_tau, const double* in, double* out, cudaStream_t s,
+                         Skip skip = {});
+
 // n1 / n_tau / (real, pair) x-mode counts the kernel is instantiated for
 bool fdm2_supported(const Geometry& g, int n_tau, int nr, int np);
 int launch_precond_fdm2(const FdmCoef2* coef, const FdmCoef2& host_coef, const Geometry& g,

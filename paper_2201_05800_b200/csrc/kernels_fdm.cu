@@ -777,6 +777,243 @@ __global__ void __launch_bounds__(f2::Shape<N1, NT, NR, NP>::THREADS)
   if (tid == 0) ptxh::bulk_wait0();
 }
 
+// ---------------------------------------------------------------------------
+// fdm2i_kernel: fdm2 in place (see FdmCoef2i in kernels.hpp).  Plane layout
+// after phase A, per (t, cell): for each real x-mode j < NR: NR real y-mode
+// values then NP complex y-pair values (n doubles); for each complex x-mode:
+// n complex y-mode values (2n doubles).  A thread per (t, cell) plane in
+// phases A / A' (lanes = cells: odd plane stride, conflict-free), one warp per
+// spatial mode in phase B (table reads are broadcasts).
+namespace f2i {
+constexpr int E = 32;
+template <int N1, int NT, int NR, int NP>
+struct Shape {
+  static constexpr int NPC = N1 * N1;
+  static constexpr int KY = NR + NP;                 // stored y-modes of a real x-column
+  static constexpr int NMODE = NR * KY + NP * N1;    // temporal solves per cell
+  static constexpr int THREADS = NT * E;
+  static constexpr int NW = THREADS / 32;
+  static constexpr int STAGE = NT * E * NPC;         // doubles
+  static constexpr int MBYTES = int(sizeof(((FdmCoef2i*)nullptr)->M));
+  static constexpr int OFF_M = 2 * STAGE * 8;
+  static constexpr int OFF_BAR = OFF_M + MBYTES;
+  static constexpr int SMEM = OFF_BAR + 64;
+  static_assert(NR + 2 * NP == N1 && (N1 & 1) && N1 <= kFdm2MaxN && NT <= kFdm2MaxN, "shape");
+  // plane offset of phase-B mode m and whether it is a real value
+  __host__ __device__ static constexpr int off(int m) {
+    return m < NR * KY ? (m / KY) * N1 + ((m % KY) < NR ? (m % KY) : NR + 2 * ((m % KY) - NR))
+                       : NR * N1 + 2 * (m - NR * KY);
+  }
+  __host__ __device__ static constexpr bool real(int m) { return m < NR * KY && (m % KY) < NR; }
+};
+}  // namespace f2i
+
+template <int N1, int NT, int NR, int NP>
+__global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
+    fdm2i_kernel(const double* __restrict__ in, double* __restrict__ out,
+                 const FdmCoef2i* __restrict__ coef, const __grid_constant__ FdmCoef2i c,
+                 const Geometry g, const Skip skip) {
+  using S = f2i::Shape<N1, NT, NR, NP>;
+  constexpr int NPC = S::NPC, KY = S::KY, E = f2i::E;
+  extern __shared__ __align__(128) unsigned char smem2i[];
+  double* st0 = reinterpret_cast<double*>(smem2i);
+  const double2* Ms = reinterpret_cast<const double2*>(smem2i + S::OFF_M);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem2i + S::OFF_BAR);
+  const uint32_t bar0 = ptxh::smem_u32(bars), bar1 = ptxh::smem_u32(bars + 1);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tA = tid / E, eA = tid % E;
+  const long long ns = g.n_sdof;
+  const int nseg = g.n_cells / E;
+  constexpr uint32_t PB = E * NPC * 8;
+  int seg = blockIdx.x;
+  if (tid == 0) {  // before the dependency wait: barriers, the temporal table
+    ptxh::mbar_init(bar0, 1);
+    ptxh::mbar_init(bar1, 1);
+    ptxh::fence_mbar_init();
+    if (seg < nseg) {
+      ptxh::mbar_expect_tx_only(bar0, S::MBYTES);
+      ptxh::bulk_g2s_1d(ptxh::smem_u32(Ms), coef->M, S::MBYTES, bar0);
+    }
+  }
+  pdl_entry();
+  __syncthreads();
+  if (skip_now(skip)) {
+    if (seg < nseg) {
+      if (tid == 0) ptxh::mbar_arrive(bar0);
+      while (!ptxh::mbar_try_wait(bar0, 0)) {
+      }
+    }
+    return;
+  }
+  auto issue = [&](int sg, int st) {
+    const uint32_t bar = st ? bar1 : bar0;
+    ptxh::mbar_expect_tx(bar, NT * PB);
+    const uint32_t dst = ptxh::smem_u32(st0 + st * S::STAGE);
+    const double* src = in + (long long)sg * E * NPC;
+    for (int t = 0; t < NT; ++t) ptxh::bulk_g2s_1d(dst + t * PB, src + t * ns, PB, bar);
+  };
+  if (tid == 0 && seg < nseg) issue(seg, 0);
+
+  for (int it = 0; seg < nseg; ++it, seg += gridDim.x) {
+    const int st = it & 1;
+    double* X = st0 + st * S::STAGE;
+    if (tid == 0 && seg + (int)gridDim.x < nseg) {
+      ptxh::bulk_wait_read0();
+      ptxh::fence_proxy_async_smem();
+      issue(seg + gridDim.x, st ^ 1);
+    }
+    while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
+    }
+    double* pl = X + (tA * E + eA) * NPC;
+    // ---- phase A: forward x then y, in place -------------------------------
+    {
+      double u[NPC];
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) u[k] = pl[k];
+      double ar[NR][N1];  // real x-modes, per y
+      C2 ac[NP][N1];      // complex x-modes, per y
+#pragma unroll
+      for (int y = 0; y < N1; ++y) {
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {
+          double a = 0.0;
+#pragma unroll
+          for (int x = 0; x < N1; ++x) a = fma(c.FX[k][x][0], u[y * N1 + x], a);
+          ar[k][y] = a;
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int x = 0; x < N1; ++x) {
+            re = fma(c.FX[NR + p][x][0], u[y * N1 + x], re);
+            im = fma(c.FX[NR + p][x][1], u[y * N1 + x], im);
+          }
+          ac[p][y] = {re, im};
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < NR; ++k) {  // real column: real y-modes, then pair members
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          double a = 0.0;
+#pragma unroll
+          for (int y = 0; y < N1; ++y) a = fma(c.FY[q][y][0], ar[k][y], a);
+          pl[k * N1 + q] = a;
+        }
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          double re = 0.0, im = 0.0;
+#pragma unroll
+          for (int y = 0; y < N1; ++y) {
+            re = fma(c.FY[NR + q][y][0], ar[k][y], re);
+            im = fma(c.FY[NR + q][y][1], ar[k][y], im);
+          }
+          pl[k * N1 + NR + 2 * q] = re;
+          pl[k * N1 + NR + 2 * q + 1] = im;
+        }
+      }
+#pragma unroll
+      for (int p = 0; p < NP; ++p) {  // complex columns: every y-mode
+#pragma unroll
+        for (int ky = 0; ky < N1; ++ky) {
+          C2 b = {0.0, 0.0};
+#pragma unroll
+          for (int y = 0; y < N1; ++y) cmac(b, c.FY[ky][y][0], c.FY[ky][y][1], ac[p][y]);
+          pl[NR * N1 + 2 * (p * N1 + ky)] = b.r;
+          pl[NR * N1 + 2 * (p * N1 + ky) + 1] = b.i;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase B: temporal solves, one warp per mode --------------------------
+#pragma unroll 1
+    for (int m = warp; m < S::NMODE; m += S::NW) {
+      const int o = S::off(m);
+      double* base = X + lane * NPC + o;
+      if (S::real(m)) {
+        double v[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) v[t] = base[t * E * NPC];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) acc = fma(Ms[(m * kFdm2MaxN + q) * kFdm2MaxN + t].x, v[t], acc);
+          base[q * E * NPC] = acc;
+        }
+      } else {
+        C2 v[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) v[t] = {base[t * E * NPC], base[t * E * NPC + 1]};
+#pragma unroll
+        for (int q = 0; q < NT; ++q) {
+          C2 acc = {0.0, 0.0};
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const double2 mm = Ms[(m * kFdm2MaxN + q) * kFdm2MaxN + t];
+            cmac(acc, mm.x, mm.y, v[t]);
+          }
+          base[q * E * NPC] = acc.r;
+          base[q * E * NPC + 1] = acc.i;
+        }
+      }
+    }
+    __syncthreads();
+    // ---- phase A': inverse y then x, in place -------------------------------
+    {
+      double h[NPC];
+#pragma unroll
+      for (int k = 0; k < NPC; ++k) h[k] = pl[k];
+#pragma unroll
+      for (int y = 0; y < N1; ++y) {
+        double mr[NR];
+        C2 mc[NP];
+#pragma unroll
+        for (int k = 0; k < NR; ++k) {  // real column: the value is real
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < NR; ++q) a = fma(c.IYW[y][q][0], h[k * N1 + q], a);
+#pragma unroll
+          for (int q = 0; q < NP; ++q)
+            a = fma(c.IYW[y][NR + q][0], h[k * N1 + NR + 2 * q],
+                    fma(-c.IYW[y][NR + q][1], h[k * N1 + NR + 2 * q + 1], a));
+          mr[k] = a;
+        }
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          C2 b = {0.0, 0.0};
+#pragma unroll
+          for (int ky = 0; ky < N1; ++ky) {
+            const C2 hv = {h[NR * N1 + 2 * (p * N1 + ky)], h[NR * N1 + 2 * (p * N1 + ky) + 1]};
+            cmac(b, c.IY[y][ky][0], c.IY[y][ky][1], hv);
+          }
+          mc[p] = b;
+        }
+#pragma unroll
+        for (int x = 0; x < N1; ++x) {
+          double o = 0.0;
+#pragma unroll
+          for (int k = 0; k < NR; ++k) o = fma(c.IX[x][k][0], mr[k], o);
+#pragma unroll
+          for (int p = 0; p < NP; ++p)
+            o = fma(c.IX[x][NR + p][0], mc[p].r, fma(-c.IX[x][NR + p][1], mc[p].i, o));
+          pl[y * N1 + x] = o;
+        }
+      }
+    }
+    ptxh::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t src = ptxh::smem_u32(X);
+      double* dst = out + (long long)seg * E * NPC;
+      for (int t = 0; t < NT; ++t) ptxh::bulk_s2g_1d(dst + t * ns, src + t * PB, PB);
+      ptxh::bulk_commit();
+    }
+  }
+  if (tid == 0) ptxh::bulk_wait0();
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                               const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                               const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -933,6 +1170,48 @@ int launch_precond_fdm2(const FdmCoef2* coef, const FdmCoef2& hc, const Geometry
   if (g.n1 == 5) return launch_fdm2_t<5, 5, 1, 2>(coef, hc, g, in, out, s, skip);
   if (g.n1 == 4) return launch_fdm2_t<4, 4, 0, 2>(coef, hc, g, in, out, s, skip);
   return launch_fdm2_t<3, 3, 1, 1>(coef, hc, g, in, out, s, skip);
+}
+
+bool fdm2i_supported(const Geometry& g, int n_tau, int nr, int np) {
+  if (g.dim != 2 || g.n_cells % f2i::E != 0 || (g.n_sdof * 8) % 16 != 0 ||
+      std::getenv("STG_NO_FDM2") || std::getenv("STG_NO_FDM2I"))
+    return false;
+  return (g.n1 == 5 && n_tau == 5 && nr == 1 && np == 2) ||
+         (g.n1 == 3 && n_tau == 3 && nr == 1 && np == 1);
+}
+
+namespace {
+template <int N1, int NT, int NR, int NP>
+int launch_fdm2i_t(const FdmCoef2i* coef, const FdmCoef2i& hc, const Geometry& g,
+                   const double* in, double* out, cudaStream_t s, Skip skip) {
+  using S = f2i::Shape<N1, NT, NR, NP>;
+  static int occ_dev[kMaxDevices];
+  const int dev = device_slot();
+  int& occ = occ_dev[dev];
+  if (occ <= 0) {
+    cudaFuncSetAttribute(fdm2i_kernel<N1, NT, NR, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fdm2i_kernel<N1, NT, NR, NP>, S::THREADS,
+                                                  S::SMEM);
+    if (occ < 1) occ = 1;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int nseg = g.n_cells / f2i::E;
+  int grid = occ * sms;
+  if (grid > nseg) grid = nseg;
+  launch_ex(kPdlFdm, fdm2i_kernel<N1, NT, NR, NP>, grid, S::THREADS, S::SMEM, s, in, out, coef,
+            hc, g, skip);
+  return 1;
+}
+}  // namespace
+
+int launch_precond_fdm2i(const FdmCoef2i* coef, const FdmCoef2i& hc, const Geometry& g, int n_tau,
+                         const double* in, double* out, cudaStream_t s, Skip skip) {
+  if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return -1;
+  if (g.n1 == 5 && n_tau == 5) return launch_fdm2i_t<5, 5, 1, 2>(coef, hc, g, in, out, s, skip);
+  if (g.n1 == 3 && n_tau == 3) return launch_fdm2i_t<3, 3, 1, 1>(coef, hc, g, in, out, s, skip);
+  return -1;
 }
 
 }  // namespace stg

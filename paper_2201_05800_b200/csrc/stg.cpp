@@ -126,6 +126,10 @@ struct stg_handle {
   stg::MixCoef fdm2_mix{};
   bool fdm2_valid = false;
   int fdm2_nr = 0, fdm2_np = 0;
+  DevBuf fdm2iM;  // in-place d = 2 FDM (fdm2i_kernel)
+  std::unique_ptr<stg::FdmCoef2i> fdm2i_host;
+  stg::MixCoef fdm2i_mix{};
+  bool fdm2i_valid = false;
   // d = 3 fast-diagonalisation factors and the mix they belong to
   stg::FdmCoef fdm{};
   stg::MixCoef fdm_mix{};
@@ -1313,6 +1317,112 @@ int resolve_precond(const stg_handle* h, int kind) {
   return kind;
 }
 
+// Complex eigen-decomposition V = P diag(th) P^-1 of a real element matrix
+// with the real eigenvalues' eigenvectors made real (phase of the largest
+// entry removed) and the mode order [real, pair members with Im > 0, their
+// conjugates]: ord[i] indexes th / the columns of P.  False when the
+// factorisation does not reproduce V to 1e-11.
+bool eig_ordered(const double (&Vm)[stg::kMaxN][stg::kMaxN], int n, std::vector<stg::cplx>& th,
+                 std::vector<stg::cplx>& P, std::vector<stg::cplx>& Pi, std::vector<int>& ord,
+                 int& nr, int& np) {
+  using stg::cplx;
+  std::vector<double> V(size_t(n) * n);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < n; ++k) V[size_t(i) * n + k] = Vm[i][k];
+  if (!stg::eig_real(V, n, th, P, Pi)) return false;
+  ord.clear();
+  nr = np = 0;
+  for (int k = 0; k < n; ++k)
+    if (th[size_t(k)].imag() == 0.0) {
+      cplx big = 0.0;
+      for (int r = 0; r < n; ++r)
+        if (std::abs(P[size_t(r) * n + k]) > std::abs(big)) big = P[size_t(r) * n + k];
+      const cplx ph = std::conj(big) / std::abs(big);
+      for (int r = 0; r < n; ++r)
+        P[size_t(r) * n + k] = cplx((P[size_t(r) * n + k] * ph).real(), 0.0);
+      ord.push_back(k);
+      ++nr;
+    }
+  std::vector<int> conj_of;
+  for (int k = 0; k < n; ++k)
+    if (th[size_t(k)].imag() > 0.0) {
+      ord.push_back(k);
+      ++np;
+      int best = -1;
+      for (int q = 0; q < n; ++q)
+        if (q != k && th[size_t(q)] == std::conj(th[size_t(k)])) best = q;
+      if (best < 0) return false;
+      conj_of.push_back(best);
+    }
+  for (int q : conj_of) ord.push_back(q);
+  if (nr + 2 * np != n || int(ord.size()) != n) return false;
+  if (!stg::cinverse(P, Pi, n)) return false;
+  double err = 0.0, mxv = 0.0;
+  for (int r = 0; r < n; ++r)
+    for (int q = 0; q < n; ++q) {
+      cplx acc = 0.0;
+      for (int k = 0; k < n; ++k) acc += P[size_t(r) * n + k] * th[size_t(k)] * Pi[size_t(k) * n + q];
+      err = std::max(err, std::abs(acc - Vm[r][q]));
+      mxv = std::max(mxv, std::abs(Vm[r][q]));
+    }
+  return err <= 1e-11 * std::max(mxv, 1e-300);
+}
+
+// Factors of fdm2i_kernel (kernels_fdm.cu, FdmCoef2i in kernels.hpp).
+bool build_fdm2i(const stg::SpatialCoef& sp, const stg::MixCoef& mx, int n, int nt,
+                 stg::FdmCoef2i& c, int& nr, int& np) {
+  using stg::cplx;
+  try {
+    std::vector<cplx> thx, Px, Pix, thy, Py, Piy;
+    std::vector<int> ox, oy;
+    int nry = 0, npy = 0;
+    if (!eig_ordered(sp.V[0], n, thx, Px, Pix, ox, nr, np)) return false;
+    if (!eig_ordered(sp.V[1], n, thy, Py, Piy, oy, nry, npy)) return false;
+    if (nry != nr || npy != np) return false;
+    std::memset(&c, 0, sizeof c);
+    auto put = [](double* dst, cplx z) {
+      dst[0] = z.real();
+      dst[1] = z.imag();
+    };
+    const int kx = nr + np;
+    for (int j = 0; j < kx; ++j)
+      for (int x = 0; x < n; ++x) {
+        cplx f = Pix[size_t(ox[size_t(j)]) * n + x];
+        if (j < nr) f = cplx(f.real(), 0.0);
+        put(c.FX[j][x], f);
+        put(c.IX[x][j], (j < nr ? 1.0 : 2.0) * Px[size_t(x) * n + ox[size_t(j)]]);
+      }
+    for (int q = 0; q < n; ++q)
+      for (int y = 0; y < n; ++y) {
+        cplx f = Piy[size_t(oy[size_t(q)]) * n + y];
+        if (q < nr) f = cplx(f.real(), 0.0);
+        put(c.FY[q][y], f);
+        put(c.IY[y][q], Py[size_t(y) * n + oy[size_t(q)]]);
+        if (q < kx) put(c.IYW[y][q], (q < nr ? 1.0 : 2.0) * Py[size_t(y) * n + oy[size_t(q)]]);
+      }
+    std::vector<cplx> A(size_t(nt) * nt), Ai;
+    int m = 0;
+    auto add_mode = [&](cplx theta) {
+      for (int r = 0; r < nt; ++r)
+        for (int t = 0; t < nt; ++t) A[size_t(r) * nt + t] = mx.T[r][t] + theta * mx.S[r][t];
+      if (!stg::cinverse(A, Ai, nt)) return false;
+      for (int it = 0; it < nt; ++it)
+        for (int t = 0; t < nt; ++t) put(c.M[m][it][t], Ai[size_t(it) * nt + t]);
+      ++m;
+      return true;
+    };
+    for (int j = 0; j < nr; ++j)
+      for (int q = 0; q < kx; ++q)
+        if (!add_mode(thx[size_t(ox[size_t(j)])] + thy[size_t(oy[size_t(q)])])) return false;
+    for (int p = 0; p < np; ++p)
+      for (int ky = 0; ky < n; ++ky)
+        if (!add_mode(thx[size_t(ox[size_t(nr + p)])] + thy[size_t(oy[size_t(ky)])])) return false;
+    return true;
+  } catch (const std::exception&) {
+    return false;
+  }
+}
+
 // d = 2 dense element block (the fallback of the d = 2 FDM: meshes whose cell
 // count is not a multiple of 32, other (n, n_tau)): out = B in for every
 // element, hand-written shared-memory-tiled kernel (kernels_precond.cu)
@@ -1540,6 +1650,31 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       stg::precond_tblock(out, in, dt, nt, npc, ns, h->stream, h->skip);
       h->launches++;
     };
+  }
+  if (d == 2 && n1 <= stg::kFdm2MaxN && nt <= stg::kFdm2MaxN) {  // d = 2 FDM, in place
+    bool ok = h->fdm2i_valid && std::memcmp(&h->fdm2i_mix, &mx, sizeof mx) == 0;
+    if (!ok) {
+      auto c = std::make_unique<stg::FdmCoef2i>();
+      int nr = 0, np = 0;
+      if (build_fdm2i(h->sp, mx, n1, nt, *c, nr, np) && stg::fdm2i_supported(h->g, nt, nr, np)) {
+        h->fdm2iM.ensure(sizeof(stg::FdmCoef2i) / sizeof(double));
+        ck(cudaMemcpyAsync(h->fdm2iM.p, c.get(), sizeof(stg::FdmCoef2i), cudaMemcpyHostToDevice,
+                           h->stream), "H2D");
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        h->fdm2i_host = std::move(c);
+        h->fdm2i_mix = mx;
+        h->fdm2i_valid = ok = true;
+      }
+    }
+    if (ok) {
+      const stg::FdmCoef2i* c = reinterpret_cast<const stg::FdmCoef2i*>(h->fdm2iM.p);
+      const stg::FdmCoef2i* hc = h->fdm2i_host.get();
+      return [h, c, hc, nt](const double* in, double* out) {
+        if (stg::launch_precond_fdm2i(c, *hc, h->g, nt, in, out, h->stream, h->skip) < 0)
+          throw std::runtime_error("element-block preconditioner launch failed");
+        h->launches++;
+      };
+    }
   }
   if (d == 2 && n1 <= stg::kFdm2MaxN && nt <= stg::kFdm2MaxN) {  // d = 2 FDM
     bool ok = h->fdm2_valid && std::memcmp(&h->fdm2_mix, &mx, sizeof mx) == 0;

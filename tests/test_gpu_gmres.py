@@ -105,11 +105,13 @@ def test_forced_reorthogonalisation_same_solutions(base, tmp_path_factory):
         assert rel(other[k], base[k]) <= TOL_SOLVE, k
 
 
-def test_fdm2_solve_matches_dense_element_block(base, tmp_path_factory):
-    # d = 2: the element-block inverse by fast diagonalisation (fdm2_kernel)
-    # and by the dense block (k_eblock_dense) are the same operator, so the
-    # solves agree and take the same number of GMRES iterations
-    other = run(tmp_path_factory, STG_NO_FDM2="1")
+@pytest.mark.parametrize("knob", ["STG_NO_FDM2", "STG_NO_FDM2I"])
+def test_fdm2_solve_matches_dense_element_block(base, tmp_path_factory, knob):
+    # d = 2: the element-block inverse by in-place fast diagonalisation
+    # (fdm2i_kernel, default), by the tiled one (fdm2_kernel, STG_NO_FDM2I)
+    # and by the dense block (k_eblock_dense, STG_NO_FDM2) are the same
+    # operator, so the solves agree and take the same number of iterations
+    other = run(tmp_path_factory, **{knob: "1"})
     for k in ["c2", "c2rk"]:
         assert rel(other[k], base[k]) <= TOL_SOLVE, k
     assert base["c2_its"][1] == other["c2_its"][1]

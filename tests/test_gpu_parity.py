@@ -459,17 +459,21 @@ def test_full_c3_residual_parity():
 
 @pytest.mark.parametrize("cells,velocity,degree", [
     ((4, 3), (1.0, -0.5), 4),      # 12 cells: the dense block (kernels_precond.cu)
-    ((8, 4), (1.0, -0.5), 4),      # 32 cells: fdm2_kernel <5, 5, 1, 2>
+    ((8, 4), (1.0, -0.5), 4),      # 32 cells: fdm2i_kernel <5, 5, 1, 2> (in place)
     ((16, 4), (-0.8, 0.3), 4),
     ((8, 8), (1.0, 0.5), 4),
     ((8, 4), (0.0, 0.7), 4),       # b_x = 0: V_x has no FDM form -> dense block
     ((8, 4), (0.6, -1.1), 3),      # n = 4, n_tau = 4: fdm2_kernel <4, 4, 0, 2>
-    ((16, 2), (1.0, 1.0), 2),      # n = 3, n_tau = 3: fdm2_kernel <3, 3, 1, 1>
+    ((16, 2), (1.0, 1.0), 2),      # n = 3, n_tau = 3: fdm2i_kernel <3, 3, 1, 1>
 ])
-def test_2d_element_block_is_exact_local_inverse(cells, velocity, degree):
+@pytest.mark.parametrize("variant", ["default", "STG_NO_FDM2I"])
+def test_2d_element_block_is_exact_local_inverse(cells, velocity, degree, variant, monkeypatch):
     """d = 2 EBLOCK (fast diagonalisation, kernels_fdm.cu fdm2_kernel, or the
     shared dense block) = the exact inverse of the element-local block read
-    off the oracle's J.v."""
+    off the oracle's J.v.  STG_NO_FDM2I selects the tiled fdm2_kernel (read
+    at each preconditioner build)."""
+    if variant != "default":
+        monkeypatch.setenv(variant, "1")
     cfg = make(2, degree, degree + 1, cells, velocity, dt=0.003)
     op, pr = pair(cfg)
     ns, npc, nt = op.n_sdof, (degree + 1) ** 2, degree + 1
