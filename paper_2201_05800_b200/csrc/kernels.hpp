@@ -292,12 +292,18 @@ int launch_precond_fdm(const FdmCoef& c, const Geometry& g, const double* in, do
 // memory, [iz][it][t][q] with q = iy * 2 + j fastest (M).
 // One device block, copied to shared memory by one bulk copy per CTA:
 // the spatial factors (complex [re, im]) followed by the temporal table.
+// Every axis has two complex-conjugate eigenvalue pairs (2P, 2P + 1), whose
+// eigenvector columns (rows of P^-1) are exact conjugates, so one member of a
+// pair carries the pair: with a row p + iq of P^-1, the coefficients of the
+// pair members of a complex vector u are (p.Re u - q.Im u) + i(p.Im u + q.Re u)
+// and (p.Re u + q.Im u) + i(p.Im u - q.Re u), four real dots and four adds
+// instead of two complex dots; the inverse side likewise.
 struct FdmCoef3 {
   double FX[2][4][2];  // rows 0, 2 of Px^-1 (one of each conjugate pair)
-  double FY[4][4][2];  // Py^-1
-  double FZ[4][4][2];  // Pz^-1
-  double IZ[4][4][2];  // Pz
-  double IY[4][4][2];  // Py
+  double FY[2][4][2];  // rows 0, 2 of Py^-1 ([P][y] = p + iq of row 2P)
+  double FZ[2][4][2];  // rows 0, 2 of Pz^-1
+  double IZ[4][2][2];  // columns 0, 2 of Pz ([z][P])
+  double IY[4][2][2];  // columns 0, 2 of Py
   double IX[4][2][2];  // 2 x columns 0, 2 of Px (the factor 2 of 2 Re(.) folded in)
   double M[4][4][4][8][2];  // [iz][it][t][q]: (T + theta S)^-1, q = iy * 2 + j
 };

@@ -296,8 +296,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // ---------------------------------------------------------------------------
 // fdm3_kernel: the same element-block inverse with the temporal direction
 // solved directly per spatial mode, M_theta = (T + theta S)^-1 (4 x 4
-// complex), instead of Q^-1 S^-1, 1/Lambda and Q: 12.3k FMA per cell instead
-// of 15k.  16 cells per segment and one thread per (cell, iy, j) unit in
+// complex), instead of Q^-1 S^-1, 1/Lambda and Q, and the y / z transforms
+// by conjugate pairs: 9.2k FP64 ops per cell (12.3k with plain complex y / z
+// transforms, 15k with the eigen-decomposed t direction).  16 cells per segment and one thread per (cell, iy, j) unit in
 // phase B, so every phase is one pass over the tile: three CTA barriers per
 // 16 cells (the two-half phase B above needs six per 8).  The complex tile
 // lives in place of the real one (a (t, z) row of 16 reals becomes 8 complex
@@ -334,6 +335,34 @@ __device__ __forceinline__ void mac(C2& acc, const C2& a, const C2& b) {
 }
 }  // namespace f3
 
+// The y and z transforms run on complex data by conjugate pairs (FdmCoef3):
+// fwd_pair returns the pair members' coefficients of the complex 4-vector
+// (ur, ui) from the member row (p + iq): 16 FMA + 4 adds for two modes
+// instead of 32 FMA.
+namespace f3 {
+template <bool PARAM>
+__device__ __forceinline__ void fwd_pair(const double (&row)[4][2], const double (&ur)[4],
+                                         const double (&ui)[4], C2& m0, C2& m1) {
+  double A = 0.0, B = 0.0, Cc = 0.0, D = 0.0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const C2 f = cf<PARAM>(row[k]);
+    A = fma(f.r, ur[k], A);
+    B = fma(f.i, ur[k], B);
+    Cc = fma(f.r, ui[k], Cc);
+    D = fma(f.i, ui[k], D);
+  }
+  m0 = {A - D, Cc + B};
+  m1 = {A + D, Cc - B};
+}
+// the inverse side: out += (pc + i qc) m0 + (pc - i qc) m1 = pc s + i qc d,
+// s = m0 + m1, d = m0 - m1 (formed once per pair by the caller)
+__device__ __forceinline__ void inv_pair(const C2& col, const C2& s, const C2& d, C2& out) {
+  out.r = fma(col.r, s.r, fma(-col.i, d.i, out.r));
+  out.i = fma(col.r, s.i, fma(col.i, d.r, out.i));
+}
+}  // namespace f3
+
 // phase A on one (t, cell, z) row: forward x (kept modes j) and y, in place
 template <bool PARAM>
 __device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int row) {
@@ -345,7 +374,7 @@ __device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int r
     r[2 * q] = v.x;
     r[2 * q + 1] = v.y;
   }
-  C2 a[4][2];
+  double ar[2][4], ai[2][4];  // [j][y]: x-mode j of line y
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     C2 fx[4];
@@ -359,51 +388,48 @@ __device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int r
         re = fma(fx[x].r, r[4 * y + x], re);
         im = fma(fx[x].i, r[4 * y + x], im);
       }
-      a[y][j] = {re, im};
+      ar[j][y] = re;
+      ai[j][y] = im;
     }
   }
 #pragma unroll
-  for (int iy = 0; iy < 4; ++iy) {
-    C2 fy[4];
-#pragma unroll
-    for (int y = 0; y < 4; ++y) fy[y] = f3::cf<PARAM>(c.FY[iy][y]);
+  for (int pr = 0; pr < 2; ++pr)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      C2 b = {0.0, 0.0};
-#pragma unroll
-      for (int y = 0; y < 4; ++y) f3::mac(b, fy[y], a[y][j]);
-      *reinterpret_cast<double2*>(X + row * 16 + (((iy * 2 + j) ^ sw) << 1)) =
-          make_double2(b.r, b.i);
+      C2 m0, m1;
+      f3::fwd_pair<PARAM>(c.FY[pr], ar[j], ai[j], m0, m1);
+      *reinterpret_cast<double2*>(X + row * 16 + ((((2 * pr) * 2 + j) ^ sw) << 1)) =
+          make_double2(m0.r, m0.i);
+      *reinterpret_cast<double2*>(X + row * 16 + ((((2 * pr + 1) * 2 + j) ^ sw) << 1)) =
+          make_double2(m1.r, m1.i);
     }
-  }
 }
 
 // phase A' on one row: inverse y and x (2 Re, the 2 folded into IX), in place
 template <bool PARAM>
 __device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int row) {
   const int sw = row & 7;
-  C2 h[4][2];
+  C2 s[2][2], d[2][2];  // [P][j]: sum and difference of the pair members
 #pragma unroll
-  for (int iy = 0; iy < 4; ++iy)
+  for (int pr = 0; pr < 2; ++pr)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-      const double2 v =
-          *reinterpret_cast<const double2*>(X + row * 16 + (((iy * 2 + j) ^ sw) << 1));
-      h[iy][j] = {v.x, v.y};
+      const double2 v0 =
+          *reinterpret_cast<const double2*>(X + row * 16 + ((((2 * pr) * 2 + j) ^ sw) << 1));
+      const double2 v1 =
+          *reinterpret_cast<const double2*>(X + row * 16 + ((((2 * pr + 1) * 2 + j) ^ sw) << 1));
+      s[pr][j] = {v0.x + v1.x, v0.y + v1.y};
+      d[pr][j] = {v0.x - v1.x, v0.y - v1.y};
     }
   double o[16];
 #pragma unroll
   for (int y = 0; y < 4; ++y) {
-    C2 iyc[4];
+    C2 m[2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
-    for (int iy = 0; iy < 4; ++iy) iyc[iy] = f3::cf<PARAM>(c.IY[y][iy]);
-    C2 m[2];
+    for (int pr = 0; pr < 2; ++pr) {
+      const C2 col = f3::cf<PARAM>(c.IY[y][pr]);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      C2 sacc = {0.0, 0.0};
-#pragma unroll
-      for (int iy = 0; iy < 4; ++iy) f3::mac(sacc, iyc[iy], h[iy][j]);
-      m[j] = sacc;
+      for (int j = 0; j < 2; ++j) f3::inv_pair(col, s[pr][j], d[pr][j], m[j]);
     }
 #pragma unroll
     for (int x = 0; x < 4; ++x) {
@@ -426,26 +452,19 @@ __device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int r
 template <bool PARAM>
 __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs, double* X, int e,
                                           int q) {
-  C2 v[4][4];  // [t][z] -> [t][iz] -> [it][iz] -> [t][z], in place in registers
+  C2 v[4][4];  // [t][iz] -> [it][iz] -> [t][z], in place in registers
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+  for (int t = 0; t < 4; ++t) {  // loaded and forward z, row by row
+    double ur[4], ui[4];
 #pragma unroll
     for (int z = 0; z < 4; ++z) {
       const double2 d = *f3::at(X, f3::row_of(t, e, z), q);
-      v[t][z] = {d.x, d.y};
+      ur[z] = d.x;
+      ui[z] = d.y;
     }
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {  // forward z, row by row
-    C2 w[4];
-#pragma unroll
-    for (int iz = 0; iz < 4; ++iz) {
-      C2 acc = {0.0, 0.0};
-#pragma unroll
-      for (int z = 0; z < 4; ++z) f3::mac(acc, f3::cf<PARAM>(c.FZ[iz][z]), v[t][z]);
-      w[iz] = acc;
-    }
-#pragma unroll
-    for (int iz = 0; iz < 4; ++iz) v[t][iz] = w[iz];
+    for (int pr = 0; pr < 2; ++pr)
+      f3::fwd_pair<PARAM>(c.FZ[pr], ur, ui, v[t][2 * pr], v[t][2 * pr + 1]);
   }
 #pragma unroll
   for (int iz = 0; iz < 4; ++iz) {  // temporal solve of mode (iz, q), column by column
@@ -462,11 +481,17 @@ __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs,
   }
 #pragma unroll
   for (int t = 0; t < 4; ++t) {  // inverse z, stored
+    C2 s[2], d[2];
+#pragma unroll
+    for (int pr = 0; pr < 2; ++pr) {
+      s[pr] = {v[t][2 * pr].r + v[t][2 * pr + 1].r, v[t][2 * pr].i + v[t][2 * pr + 1].i};
+      d[pr] = {v[t][2 * pr].r - v[t][2 * pr + 1].r, v[t][2 * pr].i - v[t][2 * pr + 1].i};
+    }
 #pragma unroll
     for (int z = 0; z < 4; ++z) {
       C2 acc = {0.0, 0.0};
 #pragma unroll
-      for (int iz = 0; iz < 4; ++iz) f3::mac(acc, f3::cf<PARAM>(c.IZ[z][iz]), v[t][iz]);
+      for (int pr = 0; pr < 2; ++pr) f3::inv_pair(f3::cf<PARAM>(c.IZ[z][pr]), s[pr], d[pr], acc);
       *f3::at(X, f3::row_of(t, e, z), q) = make_double2(acc.r, acc.i);
     }
   }

@@ -1233,20 +1233,28 @@ bool build_fdm3(const stg::SpatialCoef& sp, const stg::MixCoef& mx, stg::FdmCoef
         for (int k = 0; k < n; ++k) V[size_t(i) * n + k] = sp.V[a][i][k];
       if (!stg::eig_real(V, n, th[a], P[a], Pi[a])) return false;
     }
-    for (int j = 0; j < 2; ++j)  // x modes: one member of each conjugate pair (0, 2)
-      if (!(th[0][size_t(2 * j)].imag() > 0.0) ||
-          th[0][size_t(2 * j + 1)] != std::conj(th[0][size_t(2 * j)]))
-        return false;
+    // every axis: two conjugate pairs (2P, 2P + 1) with conjugate eigenvector
+    // columns and P^-1 rows (the kernel forms the partner from the member)
+    for (int a = 0; a < 3; ++a)
+      for (int pr = 0; pr < 2; ++pr) {
+        const size_t m0 = size_t(2 * pr), m1 = m0 + 1;
+        if (!(th[a][m0].imag() > 0.0) || th[a][m1] != std::conj(th[a][m0])) return false;
+        for (int k = 0; k < n; ++k) {
+          if (P[a][size_t(k) * n + m1] != std::conj(P[a][size_t(k) * n + m0])) return false;
+          const cplx d = Pi[a][m1 * n + size_t(k)] - std::conj(Pi[a][m0 * n + size_t(k)]);
+          if (std::abs(d) > 1e-12 * (1.0 + std::abs(Pi[a][m0 * n + size_t(k)]))) return false;
+        }
+      }
     auto put = [](double* dst, cplx z) {
       dst[0] = z.real();
       dst[1] = z.imag();
     };
-    for (int r = 0; r < n; ++r)
+    for (int pr = 0; pr < 2; ++pr)
       for (int q = 0; q < n; ++q) {
-        put(c.FZ[r][q], Pi[2][size_t(r) * n + q]);
-        put(c.IZ[r][q], P[2][size_t(r) * n + q]);
-        put(c.FY[r][q], Pi[1][size_t(r) * n + q]);
-        put(c.IY[r][q], P[1][size_t(r) * n + q]);
+        put(c.FZ[pr][q], Pi[2][size_t(2 * pr) * n + q]);
+        put(c.IZ[q][pr], P[2][size_t(q) * n + 2 * pr]);
+        put(c.FY[pr][q], Pi[1][size_t(2 * pr) * n + q]);
+        put(c.IY[q][pr], P[1][size_t(q) * n + 2 * pr]);
       }
     for (int j = 0; j < 2; ++j)
       for (int x = 0; x < n; ++x) {
