@@ -94,6 +94,13 @@ extern "C" {
  * provided so the device solve can run the reference's own algorithm.
  * Advection only. */
 #define STG_PRECOND_JACOBI 4
+/* Upwind block sweep (d = 1 Burgers, n_tau = 4, degree 1 or 3; the AUTO
+ * choice there): block Gauss-Seidel in +x, the element blocks plus each
+ * element's inflow coupling to its left neighbour, solved exactly around the
+ * periodic ring by a parallel scan (the paper's GMRES + SOR, PAPER.md
+ * 1319-1321, as one exact sweep).  Reduces to element-block Jacobi where the
+ * flow runs in -x. */
+#define STG_PRECOND_SWEEP 5
 
 /* Kernel selection (for tests / benchmarking; AUTO picks the fastest valid). */
 #define STG_KERNEL_AUTO 0

@@ -381,9 +381,19 @@ bool gen_eblock_invert(double* Binv, const double* K, const MixCoef& mx, int nt,
                        int ncells, cudaStream_t s);
 // per-element inverse blocks of the 1-D Burgers slab/stage Jacobian at U,
 // stored in fp32 (a preconditioner; applied in fp64 arithmetic)
-bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s);
+// G (may be null): the upwind-sweep inflow couplings B_e^-1 L_e (fp32)
+bool build_burgers_eblock(float* Binv, float* G, const double* U, const SlabArgs& a,
+                          cudaStream_t s);
 // out_e = B_e in_e with per-element fp32 blocks, nt*n1 <= 16 and even
 bool eblock_f32_supported(int nt, int n1);
+// d = 1 upwind block sweep (kernels_precond.cu: k_eblock2, k_sweep_win): the
+// element blocks B (fp32, build_burgers_eblock) plus the inflow couplings G;
+// work: sweep_work_doubles(nt, ncells, n1) doubles (y = B^-1 in).
+// n_tau = 4, N + 1 in {2, 4}.
+bool sweep_supported(int nt, int n1);
+size_t sweep_work_doubles(int nt, int ncells, int n1);
+void precond_sweep(double* out, const double* in, const float* B, const float* G, double* work,
+                   int nt, int n1, int ncells, long long ns, cudaStream_t s, Skip skip);
 void precond_eblock_f32(double* out, const double* in, const float* B, int nt, int n1,
                         int ncells, long long ns, cudaStream_t s, Skip skip = {});
 

@@ -100,8 +100,17 @@ __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
 // At the end the pivot lane of column col holds row col of the inverse.
 // (One element per warp with shuffled rows took 853 us for the 65,536 c3
 // blocks.)
+//
+// With G != nullptr it also forms the inflow coupling of the upwind sweep
+// (k_sweep_win): G_e = B_e^-1 L_e, where L_e is the block of the
+// Jacobian coupling element e's rows to its left neighbour's outflow trace,
+// nonzero in rows (r, node 0) only: L_e[(r, 0)][j] = S(r, j) l_{e,j},
+// l_{e,j} = (2/h)(1/w_0) dH/du_L (u_{e-1,N}(t_j), u_{e,0}(t_j)) (the LLF
+// flux of the left face, spatial.hpp:20-25 with f = u^2/2).  Stored fp32
+// [e][row][j], NT floats per row.
 template <int N1, int NT>
 __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict__ Binv,
+                                                              float* __restrict__ G,
                                                               const double* __restrict__ U,
                                                               const SlabArgs a) {
   pdl_entry();
@@ -118,7 +127,7 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
   const int cl = ce == 0 ? K - 1 : ce - 1, cr = ce == K - 1 ? 0 : ce + 1;
   const bool act = l < NB;
   const int r = act ? l / N1 : 0, i = act ? l - (l / N1) * N1 : 0;
-  double row[NB], inv[NB];
+  double row[NB], inv[NB], lin[NT];
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     double u[N1];
@@ -126,6 +135,12 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
     for (int k = 0; k < N1; ++k) u[k] = U[j * ns + (long long)ce * N1 + k];
     const double ul = U[j * ns + (long long)cl * N1 + N1 - 1];
     const double ur = U[j * ns + (long long)cr * N1];
+    {  // d/du_L of LLF(ul, u_0) at the left face: the inflow coupling l_{e,j}
+      const double aL = fabs(ul), aR = fabs(u[0]);
+      const double dH = aL >= aR ? 0.5 * ul + 0.5 * (ul >= 0 ? 1.0 : -1.0) * (ul - u[0]) + 0.5 * aL
+                                 : 0.5 * ul + 0.5 * aR;
+      lin[j] = a.sp.sc * a.sp.inv_w0 * dH;
+    }
 #pragma unroll
     for (int q = 0; q < N1; ++q) {
       // d F_i(U_j) / d u_q: own element, neighbour states fixed
@@ -212,6 +227,16 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
     float* M = Binv + (size_t)c * NB * NB + (size_t)my_col * NB;
 #pragma unroll
     for (int q = 0; q < NB; q += 2) *reinterpret_cast<float2*>(M + q) = make_float2(float(inv[q]), float(inv[q + 1]));
+    if (G) {  // row my_col of B_e^-1 L_e
+      float* Gr = G + ((size_t)c * NB + my_col) * NT;
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int r2 = 0; r2 < NT; ++r2) acc = fma(inv[r2 * N1], a.mx.S[r2][j], acc);
+        Gr[j] = float(acc * lin[j]);
+      }
+    }
   }
 }
 
@@ -261,6 +286,119 @@ __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
     for (int q = 0; q < NB; ++q)
       acc = fma(double(bv[q]), __shfl_sync(0xffffffffu, x, (h << 4) + q), acc);
     if (act) out[t * ns + c * n1 + k] = acc;
+  }
+}
+
+// ---- d = 1 upwind block sweep (block Gauss-Seidel in +x, periodic) --------
+// P = blockdiag(B_e) + L: the element blocks plus the inflow coupling of each
+// element to its left neighbour (the Jacobian without its downwind part, an
+// O(jump) term for LLF with u > 0).  P z = r is the recurrence
+//   z_e = y_e - G_e s_{e-1},  y_e = B_e^-1 r_e,  G_e = B_e^-1 L_e,
+//   s_e = (z_e at node N, all temporal nodes) = a_e + C_e s_{e-1},
+//   a_e = y_e at node N, C_e = -G_e rows at node N,
+// around the periodic ring.  The influence of s_{e-m} on s_e is the product
+// C_e ... C_{e-m+1}, which decays geometrically (c3, CFL ~1.5: |C_e| ~ 0.54,
+// the product over 16 elements ~1e-11, over 32 ~1e-23; CFL 6: ~4e-6 over
+// 32), so every element starts the recurrence from s = 0 kSwHalo elements
+// upstream -- the sweep is exact up to that product, in one pass with no
+// global scan:
+//   k_eblock2   : y = B^-1 r (into a work vector);
+//   k_sweep_win : per chunk of kSwCh elements, the chunk and its kSwHalo
+//                 upstream elements' C_e and a_e staged in shared memory;
+//                 each owned element runs the recurrence over its window;
+//                 then z_e = y_e - G_e s_{e-1} (lane per block row).
+// Where the flow runs in -x the inflow coupling vanishes (dH/du_L = 0 without
+// jumps) and the sweep reduces to the element-block Jacobi there.
+constexpr int kSwCh = 256;   // owned elements per CTA (= threads)
+constexpr int kSwHalo = 32;  // upstream window
+
+template <int N1, int NT>
+__global__ void __launch_bounds__(kSwCh) k_sweep_win(double* __restrict__ out,
+                                                     const double* __restrict__ y,
+                                                     const float* __restrict__ G, int ncells,
+                                                     long long ns, Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  constexpr int NB = N1 * NT, NE = kSwCh + kSwHalo;
+  static_assert(NT == 4, "one float4 per coupling row");
+  // C_e and a_e of the window, converted to fp64 once (F2F.F64.F32 issues at
+  // a fraction of the FP64 rate: converting inside the recurrence cost 3x)
+  // element index fastest: the recurrence's lanes read consecutive doubles
+  extern __shared__ double sw_smem[];
+  double(*Cs)[NT][NE] = reinterpret_cast<double(*)[NT][NE]>(sw_smem);  // C_e [r][q][e]
+  double(*As)[NE] = reinterpret_cast<double(*)[NE]>(sw_smem + NE * NT * NT);  // a_e [r][e]
+  double(*Ss)[NT + 1] = reinterpret_cast<double(*)[NT + 1]>(sw_smem + NE * (NT * NT + NT));
+  const int e0 = blockIdx.x * kSwCh;
+  for (int j = threadIdx.x; j < NE; j += kSwCh) {
+    int el = e0 - kSwHalo + j;
+    el = el < 0 ? el + ncells * ((kSwHalo + ncells - 1) / ncells) : el;
+    el = el % ncells;
+    const float* Ge = G + (size_t)el * NB * NT;
+#pragma unroll
+    for (int i = 0; i < NT; ++i) {
+      const float4 c = __ldg(reinterpret_cast<const float4*>(Ge + (i * N1 + N1 - 1) * NT));
+      Cs[i][0][j] = -double(c.x);
+      Cs[i][1][j] = -double(c.y);
+      Cs[i][2][j] = -double(c.z);
+      Cs[i][3][j] = -double(c.w);
+      As[i][j] = y[i * ns + (long long)el * N1 + N1 - 1];
+    }
+  }
+  __syncthreads();
+  {
+    const int i = threadIdx.x;
+    double st[NT] = {};
+#pragma unroll 4
+    for (int k = 0; k < kSwHalo; ++k) {
+      const int j = i + k;
+      double nx[NT];
+#pragma unroll
+      for (int r = 0; r < NT; ++r) {
+        double v = As[r][j];
+#pragma unroll
+        for (int q = 0; q < NT; ++q) v = fma(Cs[r][q][j], st[q], v);
+        nx[r] = v;
+      }
+#pragma unroll
+      for (int r = 0; r < NT; ++r) st[r] = nx[r];
+    }
+#pragma unroll
+    for (int r = 0; r < NT; ++r) Ss[i][r] = st[r];
+  }
+  __syncthreads();
+  // z_e = y_e - G_e s_{e-1}: per temporal node t, thread q of the chunk's
+  // kSwCh * N1 nodes (coalesced); all loads of a batch issued first
+  constexpr int PER = NT * kSwCh * N1 / kSwCh, BATCH = PER / 2;
+#pragma unroll
+  for (int b0 = 0; b0 < PER; b0 += BATCH) {
+    float4 g[BATCH];
+    double yv[BATCH];
+#pragma unroll
+    for (int b = 0; b < BATCH; ++b) {
+      const int q = (b0 + b) * kSwCh + threadIdx.x;  // (t, element, node), node fastest
+      const int t = q / (kSwCh * N1), rem = q - t * (kSwCh * N1);
+      const int il = rem / N1, k = rem - il * N1;
+      const long long c = (long long)e0 + il;
+      const bool act = c < ncells;
+      g[b] = act ? __ldg(reinterpret_cast<const float4*>(G + ((size_t)c * NB + t * N1 + k) * NT))
+                 : make_float4(0.f, 0.f, 0.f, 0.f);
+      yv[b] = act ? y[t * ns + c * N1 + k] : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < BATCH; ++b) {
+      const int q = (b0 + b) * kSwCh + threadIdx.x;
+      const int t = q / (kSwCh * N1), rem = q - t * (kSwCh * N1);
+      const int il = rem / N1, k = rem - il * N1;
+      const long long c = (long long)e0 + il;
+      if (c < ncells) {
+        double z = yv[b];
+        z = fma(-double(g[b].x), Ss[il][0], z);
+        z = fma(-double(g[b].y), Ss[il][1], z);
+        z = fma(-double(g[b].z), Ss[il][2], z);
+        z = fma(-double(g[b].w), Ss[il][3], z);
+        out[t * ns + c * N1 + k] = z;
+      }
+    }
   }
 }
 
@@ -497,13 +635,13 @@ __global__ void __launch_bounds__(128) k_gen_eblock(double* __restrict__ Binv,
 }
 
 template <int N1>
-bool build_nt(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
+bool build_nt(float* Binv, float* G, const double* U, const SlabArgs& a, cudaStream_t s) {
   const long long warps = ((long long)a.g.nx + 1) / 2;  // two elements per warp
   const int blocks = int((warps * 32 + 127) / 128);
   auto go = [&](auto nt_tag) {
     constexpr int NT = decltype(nt_tag)::value;
     if constexpr (N1 * NT <= 16 && (N1 * NT) % 2 == 0) {
-      launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, NT>, blocks, 128, 0, s, Binv, U, a);
+      launch_ex(kPdlPrecond, k_build_burgers_eblock<N1, NT>, blocks, 128, 0, s, Binv, G, U, a);
       return true;
     } else {
       return false;  // the fp32 block apply takes n_tau * (N+1) <= 16, even
@@ -575,16 +713,45 @@ void precond_eblock_f32(double* out, const double* in, const float* B, int nt, i
   }
 }
 
+bool sweep_supported(int nt, int n1) {
+  return nt == 4 && (n1 == 2 || n1 == 4);
+}
+
+size_t sweep_work_doubles(int nt, int ncells, int n1) { return size_t(ncells) * n1 * nt; }
+
+void precond_sweep(double* out, const double* in, const float* B, const float* G, double* work,
+                   int nt, int n1, int ncells, long long ns, cudaStream_t s, Skip skip) {
+  long long g = ((ncells + 1) / 2 + 7) / 8;
+  if (g > 148 * 16) g = 148 * 16;
+  const int nch = (ncells + kSwCh - 1) / kSwCh;
+  auto go = [&](auto n1_tag) {
+    constexpr int N1 = decltype(n1_tag)::value;
+    launch_ex(kPdlPrecond, k_eblock2<N1 * 4>, int(g), 256, 0, s, work, in, B, n1, ncells, ns, skip);
+    constexpr size_t smem = sizeof(double) * ((kSwCh + kSwHalo) * (16 + 4) + kSwCh * 5);
+    static bool set_dev[kMaxDevices];
+    bool& set = set_dev[device_slot()];
+    if (!set) {
+      cudaFuncSetAttribute(k_sweep_win<N1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      set = true;
+    }
+    launch_ex(kPdlPrecond, k_sweep_win<N1, 4>, nch, kSwCh, smem, s, out, work, G, ncells, ns, skip);
+  };
+  if (nt != 4) return;
+  if (n1 == 4) go(std::integral_constant<int, 4>{});
+  else if (n1 == 2) go(std::integral_constant<int, 2>{});
+}
+
 bool eblock_f32_supported(int nt, int n1) {
   const int nb = nt * n1;
   return nb <= 16 && nb % 2 == 0;
 }
 
-bool build_burgers_eblock(float* Binv, const double* U, const SlabArgs& a, cudaStream_t s) {
+bool build_burgers_eblock(float* Binv, float* G, const double* U, const SlabArgs& a,
+                          cudaStream_t s) {
   switch (a.g.n1) {
-    case 2: return build_nt<2>(Binv, U, a, s);
-    case 3: return build_nt<3>(Binv, U, a, s);
-    case 4: return build_nt<4>(Binv, U, a, s);
+    case 2: return build_nt<2>(Binv, G, U, a, s);
+    case 3: return build_nt<3>(Binv, G, U, a, s);
+    case 4: return build_nt<4>(Binv, G, U, a, s);
     default: return false;
   }
 }

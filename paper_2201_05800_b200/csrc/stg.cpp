@@ -114,6 +114,8 @@ struct stg_handle {
   // reused for the rest of it (a lagged preconditioner; STG_PRECOND_REBUILD=1
   // rebuilds every iteration)
   bool eblock_valid = false;
+  bool eblock_sweep = false;  // ... with the sweep's inflow couplings in sweepG
+  DevBuf sweepG, sweepW;      // d = 1 upwind sweep: couplings (fp32), y = B^-1 r
   // d = 2 dense element block: the uploaded inverse and the mix it belongs to
   DevBuf etab;  // d = 1 advection element block (shared), keyed by mix
   stg::MixCoef etab_mix{};
@@ -1307,7 +1309,13 @@ int resolve_precond(const stg_handle* h, int kind) {
         "advdiff model with n_tau * (N+1)^d <= 32 only");
   }
   if (kind == STG_PRECOND_AUTO && h->desc.dim == 1 && h->desc.model == STG_MODEL_BURGERS)
-    return stg::eblock_f32_supported(h->nt, h->n1) ? STG_PRECOND_EBLOCK : STG_PRECOND_NONE;
+    return stg::eblock_f32_supported(h->nt, h->n1)
+               ? (stg::sweep_supported(h->nt, h->n1) ? STG_PRECOND_SWEEP : STG_PRECOND_EBLOCK)
+               : STG_PRECOND_NONE;
+  if (kind == STG_PRECOND_SWEEP &&
+      !(h->desc.dim == 1 && h->desc.model == STG_MODEL_BURGERS &&
+        stg::eblock_f32_supported(h->nt, h->n1) && stg::sweep_supported(h->nt, h->n1)))
+    throw std::invalid_argument("upwind block sweep: d = 1 Burgers, n_tau = 4, degree 1 or 3");
   if (kind == STG_PRECOND_AUTO)
     return (h->desc.dim == 1 || fdm_ok(h) || dense2d_ok(h))
                ? STG_PRECOND_EBLOCK
@@ -1320,7 +1328,7 @@ int resolve_precond(const stg_handle* h, int kind) {
     throw std::invalid_argument("temporal-block Jacobi: advection only");
   if (kind == STG_PRECOND_JACOBI && h->desc.model != STG_MODEL_ADVECTION)
     throw std::invalid_argument("diagonal (Jacobi) preconditioner: advection only");
-  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_JACOBI)
+  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_SWEEP)
     throw std::invalid_argument("unknown preconditioner");
   return kind;
 }
@@ -1807,16 +1815,32 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
     if (!stg::eblock_f32_supported(nt, n1))
       throw std::invalid_argument("element-block Jacobi (Burgers): n_tau * (N+1) <= 16 and even");
     static const bool rebuild = std::getenv("STG_PRECOND_REBUILD") != nullptr;
+    const bool sweep = kind == STG_PRECOND_SWEEP;
     float* fb = reinterpret_cast<float*>(h->ptab.p);
-    if (!h->eblock_valid || rebuild) {
+    if (!h->eblock_valid || rebuild || (sweep && !h->eblock_sweep)) {
       h->ptab_kind = -1;  // ptab now holds Burgers blocks
       h->ptab.ensure((size_t(ncells) * nb * nb + 1) / 2);  // fp32 blocks
       fb = reinterpret_cast<float*>(h->ptab.p);
-      if (!stg::build_burgers_eblock(fb, U, a, h->stream))
+      float* G = nullptr;
+      if (sweep) {
+        h->sweepG.ensure((size_t(ncells) * nb * nt + 1) / 2);
+        G = reinterpret_cast<float*>(h->sweepG.p);
+      }
+      if (!stg::build_burgers_eblock(fb, G, U, a, h->stream))
         throw std::invalid_argument("element-block Jacobi: degree <= 3 for Burgers");
       h->launches++;
       check_launch(h);
       h->eblock_valid = true;
+      h->eblock_sweep = sweep;
+    }
+    if (sweep) {
+      h->sweepW.ensure(stg::sweep_work_doubles(nt, ncells, n1));
+      const float* G = reinterpret_cast<const float*>(h->sweepG.p);
+      double* wk = h->sweepW.p;
+      return [h, fb, G, wk, nt, n1, ncells, ns](const double* in, double* out) {
+        stg::precond_sweep(out, in, fb, G, wk, nt, n1, ncells, ns, h->stream, h->skip);
+        h->launches += 2;
+      };
     }
     return [h, fb, nt, n1, ncells, ns](const double* in, double* out) {
       stg::precond_eblock_f32(out, in, fb, nt, n1, ncells, ns, h->stream, h->skip);

@@ -274,7 +274,7 @@ def test_burgers_newton_vs_oracle():
     ("c4", (8, 8, 8), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK]),
     ("c2", (16, 16), [L.STG_PRECOND_NONE, L.STG_PRECOND_TBLOCK, L.STG_PRECOND_EBLOCK]),
     ("c1", (64,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
-    ("c3", (256,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK]),
+    ("c3", (256,), [L.STG_PRECOND_NONE, L.STG_PRECOND_EBLOCK, L.STG_PRECOND_SWEEP]),
 ])
 def test_preconditioners_same_solution_fewer_iterations(name, cells, pcs):
     cfg = C.CONFIGS[name].scaled(cells)
