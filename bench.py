@@ -39,7 +39,14 @@ UNIT = "DOF/s"
 WORKLOAD = "c4"
 FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only if MEASURED_PEAKS.json is absent)
 NSETS = 3  # rotating input/output sets (each > 126 MB L2 at c2 / c4)
-GATE_CYCLES = 400_000  # ~0.2 ms at 1.9 GHz (torch.cuda._sleep before the timed region)
+def gate_cycles(steps: int) -> int:
+    """Device spin (torch.cuda._sleep cycles, ~2 GHz) queued ahead of a timed
+    region: long enough for the host to enqueue every step of a short burst
+    (~10 us per launch through ctypes, more while the NVML sampler thread
+    holds the GIL) before the first one runs, so the region times the steps
+    and not the host; capped at ~20 ms (longer runs keep the queue full on
+    their own: a launch costs the host a third of the kernel's time)."""
+    return min(max(400_000, int(steps * 45e-6 * 2.0e9)), 40_000_000)
 
 # The bench workloads restated for the reference arm, which must not import
 # or load the product (paper_2201_05800_b200): the same numbers as
@@ -134,7 +141,13 @@ class ClockSampler:
         self.samples = []
         self.marks = {}
         self._stop = threading.Event()
+        self._wake = threading.Event()
         self._t = None
+
+    def sample_now(self):
+        """Wake the sampler for an immediate sample (called once the timed
+        region's first step is running, so a short region gets one)."""
+        self._wake.set()
 
     def mark(self, name: str):
         """Sample index at which a phase starts ("timed", "end")."""
@@ -156,7 +169,8 @@ class ClockSampler:
                 r = get_reasons(h)
                 act = ["Active" if r & b else "Not Active" for b in bits]
                 self.samples.append([str(sm), str(mx), "", "", *act])
-                self._stop.wait(0.005)
+                self._wake.wait(0.005)
+                self._wake.clear()
         finally:
             N.nvmlShutdown()
 
@@ -184,25 +198,29 @@ class ClockSampler:
 
     def __exit__(self, *a):
         self._stop.set()
+        self._wake.set()
         self._t.join(timeout=10)
 
     def summary(self):
-        """Median SM clock and the active event reasons over the samples taken
-        under load: the clock pre-roll, the warm-up and the timed region (the
-        same kernel throughout); `samples_timed` counts those inside the
-        timed region itself."""
+        """Median SM clock over the samples inside the timed region (the
+        sampler is woken once its first step runs; all samples when none
+        landed there) and the event reasons active in any sample (warm-up
+        and timed region, the same kernel); `samples_timed` counts those
+        inside the timed region."""
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"], "samples": 0}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        t0, t1 = self.marks.get("timed", 0), self.marks.get("end", len(self.samples))
+        timed = self.samples[t0:t1] or self.samples
+        sm = [float(s[0]) for s in timed if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4)
                           if len(s) > 4 + i and s[4 + i].lower().startswith("active")})
-        t0, t1 = self.marks.get("timed", 0), self.marks.get("end", len(self.samples))
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
                 "samples": len(self.samples), "samples_timed": max(0, t1 - t0),
-                "window": "clock pre-roll + warm-up + timed region (same kernel)"}
+                "window": "warm-up + timed region (same kernel); one sample forced once the "
+                          "first timed step runs"}
 
 
 def oracle_inputs(name, O):
@@ -318,12 +336,11 @@ def run_ours(args):
 
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev.index) as clk:
-        # clock pre-roll: the same apply for >= preroll_s (0.1 s) before the
-        # warm-up, so the clocks are sampled under this load even when the
-        # timed region itself is shorter than one NVML sample (20 steps =
-        # 0.6 ms).  Kept short: seconds of back-to-back applies engage the
-        # power cap (sw_power_cap, SM ~1.85 GHz, R(U) 29.3 -> 31 us), which a
-        # 20-step burst does not see.
+        # optional pre-roll (--preroll-s, default 0): seconds of back-to-back
+        # applies ahead of the warm-up.  Off by default: a 0.1 s pre-roll left
+        # the next short bursts ~7 % slower (31.1 vs 29.0 us per R(U),
+        # scripts/burst_probe.py) while the SM clock read 1965 MHz, and long
+        # runs engage the power cap (sw_power_cap, ~1.7 GHz) on their own.
         t0 = time.perf_counter()
         i = 0
         while time.perf_counter() - t0 < args.preroll_s:
@@ -339,14 +356,19 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
         clk.mark("timed")
-        # launch-latency gate: a ~0.2 ms device spin queued ahead of ev0 keeps
-        # the GPU busy while the host enqueues the first steps, so the timed
-        # region holds the K steps and not the host's first-launch latency
-        torch.cuda._sleep(GATE_CYCLES)
+        # launch-latency gate: a device spin queued ahead of ev0 keeps the GPU
+        # busy while the host enqueues the steps (gate_cycles), so the timed
+        # region holds the K steps and not the host's launch latency
+        torch.cuda._sleep(gate_cycles(args.steps))
         ev0.record(stream)
+        h0 = time.perf_counter()
         for i in range(args.steps):
             step(i)
+        enqueue_s = time.perf_counter() - h0
         ev1.record(stream)
+        while not ev0.query():  # the first step is running: one clock sample inside
+            pass
+        clk.sample_now()
         torch.cuda.synchronize()
         clk.mark("end")
         if dist:
@@ -435,6 +457,8 @@ def run_ours(args):
                     "output_bitwise_equal_device": e2e_exact,
                     "pageable_dof_per_s": cfg.n_dof / pg_s},
             "gpu_launches": launches,
+            "launch_gate": {"spin_cycles": gate_cycles(args.steps),
+                            "host_enqueue_ms": 1e3 * enqueue_s, "timed_ms": ms},
             "clocks": clk.summary(),
             "extra": extra,
         }
@@ -450,7 +474,7 @@ def timed(fn, stream, torch, reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     fn(0)
     torch.cuda.synchronize()
-    torch.cuda._sleep(GATE_CYCLES)  # launch-latency gate (see run_ours)
+    torch.cuda._sleep(gate_cycles(reps))  # launch-latency gate (see run_ours)
     e0.record(stream)
     for i in range(reps):
         fn(i)
@@ -802,7 +826,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-extra", action="store_true")
-    ap.add_argument("--preroll-s", type=float, default=0.1)
+    ap.add_argument("--preroll-s", type=float, default=0.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
