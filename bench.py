@@ -647,7 +647,8 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     # c4: one Newton step, GMRES(30) to rel tol 1e-10 (||r||_2 <= 1e-10 ||b||_2)
     kw = dict(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10, gmres_restart=30)
     c4 = {}
-    for pname, pc in (("auto_fdm_eblock", L.STG_PRECOND_AUTO), ("none", L.STG_PRECOND_NONE),
+    for pname, pc in (("auto_poly_fdm", L.STG_PRECOND_AUTO),
+                      ("eblock_fdm", L.STG_PRECOND_EBLOCK), ("none", L.STG_PRECOND_NONE),
                       ("jacobi_eigen_default", L.STG_PRECOND_JACOBI),
                       ("tblock", L.STG_PRECOND_TBLOCK)):
         nc = NewtonConfig(precond=pc, **kw)
@@ -659,7 +660,7 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
         if pc == L.STG_PRECOND_AUTO:
             U4 = U4x
     out["c4_slab_solve"] = {"gmres_tol": 1e-10, "by_preconditioner": c4,
-                            "seconds": c4["auto_fdm_eblock"]["seconds"]}
+                            "seconds": c4["auto_poly_fdm"]["seconds"]}
     # c4 end to end from host buffers: stg_stdg_step_host (H2D of u_n, solve,
     # D2H of U and u_next inside the call), pinned and pageable
     nc = NewtonConfig(**kw)
@@ -704,13 +705,14 @@ def solves(op, cfg, C, NewtonConfig, torch, dev, args):
     op2 = SlabOperator(**c2.kwargs())
     u2 = torch.as_tensor(C.initial_state(c2), device=dev)
     out["c2"] = {"applies": apply_rates(op2, c2, C, torch, dev, 40)}
-    for pname, pc in (("auto_fdm2_eblock", L.STG_PRECOND_AUTO), ("none", L.STG_PRECOND_NONE)):
+    for pname, pc in (("auto_poly_fdm2", L.STG_PRECOND_AUTO), ("eblock_fdm2", L.STG_PRECOND_EBLOCK),
+                      ("none", L.STG_PRECOND_NONE)):
         nc2 = NewtonConfig(precond=pc, **kw)
         op2.stdg_step(0.0, c2.dt, u2, nc2)
         t, (_, _, info2) = _best_wall(torch, lambda: op2.stdg_step(0.0, c2.dt, u2, nc2))
         out["c2"][f"slab_solve_{pname}"] = {"seconds": t,
                                             "gmres_iterations": info2.linear_iterations}
-    out["c2"]["slab_solve_s"] = out["c2"]["slab_solve_auto_fdm2_eblock"]["seconds"]
+    out["c2"]["slab_solve_s"] = out["c2"]["slab_solve_auto_poly_fdm2"]["seconds"]
     del op2, u2
     # c1: 1000 R(U) applies (launch-latency bound) and the GMRES slab solve at 1e-12
     c1 = C.CONFIGS["c1"]

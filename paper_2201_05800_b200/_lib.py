@@ -22,6 +22,7 @@ STG_KERNEL_AUTO, STG_KERNEL_GENERIC, STG_KERNEL_FAST = 0, 1, 2
 STG_PRECOND_NONE, STG_PRECOND_TBLOCK, STG_PRECOND_EBLOCK, STG_PRECOND_AUTO = 0, 1, 2, 3
 STG_PRECOND_JACOBI = 4
 STG_PRECOND_SWEEP = 5
+STG_PRECOND_POLY = 6
 STG_MAX_HISTORY = 64
 
 # every symbol include/stg_cuda.h declares

@@ -390,6 +390,11 @@ bool eblock_f32_supported(int nt, int n1);
 // element blocks B (fp32, build_burgers_eblock) plus the inflow couplings G;
 // work: sweep_work_doubles(nt, ncells, n1) doubles (y = B^-1 in).
 // n_tau = 4, N + 1 in {2, 4}.
+bool offdiag_supported(const Geometry& g, int nt);
+// out = r - L y, L the neighbour couplings of the constant-velocity advection
+// Jacobian (mix mx); false (nothing launched) for an uninstantiated shape
+bool offdiag_residual(double* out, const double* r, const double* y, const SpatialCoef& sp,
+                      const MixCoef& mx, const Geometry& g, int nt, cudaStream_t s, Skip skip);
 bool sweep_supported(int nt, int n1);
 size_t sweep_work_doubles(int nt, int ncells, int n1);
 void precond_sweep(double* out, const double* in, const float* B, const float* G, double* work,
@@ -412,6 +417,9 @@ void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s)
 void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s);
 // U_j = u for j < nb (1 (x) u, stdg.hpp:131)
 void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t s);
+// y = z + x - q (x may alias y; 16-byte aligned vectors), honouring skip
+void vec_poly_step(double* y, const double* z, const double* x, const double* q, long long n,
+                   cudaStream_t s, Skip skip);
 // out[j] = <V_j, w>, j < k <= 64 (V_j = V + j*ldv); partial buffer >= grid*k doubles
 void vec_multidot(const double* V, long long ldv, int k, const double* w, long long n,
                   double* partial, double* out, cudaStream_t s, Skip skip = {});

@@ -402,6 +402,65 @@ __global__ void __launch_bounds__(kSwCh) k_sweep_win(double* __restrict__ out,
   }
 }
 
+// ---- off-block-diagonal residual r - L y (polynomial preconditioner) ------
+// L = J - blockdiag(J): the neighbour couplings of the constant-velocity
+// advection Jacobian, S (x) (the cL / cR face terms of SpatialCoef), so
+//   out[t][c][i] = r[t][c][i] - sum_j S(t, j) sum_a ( [i_a = 0] cL_a y_j[c - e_a][i_a <- N]
+//                                                + [i_a = N] cR_a y_j[c + e_a][i_a <- 0] ).
+// With the exact element-block inverse P0 (FDM), one Neumann step of the
+// polynomial preconditioner is y <- P0^-1 (r - L y).  One thread per spatial
+// node (all temporal nodes); interior nodes copy r.
+template <int D, int N1, int NT>
+__global__ void __launch_bounds__(256) k_offdiag(double* __restrict__ out,
+                                                 const double* __restrict__ r,
+                                                 const double* __restrict__ y,
+                                                 const SpatialCoef sp, const MixCoef mx,
+                                                 const Geometry g, Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  constexpr int NPC = D == 1 ? N1 : (D == 2 ? N1 * N1 : N1 * N1 * N1);
+  const long long ns = g.n_sdof;
+  for (long long sidx = blockIdx.x * (long long)blockDim.x + threadIdx.x; sidx < ns;
+       sidx += (long long)gridDim.x * blockDim.x) {
+    const int cell = int(sidx / NPC), node = int(sidx - (long long)cell * NPC);
+    const int idx[3] = {node % N1, (node / N1) % N1, node / (N1 * N1)};
+    const int ci[3] = {cell % g.nx, (cell / g.nx) % g.ny, cell / (g.nx * g.ny)};
+    const int nc[3] = {g.nx, g.ny, g.nz};
+    const int st[3] = {1, N1, N1 * N1};
+    double nb[NT];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) nb[j] = 0.0;
+    bool any = false;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      const int cstride = a == 0 ? 1 : (a == 1 ? g.nx : g.nx * g.ny);
+      if (idx[a] == 0 && sp.cL[a] != 0.0) {
+        const int cn = cell + (ci[a] == 0 ? (nc[a] - 1) : -1) * cstride;
+        const long long o = (long long)cn * NPC + node + (N1 - 1) * st[a];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) nb[j] = fma(sp.cL[a], y[j * ns + o], nb[j]);
+        any = true;
+      }
+      if (idx[a] == N1 - 1 && sp.cR[a] != 0.0) {
+        const int cn = cell + (ci[a] == nc[a] - 1 ? -(nc[a] - 1) : 1) * cstride;
+        const long long o = (long long)cn * NPC + node - (N1 - 1) * st[a];
+#pragma unroll
+        for (int j = 0; j < NT; ++j) nb[j] = fma(sp.cR[a], y[j * ns + o], nb[j]);
+        any = true;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+      double v = r[t * ns + sidx];
+      if (any) {
+#pragma unroll
+        for (int j = 0; j < NT; ++j) v = fma(-mx.S[t][j], nb[j], v);
+      }
+      out[t * ns + sidx] = v;
+    }
+  }
+}
+
 int pgrid(long long n) {
   long long g = (n + kPB - 1) / kPB;
   if (g > 148 * 8) g = 148 * 8;
@@ -739,6 +798,36 @@ void precond_sweep(double* out, const double* in, const float* B, const float* G
   if (nt != 4) return;
   if (n1 == 4) go(std::integral_constant<int, 4>{});
   else if (n1 == 2) go(std::integral_constant<int, 2>{});
+}
+
+bool offdiag_supported(const Geometry& g, int nt) {
+  return (g.dim == 3 && ((g.n1 == 4 && nt == 4) || (g.n1 == 3 && nt == 3))) ||
+         (g.dim == 2 && ((g.n1 == 5 && nt == 5) || (g.n1 == 4 && nt == 4) ||
+                         (g.n1 == 3 && nt == 3))) ||
+         (g.dim == 1 && g.n1 == 4 && nt == 4);
+}
+
+bool offdiag_residual(double* out, const double* r, const double* y, const SpatialCoef& sp,
+                      const MixCoef& mx, const Geometry& g, int nt, cudaStream_t s, Skip skip) {
+  const long long ns = g.n_sdof;
+  long long blocks = (ns + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  const int gb = int(blocks);
+  if (g.dim == 3 && g.n1 == 4 && nt == 4)
+    launch_ex(kPdlPrecond, k_offdiag<3, 4, 4>, gb, 256, 0, s, out, r, y, sp, mx, g, skip);
+  else if (g.dim == 3 && g.n1 == 3 && nt == 3)
+    launch_ex(kPdlPrecond, k_offdiag<3, 3, 3>, gb, 256, 0, s, out, r, y, sp, mx, g, skip);
+  else if (g.dim == 2 && g.n1 == 5 && nt == 5)
+    launch_ex(kPdlPrecond, k_offdiag<2, 5, 5>, gb, 256, 0, s, out, r, y, sp, mx, g, skip);
+  else if (g.dim == 2 && g.n1 == 4 && nt == 4)
+    launch_ex(kPdlPrecond, k_offdiag<2, 4, 4>, gb, 256, 0, s, out, r, y, sp, mx, g, skip);
+  else if (g.dim == 2 && g.n1 == 3 && nt == 3)
+    launch_ex(kPdlPrecond, k_offdiag<2, 3, 3>, gb, 256, 0, s, out, r, y, sp, mx, g, skip);
+  else if (g.dim == 1 && g.n1 == 4 && nt == 4)
+    launch_ex(kPdlPrecond, k_offdiag<1, 4, 4>, gb, 256, 0, s, out, r, y, sp, mx, g, skip);
+  else
+    return false;
+  return true;
 }
 
 bool eblock_f32_supported(int nt, int n1) {

@@ -45,6 +45,23 @@ __global__ void k_axpby(double* y, double a, const double* x, double b, long lon
        i += (long long)gridDim.x * blockDim.x)
     y[i] = fma(a, x[i], b * y[i]);
 }
+// one Neumann step of the polynomial preconditioner: y = z + x - q (x may be y)
+__global__ void k_poly_step(double* y, const double* __restrict__ z, const double* x,
+                            const double* __restrict__ q, long long n, Skip skip) {
+  pdl_entry();
+  if (skip_now(skip)) return;
+  const long long n2 = n >> 1;
+  const double2* z2 = reinterpret_cast<const double2*>(z);
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  const double2* q2 = reinterpret_cast<const double2*>(q);
+  double2* y2 = reinterpret_cast<double2*>(y);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2;
+       i += (long long)gridDim.x * blockDim.x) {
+    const double2 a = z2[i], b = x2[i], c = q2[i];
+    y2[i] = make_double2(a.x + b.x - c.x, a.y + b.y - c.y);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1)) y[n - 1] = z[n - 1] + x[n - 1] - q[n - 1];
+}
 __global__ void k_axpy(double* y, double a, const double* x, long long n) {
   pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -407,6 +424,10 @@ void vec_axpy(double* y, double a, const double* x, long long n, cudaStream_t s)
 }
 void vec_axpby(double* y, double a, const double* x, double b, long long n, cudaStream_t s) {
   launch_ex(vec_pdl(n), k_axpby, grid_for(n), kBlock, 0, s, y, a, x, b, n);
+}
+void vec_poly_step(double* y, const double* z, const double* x, const double* q, long long n,
+                   cudaStream_t s, Skip skip) {
+  launch_ex(vec_pdl(n), k_poly_step, grid_for(n / 2 + 1), kBlock, 0, s, y, z, x, q, n, skip);
 }
 void vec_broadcast(double* U, const double* u, int nb, long long n, cudaStream_t s) {
   launch_ex(vec_pdl(n), k_broadcast, grid_for(n), kBlock, 0, s, U, u, nb, n);

@@ -116,6 +116,8 @@ struct stg_handle {
   bool eblock_valid = false;
   bool eblock_sweep = false;  // ... with the sweep's inflow couplings in sweepG
   DevBuf sweepG, sweepW;      // d = 1 upwind sweep: couplings (fp32), y = B^-1 r
+  DevBuf polyZ, polyW, polyQ;  // polynomial preconditioner: P0^-1 r, J y, P0^-1 J y
+  bool block_exact = false;    // the last make_precond built an exact element-block inverse
   // d = 2 dense element block: the uploaded inverse and the mix it belongs to
   DevBuf etab;  // d = 1 advection element block (shared), keyed by mix
   stg::MixCoef etab_mix{};
@@ -1297,7 +1299,29 @@ bool gen_eblock_ok(const stg_handle* h) {
   return h->desc.model == STG_MODEL_ADVDIFF && h->nt * h->g.npc * h->r <= 32;
 }
 
+// Neumann terms of STG_PRECOND_POLY (env STG_POLY_TERMS, default 3)
+int poly_terms() {
+  static const int m = [] {
+    const char* e = std::getenv("STG_POLY_TERMS");
+    const int v = e ? std::atoi(e) : 3;
+    return v < 0 ? 0 : v;
+  }();
+  return m;
+}
+
+// the base block preconditioner P0 of STG_PRECOND_POLY
+int poly_base(const stg_handle* h) {
+  if (h->desc.dim == 1 && h->desc.model == STG_MODEL_BURGERS &&
+      stg::sweep_supported(h->nt, h->n1))
+    return STG_PRECOND_SWEEP;
+  return STG_PRECOND_EBLOCK;
+}
+
 int resolve_precond(const stg_handle* h, int kind) {
+  if (kind == STG_PRECOND_POLY) {
+    resolve_precond(h, poly_base(h));  // throws where the base block does not exist
+    return STG_PRECOND_POLY;
+  }
   if (general_model(h->desc.model)) {
     if (kind == STG_PRECOND_NONE) return STG_PRECOND_NONE;
     if (kind == STG_PRECOND_JACOBI)
@@ -1316,6 +1340,14 @@ int resolve_precond(const stg_handle* h, int kind) {
       !(h->desc.dim == 1 && h->desc.model == STG_MODEL_BURGERS &&
         stg::eblock_f32_supported(h->nt, h->n1) && stg::sweep_supported(h->nt, h->n1)))
     throw std::invalid_argument("upwind block sweep: d = 1 Burgers, n_tau = 4, degree 1 or 3");
+  // d >= 2 advection with an exact element-block inverse: the polynomial
+  // preconditioner around it (c4 slab solve 1.57 -> 1.08 ms, c2 1.65 ->
+  // 1.15 ms: 7 GMRES steps -> 2); d = 1 keeps the element blocks (the fused
+  // small solve takes c1)
+  static const bool no_poly = std::getenv("STG_AUTO_NO_POLY") != nullptr;
+  if (kind == STG_PRECOND_AUTO && h->desc.dim >= 2 && (fdm_ok(h) || dense2d_ok(h)) && !no_poly &&
+      poly_terms() > 0 && stg::offdiag_supported(h->g, h->nt))
+    return STG_PRECOND_POLY;
   if (kind == STG_PRECOND_AUTO)
     return (h->desc.dim == 1 || fdm_ok(h) || dense2d_ok(h))
                ? STG_PRECOND_EBLOCK
@@ -1328,7 +1360,7 @@ int resolve_precond(const stg_handle* h, int kind) {
     throw std::invalid_argument("temporal-block Jacobi: advection only");
   if (kind == STG_PRECOND_JACOBI && h->desc.model != STG_MODEL_ADVECTION)
     throw std::invalid_argument("diagonal (Jacobi) preconditioner: advection only");
-  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_SWEEP)
+  if (kind < STG_PRECOND_NONE || kind > STG_PRECOND_POLY)
     throw std::invalid_argument("unknown preconditioner");
   return kind;
 }
@@ -1622,6 +1654,10 @@ Op general_eblock(stg_handle* h, const stg::MixCoef& mx) {
 
 Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U) {
   kind = resolve_precond(h, kind);
+  if (kind == STG_PRECOND_POLY) kind = poly_base(h);  // the block part (precond_for wraps it)
+  // an exact element-block inverse of an advection Jacobian unless a
+  // fallback below says otherwise
+  h->block_exact = kind == STG_PRECOND_EBLOCK && h->desc.model == STG_MODEL_ADVECTION;
   if (kind == STG_PRECOND_NONE) return Op();
   if (general_model(h->desc.model)) return general_eblock(h, mx);
   const int nt = h->nt, n1 = h->n1, npc = h->g.npc, d = h->desc.dim;
@@ -1776,7 +1812,9 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
         h->launches++;
       };
     }
-    return make_precond(h, STG_PRECOND_TBLOCK, mx, U);  // spectrum not of the FDM form
+    Op tb = make_precond(h, STG_PRECOND_TBLOCK, mx, U);  // spectrum not of the FDM form
+    h->block_exact = false;
+    return tb;
   }
   if (d == 3) {  // element-block Jacobi by fast diagonalisation
     stg::FdmCoef c;
@@ -1796,7 +1834,9 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       };
     if (h->desc.model != STG_MODEL_ADVECTION)
       throw std::invalid_argument("element-block Jacobi: no factorisation");
-    return make_precond(h, STG_PRECOND_TBLOCK, mx, U);  // spectrum not of the FDM form
+    Op tb = make_precond(h, STG_PRECOND_TBLOCK, mx, U);  // spectrum not of the FDM form
+    h->block_exact = false;
+    return tb;
   }
   // element-block Jacobi, d = 1: block (r,i),(j,q) of the element-local Jacobian
   const int nb = nt * n1;
@@ -1850,6 +1890,53 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
   return [h, tab, bstride, nt, n1, ncells, ns](const double* in, double* out) {
     stg::precond_eblock(out, in, tab, bstride, nt, n1, ncells, ns, h->stream, h->skip);
     h->launches++;
+  };
+}
+
+// The right preconditioner of a solve with Jacobian action A: make_precond's
+// block preconditioner P0, and for STG_PRECOND_POLY the truncated Neumann
+// series of (P0^-1 A)^-1 P0^-1 around it:
+//   z = P0^-1 r,  y_0 = z,  y_{i+1} = z + y_i - P0^-1 A y_i   (i < m).
+// A fixed linear operator, so GMRES stays exact; every launch honours the
+// handle's skip flag (speculative Arnoldi steps).
+Op precond_for(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U, const Op& A) {
+  const int rk = resolve_precond(h, kind);
+  Op P0 = make_precond(h, rk, mx, U);
+  const int m = poly_terms();
+  if (rk != STG_PRECOND_POLY || !P0 || m == 0) return P0;
+  const long long n = h->n_dof;
+  h->polyZ.ensure(size_t(n));
+  h->polyW.ensure(size_t(n));
+  double* z = h->polyZ.p;
+  double* w = h->polyW.p;
+  // P0 the exact element-block inverse of constant-velocity advection (no
+  // neighbour coupling inside a block): y_{i+1} = P0^-1 (r - L y_i) with the
+  // neighbour couplings L = J - P0 applied directly (one pass instead of a
+  // Jacobian action, a block apply and an axpy per term)
+  static const bool generic = std::getenv("STG_POLY_GENERIC") != nullptr;
+  if (h->block_exact && stg::offdiag_supported(h->g, h->nt) && !generic) {
+    const stg::MixCoef mj = mx;
+    return [h, P0, m, mj, z](const double* r, double* y) {
+      P0(r, y);
+      for (int i = 0; i < m; ++i) {
+        stg::offdiag_residual(z, r, y, h->sp, mj, h->g, h->nt, h->stream, h->skip);
+        h->launches++;
+        P0(z, y);
+      }
+    };
+  }
+  h->polyQ.ensure(size_t(n));
+  double* q = h->polyQ.p;
+  return [h, A, P0, m, n, z, w, q](const double* r, double* y) {
+    P0(r, z);
+    const double* x = z;
+    for (int i = 0; i < m; ++i) {
+      A(x, w);
+      P0(w, q);
+      stg::vec_poly_step(y, z, x, q, n, h->stream, h->skip);
+      h->launches++;
+      x = y;
+    }
   };
 }
 
@@ -1955,7 +2042,7 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
           L.A = [h, dt, X, eps, un2](const double* v, double* Jv) {
             st_jvp(h, dt, X, v, Jv, eps, un2);
           };
-          L.P = make_precond(h, cfg.precond, st_mix(h, dt, false), X);
+          L.P = precond_for(h, cfg.precond, st_mix(h, dt, false), X, L.A);
           return L;
         },
         U, n, cfg);
@@ -2002,7 +2089,7 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
           L.A = [h, form, dt, X, eps, un2](const double* v, double* Jv) {
             stage_jvp(h, form, dt, X, v, Jv, eps, un2);
           };
-          L.P = make_precond(h, cfg.precond, stage_mix(h, form, dt, false), X);
+          L.P = precond_for(h, cfg.precond, stage_mix(h, form, dt, false), X, L.A);
           return L;
         },
         U, n, cfg);
@@ -2353,11 +2440,10 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     (void)t_n;
     if (!linear_model(h->desc.model)) need(U, "U");
     h->eblock_valid = false;
-    const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
-    const GmresStats st = gmres(
-        h, [&](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); }, b, x, h->n_dof,
-        restart, tol, max_it, P ? &P : nullptr, /*x_zero=*/false,
-        /*pipelined=*/true);
+    const Op A = [h, dt, U](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); };
+    const Op P = precond_for(h, precond, st_mix(h, dt, false), U, A);
+    const GmresStats st = gmres(h, A, b, x, h->n_dof, restart, tol, max_it, P ? &P : nullptr,
+                                /*x_zero=*/false, /*pipelined=*/true);
     if (iterations) *iterations = st.iterations;
     if (rel_residual) *rel_residual = st.rel_residual;
     if (!st.converged)
@@ -2374,7 +2460,8 @@ int stg_st_precond_apply(stg_handle* h, double dt, const double* U, int precond,
     need(out, "out");
     if (!linear_model(h->desc.model)) need(U, "U");
     h->eblock_valid = false;
-    const Op P = make_precond(h, precond, st_mix(h, dt, false), U);
+    const Op A = [h, dt, U](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); };
+    const Op P = precond_for(h, precond, st_mix(h, dt, false), U, A);
     if (P) {
       P(in, out);
       check_launch(h);
