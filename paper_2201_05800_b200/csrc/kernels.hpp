@@ -311,8 +311,18 @@ static_assert(sizeof(FdmCoef3) % 16 == 0, "bulk-copied block");
 bool fdm3_supported(const Geometry& g, int n_tau);
 // coef: a device copy of host_coef (the kernel reads its spatial factors as
 // parameters and bulk-copies the temporal table)
+// The neighbour couplings of a Neumann step folded into the block apply:
+// with od, fdm3_kernel computes out = P0^-1 (in - L y) (L: the upwind face
+// terms cL / cR of the constant-velocity advection Jacobian, mixed by the
+// diagonal S), reading y's neighbour traces while it stages each row.
+struct FdmOffdiag {
+  const double* y;
+  double S[4];          // diagonal of the temporal mix S
+  double cL[3], cR[3];  // SpatialCoef face coefficients
+};
 int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const Geometry& g,
-                        const double* in, double* out, cudaStream_t s, Skip skip = {});
+                        const double* in, double* out, cudaStream_t s, Skip skip = {},
+                        const FdmOffdiag* od = nullptr);
 
 // d = 2 element-block inverse by fast diagonalisation (kernels_fdm.cu,
 // fdm2_kernel): L_e^-1 = (I (x) Py (x) Px) blockdiag_theta((T + theta S)^-1)

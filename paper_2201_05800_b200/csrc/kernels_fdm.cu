@@ -363,9 +363,108 @@ __device__ __forceinline__ void inv_pair(const C2& col, const C2& s, const C2& d
 }
 }  // namespace f3
 
+// OD: the row minus its neighbour couplings, -S(t,t) sum_a (cL_a y[c - e_a]
+// trace + cR_a y[c + e_a] trace), before the transforms (FdmOffdiag).  The
+// traces are loaded into registers at the top of the segment (both rows of
+// the thread at once, ahead of the tile wait): the x / y face lines of the
+// row itself, and a quarter of the z-face plane -- the four lanes of one
+// (t, cell) hold the four rows z = 0..3 and each loads one line of the
+// plane, which the z = 0 (cL) / z = 3 (cR) lane gathers by shuffles.
+struct RowTr {
+  double x[4], y[4], z[4];
+};
+
+template <bool OD>
+__device__ __forceinline__ void fdm3_row_prefetch(RowTr& tr, const FdmOffdiag& od,
+                                                  const Geometry& g, int seg, int row) {
+  if constexpr (OD) {
+    const int t = row / (f3::E * 4), e = (row >> 2) & (f3::E - 1), z = row & 3;
+    const int cell = seg * f3::E + e;
+    const int cx = cell % g.nx, cy = (cell / g.nx) % g.ny, cz = cell / (g.nx * g.ny);
+    const double* yt = od.y + t * g.n_sdof;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tr.x[q] = tr.y[q] = tr.z[q] = 0.0;
+    if (od.cL[0] != 0.0 || od.cR[0] != 0.0) {  // x- (ix = 3) or x+ (ix = 0) neighbour line
+      const bool L = od.cL[0] != 0.0;
+      const int dc = L ? (cx == 0 ? g.nx - 1 : -1) : (cx == g.nx - 1 ? 1 - g.nx : 1);
+      const double* p = yt + (long long)(cell + dc) * 64 + z * 16 + (L ? 3 : 0);
+#pragma unroll
+      for (int iy = 0; iy < 4; ++iy) tr.x[iy] = __ldg(p + 4 * iy);
+    }
+    if (od.cL[1] != 0.0 || od.cR[1] != 0.0) {  // y- (iy = 3) or y+ (iy = 0) neighbour line
+      const bool L = od.cL[1] != 0.0;
+      const int dc = L ? (cy == 0 ? (g.ny - 1) * g.nx : -g.nx)
+                       : (cy == g.ny - 1 ? -(g.ny - 1) * g.nx : g.nx);
+      const double2* p =
+          reinterpret_cast<const double2*>(yt + (long long)(cell + dc) * 64 + z * 16 + (L ? 12 : 0));
+      const double2 a = __ldg(p), b = __ldg(p + 1);
+      tr.y[0] = a.x;
+      tr.y[1] = a.y;
+      tr.y[2] = b.x;
+      tr.y[3] = b.y;
+    }
+    if (od.cL[2] != 0.0 || od.cR[2] != 0.0) {  // line z of the z- (iz = 3) / z+ (iz = 0) plane
+      const bool L = od.cL[2] != 0.0;
+      const long long pl = (long long)g.nx * g.ny;
+      const long long dc = L ? (cz == 0 ? (g.nz - 1) * pl : -pl) : (cz == g.nz - 1 ? -(g.nz - 1) * pl : pl);
+      const double2* p =
+          reinterpret_cast<const double2*>(yt + (cell + dc) * 64 + (L ? 48 : 0) + 4 * z);
+      const double2 a = __ldg(p), b = __ldg(p + 1);
+      tr.z[0] = a.x;
+      tr.z[1] = a.y;
+      tr.z[2] = b.x;
+      tr.z[3] = b.y;
+    }
+  }
+}
+
+// every lane calls it (the z-plane gather shuffles within the 4-lane group)
+template <bool OD>
+__device__ __forceinline__ void fdm3_row_offdiag(double (&r)[16], const RowTr& tr,
+                                                 const FdmOffdiag& od, int row) {
+  if constexpr (OD) {
+    const int t = row / (f3::E * 4), z = row & 3;
+    // (a select chain: a dynamic index into the parameter struct would copy
+    // it to local memory)
+    const double s = t == 0 ? od.S[0] : (t == 1 ? od.S[1] : (t == 2 ? od.S[2] : od.S[3]));
+    if (od.cL[0] != 0.0 || od.cR[0] != 0.0) {
+      const int ix = od.cL[0] != 0.0 ? 0 : 3;
+      const double f = s * (od.cL[0] != 0.0 ? od.cL[0] : od.cR[0]);
+#pragma unroll
+      for (int iy = 0; iy < 4; ++iy) {
+        if (ix == 0) r[4 * iy] = fma(-f, tr.x[iy], r[4 * iy]);
+        else r[4 * iy + 3] = fma(-f, tr.x[iy], r[4 * iy + 3]);
+      }
+    }
+    if (od.cL[1] != 0.0 || od.cR[1] != 0.0) {
+      const int o = od.cL[1] != 0.0 ? 0 : 12;
+      const double f = s * (od.cL[1] != 0.0 ? od.cL[1] : od.cR[1]);
+#pragma unroll
+      for (int ix = 0; ix < 4; ++ix) {
+        if (o == 0) r[ix] = fma(-f, tr.y[ix], r[ix]);
+        else r[12 + ix] = fma(-f, tr.y[ix], r[12 + ix]);
+      }
+    }
+    if (od.cL[2] != 0.0 || od.cR[2] != 0.0) {
+      const bool L = od.cL[2] != 0.0;
+      const int owner = L ? 0 : 3;
+      const double f = s * (L ? od.cL[2] : od.cR[2]);
+      const int base = (threadIdx.x & 31) & ~3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const double v = __shfl_sync(0xffffffffu, tr.z[k], base + q);
+          if (z == owner) r[4 * q + k] = fma(-f, v, r[4 * q + k]);
+        }
+    }
+  }
+}
+
 // phase A on one (t, cell, z) row: forward x (kept modes j) and y, in place
-template <bool PARAM>
-__device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int row) {
+template <bool PARAM, bool OD>
+__device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int row,
+                                             const FdmOffdiag& od, const RowTr& tr) {
   const int sw = row & 7;
   double r[16];
 #pragma unroll
@@ -374,6 +473,7 @@ __device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int r
     r[2 * q] = v.x;
     r[2 * q + 1] = v.y;
   }
+  fdm3_row_offdiag<OD>(r, tr, od, row);
   double ar[2][4], ai[2][4];  // [j][y]: x-mode j of line y
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
@@ -509,11 +609,11 @@ __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs,
 namespace f3 {
 constexpr int kRowUnroll = STG_FDM3_ROW_UNROLL;
 }
-template <bool PARAM>
+template <bool PARAM, bool OD>
 __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
     fdm3_kernel(const __grid_constant__ CUtensorMap tm, const __grid_constant__ CUtensorMap tm_out,
                 const FdmCoef3* __restrict__ coef, const __grid_constant__ FdmCoef3 cp,
-                const Geometry g, const Skip skip) {
+                const Geometry g, const Skip skip, const FdmOffdiag od) {
   extern __shared__ unsigned char smem_raw[];
   unsigned char* base = smem_raw + ((1024u - (ptxh::smem_u32(smem_raw) & 1023u)) & 1023u);
   const FdmCoef3& cs = *reinterpret_cast<const FdmCoef3*>(base + f3::OFF_C);
@@ -568,10 +668,13 @@ __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
       ptxh::fence_proxy_async_smem();
       issue(seg + gridDim.x, st ^ 1);
     }
+    RowTr tr0, tr1;
+    fdm3_row_prefetch<OD>(tr0, od, g, seg, tid);
+    fdm3_row_prefetch<OD>(tr1, od, g, seg, tid + f3::THREADS);
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
-#pragma unroll(f3::kRowUnroll)
-    for (int k = 0; k < 2; ++k) fdm3_fwd_row<PARAM>(c, X, tid + k * f3::THREADS);
+    fdm3_fwd_row<PARAM, OD>(c, X, tid, od, tr0);
+    fdm3_fwd_row<PARAM, OD>(c, X, tid + f3::THREADS, od, tr1);
     __syncthreads();
     fdm3_unit<PARAM>(c, cs, X, eB, qB);
     __syncthreads();
@@ -1115,7 +1218,8 @@ bool fdm3_supported(const Geometry& g, int n_tau) {
 }
 
 int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const Geometry& g,
-                        const double* in, double* out, cudaStream_t s, Skip skip) {
+                        const double* in, double* out, cudaStream_t s, Skip skip,
+                        const FdmOffdiag* od) {
   EncodeFn enc = encode_fn();
   if (!enc || (reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
     return -1;
@@ -1133,12 +1237,14 @@ int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const G
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   static const bool smem_coef = std::getenv("STG_FDM3_SMEMC") != nullptr;
-  auto kern = smem_coef ? fdm3_kernel<false> : fdm3_kernel<true>;
+  auto kern = od ? (smem_coef ? fdm3_kernel<false, true> : fdm3_kernel<true, true>)
+                 : (smem_coef ? fdm3_kernel<false, false> : fdm3_kernel<true, false>);
   static int occ_dev[kMaxDevices];
   const int dev = device_slot();
   int& occ = occ_dev[dev];
   if (occ <= 0) {
-    for (auto k : {fdm3_kernel<false>, fdm3_kernel<true>})
+    for (auto k : {fdm3_kernel<false, false>, fdm3_kernel<true, false>, fdm3_kernel<false, true>,
+                   fdm3_kernel<true, true>})
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, f3::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, f3::THREADS, f3::SMEM);
     if (occ < 1) occ = 1;
@@ -1148,7 +1254,8 @@ int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const G
   const int nseg = g.n_cells / f3::E;
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
-  launch_ex(kPdlFdm, kern, grid, f3::THREADS, f3::SMEM, s, map, map_out, coef, host_coef, g, skip);
+  launch_ex(kPdlFdm, kern, grid, f3::THREADS, f3::SMEM, s, map, map_out, coef, host_coef, g, skip,
+            od ? *od : FdmOffdiag{});
   return 1;
 }
 

@@ -1914,6 +1914,38 @@ Op precond_for(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U,
   // neighbour couplings L = J - P0 applied directly (one pass instead of a
   // Jacobian action, a block apply and an axpy per term)
   static const bool generic = std::getenv("STG_POLY_GENERIC") != nullptr;
+  // d = 3 with the fdm3 blocks and a diagonal temporal mix: the neighbour
+  // couplings are folded into the block apply (fdm3_kernel with FdmOffdiag),
+  // y_{i+1} = P0^-1 (r - L y_i) in one pass, ping-ponging between z and y
+  bool s_diag = true;
+  for (int t = 0; t < h->nt; ++t)
+    for (int j = 0; j < h->nt; ++j)
+      if (t != j && mx.S[t][j] != 0.0) s_diag = false;
+  static const bool no_fused = std::getenv("STG_POLY_UNFUSED") != nullptr;
+  if (h->block_exact && h->desc.dim == 3 && stg::fdm3_supported(h->g, h->nt) && h->fdm3_valid &&
+      std::memcmp(&h->fdm3_mix, &mx, sizeof mx) == 0 && s_diag && !generic && !no_fused) {
+    stg::FdmOffdiag od{};
+    for (int t = 0; t < 4; ++t) od.S[t] = mx.S[t][t];
+    for (int a = 0; a < 3; ++a) {
+      od.cL[a] = h->sp.cL[a];
+      od.cR[a] = h->sp.cR[a];
+    }
+    const stg::FdmCoef3* c = reinterpret_cast<const stg::FdmCoef3*>(h->fdm3M.p);
+    const stg::FdmCoef3* hc = h->fdm3_host.get();
+    return [h, P0, m, od, c, hc, z](const double* r, double* y) {
+      double* buf[2] = {z, y};
+      int cur = (m & 1) ? 0 : 1;  // the last term lands in y
+      P0(r, buf[cur]);
+      for (int i = 0; i < m; ++i) {
+        stg::FdmOffdiag o = od;
+        o.y = buf[cur];
+        if (stg::launch_precond_fdm3(c, *hc, h->g, r, buf[cur ^ 1], h->stream, h->skip, &o) < 0)
+          throw std::runtime_error("element-block preconditioner launch failed");
+        h->launches++;
+        cur ^= 1;
+      }
+    };
+  }
   if (h->block_exact && stg::offdiag_supported(h->g, h->nt) && !generic) {
     const stg::MixCoef mj = mx;
     return [h, P0, m, mj, z](const double* r, double* y) {

@@ -320,7 +320,9 @@ def test_fdm_element_block_is_exact_local_inverse(velocity, cells):
 
 
 @pytest.mark.parametrize("dim,cells,velocity,degree", [
-    (3, (2, 2, 4), (1.0, 1.0, 1.0), 3),      # fdm3 blocks + k_offdiag<3,4,4>
+    (3, (2, 2, 4), (1.0, 1.0, 1.0), 3),      # fdm3 with the couplings folded in
+    (3, (4, 2, 2), (-0.7, 0.4, -1.1), 3),    # ... upwind on both sides
+    (3, (8, 4, 2), (0.3, -1.2, 0.8), 3),     # ... 64 cells: several segments per row
     (3, (2, 2, 2), (-0.7, 0.4, -1.1), 3),    # fdm (two-half) blocks, upwind on both sides
     (2, (8, 4), (1.0, 0.5), 4),              # fdm2i blocks + k_offdiag<2,5,5>
     (2, (4, 4), (-0.6, 1.1), 3),             # fdm2 blocks + k_offdiag<2,4,4>
@@ -329,7 +331,8 @@ def test_poly_precond_is_the_neumann_series(dim, cells, velocity, degree):
     """STG_PRECOND_POLY (the AUTO choice for d >= 2 advection) applies
     sum_{i=0..m} (I - P0^-1 J)^i P0^-1 with P0 the exact element blocks and m
     = 3: checked against the series formed in numpy from the oracle's J.v and
-    dense block solves."""
+    dense block solves.  d = 3 meshes of 16k cells run the fused fdm3 +
+    neighbour-coupling kernel, the others k_offdiag + the block apply."""
     cfg = make(dim, degree, degree + 1, cells, velocity, dt=0.02)
     op, pr = pair(cfg)
     ns, nt = op.n_sdof, degree + 1
