@@ -59,6 +59,7 @@ __device__ __forceinline__ void block_finish_sum(const double* part, int nblocks
 // same arithmetic as the host loop it replaces: H(j,k) = c_k c_j d_j with
 // c_j = 1/||S_j||, h_{k+1,k} = c_k ||S_{k+1}|| / scale, then the previous
 // rotations, a new rotation, and the residual estimate |g_{k+1}|.
+constexpr int kGivensLocal = 64;  // restart lengths up to this decide convergence before a 2nd pass
 __device__ __noinline__ void gmres_givens(const GivensArgs& a, const double* d, double sc,
                                           const double* hn2, double n2) {
   GmresDev* G = a.G;
@@ -72,7 +73,43 @@ __device__ __noinline__ void gmres_givens(const GivensArgs& a, const double* d, 
     double hh = 0.0;
     for (int j = 0; j <= k; ++j) hh += d1[j] * d1[j] / hn2[j];
     if (!(ww - hh > G->reorth_tol * ww) || !(n2 > 0.0)) {
-      // heavy cancellation: the host enqueues a second pass for this step
+      // heavy cancellation.  A nearly exact preconditioner makes A P^-1 v_k
+      // almost a combination of the basis, so the step that converges is
+      // exactly the one that cancels: decide convergence first, with the
+      // exact norm n2 this pass has reduced (accurate to ~eps * ||w|| / ||S||
+      // relative; the single pass's orthogonality loss only matters for
+      // later steps, and there are none).  Converged: commit the step.
+      // Otherwise the host enqueues a second pass for this step.
+      if (n2 > 0.0 && ww > 0.0 && k < kGivensLocal) {
+        double col[kGivensLocal + 1];
+        for (int j = 0; j <= k; ++j) col[j] = ckk * G->cn[j] * d1[j];
+        for (int j = 0; j < k; ++j) {
+          const double a0 = col[j], a1 = col[j + 1];
+          col[j] = G->cs[j] * a0 + G->sn[j] * a1;
+          col[j + 1] = -G->sn[j] * a0 + G->cs[j] * a1;
+        }
+        const double hnt = ckk * sqrt(n2) / sc;
+        const double dent = hypot(col[k], hnt);
+        const double snt = dent == 0.0 ? 0.0 : hnt / dent;
+        if (fabs(snt * G->g[k]) <= G->tol_abs) {
+          for (int j = 0; j <= k; ++j) Hc[j * m + k] = col[j];
+          const double ct = dent == 0.0 ? 1.0 : col[k] / dent;
+          G->cn[kk] = 1.0 / sqrt(n2);
+          G->cs[k] = ct;
+          G->sn[k] = snt;
+          Hc[k * m + k] = dent;
+          Hc[kk * m + k] = 0.0;
+          const double gk = G->g[k];
+          G->g[kk] = -snt * gk;
+          G->g[k] = ct * gk;
+          G->est = fabs(G->g[kk]);
+          G->k_done = kk;
+          G->status = 1;
+          reinterpret_cast<volatile int*>(a.host)[k] = 1;
+          __threadfence_system();
+          return;
+        }
+      }
       G->status = 3;
       reinterpret_cast<volatile int*>(a.host)[k] = 3;
       __threadfence_system();
