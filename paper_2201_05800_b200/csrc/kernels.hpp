@@ -407,8 +407,11 @@ bool offdiag_residual(double* out, const double* r, const double* y, const Spati
                       const MixCoef& mx, const Geometry& g, int nt, cudaStream_t s, Skip skip);
 bool sweep_supported(int nt, int n1);
 size_t sweep_work_doubles(int nt, int ncells, int n1);
+// vv (with partial): also <out, out> into *vv
 void precond_sweep(double* out, const double* in, const float* B, const float* G, double* work,
-                   int nt, int n1, int ncells, long long ns, cudaStream_t s, Skip skip);
+                   int nt, int n1, int ncells, long long ns, cudaStream_t s, Skip skip,
+                   double* partial = nullptr, double* vv = nullptr);
+unsigned* counter_of(double* partial);
 void precond_eblock_f32(double* out, const double* in, const float* B, int nt, int n1,
                         int ncells, long long ns, cudaStream_t s, Skip skip = {});
 

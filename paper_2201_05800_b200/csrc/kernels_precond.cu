@@ -16,6 +16,7 @@
 #include <type_traits>
 
 #include "kernels.hpp"
+#include "krylov.cuh"
 
 namespace stg {
 namespace {
@@ -310,13 +311,16 @@ __global__ void __launch_bounds__(256) k_eblock2(double* __restrict__ out,
 // Where the flow runs in -x the inflow coupling vanishes (dH/du_L = 0 without
 // jumps) and the sweep reduces to the element-block Jacobi there.
 constexpr int kSwCh = 256;   // owned elements per CTA (= threads)
-constexpr int kSwHalo = 32;  // upstream window
+constexpr int kSwHalo = 16;  // upstream window
 
+// vv != nullptr: also <z, z> into *vv (fixed-order block partials, the last
+// block finishes), which the following FD Jacobian action needs for its step
 template <int N1, int NT>
 __global__ void __launch_bounds__(kSwCh) k_sweep_win(double* __restrict__ out,
                                                      const double* __restrict__ y,
                                                      const float* __restrict__ G, int ncells,
-                                                     long long ns, Skip skip) {
+                                                     long long ns, Skip skip, double* part,
+                                                     double* vv, unsigned* counter) {
   pdl_entry();
   if (skip_now(skip)) return;
   constexpr int NB = N1 * NT, NE = kSwCh + kSwHalo;
@@ -369,6 +373,7 @@ __global__ void __launch_bounds__(kSwCh) k_sweep_win(double* __restrict__ out,
   // z_e = y_e - G_e s_{e-1}: per temporal node t, thread q of the chunk's
   // kSwCh * N1 nodes (coalesced); all loads of a batch issued first
   constexpr int PER = NT * kSwCh * N1 / kSwCh, BATCH = PER / 2;
+  double zz = 0.0;
 #pragma unroll
   for (int b0 = 0; b0 < PER; b0 += BATCH) {
     float4 g[BATCH];
@@ -397,8 +402,22 @@ __global__ void __launch_bounds__(kSwCh) k_sweep_win(double* __restrict__ out,
         z = fma(-double(g[b].z), Ss[il][2], z);
         z = fma(-double(g[b].w), Ss[il][3], z);
         out[t * ns + c * N1 + k] = z;
+        zz = fma(z, z, zz);
       }
     }
+  }
+  if (vv) {
+    __shared__ double red[kSwCh / 32];
+    const double w = warp_sum(zz);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = 0.0;
+#pragma unroll
+      for (int q = 0; q < kSwCh / 32; ++q) b += red[q];
+      part[blockIdx.x] = b;
+    }
+    if (is_last_block(counter)) block_finish_sum(part, gridDim.x, 1, vv, counter);
   }
 }
 
@@ -779,7 +798,8 @@ bool sweep_supported(int nt, int n1) {
 size_t sweep_work_doubles(int nt, int ncells, int n1) { return size_t(ncells) * n1 * nt; }
 
 void precond_sweep(double* out, const double* in, const float* B, const float* G, double* work,
-                   int nt, int n1, int ncells, long long ns, cudaStream_t s, Skip skip) {
+                   int nt, int n1, int ncells, long long ns, cudaStream_t s, Skip skip,
+                   double* partial, double* vv) {
   long long g = ((ncells + 1) / 2 + 7) / 8;
   if (g > 148 * 16) g = 148 * 16;
   const int nch = (ncells + kSwCh - 1) / kSwCh;
@@ -793,7 +813,8 @@ void precond_sweep(double* out, const double* in, const float* B, const float* G
       cudaFuncSetAttribute(k_sweep_win<N1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       set = true;
     }
-    launch_ex(kPdlPrecond, k_sweep_win<N1, 4>, nch, kSwCh, smem, s, out, work, G, ncells, ns, skip);
+    launch_ex(kPdlPrecond, k_sweep_win<N1, 4>, nch, kSwCh, smem, s, out, work, G, ncells, ns, skip,
+              partial, vv, partial ? counter_of(partial) : nullptr);
   };
   if (nt != 4) return;
   if (n1 == 4) go(std::integral_constant<int, 4>{});

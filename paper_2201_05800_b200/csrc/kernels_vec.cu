@@ -397,6 +397,12 @@ int grid_for(long long n) {
 
 }  // namespace
 
+// The completion counter lives right after the partial-sum area (see
+// kPartialDoubles in kernels.hpp); it is zero between launches.
+unsigned* counter_of(double* partial) {
+  return reinterpret_cast<unsigned*>(partial + kPartialDoubles);
+}
+
 int reduce_grid(long long n) { return grid_for(n); }
 
 // Vector kernels use PDL only below 4 Mi elements: there the launch latency
@@ -463,11 +469,6 @@ int multi_grid(long long n) {
   return int(std::max(1LL, std::min(g, (long long)cap)));
 }
 
-// The completion counter lives right after the partial-sum area (see
-// kPartialDoubles in kernels.hpp); it is zero between launches.
-unsigned* counter_of(double* partial) {
-  return reinterpret_cast<unsigned*>(partial + kPartialDoubles);
-}
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 

@@ -118,6 +118,9 @@ struct stg_handle {
   DevBuf sweepG, sweepW;      // d = 1 upwind sweep: couplings (fp32), y = B^-1 r
   DevBuf polyZ, polyW, polyQ;  // polynomial preconditioner: P0^-1 r, J y, P0^-1 J y
   bool block_exact = false;    // the last make_precond built an exact element-block inverse
+  // the vector whose <v, v> small[kVVSlot] holds (set by the preconditioner
+  // that wrote it, consumed by the next FD Jacobian action; reset per call)
+  const double* vv_of = nullptr;
   // d = 2 dense element block: the uploaded inverse and the mix it belongs to
   DevBuf etab;  // d = 1 advection element block (shared), keyed by mix
   stg::MixCoef etab_mix{};
@@ -194,6 +197,7 @@ void check_launch(stg_handle* h) {
 // step data; kRedSsSlot is where the deferred first GMRES cycle reads <b,b>)
 constexpr int kRedMaxSlot = 1010;
 constexpr int kRedSsSlot = 200;
+constexpr int kVVSlot = 1000;  // <v, v> of the FD Jacobian action's direction
 // Euler's admissibility flag (1 + first failing temporal block, set by the
 // rhs kernel) is raised as AdmissibilityError naming the temporal node
 // (stdg.hpp:41-50).  Outside a solve every apply checks it (one sync); inside
@@ -909,7 +913,7 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
     a.fdv = v;
     a.skip = h->skip;
     if (stg::fd_fused_supported(a)) {
-      double* vv = h->small.p + 1000;
+      double* vv = h->small.p + kVVSlot;
       if (un2 == kUUOnDevice) {
         a.fd_uu = h->small.p + kUUSlot;
         a.fd_c = fd_eps;
@@ -917,7 +921,9 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
         const double un = un2 >= 0.0 ? un2 : std::sqrt(dev_dot(h, U, U, n));
         a.fd_c = fd_eps * std::sqrt(1.0 + un);
       }
-      stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
+      if (v != h->vv_of)  // (else the preconditioner that produced v reduced it)
+        stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
+      h->vv_of = nullptr;
       a.fd_vv = vv;
       if (stg::launch_slab_generic(a, h->stream) < 0)
         throw std::runtime_error("fused FD Jacobian launch failed");
@@ -928,8 +934,9 @@ void fd_jvp(stg_handle* h, const stg::MixCoef& mix, bool full, const double* U, 
   }
   // central difference, the same two applies as a forward difference, O(h^2);
   // the step h is formed on the device from <v,v> (and <U,U>): no host sync
-  double* vv = h->small.p + 1000;
-  stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
+  double* vv = h->small.p + kVVSlot;
+  if (v != h->vv_of) stg::vec_dot(v, v, n, h->partial.p, vv, h->stream, h->skip);
+  h->vv_of = nullptr;
   const double* uu = nullptr;
   double c = fd_eps;
   if (un2 == kUUOnDevice) {
@@ -1877,8 +1884,12 @@ Op make_precond(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U
       h->sweepW.ensure(stg::sweep_work_doubles(nt, ncells, n1));
       const float* G = reinterpret_cast<const float*>(h->sweepG.p);
       double* wk = h->sweepW.p;
+      // the sweep also reduces <out, out> into the slot the FD Jacobian
+      // action reads its step from (fd_jvp skips its own dot for out)
       return [h, fb, G, wk, nt, n1, ncells, ns](const double* in, double* out) {
-        stg::precond_sweep(out, in, fb, G, wk, nt, n1, ncells, ns, h->stream, h->skip);
+        stg::precond_sweep(out, in, fb, G, wk, nt, n1, ncells, ns, h->stream, h->skip,
+                           h->partial.p, h->small.p + kVVSlot);
+        h->vv_of = out;
         h->launches += 2;
       };
     }
@@ -2151,8 +2162,10 @@ int guarded(stg_handle* h, F&& f) {
       cudaMemsetAsync(h->genFlag.p, 0, sizeof(int), h->stream);
     }
   };
+  if (h) h->vv_of = nullptr;  // no <v, v> carries over between calls
   try {
     f();
+    if (h) h->vv_of = nullptr;
     return STG_OK;
   } catch (const NonconvergenceError& e) {
     clear();
