@@ -93,14 +93,18 @@ __global__ void __launch_bounds__(256) k_eblock(double* __restrict__ out,
 // node q (neighbour inputs zero; neighbour STATES enter through the exact
 // linearisation).  Two elements per warp: lane (h, l) with l < NB owns row
 // l = (r, i) of element 2w + h's block and of the identity, in registers.
-// Gauss-Jordan with partial pivoting WITHOUT row exchanges: at column `col`
-// the unused lane of the half with the largest |a[col]| (lowest lane on
-// ties) becomes the pivot, normalises its row and publishes it through
-// shared memory (one 16-byte load per two entries for the other lanes,
-// instead of two 32-bit shuffles per entry); every other lane eliminates it.
-// At the end the pivot lane of column col holds row col of the inverse.
-// (One element per warp with shuffled rows took 853 us for the 65,536 c3
-// blocks.)
+// In-place Gauss-Jordan with partial pivoting WITHOUT row exchanges: at
+// column `col` the unused lane of the half with the largest |a[col]| (four
+// xor-shuffles of a key from the magnitude's top 28 bits and the lane,
+// lowest lane on ties) becomes the
+// pivot, normalises its row (the pivot entry becomes 1/pivot) and publishes
+// it through shared memory (one 16-byte load per two entries for the other
+// lanes); every other lane eliminates it (its own pivot-column entry
+// becomes -a[col]/pivot).  At the end the pivot lane of column col holds
+// row col of the inverse, its entry at position c' belonging to column
+// piv[c'].  (The augmented [A | I] version with a shuffle-tree pivot search
+// took 198 us for the 65,536 c3 blocks; one element per warp with shuffled
+// rows 853 us.)
 //
 // With G != nullptr it also forms the inflow coupling of the upwind sweep
 // (k_sweep_win): G_e = B_e^-1 L_e, where L_e is the block of the
@@ -117,7 +121,7 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
   pdl_entry();
   constexpr int NB = N1 * NT;
   static_assert(NB <= 16 && NB % 2 == 0, "two elements per warp, even block size");
-  constexpr int PS = 2 * NB + 4;  // published-row stride (doubles): halves on different banks
+  constexpr int PS = NB + 4;  // published-row stride (doubles): halves on different banks
   __shared__ __align__(16) double pub[4][2][PS];
   const int lane = threadIdx.x & 31, h = lane >> 4, l = lane & 15, wib = threadIdx.x >> 5;
   const int K = a.g.nx;
@@ -128,12 +132,25 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
   const int cl = ce == 0 ? K - 1 : ce - 1, cr = ce == K - 1 ? 0 : ce + 1;
   const bool act = l < NB;
   const int r = act ? l / N1 : 0, i = act ? l - (l / N1) * N1 : 0;
-  double row[NB], inv[NB], lin[NT];
+  double row[NB], lin[NT];
+  // row i of D by selects (a dynamic index into the parameter struct, or
+  // into u[], would go through local memory)
+  double dmi[N1];
+#pragma unroll
+  for (int k = 0; k < N1; ++k) {
+    double v = a.sp.Dm[0][k];
+#pragma unroll
+    for (int ii = 1; ii < N1; ++ii) v = i == ii ? a.sp.Dm[ii][k] : v;
+    dmi[k] = v;
+  }
 #pragma unroll
   for (int j = 0; j < NT; ++j) {
     double u[N1];
 #pragma unroll
     for (int k = 0; k < N1; ++k) u[k] = U[j * ns + (long long)ce * N1 + k];
+    double ui = u[0];
+#pragma unroll
+    for (int ii = 1; ii < N1; ++ii) ui = i == ii ? u[ii] : ui;
     const double ul = U[j * ns + (long long)cl * N1 + N1 - 1];
     const double ur = U[j * ns + (long long)cr * N1];
     {  // d/du_L of LLF(ul, u_0) at the left face: the inflow coupling l_{e,j}
@@ -142,99 +159,104 @@ __global__ void __launch_bounds__(128) k_build_burgers_eblock(float* __restrict_
                                  : 0.5 * ul + 0.5 * aR;
       lin[j] = a.sp.sc * a.sp.inv_w0 * dH;
     }
+    // d F_i(U_j) / d u_q, own element, neighbour states fixed:
+    //   -(2/h)/3 [ delta_iq sum_k D_ik (2 u_i + u_k) + D_iq (u_i + 2 u_q) ]
+    // plus, at q = i, the own-trace derivative of the face flux
+    double sdi = 0.0;
+#pragma unroll
+    for (int k = 0; k < N1; ++k) sdi = fma(dmi[k], 2.0 * ui + u[k], sdi);
+    double face = 0.0;
+    if (i == N1 - 1) {  // d/duL of LLF(uL, ur) - f(uL), right face
+      const double aL = fabs(u[N1 - 1]), aR = fabs(ur);
+      const double dH = aL >= aR ? 0.5 * u[N1 - 1] +
+                                       0.5 * (u[N1 - 1] >= 0 ? 1.0 : -1.0) * (u[N1 - 1] - ur) +
+                                       0.5 * aL
+                                 : 0.5 * u[N1 - 1] + 0.5 * aR;
+      face = -a.sp.sc * (dH - u[N1 - 1]) * a.sp.inv_wN;
+    }
+    if (i == 0) {  // d/duR of LLF(ul, uR) - f(uR), left face
+      const double aL = fabs(ul), aR = fabs(u[0]);
+      const double dH = aL >= aR ? 0.5 * u[0] - 0.5 * aL
+                                 : 0.5 * u[0] + 0.5 * (u[0] >= 0 ? 1.0 : -1.0) * (ul - u[0]) -
+                                       0.5 * aR;
+      face += a.sp.sc * (dH - u[0]) * a.sp.inv_w0;
+    }
+    const double trj = a.mx.T[r][j], srj = a.mx.S[r][j], c3 = -a.sp.sc * (1.0 / 3.0);
 #pragma unroll
     for (int q = 0; q < N1; ++q) {
-      // d F_i(U_j) / d u_q: own element, neighbour states fixed
-      double vol = 0.0;
-#pragma unroll
-      for (int k = 0; k < N1; ++k) {
-        const double dvi = (i == q ? 1.0 : 0.0), dvk = (k == q ? 1.0 : 0.0);
-        vol += a.sp.Dm[i][k] * ((2.0 * u[i] + u[k]) * dvi + (u[i] + 2.0 * u[k]) * dvk) * (1.0 / 3.0);
-      }
-      double g = -a.sp.sc * vol;
-      if (i == N1 - 1 && q == N1 - 1) {  // d/duL of LLF(uL, ur) - f(uL), right face
-        const double aL = fabs(u[N1 - 1]), aR = fabs(ur);
-        const double dH = aL >= aR
-                              ? 0.5 * u[N1 - 1] + 0.5 * (u[N1 - 1] >= 0 ? 1.0 : -1.0) *
-                                                      (u[N1 - 1] - ur) + 0.5 * aL
-                              : 0.5 * u[N1 - 1] + 0.5 * aR;
-        g -= a.sp.sc * (dH - u[N1 - 1]) * a.sp.inv_wN;
-      }
-      if (i == 0 && q == 0) {  // d/duR of LLF(ul, uR) - f(uR), left face
-        const double aL = fabs(ul), aR = fabs(u[0]);
-        const double dH = aL >= aR ? 0.5 * u[0] - 0.5 * aL
-                                   : 0.5 * u[0] + 0.5 * (u[0] >= 0 ? 1.0 : -1.0) * (ul - u[0]) -
-                                         0.5 * aR;
-        g += a.sp.sc * (dH - u[0]) * a.sp.inv_w0;
-      }
-      row[j * N1 + q] = act ? (i == q ? a.mx.T[r][j] : 0.0) + a.mx.S[r][j] * g : 0.0;
+      double g = c3 * ((i == q ? sdi : 0.0) + dmi[q] * (ui + 2.0 * u[q]));
+      if (i == q) g += face;
+      row[j * N1 + q] = act ? (i == q ? trj : 0.0) + srj * g : 0.0;
     }
   }
-#pragma unroll
-  for (int q = 0; q < NB; ++q) inv[q] = (q == l) ? 1.0 : 0.0;
+  // in-place Gauss-Jordan: row[] becomes the lane's row of (P B)^-1, P the
+  // pivot order (no row exchanges: the pivot lane of column col ends up with
+  // row col of B^-1, its entry at position c' belonging to column piv[c'])
   bool used = !act;
   int my_col = 0;
+  int piv[NB];
   double* P = pub[wib][h];
 #pragma unroll
   for (int col = 0; col < NB; ++col) {
-    // pivot lane of this half: max |row[col]| among unused lanes, lowest lane on ties
-    double v = used ? -1.0 : fabs(row[col]);
-    int idx = l;
+    // pivot lane of this half: the largest |row[col]| among unused lanes by
+    // the top 28 bits of the magnitude (ties in those bits -- a relative
+    // difference below 2^-16 -- go to the lowest lane)
+    // key: magnitude's top 28 bits above (15 - lane): unique per lane, the
+    // lowest lane wins ties; a max over the half by four xor-shuffles
+    unsigned key =
+        used ? 0u
+             : ((unsigned((unsigned long long)__double_as_longlong(fabs(row[col])) >> 32) & ~15u) |
+                unsigned(15 - l));
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-      const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-      const int i2 = __shfl_xor_sync(0xffffffffu, idx, o);
-      if (v2 > v || (v2 == v && i2 < idx)) {
-        v = v2;
-        idx = i2;
-      }
-    }
-    const double f = row[col];
-    // block columns <= col are finished (never read again), so only the
-    // entries right of the pivot column and the identity part are updated
-    const int qa = (col + 1) & ~1;  // first updated pair (col: unrolled constant)
+    for (int o = 8; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+    const int idx = 15 - int(key & 15u);
+    piv[col] = idx;
     if (l == idx) {
-      const double ip = 1.0 / f;
+      // fp32 seed + two Newton steps: fp64-accurate, no division sequence
+      const double pv = row[col];
+      double ip = double(__frcp_rn(float(pv)));
+      ip = ip * fma(-pv, ip, 2.0);
+      ip = ip * fma(-pv, ip, 2.0);
 #pragma unroll
-      for (int q = 0; q < NB; ++q) {
-        if (q > col) row[q] *= ip;
-        inv[q] *= ip;
-      }
+      for (int q = 0; q < NB; ++q) row[q] = q == col ? ip : row[q] * ip;
 #pragma unroll
-      for (int q = 0; q < NB; q += 2) {
-        if (q >= qa) *reinterpret_cast<double2*>(P + q) = make_double2(row[q], row[q + 1]);
-        *reinterpret_cast<double2*>(P + NB + q) = make_double2(inv[q], inv[q + 1]);
-      }
+      for (int q = 0; q < NB; q += 2)
+        *reinterpret_cast<double2*>(P + q) = make_double2(row[q], row[q + 1]);
       used = true;
       my_col = col;
     }
     __syncwarp();
     if (l != idx) {
+      const double f = row[col];
 #pragma unroll
       for (int q = 0; q < NB; q += 2) {
-        if (q >= qa) {
-          const double2 pr = *reinterpret_cast<const double2*>(P + q);
-          row[q] = fma(-f, pr.x, row[q]);
-          row[q + 1] = fma(-f, pr.y, row[q + 1]);
-        }
-        const double2 pi = *reinterpret_cast<const double2*>(P + NB + q);
-        inv[q] = fma(-f, pi.x, inv[q]);
-        inv[q + 1] = fma(-f, pi.y, inv[q + 1]);
+        const double2 pr = *reinterpret_cast<const double2*>(P + q);
+        row[q] = q == col ? -f * pr.x : fma(-f, pr.x, row[q]);
+        row[q + 1] = q + 1 == col ? -f * pr.y : fma(-f, pr.y, row[q + 1]);
       }
     }
     __syncwarp();  // the published row is consumed before the next pivot writes
   }
   if (act && live) {  // stored in fp32: a preconditioner; GMRES itself stays fp64
+    // the pivot lane of column c owns the identity column of row piv[c]
     float* M = Binv + (size_t)c * NB * NB + (size_t)my_col * NB;
 #pragma unroll
-    for (int q = 0; q < NB; q += 2) *reinterpret_cast<float2*>(M + q) = make_float2(float(inv[q]), float(inv[q + 1]));
-    if (G) {  // row my_col of B_e^-1 L_e
+    for (int q = 0; q < NB; ++q) M[piv[q]] = float(row[q]);
+    if (G) {  // row my_col of B_e^-1 L_e (entries of B_e^-1 at columns (r, node 0))
+      double b0[NT];
+#pragma unroll
+      for (int r2 = 0; r2 < NT; ++r2) {
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) v = piv[q] == r2 * N1 ? row[q] : v;
+        b0[r2] = v;
+      }
       float* Gr = G + ((size_t)c * NB + my_col) * NT;
 #pragma unroll
       for (int j = 0; j < NT; ++j) {
         double acc = 0.0;
 #pragma unroll
-        for (int r2 = 0; r2 < NT; ++r2) acc = fma(inv[r2 * N1], a.mx.S[r2][j], acc);
+        for (int r2 = 0; r2 < NT; ++r2) acc = fma(b0[r2], a.mx.S[r2][j], acc);
         Gr[j] = float(acc * lin[j]);
       }
     }
