@@ -423,12 +423,29 @@ def run_ours(args):
     torch.cuda.synchronize()
     pg_s = (time.perf_counter() - t0) / max(3, e2e_steps // 5)
 
-    # this box's PCIe rates for the same pinned buffers (the e2e bound)
+    # this box's PCIe rates for the same pinned buffers (the e2e bound): one
+    # way each, and the e2e call's bytes (U + u_n in, R out) both ways at once
     pcie = {}
     try:
         dU = torch.empty(cfg.n_dof, dtype=torch.float64, device=dev)
+        dR = torch.empty(cfg.n_dof, dtype=torch.float64, device=dev)
+        dun = torch.empty(cfg.n_sdof, dtype=torch.float64, device=dev)
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+
+        def duplex():
+            s_in.wait_stream(stream)
+            s_out.wait_stream(stream)
+            with torch.cuda.stream(s_in):
+                dU.copy_(pin_U, non_blocking=True)
+                dun.copy_(pin_un, non_blocking=True)
+            with torch.cuda.stream(s_out):
+                pin_R.copy_(dR, non_blocking=True)
+            stream.wait_stream(s_in)
+            stream.wait_stream(s_out)
+
         for name, fn in (("h2d_GBps", lambda: dU.copy_(pin_U, non_blocking=True)),
-                         ("d2h_GBps", lambda: pin_R.copy_(dU, non_blocking=True))):
+                         ("d2h_GBps", lambda: pin_R.copy_(dU, non_blocking=True)),
+                         ("duplex_ms_e2e_bytes", duplex)):
             fn()
             torch.cuda.synchronize()
             ev0.record(stream)
@@ -436,8 +453,10 @@ def run_ours(args):
                 fn()
             ev1.record(stream)
             torch.cuda.synchronize()
-            pcie[name] = 5 * 8 * cfg.n_dof / (ev0.elapsed_time(ev1) * 1e-3) / 1e9
-        del dU
+            ms5 = ev0.elapsed_time(ev1) / 5
+            pcie[name] = ms5 if name.endswith("_ms_e2e_bytes") else 8 * cfg.n_dof / (ms5 * 1e-3) / 1e9
+        pcie["e2e_ms_per_call"] = e2e_ms / e2e_steps
+        del dU, dR, dun
     except Exception as e:  # report, do not fail the bench
         pcie = {"unavailable": str(e)}
 
