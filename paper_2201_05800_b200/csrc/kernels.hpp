@@ -315,11 +315,20 @@ bool fdm3_supported(const Geometry& g, int n_tau);
 // with od, fdm3_kernel computes out = P0^-1 (in - L y) (L: the upwind face
 // terms cL / cR of the constant-velocity advection Jacobian, mixed by the
 // diagonal S), reading y's neighbour traces while it stages each row.
+// The neighbour traces travel between the chain's steps in a compact array
+// instead of the full iterate: trace[a][t][cell][16] holds, per axis a, the
+// face of the cell its downstream neighbour reads (i_a = N for cL_a != 0,
+// i_a = 0 for cR_a != 0): x [z][iy], y [z][ix], z [iy][ix].
 struct FdmOffdiag {
-  const double* y;
+  const double* tr_in;  // traces of y_i (nullptr: no coupling, the plain block apply)
+  double* tr_out;       // traces of the result (nullptr: none)
+  int full_out;         // 0: the result itself is not stored (an intermediate term)
   double S[4];          // diagonal of the temporal mix S
   double cL[3], cR[3];  // SpatialCoef face coefficients
 };
+inline long long fdm_trace_doubles(const Geometry& g, int nt) {
+  return 3LL * nt * g.n_cells * 16;
+}
 int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const Geometry& g,
                         const double* in, double* out, cudaStream_t s, Skip skip = {},
                         const FdmOffdiag* od = nullptr);

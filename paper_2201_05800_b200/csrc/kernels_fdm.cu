@@ -381,39 +381,34 @@ __device__ __forceinline__ void fdm3_row_prefetch(RowTr& tr, const FdmOffdiag& o
     const int t = row / (f3::E * 4), e = (row >> 2) & (f3::E - 1), z = row & 3;
     const int cell = seg * f3::E + e;
     const int cx = cell % g.nx, cy = (cell / g.nx) % g.ny, cz = cell / (g.nx * g.ny);
-    const double* yt = od.y + t * g.n_sdof;
+    const long long plane = (long long)4 * g.n_cells * 16;  // one axis' traces
+    const double* tt = od.tr_in + (long long)t * g.n_cells * 16;
+    auto ld4 = [](const double* p, double (&v)[4]) {
+      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+      const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+      v[0] = a.x;
+      v[1] = a.y;
+      v[2] = b.x;
+      v[3] = b.y;
+    };
 #pragma unroll
     for (int q = 0; q < 4; ++q) tr.x[q] = tr.y[q] = tr.z[q] = 0.0;
-    if (od.cL[0] != 0.0 || od.cR[0] != 0.0) {  // x- (ix = 3) or x+ (ix = 0) neighbour line
+    if (od.cL[0] != 0.0 || od.cR[0] != 0.0) {  // the x-neighbour's face line z: [z][iy]
       const bool L = od.cL[0] != 0.0;
       const int dc = L ? (cx == 0 ? g.nx - 1 : -1) : (cx == g.nx - 1 ? 1 - g.nx : 1);
-      const double* p = yt + (long long)(cell + dc) * 64 + z * 16 + (L ? 3 : 0);
-#pragma unroll
-      for (int iy = 0; iy < 4; ++iy) tr.x[iy] = __ldg(p + 4 * iy);
+      ld4(tt + (long long)(cell + dc) * 16 + z * 4, tr.x);
     }
-    if (od.cL[1] != 0.0 || od.cR[1] != 0.0) {  // y- (iy = 3) or y+ (iy = 0) neighbour line
+    if (od.cL[1] != 0.0 || od.cR[1] != 0.0) {  // the y-neighbour's face line z: [z][ix]
       const bool L = od.cL[1] != 0.0;
       const int dc = L ? (cy == 0 ? (g.ny - 1) * g.nx : -g.nx)
                        : (cy == g.ny - 1 ? -(g.ny - 1) * g.nx : g.nx);
-      const double2* p =
-          reinterpret_cast<const double2*>(yt + (long long)(cell + dc) * 64 + z * 16 + (L ? 12 : 0));
-      const double2 a = __ldg(p), b = __ldg(p + 1);
-      tr.y[0] = a.x;
-      tr.y[1] = a.y;
-      tr.y[2] = b.x;
-      tr.y[3] = b.y;
+      ld4(tt + plane + (long long)(cell + dc) * 16 + z * 4, tr.y);
     }
-    if (od.cL[2] != 0.0 || od.cR[2] != 0.0) {  // line z of the z- (iz = 3) / z+ (iz = 0) plane
+    if (od.cL[2] != 0.0 || od.cR[2] != 0.0) {  // line iy = z of the z-neighbour's face
       const bool L = od.cL[2] != 0.0;
       const long long pl = (long long)g.nx * g.ny;
       const long long dc = L ? (cz == 0 ? (g.nz - 1) * pl : -pl) : (cz == g.nz - 1 ? -(g.nz - 1) * pl : pl);
-      const double2* p =
-          reinterpret_cast<const double2*>(yt + (cell + dc) * 64 + (L ? 48 : 0) + 4 * z);
-      const double2 a = __ldg(p), b = __ldg(p + 1);
-      tr.z[0] = a.x;
-      tr.z[1] = a.y;
-      tr.z[2] = b.x;
-      tr.z[3] = b.y;
+      ld4(tt + 2 * plane + (cell + dc) * 16 + z * 4, tr.z);
     }
   }
 }
@@ -507,7 +502,9 @@ __device__ __forceinline__ void fdm3_fwd_row(const FdmCoef3& c, double* X, int r
 
 // phase A' on one row: inverse y and x (2 Re, the 2 folded into IX), in place
 template <bool PARAM>
-__device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int row) {
+__device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int row,
+                                             const FdmOffdiag& od, const Geometry& g, int seg,
+                                             bool trace_out, bool full_out) {
   const int sw = row & 7;
   C2 s[2][2], d[2][2];  // [P][j]: sum and difference of the pair members
 #pragma unroll
@@ -542,6 +539,34 @@ __device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int r
       o[4 * y + x] = re;
     }
   }
+  if (trace_out) {  // the faces the downstream neighbours read (FdmOffdiag)
+    const int t = row / (f3::E * 4), e = (row >> 2) & (f3::E - 1), z = row & 3;
+    const long long cell = (long long)seg * f3::E + e;
+    const long long plane = (long long)4 * g.n_cells * 16;
+    double* tt = od.tr_out + (long long)t * g.n_cells * 16 + cell * 16;
+    auto st4 = [](double* p, double a0, double a1, double a2, double a3) {
+      reinterpret_cast<double2*>(p)[0] = make_double2(a0, a1);
+      reinterpret_cast<double2*>(p)[1] = make_double2(a2, a3);
+    };
+    // (constant indices into o[] in both branches: a runtime index would put
+    // o in local memory)
+    if (od.cL[0] != 0.0)
+      st4(tt + z * 4, o[3], o[7], o[11], o[15]);
+    else if (od.cR[0] != 0.0)
+      st4(tt + z * 4, o[0], o[4], o[8], o[12]);
+    if (od.cL[1] != 0.0)
+      st4(tt + plane + z * 4, o[12], o[13], o[14], o[15]);
+    else if (od.cR[1] != 0.0)
+      st4(tt + plane + z * 4, o[0], o[1], o[2], o[3]);
+    if (od.cL[2] != 0.0 || od.cR[2] != 0.0) {
+      if (z == (od.cL[2] != 0.0 ? 3 : 0)) {
+#pragma unroll
+        for (int iy = 0; iy < 4; ++iy)
+          st4(tt + 2 * plane + iy * 4, o[4 * iy], o[4 * iy + 1], o[4 * iy + 2], o[4 * iy + 3]);
+      }
+    }
+  }
+  if (!full_out) return;
 #pragma unroll
   for (int q = 0; q < 8; ++q)
     *reinterpret_cast<double2*>(X + row * 16 + ((q ^ sw) << 1)) = make_double2(o[2 * q], o[2 * q + 1]);
@@ -678,11 +703,13 @@ __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
     __syncthreads();
     fdm3_unit<PARAM>(c, cs, X, eB, qB);
     __syncthreads();
+    const bool tr_out = od.tr_out != nullptr, full = od.full_out != 0 || !od.tr_out;
 #pragma unroll(f3::kRowUnroll)
-    for (int k = 0; k < 2; ++k) fdm3_inv_row<PARAM>(c, X, tid + k * f3::THREADS);
+    for (int k = 0; k < 2; ++k)
+      fdm3_inv_row<PARAM>(c, X, tid + k * f3::THREADS, od, g, seg, tr_out, full);
     ptxh::fence_proxy_async_smem();
     __syncthreads();  // result tile complete
-    if (tid == 0) {
+    if (full && tid == 0) {
       ptxh::tma_store_4d(&tm_out, ptxh::smem_u32(X), 0, 0, seg * f3::E, 0);
       ptxh::bulk_commit();
     }
@@ -1237,8 +1264,9 @@ int launch_precond_fdm3(const FdmCoef3* coef, const FdmCoef3& host_coef, const G
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return -1;
   static const bool smem_coef = std::getenv("STG_FDM3_SMEMC") != nullptr;
-  auto kern = od ? (smem_coef ? fdm3_kernel<false, true> : fdm3_kernel<true, true>)
-                 : (smem_coef ? fdm3_kernel<false, false> : fdm3_kernel<true, false>);
+  const bool coupled = od && od->tr_in;
+  auto kern = coupled ? (smem_coef ? fdm3_kernel<false, true> : fdm3_kernel<true, true>)
+                      : (smem_coef ? fdm3_kernel<false, false> : fdm3_kernel<true, false>);
   static int occ_dev[kMaxDevices];
   const int dev = device_slot();
   int& occ = occ_dev[dev];

@@ -1943,17 +1943,28 @@ Op precond_for(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U,
     }
     const stg::FdmCoef3* c = reinterpret_cast<const stg::FdmCoef3*>(h->fdm3M.p);
     const stg::FdmCoef3* hc = h->fdm3_host.get();
-    return [h, P0, m, od, c, hc, z](const double* r, double* y) {
-      double* buf[2] = {z, y};
-      int cur = (m & 1) ? 0 : 1;  // the last term lands in y
-      P0(r, buf[cur]);
+    // intermediate terms exist only as their face traces (compact, ping-pong
+    // in z): the first apply and every coupled step but the last write the
+    // traces alone, the last writes the result
+    const long long nt3 = stg::fdm_trace_doubles(h->g, h->nt);
+    h->polyZ.ensure(size_t(2 * nt3));
+    double* tr[2] = {h->polyZ.p, h->polyZ.p + nt3};
+    return [h, m, od, c, hc, tr](const double* r, double* y) {
+      stg::FdmOffdiag o = od;
+      o.tr_in = nullptr;
+      o.tr_out = tr[0];
+      o.full_out = 0;
+      if (stg::launch_precond_fdm3(c, *hc, h->g, r, y, h->stream, h->skip, &o) < 0)
+        throw std::runtime_error("element-block preconditioner launch failed");
+      h->launches++;
       for (int i = 0; i < m; ++i) {
-        stg::FdmOffdiag o = od;
-        o.y = buf[cur];
-        if (stg::launch_precond_fdm3(c, *hc, h->g, r, buf[cur ^ 1], h->stream, h->skip, &o) < 0)
+        const bool last = i + 1 == m;
+        o.tr_in = tr[i & 1];
+        o.tr_out = last ? nullptr : tr[(i + 1) & 1];
+        o.full_out = last ? 1 : 0;
+        if (stg::launch_precond_fdm3(c, *hc, h->g, r, y, h->stream, h->skip, &o) < 0)
           throw std::runtime_error("element-block preconditioner launch failed");
         h->launches++;
-        cur ^= 1;
       }
     };
   }
