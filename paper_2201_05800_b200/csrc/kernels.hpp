@@ -369,9 +369,21 @@ struct FdmCoef2i {
 };
 static_assert(sizeof(FdmCoef2i) % 16 == 0, "bulk-copied block");
 bool fdm2i_supported(const Geometry& g, int n_tau, int nr, int np);
+// d = 2 analogue of FdmOffdiag for fdm2i_kernel: trace[a][t][cell][n]
+// holds the face line its downstream neighbour reads (x: [iy], y: [ix]).
+struct FdmOffdiag2 {
+  const double* tr_in;
+  double* tr_out;
+  int full_out;
+  double S[kFdm2MaxN];
+  double cL[2], cR[2];
+};
+inline long long fdm2_trace_doubles(const Geometry& g, int nt) {
+  return 2LL * nt * g.n_cells * g.n1;
+}
 int launch_precond_fdm2i(const FdmCoef2i* coef, const FdmCoef2i& host_coef, const Geometry& g,
                          int n_tau, const double* in, double* out, cudaStream_t s,
-                         Skip skip = {});
+                         Skip skip = {}, const FdmOffdiag2* od = nullptr);
 
 // n1 / n_tau / (real, pair) x-mode counts the kernel is instantiated for
 bool fdm2_supported(const Geometry& g, int n_tau, int nr, int np);

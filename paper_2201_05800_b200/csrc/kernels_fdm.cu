@@ -963,11 +963,13 @@ struct Shape {
 };
 }  // namespace f2i
 
-template <int N1, int NT, int NR, int NP>
+// OD: P0^-1 (in - L y) with y's faces from od.tr_in (FdmOffdiag2); with
+// od.tr_out the result's faces are written, with !od.full_out only those
+template <int N1, int NT, int NR, int NP, bool OD>
 __global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
     fdm2i_kernel(const double* __restrict__ in, double* __restrict__ out,
                  const FdmCoef2i* __restrict__ coef, const __grid_constant__ FdmCoef2i c,
-                 const Geometry g, const Skip skip) {
+                 const Geometry g, const Skip skip, const FdmOffdiag2 od) {
   using S = f2i::Shape<N1, NT, NR, NP>;
   constexpr int NPC = S::NPC, KY = S::KY, E = f2i::E;
   extern __shared__ __align__(128) unsigned char smem2i[];
@@ -1017,6 +1019,26 @@ __global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
       ptxh::fence_proxy_async_smem();
       issue(seg + gridDim.x, st ^ 1);
     }
+    const int cell = seg * E + eA;
+    double trx[N1], try_[N1];  // the upwind neighbours' face lines (OD)
+    if constexpr (OD) {
+      const int cx = cell % g.nx, cy = cell / g.nx;
+      const double* tt = od.tr_in + (long long)tA * g.n_cells * N1;
+      const long long plane = (long long)NT * g.n_cells * N1;
+#pragma unroll
+      for (int q = 0; q < N1; ++q) trx[q] = try_[q] = 0.0;
+      if (od.cL[0] != 0.0 || od.cR[0] != 0.0) {
+        const int dc = od.cL[0] != 0.0 ? (cx == 0 ? g.nx - 1 : -1) : (cx == g.nx - 1 ? 1 - g.nx : 1);
+#pragma unroll
+        for (int q = 0; q < N1; ++q) trx[q] = __ldg(tt + (long long)(cell + dc) * N1 + q);
+      }
+      if (od.cL[1] != 0.0 || od.cR[1] != 0.0) {
+        const int dc = od.cL[1] != 0.0 ? (cy == 0 ? (g.ny - 1) * g.nx : -g.nx)
+                                       : (cy == g.ny - 1 ? -(g.ny - 1) * g.nx : g.nx);
+#pragma unroll
+        for (int q = 0; q < N1; ++q) try_[q] = __ldg(tt + plane + (long long)(cell + dc) * N1 + q);
+      }
+    }
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
     double* pl = X + (tA * E + eA) * NPC;
@@ -1025,6 +1047,27 @@ __global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
       double u[NPC];
 #pragma unroll
       for (int k = 0; k < NPC; ++k) u[k] = pl[k];
+      if constexpr (OD) {  // minus the neighbour couplings: S(t,t) (cL / cR) face terms
+        double sd = od.S[0];
+#pragma unroll
+        for (int q = 1; q < NT; ++q) sd = tA == q ? od.S[q] : sd;
+        if (od.cL[0] != 0.0) {
+#pragma unroll
+          for (int y = 0; y < N1; ++y) u[y * N1] = fma(-sd * od.cL[0], trx[y], u[y * N1]);
+        } else if (od.cR[0] != 0.0) {
+#pragma unroll
+          for (int y = 0; y < N1; ++y)
+            u[y * N1 + N1 - 1] = fma(-sd * od.cR[0], trx[y], u[y * N1 + N1 - 1]);
+        }
+        if (od.cL[1] != 0.0) {
+#pragma unroll
+          for (int x = 0; x < N1; ++x) u[x] = fma(-sd * od.cL[1], try_[x], u[x]);
+        } else if (od.cR[1] != 0.0) {
+#pragma unroll
+          for (int x = 0; x < N1; ++x)
+            u[(N1 - 1) * N1 + x] = fma(-sd * od.cR[1], try_[x], u[(N1 - 1) * N1 + x]);
+        }
+      }
       double ar[NR][N1];  // real x-modes, per y
       C2 ac[NP][N1];      // complex x-modes, per y
 #pragma unroll
@@ -1116,6 +1159,7 @@ __global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
     }
     __syncthreads();
     // ---- phase A': inverse y then x, in place -------------------------------
+    const bool full = od.full_out != 0 || !od.tr_out;
     {
       double h[NPC];
 #pragma unroll
@@ -1145,6 +1189,7 @@ __global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
           }
           mc[p] = b;
         }
+        double orow[N1];
 #pragma unroll
         for (int x = 0; x < N1; ++x) {
           double o = 0.0;
@@ -1153,13 +1198,24 @@ __global__ void __launch_bounds__(f2i::Shape<N1, NT, NR, NP>::THREADS, 3)
 #pragma unroll
           for (int p = 0; p < NP; ++p)
             o = fma(c.IX[x][NR + p][0], mc[p].r, fma(-c.IX[x][NR + p][1], mc[p].i, o));
-          pl[y * N1 + x] = o;
+          orow[x] = o;
+          if (full) pl[y * N1 + x] = o;
+        }
+        if (od.tr_out) {  // the faces the downstream neighbours read
+          double* tt = od.tr_out + ((long long)tA * g.n_cells + cell) * N1;
+          const long long plane = (long long)NT * g.n_cells * N1;
+          if (od.cL[0] != 0.0) tt[y] = orow[N1 - 1];
+          else if (od.cR[0] != 0.0) tt[y] = orow[0];
+          if ((od.cL[1] != 0.0 && y == N1 - 1) || (od.cR[1] != 0.0 && y == 0)) {
+#pragma unroll
+            for (int x = 0; x < N1; ++x) tt[plane + x] = orow[x];
+          }
         }
       }
     }
     ptxh::fence_proxy_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (full && tid == 0) {
       const uint32_t src = ptxh::smem_u32(X);
       double* dst = out + (long long)seg * E * NPC;
       for (int t = 0; t < NT; ++t) ptxh::bulk_s2g_1d(dst + t * ns, src + t * PB, PB);
@@ -1343,16 +1399,17 @@ bool fdm2i_supported(const Geometry& g, int n_tau, int nr, int np) {
 namespace {
 template <int N1, int NT, int NR, int NP>
 int launch_fdm2i_t(const FdmCoef2i* coef, const FdmCoef2i& hc, const Geometry& g,
-                   const double* in, double* out, cudaStream_t s, Skip skip) {
+                   const double* in, double* out, cudaStream_t s, Skip skip,
+                   const FdmOffdiag2* od) {
   using S = f2i::Shape<N1, NT, NR, NP>;
   static int occ_dev[kMaxDevices];
   const int dev = device_slot();
   int& occ = occ_dev[dev];
   if (occ <= 0) {
-    cudaFuncSetAttribute(fdm2i_kernel<N1, NT, NR, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         S::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fdm2i_kernel<N1, NT, NR, NP>, S::THREADS,
-                                                  S::SMEM);
+    for (auto k : {fdm2i_kernel<N1, NT, NR, NP, false>, fdm2i_kernel<N1, NT, NR, NP, true>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, S::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fdm2i_kernel<N1, NT, NR, NP, true>,
+                                                  S::THREADS, S::SMEM);
     if (occ < 1) occ = 1;
   }
   int sms = 148;
@@ -1360,17 +1417,20 @@ int launch_fdm2i_t(const FdmCoef2i* coef, const FdmCoef2i& hc, const Geometry& g
   const int nseg = g.n_cells / f2i::E;
   int grid = occ * sms;
   if (grid > nseg) grid = nseg;
-  launch_ex(kPdlFdm, fdm2i_kernel<N1, NT, NR, NP>, grid, S::THREADS, S::SMEM, s, in, out, coef,
-            hc, g, skip);
+  auto kern = od && od->tr_in ? fdm2i_kernel<N1, NT, NR, NP, true>
+                              : fdm2i_kernel<N1, NT, NR, NP, false>;
+  launch_ex(kPdlFdm, kern, grid, S::THREADS, S::SMEM, s, in, out, coef, hc, g, skip,
+            od ? *od : FdmOffdiag2{});
   return 1;
 }
 }  // namespace
 
 int launch_precond_fdm2i(const FdmCoef2i* coef, const FdmCoef2i& hc, const Geometry& g, int n_tau,
-                         const double* in, double* out, cudaStream_t s, Skip skip) {
+                         const double* in, double* out, cudaStream_t s, Skip skip,
+                         const FdmOffdiag2* od) {
   if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return -1;
-  if (g.n1 == 5 && n_tau == 5) return launch_fdm2i_t<5, 5, 1, 2>(coef, hc, g, in, out, s, skip);
-  if (g.n1 == 3 && n_tau == 3) return launch_fdm2i_t<3, 3, 1, 1>(coef, hc, g, in, out, s, skip);
+  if (g.n1 == 5 && n_tau == 5) return launch_fdm2i_t<5, 5, 1, 2>(coef, hc, g, in, out, s, skip, od);
+  if (g.n1 == 3 && n_tau == 3) return launch_fdm2i_t<3, 3, 1, 1>(coef, hc, g, in, out, s, skip, od);
   return -1;
 }
 

@@ -1968,6 +1968,41 @@ Op precond_for(stg_handle* h, int kind, const stg::MixCoef& mx, const double* U,
       }
     };
   }
+  // d = 2 with the in-place FDM blocks: the same with fdm2i_kernel
+  if (h->block_exact && h->desc.dim == 2 && h->fdm2i_valid &&
+      std::memcmp(&h->fdm2i_mix, &mx, sizeof mx) == 0 && s_diag && !generic && !no_fused &&
+      h->nt <= stg::kFdm2MaxN) {
+    stg::FdmOffdiag2 od{};
+    for (int t = 0; t < h->nt; ++t) od.S[t] = mx.S[t][t];
+    for (int a = 0; a < 2; ++a) {
+      od.cL[a] = h->sp.cL[a];
+      od.cR[a] = h->sp.cR[a];
+    }
+    const stg::FdmCoef2i* c = reinterpret_cast<const stg::FdmCoef2i*>(h->fdm2iM.p);
+    const stg::FdmCoef2i* hc = h->fdm2i_host.get();
+    const long long nt2 = stg::fdm2_trace_doubles(h->g, h->nt);
+    h->polyZ.ensure(size_t(2 * nt2));
+    double* tr[2] = {h->polyZ.p, h->polyZ.p + nt2};
+    const int nt = h->nt;
+    return [h, m, od, c, hc, tr, nt](const double* r, double* y) {
+      stg::FdmOffdiag2 o = od;
+      o.tr_in = nullptr;
+      o.tr_out = tr[0];
+      o.full_out = 0;
+      if (stg::launch_precond_fdm2i(c, *hc, h->g, nt, r, y, h->stream, h->skip, &o) < 0)
+        throw std::runtime_error("element-block preconditioner launch failed");
+      h->launches++;
+      for (int i = 0; i < m; ++i) {
+        const bool last = i + 1 == m;
+        o.tr_in = tr[i & 1];
+        o.tr_out = last ? nullptr : tr[(i + 1) & 1];
+        o.full_out = last ? 1 : 0;
+        if (stg::launch_precond_fdm2i(c, *hc, h->g, nt, r, y, h->stream, h->skip, &o) < 0)
+          throw std::runtime_error("element-block preconditioner launch failed");
+        h->launches++;
+      }
+    };
+  }
   if (h->block_exact && stg::offdiag_supported(h->g, h->nt) && !generic) {
     const stg::MixCoef mj = mx;
     return [h, P0, m, mj, z](const double* r, double* y) {
