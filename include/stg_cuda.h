@@ -103,10 +103,10 @@ extern "C" {
 #define STG_PRECOND_SWEEP 5
 /* Polynomial (Neumann) preconditioner over the element-block Jacobi P0 = the
  * EBLOCK (or, d = 1 Burgers, SWEEP) choice:
- *   P^-1 = sum_{i=0..m} (I - P0^-1 J)^i P0^-1,  m = 3 (env STG_POLY_TERMS)
+ *   P^-1 = sum_{i=0..m} (I - P0^-1 J)^i P0^-1,  m = 7 (env STG_POLY_TERMS)
  * applied as y_0 = z = P0^-1 r, y_{i+1} = z + y_i - P0^-1 J y_i: m Jacobian
  * actions and m + 1 block applies per GMRES step, in exchange for fewer
- * GMRES steps (c4: 7 -> 2) and their quadratically growing Gram-Schmidt
+ * GMRES steps (c4: 7 -> 1) and their quadratically growing Gram-Schmidt
  * passes.  Any model whose EBLOCK exists. */
 #define STG_PRECOND_POLY 6
 

@@ -1306,11 +1306,16 @@ bool gen_eblock_ok(const stg_handle* h) {
   return h->desc.model == STG_MODEL_ADVDIFF && h->nt * h->g.npc * h->r <= 32;
 }
 
-// Neumann terms of STG_PRECOND_POLY (env STG_POLY_TERMS, default 3)
+// Neumann terms of STG_PRECOND_POLY (env STG_POLY_TERMS, default 7).  With
+// the couplings fused into the block apply a term costs ~50 us at c4 size
+// against ~100 us for a GMRES step's operator apply and Gram-Schmidt passes:
+// m = 7 converges c4, c2 and c5 in one GMRES step at 1e-10 (c4 / c2 / c5
+// slab solves 0.72 / 0.68 / 0.82 ms; m = 3: two steps, 0.81 / 0.78 / 0.91;
+// m = 6 takes c4 alone to one step, 0.67 ms, but c2 and c5 to two)
 int poly_terms() {
   static const int m = [] {
     const char* e = std::getenv("STG_POLY_TERMS");
-    const int v = e ? std::atoi(e) : 3;
+    const int v = e ? std::atoi(e) : 7;
     return v < 0 ? 0 : v;
   }();
   return m;

@@ -16,7 +16,7 @@ from paper_2201_05800_b200.api import NewtonConfig, SlabOperator  # noqa: E402
 
 names = sys.argv[1:] or ["c4", "c2", "c5", "c3"]
 pcs = {"auto": L.STG_PRECOND_AUTO, "poly": L.STG_PRECOND_POLY}
-out = {"m": int(os.environ.get("STG_POLY_TERMS", "3"))}
+out = {"m": int(os.environ.get("STG_POLY_TERMS", "7"))}
 for name in names:
     cfg = C.CONFIGS[name]
     op = SlabOperator(**cfg.kwargs())
