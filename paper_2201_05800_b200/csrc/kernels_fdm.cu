@@ -374,41 +374,54 @@ struct RowTr {
   double x[4], y[4], z[4];
 };
 
+__device__ __forceinline__ void ld4_nc(const double* p, double (&v)[4]) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void st4_g(double* p, double a0, double a1, double a2, double a3) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a0), "d"(a1), "d"(a2),
+               "d"(a3)
+               : "memory");
+}
+
+// both rows of the thread (tid and tid + 128: the same cell and z, temporal
+// nodes t and t + 2): the neighbour cells once, six 32-byte loads
 template <bool OD>
-__device__ __forceinline__ void fdm3_row_prefetch(RowTr& tr, const FdmOffdiag& od,
-                                                  const Geometry& g, int seg, int row) {
+__device__ __forceinline__ void fdm3_rows_prefetch(RowTr& tr0, RowTr& tr1, const FdmOffdiag& od,
+                                                   const Geometry& g, int seg, int row) {
   if constexpr (OD) {
     const int t = row / (f3::E * 4), e = (row >> 2) & (f3::E - 1), z = row & 3;
     const int cell = seg * f3::E + e;
-    const int cx = cell % g.nx, cy = (cell / g.nx) % g.ny, cz = cell / (g.nx * g.ny);
+    const int cxy = cell % (g.nx * g.ny);
+    const int cx = cxy % g.nx, cy = cxy / g.nx, cz = cell / (g.nx * g.ny);
     const long long plane = (long long)4 * g.n_cells * 16;  // one axis' traces
+    const long long tstep = 2LL * g.n_cells * 16;           // t -> t + 2
     const double* tt = od.tr_in + (long long)t * g.n_cells * 16;
-    auto ld4 = [](const double* p, double (&v)[4]) {
-      const double2 a = __ldg(reinterpret_cast<const double2*>(p));
-      const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-      v[0] = a.x;
-      v[1] = a.y;
-      v[2] = b.x;
-      v[3] = b.y;
-    };
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tr.x[q] = tr.y[q] = tr.z[q] = 0.0;
+    for (int q = 0; q < 4; ++q) tr0.x[q] = tr0.y[q] = tr0.z[q] = tr1.x[q] = tr1.y[q] = tr1.z[q] = 0.0;
     if (od.cL[0] != 0.0 || od.cR[0] != 0.0) {  // the x-neighbour's face line z: [z][iy]
       const bool L = od.cL[0] != 0.0;
       const int dc = L ? (cx == 0 ? g.nx - 1 : -1) : (cx == g.nx - 1 ? 1 - g.nx : 1);
-      ld4(tt + (long long)(cell + dc) * 16 + z * 4, tr.x);
+      const double* p = tt + (long long)(cell + dc) * 16 + z * 4;
+      ld4_nc(p, tr0.x);
+      ld4_nc(p + tstep, tr1.x);
     }
     if (od.cL[1] != 0.0 || od.cR[1] != 0.0) {  // the y-neighbour's face line z: [z][ix]
       const bool L = od.cL[1] != 0.0;
       const int dc = L ? (cy == 0 ? (g.ny - 1) * g.nx : -g.nx)
                        : (cy == g.ny - 1 ? -(g.ny - 1) * g.nx : g.nx);
-      ld4(tt + plane + (long long)(cell + dc) * 16 + z * 4, tr.y);
+      const double* p = tt + plane + (long long)(cell + dc) * 16 + z * 4;
+      ld4_nc(p, tr0.y);
+      ld4_nc(p + tstep, tr1.y);
     }
     if (od.cL[2] != 0.0 || od.cR[2] != 0.0) {  // line iy = z of the z-neighbour's face
       const bool L = od.cL[2] != 0.0;
       const long long pl = (long long)g.nx * g.ny;
       const long long dc = L ? (cz == 0 ? (g.nz - 1) * pl : -pl) : (cz == g.nz - 1 ? -(g.nz - 1) * pl : pl);
-      ld4(tt + 2 * plane + (cell + dc) * 16 + z * 4, tr.z);
+      const double* p = tt + 2 * plane + (cell + dc) * 16 + z * 4;
+      ld4_nc(p, tr0.z);
+      ld4_nc(p + tstep, tr1.z);
     }
   }
 }
@@ -545,8 +558,7 @@ __device__ __forceinline__ void fdm3_inv_row(const FdmCoef3& c, double* X, int r
     const long long plane = (long long)4 * g.n_cells * 16;
     double* tt = od.tr_out + (long long)t * g.n_cells * 16 + cell * 16;
     auto st4 = [](double* p, double a0, double a1, double a2, double a3) {
-      reinterpret_cast<double2*>(p)[0] = make_double2(a0, a1);
-      reinterpret_cast<double2*>(p)[1] = make_double2(a2, a3);
+      st4_g(p, a0, a1, a2, a3);
     };
     // (constant indices into o[] in both branches: a runtime index would put
     // o in local memory)
@@ -694,8 +706,7 @@ __global__ void __launch_bounds__(f3::THREADS, STG_FDM3_MINB)
       issue(seg + gridDim.x, st ^ 1);
     }
     RowTr tr0, tr1;
-    fdm3_row_prefetch<OD>(tr0, od, g, seg, tid);
-    fdm3_row_prefetch<OD>(tr1, od, g, seg, tid + f3::THREADS);
+    fdm3_rows_prefetch<OD>(tr0, tr1, od, g, seg, tid);
     while (!ptxh::mbar_try_wait(st ? bar1 : bar0, (it >> 1) & 1)) {
     }
     fdm3_fwd_row<PARAM, OD>(c, X, tid, od, tr0);
