@@ -935,7 +935,9 @@ struct Plane3 {
   static constexpr int SMEM = (3 * STAGE + 2 * PLANE) * 8 + 64;
 };
 
-template <int N1, int NT, int E>
+// RED: also max |R| and <R,R> (the Newton residual norm and the next GMRES's
+// <b,b>), as in slab3d_n4_persist
+template <int N1, int NT, int E, bool RED = false>
 __global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
     slab2d_plane3(const SlabArgs a) {
   pdl_entry();
@@ -1004,6 +1006,7 @@ __global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
   };
 
   int seg = blockIdx.x;
+  double rmax = 0.0, rss = 0.0;  // RED
   if (tid == 0) {
     if (seg < nseg) issue(seg, 0, 0);
     if (seg + (int)gridDim.x < nseg) issue(seg + gridDim.x, 1, 1);
@@ -1074,7 +1077,13 @@ __global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
     }
     double* outp = X + tp(t, e);
 #pragma unroll
-    for (int k = 0; k < NPC; ++k) outp[k] = r[k];
+    for (int k = 0; k < NPC; ++k) {
+      outp[k] = r[k];
+      if (RED) {
+        rmax = nan_max(rmax, fabs(r[k]));
+        rss = fma(r[k], r[k], rss);
+      }
+    }
     ptx::fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -1083,6 +1092,7 @@ __global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
       bulk_commit();
     }
   }
+  if (RED) block_reduce_r(a, rmax, rss);
   if (tid == 0) bulk_wait0();
 }
 
@@ -1723,22 +1733,30 @@ bool plane3_ok(const SlabArgs& a) {
          Plane3<N1, NT, E>::SMEM <= 113 * 1024;
 }
 
+// the launch that ran last on this thread formed the residual norms (RED)
+thread_local bool t_last_reduced = false;
+
 template <int N1, int NT, int E>
 int launch_plane3(const SlabArgs& a, cudaStream_t s) {
   using Q = Plane3<N1, NT, E>;
   static int occ_dev[kMaxDevices];
   int& occ = occ_dev[device_slot()];
   if (occ <= 0) {
-    cudaFuncSetAttribute(slab2d_plane3<N1, NT, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Q::SMEM);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane3<N1, NT, E>, Q::THREADS,
+    for (auto k : {slab2d_plane3<N1, NT, E, false>, slab2d_plane3<N1, NT, E, true>})
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, slab2d_plane3<N1, NT, E, true>, Q::THREADS,
                                                   Q::SMEM);
     if (occ < 1) occ = 1;
   }
   const int nseg = a.g.n_cells / E;
   int grid = occ * num_sms_cached();
   if (grid > nseg) grid = nseg;
-  launch_ex(kPdlSlab, slab2d_plane3<N1, NT, E>, grid, Q::THREADS, Q::SMEM, s, a);
+  const bool red = a.red_max != nullptr && a.red_ss != nullptr && a.red_part != nullptr &&
+                   a.seg_end == 0 && grid <= kPartialDoubles;
+  if (red) cudaMemsetAsync(a.red_max, 0, sizeof(unsigned long long), s);  // the atomic max
+  launch_ex(kPdlSlab, red ? slab2d_plane3<N1, NT, E, true> : slab2d_plane3<N1, NT, E, false>,
+            grid, Q::THREADS, Q::SMEM, s, a);
+  t_last_reduced = red;
   return 1;
 }
 
@@ -1849,12 +1867,14 @@ EncodeFn get_encode() {
 // the generic launchers reduce R only in the d = 1 lane kernel (the d = 2
 // plane kernel's reducing instance spilled and gained nothing on c2)
 bool slab_generic_reduces(const SlabArgs& a) {
+  if (a.g.dim == 2) return t_last_reduced;  // (asked right after the launch)
   return a.g.dim == 1 && lane_reduces(a) && a.g.nx >= 4096 && a.n_out <= a.n_in &&
          a.n_in >= 2 && a.n_in <= 6 && a.g.n1 >= 2 && a.g.n1 <= 6 && !std::getenv("STG_1D_V1");
 }
 
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
   const int d = a.g.dim, n1 = a.g.n1;
+  t_last_reduced = false;
   if (d == 1) {
     switch (n1) {
       case 2: return launch1d<2>(a, s);
