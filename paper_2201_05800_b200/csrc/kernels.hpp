@@ -150,8 +150,10 @@ struct GivensArgs {
 // bb != null: beta = sqrt(*bb) on the device and tol is relative (first
 // cycle from x = 0, no host round trip); else beta and tol_abs = tol given.
 // beta = 0 sets status 4 ("no work") and writes it to every host slot.
+// s0_sign != 0: S_0 is b itself, unnormalised (c_0 = 1/||b||, ||S_0||^2 =
+// <b,b>), and the right-hand side's sign goes into g_0 = s0_sign ||b||
 void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,
-                double* hn2_0, int* host, cudaStream_t s);
+                double* hn2_0, int* host, cudaStream_t s, double s0_sign = 0.0);
 // out[j] = y_j c_j, y = R^-1 g over the first k columns (the cycle's update)
 void gmres_backsub(const GmresDev* G, int k, double* out, cudaStream_t s);
 

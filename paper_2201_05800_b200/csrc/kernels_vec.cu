@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
 }
 
 __global__ void k_gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol,
-                             double reorth_tol, double* hn2_0, int* host) {
+                             double reorth_tol, double* hn2_0, int* host, double s0_sign) {
   pdl_entry();
   double tol_abs = tol;
   if (bb) {  // first cycle from x = 0: ||r|| = ||b|| is only known here
@@ -295,6 +295,11 @@ __global__ void k_gmres_init(GmresDev* G, int m, const double* bb, double beta, 
   for (int j = 1; j <= m; ++j) G->g[j] = 0.0;
   G->cn[0] = 1.0;
   if (hn2_0) *hn2_0 = 1.0;  // ||S_0||^2 = 1 (S_0 = r / ||r||)
+  if (s0_sign != 0.0 && beta > 0.0) {  // S_0 = b unnormalised; the sign rides on g_0
+    G->g[0] = s0_sign * beta;
+    G->cn[0] = 1.0 / beta;
+    if (hn2_0) *hn2_0 = beta * beta;
+  }
 }
 
 __device__ __forceinline__ double fd_step(const double* vv, const double* uu, double c) {
@@ -532,8 +537,9 @@ void gmres_backsub(const GmresDev* G, int k, double* out, cudaStream_t s) {
 }
 
 void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, double reorth_tol,
-                double* hn2_0, int* host, cudaStream_t s) {
-  launch_ex(kPdlVec, k_gmres_init, 1, 1, 0, s, G, m, bb, beta, tol, reorth_tol, hn2_0, host);
+                double* hn2_0, int* host, cudaStream_t s, double s0_sign) {
+  launch_ex(kPdlVec, k_gmres_init, 1, 1, 0, s, G, m, bb, beta, tol, reorth_tol, hn2_0, host,
+            s0_sign);
 }
 
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,

@@ -97,7 +97,7 @@ struct stg_handle {
   // workspace
   DevBuf small;    // device scalars / Hessenberg columns
   DevBuf partial;  // reduction partials
-  DevBuf basis, wv, rv, res, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
+  DevBuf basis, wv, rv, res, res2, delta, tmp1, tmp2, Ustage, host_U, host_R, host_u, host_u2;
   DevBuf ptab;          // preconditioner block tables
   int ptab_kind = -1;   // TBLOCK / JACOBI table in ptab and its mix (-1: none)
   stg::MixCoef ptab_mix{};
@@ -653,13 +653,28 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
   int total = 0;
   bool first = true;
   bool x_set = !x_zero;  // x_zero: x is written (not accumulated) by the first update
+  // b may be the basis' first slot itself (Newton writes its residual there):
+  // then the first cycle from x = 0 keeps S_0 = b unnormalised (no scaling
+  // pass), and a restart first moves b out of the slot it would overwrite
+  bool s0_is_b = false;
   while (true) {
     double beta = -1.0;  // < 0: on the device only (deferred first cycle)
+    s0_is_b = false;
     if (first && x_zero) {  // x = 0: r = b and ||r|| = ||b|| (no operator apply, no sync)
-      stg::vec_scale_invsqrt(V, b, dsm + 200, n, s, b_sign);  // S_0 = b / ||b|| (dsm[200] = <b,b>)
-      h->launches++;
+      if (b == V) {
+        s0_is_b = true;
+      } else {
+        stg::vec_scale_invsqrt(V, b, dsm + 200, n, s, b_sign);  // S_0 = b / ||b|| (dsm[200] = <b,b>)
+        h->launches++;
+      }
       if (!defer) beta = bnorm;
     } else {
+      if (b == V) {  // keep b for this and later restarts
+        h->res2.ensure(size_t(n));
+        stg::vec_copy(h->res2.p, b, n, s);
+        h->launches++;
+        b = h->res2.p;
+      }
       A(x, w);                                   // w = A x
       stg::vec_axpby(w, b_sign, b, -1.0, n, s);  // w = b - A x
       h->launches++;
@@ -682,10 +697,11 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     }
     if (total >= max_it) break;
     for (int j = 0; j <= m; ++j) mapped[j] = -1;  // per-step status slots
+    const double s0 = s0_is_b ? b_sign : 0.0;
     if (beta >= 0.0)
-      stg::gmres_init(G, m, nullptr, beta, tol * bnorm, reorth_tol, dsm + 64, mapped_dev, s);
+      stg::gmres_init(G, m, nullptr, beta, tol * bnorm, reorth_tol, dsm + 64, mapped_dev, s, s0);
     else
-      stg::gmres_init(G, m, dsm + 200, 0.0, tol, reorth_tol, dsm + 64, mapped_dev, s);
+      stg::gmres_init(G, m, dsm + 200, 0.0, tol, reorth_tol, dsm + 64, mapped_dev, s, s0);
     h->launches++;
     auto can_enqueue = [&](int j) { return j < m && total + j < max_it; };
     int k = 0, enq = 0, status = 0;
@@ -796,9 +812,11 @@ NewtonOut newton(stg_handle* h, const Op& residual,
                  const std::function<LinSys(const double*)>& jacobian, double* u, long long n,
                  const stg_newton_config& cfg) {
   ensure_workspace(h);
-  h->res.ensure(size_t(n));
   h->delta.ensure(size_t(n));
-  double* r = h->res.p;
+  // the residual is written straight into the first Krylov basis slot: the
+  // GMRES that follows starts from it unnormalised (no copy or scaling pass)
+  h->basis.ensure(size_t(round_up(n, 32)) * (cfg.gmres_restart + 1));
+  double* r = h->basis.p;
   double* du = h->delta.p;
   NewtonOut out;
   AdmDefer defer(h);
