@@ -314,7 +314,7 @@ struct NewtonConfig {  // newton.hpp:30-38
   double gmres_tol = 1e-12;
   int gmres_max_it = 1000;
   double fd_eps = 0.0;
-  int precond = STG_PRECOND_AUTO;  // block-Jacobi right preconditioner (stg_cuda.h)
+  int precond = STG_PRECOND_AUTO;  // right preconditioner, STG_PRECOND_* (stg_cuda.h)
   stg_newton_config c() const {
     return stg_newton_config{abs_tol,      rel_tol, max_iter, int(linear), gmres_restart,
                              gmres_tol,    gmres_max_it, fd_eps, precond};

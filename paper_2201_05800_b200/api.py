@@ -70,7 +70,7 @@ class NewtonConfig:  # newton.hpp:30-38 (+ fd_eps for nonlinear J v)
     gmres_tol: float = 1e-12
     gmres_max_it: int = 1000
     fd_eps: float = 0.0
-    precond: int = L.STG_PRECOND_AUTO  # block-Jacobi right preconditioner (stg_cuda.h)
+    precond: int = L.STG_PRECOND_AUTO  # right preconditioner, STG_PRECOND_* (stg_cuda.h)
 
     def to_c(self) -> L.StgNewtonConfig:
         return L.StgNewtonConfig(self.abs_tol, self.rel_tol, self.max_iter, self.linear,
