@@ -298,19 +298,28 @@ __global__ void __launch_bounds__(THREADS, MINB)
 // solved directly per spatial mode, M_theta = (T + theta S)^-1 (4 x 4
 // complex), instead of Q^-1 S^-1, 1/Lambda and Q, and the y / z transforms
 // by conjugate pairs: 9.2k FP64 ops per cell (12.3k with plain complex y / z
-// transforms, 15k with the eigen-decomposed t direction).  16 cells per segment and one thread per (cell, iy, j) unit in
+// transforms, 15k with the eigen-decomposed t direction).  E cells per segment (8, below) and one thread per (cell, iy, j) unit in
 // phase B, so every phase is one pass over the tile: three CTA barriers per
-// 16 cells (the two-half phase B above needs six per 8).  The complex tile
+// segment (the two-half phase B above needs six per 8 cells).  The complex tile
 // lives in place of the real one (a (t, z) row of 16 reals becomes 8 complex
 // (iy, j) values).  All factors (FdmCoef3, 9.5 KB) arrive with the first tile
 // by one bulk copy and are read from shared memory: warp-uniform addresses
 // (broadcast) for the spatial factors, one 128-byte wavefront per table read
 // (q fastest) -- kernel-parameter operands had the compiler keep ~100 of them
 // in uniform registers and spill those.
+// cells per segment: 8 (64-thread CTAs, 4 per SM) measured best for the
+// coupled apply that dominates the c4 / c5 solves (c4 slab solve 0.678 ->
+// 0.652 ms against 16 cells x 3 CTAs/SM; the plain apply 31.9 -> 30.2 us):
+// half the first-tile wait and last-tile drain per CTA, 8 warps per SM at up
+// to 254 registers without spills.  4 cells (one-warp CTAs, 8 per SM) gives
+// the plain apply 29.1 us but the coupled one less.
+#ifndef STG_FDM3_E
+#define STG_FDM3_E 8
+#endif
 namespace f3 {
-constexpr int E = 16;              // cells per segment
-constexpr int THREADS = 128;
-constexpr int TILE = E * 256 * 8;  // 32 KB: [t][cell][z] rows of 16 doubles
+constexpr int E = STG_FDM3_E;      // cells per segment
+constexpr int THREADS = 8 * E;     // two tile rows per thread, one phase-B unit per thread
+constexpr int TILE = E * 256 * 8;  // 32 KB at E = 16: [t][cell][z] rows of 16 doubles
 constexpr int COEF = int(sizeof(FdmCoef3));
 constexpr int OFF_C = 2 * TILE;
 constexpr int OFF_BAR = OFF_C + COEF;
@@ -385,7 +394,7 @@ __device__ __forceinline__ void st4_g(double* p, double a0, double a1, double a2
                : "memory");
 }
 
-// both rows of the thread (tid and tid + 128: the same cell and z, temporal
+// both rows of the thread (tid and tid + THREADS: the same cell and z, temporal
 // nodes t and t + 2): the neighbour cells once, six 32-byte loads
 template <bool OD>
 __device__ __forceinline__ void fdm3_rows_prefetch(RowTr& tr0, RowTr& tr1, const FdmOffdiag& od,
@@ -638,7 +647,7 @@ __device__ __forceinline__ void fdm3_unit(const FdmCoef3& c, const FdmCoef3& cs,
 // the FdmCoef3 by value); otherwise from the shared copy.  The temporal
 // table is always read from shared memory (per-lane addresses).
 #ifndef STG_FDM3_MINB
-#define STG_FDM3_MINB 3
+#define STG_FDM3_MINB (STG_FDM3_E >= 16 ? 3 : (STG_FDM3_E == 8 ? 4 : 8))
 #endif
 #ifndef STG_FDM3_ROW_UNROLL
 #define STG_FDM3_ROW_UNROLL 1
