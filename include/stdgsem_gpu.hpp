@@ -7,18 +7,25 @@
 //   stdg_step     stdg.hpp:120-143      stdg_integrate stdg.hpp:152-173
 //   rk_step       lodg.hpp:89-149       integrate    lodg.hpp:158-181
 //   NewtonConfig  newton.hpp:30-38      NonconvergenceError newton.hpp:40-48
-// Vectors are std::vector<double> on the host (the reference's Eigen::VectorXd
-// role); each call moves them to the device once, runs there, and copies the
-// result back.  For device-resident loops use the DeviceVec overloads.
+// Vec is a std::vector<double> on the host (the reference's Eigen::VectorXd
+// role) whose allocator hands out page-locked memory for large vectors, so
+// every call's copies are plain DMA from / to the caller's vectors; each call
+// moves them to the device once, runs there, and copies the result back.  For
+// device-resident loops use the DeviceVec overloads.
 // Status codes map back to std::invalid_argument / std::runtime_error /
 // NonconvergenceError / AdmissibilityError; CUDA failures throw CudaError
 // (there is no CPU path).
 #pragma once
 
 #include <cmath>
+#include <cstdlib>
+#include <map>
 #include <memory>
+#include <mutex>
+#include <new>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -27,7 +34,105 @@
 namespace stdgsem {
 namespace gpu {
 
-using Vec = std::vector<double>;
+// Allocator behind Vec.  Blocks of kPinBytes or more are page-locked
+// (stg_host_alloc) and recycled through a process-wide free list keyed by
+// size, so a time-marching loop that keeps creating result vectors, as the
+// reference's value-returning API makes it, pays cudaHostAlloc and the first-
+// touch page faults once per size, not per call (c4 stdg_step on fresh
+// std::vector<double> results: 37 ms per call, of which 2.5 ms is the solve
+// and its copies).  Smaller blocks, and every block when no device is present
+// (host-only helpers), come from malloc.  Like Eigen::VectorXd(n), Vec(n)
+// leaves its entries uninitialised; Vec(n, 0.0) zero-fills.
+namespace detail {
+constexpr std::size_t kPinBytes = std::size_t(256) << 10;
+constexpr std::size_t kPoolCapBytes = std::size_t(2) << 30;  // cached free blocks
+
+struct PinnedPool {
+  std::mutex mu;
+  std::multimap<std::size_t, double*> free_blocks;
+  std::size_t cached = 0;
+  int mode = 0;  // 0 undecided, 1 page-locked, 2 malloc (no device)
+
+  double* take(std::size_t bytes) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      auto it = free_blocks.find(bytes);
+      if (it != free_blocks.end()) {
+        double* p = it->second;
+        free_blocks.erase(it);
+        cached -= bytes;
+        return p;
+      }
+      if (mode == 2) return nullptr;
+    }
+    double* p = nullptr;
+    const int code = stg_host_alloc((long long)(bytes / sizeof(double)), &p);
+    std::lock_guard<std::mutex> lk(mu);
+    if (code == STG_OK && p) {
+      mode = 1;
+      return p;
+    }
+    if (mode == 1) throw std::bad_alloc();  // page-locked memory exhausted
+    mode = 2;
+    return nullptr;
+  }
+  // returns false when the block is not the pool's (malloc mode)
+  bool give(double* p, std::size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (mode != 1) return false;
+    if (cached + bytes <= kPoolCapBytes) {
+      free_blocks.emplace(bytes, p);
+      cached += bytes;
+    } else {
+      stg_host_free(p);
+    }
+    return true;
+  }
+};
+
+inline PinnedPool& pinned_pool() {
+  static PinnedPool* pool = new PinnedPool;  // never destroyed: outlives the CUDA context's users
+  return *pool;
+}
+}  // namespace detail
+
+template <class T>
+struct HostAllocator {
+  using value_type = T;
+  HostAllocator() = default;
+  template <class U>
+  HostAllocator(const HostAllocator<U>&) noexcept {}
+  T* allocate(std::size_t n) {
+    const std::size_t bytes = n * sizeof(T);
+    if (bytes >= detail::kPinBytes && bytes % sizeof(double) == 0)
+      if (double* p = detail::pinned_pool().take(bytes)) return reinterpret_cast<T*>(p);
+    void* p = std::malloc(bytes ? bytes : 1);
+    if (!p) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, std::size_t n) noexcept {
+    const std::size_t bytes = n * sizeof(T);
+    if (bytes >= detail::kPinBytes && bytes % sizeof(double) == 0 &&
+        detail::pinned_pool().give(reinterpret_cast<double*>(p), bytes))
+      return;
+    std::free(p);
+  }
+  // default-initialise (no zero fill of a vector about to be overwritten)
+  template <class U>
+  void construct(U* p) noexcept(std::is_nothrow_default_constructible<U>::value) {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+  template <class U>
+  bool operator==(const HostAllocator<U>&) const noexcept { return true; }
+  template <class U>
+  bool operator!=(const HostAllocator<U>&) const noexcept { return false; }
+};
+
+using Vec = std::vector<double, HostAllocator<double>>;
 
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;

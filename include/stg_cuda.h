@@ -282,6 +282,12 @@ int stg_device_free(double* p);
 /* dir: 0 = host -> device, 1 = device -> host, 2 = device -> device */
 int stg_memcpy(double* dst, const double* src, long long n_doubles, int dir);
 int stg_device_synchronize(void);
+/* Page-locked host memory for the *_host entry points: buffers from here are
+ * copied by DMA straight from / to the caller's memory (pageable buffers go
+ * through the library's own pinned staging).  Fails with
+ * STG_ERR_CUDA when no device is present. */
+int stg_host_alloc(long long n_doubles, double** out);
+int stg_host_free(double* p);
 
 /* ---- host-only constants (no device needed) -------------------------------- */
 /* lgl_rule (quadrature.hpp:66-105): n nodes and weights. */

@@ -35,6 +35,7 @@ EXPORTS = (
     "stg_st_residual_host", "stg_stdg_step_host", "stg_rk_step_host", "stg_kernel_launches",
     "stg_lgl_rule", "stg_diff_matrix", "stg_lobatto_tableau",
     "stg_device_alloc", "stg_device_free", "stg_memcpy", "stg_device_synchronize",
+    "stg_host_alloc", "stg_host_free",
 )
 
 
@@ -118,6 +119,8 @@ def load() -> ctypes.CDLL:
     L.stg_lobatto_tableau.argtypes = [_i, _vp, _vp, _vp]
     L.stg_device_alloc.argtypes = [ctypes.c_longlong, ctypes.POINTER(_vp)]
     L.stg_device_free.argtypes = [_vp]
+    L.stg_host_alloc.argtypes = [ctypes.c_longlong, ctypes.POINTER(_vp)]
+    L.stg_host_free.argtypes = [_vp]
     L.stg_memcpy.argtypes = [_vp, _vp, ctypes.c_longlong, _i]
     _LIB = L
     return L

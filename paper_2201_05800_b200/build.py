@@ -24,7 +24,7 @@ OBJDIR = PKG / "build_obj"
 
 SOURCES = ["kernels_slab.cu", "kernels_vec.cu", "kernels_precond.cu", "kernels_fdm.cu",
            "kernels_general.cu", "kernels_small.cu", "stg.cpp"]
-HEADERS = ["kernels.hpp", "constants.hpp", "eig.hpp", "ptx.cuh", "krylov.cuh"]
+HEADERS = ["kernels.hpp", "constants.hpp", "eig.hpp", "ptx.cuh", "krylov.cuh", "hostcopy.hpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                   "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}"]
@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     # no library kernels: static CUDA runtime only
-    cmd = cc + ARCH + ["-shared", "-o", str(tmp)] + objs
+    cmd = cc + ARCH + ["-shared", "-Xcompiler", "-pthread", "-o", str(tmp)] + objs
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)

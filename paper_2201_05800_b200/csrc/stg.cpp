@@ -19,6 +19,7 @@
 #include "../../include/stg_cuda.h"
 #include "constants.hpp"
 #include "eig.hpp"
+#include "hostcopy.hpp"
 #include "kernels.hpp"
 
 namespace {
@@ -68,6 +69,34 @@ struct DevBuf {
     if (p) cudaFree(p);
   }
 };
+
+// page-locked host mirror of a caller's pageable buffer (hostcopy.hpp)
+struct PinBuf {
+  double* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    ck(cudaHostAlloc(reinterpret_cast<void**>(&p), count * sizeof(double), cudaHostAllocDefault),
+       "cudaHostAlloc");
+    n = count;
+  }
+  ~PinBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+// whether the driver would have to stage copies from / to p itself
+bool pageable(const void* p) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeUnregistered;
+}
 
 long long round_up(long long v, long long m) { return (v + m - 1) / m * m; }
 
@@ -166,8 +195,12 @@ struct stg_handle {
   static constexpr int kChunks = 8;
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_start = nullptr, ev_in[kChunks] = {}, ev_c[kChunks] = {};
+  // pageable callers: page-locked mirrors and the events of their D2H chunks
+  PinBuf pin_U, pin_R, pin_u, pin_u2;
+  std::vector<cudaEvent_t> ev_stage;
 
   ~stg_handle() {
+    for (cudaEvent_t e : ev_stage) cudaEventDestroy(e);
     if (pinned) cudaFreeHost(pinned);
     if (gpin) cudaFreeHost(gpin);
     if (mapped) cudaFreeHost(mapped);
@@ -1120,6 +1153,215 @@ bool st_residual_host_pipelined(stg_handle* h, double dt, const double* un_host,
     for (cudaEvent_t e : tev) cudaEventDestroy(e);
   }
   return true;
+}
+
+// ---- pageable callers (hostcopy.hpp) ----------------------------------------
+constexpr size_t kStageChunk = size_t(1) << 20;  // doubles per staged chunk (8 MiB)
+
+cudaEvent_t stage_event(stg_handle* h, size_t i) {
+  while (h->ev_stage.size() <= i) {
+    cudaEvent_t e;
+    ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    h->ev_stage.push_back(e);
+  }
+  return h->ev_stage[i];
+}
+
+// n doubles from pageable host memory to the device on stream s: worker
+// threads fill the page-locked mirror chunk by chunk while the copy engine
+// moves the previous chunk
+void staged_h2d(stg_handle* h, double* dev, const double* host, size_t n, PinBuf& pin,
+                cudaStream_t s) {
+  pin.ensure(n);
+  stg::HostCopyPool& pool = stg::HostCopyPool::get();
+  for (size_t off = 0; off < n; off += kStageChunk) {
+    const size_t cnt = std::min(kStageChunk, n - off);
+    const stg::CopyItem it{pin.p + off, host + off, cnt * sizeof(double)};
+    pool.par_copy(&it, 1);
+    ck(cudaMemcpyAsync(dev + off, pin.p + off, cnt * sizeof(double), cudaMemcpyHostToDevice, s),
+       "H2D");
+  }
+  (void)h;
+}
+
+// n doubles from the device to pageable host memory, in two halves: enqueue
+// every chunk's D2H into the mirror on s (an event after each), then drain:
+// the workers copy chunk i out to `host` while the copy engine moves chunk
+// i + 1.  ev_base: first index into the handle's staging events (two
+// transfers of one call do not share events).
+void staged_d2h_enqueue(stg_handle* h, const double* dev, size_t n, PinBuf& pin, cudaStream_t s,
+                        size_t ev_base) {
+  pin.ensure(n);
+  size_t i = 0;
+  for (size_t off = 0; off < n; off += kStageChunk, ++i) {
+    const size_t cnt = std::min(kStageChunk, n - off);
+    ck(cudaMemcpyAsync(pin.p + off, dev + off, cnt * sizeof(double), cudaMemcpyDeviceToHost, s),
+       "D2H");
+    ck(cudaEventRecord(stage_event(h, ev_base + i), s), "event");
+  }
+}
+
+void staged_d2h_drain(stg_handle* h, double* host, size_t n, PinBuf& pin, size_t ev_base) {
+  stg::HostCopyPool& pool = stg::HostCopyPool::get();
+  size_t i = 0;
+  for (size_t off = 0; off < n; off += kStageChunk, ++i) {
+    const size_t cnt = std::min(kStageChunk, n - off);
+    ck(cudaEventSynchronize(h->ev_stage[ev_base + i]), "sync");
+    const stg::CopyItem it{host + off, pin.p + off, cnt * sizeof(double)};
+    pool.par_copy(&it, 1);
+  }
+}
+
+void staged_d2h(stg_handle* h, double* host, const double* dev, size_t n, PinBuf& pin,
+                cudaStream_t s) {
+  staged_d2h_enqueue(h, dev, n, pin, s, 0);
+  staged_d2h_drain(h, host, n, pin, 0);
+}
+
+// The pipelined host-buffer R(U) (st_residual_host_pipelined) for pageable
+// caller memory: K equal z-chunks; the workers gather chunk k (its slice of
+// every temporal block of U, and of u_n) into the page-locked mirrors, its
+// H2D, kernel launch and D2H (into the mirror of R) are enqueued, and while
+// those run the workers gather chunk k + 1; finished chunks of R are copied
+// out to the caller as their D2H events complete.  Returns false when the
+// fast kernel does not apply.
+bool st_residual_host_staged(stg_handle* h, double dt, const double* un_host,
+                             const double* U_host, double* R_host) {
+  const stg::Geometry& g = h->g;
+  if (h->kernel_pref == STG_KERNEL_GENERIC || g.dim != 3 || g.nz < 2) return false;
+  int K = std::min<int>(stg_handle::kChunks, g.nz);
+  if (K < 2) return false;
+  const long long ns = h->n_sdof, nd = h->n_dof;
+  h->host_U.ensure(size_t(nd));
+  h->host_R.ensure(size_t(nd));
+  h->host_u.ensure(size_t(ns));
+  stg::SlabArgs a{};
+  a.sp = h->sp;
+  a.mx = st_mix(h, dt, true);
+  a.g = g;
+  a.n_in = a.n_out = h->nt;
+  a.has_w = 1;
+  a.model = h->desc.model;
+  a.X = h->host_U.p;
+  a.W = h->host_u.p;
+  a.R = h->host_R.p;
+  a.no_pdl = 1;
+  if (!stg::slab_fast_supported(a)) return false;
+  h->pin_U.ensure(size_t(nd));
+  h->pin_R.ensure(size_t(nd));
+  h->pin_u.ensure(size_t(ns));
+  if (!h->s_in) {
+    ck(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking), "stream");
+    ck(cudaEventCreateWithFlags(&h->ev_start, cudaEventDisableTiming), "event");
+    for (int k = 0; k < stg_handle::kChunks; ++k) {
+      ck(cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&h->ev_c[k], cudaEventDisableTiming), "event");
+    }
+  }
+  stage_event(h, size_t(K));
+  int zb[stg_handle::kChunks + 1];
+  for (int k = 0; k <= K; ++k) zb[k] = int((long long)g.nz * k / K);
+  const long long layer = (long long)g.nx * g.ny * g.npc;
+  const int seg_per_layer = g.nx * g.ny / 8;
+  const bool needL = h->sp.cL[2] != 0.0, needR = h->sp.cR[2] != 0.0;
+  const size_t pitch = sizeof(double) * size_t(ns);
+  const int nt = h->nt;
+  stg::HostCopyPool& pool = stg::HostCopyPool::get();
+  ck(cudaEventRecord(h->ev_start, h->stream), "event");
+  ck(cudaStreamWaitEvent(h->s_in, h->ev_start, 0), "wait");
+  // gather layers [z0, z0 + nl) into the mirrors and enqueue their H2D
+  auto in_layers = [&](int z0, int nl) {
+    const long long off = z0 * layer, cnt = nl * layer;
+    stg::CopyItem items[8];
+    int ni = 0;
+    for (int t = 0; t < nt; ++t)
+      items[ni++] = {h->pin_U.p + t * ns + off, U_host + t * ns + off, sizeof(double) * size_t(cnt)};
+    items[ni++] = {h->pin_u.p + off, un_host + off, sizeof(double) * size_t(cnt)};
+    pool.par_copy(items, ni);
+    ck(cudaMemcpy2DAsync(h->host_U.p + off, pitch, h->pin_U.p + off, pitch, sizeof(double) * cnt,
+                         size_t(nt), cudaMemcpyHostToDevice, h->s_in), "H2D");
+    ck(cudaMemcpyAsync(h->host_u.p + off, h->pin_u.p + off, sizeof(double) * cnt,
+                       cudaMemcpyHostToDevice, h->s_in), "H2D");
+  };
+  // launch chunk j (its inputs' events recorded) and enqueue its D2H
+  auto run_chunk = [&](int j) {
+    ck(cudaStreamWaitEvent(h->stream, h->ev_in[needR ? std::min(j + 1, K - 1) : j], 0), "wait");
+    a.seg_begin = zb[j] * seg_per_layer;
+    a.seg_end = zb[j + 1] * seg_per_layer;
+    if (stg::launch_slab_fast(a, h->stream) < 0)
+      throw std::runtime_error("fast kernel launch failed in the staged host path");
+    h->launches++;
+    check_launch(h);
+    ck(cudaEventRecord(h->ev_c[j], h->stream), "event");
+    ck(cudaStreamWaitEvent(h->s_out, h->ev_c[j], 0), "wait");
+    const long long off = zb[j] * layer, cnt = (zb[j + 1] - zb[j]) * layer;
+    ck(cudaMemcpy2DAsync(h->pin_R.p + off, pitch, h->host_R.p + off, pitch, sizeof(double) * cnt,
+                         size_t(nt), cudaMemcpyDeviceToHost, h->s_out), "D2H");
+    ck(cudaEventRecord(h->ev_stage[size_t(j)], h->s_out), "event");
+  };
+  int copied_out = 0;  // chunks of R already handed to the caller
+  auto out_chunk = [&](int j) {
+    const long long off = zb[j] * layer, cnt = (zb[j + 1] - zb[j]) * layer;
+    stg::CopyItem items[8];
+    int ni = 0;
+    for (int t = 0; t < nt; ++t)
+      items[ni++] = {R_host + t * ns + off, h->pin_R.p + t * ns + off, sizeof(double) * size_t(cnt)};
+    pool.par_copy(items, ni);
+  };
+  if (needL) in_layers(g.nz - 1, 1);  // periodic z- neighbour of chunk 0
+  for (int k = 0; k < K; ++k) {
+    in_layers(zb[k], zb[k + 1] - zb[k]);
+    ck(cudaEventRecord(h->ev_in[k], h->s_in), "event");
+    if (!needR) run_chunk(k);
+    else if (k > 0) run_chunk(k - 1);
+    // hand finished chunks out between gathers (keeps the tail short)
+    while (copied_out < k && cudaEventQuery(h->ev_stage[size_t(copied_out)]) == cudaSuccess)
+      out_chunk(copied_out++);
+  }
+  if (needR) run_chunk(K - 1);
+  for (; copied_out < K; ++copied_out) {
+    ck(cudaEventSynchronize(h->ev_stage[size_t(copied_out)]), "sync");
+    out_chunk(copied_out);
+  }
+  return true;
+}
+
+// whether this handle's vectors are worth the worker threads (below 1 MiB the
+// driver's own staging is as fast) and staging is not switched off
+bool stage_large(const stg_handle* h) {
+  static const bool off = std::getenv("STG_HOST_NO_STAGING") != nullptr;
+  return !off && size_t(h->n_dof) * sizeof(double) >= (size_t(1) << 20);
+}
+
+// copy-in / copy-out of the host-buffer slab steps (stg_stdg_step_host,
+// stg_rk_step_host): plain async copies for page-locked caller memory, the
+// staged ones for pageable memory
+void step_host_in(stg_handle* h, const double* u) {
+  cudaStream_t s = h->stream;
+  if (stage_large(h) && pageable(u))
+    staged_h2d(h, h->host_u.p, u, size_t(h->n_sdof), h->pin_u, s);
+  else
+    ck(cudaMemcpyAsync(h->host_u.p, u, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
+       "H2D");
+}
+
+void step_host_out(stg_handle* h, double* U, double* u_next) {
+  cudaStream_t s = h->stream;
+  const bool stU = stage_large(h) && pageable(U);
+  const bool stu = u_next && stage_large(h) && pageable(u_next);
+  // page-locked destinations first: their DMA runs while the workers copy
+  if (!stU)
+    ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
+  if (u_next && !stu)
+    ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,
+                       s), "D2H");
+  const size_t nU = (size_t(h->n_dof) + kStageChunk - 1) / kStageChunk;
+  if (stU) staged_d2h_enqueue(h, h->host_U.p, size_t(h->n_dof), h->pin_U, s, 0);
+  if (stu) staged_d2h_enqueue(h, h->host_u2.p, size_t(h->n_sdof), h->pin_u2, s, nU);
+  if (stU) staged_d2h_drain(h, U, size_t(h->n_dof), h->pin_U, 0);
+  if (stu) staged_d2h_drain(h, u_next, size_t(h->n_sdof), h->pin_u2, nU);
+  ck(cudaStreamSynchronize(s), "sync");
 }
 
 // Euler has no exact linearisation here: a finite-difference step is always used
@@ -2404,6 +2646,23 @@ int stg_device_free(double* p) {
   });
 }
 
+int stg_host_alloc(long long n, double** out) {
+  return guarded(nullptr, [&] {
+    need(out, "stg_host_alloc");
+    if (n < 0) throw std::invalid_argument("stg_host_alloc: n >= 0");
+    *out = nullptr;
+    if (n > 0)
+      ck(cudaHostAlloc(reinterpret_cast<void**>(out), size_t(n) * sizeof(double),
+                       cudaHostAllocPortable), "cudaHostAlloc");
+  });
+}
+
+int stg_host_free(double* p) {
+  return guarded(nullptr, [&] {
+    if (p) ck(cudaFreeHost(p), "cudaFreeHost");
+  });
+}
+
 int stg_memcpy(double* dst, const double* src, long long n, int dir) {
   return guarded(nullptr, [&] {
     if (n < 0 || dir < 0 || dir > 2) throw std::invalid_argument("stg_memcpy: bad arguments");
@@ -2644,12 +2903,24 @@ int stg_st_residual_host(stg_handle* h, double t_n, double dt, const double* u_n
     need(U, "U");
     need(R, "R");
     (void)t_n;
-    if (!std::getenv("STG_HOST_NO_PIPELINE") && st_residual_host_pipelined(h, dt, u_n, U, R))
+    // pageable caller memory goes through the library's own page-locked
+    // mirrors (hostcopy.hpp); STG_HOST_NO_STAGING=1 leaves it to the driver
+    const bool staged = stage_large(h) && (pageable(U) || pageable(R) || pageable(u_n));
+    if (!std::getenv("STG_HOST_NO_PIPELINE") &&
+        (staged ? st_residual_host_staged(h, dt, u_n, U, R)
+                : st_residual_host_pipelined(h, dt, u_n, U, R)))
       return;
     h->host_U.ensure(size_t(h->n_dof));
     h->host_R.ensure(size_t(h->n_dof));
     h->host_u.ensure(size_t(h->n_sdof));
     cudaStream_t s = h->stream;
+    if (staged) {
+      staged_h2d(h, h->host_U.p, U, size_t(h->n_dof), h->pin_U, s);
+      staged_h2d(h, h->host_u.p, u_n, size_t(h->n_sdof), h->pin_u, s);
+      st_residual(h, dt, h->host_u.p, h->host_U.p, h->host_R.p);
+      staged_d2h(h, R, h->host_R.p, size_t(h->n_dof), h->pin_R, s);
+      return;
+    }
     ck(cudaMemcpyAsync(h->host_U.p, U, sizeof(double) * h->n_dof, cudaMemcpyHostToDevice, s), "H2D");
     ck(cudaMemcpyAsync(h->host_u.p, u_n, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
        "H2D");
@@ -2669,23 +2940,14 @@ int stg_stdg_step_host(stg_handle* h, double t_n, double dt, const double* u_n,
     h->host_U.ensure(size_t(h->n_dof));
     h->host_u.ensure(size_t(h->n_sdof));
     h->host_u2.ensure(size_t(h->n_sdof));
-    cudaStream_t s = h->stream;
-    ck(cudaMemcpyAsync(h->host_u.p, u_n, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
-       "H2D");
+    step_host_in(h, u_n);
     try {
       do_stdg_step(h, t_n, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
     } catch (const NonconvergenceError&) {  // the last iterate goes back to U
-      ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s),
-         "D2H");
-      ck(cudaStreamSynchronize(s), "sync");
+      step_host_out(h, U, nullptr);
       throw;
     }
-    ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
-    if (u_next)
-      ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,
-                         s),
-         "D2H");
-    ck(cudaStreamSynchronize(s), "sync");
+    step_host_out(h, U, u_next);
   });
 }
 
@@ -2699,23 +2961,14 @@ int stg_rk_step_host(stg_handle* h, int form, double t, double dt, const double*
     h->host_U.ensure(size_t(h->n_dof));
     h->host_u.ensure(size_t(h->n_sdof));
     h->host_u2.ensure(size_t(h->n_sdof));
-    cudaStream_t s = h->stream;
-    ck(cudaMemcpyAsync(h->host_u.p, u, sizeof(double) * h->n_sdof, cudaMemcpyHostToDevice, s),
-       "H2D");
+    step_host_in(h, u);
     try {
       do_rk_step(h, form, t, dt, h->host_u.p, cfg, h->host_U.p, h->host_u2.p, info);
     } catch (const NonconvergenceError&) {  // the last iterate goes back to U
-      ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s),
-         "D2H");
-      ck(cudaStreamSynchronize(s), "sync");
+      step_host_out(h, U, nullptr);
       throw;
     }
-    ck(cudaMemcpyAsync(U, h->host_U.p, sizeof(double) * h->n_dof, cudaMemcpyDeviceToHost, s), "D2H");
-    if (u_next)
-      ck(cudaMemcpyAsync(u_next, h->host_u2.p, sizeof(double) * h->n_sdof, cudaMemcpyDeviceToHost,
-                         s),
-         "D2H");
-    ck(cudaStreamSynchronize(s), "sync");
+    step_host_out(h, U, u_next);
   });
 }
 

@@ -108,6 +108,54 @@ __global__ void zc_copy(const double2* __restrict__ src, double2* __restrict__ d
     dst[i] = src[i];
 }
 
+// rows x cnt2 double2 elements, row pitch pitch2 (double2): one chunk of all temporal blocks
+__global__ void zc_copy2d(const double2* __restrict__ src, double2* __restrict__ dst, size_t cnt2,
+                          size_t pitch2, int rows) {
+  const size_t n = cnt2 * rows;
+  for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t r = i / cnt2, c = i - r * cnt2;
+    dst[r * pitch2 + c] = src[r * pitch2 + c];
+  }
+}
+
+// copy engine in (chunked), SM-written zero-copy out per chunk (blocks CTAs of 512 threads)
+void chain_zc(int K, bool ramp, int blocks) {
+  auto zb = bounds(K, ramp);
+  const size_t pitch = NS * sizeof(double);
+  fork(2);
+  for (int k = 0; k < K; ++k) {
+    const size_t off = zb[k] * LAYER, cnt = (zb[k + 1] - zb[k]) * LAYER;
+    CK(cudaMemcpy2DAsync(dU + off, pitch, hU + off, pitch, cnt * 8, NT, cudaMemcpyHostToDevice, st[0]));
+    CK(cudaMemcpyAsync(du + off, hu + off, cnt * 8, cudaMemcpyHostToDevice, st[0]));
+    cudaEventRecord(ev[k], st[0]);
+  }
+  for (int k = 0; k < K; ++k) {
+    cudaStreamWaitEvent(st[1], ev[k], 0);
+    const size_t off = zb[k] * LAYER, cnt = (zb[k + 1] - zb[k]) * LAYER;
+    zc_copy2d<<<blocks, 512, 0, st[1]>>>((const double2*)(dR + off), (double2*)(hR + off), cnt / 2, NS / 2, NT);
+  }
+  join(2);
+}
+
+// SM-issued zero-copy reads in (one kernel per chunk, in stream order), copy engine out
+void chain_zcin(int K, bool ramp, int blocks) {
+  auto zb = bounds(K, ramp);
+  const size_t pitch = NS * sizeof(double);
+  fork(2);
+  for (int k = 0; k < K; ++k) {
+    const size_t off = zb[k] * LAYER, cnt = (zb[k + 1] - zb[k]) * LAYER;
+    zc_copy2d<<<blocks, 512, 0, st[0]>>>((const double2*)(hU + off), (double2*)(dU + off), cnt / 2, NS / 2, NT);
+    zc_copy2d<<<blocks, 512, 0, st[0]>>>((const double2*)(hu + off), (double2*)(du + off), cnt / 2, NS / 2, 1);
+    cudaEventRecord(ev[k], st[0]);
+  }
+  for (int k = 0; k < K; ++k) {
+    cudaStreamWaitEvent(st[1], ev[k], 0);
+    const size_t off = zb[k] * LAYER, cnt = (zb[k + 1] - zb[k]) * LAYER;
+    CK(cudaMemcpy2DAsync(hR + off, pitch, dR + off, pitch, cnt * 8, NT, cudaMemcpyDeviceToHost, st[1]));
+  }
+  join(2);
+}
+
 int main() {
   CK(cudaHostAlloc(&hU, ND * 8, cudaHostAllocMapped));
   CK(cudaHostAlloc(&hu, NS * 8, cudaHostAllocMapped));
@@ -135,7 +183,7 @@ int main() {
     cudaMemcpyAsync(hR, dR, ND * 8, cudaMemcpyDeviceToHost, st[1]);
     join(2);
   }));
-  for (int K : {4, 8, 16})
+  for (int K : {8})
     for (int ramp : {0, 1})
       for (int nin : {1, 2})
         for (int nout : {1, 2})
@@ -168,6 +216,26 @@ int main() {
       join(2);
     }));
   }
+  for (int K : {8})
+    for (int ramp : {0, 1})
+      for (int blocks : {148}) {
+        float t = timed([&] { chain_zc(K, ramp, blocks); });
+        std::printf(", \"chainzc_K%d_r%d_b%d\": %.4f", K, ramp, blocks, t);
+      }
+  for (int blocks : {148, 592})
+    std::printf(", \"zc_in_ce_out_b%d\": %.4f", blocks, timed([&] {
+      fork(2);
+      zc_copy<<<blocks, 512, 0, st[0]>>>((const double2*)hU, (double2*)dU, ND / 2);
+      zc_copy<<<blocks, 512, 0, st[0]>>>((const double2*)hu, (double2*)du, NS / 2);
+      cudaMemcpyAsync(hR, dR, ND * 8, cudaMemcpyDeviceToHost, st[1]);
+      join(2);
+    }));
+  for (int K : {8, 16, 32})
+    for (int ramp : {0, 1})
+      for (int blocks : {148, 592}) {
+        float t = timed([&] { chain_zcin(K, ramp, blocks); });
+        std::printf(", \"chainzcin_K%d_r%d_b%d\": %.4f", K, ramp, blocks, t);
+      }
   std::printf("}\n");
   CK(cudaDeviceSynchronize());
   return 0;

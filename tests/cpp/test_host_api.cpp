@@ -335,14 +335,49 @@ static void test_general_models() {  // test_spatial.cpp:67-89, models.hpp:108-1
   CHECK(mismatch);
 }
 
+// Vec's allocator: large blocks are page-locked and recycled by size when a
+// device is present, plain malloc otherwise; either way a vector works.
+static void test_vec_allocator(bool device) {
+  const size_t n = size_t(1) << 17;  // 1 MiB: above the page-locking threshold
+  const double *first = nullptr, *second = nullptr;
+  {
+    Vec a(n, 1.5);
+    first = a.data();
+    double s = 0.0;
+    for (double v : a) s += v;
+    CHECK(s == 1.5 * double(n));
+    Vec b(a);  // a second live block of the same size
+    CHECK(b.data() != a.data() && b[n - 1] == 1.5);
+    second = b.data();
+  }
+  Vec c(n);  // uninitialised, like Eigen::VectorXd(n)
+  c[0] = 2.0;
+  CHECK(c[0] == 2.0);
+  if (device) CHECK(c.data() == first || c.data() == second);  // recycled by size
+  Vec small(3, 0.25), grown;
+  for (int i = 0; i < 100000; ++i) grown.push_back(double(i));  // crosses the threshold
+  CHECK(small[2] == 0.25 && grown[99999] == 99999.0);
+}
+
+static void test_vec_pool_recycles() {  // needs a device
+  const size_t n = size_t(1) << 18;
+  const double* p0;
+  { Vec a(n); p0 = a.data(); }
+  Vec b(n);
+  CHECK(b.data() == p0);  // the freed page-locked block is handed out again
+}
+
 int main(int argc, char** argv) {
   test_node_coords();
   test_global_mass();
   test_interpolate_and_l2();
   if (argc > 1 && std::string(argv[1]) == "--host-only") {  // no device needed
+    test_vec_allocator(false);
     std::printf("passed %d failed %d\n", g_pass, g_fail);
     return g_fail == 0 ? 0 : 1;
   }
+  test_vec_allocator(true);
+  test_vec_pool_recycles();
   test_stdg_equals_rk();
   test_st_residual_constant_and_dt();
   test_st_jacobian_fd();

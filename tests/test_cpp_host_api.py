@@ -44,3 +44,17 @@ def test_cpp_host_api_runs(tmp_path):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "failed 0" in r.stdout
+
+
+@pytest.mark.parametrize("threads", ["1", "3", "8"])
+def test_host_copy_pool_equals_memcpy(tmp_path, threads):
+    """The worker-thread copies behind pageable host buffers
+    (csrc/hostcopy.hpp): ragged multi-item copies equal memcpy."""
+    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else shutil.which("g++")
+    exe = tmp_path / "test_hostcopy"
+    subprocess.run([cxx, "-std=c++17", "-O2", "-Wall", "-Wextra", "-pthread",
+                    str(ROOT / "tests" / "cpp" / "test_hostcopy.cpp"), "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120,
+                       env={**os.environ, "STG_HOST_THREADS": threads})
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert f"threads {threads} failed 0" in r.stdout

@@ -210,6 +210,44 @@ def test_host_buffer_variant_matches_device(cfg):
     assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("cfg", [
+    make(3, 3, 4, (16, 8, 6), (-0.7, 0.4, -1.1)),      # fast kernel, z-downwind neighbours
+    make(3, 3, 4, (8, 8, 5), (0.3, -0.4, 1.1)),        # chunks of unequal size (5 layers, K = 5)
+    make(2, 4, 5, (40, 32), (1.0, 0.5)),               # plane kernel: staged copies around it
+    make(1, 3, 4, (16384,), (1.0,)),                   # lane kernel
+], ids=["negvel", "ragged", "d2", "d1"])
+def test_pageable_and_pinned_host_buffers_agree(cfg):
+    """Pageable caller memory goes through the library's page-locked mirrors
+    and worker threads (hostcopy.hpp), page-locked memory straight to the
+    copy engines: R(U), the slab step and the stage step return the same bits
+    as the device-resident calls either way, call after call."""
+    assert cfg.n_dof * 8 >= 1 << 20  # large enough for the staged path
+    op = SlabOperator(**cfg.kwargs())
+    U, un = C.random_slab(cfg), C.initial_state(cfg)
+    Rd = op.st_residual(0.0, cfg.dt, dev(un), dev(U)).cpu().numpy()
+    pU = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    pu = torch.empty(cfg.n_sdof, dtype=torch.float64, pin_memory=True)
+    pR = torch.empty(cfg.n_dof, dtype=torch.float64, pin_memory=True)
+    pU.numpy()[:] = U
+    pu.numpy()[:] = un
+    for _ in range(3):
+        assert np.array_equal(op.st_residual_host(0.0, cfg.dt, un, U), Rd)
+        pR.zero_()
+        op.st_residual_host(0.0, cfg.dt, pu.numpy(), pU.numpy(), out=pR.numpy())
+        assert np.array_equal(pR.numpy(), Rd)
+        # mixed: page-locked inputs, pageable result
+        assert np.array_equal(op.st_residual_host(0.0, cfg.dt, pu.numpy(), pU.numpy()), Rd)
+    nc = NewtonConfig(abs_tol=0.0, rel_tol=1e-9, gmres_tol=1e-10)
+    Ud, ud, _ = op.stdg_step(0.0, cfg.dt, dev(un), nc)
+    Uh, uh, _ = op.stdg_step_host(0.0, cfg.dt, un, nc)
+    assert np.array_equal(Uh, Ud.cpu().numpy()) and np.array_equal(uh, ud.cpu().numpy())
+    Uh, uh, _ = op.stdg_step_host(0.0, cfg.dt, pu.numpy(), nc)
+    assert np.array_equal(Uh, Ud.cpu().numpy()) and np.array_equal(uh, ud.cpu().numpy())
+    Sd, sd, _ = op.rk_step(L.STG_FORM_A_INV, 0.0, cfg.dt, dev(un), nc)
+    Sh, sh, _ = op.rk_step_host(L.STG_FORM_A_INV, 0.0, cfg.dt, un, nc)
+    assert np.array_equal(Sh, Sd.cpu().numpy()) and np.array_equal(sh, sd.cpu().numpy())
+
+
 # ---- solvers ---------------------------------------------------------------------
 def test_c1_slab_solve_vs_oracle():
     cfg = C.CONFIGS["c1"]
