@@ -422,6 +422,7 @@ def run_ours(args):
         op.st_residual_host(0.0, cfg.dt, pgun, pgU, out=pgR)
     torch.cuda.synchronize()
     pg_s = (time.perf_counter() - t0) / max(3, e2e_steps // 5)
+    pg_exact = bool(np.array_equal(pgR, npR))
 
     # this box's PCIe rates for the same pinned buffers (the e2e bound): one
     # way each, and the e2e call's bytes (U + u_n in, R out) both ways at once
@@ -492,7 +493,10 @@ def run_ours(args):
                     "d2h_bytes_per_step": 8 * cfg.n_dof,
                     "path": "stg_st_residual_host (pinned host buffers)",
                     "output_bitwise_equal_device": e2e_exact,
-                    "pageable_dof_per_s": cfg.n_dof / pg_s, "pcie_pinned": pcie},
+                    "pageable_dof_per_s": cfg.n_dof / pg_s,
+                    "pageable_path": "the library's worker threads stage the caller's pageable "
+                                     "buffers through page-locked mirrors (csrc/hostcopy.hpp)",
+                    "pageable_bitwise_equal_pinned": pg_exact, "pcie_pinned": pcie},
             "gpu_launches": launches,
             "launch_gate": {"spin_cycles": gate_cycles(args.steps),
                             "host_enqueue_ms": 1e3 * enqueue_s, "timed_ms": ms},

@@ -212,9 +212,9 @@ def test_host_buffer_variant_matches_device(cfg):
 
 @pytest.mark.parametrize("cfg", [
     make(3, 3, 4, (16, 8, 6), (-0.7, 0.4, -1.1)),      # fast kernel, z-downwind neighbours
-    make(3, 3, 4, (8, 8, 5), (0.3, -0.4, 1.1)),        # chunks of unequal size (5 layers, K = 5)
+    make(3, 3, 4, (8, 8, 10), (0.3, -0.4, 1.1)),       # chunks of unequal size (10 layers, K = 8)
     make(2, 4, 5, (40, 32), (1.0, 0.5)),               # plane kernel: staged copies around it
-    make(1, 3, 4, (16384,), (1.0,)),                   # lane kernel
+    make(1, 3, 4, (16384,), (1.0,), dt=1e-4),          # lane kernel
 ], ids=["negvel", "ragged", "d2", "d1"])
 def test_pageable_and_pinned_host_buffers_agree(cfg):
     """Pageable caller memory goes through the library's page-locked mirrors
