@@ -195,6 +195,12 @@ struct stg_handle {
   static constexpr int kChunks = 8;
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_start = nullptr, ev_in[kChunks] = {}, ev_c[kChunks] = {};
+  // GMRES speculation: the iteration count of the last converged solve, per
+  // Newton-iteration index of the enclosing newton() call (slot 0 outside
+  // one); the driver does not enqueue a speculative Arnoldi step past it
+  static constexpr int kPredSlots = 8;
+  int gmres_pred[kPredSlots] = {};
+  int pred_slot = 0;
   // pageable callers: page-locked mirrors and the events of their D2H chunks
   PinBuf pin_U, pin_R, pin_u, pin_u2;
   std::vector<cudaEvent_t> ev_stage;
@@ -563,6 +569,12 @@ struct GmresStats {
 // launches once step k has converged or broken down, or needs a second
 // Gram-Schmidt pass -- which the host then enqueues before re-enqueueing step
 // k+1.  lag 0 (pipelined = false, or STG_GMRES_SYNC=1) waits after every step.
+// The speculation stops at the iteration count the previous solve in the same
+// position (the same Newton-iteration index) converged at: slab after slab
+// the counts repeat, so the step that would only be a row of empty launches
+// (2-4 us each: 11 of them per c4 step) is not enqueued; a solve that needs
+// more pays one host round trip there and speculates on
+// (STG_GMRES_NO_PREDICT=1: always speculate).
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
                  bool pipelined = true, double b_sign = 1.0, bool want_rel = true,
@@ -682,6 +694,8 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     ck(cudaEventRecord(h->ev_re, s), "event");
   };
 
+  static const bool no_predict = std::getenv("STG_GMRES_NO_PREDICT") != nullptr;
+  const int pred = no_predict ? 0 : h->gmres_pred[h->pred_slot];  // 0: none yet
   std::vector<double> y(static_cast<size_t>(m), 0.0);
   int total = 0;
   bool first = true;
@@ -738,8 +752,11 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     h->launches++;
     auto can_enqueue = [&](int j) { return j < m && total + j < max_it; };
     int k = 0, enq = 0, status = 0;
+    // a speculative step (e > k) that would be iteration pred + 1 waits for
+    // step pred's outcome
+    auto worth = [&](int e) { return e <= k || total + e != pred; };
     while (true) {
-      while (enq <= k + lag && can_enqueue(enq)) {  // step k and, speculatively, k + lag
+      while (enq <= k + lag && can_enqueue(enq) && worth(enq)) {  // step k and, speculatively, k + lag
         enqueue_step(enq);
         ++enq;
       }
@@ -822,6 +839,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     h->launches++;
   }
   st.iterations = total;
+  if (st.converged) h->gmres_pred[h->pred_slot] = total;
   check_launch(h);
   return st;
 }
@@ -890,6 +908,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     // zero fill (gmres with x_zero writes it)
     GmresStats gs;
     {
+      h->pred_slot = std::min(out.iterations, stg_handle::kPredSlots - 1);
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
                  J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/true,
                  /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready, /*add_to=*/u);
@@ -2815,6 +2834,7 @@ int stg_gmres_st(stg_handle* h, double t_n, double dt, const double* U, const do
     h->eblock_valid = false;
     const Op A = [h, dt, U](const double* v, double* Jv) { st_jvp(h, dt, U, v, Jv, 0.0); };
     const Op P = precond_for(h, precond, st_mix(h, dt, false), U, A);
+    h->pred_slot = 0;
     const GmresStats st = gmres(h, A, b, x, h->n_dof, restart, tol, max_it, P ? &P : nullptr,
                                 /*x_zero=*/false, /*pipelined=*/true);
     if (iterations) *iterations = st.iterations;
