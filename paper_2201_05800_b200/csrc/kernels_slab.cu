@@ -2023,6 +2023,13 @@ int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   if (occ < 1) occ = 1;
   int grid = occ * num_sms();
   if (grid > nseg) grid = nseg;
+  // STG_FAST_GRID=g: A/B knob for the persistent grid size (scripts/grid_sweep.sh:
+  // 410 CTAs, ten equal rounds of the 4096 c4 segments, is no faster than 444)
+  static const int grid_env = [] {
+    const char* e = std::getenv("STG_FAST_GRID");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (grid_env > 0 && grid_env < grid) grid = grid_env;
   if (red) cudaMemsetAsync(a.red_max, 0, sizeof(unsigned long long), s);
   launch_ex(a.no_pdl ? 0 : kPdlSlab, kern, grid, pst::THREADS, lay.smem, s, m, a, lay);
   return 1;
