@@ -12,6 +12,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -2682,12 +2683,75 @@ int stg_host_free(double* p) {
   });
 }
 
+namespace {
+// stg_memcpy between pageable host memory and the device: a process-wide ring
+// of four 8 MiB page-locked slots on the legacy default stream (the ordering
+// cudaMemcpy has); the worker threads (hostcopy.hpp) fill or drain one slot
+// while the copy engine moves the others.
+void memcpy_staged(double* dst, const double* src, size_t n, bool h2d) {
+  constexpr int kSlots = 4;
+  constexpr size_t kSlot = kStageChunk;
+  static std::mutex mu;
+  static double* slot[kSlots] = {};
+  std::lock_guard<std::mutex> lk(mu);
+  for (double*& p : slot)
+    if (!p)
+      ck(cudaHostAlloc(reinterpret_cast<void**>(&p), kSlot * sizeof(double), cudaHostAllocPortable),
+         "cudaHostAlloc");
+  cudaEvent_t ev[kSlots] = {};
+  struct Guard {
+    cudaEvent_t* e;
+    ~Guard() {
+      for (int i = 0; i < kSlots; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  for (cudaEvent_t& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  stg::HostCopyPool& pool = stg::HostCopyPool::get();
+  const size_t nchunk = (n + kSlot - 1) / kSlot;
+  auto cnt_of = [&](size_t i) { return std::min(kSlot, n - i * kSlot); };
+  if (h2d) {
+    for (size_t i = 0; i < nchunk; ++i) {
+      const int sl = int(i % kSlots);
+      if (i >= size_t(kSlots)) ck(cudaEventSynchronize(ev[sl]), "sync");  // slot drained
+      const stg::CopyItem it{slot[sl], src + i * kSlot, cnt_of(i) * sizeof(double)};
+      pool.par_copy(&it, 1);
+      ck(cudaMemcpyAsync(dst + i * kSlot, slot[sl], cnt_of(i) * sizeof(double),
+                         cudaMemcpyHostToDevice, cudaStreamLegacy), "H2D");
+      ck(cudaEventRecord(ev[sl], cudaStreamLegacy), "event");
+    }
+    ck(cudaStreamSynchronize(cudaStreamLegacy), "sync");
+    return;
+  }
+  auto issue = [&](size_t i) {
+    const int sl = int(i % kSlots);
+    ck(cudaMemcpyAsync(slot[sl], src + i * kSlot, cnt_of(i) * sizeof(double),
+                       cudaMemcpyDeviceToHost, cudaStreamLegacy), "D2H");
+    ck(cudaEventRecord(ev[sl], cudaStreamLegacy), "event");
+  };
+  for (size_t i = 0; i < std::min(nchunk, size_t(kSlots)); ++i) issue(i);
+  for (size_t i = 0; i < nchunk; ++i) {
+    const int sl = int(i % kSlots);
+    ck(cudaEventSynchronize(ev[sl]), "sync");
+    const stg::CopyItem it{dst + i * kSlot, slot[sl], cnt_of(i) * sizeof(double)};
+    pool.par_copy(&it, 1);
+    if (i + kSlots < nchunk) issue(i + kSlots);
+  }
+}
+}  // namespace
+
 int stg_memcpy(double* dst, const double* src, long long n, int dir) {
   return guarded(nullptr, [&] {
     if (n < 0 || dir < 0 || dir > 2) throw std::invalid_argument("stg_memcpy: bad arguments");
     if (n == 0) return;
     need(dst, "dst");
     need(src, "src");
+    static const bool no_staging = std::getenv("STG_HOST_NO_STAGING") != nullptr;
+    if (dir < 2 && !no_staging && size_t(n) * sizeof(double) >= (size_t(1) << 21) &&
+        pageable(dir == 0 ? static_cast<const void*>(src) : static_cast<const void*>(dst))) {
+      memcpy_staged(dst, src, size_t(n), dir == 0);
+      return;
+    }
     const cudaMemcpyKind k = dir == 0   ? cudaMemcpyHostToDevice
                              : dir == 1 ? cudaMemcpyDeviceToHost
                                         : cudaMemcpyDeviceToDevice;
