@@ -168,6 +168,10 @@ struct SlabArgs {
   int full_s;   // S not diagonal
   int model;
   const double* X;  // n_in blocks
+  // X holds ONE spatial block standing for all n_in (the initial guess
+  // 1 (x) u_n of a slab solve, never written out): fast 3-D kernel only (its
+  // tensor maps get a zero temporal stride); other launchers return -1
+  int x_bcast;
   const double* U;  // linearisation point (jvp && burgers), n_in blocks
   const double* W;  // spatial vector or null
   double* R;        // n_out blocks
@@ -210,6 +214,7 @@ bool fd_fused_supported(const SlabArgs& a);
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s);
 // Fast TMA path: d = 3, n = 4, n_in = n_out = 4, advection, nx % 8 == 0.
 bool slab_fast_supported(const SlabArgs& a);
+bool slab_fast_bcast_ok();
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s);
 
 // ---- general flux models, d in {1, 2} (kernels_general.cu) -----------------
@@ -472,9 +477,12 @@ void vec_update_dot(double* w, const double* V, long long ldv, int k, const doub
 // y = sign * x / sqrt(*nrm2)  (nrm2 on device)
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
                        cudaStream_t s, double sign = 1.0);
-// x = (accumulate ? x : 0) + sum_{j<k} y[j] V_j (y on device), k <= 64
+// x = (accumulate ? x : 0) + sum_{j<k} y[j] V_j (y on device), k <= 64.
+// bsrc != null: the old x is bsrc repeated with period bper doubles (n a
+// multiple of bper) and is not read from x: x = 1 (x) bsrc + sum y_j V_j.
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
-                 cudaStream_t s, bool accumulate = true);
+                 cudaStream_t s, bool accumulate = true, const double* bsrc = nullptr,
+                 long long bper = 1);
 // Central-difference Jacobian action on the device, no host scalars:
 // e = c * sqrt(1 + sqrt(*uu)) / sqrt(*vv) (uu null: e = c / sqrt(*vv); e = 1
 // if <v,v> = 0).  fd_pm: Up = U + e v, Um = U - e v.  fd_diff: Jv = (Jv - Fm) / 2e.

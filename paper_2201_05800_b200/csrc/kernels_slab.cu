@@ -1873,6 +1873,7 @@ bool slab_generic_reduces(const SlabArgs& a) {
 }
 
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
+  if (a.x_bcast) return -1;  // (the caller writes the broadcast out first)
   const int d = a.g.dim, n1 = a.g.n1;
   t_last_reduced = false;
   if (d == 1) {
@@ -1956,11 +1957,28 @@ bool slab_fast_reduces(const SlabArgs& a) {
          a.seg_end == 0 && slab_fast_supported(a) && fast_variant() != 1;
 }
 
+// whether the driver encodes a tensor map whose temporal stride is 0 (X one
+// spatial block read as all n_in: SlabArgs::x_bcast)
+bool slab_fast_bcast_ok() {
+  static const int ok = [] {
+    EncodeFn enc = get_encode();
+    if (!enc || std::getenv("STG_NO_LAZY_GUESS")) return 0;
+    alignas(64) static double dummy[8];
+    CUtensorMap map;
+    const cuuint64_t gdim[4] = {16, 4, pst::E, 4};
+    const cuuint64_t gstride[3] = {128, 512, 0};
+    const cuuint32_t box[4] = {16, 4, pst::E, 4};
+    return encode(enc, &map, dummy, 4, gdim, gstride, box, CU_TENSOR_MAP_SWIZZLE_128B) ? 1 : 0;
+  }();
+  return ok != 0;
+}
+
 int launch_slab_fast(const SlabArgs& a, cudaStream_t s) {
   EncodeFn enc = get_encode();
   if (!enc) return -1;
+  if (a.x_bcast && !slab_fast_bcast_ok()) return -1;
   const cuuint64_t cells = cuuint64_t(a.g.n_cells);
-  const cuuint64_t tstride = cuuint64_t(a.g.n_sdof) * 8;
+  const cuuint64_t tstride = a.x_bcast ? 0 : cuuint64_t(a.g.n_sdof) * 8;
   if (fast_variant() == 1) {
     CUtensorMap map;
     const cuuint64_t gdim[4] = {16, 4, cells, 4};

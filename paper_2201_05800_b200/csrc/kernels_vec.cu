@@ -210,7 +210,9 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
                                                       double* scale_out, double* out,
                                                       unsigned* counter,
                                                       const double* __restrict__ hn2, Skip skip,
-                                                      GivensArgs gv) {
+                                                      GivensArgs gv,
+                                                      const double* __restrict__ bsrc,
+                                                      long long bper) {
   pdl_entry();
   if (skip_now(skip)) return;
   using O = VecT<W>;
@@ -245,7 +247,11 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
   double acc[1] = {0.0};
   for (long long i = blockIdx.x * (long long)kVecBlock + threadIdx.x; i < nw;
        i += (long long)gridDim.x * kVecBlock) {
-    typename O::T x = accumulate ? O::ld(w, i) : O::zero();
+    // accumulate 2: the old w is bsrc repeated with period bper (the lazy
+    // initial guess 1 (x) u_n, never written out)
+    typename O::T x = accumulate == 1   ? O::ld(w, i)
+                      : accumulate == 2 ? O::ld(bsrc, i % bper)
+                                        : O::zero();
 #pragma unroll
     for (int g = 0; g < KMAX; g += kGroup) {
       if (g < kk) {
@@ -550,20 +556,24 @@ void vec_update_dot(double* w, const double* V, long long ldv, int k, const doub
   unsigned* c = counter_of(partial);
   STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_update<KM, WW>, multi_grid<KM, WW, true>(n), kVecBlock, 0, s, 
                            w, V, ldv, k, h, n / WW, -1.0, 1, partial, scale_src, scale_out,
-                           out2 + k, c, hn2, skip, gv)));
+                           out2 + k, c, hn2, skip, gv, nullptr, 1LL)));
   if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s, skip);  // <V_j, w_new>
 }
 
 void vec_combine(double* x, const double* V, long long ldv, int k, const double* y, long long n,
-                 cudaStream_t s, bool accumulate) {
+                 cudaStream_t s, bool accumulate, const double* bsrc, long long bper) {
   if (k == 0) {
-    if (!accumulate) vec_fill(x, 0.0, n, s);
+    if (bsrc) vec_broadcast(x, bsrc, int(n / bper), bper, s);
+    else if (!accumulate) vec_fill(x, 0.0, n, s);
     return;
   }
-  const int W = vec_width(n, ldv, V, x);
+  int W = vec_width(n, ldv, V, x);
+  if (bsrc && (bper % 2 != 0 || !aligned16(bsrc))) W = 1;
+  const int mode = bsrc ? 2 : (accumulate ? 1 : 0);
   STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_update<KM, WW>, multi_grid<KM, WW, true>(n), kVecBlock, 0, s, 
-                           x, V, ldv, k, y, n / WW, 1.0, accumulate ? 1 : 0, nullptr, nullptr,
-                           nullptr, nullptr, nullptr, nullptr, Skip{}, GivensArgs{})));
+                           x, V, ldv, k, y, n / WW, 1.0, mode, nullptr, nullptr,
+                           nullptr, nullptr, nullptr, nullptr, Skip{}, GivensArgs{}, bsrc,
+                           bper / WW)));
 }
 
 void vec_maxabs(const double* x, long long n, double* partial, double* out, cudaStream_t s) {

@@ -196,6 +196,13 @@ struct stg_handle {
   static constexpr int kChunks = 8;
   cudaStream_t s_in = nullptr, s_out = nullptr;
   cudaEvent_t ev_start = nullptr, ev_in[kChunks] = {}, ev_c[kChunks] = {};
+  // Lazy initial guess of a slab / stage solve: lazy_dst (the solve's U) is
+  // notionally 1 (x) lazy_src but has not been written; the fast 3-D kernel
+  // reads lazy_src through zero-stride tensor maps and the first Newton
+  // update writes U = 1 (x) lazy_src + correction.  materialise() writes it
+  // out for any other reader.
+  const double* lazy_src = nullptr;
+  double* lazy_dst = nullptr;
   // GMRES speculation: the iteration count of the last converged solve, per
   // Newton-iteration index of the enclosing newton() call (slot 0 outside
   // one); the driver does not enqueue a speculative Arnoldi step past it
@@ -296,11 +303,37 @@ void apply_general(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, c
   }
 }
 
+// write the lazy initial guess out (no-op when there is none)
+void materialise(stg_handle* h) {
+  if (!h->lazy_src) return;
+  stg::vec_broadcast(h->lazy_dst, h->lazy_src, h->nt, h->n_sdof, h->stream);
+  h->launches++;
+  h->lazy_src = nullptr;
+}
+
 void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const double* X,
            const double* U, const double* W, double* R, bool jvp, bool full_s,
            int seg_begin = 0, int seg_end = 0) {
   h->red_done = false;
   stg::SlabArgs a{};
+  if (h->lazy_src && (X == h->lazy_dst || U == h->lazy_dst || W == h->lazy_dst)) {
+    // the fast 3-D kernel can read the unwritten guess; everything else
+    // needs it in memory
+    stg::SlabArgs probe{};
+    probe.g = h->g;
+    probe.n_in = n_in;
+    probe.n_out = n_out;
+    probe.model = h->desc.model;
+    probe.X = h->lazy_src;
+    if (X == h->lazy_dst && U != h->lazy_dst && W != h->lazy_dst && !jvp && n_in == h->nt &&
+        seg_end == 0 && h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(probe) &&
+        stg::slab_fast_bcast_ok()) {
+      X = h->lazy_src;
+      a.x_bcast = 1;
+    } else {
+      materialise(h);
+    }
+  }
   a.seg_begin = seg_begin;
   a.seg_end = seg_end;
   a.sp = h->sp;
@@ -790,7 +823,13 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       // caller's vector (Newton's u += du without du)
       stg::gmres_backsub(G, k, dsm + 256, s);
       if (add_to && !x_set) {
-        stg::vec_combine(add_to, P ? Z : V, ld, k, dsm + 256, n, s, true);
+        if (h->lazy_src && add_to == h->lazy_dst) {  // u = 1 (x) lazy_src + correction
+          stg::vec_combine(add_to, P ? Z : V, ld, k, dsm + 256, n, s, true, h->lazy_src,
+                           h->n_sdof);
+          h->lazy_src = nullptr;
+        } else {
+          stg::vec_combine(add_to, P ? Z : V, ld, k, dsm + 256, n, s, true);
+        }
         st.added = true;
       } else {
         stg::vec_combine(x, P ? Z : V, ld, k, dsm + 256, n, s, x_set);
@@ -920,6 +959,7 @@ NewtonOut newton(stg_handle* h, const Op& residual,
       throw std::runtime_error("linear_solve: GMRES did not converge, error " +
                                fmt_short(gs.rel_residual));
     if (!gs.added) {  // (gmres added the correction into u itself otherwise)
+      if (u == h->lazy_dst) materialise(h);
       stg::vec_axpy(u, 1.0, du, n, h->stream);
       h->launches++;
     }
@@ -2391,6 +2431,33 @@ bool small_solve(stg_handle* h, bool rk, const stg::MixCoef& mres, const stg::Mi
   return true;
 }
 
+// The initial guess 1 (x) u of a slab / stage solve.  For linear advection on
+// the fast 3-D path it is not written: the first residual reads u through
+// zero-stride tensor maps and the first Newton update writes
+// U = 1 (x) u + correction (apply, gmres).  Otherwise, and whenever anything
+// else needs U, it is broadcast into U.  The destructor writes it out if it
+// is still pending (Newton converged at once, or an exception: U must hold
+// the last iterate, newton.hpp:40-48).
+struct LazyGuess {
+  stg_handle* h;
+  LazyGuess(stg_handle* hh, double* U, const double* u) : h(hh) {
+    h->lazy_dst = U;
+    h->lazy_src = u;
+    const bool lazy = h->desc.model == STG_MODEL_ADVECTION && h->g.dim == 3 &&
+                      h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_bcast_ok();
+    if (!lazy) materialise(h);
+  }
+  ~LazyGuess() {
+    try {
+      materialise(h);
+    } catch (...) {
+    }
+    h->lazy_dst = nullptr;
+  }
+  LazyGuess(const LazyGuess&) = delete;
+  LazyGuess& operator=(const LazyGuess&) = delete;
+};
+
 void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
                   const stg_newton_config* cfgp, double* U, double* u_next,
                   stg_solve_info* info) {
@@ -2403,8 +2470,8 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
                   "stdg_step element at t=" + fmt_short(t_n) + ", dt=" + fmt_short(dt)))
     return;
   h->eblock_valid = false;
-  stg::vec_broadcast(U, u_n, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u_n (stdg.hpp:131)
-  h->launches++;
+  // guess 1 (x) u_n (stdg.hpp:131)
+  LazyGuess guess(h, U, u_n);
   const double eps = cfg.fd_eps;
   NewtonOut o;
   try {
@@ -2428,6 +2495,7 @@ void do_stdg_step(stg_handle* h, double t_n, double dt, const double* u_n,
                                   ": " + e.what(),
                               e.history, e.linear_iterations);
   }
+  materialise(h);  // (Newton converged at the initial guess)
   if (u_next) {
     stg::vec_copy(u_next, U + (h->nt - 1) * h->n_sdof, h->n_sdof, h->stream);
     h->launches++;
@@ -2450,8 +2518,8 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
       return;
   }
   h->eblock_valid = false;
-  stg::vec_broadcast(U, u, h->nt, h->n_sdof, h->stream);  // guess 1 (x) u (lodg.hpp:131)
-  h->launches++;
+  // guess 1 (x) u (lodg.hpp:131)
+  LazyGuess guess(h, U, u);
   const double eps = cfg.fd_eps;
   NewtonOut o;
   try {
@@ -2473,6 +2541,7 @@ void do_rk_step(stg_handle* h, int form, double t, double dt, const double* u,
                                   e.what(),
                               e.history, e.linear_iterations);
   }
+  materialise(h);  // (Newton converged at the initial guess)
   if (u_next) {
     // u_next = u + dt sum_j b_j F(U_j)  (lodg.hpp:142-145)
     stg::MixCoef m = zero_mix();
