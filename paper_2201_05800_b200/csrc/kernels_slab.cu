@@ -953,6 +953,7 @@ __global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
   const int e = tid % E, t = tid / E;
   const int nx = a.g.nx, ny = a.g.ny;
   const long long ns = a.g.n_sdof;
+  const long long xs = a.x_bcast ? 0 : ns;  // temporal stride of X (x_bcast: one block)
   const int nseg = a.g.n_cells / E;
   const uint32_t pbytes = PL * 8;
   const bool nLx = a.sp.cL[0] != 0.0, nRx = a.sp.cR[0] != 0.0;
@@ -975,13 +976,13 @@ __global__ void __launch_bounds__(Plane3<N1, NT, E>::THREADS, 2)
     ptx::mbar_expect_tx(bar, (NT + (hw ? 1 : 0)) * pbytes);
     const uint32_t dst = ptx::smem_u32(sm3 + stg * P::STAGE);
     const double* src = a.X + (long long)sg * PL;
-    for (int j = 0; j < NT; ++j) bulk_g2s(dst + j * pbytes, src + j * ns, pbytes, bar);
+    for (int j = 0; j < NT; ++j) bulk_g2s(dst + j * pbytes, src + j * xs, pbytes, bar);
     if (hw) bulk_g2s(ptx::smem_u32(Ws + wsl * PL), a.W + (long long)sg * PL, pbytes, bar);
   };
   auto faces = [&](int sg, double* xl, double* xr, double* yl, double* yr) {
     const int cell = sg * E + e;
     const int cx = cell % nx, cy = (cell / nx) % ny;
-    const double* Xt = a.X + t * ns;
+    const double* Xt = a.X + t * xs;
     if (nLx && !(e > 0 && cx > 0)) {
       const double* q = Xt + (long long)(cell - cx + (cx == 0 ? nx - 1 : cx - 1)) * CS + N1 - 1;
 #pragma unroll
@@ -1784,6 +1785,12 @@ int launch2d_t(const SlabArgs& a, cudaStream_t s) {
   using Sh = Shape2d<N1, NT>;
   using P = P2d<N1, NT>;
   if constexpr (N1 <= 5) {  // n = 6 would spill the register tile
+    if (a.x_bcast) {  // only the 3-stage plane kernel reads a one-block X
+      static const bool p2b = std::getenv("STG_2D_PLANE2") != nullptr;
+      if (!p2b && kPlaneEnv == 32 && plane3_ok<N1, NT, 32>(a))
+        return launch_plane3<N1, NT, 32>(a, s);
+      return -1;
+    }
     if (kPlaneEnv == 16 && plane2d_ok<N1, NT, 16>(a)) return launch_plane2d<N1, NT, 16, 3>(a, s);
     if (kPlaneEnv == 33 && plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 1>(a, s);
     // 2 CTAs/SM: caps the tile kernel at 200 registers (202 would round to
@@ -1794,6 +1801,7 @@ int launch2d_t(const SlabArgs& a, cudaStream_t s) {
     if (!p2 && kPlaneEnv == 32 && plane3_ok<N1, NT, 32>(a)) return launch_plane3<N1, NT, 32>(a, s);
     if (plane2d_ok<N1, NT, 32>(a)) return launch_plane2d<N1, NT, 32, 2>(a, s);
   }
+  if (a.x_bcast) return -1;
   if (a.g.n_cells % Sh::E == 0 && (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 &&
       (a.g.n_sdof % 2) == 0 && !std::getenv("STG_2D_NONPERSIST")) {
     static int occ_dev[kMaxDevices];
@@ -1873,9 +1881,14 @@ bool slab_generic_reduces(const SlabArgs& a) {
 }
 
 int launch_slab_generic(const SlabArgs& a, cudaStream_t s) {
-  if (a.x_bcast) return -1;  // (the caller writes the broadcast out first)
   const int d = a.g.dim, n1 = a.g.n1;
   t_last_reduced = false;
+  // a one-block X (x_bcast) is read by the d = 2 plane kernel only: -1
+  // elsewhere, before anything is launched (the caller writes the broadcast
+  // out and calls again)
+  if (a.x_bcast && !(d == 2 && a.model == int(Model::advection) && a.n_out <= a.n_in &&
+                     slab_fast_bcast_ok() && !std::getenv("STG_GENERIC_2D")))
+    return -1;
   if (d == 1) {
     switch (n1) {
       case 2: return launch1d<2>(a, s);

@@ -316,23 +316,14 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
            int seg_begin = 0, int seg_end = 0) {
   h->red_done = false;
   stg::SlabArgs a{};
+  // the lazy initial guess as X: the fast 3-D kernel and the d = 2 plane
+  // kernel read the one block it stands for; every other reader needs it in
+  // memory
+  bool lazy_x = false;
   if (h->lazy_src && (X == h->lazy_dst || U == h->lazy_dst || W == h->lazy_dst)) {
-    // the fast 3-D kernel can read the unwritten guess; everything else
-    // needs it in memory
-    stg::SlabArgs probe{};
-    probe.g = h->g;
-    probe.n_in = n_in;
-    probe.n_out = n_out;
-    probe.model = h->desc.model;
-    probe.X = h->lazy_src;
-    if (X == h->lazy_dst && U != h->lazy_dst && W != h->lazy_dst && !jvp && n_in == h->nt &&
-        seg_end == 0 && h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(probe) &&
-        stg::slab_fast_bcast_ok()) {
-      X = h->lazy_src;
-      a.x_bcast = 1;
-    } else {
-      materialise(h);
-    }
+    lazy_x = X == h->lazy_dst && U != h->lazy_dst && W != h->lazy_dst && !jvp &&
+             n_in == h->nt && seg_end == 0 && !general_model(h->desc.model);
+    if (!lazy_x) materialise(h);
   }
   a.seg_begin = seg_begin;
   a.seg_end = seg_end;
@@ -345,7 +336,8 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
   a.jvp = jvp ? 1 : 0;
   a.full_s = full_s ? 1 : 0;
   a.model = h->desc.model;
-  a.X = X;
+  a.X = lazy_x ? h->lazy_src : X;
+  a.x_bcast = lazy_x ? 1 : 0;
   a.U = U;
   a.W = W;
   a.R = R;
@@ -360,15 +352,24 @@ void apply(stg_handle* h, const stg::MixCoef& mx, int n_in, int n_out, const dou
     return;
   }
   int launched = -1;
-  if (h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(a)) {
-    launched = stg::launch_slab_fast(a, h->stream);
-    if (launched >= 0) h->red_done = h->red && stg::slab_fast_reduces(a);
-  } else if (h->kernel_pref == STG_KERNEL_FAST) {
-    throw std::invalid_argument("fast kernel requested but not applicable to this problem");
-  }
-  if (launched < 0) {
-    launched = stg::launch_slab_generic(a, h->stream);
-    h->red_done = h->red && launched >= 0 && stg::slab_generic_reduces(a);
+  auto launch = [&] {
+    if (h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_supported(a)) {
+      launched = stg::launch_slab_fast(a, h->stream);
+      if (launched >= 0) h->red_done = h->red && stg::slab_fast_reduces(a);
+    } else if (h->kernel_pref == STG_KERNEL_FAST) {
+      throw std::invalid_argument("fast kernel requested but not applicable to this problem");
+    }
+    if (launched < 0) {
+      launched = stg::launch_slab_generic(a, h->stream);
+      h->red_done = h->red && launched >= 0 && stg::slab_generic_reduces(a);
+    }
+  };
+  launch();
+  if (launched < 0 && a.x_bcast) {  // no kernel reads the one-block X here: write it out
+    materialise(h);
+    a.X = X;
+    a.x_bcast = 0;
+    launch();
   }
   if (launched < 0) throw std::invalid_argument("no kernel for this (dim, degree, model)");
   h->launches += launched;
@@ -2443,8 +2444,8 @@ struct LazyGuess {
   LazyGuess(stg_handle* hh, double* U, const double* u) : h(hh) {
     h->lazy_dst = U;
     h->lazy_src = u;
-    const bool lazy = h->desc.model == STG_MODEL_ADVECTION && h->g.dim == 3 &&
-                      h->kernel_pref != STG_KERNEL_GENERIC && stg::slab_fast_bcast_ok();
+    const bool lazy = h->desc.model == STG_MODEL_ADVECTION && h->g.dim >= 2 &&
+                      stg::slab_fast_bcast_ok();
     if (!lazy) materialise(h);
   }
   ~LazyGuess() {
