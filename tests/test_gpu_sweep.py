@@ -175,3 +175,36 @@ def test_sweep_stage_solves_match_block_jacobi(form):
         its.append(info.linear_iterations)
     assert rel(sols[1], sols[0]) <= TOL_SOLVE
     assert its[1] < its[0], its
+
+
+@pytest.mark.parametrize("tight", [False, True], ids=["default_budget", "tight_budget"])
+def test_lagged_blocks_are_rebuilt_when_the_state_changes(tight):
+    """The Burgers element blocks (and sweep couplings) of one step serve the
+    next few steps of a march (STG_PRECOND_LAG_STEPS).  A handle that is then
+    given an unrelated state still returns the fresh-handle solution: blocks
+    that cost clearly more GMRES steps are rebuilt, and with an iteration
+    budget the stale blocks cannot meet the solve is repeated with blocks
+    built at the current state (newton(), stg.cpp)."""
+    cfg = C.CONFIGS["c3"].scaled((4096,))
+    x = np.asarray(C.initial_state(cfg))
+    n = x.size
+    # a shock-forming state far from the smooth initial one
+    s = np.linspace(0.0, 2 * np.pi, n, endpoint=False)
+    other = dev(1.5 + 1.2 * np.sin(3 * s) + 0.4 * np.cos(7 * s))
+    kw = dict(abs_tol=1e-12, rel_tol=1e-10, gmres_tol=1e-8, fd_eps=1e-7)
+    fresh = SlabOperator(**cfg.kwargs())
+    Uf, uf, inf = fresh.stdg_step(0.0, 4 * cfg.dt, other, NewtonConfig(**kw))
+    if tight:  # barely what the fresh blocks need per Newton iteration
+        kw["gmres_max_it"] = -(-inf.linear_iterations // inf.newton_iterations) + 2
+        Uf, uf, inf = SlabOperator(**cfg.kwargs()).stdg_step(0.0, 4 * cfg.dt, other,
+                                                             NewtonConfig(**kw))
+    op = SlabOperator(**cfg.kwargs())
+    op.stdg_step(0.0, cfg.dt, dev(x), NewtonConfig(**kw))  # blocks built at the smooth state
+    Ul, ul, inl = op.stdg_step(0.0, 4 * cfg.dt, other, NewtonConfig(**kw))
+    assert rel(Ul, Uf.cpu().numpy()) <= 1e-7  # both solved to the inexact-Newton tolerance
+    assert inl.final_residual <= max(1e-12, 1e-10 * inl.residual_history[0])
+    # and a march keeps converging with the blocks of its first step
+    u = dev(x)
+    for k in range(6):
+        _, u, info = op.stdg_step(k * cfg.dt, cfg.dt, u, NewtonConfig(**kw))
+        assert info.final_residual <= max(1e-12, 1e-10 * info.residual_history[0])
