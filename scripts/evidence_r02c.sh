@@ -5,7 +5,7 @@
 # kernels inside warm solves, and their markdown summary.
 set -u
 cd "$(dirname "$0")/.." || exit 1
-O=gpurun_out/ev5; mkdir -p $O
+O=gpurun_out/ev6; mkdir -p $O
 T0=$SECONDS; python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench.py wall $((SECONDS - T0)) s" > $O/bench_time.txt
 python bench.py --impl reference --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
@@ -22,7 +22,7 @@ ncu $F -k regex:fdm3_kernel -c 1 -o $O/fdm3 python scripts/prof_solve.py c4 > $O
 ncu $F -k regex:fdm3_kernel -s 1 -c 1 -o $O/fdm3_coupled python scripts/prof_solve.py c4 > $O/l2.log 2>&1
 ncu $F -k regex:fdm2i_kernel -s 1 -c 1 -o $O/fdm2i_coupled python scripts/prof_solve.py c2 > $O/l3.log 2>&1
 ncu $F -k regex:k_sweep_win -s 2 -c 1 -o $O/sweep_win python scripts/prof_solve.py c3 > $O/l4.log 2>&1
-ncu $F -k regex:k_build_burgers -c 1 -o $O/build_blocks python scripts/prof_solve.py c3 > $O/l5.log 2>&1
+STG_PRECOND_LAG_STEPS=1 ncu $F -k regex:k_build_burgers -c 1 -o $O/build_blocks python scripts/prof_solve.py c3 > $O/l5.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:slab3d_n4_persist -s 20 -c 1 \
     -o $O/slab3d python bench.py --steps 20 --warmup 5 --no-extra --no-cpu > $O/l6.log 2>&1
 echo done > $O/done
