@@ -95,6 +95,23 @@ def test_no_cpu_fallback_without_device(lib):
     assert lib.stg_create(ctypes.byref(d), ctypes.byref(h)) == L.STG_ERR_CUDA
 
 
+def test_host_alloc_argument_checks(lib):
+    """stg_host_alloc / stg_host_free: n = 0 gives a null pointer, n < 0 is
+    invalid, and without a device a real allocation fails with STG_ERR_CUDA
+    (the C++ mirror's Vec then falls back to malloc)."""
+    from conftest import cuda_available
+    p = ctypes.c_void_p(1)
+    assert lib.stg_host_alloc(0, ctypes.byref(p)) == L.STG_OK and not p.value
+    assert lib.stg_host_alloc(-1, ctypes.byref(p)) == L.STG_ERR_INVALID
+    assert lib.stg_host_free(None) == L.STG_OK
+    code = lib.stg_host_alloc(1 << 10, ctypes.byref(p))
+    if cuda_available():
+        assert code == L.STG_OK and p.value
+        assert lib.stg_host_free(p) == L.STG_OK
+    else:
+        assert code == L.STG_ERR_CUDA and not p.value
+
+
 def test_newton_config_defaults(lib):  # newton.hpp:30-38
     c = L.StgNewtonConfig()
     lib.stg_newton_config_default(ctypes.byref(c))
