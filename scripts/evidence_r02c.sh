@@ -5,7 +5,7 @@
 # kernels inside warm solves, and their markdown summary.
 set -u
 cd "$(dirname "$0")/.." || exit 1
-O=gpurun_out/ev6; mkdir -p $O
+O=gpurun_out/ev8; mkdir -p $O
 T0=$SECONDS; python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench.py wall $((SECONDS - T0)) s" > $O/bench_time.txt
 python bench.py --impl reference --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
