@@ -146,7 +146,11 @@ struct GivensArgs {
   const double* d1 = nullptr;
   const double* sc1 = nullptr;  // scale applied by pass 0 (pass 1 reads it)
   int* host = nullptr;          // mapped pinned per-step status slots
+  // a step that converges within kInlineBacksub columns also leaves the
+  // cycle's update coefficients y_j c_j here (no k_gmres_backsub launch)
+  double* ysol = nullptr;
 };
+constexpr int kInlineBacksub = 8;
 // bb != null: beta = sqrt(*bb) on the device and tol is relative (first
 // cycle from x = 0, no host round trip); else beta and tol_abs = tol given.
 // beta = 0 sets status 4 ("no work") and writes it to every host slot.

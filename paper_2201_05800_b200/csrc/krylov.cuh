@@ -60,6 +60,19 @@ __device__ __forceinline__ void block_finish_sum(const double* part, int nblocks
 // c_j = 1/||S_j||, h_{k+1,k} = c_k ||S_{k+1}|| / scale, then the previous
 // rotations, a new rotation, and the residual estimate |g_{k+1}|.
 constexpr int kGivensLocal = 64;  // restart lengths up to this decide convergence before a 2nd pass
+// out[j] = y_j c_j, y = R^-1 g over the first kk columns (one thread; the
+// same arithmetic as k_gmres_backsub)
+__device__ __forceinline__ void givens_backsub(const GmresDev* G, int kk, double* out) {
+  const int m = G->m;
+  double y[kInlineBacksub];
+  for (int i = kk - 1; i >= 0; --i) {
+    double acc = G->g[i];
+    for (int j = i + 1; j < kk; ++j) acc -= G->H[i * m + j] * y[j];
+    y[i] = acc / G->H[i * m + i];
+  }
+  for (int j = 0; j < kk; ++j) out[j] = y[j] * G->cn[j];
+}
+
 __device__ __noinline__ void gmres_givens(const GivensArgs& a, const double* d, double sc,
                                           const double* hn2, double n2) {
   GmresDev* G = a.G;
@@ -105,6 +118,7 @@ __device__ __noinline__ void gmres_givens(const GivensArgs& a, const double* d, 
           G->est = fabs(G->g[kk]);
           G->k_done = kk;
           G->status = 1;
+          if (a.ysol && kk <= kInlineBacksub) givens_backsub(G, kk, a.ysol);
           reinterpret_cast<volatile int*>(a.host)[k] = 1;
           __threadfence_system();
           return;
@@ -146,6 +160,7 @@ __device__ __noinline__ void gmres_givens(const GivensArgs& a, const double* d, 
   G->k_done = kk;
   const int st = est <= G->tol_abs ? 1 : ((hn == 0.0 || !isfinite(hn)) ? 2 : 0);
   G->status = st;
+  if (st == 1 && a.ysol && kk <= kInlineBacksub) givens_backsub(G, kk, a.ysol);
   reinterpret_cast<volatile int*>(a.host)[k] = st;
   __threadfence_system();
 }

@@ -713,6 +713,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     gv.pass = 0;
     gv.d1 = dsm;
     gv.host = mapped_dev;
+    gv.ysol = want_rel ? nullptr : dsm + 256;
     stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s, run0);  // [d_0..d_k, <w,w>]
     stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190,
                         dsm + 64, run0, gv);
@@ -732,6 +733,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     gv.d1 = dsm;
     gv.sc1 = dsm + 190;
     gv.host = mapped_dev;
+    gv.ysol = want_rel ? nullptr : dsm + 256;
     stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm + 128, s, run_re);
     stg::vec_update_dot(vn, V, ld, kk, dsm + 128, n, 0, h->partial.p, dsm + 64, s, dsm + 128,
                         dsm + 191, dsm + 64, run_re, gv);
@@ -832,7 +834,12 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       // back substitution and the update run on the device, no round trip.
       // add_to (first cycle from x = 0): the solution goes straight into the
       // caller's vector (Newton's u += du without du)
-      stg::gmres_backsub(G, k, dsm + 256, s);
+      // (a step that converged within kInlineBacksub columns left the
+      // coefficients in dsm + 256 itself)
+      if (k > stg::kInlineBacksub) {
+        stg::gmres_backsub(G, k, dsm + 256, s);
+        h->launches++;
+      }
       if (add_to && !x_set) {
         if (h->lazy_src && add_to == h->lazy_dst) {  // u = 1 (x) lazy_src + correction
           stg::vec_combine(add_to, P ? Z : V, ld, k, dsm + 256, n, s, true, h->lazy_src,
@@ -845,7 +852,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       } else {
         stg::vec_combine(x, P ? Z : V, ld, k, dsm + 256, n, s, x_set);
       }
-      h->launches += 2;
+      h->launches += 1;
       x_set = true;
       st.converged = true;
       st.rel_residual = -1.0;  // not read back
