@@ -1622,7 +1622,10 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
         }
       double* Rb = a.R + (long long)cellB * 64 + qB;
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < 4; ++r) {
+        // n_out < 4: only the first output blocks exist (the stage update
+        // u_next = u + dt sum_j b_j F(U_j) has one)
+        if (r >= a.n_out) break;
 #pragma unroll
         for (int z = 0; z < 4; ++z) {
           double acc = a.mx.c[r] * w[z];
@@ -1640,6 +1643,7 @@ __global__ void __launch_bounds__(pst::THREADS, 3)
             rss = fma(acc, acc, rss);
           }
         }
+      }
     }
 #pragma unroll
     for (int z = 0; z < 4; ++z) w[z] = wn[z];
@@ -1938,8 +1942,15 @@ bool fd_fused_supported(const SlabArgs& a) {
          !std::getenv("STG_1D_V1");
 }
 
+namespace {
+int fast_variant();
+}  // namespace
+
 bool slab_fast_supported(const SlabArgs& a) {
-  return a.g.dim == 3 && a.g.n1 == 4 && a.n_in == 4 && a.n_out == 4 &&
+  // n_out < 4 (fewer output blocks than stages: the stage update u_next) is
+  // taken by the persistent kernel only
+  const bool nout_ok = a.n_out == 4 || (a.n_out >= 1 && a.n_out < 4 && fast_variant() != 1);
+  return a.g.dim == 3 && a.g.n1 == 4 && a.n_in == 4 && nout_ok &&
          a.model == int(Model::advection) && a.g.nx % fast::E == 0 &&
          (reinterpret_cast<uintptr_t>(a.X) & 15) == 0 && get_encode() != nullptr;
 }
