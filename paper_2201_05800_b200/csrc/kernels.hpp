@@ -472,12 +472,14 @@ void vec_multidot(const double* V, long long ldv, int k, const double* w, long l
 // if want_dots, out2[j] = <V_j, w> (an extra pass); partial buffer >= grid*(k+1).  s = 1 unless
 // scale_src = [h_0..h_{k-1}, <w,w>] is given: then s = 1/sqrt(<w,w> - sum h^2)
 // (Pythagorean norm of the projected vector), written to scale_out[0].
+// norm_only: w_new is reduced (its exact norm, the Givens step) but not stored.
 // hn2 (optional, device) = ||V_j||^2 for basis vectors stored unnormalised:
 // the coefficients become h_j / hn2[j] and sum h^2 becomes sum h_j^2 / hn2[j].
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
                     const double* scale_src = nullptr, double* scale_out = nullptr,
-                    const double* hn2 = nullptr, Skip skip = {}, GivensArgs gv = {});
+                    const double* hn2 = nullptr, Skip skip = {}, GivensArgs gv = {},
+                    bool norm_only = false);
 // y = sign * x / sqrt(*nrm2)  (nrm2 on device)
 void vec_scale_invsqrt(double* y, const double* x, const double* nrm2, long long n,
                        cudaStream_t s, double sign = 1.0);

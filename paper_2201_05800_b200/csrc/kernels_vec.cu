@@ -249,7 +249,9 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
        i += (long long)gridDim.x * kVecBlock) {
     // accumulate 2: the old w is bsrc repeated with period bper (the lazy
     // initial guess 1 (x) u_n, never written out)
-    typename O::T x = accumulate == 1   ? O::ld(w, i)
+    // accumulate 3: as 1, but the result is only reduced, not stored (the
+    // step is expected to converge: its new basis vector is never read)
+    typename O::T x = (accumulate & 1)  ? O::ld(w, i)
                       : accumulate == 2 ? O::ld(bsrc, i % bper)
                                         : O::zero();
 #pragma unroll
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(kVecBlock) k_update(double* __restrict__ w,
       }
     }
     x = O::scale(x, s);
-    O::st(w, i, x);
+    if (accumulate != 3) O::st(w, i, x);
     acc[0] = O::dot(x, x, acc[0]);
   }
   if (part == nullptr) return;
@@ -551,11 +553,11 @@ void gmres_init(GmresDev* G, int m, const double* bb, double beta, double tol, d
 void vec_update_dot(double* w, const double* V, long long ldv, int k, const double* h,
                     long long n, int want_dots, double* partial, double* out2, cudaStream_t s,
                     const double* scale_src, double* scale_out, const double* hn2, Skip skip,
-                    GivensArgs gv) {
+                    GivensArgs gv, bool norm_only) {
   const int W = vec_width(n, ldv, V, w);
   unsigned* c = counter_of(partial);
   STG_DISPATCH_K(k, W, (launch_ex(vec_pdl(n), k_update<KM, WW>, multi_grid<KM, WW, true>(n), kVecBlock, 0, s, 
-                           w, V, ldv, k, h, n / WW, -1.0, 1, partial, scale_src, scale_out,
+                           w, V, ldv, k, h, n / WW, -1.0, norm_only ? 3 : 1, partial, scale_src, scale_out,
                            out2 + k, c, hn2, skip, gv, nullptr, 1LL)));
   if (want_dots) vec_multidot(V, ldv, k, w, n, partial, out2, s, skip);  // <V_j, w_new>
 }

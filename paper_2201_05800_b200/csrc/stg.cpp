@@ -692,6 +692,10 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     }
   }
   const stg::Skip run0{&G->status, 0}, run_re{&G->status, 3};
+  static const bool no_predict = std::getenv("STG_GMRES_NO_PREDICT") != nullptr;
+  const int pred = no_predict ? 0 : h->gmres_pred[h->pred_slot];  // 0: none yet
+  std::vector<char> norm_only(size_t(m) + 1, 0);
+  int total = 0;
   // Arnoldi step k: S_{k+1} <- A P^-1 S_k, then the two fused passes; the
   // update pass's last block runs the Givens step and publishes the status
   auto enqueue_step = [&](int k) {
@@ -715,10 +719,23 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     gv.host = mapped_dev;
     gv.ysol = want_rel ? nullptr : dsm + 256;
     stg::vec_multidot(V, ld, kk + 1, vn, n, h->partial.p, dsm, s, run0);  // [d_0..d_k, <w,w>]
+    // the step the previous solve converged at: reduce the new vector's norm
+    // (the convergence decision) without storing it; store_step() writes it
+    // if the solve goes on after all
+    norm_only[k] = !no_predict && pred > 0 && total + k + 1 == pred;
     stg::vec_update_dot(vn, V, ld, kk, dsm, n, 0, h->partial.p, dsm + 64, s, dsm, dsm + 190,
-                        dsm + 64, run0, gv);
+                        dsm + 64, run0, gv, norm_only[k]);
     h->launches += 2;
     ck(cudaEventRecord(h->ev_step[k & 1], s), "event");
+  };
+  // the projected, scaled S_{k+1} of a norm-only step, written after the fact
+  // (same dots, same scale; no reduction and no Givens step)
+  auto store_step = [&](int k) {
+    double* vn = V + size_t(k + 1) * ld;
+    stg::vec_update_dot(vn, V, ld, k + 1, dsm, n, 0, nullptr, dsm + 64, s, dsm, dsm + 190,
+                        dsm + 64, stg::Skip{}, stg::GivensArgs{});
+    h->launches++;
+    norm_only[k] = false;
   };
   // second classical pass on S_{k+1}: [g2, <S,S>] = [V, S]^T S, then
   // S' = (S - sum g2_j / ||S_j||^2 S_j) * Pythagorean scale; runs only while
@@ -741,10 +758,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
     ck(cudaEventRecord(h->ev_re, s), "event");
   };
 
-  static const bool no_predict = std::getenv("STG_GMRES_NO_PREDICT") != nullptr;
-  const int pred = no_predict ? 0 : h->gmres_pred[h->pred_slot];  // 0: none yet
   std::vector<double> y(static_cast<size_t>(m), 0.0);
-  int total = 0;
   bool first = true;
   bool x_set = !x_zero;  // x_zero: x is written (not accumulated) by the first update
   // b may be the basis' first slot itself (Newton writes its residual there):
@@ -816,6 +830,7 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
         st.rel_residual = std::numeric_limits<double>::quiet_NaN();
         return st;
       }
+      if (norm_only[k] && (status == 0 || status == 3)) store_step(k);  // the solve goes on
       if (status == 3) {  // step k needs a second Gram-Schmidt pass
         enqueue_reorth(k);
         h->reorth++;
