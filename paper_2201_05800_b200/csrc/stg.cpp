@@ -595,6 +595,7 @@ struct GmresStats {
   double rel_residual = 0.0;
   bool converged = false;
   bool added = false;  // the solution was added into add_to instead of written to x
+  bool aborted = false;  // early_stop() said the solve is not needed: x / add_to untouched
 };
 
 // Restarted GMRES(m), right-preconditioned (A P^-1 y = b, x = P^-1 y; P null:
@@ -623,7 +624,8 @@ struct GmresStats {
 GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long long n, int m,
                  double tol, int max_it, const Op* P = nullptr, bool x_zero = false,
                  bool pipelined = true, double b_sign = 1.0, bool want_rel = true,
-                 bool bb_ready = false, double* add_to = nullptr) {
+                 bool bb_ready = false, double* add_to = nullptr,
+                 const std::function<bool()>* early_stop = nullptr) {
   ensure_workspace(h);
   if (m < 1) throw std::invalid_argument("gmres: restart >= 1");
   if (m > stg::kGmresMaxRestart) throw std::invalid_argument("gmres: restart <= 60");
@@ -823,6 +825,18 @@ GmresStats gmres(stg_handle* h, const Op& A, const double* b, double* x, long lo
       }
       if (k >= enq) break;  // end of the cycle (restart length or max_it)
       ck(cudaEventSynchronize(h->ev_step[k & 1]), "sync");  // step k done
+      // the caller's deferred check (newton: the residual norm it enqueued the
+      // read-back of before this solve has arrived with this first wait): the
+      // solve may turn out not to be needed; nothing has touched x or add_to
+      if (early_stop && total == 0 && k == 0) {
+        const bool stop = (*early_stop)();
+        early_stop = nullptr;
+        if (stop) {
+          st.aborted = true;
+          ck(cudaStreamSynchronize(s), "sync");  // drain the speculative launches
+          return st;
+        }
+      }
       status = mapped[k];
       if (status == 4) break;  // b = 0 (deferred norm): no step ran
       if (status == 5) {       // ||r|| NaN / inf: no step ran, the solve failed
@@ -961,13 +975,44 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     ck(cudaStreamSynchronize(h->stream), "sync");
     return h->pinned[kRedMaxSlot];  // the bits of a non-negative double
   };
-  double norm = residual_norm();
-  check_admissibility(h);
-  const double norm0 = norm;
-  out.history.push_back(norm);
+  // The first residual's norm is not waited for where the apply reduced it
+  // itself: its read-back is enqueued, the first linear solve is enqueued
+  // behind it, and the convergence test at the initial guess runs at that
+  // solve's first host wait (gmres: early_stop), so the device does not idle
+  // through a host round trip and the Jacobian / preconditioner set-up
+  // between the residual and the solve (c4: ~45 us).  If the guess turns out
+  // converged, the solve is abandoned before it touches u.
+  // STG_NEWTON_SYNC_FIRST=1 waits for the norm first.
+  static const bool sync_first = std::getenv("STG_NEWTON_SYNC_FIRST") != nullptr;
+  double norm = 0.0, norm0 = 0.0;
+  bool deferred = false;
+  if (!sync_first && cfg.max_iter > 0 && cfg.gmres_tol < 1.0) {
+    h->red = true;
+    try {
+      residual(u, r);
+    } catch (...) {
+      h->red = false;
+      throw;
+    }
+    h->red = false;
+    if (h->red_done) {
+      ck(cudaMemcpyAsync(h->pinned + kRedMaxSlot, h->small.p + kRedMaxSlot, sizeof(double),
+                         cudaMemcpyDeviceToHost, h->stream), "memcpy");
+      deferred = true;
+    } else {
+      norm = dev_maxabs(h, r, n);
+    }
+  } else {
+    norm = residual_norm();
+  }
   auto converged = [&](double v) { return v <= cfg.abs_tol || v <= cfg.rel_tol * norm0; };
-  while (!converged(norm)) {
-    if (out.iterations >= cfg.max_iter)
+  if (!deferred) {
+    check_admissibility(h);
+    norm0 = norm;
+    out.history.push_back(norm);
+  }
+  while (deferred || !converged(norm)) {
+    if (!deferred && out.iterations >= cfg.max_iter)
       throw NonconvergenceError("newton_solve: no convergence in " +
                                     std::to_string(cfg.max_iter) + " iterations, residual " +
                                     fmt_short(norm),
@@ -981,14 +1026,33 @@ NewtonOut newton(stg_handle* h, const Op& residual,
     // J du = -r: the sign is folded into GMRES (b_sign = -1); du needs no
     // zero fill (gmres with x_zero writes it)
     GmresStats gs;
+    // deferred first norm: read when the solve first waits on the device
+    bool norm_read = false, stop = false;
+    const std::function<bool()> first_norm = [&] {
+      norm_read = true;
+      norm = norm0 = h->pinned[kRedMaxSlot];  // the bits of a non-negative double
+      out.history.push_back(norm);
+      stop = converged(norm);
+      return stop;
+    };
     auto solve = [&] {
       h->pred_slot = std::min(out.iterations, stg_handle::kPredSlots - 1);
       gs = gmres(h, J.A, r, du, n, cfg.gmres_restart, cfg.gmres_tol, cfg.gmres_max_it,
                  J.P ? &J.P : nullptr, /*x_zero=*/true, /*pipelined=*/true,
-                 /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready, /*add_to=*/u);
+                 /*b_sign=*/-1.0, /*want_rel=*/false, /*bb_ready=*/bb_ready, /*add_to=*/u,
+                 deferred ? &first_norm : nullptr);
       out.linear_iterations += gs.iterations;
     };
     solve();
+    if (deferred) {
+      deferred = false;
+      if (!norm_read) {  // the solve never waited (no step was enqueued)
+        ck(cudaStreamSynchronize(h->stream), "sync");
+        first_norm();
+      }
+      check_admissibility(h);
+      if (stop) break;  // converged at the initial guess: u untouched
+    }
     // Lagged Burgers element blocks (built for an earlier step's state): if
     // the solve failed with them, rebuild at u and solve again (the residual
     // slot was overwritten by the restarts: recompute it); if it merely took

@@ -92,7 +92,7 @@ def test_gmres_st_nonzero_guess_residual(base):
 
 
 @pytest.mark.parametrize("knob", ["STG_GMRES_SYNC", "STG_NO_PDL", "STG_GMRES_NO_PREDICT",
-                                  "STG_NO_LAZY_GUESS"])
+                                  "STG_NO_LAZY_GUESS", "STG_NEWTON_SYNC_FIRST"])
 def test_speculation_and_pdl_change_no_arithmetic(base, tmp_path_factory, knob):
     other = run(tmp_path_factory, **{knob: "1"})
     for k in KEYS:
