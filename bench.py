@@ -404,12 +404,22 @@ def run_ours(args):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    ev0.record(stream)  # the host entry point's copies run on this stream
-    for _ in range(e2e_steps):
-        op.st_residual_host(0.0, cfg.dt, npun, npU, out=npR)
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = reduce_max(ev0.elapsed_time(ev1), dist, dev)
+    # Five rounds of e2e_steps calls each, the median round reported and all
+    # of them kept in the line: on these boxes the pipelined call sometimes
+    # runs a whole round of calls with its in-bound and out-bound copies not
+    # overlapping (2.1 -> 2.8-3.0 ms per c4 call, then back; nothing differs on
+    # this side, scripts/e2e_probe.py), and a single round would report
+    # whichever mode it met.
+    E2E_ROUNDS = 5
+    round_ms = []
+    for _ in range(E2E_ROUNDS):
+        ev0.record(stream)  # the host entry point's copies run on this stream
+        for _ in range(e2e_steps):
+            op.st_residual_host(0.0, cfg.dt, npun, npU, out=npR)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        round_ms.append(reduce_max(ev0.elapsed_time(ev1), dist, dev))
+    e2e_ms = sorted(round_ms)[E2E_ROUNDS // 2]
     e2e_val = whole_job_value(ws, cfg.n_dof, e2e_steps, e2e_ms)
     # the host path's output is the device path's output, bit for bit
     e2e_exact = bool(np.array_equal(npR, Rs[0].cpu().numpy())) if NSETS else None
@@ -489,6 +499,8 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": alg},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "steps": e2e_steps,
+                    "statistic": f"median of {E2E_ROUNDS} rounds of {e2e_steps} calls",
+                    "rounds_ms_per_call": [m / e2e_steps for m in round_ms],
                     "h2d_bytes_per_step": 8 * (cfg.n_dof + cfg.n_sdof),
                     "d2h_bytes_per_step": 8 * cfg.n_dof,
                     "path": "stg_st_residual_host (pinned host buffers)",

@@ -5,14 +5,14 @@
 # kernels inside warm solves, and their markdown summary.
 set -u
 cd "$(dirname "$0")/.." || exit 1
-O=gpurun_out/ev8; mkdir -p $O
+O=gpurun_out/ev10; mkdir -p $O
 T0=$SECONDS; python bench.py --steps 20 --warmup 5 > $O/bench.json 2> $O/bench.err; echo "bench.py wall $((SECONDS - T0)) s" > $O/bench_time.txt
 python bench.py --impl reference --steps 20 --warmup 5 > $O/ref.json 2> $O/ref.err
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file $O/ncu_bench_launches.csv python bench.py --steps 20 --warmup 5 --no-extra --no-cpu \
     > $O/ncu_bench.log 2>&1
-for c in c4 c2 c3; do
+for c in c4 c2 c3 c5; do
   ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none --csv --log-file $O/ncu_${c}_solve_launches.csv python scripts/prof_solve.py $c \
       > $O/ncu_${c}_solve.log 2>&1
