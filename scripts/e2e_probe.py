@@ -27,7 +27,7 @@ for _ in range(3):
     op.st_residual_host(0.0, cfg.dt, a, b, out=c)
 torch.cuda.synchronize()
 out = {}
-for rep in range(3):
+for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 3):
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record(stream)
     walls = []
