@@ -210,3 +210,34 @@ def test_large_1d_mesh_newton_residual_norm():
         op2.stdg_step(0.0, 1e-4, u2, NewtonConfig(max_iter=0))
     R2 = op2.st_residual(0.0, 1e-4, u2, u2.repeat(4))
     assert e2.value.residual_history[0] == R2.abs().max().item()
+
+
+@pytest.mark.parametrize("name,cells", [("c4", (8, 8, 8)), ("c2", (32, 32)), ("c3", (4096,)),
+                                        ("c1", (64,))])
+def test_converged_initial_guess_returns_it_untouched(name, cells):
+    """A constant state is a steady solution of every model here, so Newton is
+    converged at its initial guess 1 (x) u_n (newton.hpp:108-114: zero
+    iterations, u0 returned).  The device enqueues the first linear solve
+    behind the residual norm's read-back and never writes the guess for linear
+    advection; both must then be undone: no Newton or GMRES iteration is
+    reported, U is exactly 1 (x) u_n and u_next is u_n, for the slab step
+    and the stage step, on a fresh handle and again after a real solve has
+    left its iteration-count prediction behind."""
+    cfg = C.CONFIGS[name].scaled(cells)
+    op = SlabOperator(**cfg.kwargs())
+    const = torch.full((cfg.n_sdof,), 0.75, dtype=torch.float64, device="cuda")
+    nc = NewtonConfig(abs_tol=1e-11, rel_tol=1e-10, gmres_tol=1e-10, fd_eps=1e-7)
+
+    def check():
+        for step in (lambda: op.stdg_step(0.0, cfg.dt, const, nc),
+                     lambda: op.rk_step(L.STG_FORM_A_INV, 0.0, cfg.dt, const, nc)):
+            U, u1, info = step()
+            assert info.newton_iterations == 0 and info.linear_iterations == 0
+            assert len(info.residual_history) == 1 and info.final_residual <= 1e-11
+            assert torch.equal(U.view(cfg.n_tau, -1), const.expand(cfg.n_tau, -1))
+            # (the stage update u + dt sum_j b_j F(U_j) carries F's round-off)
+            assert float((u1 - const).abs().max()) <= 1e-14
+
+    check()
+    op.stdg_step(0.0, cfg.dt, dev(C.initial_state(cfg)), nc)  # a real solve in between
+    check()
